@@ -1,0 +1,239 @@
+/*
+ * hpsim_b200 — C ABI of the B200-native hybrid-parallel training step.
+ *
+ * This is the drop-in boundary for the reference's `hpsim::Cluster` path
+ * (/root/reference/proj/core/include/hpsim/cluster.hpp:178-212,
+ *  src/cluster.cpp:394-711). Every entry point below names the reference
+ * interface it replaces. Plain C types only: no torch, no C++ in signatures.
+ *
+ * Conventions (mirroring the reference):
+ *   - Status codes map 1:1 onto the reference's exception types
+ *     (include/hpsim/errors.hpp:22-44): CONFIG <-> ConfigError, DIMENSION <->
+ *     DimensionError, DOMAIN <-> DomainError, USAGE <-> UsageError. CUDA and
+ *     NCCL failures have their own codes. hp_last_error() returns the message
+ *     (thread-local), with the reference's field-path wording.
+ *   - Tensors cross the boundary in the reference's layouts: batches NCHW
+ *     [b][C][H][W], targets [b][L], conv kernels [F][C][R][S], fc weights
+ *     [in][out] (shards: columns shard_range(out, K, i)). Device-side layouts
+ *     (NHWC activations, [out][in] fc weights, HWC flatten order) are private.
+ *   - The library owns all device memory. Host pointers are borrowed for the
+ *     duration of the call; device pointers (HP_MEM_DEVICE) must be ready on
+ *     the current device before the call (the call synchronises internally).
+ *   - One caller thread drives a cluster at a time (reference: single
+ *     conceptual writer).
+ */
+#ifndef HPSIM_B200_H_
+#define HPSIM_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define HP_API __attribute__((visibility("default")))
+#else
+#define HP_API
+#endif
+
+/* ---- status codes (errors.hpp:22-44) ---------------------------------- */
+enum {
+  HP_OK = 0,
+  HP_ERR_CONFIG = 1,    /* hpsim::ConfigError    */
+  HP_ERR_DIMENSION = 2, /* hpsim::DimensionError */
+  HP_ERR_DOMAIN = 3,    /* hpsim::DomainError    */
+  HP_ERR_USAGE = 4,     /* hpsim::UsageError     */
+  HP_ERR_CUDA = 5,
+  HP_ERR_NCCL = 6
+};
+
+enum { HP_SCHEME_A = 0, HP_SCHEME_B = 1, HP_SCHEME_C = 2 }; /* cluster.hpp:36 */
+enum { HP_PRECISION_SINGLE = 0, HP_PRECISION_DOUBLE = 1 };  /* tensor.hpp:28 */
+enum {
+  HP_MATH_BF16 = 0,  /* bf16 operands, fp32 accumulate (throughput mode) */
+  HP_MATH_TF32 = 1,  /* fp32 operands read as tf32                      */
+  HP_MATH_F32X3 = 2  /* 3xTF32 split: near-fp32 (parity mode)           */
+};
+enum { HP_TRANSPORT_LOGICAL = 0, HP_TRANSPORT_NCCL = 1 };
+enum { HP_MEM_HOST = 0, HP_MEM_DEVICE = 1 };
+enum { /* MsgClass, cluster.hpp:41-46 */
+  HP_MSG_FC_ACTIVATIONS = 0,
+  HP_MSG_FC_GRADIENTS = 1,
+  HP_MSG_FC_INTERNAL = 2,
+  HP_MSG_CONV_SYNC = 3
+};
+enum { /* Phase, cluster.hpp:86 */
+  HP_PHASE_CONV_FWD = 0,
+  HP_PHASE_FC_FWD = 1,
+  HP_PHASE_FC_BWD = 2,
+  HP_PHASE_CONV_BWD = 3,
+  HP_PHASE_SYNC = 4
+};
+
+/* ---- model spec (model.hpp:24-58), superset for AlexNet ---------------- */
+typedef struct hp_conv_layer {
+  int64_t in_channels;
+  int64_t out_channels;
+  int32_t kernel;
+  int32_t stride;
+  int32_t pad;
+  int32_t relu;
+  /* Superset (absent from the reference, zero = off): */
+  int32_t floor_mode;  /* output = floor((H+2p-k)/s)+1 instead of exact division */
+  int32_t lrn_size;    /* cross-channel LRN after ReLU (Krizhevsky 2012)        */
+  double lrn_alpha;    /* b = a / (k + alpha * sum_{window} a^2)^beta (alpha NOT /n) */
+  double lrn_beta;
+  double lrn_k;
+  int32_t pool_kernel; /* max-pool after (LRN,) ReLU; floor mode                   */
+  int32_t pool_stride;
+} hp_conv_layer;
+
+typedef struct hp_fc_layer {
+  int64_t in_dim;
+  int64_t out_dim;
+  int32_t relu;
+} hp_fc_layer;
+
+typedef struct hp_model_spec {
+  const hp_conv_layer* conv;
+  int32_t n_conv;
+  const hp_fc_layer* fc;
+  int32_t n_fc;
+  int64_t input_shape[3]; /* C, H, W */
+  int64_t num_classes;
+} hp_model_spec;
+
+/* ---- cluster config (cluster.hpp:59-68) + device fields ---------------- */
+typedef struct hp_cluster_config {
+  int32_t workers;            /* K */
+  int64_t per_worker_batch;   /* b */
+  int32_t scheme;             /* HP_SCHEME_*            */
+  int32_t variable_batch;     /* approximate variant     */
+  int32_t precision;          /* HP_PRECISION_SINGLE only (double -> CONFIG) */
+  uint64_t seed;
+  int32_t math_mode;          /* HP_MATH_*               */
+  int32_t transport;          /* HP_TRANSPORT_*          */
+  int32_t rank;               /* NCCL: this process's worker id */
+  int32_t device;             /* CUDA device ordinal (-1: current) */
+  unsigned char nccl_id[128]; /* NCCL: ncclUniqueId from hp_nccl_unique_id on rank 0 */
+} hp_cluster_config;
+
+/* ---- hyperparameters (optimizer.hpp:27-51) ----------------------------- */
+typedef struct hp_hyper {
+  double momentum;
+  double lr;
+  double weight_decay;
+  int32_t has_fc_partial_lr;
+  double fc_partial_lr;
+} hp_hyper;
+
+/* ---- metrics / trace (cluster.hpp:86-117) ------------------------------ */
+typedef struct hp_trace_event {
+  int32_t phase;
+  int32_t sub_batch;
+  int32_t worker;
+  int64_t bytes_total;
+  int64_t bytes_max_sender;
+} hp_trace_event;
+
+typedef struct hp_step_metrics {
+  double loss;
+  int32_t fc_update_count;
+  int32_t conv_update_count;
+  int64_t bytes_sent[4];
+  int32_t n_events; /* full trace via hp_cluster_trace */
+} hp_step_metrics;
+
+typedef struct hp_cluster hp_cluster;
+
+/* ---- errors ------------------------------------------------------------- */
+HP_API const char* hp_last_error(void);
+HP_API const char* hp_version(void);
+
+/* ---- cluster lifecycle --------------------------------------------------
+ * Replaces hpsim::Cluster::Cluster (cluster.hpp:180, cluster.cpp:394-415):
+ * validates spec and config (ModelSpec::validate model.cpp:39-91,
+ * ClusterConfig::validate cluster.cpp:50-67), draws the initial model with the
+ * reference's GaussianSampler stream (init_model model.cpp:133-162) on the
+ * host, and uploads the conv replicas and fc column shards. */
+HP_API int hp_cluster_create(const hp_model_spec* spec, const hp_cluster_config* cfg,
+                             hp_cluster** out);
+HP_API void hp_cluster_destroy(hp_cluster* c);
+
+/* NCCL transport: rank 0 creates the id and ships it to the other ranks
+ * (bench.py uses torch.distributed for that plumbing). */
+HP_API int hp_nccl_unique_id(unsigned char out[128]);
+
+/* Replaces Cluster::run_step (cluster.hpp:190-192, cluster.cpp:439-711).
+ * batches[i] / targets[i]: worker i's [b][C][H][W] images and [b][L] targets.
+ * LOGICAL transport: K entries. NCCL transport: 1 entry (this rank's).
+ * mem_kind: HP_MEM_HOST (copied in) or HP_MEM_DEVICE. */
+HP_API int hp_cluster_run_step(hp_cluster* c, const float* const* batches,
+                               const float* const* targets, int mem_kind, const hp_hyper* hp,
+                               double lr, hp_step_metrics* out);
+
+/* Trace of the last step (StepTrace, cluster.hpp:103-109). Returns count. */
+HP_API int hp_cluster_trace(const hp_cluster* c, hp_trace_event* out, int cap);
+/* Cumulative per-worker ByteCounters (cluster.hpp:49-57). */
+HP_API int hp_cluster_worker_bytes(const hp_cluster* c, int worker, int64_t sent[4],
+                                   int64_t received[4]);
+
+/* Parameter access in reference layouts (WorkerState, cluster.hpp:77-84).
+ * which: 0 conv kernels [F][C][R][S], 1 conv bias [F], 2 fc weight shard
+ * [in][out_i], 3 fc bias shard [out_i]; +4 = the matching momentum tensor.
+ * NCCL transport: only the local rank's worker is addressable. */
+enum { HP_P_CONV_K = 0, HP_P_CONV_B = 1, HP_P_FC_W = 2, HP_P_FC_B = 3, HP_P_MOMENTUM = 4 };
+HP_API int64_t hp_cluster_param_size(const hp_cluster* c, int worker, int which, int layer);
+HP_API int hp_cluster_read_param(hp_cluster* c, int worker, int which, int layer, float* dst,
+                                 int64_t n);
+HP_API int hp_cluster_write_param(hp_cluster* c, int worker, int which, int layer,
+                                  const float* src, int64_t n);
+
+/* Cluster::gathered_model (cluster.cpp:417-437): worker 0's conv replica and
+ * the fc shards pasted back by column. Pointers are host buffers in reference
+ * layouts, one per layer. NCCL transport: collective (every rank calls). */
+HP_API int hp_cluster_gather_model(hp_cluster* c, float* const* conv_k, float* const* conv_b,
+                                   float* const* fc_w, float* const* fc_b);
+
+/* Cluster::set_skip_sync_broadcast (cluster.hpp:203-205) negative control. */
+HP_API int hp_cluster_set_skip_sync_broadcast(hp_cluster* c, int v);
+
+/* Wall-clock of the last step's device work, ms (CUDA events). */
+HP_API double hp_cluster_last_step_ms(const hp_cluster* c);
+/* Number of kernels this library launched in the last step. */
+HP_API int64_t hp_cluster_last_step_launches(const hp_cluster* c);
+
+/* ---- host-side helpers shared with the reference ------------------------ */
+/* shard_range (cluster.cpp:69-75). */
+HP_API void hp_shard_range(int64_t total, int parts, int idx, int64_t* begin, int64_t* end);
+/* GaussianSampler(seed).next() x n (rng.hpp:26-56), replayed on the host. */
+HP_API void hp_gaussian_fill(uint64_t seed, double* out, int64_t n);
+/* Same stream, scaled by `scale`, rounded to float. */
+HP_API void hp_gaussian_fill_f32(uint64_t seed, float scale, float* out, int64_t n);
+
+/* ---- kernel-level entry points (device pointers, for parity tests) ------
+ * Each mirrors one dense kernel of include/hpsim/tensor.hpp:92-139 with the
+ * B200 kernel that replaces it inside the step. */
+typedef struct hp_gemm_desc {
+  int32_t math;
+  const void* a; const void* a_lo; int32_t a_mn; int64_t lda;
+  const void* b; const void* b_lo; int32_t b_mn; int64_t ldb;
+  int32_t M, N, K;
+  void* c; int64_t ldc; int32_t c_type; int32_t c_trans;
+  float alpha; int32_t beta;
+  const float* bias; int32_t bias_mode; int32_t relu;
+  const void* mask; int64_t ldmask; int32_t mask_type; int32_t mask_trans;
+  int32_t splits; int32_t bn;
+  float* ws; /* splits*M*N floats when splits > 1 */
+} hp_gemm_desc;
+/* D = A * B^T on tcgen05 (replaces matmul/_tn/_nt, tensor.cpp:254-305). */
+HP_API int hp_kernel_gemm(const hp_gemm_desc* d, void* stream);
+HP_API int hp_kernel_gemm_splits(const hp_gemm_desc* d);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HPSIM_B200_H_ */

@@ -1,0 +1,461 @@
+// tcgen05 / TMEM / TMA GEMM for sm_100a. See gemm.cuh for the contract.
+//
+// One CTA computes one 128 x BN output tile over a contiguous range of
+// k-tiles (split-K when the tile grid cannot fill 148 SMs). Warp roles:
+//   warp 0      TMA producer (one elected lane), STAGES-deep smem ring
+//   warp 1      TMEM allocator + MMA issuer (one lane issues tcgen05.mma)
+//   warps 2..5  epilogue: tcgen05.ld -> fused elementwise -> global stores
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "gemm.cuh"
+#include "ptx.cuh"
+
+namespace hp {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr uint32_t kMaxDynSmem = 232448;  // 227 KB
+
+__host__ __device__ constexpr uint32_t stage_bytes(int bn, int math) {
+  return (kBM * 128u + static_cast<uint32_t>(bn) * 128u) * (math == kMathF32x3 ? 2u : 1u);
+}
+__host__ __device__ constexpr int num_stages(int bn, int math) {
+  return static_cast<int>((kMaxDynSmem - 2048u) / stage_bytes(bn, math)) > 6
+             ? 6
+             : static_cast<int>((kMaxDynSmem - 2048u) / stage_bytes(bn, math));
+}
+__host__ __device__ constexpr uint32_t tmem_cols(int bn) {
+  return bn <= 32 ? 32u : bn <= 64 ? 64u : bn <= 128 ? 128u : 256u;
+}
+
+__device__ __forceinline__ float load_as_float(const void* p, long long off, int type) {
+  if (type == kBF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[off]);
+  return reinterpret_cast<const float*>(p)[off];
+}
+
+__device__ __forceinline__ void epi_elem(const Epi& e, int m, int n, float v) {
+  const long long off = e.c_trans ? static_cast<long long>(n) * e.ldc + m
+                                  : static_cast<long long>(m) * e.ldc + n;
+  v *= e.alpha;
+  if (e.beta) v += reinterpret_cast<const float*>(e.c)[off];
+  if (e.bias_mode == 1) v += e.bias[m];
+  if (e.bias_mode == 2) v += e.bias[n];
+  if (e.relu) v = v > 0.f ? v : 0.f;
+  if (e.mask) {
+    const long long mo = e.mask_trans ? static_cast<long long>(n) * e.ldmask + m
+                                      : static_cast<long long>(m) * e.ldmask + n;
+    if (!(load_as_float(e.mask, mo, e.mask_type) > 0.f)) v = 0.f;
+  }
+  if (e.c_type == kBF16) {
+    reinterpret_cast<__nv_bfloat16*>(e.c)[off] = __float2bfloat16_rn(v);
+  } else {
+    reinterpret_cast<float*>(e.c)[off] = v;
+  }
+}
+
+// Epilogue for 32 consecutive columns [n0, n0+32) of row m.
+__device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, const float (&v)[32]) {
+  if (m >= a.M) return;
+  if (a.raw_partial) {
+    float* dst = a.ws + static_cast<long long>(blockIdx.z) * a.M * a.N +
+                 static_cast<long long>(m) * a.N;
+    if (n0 + 32 <= a.N && (a.N & 3) == 0) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4)
+        *reinterpret_cast<float4*>(dst + n0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+      for (int i = 0; i < 32 && n0 + i < a.N; ++i) dst[n0 + i] = v[i];
+    }
+    return;
+  }
+  const Epi& e = a.epi;
+  const bool simple = !e.c_trans && !e.beta && !e.mask && n0 + 32 <= a.N;
+  if (simple && e.c_type == kF32 && (e.ldc & 3) == 0) {
+    float* dst = reinterpret_cast<float*>(e.c) + static_cast<long long>(m) * e.ldc + n0;
+    const float bm = e.bias_mode == 1 ? e.bias[m] : 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      float t[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float x = v[i + j] * e.alpha;
+        if (e.bias_mode == 1) x += bm;
+        if (e.bias_mode == 2) x += e.bias[n0 + i + j];
+        if (e.relu) x = x > 0.f ? x : 0.f;
+        t[j] = x;
+      }
+      *reinterpret_cast<float4*>(dst + i) = make_float4(t[0], t[1], t[2], t[3]);
+    }
+    return;
+  }
+  if (simple && e.c_type == kBF16 && (e.ldc & 7) == 0) {
+    __nv_bfloat16* dst =
+        reinterpret_cast<__nv_bfloat16*>(e.c) + static_cast<long long>(m) * e.ldc + n0;
+    const float bm = e.bias_mode == 1 ? e.bias[m] : 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+      __align__(16) __nv_bfloat16 t[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float x = v[i + j] * e.alpha;
+        if (e.bias_mode == 1) x += bm;
+        if (e.bias_mode == 2) x += e.bias[n0 + i + j];
+        if (e.relu) x = x > 0.f ? x : 0.f;
+        t[j] = __float2bfloat16_rn(x);
+      }
+      *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(t);
+    }
+    return;
+  }
+  for (int i = 0; i < 32; ++i) {
+    if (n0 + i < a.N) epi_elem(e, m, n0 + i, v[i]);
+  }
+}
+
+template <int ES, int BK, int ATOM>
+__device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
+                                          int mn_major, int row0, int rows, int k0) {
+  if (!mn_major) {
+    tma_load_2d(dst, tm, bar, k0, row0);
+  } else {
+    for (int a = 0; a < rows / ATOM; ++a) tma_load_2d(dst + a * (BK * 128), tm, bar, row0 + a * ATOM, k0);
+  }
+}
+
+template <int BN, int MATH>
+__global__ void __launch_bounds__(192, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                const __grid_constant__ CUtensorMap ta2, const __grid_constant__ CUtensorMap tb2,
+                const GemmArgs args) {
+  constexpr bool SPLIT = MATH == kMathF32x3;
+  constexpr int ES = MATH == kMathBF16 ? 2 : 4;
+  constexpr int BK = 128 / ES;
+  constexpr int UK = 32 / ES;
+  constexpr int ATOM = 128 / ES;
+  constexpr uint32_t A_BYTES = kBM * 128;
+  constexpr uint32_t B_BYTES = BN * 128;
+  constexpr uint32_t SB = stage_bytes(BN, MATH);
+  constexpr int STAGES = num_stages(BN, MATH);
+  constexpr uint32_t TCOLS = tmem_cols(BN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SB);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * kBM;
+  const int n0 = blockIdx.y * BN;
+  const int kt0 = blockIdx.z * args.k_tiles_per_split;
+  const int kt1 = min(args.k_tiles_total, kt0 + args.k_tiles_per_split);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+    tma_prefetch(&ta);
+    tma_prefetch(&tb);
+    if (SPLIT) {
+      tma_prefetch(&ta2);
+      tma_prefetch(&tb2);
+    }
+  }
+  if (warp == 1) tmem_alloc(tslot, TCOLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kt = kt0; kt < kt1; ++kt) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * SB;
+        uint8_t* sb = sa + A_BYTES;
+        mbar_arrive_expect_tx(&full[stage], SB);
+        load_tile<ES, BK, ATOM>(sa, &ta, &full[stage], args.a_mn, m0, kBM, kt * BK);
+        load_tile<ES, BK, ATOM>(sb, &tb, &full[stage], args.b_mn, n0, BN, kt * BK);
+        if (SPLIT) {
+          load_tile<ES, BK, ATOM>(sb + B_BYTES, &ta2, &full[stage], args.a_mn, m0, kBM, kt * BK);
+          load_tile<ES, BK, ATOM>(sb + B_BYTES + A_BYTES, &tb2, &full[stage], args.b_mn, n0, BN,
+                                  kt * BK);
+        }
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t fmt = MATH == kMathBF16 ? 1u : 2u;
+      const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
+                             (static_cast<uint32_t>(args.a_mn) << 15) |
+                             (static_cast<uint32_t>(args.b_mn) << 16) |
+                             (static_cast<uint32_t>(BN >> 3) << 17) |
+                             (static_cast<uint32_t>(kBM >> 4) << 24);
+      const uint32_t a_lbo = args.a_mn ? BK * 128 : 16;
+      const uint32_t b_lbo = args.b_mn ? BK * 128 : 16;
+      // MN-major 32-bit operands use the 32B-granule 128B swizzle: 4-row
+      // swizzle groups (SBO 512) instead of 8-row groups (SBO 1024).
+      const uint32_t a_sbo = (ES == 4 && args.a_mn) ? 512 : 1024;
+      const uint32_t b_sbo = (ES == 4 && args.b_mn) ? 512 : 1024;
+      const uint32_t a_lay = (ES == 4 && args.a_mn) ? 1 : 2;
+      const uint32_t b_lay = (ES == 4 && args.b_mn) ? 1 : 2;
+      const uint32_t a_kstep = args.a_mn ? UK * 128 : UK * ES;
+      const uint32_t b_kstep = args.b_mn ? UK * 128 : UK * ES;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kt = kt0; kt < kt1; ++kt) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + stage * SB);
+        const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / UK; ++k) {
+          const uint64_t ad = umma_desc_sw128(sa + k * a_kstep, a_lbo, a_sbo, a_lay);
+          const uint64_t bd = umma_desc_sw128(sb + k * b_kstep, b_lbo, b_sbo, b_lay);
+          const uint32_t acc = (kt > kt0 || k > 0) ? 1u : 0u;
+          if (MATH == kMathBF16) {
+            mma_f16(tmem, ad, bd, idesc, acc);
+          } else {
+            mma_tf32(tmem, ad, bd, idesc, acc);
+            if (SPLIT) {
+              const uint64_t ad2 =
+                  umma_desc_sw128(sb + B_BYTES + k * a_kstep, a_lbo, a_sbo, a_lay);
+              const uint64_t bd2 =
+                  umma_desc_sw128(sb + B_BYTES + A_BYTES + k * b_kstep, b_lbo, b_sbo, b_lay);
+              mma_tf32(tmem, ad, bd2, idesc, 1u);
+              mma_tf32(tmem, ad2, bd, idesc, 1u);
+            }
+          }
+        }
+        mma_commit(&empty[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      mma_commit(tfull);
+    }
+    __syncwarp();
+  } else {
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int m = m0 + q * 32 + lane;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c), r);
+      tmem_ld_wait();
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+      if (n0 + c < args.N) epi_row32(args, m, n0 + c, v);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TCOLS);
+  }
+}
+
+__global__ void epi_apply_kernel(const float* __restrict__ ws, int splits, int M, int N,
+                                 const Epi e) {
+  const long long total = static_cast<long long>(M) * N;
+  const long long mn = static_cast<long long>(M) * N;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float acc = ws[i];
+    for (int s = 1; s < splits; ++s) acc += ws[s * mn + i];
+    const int m = static_cast<int>(i / N);
+    const int n = static_cast<int>(i % N);
+    epi_elem(e, m, n, acc);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || p == nullptr) {
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    }
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+CUtensorMap make_map(const void* ptr, int es, long long inner, long long outer, long long ld,
+                     int box_inner, int box_outer, CUtensorMapSwizzle swz) {
+  if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0) {
+    throw std::runtime_error("gemm: operand base not 16-byte aligned");
+  }
+  if ((ld * es) % 16 != 0) throw std::runtime_error("gemm: leading dimension not 16-byte aligned");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * es)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                           2, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) +
+                             ")");
+  }
+  return m;
+}
+
+CUtensorMap operand_map(const GemmOperand& o, const void* ptr, int es, int rows, int K, int box_rows) {
+  const int BK = 128 / es;
+  const int ATOM = 128 / es;
+  if (!o.mn_major) return make_map(ptr, es, K, rows, o.ld, BK, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
+  return make_map(ptr, es, rows, K, o.ld, ATOM, BK,
+                  es == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+template <int BN, int MATH>
+void launch_inst(const GemmPlan& p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_kernel<BN, MATH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(p.smem));
+    attr = true;
+  }
+  gemm_kernel<BN, MATH><<<p.grid, 192, p.smem, s>>>(p.ta, p.tb, p.ta2, p.tb2, p.args);
+}
+
+template <int MATH>
+void launch_math(const GemmPlan& p, cudaStream_t s) {
+  switch (p.bn) {
+    case 64: launch_inst<64, MATH>(p, s); break;
+    case 128: launch_inst<128, MATH>(p, s); break;
+    case 192: launch_inst<192, MATH>(p, s); break;
+    case 256: launch_inst<256, MATH>(p, s); break;
+    default: throw std::runtime_error("gemm: unsupported BN");
+  }
+}
+
+int cdiv(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace
+
+int gemm_choose_bn(int M, int N) {
+  const int mt = cdiv(M, kBM);
+  const int cands[4] = {256, 192, 128, 64};
+  int best = 64;
+  double best_score = -1.0;
+  for (int bn : cands) {
+    const int nt = cdiv(N, bn);
+    const double fill = static_cast<double>(N) / (static_cast<double>(nt) * bn);
+    const int tiles = mt * nt;
+    const int waves = cdiv(tiles, 148);
+    const double wave_eff = static_cast<double>(tiles) / (waves * 148.0);
+    // Prefer wide tiles (fewer smem bytes per MMA flop) unless they waste work.
+    const double width = bn >= 128 ? 1.0 : 0.8;
+    const double score = fill * (tiles >= 148 ? wave_eff : 1.0) * width;
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+int gemm_choose_splits(int math, int M, int N, int K, int bn) {
+  if (bn <= 0) bn = gemm_choose_bn(M, N);
+  const int es = math == kMathBF16 ? 2 : 4;
+  const int kt = cdiv(K, 128 / es);
+  const int tiles = cdiv(M, kBM) * cdiv(N, bn);
+  if (tiles >= 120 || kt < 4) return 1;
+  int splits = std::min(cdiv(148, tiles), kt / 2);
+  splits = std::max(1, std::min(splits, 64));
+  const int kps = cdiv(kt, splits);
+  return cdiv(kt, kps);
+}
+
+GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
+                   const Epi& epi, int splits, float* ws, int bn) {
+  if (M <= 0 || N <= 0 || K <= 0) throw std::runtime_error("gemm: empty problem");
+  GemmPlan p;
+  p.math = math;
+  p.bn = bn > 0 ? bn : gemm_choose_bn(M, N);
+  const int es = math == kMathBF16 ? 2 : 4;
+  const int BK = 128 / es;
+  const int kt = cdiv(K, BK);
+  if (splits <= 0) splits = gemm_choose_splits(math, M, N, K, p.bn);
+  const int kps = cdiv(kt, splits);
+  splits = cdiv(kt, kps);
+  p.splits = splits;
+  p.args.M = M;
+  p.args.N = N;
+  p.args.K = K;
+  p.args.k_tiles_total = kt;
+  p.args.k_tiles_per_split = kps;
+  p.args.a_mn = a.mn_major;
+  p.args.b_mn = b.mn_major;
+  p.args.raw_partial = splits > 1 ? 1 : 0;
+  p.args.ws = ws;
+  p.args.epi = epi;
+  if (splits > 1 && ws == nullptr) throw std::runtime_error("gemm: split-K needs a workspace");
+  p.ta = operand_map(a, a.ptr, es, M, K, kBM);
+  p.tb = operand_map(b, b.ptr, es, N, K, p.bn);
+  if (math == kMathF32x3) {
+    if (!a.lo || !b.lo) throw std::runtime_error("gemm: 3xTF32 needs lo operands");
+    p.ta2 = operand_map(a, a.lo, es, M, K, kBM);
+    p.tb2 = operand_map(b, b.lo, es, N, K, p.bn);
+  } else {
+    p.ta2 = p.ta;
+    p.tb2 = p.tb;
+  }
+  p.grid = dim3(cdiv(M, kBM), cdiv(N, p.bn), splits);
+  p.smem = static_cast<size_t>(num_stages(p.bn, math)) * stage_bytes(p.bn, math) + 1024 + 256;
+  p.valid = true;
+  return p;
+}
+
+void epi_apply_launch(const float* ws, int splits, int M, int N, const Epi& e, cudaStream_t s) {
+  const long long total = static_cast<long long>(M) * N;
+  const int threads = 256;
+  const int blocks = static_cast<int>(std::min<long long>((total + threads - 1) / threads, 148LL * 16));
+  epi_apply_kernel<<<blocks, threads, 0, s>>>(ws, splits, M, N, e);
+}
+
+void gemm_launch(const GemmPlan& p, cudaStream_t s) {
+  if (!p.valid) throw std::runtime_error("gemm: invalid plan");
+  switch (p.math) {
+    case kMathBF16: launch_math<kMathBF16>(p, s); break;
+    case kMathTF32: launch_math<kMathTF32>(p, s); break;
+    case kMathF32x3: launch_math<kMathF32x3>(p, s); break;
+    default: throw std::runtime_error("gemm: bad math mode");
+  }
+  if (p.splits > 1) epi_apply_launch(p.args.ws, p.splits, p.args.M, p.args.N, p.args.epi, s);
+}
+
+}  // namespace hp

@@ -1,0 +1,85 @@
+// tcgen05 GEMM: D[M,N] = sum_k A[m,k] * B[n,k], fp32 accumulation in TMEM.
+//
+// Operands are staged by TMA into 128B-swizzled shared memory. Each operand
+// can be K-major (row-major [rows][K]) or MN-major (row-major [K][rows]); the
+// UMMA descriptors take either, so no transposes are ever materialised.
+// Inputs are bf16 (kind::f16), fp32 read as tf32 (kind::tf32), or fp32 split
+// into hi/lo tf32 pairs (3xTF32, near-fp32 accuracy).
+//
+// The epilogue (TMEM -> registers -> global) fuses the elementwise work that
+// follows each GEMM in the reference step: scale, accumulate (beta=1), bias
+// (per row or per column), ReLU, and a ReLU-backward mask.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace hp {
+
+enum DType : int { kF32 = 0, kBF16 = 1 };
+
+enum MathMode : int {
+  kMathBF16 = 0,   // bf16 operands, fp32 accumulate
+  kMathTF32 = 1,   // fp32 operands read as tf32
+  kMathF32x3 = 2,  // fp32 operands, 3xTF32 hi/lo split
+};
+
+struct Epi {
+  void* c = nullptr;  // output
+  long long ldc = 0;
+  int c_type = kF32;
+  int c_trans = 0;    // 1: element (m,n) stored at c[n*ldc + m]
+  float alpha = 1.f;
+  int beta = 0;       // 1: c += result (fp32 output only)
+  const float* bias = nullptr;
+  int bias_mode = 0;  // 0 none, 1 per row (m), 2 per column (n)
+  int relu = 0;
+  const void* mask = nullptr;  // keep value where mask(m,n) > 0 (ReLU backward)
+  long long ldmask = 0;
+  int mask_type = kF32;
+  int mask_trans = 0;
+};
+
+struct GemmOperand {
+  const void* ptr = nullptr;
+  const void* lo = nullptr;  // 3xTF32: tf32 residual x - tf32(x), same layout
+  int mn_major = 0;          // 0: [rows][K] (ld >= K); 1: [K][rows] (ld >= rows)
+  long long ld = 0;          // elements
+};
+
+struct GemmArgs {
+  int M, N, K;
+  int k_tiles_total;
+  int k_tiles_per_split;
+  int a_mn, b_mn;
+  int raw_partial;  // 1: write fp32 partials to ws[split][M][N]; epilogue applied by reduce
+  float* ws;
+  Epi epi;
+};
+
+// A fully prepared GEMM launch (tensor maps encoded once, reused every step).
+struct GemmPlan {
+  CUtensorMap ta, tb, ta2, tb2;
+  GemmArgs args{};
+  int math = kMathBF16;
+  int bn = 128;
+  int splits = 1;
+  dim3 grid;
+  size_t smem = 0;
+  bool valid = false;
+};
+
+// Builds a plan. `splits` <= 0 picks a split-K factor from the tile count.
+// `ws` must hold splits*M*N floats when splits > 1 (query with gemm_ws_floats).
+GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
+                   const Epi& epi, int splits, float* ws, int bn = 0);
+int gemm_choose_splits(int math, int M, int N, int K, int bn = 0);
+int gemm_choose_bn(int M, int N);
+void gemm_launch(const GemmPlan& p, cudaStream_t s);
+
+// Applies an Epi elementwise to a fp32 [M][N] source (used after split-K and
+// by the kernel tests).
+void epi_apply_launch(const float* ws, int splits, int M, int N, const Epi& e, cudaStream_t s);
+
+}  // namespace hp
