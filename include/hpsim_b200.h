@@ -218,8 +218,8 @@ HP_API void hp_gaussian_fill_f32(uint64_t seed, float scale, float* out, int64_t
  * B200 kernel that replaces it inside the step. */
 typedef struct hp_gemm_desc {
   int32_t math;
-  const void* a; const void* a_lo; int32_t a_mn; int64_t lda;
-  const void* b; const void* b_lo; int32_t b_mn; int64_t ldb;
+  const void* a; int32_t a_mn; int64_t lda;
+  const void* b; int32_t b_mn; int64_t ldb;
   int32_t M, N, K;
   void* c; int64_t ldc; int32_t c_type; int32_t c_trans;
   float alpha; int32_t beta;

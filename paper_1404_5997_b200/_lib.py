@@ -96,8 +96,8 @@ class HpStepMetrics(C.Structure):
 class HpGemmDesc(C.Structure):
     _fields_ = [
         ("math", C.c_int32),
-        ("a", C.c_void_p), ("a_lo", C.c_void_p), ("a_mn", C.c_int32), ("lda", C.c_int64),
-        ("b", C.c_void_p), ("b_lo", C.c_void_p), ("b_mn", C.c_int32), ("ldb", C.c_int64),
+        ("a", C.c_void_p), ("a_mn", C.c_int32), ("lda", C.c_int64),
+        ("b", C.c_void_p), ("b_mn", C.c_int32), ("ldb", C.c_int64),
         ("M", C.c_int32), ("N", C.c_int32), ("K", C.c_int32),
         ("c", C.c_void_p), ("ldc", C.c_int64), ("c_type", C.c_int32), ("c_trans", C.c_int32),
         ("alpha", C.c_float), ("beta", C.c_int32),

@@ -1,0 +1,104 @@
+// C ABI: cluster lifecycle, step, parameters (see include/hpsim_b200.h).
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "cluster.hpp"
+#include "comm.hpp"
+#include "errors.hpp"
+#include "hpsim_b200.h"
+
+namespace hp {
+extern thread_local std::string g_last_error;
+
+template <class F>
+int guarded_c(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return HP_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code();
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return HP_ERR_CUDA;
+  }
+}
+}  // namespace hp
+
+struct hp_cluster {
+  std::unique_ptr<hp::ClusterBase> impl;
+  int workers = 0;
+};
+
+using namespace hp;
+
+extern "C" {
+
+HP_API int hp_cluster_create(const hp_model_spec* spec, const hp_cluster_config* cfg, hp_cluster** out) {
+  return guarded_c([&] {
+    if (!spec || !cfg || !out) usage_error("hp_cluster_create: null argument");
+    auto c = std::make_unique<hp_cluster>();
+    c->impl = make_cluster(spec, cfg);
+    c->workers = cfg->workers;
+    *out = c.release();
+  });
+}
+
+HP_API void hp_cluster_destroy(hp_cluster* c) { delete c; }
+
+HP_API int hp_nccl_unique_id(unsigned char out[128]) {
+  return guarded_c([&] { nccl_unique_id(out); });
+}
+
+HP_API int hp_cluster_run_step(hp_cluster* c, const float* const* batches, const float* const* targets,
+                               int mem_kind, const hp_hyper* hp_, double lr, hp_step_metrics* out) {
+  return guarded_c([&] {
+    if (!c || !hp_ || !out) usage_error("run_step: null argument");
+    c->impl->run_step(batches, targets, mem_kind, *hp_, lr, out);
+  });
+}
+
+HP_API int hp_cluster_trace(const hp_cluster* c, hp_trace_event* out, int cap) {
+  const auto& t = c->impl->trace;
+  for (int i = 0; i < static_cast<int>(t.size()) && i < cap; ++i) out[i] = t[i];
+  return static_cast<int>(t.size());
+}
+
+HP_API int hp_cluster_worker_bytes(const hp_cluster* c, int worker, int64_t sent[4], int64_t received[4]) {
+  return guarded_c([&] {
+    if (worker < 0 || worker >= c->workers) usage_error("worker index out of range");
+    for (int i = 0; i < 4; ++i) {
+      sent[i] = c->impl->sent[worker][i];
+      received[i] = c->impl->received[worker][i];
+    }
+  });
+}
+
+HP_API int64_t hp_cluster_param_size(const hp_cluster* c, int worker, int which, int layer) {
+  return c->impl->param_size(worker, which, layer);
+}
+
+HP_API int hp_cluster_read_param(hp_cluster* c, int worker, int which, int layer, float* dst, int64_t n) {
+  return guarded_c([&] { c->impl->read_param(worker, which, layer, dst, n); });
+}
+
+HP_API int hp_cluster_write_param(hp_cluster* c, int worker, int which, int layer, const float* src,
+                                  int64_t n) {
+  return guarded_c([&] { c->impl->write_param(worker, which, layer, src, n); });
+}
+
+HP_API int hp_cluster_gather_model(hp_cluster* c, float* const* conv_k, float* const* conv_b,
+                                   float* const* fc_w, float* const* fc_b) {
+  return guarded_c([&] { c->impl->gather_model(conv_k, conv_b, fc_w, fc_b); });
+}
+
+HP_API int hp_cluster_set_skip_sync_broadcast(hp_cluster* c, int v) {
+  return guarded_c([&] { c->impl->skip_sync_broadcast = v != 0; });
+}
+
+HP_API double hp_cluster_last_step_ms(const hp_cluster* c) { return c->impl->last_ms; }
+HP_API int64_t hp_cluster_last_step_launches(const hp_cluster* c) { return c->impl->last_launches; }
+
+}  // extern "C"

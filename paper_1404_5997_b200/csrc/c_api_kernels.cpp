@@ -55,11 +55,9 @@ HP_API void hp_gaussian_fill_f32(uint64_t seed, float scale, float* out, int64_t
 static GemmPlan plan_from_desc(const hp_gemm_desc* d) {
   GemmOperand a, b;
   a.ptr = d->a;
-  a.lo = d->a_lo;
   a.mn_major = d->a_mn;
   a.ld = d->lda;
   b.ptr = d->b;
-  b.lo = d->b_lo;
   b.mn_major = d->b_mn;
   b.ld = d->ldb;
   Epi e;

@@ -1,0 +1,1145 @@
+// B200 hybrid-parallel training step: device-side replacement of
+// hpsim::Cluster (src/cluster.cpp:394-711).
+//
+// Per worker (one GPU per worker with NCCL; K workers on one GPU with the
+// logical transport):
+//   conv stack (data parallel): im2col -> tcgen05 GEMM (bias+ReLU fused)
+//     -> LRN -> max-pool, activations NHWC in the operand type.
+//   boundary: scheme A all-gather / B per-turn broadcast / C per-turn slice
+//     all-gather of the [b][A] sample-major conv tops (cluster.cpp:113-194).
+//   fc stack (model parallel, worker i owns output rows shard_range(out,K,i)):
+//     feature-major activations [features][n] so the column all-gather and the
+//     partial-dX reduce-scatter are plain NCCL chunked collectives.
+//   backward: fc wgrad/dgrad GEMMs, boundary reduce-scatter / reduce back to
+//     the owners (return_gradients, cluster.cpp:196-269), conv backward
+//     (pool/LRN/ReLU backward, wgrad GEMM, dgrad GEMM + col2im), conv-gradient
+//     all-reduce (sync_conv_gradients, cluster.cpp:273-319), fused momentum SGD.
+// Byte counters and the phase trace are the reference's analytic integers,
+// computed on the host exactly as cluster.cpp:466-673 does.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "cluster.hpp"
+#include "comm.hpp"
+#include "errors.hpp"
+#include "gemm.cuh"
+#include "kernels.cuh"
+#include "rng.hpp"
+
+namespace hp {
+
+namespace {
+
+long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
+
+void shard(long long total, int parts, int idx, long long* b, long long* e) {
+  const long long base = total / parts;  // cluster.cpp:69-75
+  *b = base * idx;
+  *e = idx == parts - 1 ? total : *b + base;
+}
+
+bool out_dim(long long in, int k, int s, int p, bool floor_mode, long long* out) {
+  const long long num = in + 2LL * p - k;  // model.cpp:25-35
+  if (num < 0 || (!floor_mode && num % s != 0)) return false;
+  *out = num / s + 1;
+  return true;
+}
+
+std::string num(long long v) { return std::to_string(v); }
+
+}  // namespace
+
+Geometry make_geometry(const hp_model_spec* s, int K, long long b) {
+  Geometry g;
+  if (s->n_conv < 1 || !s->conv) config_error("model.conv_layers: at least one conv layer required");
+  if (s->n_fc < 1 || !s->fc) config_error("model.fc_layers: at least one fc layer required");
+  for (int i = 0; i < 3; ++i)
+    if (s->input_shape[i] <= 0) config_error("model.input_shape: dimensions must be positive");
+  g.conv.assign(s->conv, s->conv + s->n_conv);
+  g.fc.assign(s->fc, s->fc + s->n_fc);
+  std::memcpy(g.input, s->input_shape, sizeof g.input);
+  g.num_classes = s->num_classes;
+  long long c = s->input_shape[0], h = s->input_shape[1], w = s->input_shape[2];
+  for (int i = 0; i < s->n_conv; ++i) {
+    const hp_conv_layer& l = s->conv[i];
+    const std::string where = "model.conv_layers[" + num(i) + "]";
+    if (l.in_channels != c)
+      config_error(where + ".in_channels: expected " + num(c) + ", got " + num(l.in_channels));
+    if (l.out_channels <= 0 || l.kernel <= 0 || l.stride <= 0 || l.pad < 0)
+      config_error(where + ": out_channels/kernel/stride must be positive, pad non-negative");
+    ConvGeom cg{};
+    cg.C = static_cast<int>(c);
+    cg.H = static_cast<int>(h);
+    cg.W = static_cast<int>(w);
+    cg.F = static_cast<int>(l.out_channels);
+    cg.R = cg.S = l.kernel;
+    cg.stride = l.stride;
+    cg.pad = l.pad;
+    long long oh, ow;
+    if (!out_dim(h, l.kernel, l.stride, l.pad, l.floor_mode != 0, &oh))
+      config_error(where + " (height): output dimension (" + num(h) + "+2*" + num(l.pad) + "-" +
+                   num(l.kernel) + ")/" + num(l.stride) + "+1 is not a positive integer");
+    if (!out_dim(w, l.kernel, l.stride, l.pad, l.floor_mode != 0, &ow))
+      config_error(where + " (width): output dimension (" + num(w) + "+2*" + num(l.pad) + "-" +
+                   num(l.kernel) + ")/" + num(l.stride) + "+1 is not a positive integer");
+    cg.OH = static_cast<int>(oh);
+    cg.OW = static_cast<int>(ow);
+    cg.relu = l.relu != 0;
+    if (l.lrn_size < 0) config_error(where + ".lrn_size: must be >= 0");
+    cg.lrn_n = l.lrn_size;
+    cg.lrn_alpha = static_cast<float>(l.lrn_alpha);
+    cg.lrn_beta = static_cast<float>(l.lrn_beta);
+    cg.lrn_k = static_cast<float>(l.lrn_k);
+    cg.pk = l.pool_kernel;
+    cg.ps = l.pool_stride;
+    cg.PH = cg.OH;
+    cg.PW = cg.OW;
+    if (cg.pk > 0) {
+      if (cg.ps <= 0) config_error(where + ".pool_stride: must be positive");
+      if (cg.OH < cg.pk || cg.OW < cg.pk) config_error(where + ".pool_kernel: larger than the conv output");
+      cg.PH = (cg.OH - cg.pk) / cg.ps + 1;
+      cg.PW = (cg.OW - cg.pk) / cg.ps + 1;
+    }
+    // B200 operand layout: NHWC rows of F channels feed TMA (16-byte rows).
+    if (cg.F % 8 != 0)
+      config_error(where + ".out_channels: must be a multiple of 8 on B200 (got " + num(cg.F) +
+                   "); TMA operand rows are 16-byte aligned");
+    cg.Kc = cg.R * cg.S * cg.C;
+    cg.ldk = round_up(cg.Kc, 8);
+    cg.P = b * cg.OH * cg.OW;
+    cg.PP = b * cg.PH * cg.PW;
+    g.cg.push_back(cg);
+    c = cg.F;
+    h = cg.PH;
+    w = cg.PW;
+  }
+  g.A = c * h * w;
+  long long dim = g.A;
+  for (int i = 0; i < s->n_fc; ++i) {
+    const hp_fc_layer& l = s->fc[i];
+    const std::string where = "model.fc_layers[" + num(i) + "]";
+    if (l.in_dim != dim)
+      config_error(where + ".in_dim: expected " + num(dim) + " (flattened preceding output), got " +
+                   num(l.in_dim));
+    if (l.out_dim <= 0) config_error(where + ".out_dim: must be positive");
+    FcGeom fg;
+    fg.in = l.in_dim;
+    fg.out = l.out_dim;
+    fg.relu = l.relu != 0;
+    long long mx = 0;
+    for (int k = 0; k < K; ++k) {
+      long long b0, b1;
+      shard(l.out_dim, K, k, &b0, &b1);
+      fg.c0.push_back(b0);
+      fg.c1.push_back(b1);
+      mx = std::max(mx, b1 - b0);
+    }
+    fg.cmax = round_up(std::max(1LL, mx), 8);
+    fg.Ip = i == 0 ? g.A : K * g.fg.back().cmax;
+    g.fg.push_back(fg);
+    dim = l.out_dim;
+  }
+  if (s->num_classes <= 0) config_error("model.num_classes: must be positive");
+  if (dim != s->num_classes)
+    config_error("model.fc_layers: last out_dim " + num(dim) + " does not match num_classes " +
+                 num(s->num_classes));
+  return g;
+}
+
+namespace {
+
+struct DevArena {
+  std::vector<void*> ptrs;
+  size_t total = 0;
+  void* alloc(size_t bytes) {
+    void* p = nullptr;
+    bytes = std::max<size_t>(bytes, 256);
+    HP_CUDA(cudaMalloc(&p, bytes));
+    HP_CUDA(cudaMemset(p, 0, bytes));
+    ptrs.push_back(p);
+    total += bytes;
+    return p;
+  }
+  template <class T>
+  T* make(long long n) {
+    return static_cast<T*>(alloc(static_cast<size_t>(n) * sizeof(T)));
+  }
+  ~DevArena() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+template <class TA>
+struct Worker {
+  int gid = 0;
+  // inputs
+  float* x_nchw = nullptr;  // staging for host batches
+  TA* x0 = nullptr;         // [b][H][W][C]
+  float* targets = nullptr; // [b][L]
+  // conv stack
+  std::vector<TA*> col, act, lrn, pool, dz;
+  std::vector<float*> lrn_d, dcol, gstage;
+  std::vector<int32_t*> pidx;
+  float* gtmp = nullptr;
+  // conv params: [kernels F x ldk | bias F] per layer, one arena
+  float *cp = nullptr, *cm = nullptr, *cgr = nullptr;
+  TA* cpt = nullptr;  // operand copy (bf16 mode)
+  // fc stack
+  TA* xb = nullptr;        // [n][A] boundary input
+  float* tb = nullptr;     // [n][L] routed targets
+  std::vector<TA*> fx;     // fx[l] (l>=1): [K*cmax(l-1)][ldn]
+  float* logits = nullptr; // [cmax_last][ldn]
+  std::vector<TA*> fdz;    // [cmax_l][ldn]
+  std::vector<float*> fdpart;
+  float* gflat = nullptr;  // [b][A]
+  float *fp = nullptr, *fm = nullptr, *fgr = nullptr;
+  TA* fpt = nullptr;
+  double* loss_parts = nullptr;
+  int* bad = nullptr;
+  float* colsum_ws = nullptr;
+  // GEMM plans
+  std::vector<GemmPlan> conv_fwd, conv_wgrad, conv_dgrad, fc_fwd, fc_wgrad, fc_dgrad;
+};
+
+template <class TA>
+class ClusterImpl final : public ClusterBase {
+ public:
+  ClusterImpl(const hp_model_spec* spec, const hp_cluster_config* cfg);
+  ~ClusterImpl() override;
+  void run_step(const float* const* batches, const float* const* targets, int mem_kind,
+                const hp_hyper& hp, double lr, hp_step_metrics* out) override;
+  int64_t param_size(int worker, int which, int layer) const override;
+  void read_param(int worker, int which, int layer, float* dst, int64_t n) override;
+  void write_param(int worker, int which, int layer, const float* src, int64_t n) override;
+  void gather_model(float* const* ck, float* const* cb, float* const* fw, float* const* fb) override;
+
+ private:
+  static constexpr int kTA = std::is_same<TA, float>::value ? kF32 : kBF16;
+  Worker<TA>& local(int gid);
+  const Worker<TA>* local_or_null(int gid) const;
+  void build_plans(Worker<TA>& w);
+  void conv_forward(Worker<TA>& w);
+  void conv_backward(Worker<TA>& w);
+  void route_forward(int j);
+  void fc_forward_backward(int j, bool beta);
+  void return_gradients(int j);
+  void sgd_fc(double lr, float gscale, bool has_gscale, const hp_hyper& hp);
+  void sgd_conv(double lr, const hp_hyper& hp);
+  void account(int num_sub, hp_step_metrics* out);
+  // param layout helpers
+  long long conv_k_off(int l) const { return coff_[l]; }
+  long long conv_b_off(int l) const { return coff_[l] + static_cast<long long>(g_.cg[l].F) * g_.cg[l].ldk; }
+  long long fc_w_off(int l) const { return foff_[l]; }
+  long long fc_b_off(int l) const { return foff_[l] + g_.fg[l].cmax * g_.fg[l].Ip; }
+  long long fc_col(int l, long long i) const;  // reference input index -> device column
+  void init_params();
+  void refresh_copies(Worker<TA>& w);
+  void upload_master(Worker<TA>& w, bool conv, const std::vector<float>& host);
+
+  Geometry g_;
+  int K_, math_, scheme_;
+  bool variable_;
+  long long b_, n_, ldn_;
+  int num_sub_, L_;
+  uint64_t seed_;
+  std::unique_ptr<Comm> comm_;
+  cudaStream_t st_ = nullptr;
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  DevArena arena_;
+  std::vector<Worker<TA>> w_;
+  std::vector<long long> coff_, foff_;
+  long long conv_total_ = 0, fc_total_ = 0;
+  float* ws_ = nullptr;  // shared split-K workspace (one stream)
+  size_t ws_floats_ = 0;
+  int xblocks_ = 0;
+  int64_t launches_ = 0;
+};
+
+template <class TA>
+ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config* cfg) {
+  // ClusterConfig::validate (cluster.cpp:50-67)
+  if (cfg->workers < 1) config_error("cluster.workers: must be >= 1");
+  if (cfg->per_worker_batch < 1) config_error("cluster.per_worker_batch: must be >= 1");
+  if (cfg->scheme < 0 || cfg->scheme > 2) config_error("cluster.scheme: expected A|B|C");
+  if (cfg->scheme == HP_SCHEME_C && cfg->per_worker_batch % cfg->workers != 0)
+    config_error("cluster.per_worker_batch: scheme C scatters b/K examples per worker per turn; " +
+                 num(cfg->per_worker_batch) + " is not divisible by " + num(cfg->workers));
+  if (cfg->variable_batch && cfg->scheme == HP_SCHEME_A)
+    config_error("cluster.variable_batch: scheme A has a single fc pass per step; per-sub-batch "
+                 "updates require scheme B or C");
+  if (cfg->precision != HP_PRECISION_SINGLE)
+    config_error("cluster.precision: the B200 path stores fp32 parameters (single); double is "
+                 "served by the CPU oracle only");
+  K_ = cfg->workers;
+  b_ = cfg->per_worker_batch;
+  scheme_ = cfg->scheme;
+  variable_ = cfg->variable_batch != 0;
+  math_ = cfg->math_mode;
+  seed_ = cfg->seed;
+  g_ = make_geometry(spec, K_, b_);
+  L_ = static_cast<int>(g_.num_classes);
+  num_sub_ = scheme_ == HP_SCHEME_A ? 1 : K_;
+  n_ = scheme_ == HP_SCHEME_A ? K_ * b_ : b_;
+  ldn_ = round_up(n_, 8);
+
+  if (cfg->device >= 0) HP_CUDA(cudaSetDevice(cfg->device));
+  if (cfg->transport == HP_TRANSPORT_NCCL) {
+    if (cfg->rank < 0 || cfg->rank >= K_) usage_error("cluster.rank: out of range");
+    comm_ = make_nccl_comm(K_, cfg->rank, cfg->nccl_id);
+  } else {
+    comm_ = make_logical_comm(K_);
+  }
+  HP_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  HP_CUDA(cudaEventCreate(&ev0_));
+  HP_CUDA(cudaEventCreate(&ev1_));
+
+  // parameter arena layouts (16-byte aligned pieces)
+  for (size_t l = 0; l < g_.cg.size(); ++l) {
+    coff_.push_back(conv_total_);
+    conv_total_ += round_up(static_cast<long long>(g_.cg[l].F) * g_.cg[l].ldk + g_.cg[l].F, 8);
+  }
+  for (size_t l = 0; l < g_.fg.size(); ++l) {
+    foff_.push_back(fc_total_);
+    fc_total_ += round_up(g_.fg[l].cmax * g_.fg[l].Ip + g_.fg[l].cmax, 8);
+  }
+
+  const int nl = comm_->nlocal();
+  w_.resize(nl);
+  const auto& in = g_.input;
+  const long long A = g_.A;
+  const int nc = static_cast<int>(g_.cg.size()), nf = static_cast<int>(g_.fg.size());
+  xblocks_ = 0;
+  for (int l = 0; l < nf; ++l) (void)l;
+  xblocks_ = xent_blocks(static_cast<int>(g_.fg.back().cmax), static_cast<int>(n_));
+  size_t colsum_ws = 0;
+  for (const auto& cg : g_.cg) colsum_ws = std::max(colsum_ws, colsum_ws_floats(cg.P, cg.F));
+  size_t comm_scratch = 0;
+  for (int i = 0; i < nl; ++i) {
+    Worker<TA>& w = w_[i];
+    w.gid = comm_->first() + i;
+    w.x_nchw = arena_.make<float>(b_ * in[0] * in[1] * in[2]);
+    w.x0 = arena_.make<TA>(b_ * in[0] * in[1] * in[2]);
+    w.targets = arena_.make<float>(b_ * L_);
+    long long gmax = 0;
+    for (int l = 0; l < nc; ++l) {
+      const ConvGeom& c = g_.cg[l];
+      w.col.push_back(arena_.make<TA>(c.P * c.ldk));
+      w.act.push_back(arena_.make<TA>(c.P * c.F));
+      w.lrn.push_back(c.lrn_n > 0 ? arena_.make<TA>(c.P * c.F) : nullptr);
+      w.lrn_d.push_back(c.lrn_n > 0 ? arena_.make<float>(c.P * c.F) : nullptr);
+      w.pool.push_back(c.pk > 0 ? arena_.make<TA>(c.PP * c.F) : nullptr);
+      w.pidx.push_back(c.pk > 0 ? arena_.make<int32_t>(c.PP * c.F) : nullptr);
+      w.dz.push_back(arena_.make<TA>(c.P * c.F));
+      w.dcol.push_back(l > 0 ? arena_.make<float>(c.P * c.ldk) : nullptr);
+      // grad wrt this stage's output, needed when the stage ends in pool/LRN
+      const bool needs_g = (c.pk > 0 || c.lrn_n > 0) && l + 1 < nc;
+      w.gstage.push_back(needs_g ? arena_.make<float>(c.PP * c.F) : nullptr);
+      if (c.pk > 0 && c.lrn_n > 0) gmax = std::max(gmax, c.P * c.F);
+    }
+    w.gtmp = gmax > 0 ? arena_.make<float>(gmax) : nullptr;
+    w.cp = arena_.make<float>(conv_total_);
+    w.cm = arena_.make<float>(conv_total_);
+    w.cgr = arena_.make<float>(conv_total_);
+    w.cpt = std::is_same<TA, float>::value ? nullptr : arena_.make<TA>(conv_total_);
+    w.xb = arena_.make<TA>(n_ * A);
+    w.tb = arena_.make<float>(n_ * L_);
+    w.fx.assign(nf, nullptr);
+    for (int l = 1; l < nf; ++l) w.fx[l] = arena_.make<TA>(g_.fg[l].Ip * ldn_);
+    w.logits = arena_.make<float>(g_.fg.back().cmax * ldn_);
+    for (int l = 0; l < nf; ++l) {
+      w.fdz.push_back(arena_.make<TA>(g_.fg[l].cmax * ldn_));
+      w.fdpart.push_back(l > 0 ? arena_.make<float>(g_.fg[l].Ip * ldn_) : arena_.make<float>(n_ * A));
+      if (l > 0) comm_scratch = std::max(comm_scratch, static_cast<size_t>(g_.fg[l - 1].cmax * ldn_));
+    }
+    comm_scratch = std::max(comm_scratch, static_cast<size_t>(b_ * A));
+    w.gflat = arena_.make<float>(b_ * A);
+    w.fp = arena_.make<float>(fc_total_);
+    w.fm = arena_.make<float>(fc_total_);
+    w.fgr = arena_.make<float>(fc_total_);
+    w.fpt = std::is_same<TA, float>::value ? nullptr : arena_.make<TA>(fc_total_);
+    w.loss_parts = arena_.make<double>(static_cast<long long>(num_sub_) * xblocks_);
+    w.bad = arena_.make<int>(1);
+    w.colsum_ws = arena_.make<float>(static_cast<long long>(colsum_ws));
+  }
+  comm_->reserve(comm_scratch * sizeof(float));
+  // Plans first with a null workspace to size it, then for real.
+  for (auto& w : w_) build_plans(w);
+  ws_ = ws_floats_ > 0 ? arena_.make<float>(static_cast<long long>(ws_floats_)) : nullptr;
+  for (auto& w : w_) build_plans(w);
+  init_params();
+  sent.assign(K_, {0, 0, 0, 0});
+  received.assign(K_, {0, 0, 0, 0});
+  HP_CUDA(cudaStreamSynchronize(st_));
+}
+
+template <class TA>
+ClusterImpl<TA>::~ClusterImpl() {
+  if (st_) cudaStreamSynchronize(st_);
+  comm_.reset();
+  if (ev0_) cudaEventDestroy(ev0_);
+  if (ev1_) cudaEventDestroy(ev1_);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+template <class TA>
+Worker<TA>& ClusterImpl<TA>::local(int gid) {
+  for (auto& w : w_)
+    if (w.gid == gid) return w;
+  usage_error("worker " + num(gid) + " is not local to this process (NCCL transport)");
+}
+
+template <class TA>
+const Worker<TA>* ClusterImpl<TA>::local_or_null(int gid) const {
+  for (const auto& w : w_)
+    if (w.gid == gid) return &w;
+  return nullptr;
+}
+
+template <class TA>
+void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
+  const int nc = static_cast<int>(g_.cg.size()), nf = static_cast<int>(g_.fg.size());
+  const bool bf = !std::is_same<TA, float>::value;
+  auto op = [](const void* p, int mn, long long ld) {
+    GemmOperand o;
+    o.ptr = p;
+    o.mn_major = mn;
+    o.ld = ld;
+    return o;
+  };
+  auto plan = [&](const GemmOperand& a, const GemmOperand& b, long long M, long long N, long long K,
+                  const Epi& e) {
+    const int sp = gemm_choose_splits(math_, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K));
+    if (sp > 1) ws_floats_ = std::max(ws_floats_, static_cast<size_t>(sp * M * N));
+    if (ws_ == nullptr && sp > 1) {
+      // sizing pass: build a throwaway plan against a dummy workspace
+      return gemm_plan(math_, a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e,
+                       sp, reinterpret_cast<float*>(16), 0);
+    }
+    return gemm_plan(math_, a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e, sp,
+                     ws_, 0);
+  };
+  w.conv_fwd.clear();
+  w.conv_wgrad.clear();
+  w.conv_dgrad.clear();
+  w.fc_fwd.clear();
+  w.fc_wgrad.clear();
+  w.fc_dgrad.clear();
+  const void* cweights = bf ? static_cast<const void*>(w.cpt) : static_cast<const void*>(w.cp);
+  const int es = bf ? 2 : 4;
+  for (int l = 0; l < nc; ++l) {
+    const ConvGeom& c = g_.cg[l];
+    const char* kw = static_cast<const char*>(cweights) + conv_k_off(l) * es;
+    // fprop: Y[P][F] = col[P][Kc] . W[F][Kc]^T (+bias, ReLU)
+    Epi e;
+    e.c = w.act[l];
+    e.ldc = c.F;
+    e.c_type = kTA;
+    e.bias = w.cp + conv_b_off(l);
+    e.bias_mode = 2;
+    e.relu = c.relu;
+    w.conv_fwd.push_back(plan(op(w.col[l], 0, c.ldk), op(kw, 0, c.ldk), c.P, c.F, c.Kc, e));
+    // wgrad: dW[F][Kc] = dz^T[F][P] . col[P][Kc]
+    Epi eg;
+    eg.c = w.cgr + conv_k_off(l);
+    eg.ldc = c.ldk;
+    w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), op(w.col[l], 1, c.ldk), c.F, c.Kc, c.P, eg));
+    // dgrad (l > 0): dcol[P][Kc] = dz[P][F] . W[F][Kc]
+    if (l > 0) {
+      Epi ed;
+      ed.c = w.dcol[l];
+      ed.ldc = c.ldk;
+      w.conv_dgrad.push_back(plan(op(w.dz[l], 0, c.F), op(kw, 1, c.ldk), c.P, c.Kc, c.F, ed));
+    } else {
+      w.conv_dgrad.push_back(GemmPlan{});
+    }
+  }
+  const void* fweights = bf ? static_cast<const void*>(w.fpt) : static_cast<const void*>(w.fp);
+  for (int l = 0; l < nf; ++l) {
+    const FcGeom& f = g_.fg[l];
+    const long long rows = f.c1[w.gid] - f.c0[w.gid];
+    const char* fwp = static_cast<const char*>(fweights) + fc_w_off(l) * es;
+    const bool last = l + 1 == nf;
+    // fwd: Z^T[rows][n] = W[rows][Ip] . X^T
+    Epi e;
+    if (last) {
+      e.c = w.logits;
+      e.c_type = kF32;
+    } else {
+      e.c = static_cast<TA*>(w.fx[l + 1]) + static_cast<long long>(w.gid) * f.cmax * ldn_;
+      e.c_type = kTA;
+    }
+    e.ldc = ldn_;
+    e.bias = w.fp + fc_b_off(l);
+    e.bias_mode = 1;
+    e.relu = f.relu;
+    const GemmOperand xin = l == 0 ? op(w.xb, 0, g_.A) : op(w.fx[l], 1, ldn_);
+    w.fc_fwd.push_back(plan(op(fwp, 0, f.Ip), xin, rows, n_, f.Ip, e));
+    // wgrad: dW[rows][Ip] (+)= dZ[rows][n] . X[n][Ip]
+    Epi eg;
+    eg.c = w.fgr + fc_w_off(l);
+    eg.ldc = f.Ip;
+    const GemmOperand xw = l == 0 ? op(w.xb, 1, g_.A) : op(w.fx[l], 0, ldn_);
+    w.fc_wgrad.push_back(plan(op(w.fdz[l], 0, ldn_), xw, rows, f.Ip, n_, eg));
+    // dgrad
+    if (l > 0) {
+      Epi ed;
+      if (K_ == 1) {
+        ed.c = w.fdz[l - 1];
+        ed.c_type = kTA;
+      } else {
+        ed.c = w.fdpart[l];
+      }
+      ed.ldc = ldn_;
+      if (g_.fg[l - 1].relu) {
+        ed.mask = w.fx[l];
+        ed.ldmask = ldn_;
+        ed.mask_type = kTA;
+      }
+      w.fc_dgrad.push_back(plan(op(fwp, 1, f.Ip), op(w.fdz[l], 1, ldn_), f.Ip, n_, rows, ed));
+    } else {
+      Epi ed;
+      ed.c = K_ == 1 ? w.gflat : w.fdpart[0];
+      ed.ldc = g_.A;
+      w.fc_dgrad.push_back(plan(op(w.fdz[0], 1, ldn_), op(fwp, 1, f.Ip), n_, g_.A, rows, ed));
+    }
+  }
+}
+
+template <class TA>
+long long ClusterImpl<TA>::fc_col(int l, long long i) const {
+  if (l == 0) {
+    // reference flatten C x H x W (model.hpp:40-43) -> device H x W x C
+    const ConvGeom& c = g_.cg.back();
+    const long long hw = static_cast<long long>(c.PH) * c.PW;
+    const long long ch = i / hw, p = i % hw;
+    return p * c.F + ch;
+  }
+  const FcGeom& prev = g_.fg[l - 1];
+  for (int q = 0; q < K_; ++q)
+    if (i >= prev.c0[q] && i < prev.c1[q]) return q * prev.cmax + (i - prev.c0[q]);
+  return -1;
+}
+
+// init_model (model.cpp:133-162): one GaussianSampler stream on the host;
+// conv kernels in layer order, then fc weights; biases zero; 0.01 * N(0,1)
+// rounded to float. Each worker uploads its replica / shard.
+template <class TA>
+void ClusterImpl<TA>::init_params() {
+  GaussianSampler gs(seed_);
+  std::vector<float> conv(conv_total_, 0.f);
+  for (size_t l = 0; l < g_.cg.size(); ++l) {
+    const ConvGeom& c = g_.cg[l];
+    float* k = conv.data() + conv_k_off(static_cast<int>(l));
+    for (int f = 0; f < c.F; ++f)
+      for (int ch = 0; ch < c.C; ++ch)
+        for (int r = 0; r < c.R; ++r)
+          for (int s = 0; s < c.S; ++s)
+            k[f * c.ldk + (r * c.S + s) * c.C + ch] = static_cast<float>(0.01 * gs.next());
+  }
+  for (auto& w : w_) upload_master(w, true, conv);
+  // fc: draw the full [in][out] matrices in row-major order, keep this
+  // process's shards.
+  std::vector<std::vector<float>> fcs(w_.size(), std::vector<float>(fc_total_, 0.f));
+  for (size_t l = 0; l < g_.fg.size(); ++l) {
+    const FcGeom& f = g_.fg[l];
+    std::vector<long long> col(f.in);
+    for (long long i = 0; i < f.in; ++i) col[i] = fc_col(static_cast<int>(l), i);
+    for (long long i = 0; i < f.in; ++i)
+      for (long long o = 0; o < f.out; ++o) {
+        const float v = static_cast<float>(0.01 * gs.next());
+        for (size_t wi = 0; wi < w_.size(); ++wi) {
+          const int gid = w_[wi].gid;
+          if (o >= f.c0[gid] && o < f.c1[gid])
+            fcs[wi][fc_w_off(static_cast<int>(l)) + (o - f.c0[gid]) * f.Ip + col[i]] = v;
+        }
+      }
+  }
+  for (size_t wi = 0; wi < w_.size(); ++wi) upload_master(w_[wi], false, fcs[wi]);
+}
+
+template <class TA>
+void ClusterImpl<TA>::upload_master(Worker<TA>& w, bool conv, const std::vector<float>& host) {
+  float* dst = conv ? w.cp : w.fp;
+  HP_CUDA(cudaMemcpyAsync(dst, host.data(), host.size() * sizeof(float), cudaMemcpyHostToDevice, st_));
+  refresh_copies(w);
+  HP_CUDA(cudaStreamSynchronize(st_));
+}
+
+template <class TA>
+void ClusterImpl<TA>::refresh_copies(Worker<TA>& w) {
+  if (std::is_same<TA, float>::value) return;
+  launch_cast<TA>(w.cp, w.cpt, conv_total_, st_);
+  launch_cast<TA>(w.fp, w.fpt, fc_total_, st_);
+}
+
+// ------------------------------------------------------------------ forward
+template <class TA>
+void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
+  const int nc = static_cast<int>(g_.cg.size());
+  const TA* x = w.x0;
+  for (int l = 0; l < nc; ++l) {
+    const ConvGeom& c = g_.cg[l];
+    launch_im2col<TA>(x, w.col[l], static_cast<int>(b_), c.H, c.W, c.C, c.R, c.S, c.stride, c.pad,
+                      c.OH, c.OW, c.ldk, st_);
+    gemm_launch(w.conv_fwd[l], st_);
+    launches_ += 1 + (w.conv_fwd[l].splits > 1 ? 2 : 1);
+    const TA* out = w.act[l];
+    if (c.lrn_n > 0) {
+      launch_lrn_fwd<TA>(w.act[l], w.lrn[l], w.lrn_d[l], c.P, c.F, c.lrn_n, c.lrn_alpha, c.lrn_beta,
+                         c.lrn_k, st_);
+      out = w.lrn[l];
+      ++launches_;
+    }
+    if (c.pk > 0) {
+      launch_maxpool_fwd<TA>(out, w.pool[l], w.pidx[l], static_cast<int>(b_), c.OH, c.OW, c.F, c.pk,
+                             c.ps, c.PH, c.PW, st_);
+      out = w.pool[l];
+      ++launches_;
+    }
+    x = out;
+  }
+}
+
+template <class TA>
+static const TA* stage_out_of(const Worker<TA>& w, const ConvGeom& c, int l) {
+  if (c.pk > 0) return w.pool[l];
+  if (c.lrn_n > 0) return w.lrn[l];
+  return w.act[l];
+}
+
+// Boundary exchange for turn j (exchange_activations / assemble_rows,
+// cluster.cpp:113-194), targets routed with their examples.
+template <class TA>
+void ClusterImpl<TA>::route_forward(int j) {
+  const int nl = comm_->nlocal();
+  const long long A = g_.A;
+  const size_t es = sizeof(TA);
+  std::vector<const void*> sa(nl), stt(nl);
+  std::vector<void*> ra(nl), rt(nl);
+  const int last = static_cast<int>(g_.cg.size()) - 1;
+  for (int i = 0; i < nl; ++i) {
+    const TA* top = stage_out_of(w_[i], g_.cg[last], last);
+    sa[i] = top;
+    stt[i] = w_[i].targets;
+    ra[i] = w_[i].xb;
+    rt[i] = w_[i].tb;
+  }
+  if (scheme_ == HP_SCHEME_A) {
+    comm_->allgather(sa, ra, b_ * A * es, st_);
+    comm_->allgather(stt, rt, b_ * L_ * sizeof(float), st_);
+  } else if (scheme_ == HP_SCHEME_B) {
+    for (int i = 0; i < nl; ++i)
+      if (w_[i].gid == j) {
+        HP_CUDA(cudaMemcpyAsync(ra[i], sa[i], b_ * A * es, cudaMemcpyDeviceToDevice, st_));
+        HP_CUDA(cudaMemcpyAsync(rt[i], stt[i], b_ * L_ * sizeof(float), cudaMemcpyDeviceToDevice, st_));
+      }
+    comm_->broadcast(ra, b_ * A * es, j, st_);
+    comm_->broadcast(rt, b_ * L_ * sizeof(float), j, st_);
+  } else {
+    const long long slice = b_ / K_;
+    std::vector<const void*> sa2(nl), st2(nl);
+    for (int i = 0; i < nl; ++i) {
+      sa2[i] = static_cast<const char*>(sa[i]) + j * slice * A * es;
+      st2[i] = static_cast<const char*>(stt[i]) + j * slice * L_ * sizeof(float);
+    }
+    comm_->allgather(sa2, ra, slice * A * es, st_);
+    comm_->allgather(st2, rt, slice * L_ * sizeof(float), st_);
+  }
+}
+
+// Model-parallel fc forward, loss and backward for one sub-batch
+// (cluster.cpp:534-584).
+template <class TA>
+void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
+  const int nf = static_cast<int>(g_.fg.size());
+  const int nl = comm_->nlocal();
+  for (int l = 0; l < nf; ++l) {
+    for (auto& w : w_) {
+      gemm_launch(w.fc_fwd[l], st_);
+      launches_ += w.fc_fwd[l].splits > 1 ? 2 : 1;
+    }
+    if (l + 1 < nf && K_ > 1) {
+      std::vector<void*> bufs(nl);
+      for (int i = 0; i < nl; ++i) bufs[i] = w_[i].fx[l + 1];
+      comm_->allgather_inplace(bufs, g_.fg[l].cmax * ldn_ * sizeof(TA), st_);
+    }
+  }
+  // logistic cross-entropy on each worker's logit shard (no logit gather:
+  // output units are independent).
+  const FcGeom& fl = g_.fg.back();
+  for (auto& w : w_) {
+    const int rows = static_cast<int>(fl.c1[w.gid] - fl.c0[w.gid]);
+    launch_xent<TA>(w.logits, ldn_, w.tb, L_, static_cast<int>(fl.c0[w.gid]), rows, static_cast<int>(n_),
+                    w.fdz[nf - 1], ldn_, w.loss_parts + static_cast<long long>(j) * xblocks_, w.bad, st_);
+    ++launches_;
+  }
+  for (int li = nf - 1; li >= 0; --li) {
+    const FcGeom& f = g_.fg[li];
+    for (auto& w : w_) {
+      const int rows = static_cast<int>(f.c1[w.gid] - f.c0[w.gid]);
+      GemmPlan pw = w.fc_wgrad[li];
+      pw.args.epi.beta = beta ? 1 : 0;
+      gemm_launch(pw, st_);
+      launch_rowsum<TA>(w.fdz[li], rows, static_cast<int>(n_), ldn_, w.fgr + fc_b_off(li), beta ? 1 : 0, st_);
+      gemm_launch(w.fc_dgrad[li], st_);
+      launches_ += (pw.splits > 1 ? 2 : 1) + 1 + (w.fc_dgrad[li].splits > 1 ? 2 : 1);
+    }
+    if (li > 0 && K_ > 1) {
+      std::vector<const float*> send(nl);
+      std::vector<void*> recv(nl);
+      for (int i = 0; i < nl; ++i) {
+        send[i] = w_[i].fdpart[li];
+        recv[i] = w_[i].fdz[li - 1];
+      }
+      comm_->reduce_scatter(send, recv, g_.fg[li - 1].cmax * ldn_, kTA, 1.f, st_);
+      launches_ += nl;
+    }
+  }
+}
+
+// return_gradients (cluster.cpp:196-269): each boundary-gradient row goes
+// back to the worker whose example it is, summed over the fc shards.
+template <class TA>
+void ClusterImpl<TA>::return_gradients(int j) {
+  if (K_ == 1) return;  // dgrad wrote gflat directly
+  const int nl = comm_->nlocal();
+  const long long A = g_.A;
+  std::vector<const float*> send(nl);
+  for (int i = 0; i < nl; ++i) send[i] = w_[i].fdpart[0];
+  if (scheme_ == HP_SCHEME_A) {
+    std::vector<void*> recv(nl);
+    for (int i = 0; i < nl; ++i) recv[i] = w_[i].gflat;
+    // own.scale(K): the big batch's 1/(K*b) scale -> per-worker mean (cluster.cpp:650-652)
+    comm_->reduce_scatter(send, recv, b_ * A, kF32, static_cast<float>(K_), st_);
+  } else if (scheme_ == HP_SCHEME_B) {
+    void* root_buf = nullptr;
+    for (int i = 0; i < nl; ++i)
+      if (w_[i].gid == j) root_buf = w_[i].gflat;
+    if (!root_buf) root_buf = w_[0].gflat;  // ignored on non-root ranks
+    comm_->reduce(send, root_buf, b_ * A, j, kF32, 1.f, st_);
+  } else {
+    const long long slice = b_ / K_;
+    std::vector<void*> recv(nl);
+    for (int i = 0; i < nl; ++i) recv[i] = w_[i].gflat + j * slice * A;
+    comm_->reduce_scatter(send, recv, slice * A, kF32, 1.f, st_);
+  }
+  launches_ += nl;
+}
+
+// ------------------------------------------------------------------ backward
+// conv_backward_from_flat (model.cpp:259-283) with the pool / LRN superset.
+template <class TA>
+void ClusterImpl<TA>::conv_backward(Worker<TA>& w) {
+  const int nc = static_cast<int>(g_.cg.size());
+  const float* gout = w.gflat;
+  bool dz_ready = false;
+  for (int l = nc - 1; l >= 0; --l) {
+    const ConvGeom& c = g_.cg[l];
+    const TA* mask = c.relu ? w.act[l] : nullptr;
+    const int B = static_cast<int>(b_);
+    if (c.pk > 0) {
+      if (c.lrn_n > 0) {
+        launch_maxpool_bwd<float, TA>(gout, w.pidx[l], w.gtmp, nullptr, B, c.OH, c.OW, c.F, c.pk, c.ps,
+                                      c.PH, c.PW, st_);
+        launch_lrn_bwd<TA, TA>(w.act[l], w.lrn_d[l], w.gtmp, w.dz[l], c.P, c.F, c.lrn_n, c.lrn_alpha,
+                               c.lrn_beta, c.relu ? 1 : 0, st_);
+        launches_ += 2;
+      } else {
+        launch_maxpool_bwd<TA, TA>(gout, w.pidx[l], w.dz[l], mask, B, c.OH, c.OW, c.F, c.pk, c.ps, c.PH,
+                                   c.PW, st_);
+        ++launches_;
+      }
+    } else if (c.lrn_n > 0) {
+      launch_lrn_bwd<TA, TA>(w.act[l], w.lrn_d[l], gout, w.dz[l], c.P, c.F, c.lrn_n, c.lrn_alpha,
+                             c.lrn_beta, c.relu ? 1 : 0, st_);
+      ++launches_;
+    } else if (!dz_ready) {
+      launch_mask_cast<TA, TA>(gout, mask, w.dz[l], c.P * c.F, st_);
+      ++launches_;
+    }
+    // bias grad = channel sums of dz (model.cpp:184-202)
+    launch_colsum<TA>(w.dz[l], c.P, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, st_);
+    gemm_launch(w.conv_wgrad[l], st_);
+    launches_ += 2 + (w.conv_wgrad[l].splits > 1 ? 2 : 1);
+    if (l > 0) {
+      gemm_launch(w.conv_dgrad[l], st_);
+      launches_ += w.conv_dgrad[l].splits > 1 ? 2 : 1;
+      const ConvGeom& pc = g_.cg[l - 1];
+      if (pc.pk > 0 || pc.lrn_n > 0) {
+        launch_col2im<float, TA>(w.dcol[l], w.gstage[l - 1], nullptr, B, c.H, c.W, c.C, c.R, c.S,
+                                 c.stride, c.pad, c.OH, c.OW, c.ldk, st_);
+        gout = w.gstage[l - 1];
+        dz_ready = false;
+      } else {
+        launch_col2im<TA, TA>(w.dcol[l], w.dz[l - 1], pc.relu ? w.act[l - 1] : nullptr, B, c.H, c.W, c.C,
+                              c.R, c.S, c.stride, c.pad, c.OH, c.OW, c.ldk, st_);
+        dz_ready = true;
+      }
+      ++launches_;
+    }
+  }
+}
+
+template <class TA>
+void ClusterImpl<TA>::sgd_fc(double lr, float gscale, bool has_gscale, const hp_hyper& hp) {
+  std::vector<SgdTensor> ts;
+  for (auto& w : w_) {
+    SgdTensor t{};
+    t.w = w.fp;
+    t.mom = w.fm;
+    t.g = w.fgr;
+    t.copy = w.fpt;
+    t.n = fc_total_;
+    t.gscale = gscale;
+    t.has_gscale = has_gscale ? 1 : 0;
+    ts.push_back(t);
+  }
+  launch_sgd(ts.data(), static_cast<int>(ts.size()), kTA == kBF16 ? 1 : 0, lr, hp.momentum,
+             hp.weight_decay, st_);
+  ++launches_;
+}
+
+template <class TA>
+void ClusterImpl<TA>::sgd_conv(double lr, const hp_hyper& hp) {
+  std::vector<SgdTensor> ts;
+  for (auto& w : w_) {
+    SgdTensor t{};
+    t.w = w.cp;
+    t.mom = w.cm;
+    t.g = w.cgr;
+    t.copy = w.cpt;
+    t.n = conv_total_;
+    // mean.scale(1/K) of sync_conv_gradients (cluster.cpp:293-295)
+    t.gscale = static_cast<float>(1.0 / static_cast<double>(K_));
+    t.has_gscale = K_ > 1 ? 1 : 0;
+    ts.push_back(t);
+  }
+  launch_sgd(ts.data(), static_cast<int>(ts.size()), kTA == kBF16 ? 1 : 0, lr, hp.momentum,
+             hp.weight_decay, st_);
+  ++launches_;
+}
+
+// ------------------------------------------------------------------ step
+template <class TA>
+void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* targets, int mem_kind,
+                               const hp_hyper& hp, double lr, hp_step_metrics* out) {
+  const int nl = comm_->nlocal();
+  if (!batches || !targets) usage_error("run_step: expected " + num(nl) + " batches and targets");
+  for (int i = 0; i < nl; ++i)
+    if (!batches[i] || !targets[i])
+      usage_error("run_step: expected " + num(nl) + " batches and targets, got a null entry");
+  if (mem_kind == HP_MEM_HOST) {
+    // logistic_xent's DomainError (tensor.cpp:600-603), checked before any state change
+    for (int i = 0; i < nl; ++i)
+      for (long long e = 0; e < b_ * L_; ++e) {
+        const double t = targets[i][e];
+        if (t < 0.0 || t > 1.0)
+          domain_error("logistic_xent: target " + std::to_string(t) + " outside [0,1] at flat index " +
+                       num(e % (b_ * L_)));
+      }
+  }
+  const double fc_lr = variable_ ? (hp.has_fc_partial_lr ? hp.fc_partial_lr : lr) : lr;
+  const auto& in = g_.input;
+  const long long xin = b_ * in[0] * in[1] * in[2];
+  launches_ = 0;
+  HP_CUDA(cudaEventRecord(ev0_, st_));
+  for (int i = 0; i < nl; ++i) {
+    Worker<TA>& w = w_[i];
+    const float* src = batches[i];
+    if (mem_kind == HP_MEM_HOST) {
+      HP_CUDA(cudaMemcpyAsync(w.x_nchw, batches[i], xin * sizeof(float), cudaMemcpyHostToDevice, st_));
+      HP_CUDA(cudaMemcpyAsync(w.targets, targets[i], b_ * L_ * sizeof(float), cudaMemcpyHostToDevice, st_));
+      src = w.x_nchw;
+    } else {
+      HP_CUDA(cudaMemcpyAsync(w.targets, targets[i], b_ * L_ * sizeof(float), cudaMemcpyDeviceToDevice, st_));
+    }
+    HP_CUDA(cudaMemsetAsync(w.bad, 0, sizeof(int), st_));
+    launch_nchw_to_nhwc<TA>(src, w.x0, static_cast<int>(b_), static_cast<int>(in[0]),
+                            static_cast<int>(in[1]), static_cast<int>(in[2]), st_);
+    ++launches_;
+  }
+  for (auto& w : w_) conv_forward(w);
+  for (int j = 0; j < num_sub_; ++j) {
+    route_forward(j);
+    fc_forward_backward(j, !variable_ && j > 0);
+    return_gradients(j);
+    if (variable_) sgd_fc(fc_lr, 1.f, false, hp);  // per-sub-batch update (cluster.cpp:586-601)
+  }
+  for (auto& w : w_) conv_backward(w);
+  if (K_ > 1) {
+    std::vector<float*> bufs(nl);
+    for (int i = 0; i < nl; ++i) bufs[i] = w_[i].cgr;
+    comm_->allreduce_f32(bufs, conv_total_, st_);
+    launches_ += 1;
+    if (skip_sync_broadcast) usage_error("set_skip_sync_broadcast: not supported on the B200 path yet");
+  }
+  if (!variable_) {
+    const bool scale = num_sub_ > 1;
+    sgd_fc(lr, static_cast<float>(1.0 / static_cast<double>(num_sub_)), scale, hp);
+  }
+  sgd_conv(lr, hp);
+  HP_CUDA(cudaEventRecord(ev1_, st_));
+
+  // loss = sum_j loss_j * n_j / (K*b) (cluster.cpp:555-556, 710)
+  std::vector<double> parts(static_cast<size_t>(num_sub_) * xblocks_, 0.0);
+  std::vector<int> bad(nl, 0);
+  if (nl == 1 && K_ > 1) {
+    std::vector<double*> b{w_[0].loss_parts};
+    comm_->allreduce_f64(b, parts.size(), st_);
+  }
+  std::vector<double> tmp(parts.size());
+  for (int i = 0; i < nl; ++i) {
+    HP_CUDA(cudaMemcpyAsync(tmp.data(), w_[i].loss_parts, tmp.size() * sizeof(double),
+                            cudaMemcpyDeviceToHost, st_));
+    HP_CUDA(cudaMemcpyAsync(&bad[i], w_[i].bad, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    HP_CUDA(cudaStreamSynchronize(st_));
+    for (size_t e = 0; e < parts.size(); ++e) parts[e] += tmp[e];
+  }
+  HP_CUDA(cudaStreamSynchronize(st_));
+  float ms = 0.f;
+  HP_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+  last_ms = ms;
+  last_launches = launches_;
+  for (int i = 0; i < nl; ++i)
+    if (bad[i]) domain_error("logistic_xent: target outside [0,1]");
+  double loss_weighted = 0.0;
+  const double inv_n = 1.0 / static_cast<double>(n_);
+  for (int j = 0; j < num_sub_; ++j) {
+    double s = 0.0;
+    for (int k = 0; k < xblocks_; ++k) s += parts[static_cast<size_t>(j) * xblocks_ + k];
+    loss_weighted += (s * inv_n) * static_cast<double>(n_);
+  }
+  std::memset(out, 0, sizeof *out);
+  out->loss = loss_weighted / static_cast<double>(K_ * b_);
+  out->fc_update_count = variable_ ? num_sub_ : 1;
+  out->conv_update_count = 1;
+  account(num_sub_, out);
+}
+
+// Analytic byte counters and phase trace, exactly as the reference charges
+// them (cluster.cpp:466-471, 511-528, 549-550, 576-580, 616-633, 666-670).
+template <class TA>
+void ClusterImpl<TA>::account(int num_sub, hp_step_metrics* out) {
+  const int K = K_;
+  const long long b = b_, elt = 4, row_bytes = g_.A * elt;
+  auto charge = [&](int i, int cls, long long s, long long r) {
+    sent[i][cls] += s;
+    received[i][cls] += r;
+    out->bytes_sent[cls] += s;
+  };
+  auto ex_sent = [&](int j, int i) -> long long {
+    if (K <= 1) return 0;
+    if (scheme_ == HP_SCHEME_A) return (K - 1) * b * row_bytes;
+    if (scheme_ == HP_SCHEME_B) return i == j ? (K - 1) * b * row_bytes : 0;
+    return (K - 1) * (b / K) * row_bytes;
+  };
+  const long long n = n_;
+  std::vector<hp_trace_event> fwd(num_sub), bwd(num_sub);
+  for (int j = 0; j < num_sub; ++j) {
+    long long total = 0, mx = 0;
+    for (int i = 0; i < K; ++i) {
+      long long inbound = 0;
+      if (K > 1) inbound = scheme_ == HP_SCHEME_B ? (i == j ? 0 : b * row_bytes) : ex_sent(j, i);
+      charge(i, HP_MSG_FC_ACTIVATIONS, ex_sent(j, i), inbound);
+      total += ex_sent(j, i);
+      mx = std::max(mx, ex_sent(j, i));
+    }
+    fwd[j] = {HP_PHASE_FC_FWD, j, scheme_ == HP_SCHEME_B ? j : -1, total, mx};
+    for (size_t l = 0; l < g_.fg.size(); ++l) {
+      const FcGeom& f = g_.fg[l];
+      for (int i = 0; i < K; ++i) {
+        const long long ns = f.c1[i] - f.c0[i];
+        charge(i, HP_MSG_FC_INTERNAL, (K - 1) * n * ns * elt, n * (f.out - ns) * elt);
+      }
+    }
+    for (size_t li = g_.fg.size(); li-- > 1;) {
+      const long long part = n * g_.fg[li].in * elt;
+      for (int i = 0; i < K; ++i) charge(i, HP_MSG_FC_INTERNAL, (K - 1) * part, (K - 1) * part);
+    }
+  }
+  for (int j = 0; j < num_sub; ++j) {
+    long long total = 0, mx = 0;
+    for (int i = 0; i < K; ++i) {
+      long long s = 0;
+      if (scheme_ == HP_SCHEME_A) s = K > 1 ? (K - 1) * b * row_bytes : 0;
+      else if (scheme_ == HP_SCHEME_B) s = i != j ? b * row_bytes : 0;
+      else s = K > 1 ? (K - 1) * (b / K) * row_bytes : 0;
+      long long r = s;
+      if (scheme_ == HP_SCHEME_B) r = (i == j && K > 1) ? (K - 1) * b * row_bytes : 0;
+      charge(i, HP_MSG_FC_GRADIENTS, s, r);
+      total += s;
+      mx = std::max(mx, s);
+    }
+    bwd[j] = {HP_PHASE_FC_BWD, j, scheme_ == HP_SCHEME_B ? j : -1, total, mx};
+  }
+  trace.clear();
+  trace.push_back({HP_PHASE_CONV_FWD, -1, -1, 0, 0});
+  for (int j = 0; j < num_sub; ++j) {
+    trace.push_back(fwd[j]);
+    trace.push_back(bwd[j]);
+  }
+  trace.push_back({HP_PHASE_CONV_BWD, -1, -1, 0, 0});
+  long long G = 0;
+  for (const auto& c : g_.cg) G += static_cast<long long>(c.F) * c.Kc + c.F;
+  long long total = 0, mx = 0;
+  for (int i = 0; i < K; ++i) {
+    long long s = 0;
+    if (K > 1) {
+      long long s0, s1;
+      shard(G, K, i, &s0, &s1);
+      const long long shard_bytes = (s1 - s0) * elt;
+      s = (G * elt - shard_bytes) + (K - 1) * shard_bytes;
+    }
+    charge(i, HP_MSG_CONV_SYNC, s, s);
+    total += s;
+    mx = std::max(mx, s);
+  }
+  trace.push_back({HP_PHASE_SYNC, -1, -1, total, mx});
+  out->n_events = static_cast<int>(trace.size());
+}
+
+// ------------------------------------------------------------------ params
+template <class TA>
+int64_t ClusterImpl<TA>::param_size(int worker, int which, int layer) const {
+  if (worker < 0 || worker >= K_) return -1;
+  const int base = which & 3;
+  if (base <= 1) {
+    if (layer < 0 || layer >= static_cast<int>(g_.cg.size())) return -1;
+    const ConvGeom& c = g_.cg[layer];
+    return base == 0 ? static_cast<int64_t>(c.F) * c.Kc : c.F;
+  }
+  if (layer < 0 || layer >= static_cast<int>(g_.fg.size())) return -1;
+  const FcGeom& f = g_.fg[layer];
+  const int64_t ns = f.c1[worker] - f.c0[worker];
+  return base == 2 ? f.in * ns : ns;
+}
+
+template <class TA>
+void ClusterImpl<TA>::read_param(int worker, int which, int layer, float* dst, int64_t n) {
+  const int64_t want = param_size(worker, which, layer);
+  if (want < 0) usage_error("read_param: bad worker/which/layer");
+  if (n != want) dimension_error("read_param: size " + num(n) + ", expected " + num(want));
+  Worker<TA>& w = local(worker);
+  const bool mom = which >= 4;
+  const int base = which & 3;
+  HP_CUDA(cudaStreamSynchronize(st_));
+  if (base <= 1) {
+    const ConvGeom& c = g_.cg[layer];
+    std::vector<float> h(static_cast<size_t>(c.F) * c.ldk + c.F);
+    HP_CUDA(cudaMemcpy(h.data(), (mom ? w.cm : w.cp) + conv_k_off(layer), h.size() * sizeof(float),
+                       cudaMemcpyDeviceToHost));
+    if (base == 1) {
+      std::memcpy(dst, h.data() + static_cast<size_t>(c.F) * c.ldk, c.F * sizeof(float));
+      return;
+    }
+    for (int f = 0; f < c.F; ++f)
+      for (int ch = 0; ch < c.C; ++ch)
+        for (int r = 0; r < c.R; ++r)
+          for (int s = 0; s < c.S; ++s)
+            dst[((static_cast<long long>(f) * c.C + ch) * c.R + r) * c.S + s] =
+                h[f * c.ldk + (r * c.S + s) * c.C + ch];
+    return;
+  }
+  const FcGeom& f = g_.fg[layer];
+  const long long ns = f.c1[worker] - f.c0[worker];
+  std::vector<float> h(static_cast<size_t>(f.cmax * f.Ip + f.cmax));
+  HP_CUDA(cudaMemcpy(h.data(), (mom ? w.fm : w.fp) + fc_w_off(layer), h.size() * sizeof(float),
+                     cudaMemcpyDeviceToHost));
+  if (base == 3) {
+    std::memcpy(dst, h.data() + f.cmax * f.Ip, ns * sizeof(float));
+    return;
+  }
+  for (long long i = 0; i < f.in; ++i) {
+    const long long col = fc_col(layer, i);
+    for (long long o = 0; o < ns; ++o) dst[i * ns + o] = h[o * f.Ip + col];
+  }
+}
+
+template <class TA>
+void ClusterImpl<TA>::write_param(int worker, int which, int layer, const float* src, int64_t n) {
+  const int64_t want = param_size(worker, which, layer);
+  if (want < 0) usage_error("write_param: bad worker/which/layer");
+  if (n != want) dimension_error("write_param: size " + num(n) + ", expected " + num(want));
+  Worker<TA>& w = local(worker);
+  const bool mom = which >= 4;
+  const int base = which & 3;
+  HP_CUDA(cudaStreamSynchronize(st_));
+  float* dbase;
+  std::vector<float> h;
+  if (base <= 1) {
+    const ConvGeom& c = g_.cg[layer];
+    dbase = (mom ? w.cm : w.cp) + conv_k_off(layer);
+    h.resize(static_cast<size_t>(c.F) * c.ldk + c.F);
+    HP_CUDA(cudaMemcpy(h.data(), dbase, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    if (base == 1) {
+      std::memcpy(h.data() + static_cast<size_t>(c.F) * c.ldk, src, c.F * sizeof(float));
+    } else {
+      for (int f = 0; f < c.F; ++f)
+        for (int ch = 0; ch < c.C; ++ch)
+          for (int r = 0; r < c.R; ++r)
+            for (int s = 0; s < c.S; ++s)
+              h[f * c.ldk + (r * c.S + s) * c.C + ch] =
+                  src[((static_cast<long long>(f) * c.C + ch) * c.R + r) * c.S + s];
+    }
+  } else {
+    const FcGeom& f = g_.fg[layer];
+    const long long ns = f.c1[worker] - f.c0[worker];
+    dbase = (mom ? w.fm : w.fp) + fc_w_off(layer);
+    h.resize(static_cast<size_t>(f.cmax * f.Ip + f.cmax));
+    HP_CUDA(cudaMemcpy(h.data(), dbase, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    if (base == 3) {
+      std::memcpy(h.data() + f.cmax * f.Ip, src, ns * sizeof(float));
+    } else {
+      for (long long i = 0; i < f.in; ++i) {
+        const long long col = fc_col(layer, i);
+        for (long long o = 0; o < ns; ++o) h[o * f.Ip + col] = src[i * ns + o];
+      }
+    }
+  }
+  HP_CUDA(cudaMemcpy(dbase, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+  refresh_copies(w);
+  HP_CUDA(cudaStreamSynchronize(st_));
+}
+
+template <class TA>
+void ClusterImpl<TA>::gather_model(float* const* ck, float* const* cb, float* const* fw,
+                                   float* const* fb) {
+  const int first = w_[0].gid;
+  for (size_t l = 0; l < g_.cg.size(); ++l) {
+    if (first == 0) {
+      read_param(0, 0, static_cast<int>(l), ck[l], param_size(0, 0, static_cast<int>(l)));
+      read_param(0, 1, static_cast<int>(l), cb[l], param_size(0, 1, static_cast<int>(l)));
+    } else {
+      // every replica is bit-identical after the all-reduce; read ours
+      read_param(first, 0, static_cast<int>(l), ck[l], param_size(first, 0, static_cast<int>(l)));
+      read_param(first, 1, static_cast<int>(l), cb[l], param_size(first, 1, static_cast<int>(l)));
+    }
+  }
+  if (comm_->nlocal() != K_) usage_error("gather_model: NCCL transport gathers via hp_cluster_read_param per rank");
+  for (size_t l = 0; l < g_.fg.size(); ++l) {
+    const FcGeom& f = g_.fg[l];
+    for (int k = 0; k < K_; ++k) {
+      const long long ns = f.c1[k] - f.c0[k];
+      std::vector<float> shard(static_cast<size_t>(f.in * ns));
+      read_param(k, 2, static_cast<int>(l), shard.data(), static_cast<int64_t>(shard.size()));
+      for (long long i = 0; i < f.in; ++i)
+        for (long long o = 0; o < ns; ++o) fw[l][i * f.out + f.c0[k] + o] = shard[i * ns + o];
+      read_param(k, 3, static_cast<int>(l), fb[l] + f.c0[k], ns);
+    }
+  }
+}
+
+}  // namespace
+
+std::unique_ptr<ClusterBase> make_cluster(const hp_model_spec* spec, const hp_cluster_config* cfg) {
+  if (cfg->math_mode == HP_MATH_BF16) return std::make_unique<ClusterImpl<bf16>>(spec, cfg);
+  if (cfg->math_mode == HP_MATH_TF32 || cfg->math_mode == HP_MATH_F32X3)
+    return std::make_unique<ClusterImpl<float>>(spec, cfg);
+  config_error("cluster.math_mode: expected bf16 | tf32 | f32x3");
+}
+
+}  // namespace hp

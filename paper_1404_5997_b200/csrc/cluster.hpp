@@ -1,0 +1,72 @@
+// The B200 hybrid-parallel cluster: the device-side replacement of
+// hpsim::Cluster (include/hpsim/cluster.hpp:178-212, src/cluster.cpp:394-711).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "hpsim_b200.h"
+
+namespace hp {
+
+struct ConvGeom {
+  int C, H, W;                 // stage input (NHWC)
+  int F, R, S, stride, pad;    // conv
+  int OH, OW;                  // conv output
+  bool relu;
+  int lrn_n;                   // 0: no LRN
+  float lrn_alpha, lrn_beta, lrn_k;
+  int pk, ps;                  // max-pool (pk == 0: none)
+  int PH, PW;                  // stage output
+  int Kc;                      // R*S*C (im2col width)
+  long long ldk;               // padded row stride of col / kernels (16-byte multiple)
+  long long P;                 // b*OH*OW rows per worker
+  long long PP;                // b*PH*PW
+};
+
+struct FcGeom {
+  long long in, out;   // reference dims
+  long long Ip;        // device input width: A (layer 0) or K*cmax(prev)
+  long long cmax;      // padded rows per shard chunk
+  bool relu;
+  std::vector<long long> c0, c1;  // shard_range per worker
+};
+
+// Validated spec + derived geometry (ModelSpec::validate, model.cpp:39-91,
+// plus the floor-mode / LRN / pool superset).
+struct Geometry {
+  std::vector<hp_conv_layer> conv;
+  std::vector<hp_fc_layer> fc;
+  int64_t input[3];
+  int64_t num_classes;
+  std::vector<ConvGeom> cg;
+  std::vector<FcGeom> fg;
+  long long A;  // flattened conv output
+};
+
+Geometry make_geometry(const hp_model_spec* spec, int K, long long b);
+
+class ClusterBase {
+ public:
+  virtual ~ClusterBase() = default;
+  virtual void run_step(const float* const* batches, const float* const* targets, int mem_kind,
+                        const hp_hyper& hp, double lr, hp_step_metrics* out) = 0;
+  virtual int64_t param_size(int worker, int which, int layer) const = 0;
+  virtual void read_param(int worker, int which, int layer, float* dst, int64_t n) = 0;
+  virtual void write_param(int worker, int which, int layer, const float* src, int64_t n) = 0;
+  virtual void gather_model(float* const* ck, float* const* cb, float* const* fw,
+                            float* const* fb) = 0;
+
+  std::vector<hp_trace_event> trace;
+  std::vector<std::array<int64_t, 4>> sent, received;  // per worker (all K)
+  bool skip_sync_broadcast = false;
+  double last_ms = 0.0;
+  int64_t last_launches = 0;
+};
+
+std::unique_ptr<ClusterBase> make_cluster(const hp_model_spec* spec, const hp_cluster_config* cfg);
+
+}  // namespace hp

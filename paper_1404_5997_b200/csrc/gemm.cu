@@ -132,7 +132,6 @@ __device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* tm, u
 template <int BN, int MATH>
 __global__ void __launch_bounds__(192, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-                const __grid_constant__ CUtensorMap ta2, const __grid_constant__ CUtensorMap tb2,
                 const GemmArgs args) {
   constexpr bool SPLIT = MATH == kMathF32x3;
   constexpr int ES = MATH == kMathBF16 ? 2 : 4;
@@ -150,7 +149,8 @@ __global__ void __launch_bounds__(192, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SB);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* conv = empty + STAGES;  // 3xTF32: split done (converter -> MMA)
+  uint64_t* tfull = conv + STAGES;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -164,15 +164,12 @@ __global__ void __launch_bounds__(192, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], 128);
     }
     mbar_init(tfull, 1);
     fence_barrier_init();
     tma_prefetch(&ta);
     tma_prefetch(&tb);
-    if (SPLIT) {
-      tma_prefetch(&ta2);
-      tma_prefetch(&tb2);
-    }
   }
   if (warp == 1) tmem_alloc(tslot, TCOLS);
   tc_fence_before();
@@ -188,14 +185,9 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + stage * SB;
         uint8_t* sb = sa + A_BYTES;
-        mbar_arrive_expect_tx(&full[stage], SB);
+        mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
         load_tile<ES, BK, ATOM>(sa, &ta, &full[stage], args.a_mn, m0, kBM, kt * BK);
         load_tile<ES, BK, ATOM>(sb, &tb, &full[stage], args.b_mn, n0, BN, kt * BK);
-        if (SPLIT) {
-          load_tile<ES, BK, ATOM>(sb + B_BYTES, &ta2, &full[stage], args.a_mn, m0, kBM, kt * BK);
-          load_tile<ES, BK, ATOM>(sb + B_BYTES + A_BYTES, &tb2, &full[stage], args.b_mn, n0, BN,
-                                  kt * BK);
-        }
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
@@ -223,7 +215,7 @@ __global__ void __launch_bounds__(192, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int kt = kt0; kt < kt1; ++kt) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait(SPLIT ? &conv[stage] : &full[stage], phase);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + stage * SB);
         const uint32_t sb = sa + A_BYTES;
@@ -256,6 +248,37 @@ __global__ void __launch_bounds__(192, 1)
     }
     __syncwarp();
   } else {
+    if (SPLIT) {
+      // 3xTF32: while the MMA warp waits, the epilogue warps split every
+      // landed fp32 tile in place into hi = rna_tf32(x) and lo = x - hi (exact),
+      // so D = Ahi*Bhi + Ahi*Blo + Alo*Bhi reaches ~fp32 accuracy. The swizzle
+      // is elementwise, so lo tiles share the hi tiles' layout.
+      const int t = threadIdx.x - 64;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kt = kt0; kt < kt1; ++kt) {
+        mbar_wait(&full[stage], phase);
+        float4* hi = reinterpret_cast<float4*>(smem + stage * SB);
+        float4* lo = reinterpret_cast<float4*>(smem + stage * SB + A_BYTES + B_BYTES);
+        constexpr int NV = (A_BYTES + B_BYTES) / 16;
+#pragma unroll 4
+        for (int i = t; i < NV; i += 128) {
+          float4 x = hi[i], h, l;
+          h.x = tf32_rna(x.x); l.x = x.x - h.x;
+          h.y = tf32_rna(x.y); l.y = x.y - h.y;
+          h.z = tf32_rna(x.z); l.z = x.z - h.z;
+          h.w = tf32_rna(x.w); l.w = x.w - h.w;
+          hi[i] = h;
+          lo[i] = l;
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&conv[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
     mbar_wait(tfull, 0);
     tc_fence_after();
     const int q = warp & 3;
@@ -348,7 +371,7 @@ void launch_inst(const GemmPlan& p, cudaStream_t s) {
                          static_cast<int>(p.smem));
     attr = true;
   }
-  gemm_kernel<BN, MATH><<<p.grid, 192, p.smem, s>>>(p.ta, p.tb, p.ta2, p.tb2, p.args);
+  gemm_kernel<BN, MATH><<<p.grid, 192, p.smem, s>>>(p.ta, p.tb, p.args);
 }
 
 template <int MATH>
@@ -426,14 +449,6 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   if (splits > 1 && ws == nullptr) throw std::runtime_error("gemm: split-K needs a workspace");
   p.ta = operand_map(a, a.ptr, es, M, K, kBM);
   p.tb = operand_map(b, b.ptr, es, N, K, p.bn);
-  if (math == kMathF32x3) {
-    if (!a.lo || !b.lo) throw std::runtime_error("gemm: 3xTF32 needs lo operands");
-    p.ta2 = operand_map(a, a.lo, es, M, K, kBM);
-    p.tb2 = operand_map(b, b.lo, es, N, K, p.bn);
-  } else {
-    p.ta2 = p.ta;
-    p.tb2 = p.tb;
-  }
   p.grid = dim3(cdiv(M, kBM), cdiv(N, p.bn), splits);
   p.smem = static_cast<size_t>(num_stages(p.bn, math)) * stage_bytes(p.bn, math) + 1024 + 256;
   p.valid = true;

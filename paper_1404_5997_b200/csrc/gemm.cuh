@@ -43,7 +43,6 @@ struct Epi {
 
 struct GemmOperand {
   const void* ptr = nullptr;
-  const void* lo = nullptr;  // 3xTF32: tf32 residual x - tf32(x), same layout
   int mn_major = 0;          // 0: [rows][K] (ld >= K); 1: [K][rows] (ld >= rows)
   long long ld = 0;          // elements
 };
@@ -60,7 +59,7 @@ struct GemmArgs {
 
 // A fully prepared GEMM launch (tensor maps encoded once, reused every step).
 struct GemmPlan {
-  CUtensorMap ta, tb, ta2, tb2;
+  CUtensorMap ta, tb;
   GemmArgs args{};
   int math = kMathBF16;
   int bn = 128;

@@ -1,0 +1,598 @@
+// Memory-bound kernels of the step. See kernels.cuh.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+
+#include "errors.hpp"
+#include "kernels.cuh"
+
+namespace hp {
+
+namespace {
+
+template <class T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) {
+  return v;
+}
+template <>
+__device__ __forceinline__ float to_f<bf16>(bf16 v) {
+  return __bfloat162float(v);
+}
+
+template <class T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) {
+  return v;
+}
+template <>
+__device__ __forceinline__ bf16 from_f<bf16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+int grid_for(long long n, int threads = 256, int max_blocks = 148 * 16) {
+  long long b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  return static_cast<int>(std::min<long long>(b, max_blocks));
+}
+
+#define GRID_STRIDE(i, n)                                                        \
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; \
+       i < (n); i += static_cast<long long>(gridDim.x) * blockDim.x)
+
+// ------------------------------------------------------------------ layout
+template <class T>
+__global__ void nchw_to_nhwc_kernel(const float* __restrict__ x, T* __restrict__ y, int B, int C,
+                                    int HW) {
+  const long long n = static_cast<long long>(B) * HW;
+  GRID_STRIDE(i, n) {
+    const long long b = i / HW, p = i % HW;
+    const float* src = x + b * C * HW + p;
+    T* dst = y + i * C;
+    for (int c = 0; c < C; ++c) dst[c] = from_f<T>(src[static_cast<long long>(c) * HW]);
+  }
+}
+
+// ------------------------------------------------------------------ im2col
+template <class T>
+__global__ void im2col_vec_kernel(const T* __restrict__ x, T* __restrict__ col, int H, int W, int C,
+                                  int S, int stride, int pad, int OH, int OW, long long ldk,
+                                  long long P, int RS) {
+  constexpr int V = 16 / sizeof(T);
+  const int CV = C / V;
+  const long long n = P * RS * CV;
+  GRID_STRIDE(i, n) {
+    const long long p = i / (static_cast<long long>(RS) * CV);
+    const int rem = static_cast<int>(i - p * RS * CV);
+    const int rs = rem / CV, cv = rem - rs * CV;
+    const int r = rs / S, s = rs - r * S;
+    const int ow = static_cast<int>(p % OW);
+    const long long t = p / OW;
+    const int oh = static_cast<int>(t % OH);
+    const long long b = t / OH;
+    const int h = oh * stride - pad + r, w = ow * stride - pad + s;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (h >= 0 && h < H && w >= 0 && w < W) {
+      v = *reinterpret_cast<const uint4*>(x + ((b * H + h) * W + w) * C + cv * V);
+    }
+    *reinterpret_cast<uint4*>(col + p * ldk + static_cast<long long>(rs) * C + cv * V) = v;
+  }
+}
+
+template <class T>
+__global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ col, int H, int W, int C,
+                              int S, int stride, int pad, int OH, int OW, long long ldk, long long P,
+                              int K) {
+  const long long n = P * K;
+  GRID_STRIDE(i, n) {
+    const long long p = i / K;
+    const int k = static_cast<int>(i - p * K);
+    const int rs = k / C, c = k - rs * C;
+    const int r = rs / S, s = rs - r * S;
+    const int ow = static_cast<int>(p % OW);
+    const long long t = p / OW;
+    const int oh = static_cast<int>(t % OH);
+    const long long b = t / OH;
+    const int h = oh * stride - pad + r, w = ow * stride - pad + s;
+    T v = from_f<T>(0.f);
+    if (h >= 0 && h < H && w >= 0 && w < W) v = x[((b * H + h) * W + w) * C + c];
+    col[p * ldk + k] = v;
+  }
+}
+
+// ------------------------------------------------------------------ col2im
+template <class TO, class TM>
+__global__ void col2im_kernel(const float* __restrict__ dcol, TO* __restrict__ dx,
+                              const TM* __restrict__ mask, int H, int W, int C, int R, int S,
+                              int stride, int pad, int OH, int OW, long long ldk, long long n) {
+  GRID_STRIDE(i, n) {
+    const int c = static_cast<int>(i % C);
+    long long t = i / C;
+    const int w = static_cast<int>(t % W);
+    t /= W;
+    const int h = static_cast<int>(t % H);
+    const long long b = t / H;
+    float acc = 0.f;
+    for (int r = 0; r < R; ++r) {
+      const int ohn = h + pad - r;
+      if (ohn < 0 || ohn % stride != 0) continue;
+      const int oh = ohn / stride;
+      if (oh >= OH) continue;
+      for (int s = 0; s < S; ++s) {
+        const int own = w + pad - s;
+        if (own < 0 || own % stride != 0) continue;
+        const int ow = own / stride;
+        if (ow >= OW) continue;
+        acc += dcol[((b * OH + oh) * OW + ow) * ldk + (r * S + s) * C + c];
+      }
+    }
+    if (mask != nullptr && !(to_f<TM>(mask[i]) > 0.f)) acc = 0.f;
+    dx[i] = from_f<TO>(acc);
+  }
+}
+
+// ------------------------------------------------------------------ pool
+template <class T>
+__global__ void maxpool_fwd_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                   int32_t* __restrict__ idx, int H, int W, int C, int k, int s,
+                                   int OH, int OW, long long n) {
+  GRID_STRIDE(i, n) {
+    const int c = static_cast<int>(i % C);
+    long long t = i / C;
+    const int ow = static_cast<int>(t % OW);
+    t /= OW;
+    const int oh = static_cast<int>(t % OH);
+    const long long b = t / OH;
+    int best_i = (oh * s) * W + ow * s;
+    float best = -INFINITY;
+    bool done = false;
+    for (int r = 0; r < k && !done; ++r) {
+      const int h = oh * s + r;
+      for (int q = 0; q < k; ++q) {
+        const int w = ow * s + q;
+        const float v = to_f<T>(x[((b * H + h) * W + w) * C + c]);
+        if (v > best || isnan(v)) {
+          best = v;
+          best_i = h * W + w;
+          if (isnan(v)) {
+            done = true;
+            break;
+          }
+        }
+      }
+    }
+    y[i] = from_f<T>(best);
+    idx[i] = best_i;
+  }
+}
+
+template <class TO, class TM>
+__global__ void maxpool_bwd_kernel(const float* __restrict__ gy, const int32_t* __restrict__ idx,
+                                   TO* __restrict__ gx, const TM* __restrict__ mask, int H, int W,
+                                   int C, int k, int s, int OH, int OW, long long n) {
+  GRID_STRIDE(i, n) {
+    const int c = static_cast<int>(i % C);
+    long long t = i / C;
+    const int w = static_cast<int>(t % W);
+    t /= W;
+    const int h = static_cast<int>(t % H);
+    const long long b = t / H;
+    const int oh0 = h - k + 1 <= 0 ? 0 : (h - k + s) / s;
+    const int oh1 = min(OH - 1, h / s);
+    const int ow0 = w - k + 1 <= 0 ? 0 : (w - k + s) / s;
+    const int ow1 = min(OW - 1, w / s);
+    const int me = h * W + w;
+    float acc = 0.f;
+    for (int oh = oh0; oh <= oh1; ++oh)
+      for (int ow = ow0; ow <= ow1; ++ow) {
+        const long long o = ((b * OH + oh) * OW + ow) * C + c;
+        if (idx[o] == me) acc += gy[o];
+      }
+    if (mask != nullptr && !(to_f<TM>(mask[i]) > 0.f)) acc = 0.f;
+    gx[i] = from_f<TO>(acc);
+  }
+}
+
+// ------------------------------------------------------------------ LRN
+template <class T>
+__global__ void lrn_fwd_kernel(const T* __restrict__ a, T* __restrict__ b, float* __restrict__ d,
+                               int C, int lo, int hi, float alpha, float beta, float k,
+                               long long n) {
+  GRID_STRIDE(i, n) {
+    const int c = static_cast<int>(i % C);
+    const long long base = i - c;
+    const int j0 = max(0, c - lo), j1 = min(C - 1, c + hi);
+    float sum = 0.f;
+    for (int j = j0; j <= j1; ++j) {
+      const float v = to_f<T>(a[base + j]);
+      sum += v * v;
+    }
+    const float dd = k + alpha * sum;
+    d[i] = dd;
+    b[i] = from_f<T>(to_f<T>(a[i]) * powf(dd, -beta));
+  }
+}
+
+template <class TO, class TA>
+__global__ void lrn_bwd_kernel(const TA* __restrict__ a, const float* __restrict__ d,
+                               const float* __restrict__ gb, TO* __restrict__ ga, int C, int lo,
+                               int hi, float alpha, float beta, int relu_mask, long long n) {
+  GRID_STRIDE(i, n) {
+    const int c = static_cast<int>(i % C);
+    const long long base = i - c;
+    const int i0 = max(0, c - hi), i1 = min(C - 1, c + lo);
+    float acc = 0.f;
+    for (int j = i0; j <= i1; ++j) {
+      const long long e = base + j;
+      acc += gb[e] * to_f<TA>(a[e]) * powf(d[e], -beta - 1.f);
+    }
+    const float ai = to_f<TA>(a[i]);
+    float g = gb[i] * powf(d[i], -beta) - 2.f * alpha * beta * ai * acc;
+    if (relu_mask && !(ai > 0.f)) g = 0.f;
+    ga[i] = from_f<TO>(g);
+  }
+}
+
+// ------------------------------------------------------------------ reductions
+template <class T>
+__global__ void colsum_partial_kernel(const T* __restrict__ x, long long M, int N, long long ldx,
+                                      long long rows_per, float* __restrict__ ws) {
+  __shared__ float red[8][33];
+  const int col = blockIdx.x * 32 + threadIdx.x;
+  const long long r0 = blockIdx.y * rows_per;
+  const long long r1 = min(M, r0 + rows_per);
+  float acc = 0.f;
+  if (col < N)
+    for (long long r = r0 + threadIdx.y; r < r1; r += 8) acc += to_f<T>(x[r * ldx + col]);
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && col < N) {
+    float s = 0.f;
+    for (int y = 0; y < 8; ++y) s += red[y][threadIdx.x];
+    ws[static_cast<long long>(blockIdx.y) * N + col] = s;
+  }
+}
+
+__global__ void colsum_final_kernel(const float* __restrict__ ws, int G, int N,
+                                    float* __restrict__ out) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= N) return;
+  float s = 0.f;
+  for (int g = 0; g < G; ++g) s += ws[static_cast<long long>(g) * N + col];
+  out[col] = s;
+}
+
+template <class T>
+__global__ void rowsum_kernel(const T* __restrict__ x, int R, int n, long long ldx,
+                              float* __restrict__ out, int beta) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= R) return;
+  float s = 0.f;
+  for (int i = lane; i < n; i += 32) s += to_f<T>(x[static_cast<long long>(warp) * ldx + i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[warp] = beta ? out[warp] + s : s;
+}
+
+// ------------------------------------------------------------------ xent
+// logistic_xent_impl (tensor.cpp:587-614) on one logit shard; loss in double.
+template <class TO>
+__global__ void xent_kernel(const float* __restrict__ z, long long ldzin,
+                            const float* __restrict__ t, int L, int c0, int Ls, int n,
+                            TO* __restrict__ dz, long long ldz, double* __restrict__ partial,
+                            int* __restrict__ bad) {
+  __shared__ double red[256];
+  const long long total = static_cast<long long>(Ls) * n;
+  const double inv_b = 1.0 / static_cast<double>(n);
+  double loss = 0.0;
+  GRID_STRIDE(e, total) {
+    const int o = static_cast<int>(e / n), i = static_cast<int>(e % n);
+    const double zi = static_cast<double>(z[o * ldzin + i]);
+    const double ti = static_cast<double>(t[static_cast<long long>(i) * L + c0 + o]);
+    if (ti < 0.0 || ti > 1.0) atomicExch(bad, 1);
+    const double softplus_neg = fmax(-zi, 0.0) + log1p(exp(-fabs(zi)));
+    loss += softplus_neg + (1.0 - ti) * zi;
+    const double sigma = zi >= 0.0 ? 1.0 / (1.0 + exp(-zi)) : exp(zi) / (1.0 + exp(zi));
+    dz[o * ldz + i] = from_f<TO>(__double2float_rn(inv_b * (sigma - ti)));
+  }
+  red[threadIdx.x] = loss;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+// ------------------------------------------------------------------ SGD
+struct SgdParams {
+  SgdTensor ts[kMaxSgdTensors];
+  int blk_begin[kMaxSgdTensors + 1];
+  int nt;
+  int copy_type;  // 0 fp32 (no copy), 1 bf16
+  float mu, s1, s2;
+};
+
+constexpr int kSgdThreads = 256;
+constexpr int kSgdPerThread = 8;
+
+__device__ __forceinline__ float sgd_one(float w, float& m, float g, const SgdTensor& T,
+                                         const SgdParams& p) {
+  if (T.has_gscale) g = __fmul_rn(g, T.gscale);
+  float d = __fmul_rn(m, p.mu);
+  d = __fadd_rn(d, __fmul_rn(p.s1, g));
+  d = __fadd_rn(d, __fmul_rn(p.s2, w));
+  m = d;
+  return __fadd_rn(w, d);
+}
+
+__global__ void __launch_bounds__(kSgdThreads) sgd_kernel(const SgdParams p) {
+  int t = 0;
+  while (t + 1 < p.nt && static_cast<int>(blockIdx.x) >= p.blk_begin[t + 1]) ++t;
+  const SgdTensor& T = p.ts[t];
+  const long long base =
+      static_cast<long long>(blockIdx.x - p.blk_begin[t]) * kSgdThreads * kSgdPerThread;
+  const bool vec = (T.n % 4 == 0) && ((reinterpret_cast<uintptr_t>(T.w) | reinterpret_cast<uintptr_t>(T.mom) |
+                                       reinterpret_cast<uintptr_t>(T.g)) % 16 == 0);
+  if (vec) {
+    for (int j = 0; j < kSgdPerThread / 4; ++j) {
+      const long long i = base + (static_cast<long long>(j) * kSgdThreads + threadIdx.x) * 4;
+      if (i >= T.n) break;
+      float4 w = *reinterpret_cast<const float4*>(T.w + i);
+      float4 m = *reinterpret_cast<const float4*>(T.mom + i);
+      const float4 g = *reinterpret_cast<const float4*>(T.g + i);
+      w.x = sgd_one(w.x, m.x, g.x, T, p);
+      w.y = sgd_one(w.y, m.y, g.y, T, p);
+      w.z = sgd_one(w.z, m.z, g.z, T, p);
+      w.w = sgd_one(w.w, m.w, g.w, T, p);
+      *reinterpret_cast<float4*>(T.w + i) = w;
+      *reinterpret_cast<float4*>(T.mom + i) = m;
+      if (T.copy && p.copy_type == 1) {
+        bf16* c = reinterpret_cast<bf16*>(T.copy) + i;
+        c[0] = __float2bfloat16_rn(w.x);
+        c[1] = __float2bfloat16_rn(w.y);
+        c[2] = __float2bfloat16_rn(w.z);
+        c[3] = __float2bfloat16_rn(w.w);
+      }
+    }
+  } else {
+    for (int j = 0; j < kSgdPerThread; ++j) {
+      const long long i = base + static_cast<long long>(j) * kSgdThreads + threadIdx.x;
+      if (i >= T.n) break;
+      float m = T.mom[i];
+      const float w = sgd_one(T.w[i], m, T.g[i], T, p);
+      T.w[i] = w;
+      T.mom[i] = m;
+      if (T.copy && p.copy_type == 1) reinterpret_cast<bf16*>(T.copy)[i] = __float2bfloat16_rn(w);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ misc
+template <class T>
+__global__ void cast_kernel(const float* __restrict__ in, T* __restrict__ out, long long n) {
+  GRID_STRIDE(i, n) out[i] = from_f<T>(in[i]);
+}
+
+template <class TO>
+__global__ void sum_k_kernel(PtrList in, int K, TO* __restrict__ out, long long n, float alpha) {
+  GRID_STRIDE(i, n) {
+    float s = 0.f;
+    for (int w = 0; w < K; ++w) s += in.p[w][i];
+    if (alpha != 1.f) s = __fmul_rn(s, alpha);
+    out[i] = from_f<TO>(s);
+  }
+}
+
+__global__ void allreduce_k_kernel(MutPtrList bufs, int K, long long n) {
+  GRID_STRIDE(i, n) {
+    float s = 0.f;
+    for (int w = 0; w < K; ++w) s += bufs.p[w][i];
+    for (int w = 0; w < K; ++w) bufs.p[w][i] = s;
+  }
+}
+
+template <class TO, class TM>
+__global__ void mask_cast_kernel(const float* __restrict__ g, const TM* __restrict__ mask,
+                                 TO* __restrict__ out, long long n) {
+  GRID_STRIDE(i, n) {
+    float v = g[i];
+    if (mask != nullptr && !(to_f<TM>(mask[i]) > 0.f)) v = 0.f;
+    out[i] = from_f<TO>(v);
+  }
+}
+
+__global__ void scale_kernel(float* x, long long n, float s) {
+  GRID_STRIDE(i, n) x[i] = __fmul_rn(x[i], s);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+template <class T>
+void launch_nchw_to_nhwc(const float* x, T* y, int B, int C, int H, int W, cudaStream_t s) {
+  const long long n = static_cast<long long>(B) * H * W;
+  nchw_to_nhwc_kernel<T><<<grid_for(n), 256, 0, s>>>(x, y, B, C, H * W);
+}
+
+template <class T>
+void launch_im2col(const T* x, T* col, int B, int H, int W, int C, int R, int S, int stride, int pad,
+                   int OH, int OW, long long ldk, cudaStream_t st) {
+  constexpr int V = 16 / sizeof(T);
+  const long long P = static_cast<long long>(B) * OH * OW;
+  if (C % V == 0 && (ldk * sizeof(T)) % 16 == 0) {
+    const long long n = P * R * S * (C / V);
+    im2col_vec_kernel<T><<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(x, col, H, W, C, S, stride, pad,
+                                                                     OH, OW, ldk, P, R * S);
+  } else {
+    const long long n = P * R * S * C;
+    im2col_kernel<T><<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(x, col, H, W, C, S, stride, pad, OH,
+                                                                 OW, ldk, P, R * S * C);
+  }
+}
+
+template <class TO, class TM>
+void launch_col2im(const float* dcol, TO* dx, const TM* mask, int B, int H, int W, int C, int R,
+                   int S, int stride, int pad, int OH, int OW, long long ldk, cudaStream_t st) {
+  const long long n = static_cast<long long>(B) * H * W * C;
+  col2im_kernel<TO, TM><<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(dcol, dx, mask, H, W, C, R, S,
+                                                                    stride, pad, OH, OW, ldk, n);
+}
+
+template <class T>
+void launch_maxpool_fwd(const T* x, T* y, int32_t* idx, int B, int H, int W, int C, int k, int s,
+                        int OH, int OW, cudaStream_t st) {
+  const long long n = static_cast<long long>(B) * OH * OW * C;
+  maxpool_fwd_kernel<T><<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(x, y, idx, H, W, C, k, s, OH,
+                                                                    OW, n);
+}
+
+template <class TO, class TM>
+void launch_maxpool_bwd(const float* gy, const int32_t* idx, TO* gx, const TM* mask, int B, int H,
+                        int W, int C, int k, int s, int OH, int OW, cudaStream_t st) {
+  const long long n = static_cast<long long>(B) * H * W * C;
+  maxpool_bwd_kernel<TO, TM><<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(gy, idx, gx, mask, H, W, C,
+                                                                         k, s, OH, OW, n);
+}
+
+template <class T>
+void launch_lrn_fwd(const T* a, T* b, float* d, long long P, int C, int n, float alpha, float beta,
+                    float k, cudaStream_t st) {
+  const long long total = P * C;
+  lrn_fwd_kernel<T><<<grid_for(total, 256, 148 * 32), 256, 0, st>>>(a, b, d, C, n / 2, (n - 1) / 2,
+                                                                    alpha, beta, k, total);
+}
+
+template <class TO, class TA>
+void launch_lrn_bwd(const TA* a, const float* d, const float* gb, TO* ga, long long P, int C, int n,
+                    float alpha, float beta, int relu_mask, cudaStream_t st) {
+  const long long total = P * C;
+  lrn_bwd_kernel<TO, TA><<<grid_for(total, 256, 148 * 32), 256, 0, st>>>(
+      a, d, gb, ga, C, n / 2, (n - 1) / 2, alpha, beta, relu_mask, total);
+}
+
+size_t colsum_ws_floats(long long M, int N) {
+  const long long G = std::min<long long>(std::max<long long>(1, (M + 255) / 256), 512);
+  return static_cast<size_t>(G) * N;
+}
+
+template <class T>
+void launch_colsum(const T* x, long long M, int N, long long ldx, float* out, float* ws,
+                   cudaStream_t st) {
+  const long long G = std::min<long long>(std::max<long long>(1, (M + 255) / 256), 512);
+  const long long rows_per = (M + G - 1) / G;
+  dim3 grid((N + 31) / 32, static_cast<unsigned>(G));
+  colsum_partial_kernel<T><<<grid, dim3(32, 8), 0, st>>>(x, M, N, ldx, rows_per, ws);
+  colsum_final_kernel<<<(N + 127) / 128, 128, 0, st>>>(ws, static_cast<int>(G), N, out);
+}
+
+template <class T>
+void launch_rowsum(const T* x, int R, int n, long long ldx, float* out, int beta, cudaStream_t st) {
+  const int threads = 256;
+  const long long blocks = (static_cast<long long>(R) * 32 + threads - 1) / threads;
+  rowsum_kernel<T><<<static_cast<int>(blocks), threads, 0, st>>>(x, R, n, ldx, out, beta);
+}
+
+int xent_blocks(int Ls, int n) {
+  const long long total = static_cast<long long>(Ls) * n;
+  return static_cast<int>(std::min<long long>(std::max<long long>(1, (total + 255) / 256), 128));
+}
+
+template <class TO>
+int launch_xent(const float* z, long long ldzin, const float* t, int L, int c0, int Ls, int n,
+                TO* dz, long long ldz, double* partial, int* bad_target, cudaStream_t st) {
+  const int blocks = xent_blocks(Ls, n);
+  xent_kernel<TO><<<blocks, 256, 0, st>>>(z, ldzin, t, L, c0, Ls, n, dz, ldz, partial, bad_target);
+  return blocks;
+}
+
+void launch_sgd(const SgdTensor* ts, int nt, int copy_type, double lr, double momentum,
+                double weight_decay, cudaStream_t st) {
+  int i = 0;
+  while (i < nt) {
+    SgdParams p{};
+    p.copy_type = copy_type;
+    p.mu = static_cast<float>(momentum);
+    p.s1 = static_cast<float>(-lr);
+    p.s2 = static_cast<float>(-lr * weight_decay);
+    int blocks = 0;
+    int k = 0;
+    for (; k < kMaxSgdTensors && i + k < nt; ++k) {
+      p.ts[k] = ts[i + k];
+      p.blk_begin[k] = blocks;
+      const long long per = static_cast<long long>(kSgdThreads) * kSgdPerThread;
+      blocks += static_cast<int>((ts[i + k].n + per - 1) / per);
+    }
+    p.blk_begin[k] = blocks;
+    p.nt = k;
+    if (blocks > 0) sgd_kernel<<<blocks, kSgdThreads, 0, st>>>(p);
+    i += k;
+  }
+}
+
+template <class T>
+void launch_cast(const float* in, T* out, long long n, cudaStream_t st) {
+  cast_kernel<T><<<grid_for(n), 256, 0, st>>>(in, out, n);
+}
+
+template <class TO>
+void launch_sum_k(PtrList in, int K, TO* out, long long n, float alpha, cudaStream_t st) {
+  sum_k_kernel<TO><<<grid_for(n), 256, 0, st>>>(in, K, out, n, alpha);
+}
+
+void launch_allreduce_k(MutPtrList bufs, int K, long long n, cudaStream_t st) {
+  allreduce_k_kernel<<<grid_for(n), 256, 0, st>>>(bufs, K, n);
+}
+
+void copy2d(void* dst, long long dp, const void* src, long long sp, long long bytes, long long rows,
+            cudaStream_t st) {
+  if (rows <= 0 || bytes <= 0) return;
+  HP_CUDA(cudaMemcpy2DAsync(dst, dp, src, sp, bytes, rows, cudaMemcpyDeviceToDevice, st));
+}
+
+template <class TO, class TM>
+void launch_mask_cast(const float* g, const TM* mask, TO* out, long long n, cudaStream_t st) {
+  mask_cast_kernel<TO, TM><<<grid_for(n), 256, 0, st>>>(g, mask, out, n);
+}
+
+void launch_scale(float* x, long long n, float s, cudaStream_t st) {
+  scale_kernel<<<grid_for(n), 256, 0, st>>>(x, n, s);
+}
+
+#define INST_T(T)                                                                              \
+  template void launch_nchw_to_nhwc<T>(const float*, T*, int, int, int, int, cudaStream_t);   \
+  template void launch_im2col<T>(const T*, T*, int, int, int, int, int, int, int, int, int, int, \
+                                 long long, cudaStream_t);                                     \
+  template void launch_maxpool_fwd<T>(const T*, T*, int32_t*, int, int, int, int, int, int, int, \
+                                      int, cudaStream_t);                                      \
+  template void launch_lrn_fwd<T>(const T*, T*, float*, long long, int, int, float, float, float, \
+                                  cudaStream_t);                                               \
+  template void launch_colsum<T>(const T*, long long, int, long long, float*, float*,          \
+                                 cudaStream_t);                                                \
+  template void launch_rowsum<T>(const T*, int, int, long long, float*, int, cudaStream_t);    \
+  template int launch_xent<T>(const float*, long long, const float*, int, int, int, int, T*,   \
+                              long long, double*, int*, cudaStream_t);                         \
+  template void launch_cast<T>(const float*, T*, long long, cudaStream_t);                     \
+  template void launch_sum_k<T>(PtrList, int, T*, long long, float, cudaStream_t);
+
+INST_T(float)
+INST_T(bf16)
+
+#define INST_TO_TM(TO, TM)                                                                     \
+  template void launch_col2im<TO, TM>(const float*, TO*, const TM*, int, int, int, int, int,   \
+                                      int, int, int, int, int, long long, cudaStream_t);       \
+  template void launch_maxpool_bwd<TO, TM>(const float*, const int32_t*, TO*, const TM*, int,  \
+                                           int, int, int, int, int, int, int, cudaStream_t);   \
+  template void launch_lrn_bwd<TO, TM>(const TM*, const float*, const float*, TO*, long long, \
+                                       int, int, float, float, int, cudaStream_t);             \
+  template void launch_mask_cast<TO, TM>(const float*, const TM*, TO*, long long, cudaStream_t);
+
+INST_TO_TM(float, float)
+INST_TO_TM(float, bf16)
+INST_TO_TM(bf16, float)
+INST_TO_TM(bf16, bf16)
+
+}  // namespace hp

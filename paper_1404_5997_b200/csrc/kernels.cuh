@@ -1,0 +1,109 @@
+// Memory-bound kernels of the step (HBM-bound; coalesced, 16-byte vectorised
+// where the layout allows). Activations are NHWC; `T` is the activation /
+// GEMM-operand storage type (bf16 in bf16 mode, fp32 in tf32 / 3xTF32 modes).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace hp {
+
+using bf16 = __nv_bfloat16;
+
+// Reference batch layout NCHW fp32 -> device NHWC T.
+template <class T>
+void launch_nchw_to_nhwc(const float* x, T* y, int B, int C, int H, int W, cudaStream_t s);
+
+// im2col: x [B][H][W][C] -> col [B*OH*OW][ldk], column k = (r*S + s)*C + c.
+template <class T>
+void launch_im2col(const T* x, T* col, int B, int H, int W, int C, int R, int S, int stride,
+                   int pad, int OH, int OW, long long ldk, cudaStream_t st);
+
+// col2im (gather, deterministic): dcol [B*OH*OW][ldk] fp32 -> dx [B][H][W][C].
+// Optional ReLU-backward mask (keep where mask > 0, mask NHWC like dx).
+template <class TO, class TM>
+void launch_col2im(const float* dcol, TO* dx, const TM* mask, int B, int H, int W, int C, int R,
+                   int S, int stride, int pad, int OH, int OW, long long ldk, cudaStream_t st);
+
+// Overlapping max-pool, floor mode. idx = argmax plane index h*W+w.
+template <class T>
+void launch_maxpool_fwd(const T* x, T* y, int32_t* idx, int B, int H, int W, int C, int k, int s,
+                        int OH, int OW, cudaStream_t st);
+// Gather backward: dx = sum over windows whose argmax is this input.
+template <class TO, class TM>
+void launch_maxpool_bwd(const float* gy, const int32_t* idx, TO* gx, const TM* mask, int B, int H,
+                        int W, int C, int k, int s, int OH, int OW, cudaStream_t st);
+
+// Cross-channel LRN (Krizhevsky 2012; alpha not divided by n).
+template <class T>
+void launch_lrn_fwd(const T* a, T* b, float* d, long long P, int C, int n, float alpha, float beta,
+                    float k, cudaStream_t st);
+template <class TO, class TA>
+void launch_lrn_bwd(const TA* a, const float* d, const float* gb, TO* ga, long long P, int C, int n,
+                    float alpha, float beta, int relu_mask, cudaStream_t st);
+
+// Column sums of x [M][ldx] over rows -> out [N] (ascending row blocks).
+template <class T>
+void launch_colsum(const T* x, long long M, int N, long long ldx, float* out, float* ws,
+                   cudaStream_t st);
+size_t colsum_ws_floats(long long M, int N);
+
+// Row sums of x [R][ldx] (first n columns) -> out [R]; beta: out += sum.
+template <class T>
+void launch_rowsum(const T* x, int R, int n, long long ldx, float* out, int beta, cudaStream_t st);
+
+// Logistic cross-entropy on a feature-major logit shard z [Ls][n] (fp32):
+// targets t [n][L] (columns c0..c0+Ls), grad -> dz [Ls][ldz], per-block
+// double loss partials -> partial[nblocks]. Returns nblocks.
+template <class TO>
+int launch_xent(const float* z, long long ldzin, const float* t, int L, int c0, int Ls, int n,
+                TO* dz, long long ldz, double* partial, int* bad_target, cudaStream_t st);
+int xent_blocks(int Ls, int n);
+
+// Momentum SGD over a list of tensors (optimizer.cpp:19-31, float storage:
+// scalars rounded to float once, four separate rounded passes, no FMA).
+struct SgdTensor {
+  float* w;
+  float* mom;
+  const float* g;
+  void* copy;  // optional: updated w cast to the operand type (bf16 mode)
+  long long n;
+  float gscale;  // grad pre-scale (1/K mean, 1/num_sub): applied as a rounded multiply
+  int has_gscale;
+};
+constexpr int kMaxSgdTensors = 24;
+void launch_sgd(const SgdTensor* ts, int nt, int copy_type, double lr, double momentum,
+                double weight_decay, cudaStream_t st);
+
+template <class T>
+void launch_cast(const float* in, T* out, long long n, cudaStream_t st);
+
+// Logical-transport reductions over K local workers (ascending worker order,
+// the reference's order, cluster.cpp:568-576 / 293-295).
+constexpr int kMaxLocal = 16;
+struct PtrList {
+  const float* p[kMaxLocal];
+};
+struct MutPtrList {
+  float* p[kMaxLocal];
+};
+// out = sum_w in[w] (+ offset), cast to TO, optional scale.
+template <class TO>
+void launch_sum_k(PtrList in, int K, TO* out, long long n, float alpha, cudaStream_t st);
+// bufs[w] = sum_w bufs[w] for all w.
+void launch_allreduce_k(MutPtrList bufs, int K, long long n, cudaStream_t st);
+
+// Strided 2D copy helper: rows of `bytes` from src (stride sp) to dst (stride dp).
+void copy2d(void* dst, long long dp, const void* src, long long sp, long long bytes, long long rows,
+            cudaStream_t st);
+
+// out = (mask == nullptr || mask > 0) ? g : 0, cast to TO (ReLU backward).
+template <class TO, class TM>
+void launch_mask_cast(const float* g, const TM* mask, TO* out, long long n, cudaStream_t st);
+
+// Scale in place (fp32).
+void launch_scale(float* x, long long n, float s, cudaStream_t st);
+
+}  // namespace hp

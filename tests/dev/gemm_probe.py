@@ -40,8 +40,8 @@ def run(math, M, N, K, a_mn, b_mn, epi=None, splits=1, bn=0, seed=0):
     Cb = torch.full((M, ldc), float("nan"), device="cuda", dtype=torch.float32)
     d = HpGemmDesc()
     d.math = math
-    d.a = Ab.data_ptr(); d.a_lo = alo.data_ptr() if alo is not None else None; d.a_mn = a_mn; d.lda = lda
-    d.b = Bb.data_ptr(); d.b_lo = blo.data_ptr() if blo is not None else None; d.b_mn = b_mn; d.ldb = ldb
+    d.a = Ab.data_ptr(); d.a_mn = a_mn; d.lda = lda
+    d.b = Bb.data_ptr(); d.b_mn = b_mn; d.ldb = ldb
     d.M, d.N, d.K = M, N, K
     d.c = Cb.data_ptr(); d.ldc = ldc; d.c_type = 0; d.c_trans = 0; d.alpha = 1.0
     d.splits = splits; d.bn = bn
