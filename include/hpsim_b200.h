@@ -205,13 +205,33 @@ HP_API double hp_cluster_last_step_ms(const hp_cluster* c);
 /* Number of kernels this library launched in the last step. */
 HP_API int64_t hp_cluster_last_step_launches(const hp_cluster* c);
 
+/* ---- instrumentation (bench.py / profiling; not in the reference) -------- */
+/* The CUDA stream every kernel of this cluster is launched on (cudaStream_t). */
+HP_API void* hp_cluster_stream(const hp_cluster* c);
+/* Host<->device bytes the last step copied (inputs in, loss partials out). */
+HP_API void hp_cluster_last_step_io(const hp_cluster* c, int64_t* h2d, int64_t* d2h);
+/* Algorithmic FLOPs (2*M*N*K) of the tcgen05 GEMMs the last step ran. */
+HP_API double hp_cluster_last_gemm_flops(const hp_cluster* c);
+/* Bracket every GEMM with CUDA events on the launching stream (adds event
+ * records; off for timed runs). */
+HP_API int hp_cluster_set_profile(hp_cluster* c, int on);
+/* Per-GEMM record of the last profiled step: tag ("conv_fwd", ...), layer,
+ * FLOPs and event-timed ms. Returns the count. */
+typedef struct hp_gemm_prof {
+  char tag[16];
+  int32_t layer;
+  double flops;
+  double ms;
+} hp_gemm_prof;
+HP_API int hp_cluster_gemm_profile(const hp_cluster* c, hp_gemm_prof* out, int cap);
+
 /* ---- host-side helpers shared with the reference ------------------------ */
 /* shard_range (cluster.cpp:69-75). */
 HP_API void hp_shard_range(int64_t total, int parts, int idx, int64_t* begin, int64_t* end);
 /* GaussianSampler(seed).next() x n (rng.hpp:26-56), replayed on the host. */
 HP_API void hp_gaussian_fill(uint64_t seed, double* out, int64_t n);
 /* Same stream, scaled by `scale`, rounded to float. */
-HP_API void hp_gaussian_fill_f32(uint64_t seed, float scale, float* out, int64_t n);
+HP_API void hp_gaussian_fill_f32(uint64_t seed, double scale, float* out, int64_t n);
 
 /* ---- kernel-level entry points (device pointers, for parity tests) ------
  * Each mirrors one dense kernel of include/hpsim/tensor.hpp:92-139 with the

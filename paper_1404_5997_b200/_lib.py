@@ -93,6 +93,10 @@ class HpStepMetrics(C.Structure):
     ]
 
 
+class HpGemmProf(C.Structure):
+    _fields_ = [("tag", C.c_char * 16), ("layer", C.c_int32), ("flops", C.c_double), ("ms", C.c_double)]
+
+
 class HpGemmDesc(C.Structure):
     _fields_ = [
         ("math", C.c_int32),
@@ -114,14 +118,14 @@ def _load() -> C.CDLL:
         raise ImportError(
             f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
             " (there is no CPU fallback)")
-    lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+    lib = C.CDLL(LIB_PATH)
     P = C.c_void_p
     sigs = {
         "hp_last_error": ([], C.c_char_p),
         "hp_version": ([], C.c_char_p),
         "hp_shard_range": ([C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], None),
         "hp_gaussian_fill": ([C.c_uint64, C.POINTER(C.c_double), C.c_int64], None),
-        "hp_gaussian_fill_f32": ([C.c_uint64, C.c_float, C.POINTER(C.c_float), C.c_int64], None),
+        "hp_gaussian_fill_f32": ([C.c_uint64, C.c_double, C.POINTER(C.c_float), C.c_int64], None),
         "hp_kernel_gemm": ([C.POINTER(HpGemmDesc), P], C.c_int),
         "hp_kernel_gemm_splits": ([C.POINTER(HpGemmDesc)], C.c_int),
     }
@@ -141,6 +145,11 @@ def _load() -> C.CDLL:
         "hp_cluster_set_skip_sync_broadcast": ([P, C.c_int], C.c_int),
         "hp_cluster_last_step_ms": ([P], C.c_double),
         "hp_cluster_last_step_launches": ([P], C.c_int64),
+        "hp_cluster_stream": ([P], C.c_void_p),
+        "hp_cluster_last_step_io": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], None),
+        "hp_cluster_last_gemm_flops": ([P], C.c_double),
+        "hp_cluster_set_profile": ([P, C.c_int], C.c_int),
+        "hp_cluster_gemm_profile": ([P, C.POINTER(HpGemmProf), C.c_int], C.c_int),
     }
     for name, (args, res) in list(sigs.items()) + list(optional.items()):
         fn = getattr(lib, name, None)

@@ -16,8 +16,8 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import (HpClusterConfig, HpConvLayer, HpFcLayer, HpHyper, HpModelSpec, HpStepMetrics,
-                   HpTraceEvent, last_error, lib)
+from ._lib import (HpClusterConfig, HpConvLayer, HpFcLayer, HpGemmProf, HpHyper, HpModelSpec,
+                   HpStepMetrics, HpTraceEvent, last_error, lib)
 
 
 # ---------------------------------------------------------------- errors
@@ -357,6 +357,27 @@ class Cluster:
 
     def last_step_launches(self) -> int:
         return lib.hp_cluster_last_step_launches(self._h)
+
+    def stream_ptr(self) -> int:
+        """cudaStream_t every kernel of this cluster runs on (for CUDA-event timing)."""
+        return lib.hp_cluster_stream(self._h) or 0
+
+    def last_step_io(self):
+        h2d, d2h = C.c_int64(), C.c_int64()
+        lib.hp_cluster_last_step_io(self._h, C.byref(h2d), C.byref(d2h))
+        return h2d.value, d2h.value
+
+    def last_gemm_flops(self) -> float:
+        return lib.hp_cluster_last_gemm_flops(self._h)
+
+    def set_profile(self, on: bool) -> None:
+        _check(lib.hp_cluster_set_profile(self._h, int(bool(on))))
+
+    def gemm_profile(self):
+        """[(tag, layer, flops, ms)] for the last profiled step, launch order."""
+        buf = (HpGemmProf * 4096)()
+        k = lib.hp_cluster_gemm_profile(self._h, buf, 4096)
+        return [(e.tag.decode(), e.layer, e.flops, e.ms) for e in buf[:k]]
 
 
 # ---------------------------------------------------------------- host helpers

@@ -101,4 +101,29 @@ HP_API int hp_cluster_set_skip_sync_broadcast(hp_cluster* c, int v) {
 HP_API double hp_cluster_last_step_ms(const hp_cluster* c) { return c->impl->last_ms; }
 HP_API int64_t hp_cluster_last_step_launches(const hp_cluster* c) { return c->impl->last_launches; }
 
+HP_API void* hp_cluster_stream(const hp_cluster* c) { return c->impl->stream(); }
+
+HP_API void hp_cluster_last_step_io(const hp_cluster* c, int64_t* h2d, int64_t* d2h) {
+  *h2d = c->impl->io_h2d;
+  *d2h = c->impl->io_d2h;
+}
+
+HP_API double hp_cluster_last_gemm_flops(const hp_cluster* c) { return c->impl->last_gemm_flops; }
+
+HP_API int hp_cluster_set_profile(hp_cluster* c, int on) {
+  return guarded_c([&] { c->impl->profile = on != 0; });
+}
+
+HP_API int hp_cluster_gemm_profile(const hp_cluster* c, hp_gemm_prof* out, int cap) {
+  const auto& p = c->impl->prof;
+  for (int i = 0; i < static_cast<int>(p.size()) && i < cap; ++i) {
+    std::memset(out[i].tag, 0, sizeof out[i].tag);
+    std::strncpy(out[i].tag, p[i].tag, sizeof out[i].tag - 1);
+    out[i].layer = p[i].layer;
+    out[i].flops = p[i].flops;
+    out[i].ms = p[i].ms;
+  }
+  return static_cast<int>(p.size());
+}
+
 }  // extern "C"

@@ -46,7 +46,7 @@ HP_API void hp_gaussian_fill(uint64_t seed, double* out, int64_t n) {
   for (int64_t i = 0; i < n; ++i) out[i] = g.next();
 }
 
-HP_API void hp_gaussian_fill_f32(uint64_t seed, float scale, float* out, int64_t n) {
+HP_API void hp_gaussian_fill_f32(uint64_t seed, double scale, float* out, int64_t n) {
   GaussianSampler g(seed);
   const double s = scale;
   for (int64_t i = 0; i < n; ++i) out[i] = static_cast<float>(s * g.next());

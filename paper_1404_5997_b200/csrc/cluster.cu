@@ -210,6 +210,7 @@ class ClusterImpl final : public ClusterBase {
  public:
   ClusterImpl(const hp_model_spec* spec, const hp_cluster_config* cfg);
   ~ClusterImpl() override;
+  void* stream() const override { return st_; }
   void run_step(const float* const* batches, const float* const* targets, int mem_kind,
                 const hp_hyper& hp, double lr, hp_step_metrics* out) override;
   int64_t param_size(int worker, int which, int layer) const override;
@@ -230,6 +231,8 @@ class ClusterImpl final : public ClusterBase {
   void sgd_fc(double lr, float gscale, bool has_gscale, const hp_hyper& hp);
   void sgd_conv(double lr, const hp_hyper& hp);
   void account(int num_sub, hp_step_metrics* out);
+  void gemm(const GemmPlan& p, const char* tag, int layer);
+  void collect_profile();
   // param layout helpers
   long long conv_k_off(int l) const { return coff_[l]; }
   long long conv_b_off(int l) const { return coff_[l] + static_cast<long long>(g_.cg[l].F) * g_.cg[l].ldk; }
@@ -257,6 +260,15 @@ class ClusterImpl final : public ClusterBase {
   size_t ws_floats_ = 0;
   int xblocks_ = 0;
   int64_t launches_ = 0;
+  struct ProfSlot {
+    cudaEvent_t a, b;
+    const char* tag;
+    int layer;
+    double flops;
+  };
+  std::vector<ProfSlot> prof_pool_;
+  size_t prof_used_ = 0;
+  double gemm_flops_ = 0.0;
 };
 
 template <class TA>
@@ -382,6 +394,10 @@ ClusterImpl<TA>::~ClusterImpl() {
   comm_.reset();
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
+  for (auto& s : prof_pool_) {
+    cudaEventDestroy(s.a);
+    cudaEventDestroy(s.b);
+  }
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -509,6 +525,45 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
   }
 }
 
+// Every tcgen05 GEMM of the step goes through here: launch, count, and (when
+// profiling) bracket with CUDA events on the launching stream.
+template <class TA>
+void ClusterImpl<TA>::gemm(const GemmPlan& p, const char* tag, int layer) {
+  const double flops = 2.0 * p.args.M * static_cast<double>(p.args.N) * p.args.K;
+  if (profile) {
+    if (prof_used_ == prof_pool_.size()) {
+      ProfSlot s{};
+      HP_CUDA(cudaEventCreate(&s.a));
+      HP_CUDA(cudaEventCreate(&s.b));
+      prof_pool_.push_back(s);
+    }
+    ProfSlot& s = prof_pool_[prof_used_++];
+    s.tag = tag;
+    s.layer = layer;
+    s.flops = flops;
+    HP_CUDA(cudaEventRecord(s.a, st_));
+    gemm_launch(p, st_);
+    HP_CUDA(cudaEventRecord(s.b, st_));
+  } else {
+    gemm_launch(p, st_);
+  }
+  launches_ += p.splits > 1 ? 2 : 1;
+  gemm_flops_ += flops;
+}
+
+template <class TA>
+void ClusterImpl<TA>::collect_profile() {
+  prof.clear();
+  prof_gemm_ms = 0.0;
+  for (size_t i = 0; i < prof_used_; ++i) {
+    float ms = 0.f;
+    HP_CUDA(cudaEventElapsedTime(&ms, prof_pool_[i].a, prof_pool_[i].b));
+    prof.push_back({prof_pool_[i].tag, prof_pool_[i].layer, prof_pool_[i].flops, ms});
+    prof_gemm_ms += ms;
+  }
+  prof_used_ = 0;
+}
+
 template <class TA>
 long long ClusterImpl<TA>::fc_col(int l, long long i) const {
   if (l == 0) {
@@ -585,8 +640,8 @@ void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
     const ConvGeom& c = g_.cg[l];
     launch_im2col<TA>(x, w.col[l], static_cast<int>(b_), c.H, c.W, c.C, c.R, c.S, c.stride, c.pad,
                       c.OH, c.OW, c.ldk, st_);
-    gemm_launch(w.conv_fwd[l], st_);
-    launches_ += 1 + (w.conv_fwd[l].splits > 1 ? 2 : 1);
+    gemm(w.conv_fwd[l], "conv_fwd", l);
+    ++launches_;
     const TA* out = w.act[l];
     if (c.lrn_n > 0) {
       launch_lrn_fwd<TA>(w.act[l], w.lrn[l], w.lrn_d[l], c.P, c.F, c.lrn_n, c.lrn_alpha, c.lrn_beta,
@@ -659,8 +714,7 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
   const int nl = comm_->nlocal();
   for (int l = 0; l < nf; ++l) {
     for (auto& w : w_) {
-      gemm_launch(w.fc_fwd[l], st_);
-      launches_ += w.fc_fwd[l].splits > 1 ? 2 : 1;
+      gemm(w.fc_fwd[l], "fc_fwd", l);
     }
     if (l + 1 < nf && K_ > 1) {
       std::vector<void*> bufs(nl);
@@ -683,10 +737,10 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
       const int rows = static_cast<int>(f.c1[w.gid] - f.c0[w.gid]);
       GemmPlan pw = w.fc_wgrad[li];
       pw.args.epi.beta = beta ? 1 : 0;
-      gemm_launch(pw, st_);
+      gemm(pw, "fc_wgrad", li);
       launch_rowsum<TA>(w.fdz[li], rows, static_cast<int>(n_), ldn_, w.fgr + fc_b_off(li), beta ? 1 : 0, st_);
-      gemm_launch(w.fc_dgrad[li], st_);
-      launches_ += (pw.splits > 1 ? 2 : 1) + 1 + (w.fc_dgrad[li].splits > 1 ? 2 : 1);
+      gemm(w.fc_dgrad[li], "fc_dgrad", li);
+      ++launches_;
     }
     if (li > 0 && K_ > 1) {
       std::vector<const float*> send(nl);
@@ -763,11 +817,10 @@ void ClusterImpl<TA>::conv_backward(Worker<TA>& w) {
     }
     // bias grad = channel sums of dz (model.cpp:184-202)
     launch_colsum<TA>(w.dz[l], c.P, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, st_);
-    gemm_launch(w.conv_wgrad[l], st_);
-    launches_ += 2 + (w.conv_wgrad[l].splits > 1 ? 2 : 1);
+    gemm(w.conv_wgrad[l], "conv_wgrad", l);
+    launches_ += 2;
     if (l > 0) {
-      gemm_launch(w.conv_dgrad[l], st_);
-      launches_ += w.conv_dgrad[l].splits > 1 ? 2 : 1;
+      gemm(w.conv_dgrad[l], "conv_dgrad", l);
       const ConvGeom& pc = g_.cg[l - 1];
       if (pc.pk > 0 || pc.lrn_n > 0) {
         launch_col2im<float, TA>(w.dcol[l], w.gstage[l - 1], nullptr, B, c.H, c.W, c.C, c.R, c.S,
@@ -846,6 +899,9 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
   const auto& in = g_.input;
   const long long xin = b_ * in[0] * in[1] * in[2];
   launches_ = 0;
+  gemm_flops_ = 0.0;
+  prof_used_ = 0;
+  io_h2d = io_d2h = 0;
   HP_CUDA(cudaEventRecord(ev0_, st_));
   for (int i = 0; i < nl; ++i) {
     Worker<TA>& w = w_[i];
@@ -853,6 +909,7 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
     if (mem_kind == HP_MEM_HOST) {
       HP_CUDA(cudaMemcpyAsync(w.x_nchw, batches[i], xin * sizeof(float), cudaMemcpyHostToDevice, st_));
       HP_CUDA(cudaMemcpyAsync(w.targets, targets[i], b_ * L_ * sizeof(float), cudaMemcpyHostToDevice, st_));
+      io_h2d += (xin + b_ * L_) * static_cast<int64_t>(sizeof(float));
       src = w.x_nchw;
     } else {
       HP_CUDA(cudaMemcpyAsync(w.targets, targets[i], b_ * L_ * sizeof(float), cudaMemcpyDeviceToDevice, st_));
@@ -896,6 +953,7 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
     HP_CUDA(cudaMemcpyAsync(tmp.data(), w_[i].loss_parts, tmp.size() * sizeof(double),
                             cudaMemcpyDeviceToHost, st_));
     HP_CUDA(cudaMemcpyAsync(&bad[i], w_[i].bad, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    io_d2h += static_cast<int64_t>(tmp.size() * sizeof(double) + sizeof(int));
     HP_CUDA(cudaStreamSynchronize(st_));
     for (size_t e = 0; e < parts.size(); ++e) parts[e] += tmp[e];
   }
@@ -904,6 +962,8 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
   HP_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
   last_ms = ms;
   last_launches = launches_;
+  last_gemm_flops = gemm_flops_;
+  if (profile) collect_profile();
   for (int i = 0; i < nl; ++i)
     if (bad[i]) domain_error("logistic_xent: target outside [0,1]");
   double loss_weighted = 0.0;

@@ -60,6 +60,20 @@ class ClusterBase {
   virtual void gather_model(float* const* ck, float* const* cb, float* const* fw,
                             float* const* fb) = 0;
 
+  virtual void* stream() const = 0;
+
+  struct GemmProf {
+    const char* tag;
+    int layer;
+    double flops;
+    float ms;
+  };
+  bool profile = false;            // bracket every GEMM with CUDA events
+  std::vector<GemmProf> prof;      // last step, launch order
+  double prof_gemm_ms = 0.0;
+  double last_gemm_flops = 0.0;    // algorithmic GEMM FLOPs of the last step
+  int64_t io_h2d = 0, io_d2h = 0;  // bytes copied host<->device by the last step
+
   std::vector<hp_trace_event> trace;
   std::vector<std::array<int64_t, 4>> sent, received;  // per worker (all K)
   bool skip_sync_broadcast = false;

@@ -1,0 +1,107 @@
+"""Step parity: the B200 run_step (C ABI) against the CPU oracle on identical
+inputs and seeds. The oracle restates the reference in double (pinned
+bit-exactly to the compiled reference in tests/test_oracle_vs_reference.py).
+
+Tolerances (stated; max |gpu - oracle| / max |oracle| per parameter tensor
+after the steps, weights and momenta; loss relative):
+  f32x3 (3xTF32, parity mode):   params/momenta 2e-5, loss 1e-8
+  tf32:                          momenta 8e-2, weights 1e-4, loss 1e-5
+  bf16:                          momenta 3e-1, weights 5e-4, loss 1e-4
+(momenta after two steps are pure gradient history, so they carry the GEMM
+input rounding undiluted; bf16 has 8 mantissa bits.)
+Integer outputs (byte counters, trace, update counts) must be identical."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+import paper_1404_5997_b200 as hp  # noqa: E402
+from helpers import rel_err  # noqa: E402
+
+TOL = {hp.MathMode.F32X3: (2e-5, 2e-5, 1e-8), hp.MathMode.TF32: (8e-2, 1e-4, 1e-5),
+       hp.MathMode.BF16: (3e-1, 5e-4, 1e-4)}
+
+
+def compare(spec, K, scheme, var, math, b, steps=2, lr=0.05, wscale=1.0, seed=1):
+    cfg = hp.ClusterConfig(workers=K, per_worker_batch=b, scheme=hp.Scheme.from_string(scheme),
+                           variable_batch=var, seed=seed, math_mode=math)
+    g = hp.Cluster(spec, cfg)
+    o = O.OracleCluster(spec, workers=K, per_worker_batch=b, scheme=scheme, variable_batch=var,
+                        precision="single", seed=seed)
+    nl = lambda which: len(spec.conv_layers) if (which & 3) < 2 else len(spec.fc_layers)
+    for w in range(K):  # identical initial parameters (GaussianSampler replay + layout permutations)
+        for which in range(4):
+            for l in range(nl(which)):
+                a = g.param(w, which, l)
+                assert np.array_equal(a.astype(np.float64), o.param(w, which, l))
+                if wscale != 1.0 and which in (0, 2):
+                    g.write_param(w, which, l, a * wscale)
+                    o.write_param(w, which, l, (a * wscale).astype(np.float64))
+    hpg = hp.HyperParams(momentum=0.9, lr=lr, weight_decay=5e-4)
+    hpo = O.make_hyper_c(0.9, lr, 5e-4)
+    mt, wt, lt = TOL[math]
+    for s in range(steps):
+        xs, ts = zip(*[hp.synthetic_batch(spec, b, step=s, worker=w) for w in range(K)])
+        r = g.run_step(list(xs), list(ts), hpg)
+        m = o.run_step([x.astype(np.float64) for x in xs], [t.astype(np.float64) for t in ts], hpo)
+        assert abs(r.metrics.loss - m.loss) <= lt * abs(m.loss), (r.metrics.loss, m.loss)
+        assert list(r.metrics.bytes_sent) == list(m.bytes_sent)
+        assert [(e.phase, e.sub_batch, e.worker, e.bytes_total, e.bytes_max_sender) for e in r.trace] == o.trace()
+        assert r.metrics.fc_update_count == m.fc_update_count
+        assert r.metrics.conv_update_count == m.conv_update_count
+    for w in range(K):
+        assert g.worker_bytes(w) == o.worker_bytes(w)
+        for which in range(8):
+            for l in range(nl(which)):
+                e = rel_err(g.param(w, which, l), o.param(w, which, l))
+                assert e <= (mt if which >= 4 else wt), (w, which, l, e)
+    # replica consistency: conv replicas identical across workers
+    for w in range(1, K):
+        for l in range(len(spec.conv_layers)):
+            assert np.array_equal(g.param(w, 0, l), g.param(0, 0, l))
+    return g, o
+
+
+@pytest.mark.parametrize("math", [hp.MathMode.F32X3, hp.MathMode.TF32, hp.MathMode.BF16])
+def test_tiny_k1(math):
+    """configs[0]: tiny CNN, K=1 (b=32 here for time; b=128 in test_tiny_configs)."""
+    compare(hp.tiny_cnn(), 1, "B", False, math, 32)
+
+
+@pytest.mark.parametrize("K,scheme,var", [(2, "A", False), (2, "B", False), (2, "C", True), (4, "B", True),
+                                          (4, "C", False), (4, "A", False), (3, "B", False)])
+def test_tiny_schemes(K, scheme, var):
+    """Scheme routing, uneven fc shards (K=3: 85/85/86, K=4: 10 -> 2/2/2/4), variable mode."""
+    compare(hp.tiny_cnn(), K, scheme, var, hp.MathMode.F32X3, 12 if K == 3 else 16)
+
+
+@pytest.mark.parametrize("math", [hp.MathMode.F32X3, hp.MathMode.BF16])
+def test_tiny_configs(math):
+    """configs[0..1] at their full size: K=1 b=128, and K=2 scheme A exact b=128."""
+    compare(hp.tiny_cnn(), 1, "B", False, math, 128, steps=1)
+    compare(hp.tiny_cnn(), 2, "A", False, math, 128, steps=1)
+
+
+def test_active_relus():
+    """Weights x30 so most ReLUs are active and the gradients are large."""
+    compare(hp.tiny_cnn(), 2, "C", False, hp.MathMode.F32X3, 8, steps=2, lr=0.001, wscale=30.0)
+
+
+@pytest.mark.parametrize("K,scheme,var", [(1, "B", False), (2, "C", True)])
+def test_alexnet_small_batch(K, scheme, var):
+    """AlexNet-1col (LRN, overlapping pool, floor-mode conv1) at b=2 per worker in 3xTF32."""
+    compare(hp.alexnet_1col(), K, scheme, var, hp.MathMode.F32X3, 2, steps=1, lr=0.01)
+
+
+def test_alexnet_bf16_loss_and_io():
+    """Full AlexNet b=128 bf16 step runs; loss ~ L*ln2 at init; host inputs counted."""
+    spec = hp.alexnet_1col()
+    g = hp.Cluster(spec, hp.ClusterConfig(workers=1, per_worker_batch=128, math_mode=hp.MathMode.BF16, seed=1))
+    x, t = hp.synthetic_batch(spec, 128)
+    r = g.run_step([x], [t], hp.HyperParams(lr=0.01, weight_decay=5e-4))
+    assert abs(r.metrics.loss - 1000 * np.log(2)) < 1.0
+    h2d, d2h = g.last_step_io()
+    assert h2d == x.nbytes + t.nbytes and d2h > 0
+    assert g.last_step_launches() > 20
+    assert g.last_gemm_flops() > 5e11  # ~626 GFLOP algorithmic
