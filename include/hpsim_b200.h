@@ -226,6 +226,14 @@ typedef struct hp_gemm_prof {
 HP_API int hp_cluster_gemm_profile(const hp_cluster* c, hp_gemm_prof* out, int cap);
 
 /* ---- host-side helpers shared with the reference ------------------------ */
+/* Analytic byte counters + phase trace of `steps` steps (cluster.cpp:466-673)
+ * without running anything: validates spec/config like hp_cluster_create,
+ * fills bytes_sent[4] (summed over steps), the last step's trace, and the
+ * per-worker cumulative ByteCounters (worker_sent / worker_received: K*4).
+ * This is the host logic every rank runs for all K workers. */
+HP_API int hp_step_accounting(const hp_model_spec* spec, const hp_cluster_config* cfg, int steps,
+                              int64_t bytes_sent[4], hp_trace_event* trace, int cap, int* n_events,
+                              int64_t* worker_sent, int64_t* worker_received);
 /* shard_range (cluster.cpp:69-75). */
 HP_API void hp_shard_range(int64_t total, int parts, int idx, int64_t* begin, int64_t* end);
 /* GaussianSampler(seed).next() x n (rng.hpp:26-56), replayed on the host. */
@@ -251,6 +259,24 @@ typedef struct hp_gemm_desc {
 /* D = A * B^T on tcgen05 (replaces matmul/_tn/_nt, tensor.cpp:254-305). */
 HP_API int hp_kernel_gemm(const hp_gemm_desc* d, void* stream);
 HP_API int hp_kernel_gemm_splits(const hp_gemm_desc* d);
+
+/* Implicit-GEMM convolution on tcgen05 with TMA im2col operand loads (no
+ * im2col buffer); NHWC activations in the operand type (bf16 for
+ * HP_MATH_BF16, fp32 otherwise), fp32 outputs. C must be a multiple of 128
+ * bytes of operand (64 bf16 / 32 fp32 channels). Replaces conv2d_forward /
+ * conv2d_backward (tensor.cpp:419-516, 520-552).
+ *   fprop: y[B*OH*OW][F] = conv(x[B][H][W][C], w[F][R][S][C])
+ *   wgrad: dw[F][R*S*C]  = sum_pixels dy[B*OH*OW][F] (x) im2col(x)
+ *   dgrad (stride 1): dx[B*H*W][C] = conv(dy[B][OH][OW][F], wrot[C][R][S][F]) with
+ *         wrot[c][r][s][f] = w[f][R-1-r][S-1-s][c] and padding R-1-pad. */
+HP_API int hp_kernel_conv_fprop(int math, const void* x, int B, int H, int W, int C, const void* w,
+                                int F, int R, int S, int stride, int pad, float* y, void* stream);
+HP_API int hp_kernel_conv_wgrad(int math, const void* x, int B, int H, int W, int C, const void* dy,
+                                int F, int R, int S, int stride, int pad, float* dw, float* ws,
+                                int64_t ws_floats, void* stream);
+HP_API int hp_kernel_conv_dgrad(int math, const void* dy, int B, int OH, int OW, int F,
+                                const void* wrot, int C, int R, int S, int pad, float* dx,
+                                void* stream);
 
 #ifdef __cplusplus
 }

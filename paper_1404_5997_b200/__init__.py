@@ -7,7 +7,7 @@ from ._lib import LIB_PATH, lib  # noqa: F401  (raises ImportError when the .so 
 from .api import (Cluster, ClusterConfig, ConfigError, ConvLayerSpec, CudaError, DimensionError,  # noqa: F401
                   DomainError, FcLayerSpec, HpsimError, HyperParams, MathMode, ModelSpec, MsgClass, NcclError,
                   Phase, Precision, Scheme, StepMetrics, StepResult, TraceEvent, Transport, UsageError,
-                  gaussian, gaussian_f32, nccl_unique_id, shard_range)
+                  gaussian, gaussian_f32, nccl_unique_id, shard_range, step_accounting)
 from .specs import alexnet_1col, alexnet_standin_227, synthetic_batch, tiny_cnn  # noqa: F401
 
 __version__ = "0.1.0"

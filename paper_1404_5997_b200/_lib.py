@@ -128,6 +128,12 @@ def _load() -> C.CDLL:
         "hp_gaussian_fill_f32": ([C.c_uint64, C.c_double, C.POINTER(C.c_float), C.c_int64], None),
         "hp_kernel_gemm": ([C.POINTER(HpGemmDesc), P], C.c_int),
         "hp_kernel_gemm_splits": ([C.POINTER(HpGemmDesc)], C.c_int),
+        "hp_kernel_conv_fprop": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int,
+                                  C.c_int, C.c_int, C.c_int, P, P], C.c_int),
+        "hp_kernel_conv_wgrad": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int,
+                                  C.c_int, C.c_int, C.c_int, P, P, C.c_int64, P], C.c_int),
+        "hp_kernel_conv_dgrad": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int,
+                                  C.c_int, C.c_int, P, P], C.c_int),
     }
     optional = {
         "hp_cluster_create": ([C.POINTER(HpModelSpec), C.POINTER(HpClusterConfig), C.POINTER(P)], C.c_int),
@@ -146,6 +152,9 @@ def _load() -> C.CDLL:
         "hp_cluster_last_step_ms": ([P], C.c_double),
         "hp_cluster_last_step_launches": ([P], C.c_int64),
         "hp_cluster_stream": ([P], C.c_void_p),
+        "hp_step_accounting": ([C.POINTER(HpModelSpec), C.POINTER(HpClusterConfig), C.c_int,
+                                C.POINTER(C.c_int64), C.POINTER(HpTraceEvent), C.c_int, C.POINTER(C.c_int),
+                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
         "hp_cluster_last_step_io": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], None),
         "hp_cluster_last_gemm_flops": ([P], C.c_double),
         "hp_cluster_set_profile": ([P, C.c_int], C.c_int),

@@ -381,6 +381,26 @@ class Cluster:
 
 
 # ---------------------------------------------------------------- host helpers
+def step_accounting(spec: ModelSpec, config: ClusterConfig, steps: int = 1):
+    """Analytic byte counters and trace (cluster.cpp:466-673) without a GPU:
+    (bytes_sent[4], trace, [(sent[4], received[4]) per worker])."""
+    sc, keep = _spec_c(spec)
+    cfg = HpClusterConfig()
+    cfg.workers, cfg.per_worker_batch = config.workers, config.per_worker_batch
+    cfg.scheme, cfg.variable_batch = int(config.scheme), int(bool(config.variable_batch))
+    cfg.precision, cfg.seed, cfg.math_mode = int(config.precision), config.seed, int(config.math_mode)
+    bs = (C.c_int64 * 4)()
+    tr = (HpTraceEvent * 512)()
+    ne = C.c_int()
+    K = config.workers
+    ws, wr = (C.c_int64 * (4 * K))(), (C.c_int64 * (4 * K))()
+    _check(lib.hp_step_accounting(C.byref(sc), C.byref(cfg), steps, bs, tr, 512, C.byref(ne), ws, wr))
+    trace = [(e.phase, e.sub_batch, e.worker, e.bytes_total, e.bytes_max_sender) for e in tr[:ne.value]]
+    per = [(list(ws[4 * w:4 * w + 4]), list(wr[4 * w:4 * w + 4])) for w in range(K)]
+    return list(bs), trace, per
+
+
+
 def shard_range(total: int, parts: int, idx: int):
     b, e = C.c_int64(), C.c_int64()
     lib.hp_shard_range(total, parts, idx, C.byref(b), C.byref(e))

@@ -101,6 +101,33 @@ HP_API int hp_cluster_set_skip_sync_broadcast(hp_cluster* c, int v) {
 HP_API double hp_cluster_last_step_ms(const hp_cluster* c) { return c->impl->last_ms; }
 HP_API int64_t hp_cluster_last_step_launches(const hp_cluster* c) { return c->impl->last_launches; }
 
+HP_API int hp_step_accounting(const hp_model_spec* spec, const hp_cluster_config* cfg, int steps,
+                              int64_t bytes_sent[4], hp_trace_event* trace, int cap, int* n_events,
+                              int64_t* worker_sent, int64_t* worker_received) {
+  return guarded_c([&] {
+    if (!spec || !cfg) usage_error("hp_step_accounting: null argument");
+    if (cfg->workers < 1) config_error("cluster.workers: must be >= 1");
+    if (cfg->per_worker_batch < 1) config_error("cluster.per_worker_batch: must be >= 1");
+    if (cfg->scheme == HP_SCHEME_C && cfg->per_worker_batch % cfg->workers != 0)
+      config_error("cluster.per_worker_batch: scheme C scatters b/K examples per worker per turn; " +
+                   std::to_string(cfg->per_worker_batch) + " is not divisible by " +
+                   std::to_string(cfg->workers));
+    Geometry g = make_geometry(spec, cfg->workers, cfg->per_worker_batch);
+    std::vector<std::array<int64_t, 4>> sent(cfg->workers, {0, 0, 0, 0}), recv(cfg->workers, {0, 0, 0, 0});
+    std::vector<hp_trace_event> tr;
+    for (int i = 0; i < 4; ++i) bytes_sent[i] = 0;
+    for (int s = 0; s < steps; ++s)
+      step_accounting(g, cfg->workers, cfg->per_worker_batch, cfg->scheme, sent, recv, tr, bytes_sent);
+    *n_events = static_cast<int>(tr.size());
+    for (int i = 0; i < static_cast<int>(tr.size()) && i < cap; ++i) trace[i] = tr[i];
+    for (int w = 0; w < cfg->workers; ++w)
+      for (int i = 0; i < 4; ++i) {
+        worker_sent[w * 4 + i] = sent[w][i];
+        worker_received[w * 4 + i] = recv[w][i];
+      }
+  });
+}
+
 HP_API void* hp_cluster_stream(const hp_cluster* c) { return c->impl->stream(); }
 
 HP_API void hp_cluster_last_step_io(const hp_cluster* c, int64_t* h2d, int64_t* d2h) {

@@ -89,4 +89,68 @@ HP_API int hp_kernel_gemm(const hp_gemm_desc* d, void* stream) {
   });
 }
 
+
+static int conv_out(int in, int k, int s, int p) { return (in + 2 * p - k) / s + 1; }
+
+HP_API int hp_kernel_conv_fprop(int math, const void* x, int B, int H, int W, int C, const void* w,
+                                int F, int R, int S, int stride, int pad, float* y, void* stream) {
+  return guarded([&] {
+    GemmOperand a, b;
+    a.ptr = x;
+    a.conv = Im2col{1, B, H, W, C, R, S, stride, pad, conv_out(H, R, stride, pad), conv_out(W, S, stride, pad)};
+    b.ptr = w;
+    b.ld = static_cast<long long>(R) * S * C;
+    Epi e;
+    e.c = y;
+    e.ldc = F;
+    const int M = B * a.conv.OH * a.conv.OW;
+    GemmPlan p = gemm_plan(math, a, b, M, F, R * S * C, e, 1, nullptr, 0);
+    gemm_launch(p, static_cast<cudaStream_t>(stream));
+    HP_CUDA(cudaGetLastError());
+  });
+}
+
+HP_API int hp_kernel_conv_wgrad(int math, const void* x, int B, int H, int W, int C, const void* dy,
+                                int F, int R, int S, int stride, int pad, float* dw, float* ws,
+                                int64_t ws_floats, void* stream) {
+  return guarded([&] {
+    const int OH = conv_out(H, R, stride, pad), OW = conv_out(W, S, stride, pad);
+    GemmOperand a, b;
+    a.ptr = dy;
+    a.mn_major = 1;
+    a.ld = F;
+    b.ptr = x;
+    b.mn_major = 1;
+    b.conv = Im2col{1, B, H, W, C, R, S, stride, pad, OH, OW};
+    Epi e;
+    e.c = dw;
+    e.ldc = static_cast<long long>(R) * S * C;
+    const int N = R * S * C, K = B * OH * OW;
+    int splits = gemm_choose_splits(math, F, N, K);
+    if (static_cast<int64_t>(splits) * F * N > ws_floats) splits = 1;
+    GemmPlan p = gemm_plan(math, a, b, F, N, K, e, splits, ws, 0);
+    gemm_launch(p, static_cast<cudaStream_t>(stream));
+    HP_CUDA(cudaGetLastError());
+  });
+}
+
+HP_API int hp_kernel_conv_dgrad(int math, const void* dy, int B, int OH, int OW, int F,
+                                const void* wrot, int C, int R, int S, int pad, float* dx,
+                                void* stream) {
+  return guarded([&] {
+    const int H = OH + R - 1 - 2 * pad, W = OW + S - 1 - 2 * pad;
+    GemmOperand a, b;
+    a.ptr = dy;
+    a.conv = Im2col{1, B, OH, OW, F, R, S, 1, R - 1 - pad, H, W};
+    b.ptr = wrot;
+    b.ld = static_cast<long long>(R) * S * F;
+    Epi e;
+    e.c = dx;
+    e.ldc = C;
+    GemmPlan p = gemm_plan(math, a, b, B * H * W, C, R * S * F, e, 1, nullptr, 0);
+    gemm_launch(p, static_cast<cudaStream_t>(stream));
+    HP_CUDA(cudaGetLastError());
+  });
+}
+
 }  // extern "C"

@@ -150,6 +150,88 @@ Geometry make_geometry(const hp_model_spec* s, int K, long long b) {
   return g;
 }
 
+void step_accounting(const Geometry& g_, int K, long long b, int scheme_,
+                     std::vector<std::array<int64_t, 4>>& sent,
+                     std::vector<std::array<int64_t, 4>>& received, std::vector<hp_trace_event>& trace,
+                     int64_t* bytes_sent) {
+  const long long elt = 4, row_bytes = g_.A * elt;
+  const int num_sub = scheme_ == HP_SCHEME_A ? 1 : K;
+  const long long n_ = scheme_ == HP_SCHEME_A ? K * b : b;
+  auto charge = [&](int i, int cls, long long s, long long r) {
+    sent[i][cls] += s;
+    received[i][cls] += r;
+    bytes_sent[cls] += s;
+  };
+  auto ex_sent = [&](int j, int i) -> long long {
+    if (K <= 1) return 0;
+    if (scheme_ == HP_SCHEME_A) return (K - 1) * b * row_bytes;
+    if (scheme_ == HP_SCHEME_B) return i == j ? (K - 1) * b * row_bytes : 0;
+    return (K - 1) * (b / K) * row_bytes;
+  };
+  const long long n = n_;
+  std::vector<hp_trace_event> fwd(num_sub), bwd(num_sub);
+  for (int j = 0; j < num_sub; ++j) {
+    long long total = 0, mx = 0;
+    for (int i = 0; i < K; ++i) {
+      long long inbound = 0;
+      if (K > 1) inbound = scheme_ == HP_SCHEME_B ? (i == j ? 0 : b * row_bytes) : ex_sent(j, i);
+      charge(i, HP_MSG_FC_ACTIVATIONS, ex_sent(j, i), inbound);
+      total += ex_sent(j, i);
+      mx = std::max(mx, ex_sent(j, i));
+    }
+    fwd[j] = {HP_PHASE_FC_FWD, j, scheme_ == HP_SCHEME_B ? j : -1, total, mx};
+    for (size_t l = 0; l < g_.fg.size(); ++l) {
+      const FcGeom& f = g_.fg[l];
+      for (int i = 0; i < K; ++i) {
+        const long long ns = f.c1[i] - f.c0[i];
+        charge(i, HP_MSG_FC_INTERNAL, (K - 1) * n * ns * elt, n * (f.out - ns) * elt);
+      }
+    }
+    for (size_t li = g_.fg.size(); li-- > 1;) {
+      const long long part = n * g_.fg[li].in * elt;
+      for (int i = 0; i < K; ++i) charge(i, HP_MSG_FC_INTERNAL, (K - 1) * part, (K - 1) * part);
+    }
+  }
+  for (int j = 0; j < num_sub; ++j) {
+    long long total = 0, mx = 0;
+    for (int i = 0; i < K; ++i) {
+      long long s = 0;
+      if (scheme_ == HP_SCHEME_A) s = K > 1 ? (K - 1) * b * row_bytes : 0;
+      else if (scheme_ == HP_SCHEME_B) s = i != j ? b * row_bytes : 0;
+      else s = K > 1 ? (K - 1) * (b / K) * row_bytes : 0;
+      long long r = s;
+      if (scheme_ == HP_SCHEME_B) r = (i == j && K > 1) ? (K - 1) * b * row_bytes : 0;
+      charge(i, HP_MSG_FC_GRADIENTS, s, r);
+      total += s;
+      mx = std::max(mx, s);
+    }
+    bwd[j] = {HP_PHASE_FC_BWD, j, scheme_ == HP_SCHEME_B ? j : -1, total, mx};
+  }
+  trace.clear();
+  trace.push_back({HP_PHASE_CONV_FWD, -1, -1, 0, 0});
+  for (int j = 0; j < num_sub; ++j) {
+    trace.push_back(fwd[j]);
+    trace.push_back(bwd[j]);
+  }
+  trace.push_back({HP_PHASE_CONV_BWD, -1, -1, 0, 0});
+  long long G = 0;
+  for (const auto& c : g_.cg) G += static_cast<long long>(c.F) * c.Kc + c.F;
+  long long total = 0, mx = 0;
+  for (int i = 0; i < K; ++i) {
+    long long s = 0;
+    if (K > 1) {
+      long long s0, s1;
+      shard(G, K, i, &s0, &s1);
+      const long long shard_bytes = (s1 - s0) * elt;
+      s = (G * elt - shard_bytes) + (K - 1) * shard_bytes;
+    }
+    charge(i, HP_MSG_CONV_SYNC, s, s);
+    total += s;
+    mx = std::max(mx, s);
+  }
+  trace.push_back({HP_PHASE_SYNC, -1, -1, total, mx});
+}
+
 namespace {
 
 struct DevArena {
@@ -183,8 +265,9 @@ struct Worker {
   // conv stack
   std::vector<TA*> col, act, lrn, pool, dz;
   std::vector<float*> lrn_d, dcol, gstage;
-  std::vector<int32_t*> pidx;
-  float* gtmp = nullptr;
+  std::vector<uint8_t*> widx;  // pool argmax as window offset
+  std::vector<TA*> wrot;        // rotated kernels [C][R][S][F] (implicit dgrad)
+  const float* x_src = nullptr; // this step's NCHW batch (device)
   // conv params: [kernels F x ldk | bias F] per layer, one arena
   float *cp = nullptr, *cm = nullptr, *cgr = nullptr;
   TA* cpt = nullptr;  // operand copy (bf16 mode)
@@ -224,6 +307,8 @@ class ClusterImpl final : public ClusterBase {
   const Worker<TA>* local_or_null(int gid) const;
   void build_plans(Worker<TA>& w);
   void conv_forward(Worker<TA>& w);
+  const TA* stage_in(const Worker<TA>& w, int l) const;
+  void rotate_all(Worker<TA>& w);
   void conv_backward(Worker<TA>& w);
   void route_forward(int j);
   void fc_forward_backward(int j, bool beta);
@@ -321,6 +406,14 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
 
   const int nl = comm_->nlocal();
   w_.resize(nl);
+  // implicit GEMM needs 128-byte channel blocks (TMA im2col atoms)
+  const int atom = std::is_same<TA, float>::value ? 32 : 64;
+  for (size_t l = 0; l < g_.cg.size(); ++l) {
+    ConvGeom& c = g_.cg[l];
+    c.impl_fwd = c.C % atom == 0;
+    c.impl_dgrad = l > 0 && c.stride == 1 && c.F % atom == 0 && c.pad <= c.R - 1 &&
+                   c.H == c.OH + c.R - 1 - 2 * c.pad && c.W == c.OW + c.S - 1 - 2 * c.pad;
+  }
   const auto& in = g_.input;
   const long long A = g_.A;
   const int nc = static_cast<int>(g_.cg.size()), nf = static_cast<int>(g_.fg.size());
@@ -334,25 +427,24 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     Worker<TA>& w = w_[i];
     w.gid = comm_->first() + i;
     w.x_nchw = arena_.make<float>(b_ * in[0] * in[1] * in[2]);
-    w.x0 = arena_.make<TA>(b_ * in[0] * in[1] * in[2]);
+    w.x0 = g_.cg[0].impl_fwd ? arena_.make<TA>(b_ * in[0] * in[1] * in[2]) : nullptr;
     w.targets = arena_.make<float>(b_ * L_);
-    long long gmax = 0;
     for (int l = 0; l < nc; ++l) {
       const ConvGeom& c = g_.cg[l];
-      w.col.push_back(arena_.make<TA>(c.P * c.ldk));
+      const bool lrn_only = c.lrn_n > 0 && c.pk == 0;  // fused LRN+pool keeps no LRN output
+      w.col.push_back(c.impl_fwd ? nullptr : arena_.make<TA>(c.P * c.ldk));
       w.act.push_back(arena_.make<TA>(c.P * c.F));
-      w.lrn.push_back(c.lrn_n > 0 ? arena_.make<TA>(c.P * c.F) : nullptr);
-      w.lrn_d.push_back(c.lrn_n > 0 ? arena_.make<float>(c.P * c.F) : nullptr);
+      w.lrn.push_back(lrn_only ? arena_.make<TA>(c.P * c.F) : nullptr);
+      w.lrn_d.push_back(lrn_only ? arena_.make<float>(c.P * c.F) : nullptr);
       w.pool.push_back(c.pk > 0 ? arena_.make<TA>(c.PP * c.F) : nullptr);
-      w.pidx.push_back(c.pk > 0 ? arena_.make<int32_t>(c.PP * c.F) : nullptr);
+      w.widx.push_back(c.pk > 0 ? arena_.make<uint8_t>(c.PP * c.F) : nullptr);
       w.dz.push_back(arena_.make<TA>(c.P * c.F));
-      w.dcol.push_back(l > 0 ? arena_.make<float>(c.P * c.ldk) : nullptr);
+      w.dcol.push_back(l > 0 && !c.impl_dgrad ? arena_.make<float>(c.P * c.ldk) : nullptr);
+      w.wrot.push_back(c.impl_dgrad ? arena_.make<TA>(static_cast<long long>(c.F) * c.Kc) : nullptr);
       // grad wrt this stage's output, needed when the stage ends in pool/LRN
       const bool needs_g = (c.pk > 0 || c.lrn_n > 0) && l + 1 < nc;
       w.gstage.push_back(needs_g ? arena_.make<float>(c.PP * c.F) : nullptr);
-      if (c.pk > 0 && c.lrn_n > 0) gmax = std::max(gmax, c.P * c.F);
     }
-    w.gtmp = gmax > 0 ? arena_.make<float>(gmax) : nullptr;
     w.cp = arena_.make<float>(conv_total_);
     w.cm = arena_.make<float>(conv_total_);
     w.cgr = arena_.make<float>(conv_total_);
@@ -416,6 +508,18 @@ const Worker<TA>* ClusterImpl<TA>::local_or_null(int gid) const {
 }
 
 template <class TA>
+static const TA* stage_out_of(const Worker<TA>& w, const ConvGeom& c, int l) {
+  if (c.pk > 0) return w.pool[l];
+  if (c.lrn_n > 0) return w.lrn[l];
+  return w.act[l];
+}
+
+template <class TA>
+const TA* ClusterImpl<TA>::stage_in(const Worker<TA>& w, int l) const {
+  return stage_out_of(w, g_.cg[l - 1], l - 1);
+}
+
+template <class TA>
 void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
   const int nc = static_cast<int>(g_.cg.size()), nf = static_cast<int>(g_.fg.size());
   const bool bf = !std::is_same<TA, float>::value;
@@ -449,7 +553,9 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
   for (int l = 0; l < nc; ++l) {
     const ConvGeom& c = g_.cg[l];
     const char* kw = static_cast<const char*>(cweights) + conv_k_off(l) * es;
-    // fprop: Y[P][F] = col[P][Kc] . W[F][Kc]^T (+bias, ReLU)
+    const void* in = l == 0 ? static_cast<const void*>(w.x0) : stage_in(w, l);
+    const Im2col view{1, static_cast<int>(b_), c.H, c.W, c.C, c.R, c.S, c.stride, c.pad, c.OH, c.OW};
+    // fprop: Y[P][F] = im2col(x)[P][Kc] . W[F][Kc]^T (+bias, ReLU)
     Epi e;
     e.c = w.act[l];
     e.ldc = c.F;
@@ -457,20 +563,53 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     e.bias = w.cp + conv_b_off(l);
     e.bias_mode = 2;
     e.relu = c.relu;
-    w.conv_fwd.push_back(plan(op(w.col[l], 0, c.ldk), op(kw, 0, c.ldk), c.P, c.F, c.Kc, e));
-    // wgrad: dW[F][Kc] = dz^T[F][P] . col[P][Kc]
+    GemmOperand xa = op(w.col[l], 0, c.ldk);
+    if (c.impl_fwd) {
+      xa = op(in, 0, 0);
+      xa.conv = view;
+    }
+    w.conv_fwd.push_back(plan(xa, op(kw, 0, c.ldk), c.P, c.F, c.Kc, e));
+    // wgrad: dW[F][Kc] = dz^T[F][P] . im2col(x)[P][Kc]
     Epi eg;
     eg.c = w.cgr + conv_k_off(l);
     eg.ldc = c.ldk;
-    w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), op(w.col[l], 1, c.ldk), c.F, c.Kc, c.P, eg));
-    // dgrad (l > 0): dcol[P][Kc] = dz[P][F] . W[F][Kc]
-    if (l > 0) {
+    GemmOperand xb = op(w.col[l], 1, c.ldk);
+    if (c.impl_fwd) {
+      xb = op(in, 1, 0);
+      xb.conv = view;
+    }
+    w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, c.Kc, c.P, eg));
+    if (l == 0) {
+      w.conv_dgrad.push_back(GemmPlan{});
+      continue;
+    }
+    const ConvGeom& pc = g_.cg[l - 1];
+    const bool below_fused = pc.pk > 0 || pc.lrn_n > 0;
+    if (c.impl_dgrad) {
+      // dX[b*H*W][C] = conv(dz, rotated W) with padding R-1-pad; written straight
+      // into the layer below's gradient (ReLU mask fused when nothing sits between)
+      Epi ed;
+      if (below_fused) {
+        ed.c = w.gstage[l - 1];
+      } else {
+        ed.c = w.dz[l - 1];
+        ed.c_type = kTA;
+        if (pc.relu) {
+          ed.mask = w.act[l - 1];
+          ed.ldmask = c.C;
+          ed.mask_type = kTA;
+        }
+      }
+      ed.ldc = c.C;
+      GemmOperand dy = op(w.dz[l], 0, 0);
+      dy.conv = Im2col{1, static_cast<int>(b_), c.OH, c.OW, c.F, c.R, c.S, 1, c.R - 1 - c.pad, c.H, c.W};
+      w.conv_dgrad.push_back(plan(dy, op(w.wrot[l], 0, c.Kc), b_ * c.H * c.W, c.C, c.Kc, ed));
+    } else {
+      // dcol[P][Kc] = dz[P][F] . W[F][Kc], then col2im
       Epi ed;
       ed.c = w.dcol[l];
       ed.ldc = c.ldk;
       w.conv_dgrad.push_back(plan(op(w.dz[l], 0, c.F), op(kw, 1, c.ldk), c.P, c.Kc, c.F, ed));
-    } else {
-      w.conv_dgrad.push_back(GemmPlan{});
     }
   }
   const void* fweights = bf ? static_cast<const void*>(w.fpt) : static_cast<const void*>(w.fp);
@@ -626,6 +765,7 @@ void ClusterImpl<TA>::upload_master(Worker<TA>& w, bool conv, const std::vector<
 
 template <class TA>
 void ClusterImpl<TA>::refresh_copies(Worker<TA>& w) {
+  rotate_all(w);
   if (std::is_same<TA, float>::value) return;
   launch_cast<TA>(w.cp, w.cpt, conv_total_, st_);
   launch_cast<TA>(w.fp, w.fpt, fc_total_, st_);
@@ -635,35 +775,45 @@ void ClusterImpl<TA>::refresh_copies(Worker<TA>& w) {
 template <class TA>
 void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
   const int nc = static_cast<int>(g_.cg.size());
-  const TA* x = w.x0;
+  const int B = static_cast<int>(b_);
   for (int l = 0; l < nc; ++l) {
     const ConvGeom& c = g_.cg[l];
-    launch_im2col<TA>(x, w.col[l], static_cast<int>(b_), c.H, c.W, c.C, c.R, c.S, c.stride, c.pad,
-                      c.OH, c.OW, c.ldk, st_);
+    if (!c.impl_fwd) {
+      if (l == 0) {
+        launch_im2col_nchw<TA>(w.x_src, w.col[0], B, c.C, c.H, c.W, c.R, c.S, c.stride, c.pad, c.OH,
+                               c.OW, c.ldk, st_);
+      } else {
+        launch_im2col<TA>(stage_in(w, l), w.col[l], B, c.H, c.W, c.C, c.R, c.S, c.stride, c.pad,
+                          c.OH, c.OW, c.ldk, st_);
+      }
+      ++launches_;
+    }
     gemm(w.conv_fwd[l], "conv_fwd", l);
-    ++launches_;
-    const TA* out = w.act[l];
-    if (c.lrn_n > 0) {
+    if (c.lrn_n > 0 && c.pk > 0) {
+      launch_lrn_pool_fwd<TA>(w.act[l], w.pool[l], w.widx[l], B, c.OH, c.OW, c.F, c.lrn_n, c.lrn_alpha,
+                              c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, st_);
+      ++launches_;
+    } else if (c.lrn_n > 0) {
       launch_lrn_fwd<TA>(w.act[l], w.lrn[l], w.lrn_d[l], c.P, c.F, c.lrn_n, c.lrn_alpha, c.lrn_beta,
                          c.lrn_k, st_);
-      out = w.lrn[l];
+      ++launches_;
+    } else if (c.pk > 0) {
+      launch_maxpool_fwd_w<TA>(w.act[l], w.pool[l], w.widx[l], B, c.OH, c.OW, c.F, c.pk, c.ps, c.PH,
+                               c.PW, st_);
       ++launches_;
     }
-    if (c.pk > 0) {
-      launch_maxpool_fwd<TA>(out, w.pool[l], w.pidx[l], static_cast<int>(b_), c.OH, c.OW, c.F, c.pk,
-                             c.ps, c.PH, c.PW, st_);
-      out = w.pool[l];
-      ++launches_;
-    }
-    x = out;
   }
 }
 
 template <class TA>
-static const TA* stage_out_of(const Worker<TA>& w, const ConvGeom& c, int l) {
-  if (c.pk > 0) return w.pool[l];
-  if (c.lrn_n > 0) return w.lrn[l];
-  return w.act[l];
+void ClusterImpl<TA>::rotate_all(Worker<TA>& w) {
+  for (size_t l = 0; l < g_.cg.size(); ++l) {
+    const ConvGeom& c = g_.cg[l];
+    if (!c.impl_dgrad) continue;
+    launch_rotate_weights<TA>(w.cp + conv_k_off(static_cast<int>(l)), c.ldk, w.wrot[l], c.F, c.C, c.R,
+                              c.S, st_);
+    ++launches_;
+  }
 }
 
 // Boundary exchange for turn j (exchange_activations / assemble_rows,
@@ -795,18 +945,15 @@ void ClusterImpl<TA>::conv_backward(Worker<TA>& w) {
     const ConvGeom& c = g_.cg[l];
     const TA* mask = c.relu ? w.act[l] : nullptr;
     const int B = static_cast<int>(b_);
-    if (c.pk > 0) {
-      if (c.lrn_n > 0) {
-        launch_maxpool_bwd<float, TA>(gout, w.pidx[l], w.gtmp, nullptr, B, c.OH, c.OW, c.F, c.pk, c.ps,
-                                      c.PH, c.PW, st_);
-        launch_lrn_bwd<TA, TA>(w.act[l], w.lrn_d[l], w.gtmp, w.dz[l], c.P, c.F, c.lrn_n, c.lrn_alpha,
-                               c.lrn_beta, c.relu ? 1 : 0, st_);
-        launches_ += 2;
-      } else {
-        launch_maxpool_bwd<TA, TA>(gout, w.pidx[l], w.dz[l], mask, B, c.OH, c.OW, c.F, c.pk, c.ps, c.PH,
-                                   c.PW, st_);
-        ++launches_;
-      }
+    if (c.pk > 0 && c.lrn_n > 0) {
+      launch_lrn_pool_bwd<TA>(gout, w.widx[l], w.act[l], w.dz[l], B, c.OH, c.OW, c.F, c.lrn_n,
+                              c.lrn_alpha, c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, c.relu ? 1 : 0,
+                              st_);
+      ++launches_;
+    } else if (c.pk > 0) {
+      launch_maxpool_bwd_w<TA, TA>(gout, w.widx[l], w.dz[l], mask, B, c.OH, c.OW, c.F, c.pk, c.ps,
+                                   c.PH, c.PW, st_);
+      ++launches_;
     } else if (c.lrn_n > 0) {
       launch_lrn_bwd<TA, TA>(w.act[l], w.lrn_d[l], gout, w.dz[l], c.P, c.F, c.lrn_n, c.lrn_alpha,
                              c.lrn_beta, c.relu ? 1 : 0, st_);
@@ -817,22 +964,27 @@ void ClusterImpl<TA>::conv_backward(Worker<TA>& w) {
     }
     // bias grad = channel sums of dz (model.cpp:184-202)
     launch_colsum<TA>(w.dz[l], c.P, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, st_);
-    gemm(w.conv_wgrad[l], "conv_wgrad", l);
     launches_ += 2;
-    if (l > 0) {
-      gemm(w.conv_dgrad[l], "conv_dgrad", l);
-      const ConvGeom& pc = g_.cg[l - 1];
-      if (pc.pk > 0 || pc.lrn_n > 0) {
+    gemm(w.conv_wgrad[l], "conv_wgrad", l);
+    if (l == 0) break;
+    const ConvGeom& pc = g_.cg[l - 1];
+    const bool below_fused = pc.pk > 0 || pc.lrn_n > 0;
+    gemm(w.conv_dgrad[l], "conv_dgrad", l);
+    if (!c.impl_dgrad) {
+      if (below_fused) {
         launch_col2im<float, TA>(w.dcol[l], w.gstage[l - 1], nullptr, B, c.H, c.W, c.C, c.R, c.S,
                                  c.stride, c.pad, c.OH, c.OW, c.ldk, st_);
-        gout = w.gstage[l - 1];
-        dz_ready = false;
       } else {
-        launch_col2im<TA, TA>(w.dcol[l], w.dz[l - 1], pc.relu ? w.act[l - 1] : nullptr, B, c.H, c.W, c.C,
-                              c.R, c.S, c.stride, c.pad, c.OH, c.OW, c.ldk, st_);
-        dz_ready = true;
+        launch_col2im<TA, TA>(w.dcol[l], w.dz[l - 1], pc.relu ? w.act[l - 1] : nullptr, B, c.H, c.W,
+                              c.C, c.R, c.S, c.stride, c.pad, c.OH, c.OW, c.ldk, st_);
       }
       ++launches_;
+    }
+    if (below_fused) {
+      gout = w.gstage[l - 1];
+      dz_ready = false;
+    } else {
+      dz_ready = true;
     }
   }
 }
@@ -915,9 +1067,12 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
       HP_CUDA(cudaMemcpyAsync(w.targets, targets[i], b_ * L_ * sizeof(float), cudaMemcpyDeviceToDevice, st_));
     }
     HP_CUDA(cudaMemsetAsync(w.bad, 0, sizeof(int), st_));
-    launch_nchw_to_nhwc<TA>(src, w.x0, static_cast<int>(b_), static_cast<int>(in[0]),
-                            static_cast<int>(in[1]), static_cast<int>(in[2]), st_);
-    ++launches_;
+    w.x_src = src;
+    if (g_.cg[0].impl_fwd) {
+      launch_nchw_to_nhwc<TA>(src, w.x0, static_cast<int>(b_), static_cast<int>(in[0]),
+                              static_cast<int>(in[1]), static_cast<int>(in[2]), st_);
+      ++launches_;
+    }
   }
   for (auto& w : w_) conv_forward(w);
   for (int j = 0; j < num_sub_; ++j) {
@@ -939,6 +1094,7 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
     sgd_fc(lr, static_cast<float>(1.0 / static_cast<double>(num_sub_)), scale, hp);
   }
   sgd_conv(lr, hp);
+  for (auto& w : w_) rotate_all(w);
   HP_CUDA(cudaEventRecord(ev1_, st_));
 
   // loss = sum_j loss_j * n_j / (K*b) (cluster.cpp:555-556, 710)
@@ -984,81 +1140,8 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
 // them (cluster.cpp:466-471, 511-528, 549-550, 576-580, 616-633, 666-670).
 template <class TA>
 void ClusterImpl<TA>::account(int num_sub, hp_step_metrics* out) {
-  const int K = K_;
-  const long long b = b_, elt = 4, row_bytes = g_.A * elt;
-  auto charge = [&](int i, int cls, long long s, long long r) {
-    sent[i][cls] += s;
-    received[i][cls] += r;
-    out->bytes_sent[cls] += s;
-  };
-  auto ex_sent = [&](int j, int i) -> long long {
-    if (K <= 1) return 0;
-    if (scheme_ == HP_SCHEME_A) return (K - 1) * b * row_bytes;
-    if (scheme_ == HP_SCHEME_B) return i == j ? (K - 1) * b * row_bytes : 0;
-    return (K - 1) * (b / K) * row_bytes;
-  };
-  const long long n = n_;
-  std::vector<hp_trace_event> fwd(num_sub), bwd(num_sub);
-  for (int j = 0; j < num_sub; ++j) {
-    long long total = 0, mx = 0;
-    for (int i = 0; i < K; ++i) {
-      long long inbound = 0;
-      if (K > 1) inbound = scheme_ == HP_SCHEME_B ? (i == j ? 0 : b * row_bytes) : ex_sent(j, i);
-      charge(i, HP_MSG_FC_ACTIVATIONS, ex_sent(j, i), inbound);
-      total += ex_sent(j, i);
-      mx = std::max(mx, ex_sent(j, i));
-    }
-    fwd[j] = {HP_PHASE_FC_FWD, j, scheme_ == HP_SCHEME_B ? j : -1, total, mx};
-    for (size_t l = 0; l < g_.fg.size(); ++l) {
-      const FcGeom& f = g_.fg[l];
-      for (int i = 0; i < K; ++i) {
-        const long long ns = f.c1[i] - f.c0[i];
-        charge(i, HP_MSG_FC_INTERNAL, (K - 1) * n * ns * elt, n * (f.out - ns) * elt);
-      }
-    }
-    for (size_t li = g_.fg.size(); li-- > 1;) {
-      const long long part = n * g_.fg[li].in * elt;
-      for (int i = 0; i < K; ++i) charge(i, HP_MSG_FC_INTERNAL, (K - 1) * part, (K - 1) * part);
-    }
-  }
-  for (int j = 0; j < num_sub; ++j) {
-    long long total = 0, mx = 0;
-    for (int i = 0; i < K; ++i) {
-      long long s = 0;
-      if (scheme_ == HP_SCHEME_A) s = K > 1 ? (K - 1) * b * row_bytes : 0;
-      else if (scheme_ == HP_SCHEME_B) s = i != j ? b * row_bytes : 0;
-      else s = K > 1 ? (K - 1) * (b / K) * row_bytes : 0;
-      long long r = s;
-      if (scheme_ == HP_SCHEME_B) r = (i == j && K > 1) ? (K - 1) * b * row_bytes : 0;
-      charge(i, HP_MSG_FC_GRADIENTS, s, r);
-      total += s;
-      mx = std::max(mx, s);
-    }
-    bwd[j] = {HP_PHASE_FC_BWD, j, scheme_ == HP_SCHEME_B ? j : -1, total, mx};
-  }
-  trace.clear();
-  trace.push_back({HP_PHASE_CONV_FWD, -1, -1, 0, 0});
-  for (int j = 0; j < num_sub; ++j) {
-    trace.push_back(fwd[j]);
-    trace.push_back(bwd[j]);
-  }
-  trace.push_back({HP_PHASE_CONV_BWD, -1, -1, 0, 0});
-  long long G = 0;
-  for (const auto& c : g_.cg) G += static_cast<long long>(c.F) * c.Kc + c.F;
-  long long total = 0, mx = 0;
-  for (int i = 0; i < K; ++i) {
-    long long s = 0;
-    if (K > 1) {
-      long long s0, s1;
-      shard(G, K, i, &s0, &s1);
-      const long long shard_bytes = (s1 - s0) * elt;
-      s = (G * elt - shard_bytes) + (K - 1) * shard_bytes;
-    }
-    charge(i, HP_MSG_CONV_SYNC, s, s);
-    total += s;
-    mx = std::max(mx, s);
-  }
-  trace.push_back({HP_PHASE_SYNC, -1, -1, total, mx});
+  (void)num_sub;
+  step_accounting(g_, K_, b_, scheme_, sent, received, trace, out->bytes_sent);
   out->n_events = static_cast<int>(trace.size());
 }
 

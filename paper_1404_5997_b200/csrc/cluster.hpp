@@ -22,6 +22,8 @@ struct ConvGeom {
   int pk, ps;                  // max-pool (pk == 0: none)
   int PH, PW;                  // stage output
   int Kc;                      // R*S*C (im2col width)
+  bool impl_fwd = false;       // fprop + wgrad as implicit GEMM (TMA im2col), no col buffer
+  bool impl_dgrad = false;     // stride-1 dgrad as a conv over dY with rotated weights
   long long ldk;               // padded row stride of col / kernels (16-byte multiple)
   long long P;                 // b*OH*OW rows per worker
   long long PP;                // b*PH*PW
@@ -80,6 +82,13 @@ class ClusterBase {
   double last_ms = 0.0;
   int64_t last_launches = 0;
 };
+
+// Host-only analytic accounting of one step (adds into sent/received/bytes_sent,
+// replaces trace). Every rank computes the counters of all K workers.
+void step_accounting(const Geometry& g, int K, long long b, int scheme,
+                     std::vector<std::array<int64_t, 4>>& sent,
+                     std::vector<std::array<int64_t, 4>>& received, std::vector<hp_trace_event>& trace,
+                     int64_t* bytes_sent);
 
 std::unique_ptr<ClusterBase> make_cluster(const hp_model_spec* spec, const hp_cluster_config* cfg);
 

@@ -76,41 +76,84 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, cons
     return;
   }
   const Epi& e = a.epi;
-  const bool simple = !e.c_trans && !e.beta && !e.mask && n0 + 32 <= a.N;
-  if (simple && e.c_type == kF32 && (e.ldc & 3) == 0) {
-    float* dst = reinterpret_cast<float*>(e.c) + static_cast<long long>(m) * e.ldc + n0;
+  // Vector path: 32 contiguous outputs of row m (bias/ReLU/alpha/beta/mask fused).
+  const bool vec = !e.c_trans && n0 + 32 <= a.N &&
+                   (e.c_type == kF32 ? (e.ldc & 3) == 0 : (e.ldc & 7) == 0) &&
+                   (!e.beta || e.c_type == kF32) &&
+                   (!e.mask || (e.mask_trans == 0 && (e.mask_type == kF32 ? (e.ldmask & 3) == 0
+                                                                             : (e.ldmask & 7) == 0)));
+  if (vec) {
+    float x[32];
     const float bm = e.bias_mode == 1 ? e.bias[m] : 0.f;
 #pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-      float t[4];
+    for (int i = 0; i < 32; ++i) x[i] = v[i] * e.alpha;
+    const long long off = static_cast<long long>(m) * e.ldc + n0;
+    if (e.beta) {
+      const float4* old = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.c) + off);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float x = v[i + j] * e.alpha;
-        if (e.bias_mode == 1) x += bm;
-        if (e.bias_mode == 2) x += e.bias[n0 + i + j];
-        if (e.relu) x = x > 0.f ? x : 0.f;
-        t[j] = x;
+      for (int i = 0; i < 8; ++i) {
+        const float4 o = old[i];
+        x[4 * i] += o.x;
+        x[4 * i + 1] += o.y;
+        x[4 * i + 2] += o.z;
+        x[4 * i + 3] += o.w;
       }
-      *reinterpret_cast<float4*>(dst + i) = make_float4(t[0], t[1], t[2], t[3]);
     }
-    return;
-  }
-  if (simple && e.c_type == kBF16 && (e.ldc & 7) == 0) {
-    __nv_bfloat16* dst =
-        reinterpret_cast<__nv_bfloat16*>(e.c) + static_cast<long long>(m) * e.ldc + n0;
-    const float bm = e.bias_mode == 1 ? e.bias[m] : 0.f;
+    if (e.bias_mode == 1) {
 #pragma unroll
-    for (int i = 0; i < 32; i += 8) {
-      __align__(16) __nv_bfloat16 t[8];
+      for (int i = 0; i < 32; ++i) x[i] += bm;
+    } else if (e.bias_mode == 2) {
+      const float4* bb = reinterpret_cast<const float4*>(e.bias + n0);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        float x = v[i + j] * e.alpha;
-        if (e.bias_mode == 1) x += bm;
-        if (e.bias_mode == 2) x += e.bias[n0 + i + j];
-        if (e.relu) x = x > 0.f ? x : 0.f;
-        t[j] = __float2bfloat16_rn(x);
+      for (int i = 0; i < 8; ++i) {
+        const float4 o = bb[i];
+        x[4 * i] += o.x;
+        x[4 * i + 1] += o.y;
+        x[4 * i + 2] += o.z;
+        x[4 * i + 3] += o.w;
       }
-      *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(t);
+    }
+    if (e.relu) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) x[i] = x[i] > 0.f ? x[i] : 0.f;
+    }
+    if (e.mask) {
+      const long long mo = static_cast<long long>(m) * e.ldmask + n0;
+      if (e.mask_type == kBF16) {
+        const uint4* mp = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(e.mask) + mo);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint4 u = mp[i];
+          const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (!(__bfloat162float(h[j]) > 0.f)) x[8 * i + j] = 0.f;
+        }
+      } else {
+        const float4* mp = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.mask) + mo);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 o = mp[i];
+          if (!(o.x > 0.f)) x[4 * i] = 0.f;
+          if (!(o.y > 0.f)) x[4 * i + 1] = 0.f;
+          if (!(o.z > 0.f)) x[4 * i + 2] = 0.f;
+          if (!(o.w > 0.f)) x[4 * i + 3] = 0.f;
+        }
+      }
+    }
+    if (e.c_type == kF32) {
+      float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.c) + off);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[i] = make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
+    } else {
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.c) + off);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        __align__(16) __nv_bfloat16 t[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) t[j] = __float2bfloat16_rn(x[8 * i + j]);
+        dst[i] = *reinterpret_cast<const uint4*>(t);
+      }
     }
     return;
   }
@@ -126,6 +169,40 @@ __device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* tm, u
     tma_load_2d(dst, tm, bar, k0, row0);
   } else {
     for (int a = 0; a < rows / ATOM; ++a) tma_load_2d(dst + a * (BK * 128), tm, bar, row0 + a * ATOM, k0);
+  }
+}
+
+// im2col A tile (fprop / rotated dgrad): 128 consecutive output pixels x one
+// 128-byte channel block of filter tap (r, s) for k-tile kt.
+template <int ATOM>
+__device__ __forceinline__ void load_a_im2col(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
+                                              const ConvArgs& c, int m0, int kt) {
+  const int cblks = c.C / ATOM;
+  const int cb = kt % cblks, rs = kt / cblks;
+  const int r = rs / c.S, s = rs - r * c.S;
+  const int ohw = c.OH * c.OW;
+  const int n = m0 / ohw, rem = m0 - n * ohw;
+  const int oh = rem / c.OW, ow = rem - oh * c.OW;
+  tma_load_im2col_4d(dst, tm, bar, cb * ATOM, c.lo_w + ow * c.stride, c.lo_h + oh * c.stride, n,
+                     static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+}
+
+// im2col B tile (wgrad, MN-major): BK consecutive output pixels (the K
+// dimension) x BN columns = BN/ATOM channel blocks, each at its own tap.
+template <int BK, int ATOM>
+__device__ __forceinline__ void load_b_im2col(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
+                                              const ConvArgs& c, int n0, int rows, int kt) {
+  const int ohw = c.OH * c.OW;
+  const int p0 = kt * BK;
+  const int n = p0 / ohw, rem = p0 - n * ohw;
+  const int oh = rem / c.OW, ow = rem - oh * c.OW;
+  for (int a = 0; a < rows / ATOM; ++a) {
+    const int col = n0 + a * ATOM;
+    const int rs = col / c.C, ch = col - rs * c.C;
+    const int r = rs / c.S, s = rs - r * c.S;
+    tma_load_im2col_4d(dst + a * (BK * 128), tm, bar, ch, c.lo_w + ow * c.stride,
+                       c.lo_h + oh * c.stride, n, static_cast<uint16_t>(s),
+                       static_cast<uint16_t>(r));
   }
 }
 
@@ -186,8 +263,16 @@ __global__ void __launch_bounds__(192, 1)
         uint8_t* sa = smem + stage * SB;
         uint8_t* sb = sa + A_BYTES;
         mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
-        load_tile<ES, BK, ATOM>(sa, &ta, &full[stage], args.a_mn, m0, kBM, kt * BK);
-        load_tile<ES, BK, ATOM>(sb, &tb, &full[stage], args.b_mn, n0, BN, kt * BK);
+        if (args.ca.enabled) {
+          load_a_im2col<ATOM>(sa, &ta, &full[stage], args.ca, m0, kt);
+        } else {
+          load_tile<ES, BK, ATOM>(sa, &ta, &full[stage], args.a_mn, m0, kBM, kt * BK);
+        }
+        if (args.cb.enabled) {
+          load_b_im2col<BK, ATOM>(sb, &tb, &full[stage], args.cb, n0, BN, kt);
+        } else {
+          load_tile<ES, BK, ATOM>(sb, &tb, &full[stage], args.b_mn, n0, BN, kt * BK);
+        }
         if (++stage == STAGES) {
           stage = 0;
           phase ^= 1;
@@ -355,6 +440,62 @@ CUtensorMap make_map(const void* ptr, int es, long long inner, long long outer, 
   return m;
 }
 
+PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col_fn() {
+  static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || p == nullptr) {
+      throw std::runtime_error("cuTensorMapEncodeIm2col unavailable");
+    }
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(p);
+  }
+  return fn;
+}
+
+// im2col view of an NHWC tensor: dims {C, W, H, N}; the bounding box of base
+// pixels runs from -pad to (extent + pad - filter) (WHD order, as CUTLASS's
+// make_im2col_tma_copy_desc); `pixels` output pixels x ATOM channels per load.
+CUtensorMap im2col_map(const void* ptr, int es, const Im2col& g, int pixels, bool mn_major) {
+  if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0) throw std::runtime_error("im2col: base not 16-byte aligned");
+  const int atom = 128 / es;
+  if (g.C % atom != 0) throw std::runtime_error("im2col: channels must be a multiple of 128 bytes");
+  CUtensorMap m;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.C), static_cast<cuuint64_t>(g.W),
+                        static_cast<cuuint64_t>(g.H), static_cast<cuuint64_t>(g.N)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.C) * es, static_cast<cuuint64_t>(g.W) * g.C * es,
+                           static_cast<cuuint64_t>(g.H) * g.W * g.C * es};
+  int lower[2] = {-g.pad, -g.pad};                    // {W, H}
+  int upper[2] = {g.pad - (g.S - 1), g.pad - (g.R - 1)};
+  cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(g.stride), static_cast<cuuint32_t>(g.stride), 1};
+  CUresult r = encode_im2col_fn()(&m, es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                  4, const_cast<void*>(ptr), dims, strides, lower, upper,
+                                  static_cast<cuuint32_t>(atom), static_cast<cuuint32_t>(pixels), estr,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  (mn_major && es == 4) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                                        : CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    throw std::runtime_error("cuTensorMapEncodeIm2col failed (" + std::to_string(static_cast<int>(r)) + ")");
+  }
+  return m;
+}
+
+ConvArgs conv_args(const Im2col& g) {
+  ConvArgs c{};
+  c.enabled = g.enabled;
+  c.C = g.C;
+  c.S = g.S;
+  c.OH = g.OH;
+  c.OW = g.OW;
+  c.stride = g.stride;
+  c.lo_w = -g.pad;
+  c.lo_h = -g.pad;
+  return c;
+}
+
 CUtensorMap operand_map(const GemmOperand& o, const void* ptr, int es, int rows, int K, int box_rows) {
   const int BK = 128 / es;
   const int ATOM = 128 / es;
@@ -447,8 +588,20 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   p.args.ws = ws;
   p.args.epi = epi;
   if (splits > 1 && ws == nullptr) throw std::runtime_error("gemm: split-K needs a workspace");
-  p.ta = operand_map(a, a.ptr, es, M, K, kBM);
-  p.tb = operand_map(b, b.ptr, es, N, K, p.bn);
+  if (a.conv.enabled) {
+    if (a.mn_major) throw std::runtime_error("gemm: im2col A must be K-major");
+    p.ta = im2col_map(a.ptr, es, a.conv, kBM, false);
+  } else {
+    p.ta = operand_map(a, a.ptr, es, M, K, kBM);
+  }
+  if (b.conv.enabled) {
+    if (!b.mn_major) throw std::runtime_error("gemm: im2col B must be MN-major");
+    p.tb = im2col_map(b.ptr, es, b.conv, BK, true);
+  } else {
+    p.tb = operand_map(b, b.ptr, es, N, K, p.bn);
+  }
+  p.args.ca = conv_args(a.conv);
+  p.args.cb = conv_args(b.conv);
   p.grid = dim3(cdiv(M, kBM), cdiv(N, p.bn), splits);
   p.smem = static_cast<size_t>(num_stages(p.bn, math)) * stage_bytes(p.bn, math) + 1024 + 256;
   p.valid = true;

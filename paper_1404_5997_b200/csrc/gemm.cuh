@@ -41,10 +41,28 @@ struct Epi {
   int mask_trans = 0;
 };
 
+// Implicit-GEMM convolution operand: the matrix is the im2col view of an NHWC
+// activation tensor, gathered by TMA im2col loads (no im2col buffer).
+//   as A (K-major, fprop / stride-1 dgrad): rows = output pixels (n,oh,ow),
+//       K = (r, s, c) with c fastest;
+//   as B (MN-major, wgrad): K = output pixels, N = (r, s, c).
+// Requires C % (128 bytes / element size) == 0.
+struct Im2col {
+  int enabled = 0;
+  int N = 0, H = 0, W = 0, C = 0;  // activation tensor
+  int R = 0, S = 0, stride = 1, pad = 0;
+  int OH = 0, OW = 0;              // output pixels enumerated by the GEMM
+};
+
 struct GemmOperand {
   const void* ptr = nullptr;
   int mn_major = 0;          // 0: [rows][K] (ld >= K); 1: [K][rows] (ld >= rows)
   long long ld = 0;          // elements
+  Im2col conv;               // conv.enabled: ptr is the NHWC activation, ld unused
+};
+
+struct ConvArgs {            // device-side im2col bookkeeping (see Im2col)
+  int enabled, C, S, OH, OW, stride, lo_w, lo_h;
 };
 
 struct GemmArgs {
@@ -55,6 +73,7 @@ struct GemmArgs {
   int raw_partial;  // 1: write fp32 partials to ws[split][M][N]; epilogue applied by reduce
   float* ws;
   Epi epi;
+  ConvArgs ca, cb;  // im2col bookkeeping for A / B
 };
 
 // A fully prepared GEMM launch (tensor maps encoded once, reused every step).

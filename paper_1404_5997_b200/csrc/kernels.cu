@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <stdexcept>
 
 #include "errors.hpp"
 #include "kernels.cuh"
@@ -409,9 +410,309 @@ __global__ void scale_kernel(float* x, long long n, float s) {
   GRID_STRIDE(i, n) x[i] = __fmul_rn(x[i], s);
 }
 
+// ------------------------------------------------------------------ conv1 im2col from NCHW
+template <class T>
+__global__ void im2col_nchw_kernel(const float* __restrict__ x, T* __restrict__ col, int C, int H,
+                                   int W, int S, int stride, int pad, int OH, int OW, int ldk, int K,
+                                   int P) {
+  constexpr int V = 16 / sizeof(T);
+  const int chunks = ldk / V;
+  const int n = P * chunks;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int p = i / chunks;
+    const int k0 = (i - p * chunks) * V;
+    const int ow = p % OW;
+    const int t = p / OW;
+    const int oh = t % OH;
+    const int b = t / OH;
+    int c = k0 % C;
+    int rs = k0 / C;
+    int s = rs % S;
+    int r = rs / S;
+    __align__(16) T v[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      float val = 0.f;
+      if (k0 + j < K) {
+        const int h = oh * stride - pad + r, w = ow * stride - pad + s;
+        if (h >= 0 && h < H && w >= 0 && w < W) val = __ldg(x + ((static_cast<long long>(b) * C + c) * H + h) * W + w);
+      }
+      v[j] = from_f<T>(val);
+      if (++c == C) {
+        c = 0;
+        if (++s == S) {
+          s = 0;
+          ++r;
+        }
+      }
+    }
+    *reinterpret_cast<uint4*>(col + static_cast<long long>(p) * ldk + k0) = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
+// ------------------------------------------------------------------ fused LRN + pool
+__device__ __forceinline__ float pow_neg(float d, float beta) {
+  return exp2f(-beta * __log2f(d));  // d >= k > 0
+}
+
+template <class T>
+__global__ void lrn_pool_fwd_kernel(const T* __restrict__ a, T* __restrict__ y,
+                                    uint8_t* __restrict__ widx, int H, int W, int C, int lo, int hi,
+                                    float alpha, float beta, float kk, int pk, int ps, int PH, int PW,
+                                    int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = i % C;
+    int t = i / C;
+    const int pw = t % PW;
+    t /= PW;
+    const int ph = t % PH;
+    const int b = t / PH;
+    const int j0 = max(0, c - lo), j1 = min(C - 1, c + hi);
+    float best = -INFINITY;
+    int bi = 0;
+    bool done = false;
+    for (int r = 0; r < pk && !done; ++r) {
+      const int h = ph * ps + r;
+      for (int q = 0; q < pk; ++q) {
+        const int w = pw * ps + q;
+        const T* px = a + ((b * H + h) * W + w) * C;
+        float sum = 0.f;
+        for (int j = j0; j <= j1; ++j) {
+          const float v = to_f<T>(px[j]);
+          sum += v * v;
+        }
+        const float v = to_f<T>(px[c]) * pow_neg(kk + alpha * sum, beta);
+        if (v > best || isnan(v)) {
+          best = v;
+          bi = r * pk + q;
+          if (isnan(v)) {
+            done = true;
+            break;
+          }
+        }
+      }
+    }
+    y[i] = from_f<T>(best);
+    widx[i] = static_cast<uint8_t>(bi);
+  }
+}
+
+// Block = PT consecutive pixels x all C channels, staged in shared memory.
+template <class TA>
+__global__ void lrn_pool_bwd_kernel(const float* __restrict__ gy, const uint8_t* __restrict__ widx,
+                                    const TA* __restrict__ a, TA* __restrict__ dz, int H, int W,
+                                    int C, int lo, int hi, float alpha, float beta, float kk, int pk,
+                                    int ps, int PH, int PW, int relu_mask, int npix, int PT) {
+  extern __shared__ float sm[];
+  float* sa = sm;                 // a
+  float* sg = sa + PT * C;        // gb (grad wrt LRN output)
+  float* st = sg + PT * C;        // t = gb * a * d^(-beta-1)
+  float* sd = st + PT * C;        // d^(-beta)
+  const int p0 = blockIdx.x * PT;
+  const int np = min(PT, npix - p0);
+  const int tot = np * C;
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int pl = e / C, c = e - pl * C;
+    const int p = p0 + pl;
+    const int w = p % W;
+    const int t = p / W;
+    const int h = t % H;
+    const int b = t / H;
+    sa[e] = to_f<TA>(a[p0 * C + e]);
+    const int oh0 = h - pk + 1 <= 0 ? 0 : (h - pk + ps) / ps;
+    const int oh1 = min(PH - 1, h / ps);
+    const int ow0 = w - pk + 1 <= 0 ? 0 : (w - pk + ps) / ps;
+    const int ow1 = min(PW - 1, w / ps);
+    float g = 0.f;
+    for (int oh = oh0; oh <= oh1; ++oh)
+      for (int ow = ow0; ow <= ow1; ++ow) {
+        const int o = ((b * PH + oh) * PW + ow) * C + c;
+        if (widx[o] == (h - oh * ps) * pk + (w - ow * ps)) g += gy[o];
+      }
+    sg[e] = g;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int pl = e / C, c = e - pl * C;
+    const float* row = sa + pl * C;
+    const int j0 = max(0, c - lo), j1 = min(C - 1, c + hi);
+    float sum = 0.f;
+    for (int j = j0; j <= j1; ++j) sum += row[j] * row[j];
+    const float d = kk + alpha * sum;
+    const float dn = pow_neg(d, beta);
+    sd[e] = dn;
+    st[e] = sg[e] * sa[e] * __fdividef(dn, d);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int pl = e / C, c = e - pl * C;
+    const int i0 = max(0, c - hi), i1 = min(C - 1, c + lo);
+    float acc = 0.f;
+    for (int j = i0; j <= i1; ++j) acc += st[pl * C + j];
+    const float av = sa[e];
+    float g = sg[e] * sd[e] - 2.f * alpha * beta * av * acc;
+    if (relu_mask && !(av > 0.f)) g = 0.f;
+    dz[p0 * C + e] = from_f<TA>(g);
+  }
+}
+
+template <class T>
+__global__ void maxpool_fwd_w_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                     uint8_t* __restrict__ widx, int H, int W, int C, int k, int s,
+                                     int OH, int OW, long long n) {
+  GRID_STRIDE(i, n) {
+    const int c = static_cast<int>(i % C);
+    long long t = i / C;
+    const int ow = static_cast<int>(t % OW);
+    t /= OW;
+    const int oh = static_cast<int>(t % OH);
+    const long long b = t / OH;
+    float best = -INFINITY;
+    int bi = 0;
+    bool done = false;
+    for (int r = 0; r < k && !done; ++r)
+      for (int q = 0; q < k; ++q) {
+        const float v = to_f<T>(x[((b * H + oh * s + r) * W + ow * s + q) * C + c]);
+        if (v > best || isnan(v)) {
+          best = v;
+          bi = r * k + q;
+          if (isnan(v)) {
+            done = true;
+            break;
+          }
+        }
+      }
+    y[i] = from_f<T>(best);
+    widx[i] = static_cast<uint8_t>(bi);
+  }
+}
+
+template <class TO, class TM>
+__global__ void maxpool_bwd_w_kernel(const float* __restrict__ gy, const uint8_t* __restrict__ widx,
+                                     TO* __restrict__ gx, const TM* __restrict__ mask, int H, int W,
+                                     int C, int k, int s, int OH, int OW, long long n) {
+  GRID_STRIDE(i, n) {
+    const int c = static_cast<int>(i % C);
+    long long t = i / C;
+    const int w = static_cast<int>(t % W);
+    t /= W;
+    const int h = static_cast<int>(t % H);
+    const long long b = t / H;
+    const int oh0 = h - k + 1 <= 0 ? 0 : (h - k + s) / s;
+    const int oh1 = min(OH - 1, h / s);
+    const int ow0 = w - k + 1 <= 0 ? 0 : (w - k + s) / s;
+    const int ow1 = min(OW - 1, w / s);
+    float acc = 0.f;
+    for (int oh = oh0; oh <= oh1; ++oh)
+      for (int ow = ow0; ow <= ow1; ++ow) {
+        const long long o = ((b * OH + oh) * OW + ow) * C + c;
+        if (widx[o] == (h - oh * s) * k + (w - ow * s)) acc += gy[o];
+      }
+    if (mask != nullptr && !(to_f<TM>(mask[i]) > 0.f)) acc = 0.f;
+    gx[i] = from_f<TO>(acc);
+  }
+}
+
+template <class T>
+__global__ void rotate_weights_kernel(const float* __restrict__ w, long long ldk, T* __restrict__ wr,
+                                      int F, int C, int R, int S) {
+  const long long n = static_cast<long long>(F) * C * R * S;
+  GRID_STRIDE(i, n) {
+    // output index: [c][r][s][f]
+    const int f = static_cast<int>(i % F);
+    long long t = i / F;
+    const int s = static_cast<int>(t % S);
+    t /= S;
+    const int r = static_cast<int>(t % R);
+    const int c = static_cast<int>(t / R);
+    wr[i] = from_f<T>(w[f * ldk + ((R - 1 - r) * S + (S - 1 - s)) * C + c]);
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
+template <class T>
+void launch_im2col_nchw(const float* x, T* col, int B, int C, int H, int W, int R, int S, int stride,
+                        int pad, int OH, int OW, long long ldk, cudaStream_t st) {
+  constexpr int V = 16 / sizeof(T);
+  if (ldk % V != 0) throw std::runtime_error("im2col_nchw: ldk must be a multiple of 16 bytes");
+  const long long P = static_cast<long long>(B) * OH * OW;
+  const long long n = P * (ldk / V);
+  if (n >= (1LL << 31)) throw std::runtime_error("im2col_nchw: too large for 32-bit indexing");
+  im2col_nchw_kernel<T><<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(x, col, C, H, W, S, stride, pad, OH, OW,
+                                                                    static_cast<int>(ldk), R * S * C,
+                                                                    static_cast<int>(P));
+}
+
+template <class T>
+void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, int C, int n,
+                         float alpha, float beta, float kk, int pk, int ps, int PH, int PW,
+                         cudaStream_t st) {
+  const long long total = static_cast<long long>(B) * PH * PW * C;
+  if (static_cast<long long>(B) * H * W * C >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
+  lrn_pool_fwd_kernel<T><<<grid_for(total, 256, 148 * 32), 256, 0, st>>>(
+      a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, static_cast<int>(total));
+}
+
+template <class TA>
+void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* dz, int B, int H,
+                         int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
+                         int PH, int PW, int relu_mask, cudaStream_t st) {
+  const long long npix = static_cast<long long>(B) * H * W;
+  const int PT = std::max(1, 2048 / C);
+  const size_t smem = static_cast<size_t>(PT) * C * 4 * sizeof(float);
+  const long long blocks = (npix + PT - 1) / PT;
+  if (npix * C >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
+  lrn_pool_bwd_kernel<TA><<<static_cast<unsigned>(blocks), 256, smem, st>>>(
+      gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, relu_mask,
+      static_cast<int>(npix), PT);
+}
+
+template <class T>
+void launch_maxpool_fwd_w(const T* x, T* y, uint8_t* widx, int B, int H, int W, int C, int k, int s,
+                          int OH, int OW, cudaStream_t st) {
+  const long long n = static_cast<long long>(B) * OH * OW * C;
+  maxpool_fwd_w_kernel<T><<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(x, y, widx, H, W, C, k, s, OH, OW, n);
+}
+
+template <class TO, class TM>
+void launch_maxpool_bwd_w(const float* gy, const uint8_t* widx, TO* gx, const TM* mask, int B, int H,
+                          int W, int C, int k, int s, int OH, int OW, cudaStream_t st) {
+  const long long n = static_cast<long long>(B) * H * W * C;
+  maxpool_bwd_w_kernel<TO, TM><<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(gy, widx, gx, mask, H, W, C, k,
+                                                                           s, OH, OW, n);
+}
+
+template <class T>
+void launch_rotate_weights(const float* w, long long ldk, T* wrot, int F, int C, int R, int S,
+                           cudaStream_t st) {
+  const long long n = static_cast<long long>(F) * C * R * S;
+  rotate_weights_kernel<T><<<grid_for(n), 256, 0, st>>>(w, ldk, wrot, F, C, R, S);
+}
+
+#define INST_NEW(T)                                                                             \
+  template void launch_im2col_nchw<T>(const float*, T*, int, int, int, int, int, int, int, int, int, \
+                                      int, long long, cudaStream_t);                            \
+  template void launch_lrn_pool_fwd<T>(const T*, T*, uint8_t*, int, int, int, int, int, float,   \
+                                       float, float, int, int, int, int, cudaStream_t);         \
+  template void launch_lrn_pool_bwd<T>(const float*, const uint8_t*, const T*, T*, int, int, int, \
+                                       int, int, float, float, float, int, int, int, int, int,  \
+                                       cudaStream_t);                                           \
+  template void launch_maxpool_fwd_w<T>(const T*, T*, uint8_t*, int, int, int, int, int, int, int, \
+                                        int, cudaStream_t);                                     \
+  template void launch_rotate_weights<T>(const float*, long long, T*, int, int, int, int,       \
+                                         cudaStream_t);
+
+INST_NEW(float)
+INST_NEW(bf16)
+
+#define INST_MPB(TO, TM)                                                                        \
+  template void launch_maxpool_bwd_w<TO, TM>(const float*, const uint8_t*, TO*, const TM*, int,  \
+                                             int, int, int, int, int, int, int, cudaStream_t);
+INST_MPB(float, float)
+INST_MPB(float, bf16)
+INST_MPB(bf16, bf16)
 template <class T>
 void launch_nchw_to_nhwc(const float* x, T* y, int B, int C, int H, int W, cudaStream_t s) {
   const long long n = static_cast<long long>(B) * H * W;

@@ -103,6 +103,39 @@ void copy2d(void* dst, long long dp, const void* src, long long sp, long long by
 template <class TO, class TM>
 void launch_mask_cast(const float* g, const TM* mask, TO* out, long long n, cudaStream_t st);
 
+// im2col straight from the reference's NCHW fp32 batch (first layer, C not a
+// multiple of 128 bytes): col [B*OH*OW][ldk] in T, k = (r*S+s)*C + c, columns
+// [R*S*C, ldk) zero.
+template <class T>
+void launch_im2col_nchw(const float* x, T* col, int B, int C, int H, int W, int R, int S,
+                        int stride, int pad, int OH, int OW, long long ldk, cudaStream_t st);
+
+// Fused cross-channel LRN + overlapping max-pool forward (conv1/conv2 of
+// AlexNet): y = maxpool(lrn(a)); the LRN output and its scale are never
+// written (recomputed in backward). widx = argmax window offset r*k+q.
+template <class T>
+void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, int C, int n,
+                         float alpha, float beta, float kk, int pk, int ps, int PH, int PW,
+                         cudaStream_t st);
+// Fused backward: dz = relu_mask(a) * lrn_bwd(a, pool_bwd(gy, widx)).
+template <class TA>
+void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* dz, int B, int H,
+                         int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
+                         int PH, int PW, int relu_mask, cudaStream_t st);
+// Max-pool forward / backward with window-offset argmax (no LRN).
+template <class T>
+void launch_maxpool_fwd_w(const T* x, T* y, uint8_t* widx, int B, int H, int W, int C, int k, int s,
+                          int OH, int OW, cudaStream_t st);
+template <class TO, class TM>
+void launch_maxpool_bwd_w(const float* gy, const uint8_t* widx, TO* gx, const TM* mask, int B, int H,
+                          int W, int C, int k, int s, int OH, int OW, cudaStream_t st);
+
+// wrot[c][r][s][f] = w[f][R-1-r][S-1-s][c] (w rows of stride ldk), cast to T:
+// the stride-1 dgrad as a convolution over dY.
+template <class T>
+void launch_rotate_weights(const float* w, long long ldk, T* wrot, int F, int C, int R, int S,
+                           cudaStream_t st);
+
 // Scale in place (fp32).
 void launch_scale(float* x, long long n, float s, cudaStream_t st);
 
