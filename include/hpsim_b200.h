@@ -255,6 +255,7 @@ typedef struct hp_gemm_desc {
   const void* mask; int64_t ldmask; int32_t mask_type; int32_t mask_trans;
   int32_t splits; int32_t bn;
   float* ws; /* splits*M*N floats when splits > 1 */
+  int32_t cta2; /* -1 auto (CTA pairs, M=256 tiles, for M >= 256), 0 single-CTA, 1 force pairs */
 } hp_gemm_desc;
 /* D = A * B^T on tcgen05 (replaces matmul/_tn/_nt, tensor.cpp:254-305). */
 HP_API int hp_kernel_gemm(const hp_gemm_desc* d, void* stream);

@@ -110,6 +110,7 @@ class HpGemmDesc(C.Structure):
         ("mask_trans", C.c_int32),
         ("splits", C.c_int32), ("bn", C.c_int32),
         ("ws", C.c_void_p),
+        ("cta2", C.c_int32),
     ]
 
 

@@ -74,11 +74,17 @@ static GemmPlan plan_from_desc(const hp_gemm_desc* d) {
   e.ldmask = d->ldmask;
   e.mask_type = d->mask_type;
   e.mask_trans = d->mask_trans;
-  return gemm_plan(d->math, a, b, d->M, d->N, d->K, e, d->splits, d->ws, d->bn);
+  return gemm_plan(d->math, a, b, d->M, d->N, d->K, e, d->splits, d->ws, d->bn, d->cta2);
 }
 
 HP_API int hp_kernel_gemm_splits(const hp_gemm_desc* d) {
-  return gemm_choose_splits(d->math, d->M, d->N, d->K, d->bn);
+  int splits = 1;
+  const int rc = guarded([&] {
+    hp_gemm_desc q = *d;
+    if (q.ws == nullptr) q.ws = reinterpret_cast<float*>(256);  // sizing only; never dereferenced
+    splits = plan_from_desc(&q).splits;
+  });
+  return rc == HP_OK ? splits : -rc;
 }
 
 HP_API int hp_kernel_gemm(const hp_gemm_desc* d, void* stream) {

@@ -112,6 +112,7 @@ Geometry make_geometry(const hp_model_spec* s, int K, long long b) {
     cg.ldk = round_up(cg.Kc, 8);
     cg.P = b * cg.OH * cg.OW;
     cg.PP = b * cg.PH * cg.PW;
+    cg.ldp = round_up(cg.P, 8);
     g.cg.push_back(cg);
     c = cg.F;
     h = cg.PH;
@@ -432,7 +433,10 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     for (int l = 0; l < nc; ++l) {
       const ConvGeom& c = g_.cg[l];
       const bool lrn_only = c.lrn_n > 0 && c.pk == 0;  // fused LRN+pool keeps no LRN output
-      w.col.push_back(c.impl_fwd ? nullptr : arena_.make<TA>(c.P * c.ldk));
+      // layer 0 explicit: transposed colT [Kc][P]; other explicit layers: col [P][ldk]
+      w.col.push_back(c.impl_fwd ? nullptr
+                                 : (l == 0 ? arena_.make<TA>(static_cast<long long>(c.Kc) * c.ldp)
+                                           : arena_.make<TA>(c.P * c.ldk)));
       w.act.push_back(arena_.make<TA>(c.P * c.F));
       w.lrn.push_back(lrn_only ? arena_.make<TA>(c.P * c.F) : nullptr);
       w.lrn_d.push_back(lrn_only ? arena_.make<float>(c.P * c.F) : nullptr);
@@ -563,7 +567,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     e.bias = w.cp + conv_b_off(l);
     e.bias_mode = 2;
     e.relu = c.relu;
-    GemmOperand xa = op(w.col[l], 0, c.ldk);
+    GemmOperand xa = l == 0 ? op(w.col[0], 1, c.ldp) : op(w.col[l], 0, c.ldk);
     if (c.impl_fwd) {
       xa = op(in, 0, 0);
       xa.conv = view;
@@ -573,7 +577,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     Epi eg;
     eg.c = w.cgr + conv_k_off(l);
     eg.ldc = c.ldk;
-    GemmOperand xb = op(w.col[l], 1, c.ldk);
+    GemmOperand xb = l == 0 ? op(w.col[0], 0, c.ldp) : op(w.col[l], 1, c.ldk);
     if (c.impl_fwd) {
       xb = op(in, 1, 0);
       xb.conv = view;
@@ -603,7 +607,8 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       ed.ldc = c.C;
       GemmOperand dy = op(w.dz[l], 0, 0);
       dy.conv = Im2col{1, static_cast<int>(b_), c.OH, c.OW, c.F, c.R, c.S, 1, c.R - 1 - c.pad, c.H, c.W};
-      w.conv_dgrad.push_back(plan(dy, op(w.wrot[l], 0, c.Kc), b_ * c.H * c.W, c.C, c.Kc, ed));
+      const long long kd = static_cast<long long>(c.R) * c.S * c.F;  // dgrad reduces over (r, s, f)
+      w.conv_dgrad.push_back(plan(dy, op(w.wrot[l], 0, kd), b_ * c.H * c.W, c.C, kd, ed));
     } else {
       // dcol[P][Kc] = dz[P][F] . W[F][Kc], then col2im
       Epi ed;
@@ -780,8 +785,8 @@ void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
     const ConvGeom& c = g_.cg[l];
     if (!c.impl_fwd) {
       if (l == 0) {
-        launch_im2col_nchw<TA>(w.x_src, w.col[0], B, c.C, c.H, c.W, c.R, c.S, c.stride, c.pad, c.OH,
-                               c.OW, c.ldk, st_);
+        launch_im2col_t_nchw<TA>(w.x_src, w.col[0], B, c.C, c.H, c.W, c.R, c.S, c.stride, c.pad, c.OH,
+                                 c.OW, c.ldp, st_);
       } else {
         launch_im2col<TA>(stage_in(w, l), w.col[l], B, c.H, c.W, c.C, c.R, c.S, c.stride, c.pad,
                           c.OH, c.OW, c.ldk, st_);

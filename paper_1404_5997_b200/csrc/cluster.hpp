@@ -27,6 +27,7 @@ struct ConvGeom {
   long long ldk;               // padded row stride of col / kernels (16-byte multiple)
   long long P;                 // b*OH*OW rows per worker
   long long PP;                // b*PH*PW
+  long long ldp;               // P rounded up to 8 (row stride of layer 0's transposed col)
 };
 
 struct FcGeom {

@@ -31,6 +31,7 @@ __host__ __device__ constexpr int num_stages(int bn, int math) {
              ? 6
              : static_cast<int>((kMaxDynSmem - 2048u) / stage_bytes(bn, math));
 }
+// TMEM columns of one accumulator (power of two >= 32); two are allocated.
 __host__ __device__ constexpr uint32_t tmem_cols(int bn) {
   return bn <= 32 ? 32u : bn <= 64 ? 64u : bn <= 128 ? 128u : 256u;
 }
@@ -61,10 +62,11 @@ __device__ __forceinline__ void epi_elem(const Epi& e, int m, int n, float v) {
 }
 
 // Epilogue for 32 consecutive columns [n0, n0+32) of row m.
-__device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, const float (&v)[32]) {
+__device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int split,
+                                          const float (&v)[32]) {
   if (m >= a.M) return;
   if (a.raw_partial) {
-    float* dst = a.ws + static_cast<long long>(blockIdx.z) * a.M * a.N +
+    float* dst = a.ws + static_cast<long long>(split) * a.M * a.N +
                  static_cast<long long>(m) * a.N;
     if (n0 + 32 <= a.N && (a.N & 3) == 0) {
 #pragma unroll
@@ -162,19 +164,37 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, cons
   }
 }
 
-template <int ES, int BK, int ATOM>
-__device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
-                                          int mn_major, int row0, int rows, int k0) {
-  if (!mn_major) {
-    tma_load_2d(dst, tm, bar, k0, row0);
+template <bool TWO>
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int x, int y) {
+  if (TWO) {
+    tma_load_2d_2sm(dst, tm, bar, x, y);
   } else {
-    for (int a = 0; a < rows / ATOM; ++a) tma_load_2d(dst + a * (BK * 128), tm, bar, row0 + a * ATOM, k0);
+    tma_load_2d(dst, tm, bar, x, y);
+  }
+}
+template <bool TWO>
+__device__ __forceinline__ void tma_im2col(void* dst, const CUtensorMap* tm, uint64_t* bar, int c, int w,
+                                           int h, int n, uint16_t s, uint16_t r) {
+  if (TWO) {
+    tma_load_im2col_4d_2sm(dst, tm, bar, c, w, h, n, s, r);
+  } else {
+    tma_load_im2col_4d(dst, tm, bar, c, w, h, n, s, r);
+  }
+}
+
+template <bool TWO, int BK, int ATOM>
+__device__ __forceinline__ void load_tile_t(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
+                                            int mn_major, int row0, int rows, int k0) {
+  if (!mn_major) {
+    tma2d<TWO>(dst, tm, bar, k0, row0);
+  } else {
+    for (int a = 0; a < rows / ATOM; ++a) tma2d<TWO>(dst + a * (BK * 128), tm, bar, row0 + a * ATOM, k0);
   }
 }
 
 // im2col A tile (fprop / rotated dgrad): 128 consecutive output pixels x one
 // 128-byte channel block of filter tap (r, s) for k-tile kt.
-template <int ATOM>
+template <bool TWO, int ATOM>
 __device__ __forceinline__ void load_a_im2col(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
                                               const ConvArgs& c, int m0, int kt) {
   const int cblks = c.C / ATOM;
@@ -183,13 +203,13 @@ __device__ __forceinline__ void load_a_im2col(uint8_t* dst, const CUtensorMap* t
   const int ohw = c.OH * c.OW;
   const int n = m0 / ohw, rem = m0 - n * ohw;
   const int oh = rem / c.OW, ow = rem - oh * c.OW;
-  tma_load_im2col_4d(dst, tm, bar, cb * ATOM, c.lo_w + ow * c.stride, c.lo_h + oh * c.stride, n,
-                     static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+  tma_im2col<TWO>(dst, tm, bar, cb * ATOM, c.lo_w + ow * c.stride, c.lo_h + oh * c.stride, n,
+                  static_cast<uint16_t>(s), static_cast<uint16_t>(r));
 }
 
 // im2col B tile (wgrad, MN-major): BK consecutive output pixels (the K
-// dimension) x BN columns = BN/ATOM channel blocks, each at its own tap.
-template <int BK, int ATOM>
+// dimension) x `rows` columns = rows/ATOM channel blocks, each at its own tap.
+template <bool TWO, int BK, int ATOM>
 __device__ __forceinline__ void load_b_im2col(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar,
                                               const ConvArgs& c, int n0, int rows, int kt) {
   const int ohw = c.OH * c.OW;
@@ -200,10 +220,31 @@ __device__ __forceinline__ void load_b_im2col(uint8_t* dst, const CUtensorMap* t
     const int col = n0 + a * ATOM;
     const int rs = col / c.C, ch = col - rs * c.C;
     const int r = rs / c.S, s = rs - r * c.S;
-    tma_load_im2col_4d(dst + a * (BK * 128), tm, bar, ch, c.lo_w + ow * c.stride,
-                       c.lo_h + oh * c.stride, n, static_cast<uint16_t>(s),
-                       static_cast<uint16_t>(r));
+    tma_im2col<TWO>(dst + a * (BK * 128), tm, bar, ch, c.lo_w + ow * c.stride, c.lo_h + oh * c.stride, n,
+                    static_cast<uint16_t>(s), static_cast<uint16_t>(r));
   }
+}
+
+// Persistent tile loop. Tiles t = blockIdx.x, blockIdx.x + gridDim.x, ... in
+// (split, m, n) order with n fastest, so co-resident CTAs share A tiles in L2.
+// Two TMEM accumulators: the epilogue of tile i overlaps the MMAs of tile i+1.
+// 3xTF32 runs one tile per CTA (its epilogue warps double as tile converters).
+struct TileIdx {
+  int m0, n0, split, kt0, kt1;
+};
+
+template <int BN>
+__device__ __forceinline__ TileIdx tile_idx(const GemmArgs& a, int t, int tiles_m, int tiles_n) {
+  TileIdx r;
+  const int mn = tiles_m * tiles_n;
+  r.split = t / mn;
+  const int rem = t - r.split * mn;
+  const int mb = rem / tiles_n;
+  r.m0 = mb * kBM;
+  r.n0 = (rem - mb * tiles_n) * BN;
+  r.kt0 = r.split * a.k_tiles_per_split;
+  r.kt1 = min(a.k_tiles_total, r.kt0 + a.k_tiles_per_split);
+  return r;
 }
 
 template <int BN, int MATH>
@@ -219,7 +260,9 @@ __global__ void __launch_bounds__(192, 1)
   constexpr uint32_t B_BYTES = BN * 128;
   constexpr uint32_t SB = stage_bytes(BN, MATH);
   constexpr int STAGES = num_stages(BN, MATH);
-  constexpr uint32_t TCOLS = tmem_cols(BN);
+  constexpr int NACC = SPLIT ? 1 : 2;
+  constexpr uint32_t ACOLS = tmem_cols(BN);
+  constexpr uint32_t TCOLS = ACOLS * NACC;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -227,15 +270,15 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SB);
   uint64_t* empty = full + STAGES;
   uint64_t* conv = empty + STAGES;  // 3xTF32: split done (converter -> MMA)
-  uint64_t* tfull = conv + STAGES;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = conv + STAGES;  // [NACC]
+  uint64_t* tempty = tfull + 2;     // [NACC]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * kBM;
-  const int n0 = blockIdx.y * BN;
-  const int kt0 = blockIdx.z * args.k_tiles_per_split;
-  const int kt1 = min(args.k_tiles_total, kt0 + args.k_tiles_per_split);
+  const int tiles_m = (args.M + kBM - 1) / kBM;
+  const int tiles_n = (args.N + BN - 1) / BN;
+  const int total = tiles_m * tiles_n * ((args.k_tiles_total + args.k_tiles_per_split - 1) / args.k_tiles_per_split);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -243,7 +286,10 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&empty[s], 1);
       mbar_init(&conv[s], 128);
     }
-    mbar_init(tfull, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
     fence_barrier_init();
     tma_prefetch(&ta);
     tma_prefetch(&tb);
@@ -258,24 +304,27 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int kt = kt0; kt < kt1; ++kt) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* sa = smem + stage * SB;
-        uint8_t* sb = sa + A_BYTES;
-        mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
-        if (args.ca.enabled) {
-          load_a_im2col<ATOM>(sa, &ta, &full[stage], args.ca, m0, kt);
-        } else {
-          load_tile<ES, BK, ATOM>(sa, &ta, &full[stage], args.a_mn, m0, kBM, kt * BK);
-        }
-        if (args.cb.enabled) {
-          load_b_im2col<BK, ATOM>(sb, &tb, &full[stage], args.cb, n0, BN, kt);
-        } else {
-          load_tile<ES, BK, ATOM>(sb, &tb, &full[stage], args.b_mn, n0, BN, kt * BK);
-        }
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const TileIdx ti = tile_idx<BN>(args, t, tiles_m, tiles_n);
+        for (int kt = ti.kt0; kt < ti.kt1; ++kt) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * SB;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
+          if (args.ca.enabled) {
+            load_a_im2col<false, ATOM>(sa, &ta, &full[stage], args.ca, ti.m0, kt);
+          } else {
+            load_tile_t<false, BK, ATOM>(sa, &ta, &full[stage], args.a_mn, ti.m0, kBM, kt * BK);
+          }
+          if (args.cb.enabled) {
+            load_b_im2col<false, BK, ATOM>(sb, &tb, &full[stage], args.cb, ti.n0, BN, kt);
+          } else {
+            load_tile_t<false, BK, ATOM>(sb, &tb, &full[stage], args.b_mn, ti.n0, BN, kt * BK);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -299,84 +348,103 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t b_kstep = args.b_mn ? UK * 128 : UK * ES;
       int stage = 0;
       uint32_t phase = 0;
-      for (int kt = kt0; kt < kt1; ++kt) {
-        mbar_wait(SPLIT ? &conv[stage] : &full[stage], phase);
+      int local = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+        const TileIdx ti = tile_idx<BN>(args, t, tiles_m, tiles_n);
+        const int buf = NACC == 2 ? (local & 1) : 0;
+        const uint32_t use = NACC == 2 ? static_cast<uint32_t>(local >> 1) : static_cast<uint32_t>(local);
+        mbar_wait(&tempty[buf], (use & 1) ^ 1);  // epilogue drained this accumulator
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + stage * SB);
-        const uint32_t sb = sa + A_BYTES;
+        const uint32_t d = tmem + static_cast<uint32_t>(buf) * ACOLS;
+        for (int kt = ti.kt0; kt < ti.kt1; ++kt) {
+          mbar_wait(SPLIT ? &conv[stage] : &full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * SB);
+          const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / UK; ++k) {
-          const uint64_t ad = umma_desc_sw128(sa + k * a_kstep, a_lbo, a_sbo, a_lay);
-          const uint64_t bd = umma_desc_sw128(sb + k * b_kstep, b_lbo, b_sbo, b_lay);
-          const uint32_t acc = (kt > kt0 || k > 0) ? 1u : 0u;
-          if (MATH == kMathBF16) {
-            mma_f16(tmem, ad, bd, idesc, acc);
-          } else {
-            mma_tf32(tmem, ad, bd, idesc, acc);
-            if (SPLIT) {
-              const uint64_t ad2 =
-                  umma_desc_sw128(sb + B_BYTES + k * a_kstep, a_lbo, a_sbo, a_lay);
-              const uint64_t bd2 =
-                  umma_desc_sw128(sb + B_BYTES + A_BYTES + k * b_kstep, b_lbo, b_sbo, b_lay);
-              mma_tf32(tmem, ad, bd2, idesc, 1u);
-              mma_tf32(tmem, ad2, bd, idesc, 1u);
+          for (int k = 0; k < BK / UK; ++k) {
+            const uint64_t ad = umma_desc_sw128(sa + k * a_kstep, a_lbo, a_sbo, a_lay);
+            const uint64_t bd = umma_desc_sw128(sb + k * b_kstep, b_lbo, b_sbo, b_lay);
+            const uint32_t acc = (kt > ti.kt0 || k > 0) ? 1u : 0u;
+            if (MATH == kMathBF16) {
+              mma_f16(d, ad, bd, idesc, acc);
+            } else {
+              mma_tf32(d, ad, bd, idesc, acc);
+              if (SPLIT) {
+                const uint64_t ad2 =
+                    umma_desc_sw128(sb + B_BYTES + k * a_kstep, a_lbo, a_sbo, a_lay);
+                const uint64_t bd2 =
+                    umma_desc_sw128(sb + B_BYTES + A_BYTES + k * b_kstep, b_lbo, b_sbo, b_lay);
+                mma_tf32(d, ad, bd2, idesc, 1u);
+                mma_tf32(d, ad2, bd, idesc, 1u);
+              }
             }
           }
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
-        mma_commit(&empty[stage]);
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
+        mma_commit(&tfull[buf]);
       }
-      mma_commit(tfull);
     }
     __syncwarp();
   } else {
-    if (SPLIT) {
-      // 3xTF32: while the MMA warp waits, the epilogue warps split every
-      // landed fp32 tile in place into hi = rna_tf32(x) and lo = x - hi (exact),
-      // so D = Ahi*Bhi + Ahi*Blo + Alo*Bhi reaches ~fp32 accuracy. The swizzle
-      // is elementwise, so lo tiles share the hi tiles' layout.
-      const int t = threadIdx.x - 64;
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int kt = kt0; kt < kt1; ++kt) {
-        mbar_wait(&full[stage], phase);
-        float4* hi = reinterpret_cast<float4*>(smem + stage * SB);
-        float4* lo = reinterpret_cast<float4*>(smem + stage * SB + A_BYTES + B_BYTES);
-        constexpr int NV = (A_BYTES + B_BYTES) / 16;
+    const int q = warp & 3;
+    int cstage = 0;
+    uint32_t cphase = 0;
+    int local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      const TileIdx ti = tile_idx<BN>(args, t, tiles_m, tiles_n);
+      if (SPLIT) {
+        // 3xTF32: split every landed fp32 tile in place into hi = rna_tf32(x)
+        // and lo = x - hi (exact) so D = Ahi*Bhi + Ahi*Blo + Alo*Bhi. The
+        // swizzle is elementwise, so lo tiles share the hi tiles' layout.
+        const int tt = threadIdx.x - 64;
+        for (int kt = ti.kt0; kt < ti.kt1; ++kt) {
+          mbar_wait(&full[cstage], cphase);
+          float4* hi = reinterpret_cast<float4*>(smem + cstage * SB);
+          float4* lo = reinterpret_cast<float4*>(smem + cstage * SB + A_BYTES + B_BYTES);
+          constexpr int NV = (A_BYTES + B_BYTES) / 16;
 #pragma unroll 4
-        for (int i = t; i < NV; i += 128) {
-          float4 x = hi[i], h, l;
-          h.x = tf32_rna(x.x); l.x = x.x - h.x;
-          h.y = tf32_rna(x.y); l.y = x.y - h.y;
-          h.z = tf32_rna(x.z); l.z = x.z - h.z;
-          h.w = tf32_rna(x.w); l.w = x.w - h.w;
-          hi[i] = h;
-          lo[i] = l;
-        }
-        fence_proxy_async_smem();
-        mbar_arrive(&conv[stage]);
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
+          for (int i = tt; i < NV; i += 128) {
+            float4 x = hi[i], h, l;
+            h.x = tf32_rna(x.x); l.x = x.x - h.x;
+            h.y = tf32_rna(x.y); l.y = x.y - h.y;
+            h.z = tf32_rna(x.z); l.z = x.z - h.z;
+            h.w = tf32_rna(x.w); l.w = x.w - h.w;
+            hi[i] = h;
+            lo[i] = l;
+          }
+          fence_proxy_async_smem();
+          mbar_arrive(&conv[cstage]);
+          if (++cstage == STAGES) {
+            cstage = 0;
+            cphase ^= 1;
+          }
         }
       }
-    }
-    mbar_wait(tfull, 0);
-    tc_fence_after();
-    const int q = warp & 3;
-    const int m = m0 + q * 32 + lane;
+      const int buf = NACC == 2 ? (local & 1) : 0;
+      const uint32_t use = NACC == 2 ? static_cast<uint32_t>(local >> 1) : static_cast<uint32_t>(local);
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+      const int m = ti.m0 + q * 32 + lane;
+      const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf) * ACOLS;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c), r);
-      tmem_ld_wait();
-      float v[32];
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(base + static_cast<uint32_t>(c), r);
+        tmem_ld_wait();
+        if (c + 32 >= BN) {  // accumulator fully in registers: hand it back to the MMA warp
+          tc_fence_before();
+          mbar_arrive(&tempty[buf]);
+        }
+        float v[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-      if (n0 + c < args.N) epi_row32(args, m, n0 + c, v);
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (ti.n0 + c < args.N) epi_row32(args, m, ti.n0 + c, ti.split, v);
+      }
     }
   }
   tc_fence_before();
@@ -384,6 +452,205 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, TCOLS);
+  }
+}
+
+// CTA-pair GEMM: tcgen05.mma.cta_group::2 over a 256 x BN tile. Each CTA
+// stages its own 128 rows of A and half (BN/2 rows) of B; the leader (rank 0)
+// issues the M=256 MMAs; each CTA's TMEM holds its 128 accumulator rows and
+// its epilogue stores them. Halves the B (and L2) traffic per SM vs 1-CTA.
+__host__ __device__ constexpr uint32_t stage_bytes2(int bn) {
+  return kBM * 128u + static_cast<uint32_t>(bn / 2) * 128u;
+}
+__host__ __device__ constexpr int num_stages2(int bn) {
+  return static_cast<int>((kMaxDynSmem - 2048u) / stage_bytes2(bn)) > 8
+             ? 8
+             : static_cast<int>((kMaxDynSmem - 2048u) / stage_bytes2(bn));
+}
+
+template <int BN, int MATH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                 const GemmArgs args) {
+  static_assert(MATH != kMathF32x3, "3xTF32 runs on the 1-CTA kernel");
+  constexpr int ES = MATH == kMathBF16 ? 2 : 4;
+  constexpr int BK = 128 / ES;
+  constexpr int UK = 32 / ES;
+  constexpr int ATOM = 128 / ES;
+  constexpr int BNH = BN / 2;
+  constexpr uint32_t A_BYTES = kBM * 128;
+  constexpr uint32_t SB = stage_bytes2(BN);
+  constexpr int STAGES = num_stages2(BN);
+  constexpr uint32_t ACOLS = tmem_cols(BN);
+  constexpr uint32_t TCOLS = ACOLS * 2;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SB);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int cid = blockIdx.x >> 1;
+  const int ncl = gridDim.x >> 1;
+  const int tiles_m = (args.M + 2 * kBM - 1) / (2 * kBM);
+  const int tiles_n = (args.N + BN - 1) / BN;
+  const int splits = (args.k_tiles_total + args.k_tiles_per_split - 1) / args.k_tiles_per_split;
+  const int total = tiles_m * tiles_n * splits;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 256);  // both CTAs' epilogue threads (leader's copy is used)
+    }
+    fence_barrier_init();
+    tma_prefetch(&ta);
+    tma_prefetch(&tb);
+  }
+  if (warp == 1) tmem_alloc2(tslot, TCOLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  auto tile_of = [&](int t, int& m0, int& n0, int& split, int& kt0, int& kt1) {
+    const int mn = tiles_m * tiles_n;
+    split = t / mn;
+    const int rem = t - split * mn;
+    const int mb = rem / tiles_n;
+    m0 = mb * 2 * kBM;
+    n0 = (rem - mb * tiles_n) * BN;
+    kt0 = split * args.k_tiles_per_split;
+    kt1 = min(args.k_tiles_total, kt0 + args.k_tiles_per_split);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < total; t += ncl) {
+        int m0, n0, split, kt0, kt1;
+        tile_of(t, m0, n0, split, kt0, kt1);
+        const int am = m0 + static_cast<int>(rank) * kBM;
+        const int bn0 = n0 + static_cast<int>(rank) * BNH;
+        for (int kt = kt0; kt < kt1; ++kt) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * SB;
+          uint8_t* sb = sa + A_BYTES;
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * SB);
+          if (args.ca.enabled) {
+            load_a_im2col<true, ATOM>(sa, &ta, &full[stage], args.ca, am, kt);
+          } else {
+            load_tile_t<true, BK, ATOM>(sa, &ta, &full[stage], args.a_mn, am, kBM, kt * BK);
+          }
+          if (args.cb.enabled) {
+            load_b_im2col<true, BK, ATOM>(sb, &tb, &full[stage], args.cb, bn0, BNH, kt);
+          } else {
+            load_tile_t<true, BK, ATOM>(sb, &tb, &full[stage], args.b_mn, bn0, BNH, kt * BK);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t fmt = MATH == kMathBF16 ? 1u : 2u;
+      const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
+                             (static_cast<uint32_t>(args.a_mn) << 15) |
+                             (static_cast<uint32_t>(args.b_mn) << 16) |
+                             (static_cast<uint32_t>(BN >> 3) << 17) |
+                             (static_cast<uint32_t>((2 * kBM) >> 4) << 24);
+      const uint32_t a_lbo = args.a_mn ? BK * 128 : 16;
+      const uint32_t b_lbo = args.b_mn ? BK * 128 : 16;
+      const uint32_t a_sbo = (ES == 4 && args.a_mn) ? 512 : 1024;
+      const uint32_t b_sbo = (ES == 4 && args.b_mn) ? 512 : 1024;
+      const uint32_t a_lay = (ES == 4 && args.a_mn) ? 1 : 2;
+      const uint32_t b_lay = (ES == 4 && args.b_mn) ? 1 : 2;
+      const uint32_t a_kstep = args.a_mn ? UK * 128 : UK * ES;
+      const uint32_t b_kstep = args.b_mn ? UK * 128 : UK * ES;
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = cid; t < total; t += ncl, ++local) {
+        int m0, n0, split, kt0, kt1;
+        tile_of(t, m0, n0, split, kt0, kt1);
+        const int buf = local & 1;
+        const uint32_t use = static_cast<uint32_t>(local >> 1);
+        mbar_wait(&tempty[buf], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + static_cast<uint32_t>(buf) * ACOLS;
+        for (int kt = kt0; kt < kt1; ++kt) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * SB);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k) {
+            const uint64_t ad = umma_desc_sw128(sa + k * a_kstep, a_lbo, a_sbo, a_lay);
+            const uint64_t bd = umma_desc_sw128(sb + k * b_kstep, b_lbo, b_sbo, b_lay);
+            const uint32_t acc = (kt > kt0 || k > 0) ? 1u : 0u;
+            if (MATH == kMathBF16) {
+              mma_f16_2sm(d, ad, bd, idesc, acc);
+            } else {
+              mma_tf32_2sm(d, ad, bd, idesc, acc);
+            }
+          }
+          mma_commit_2sm(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_2sm(&tfull[buf]);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    const uint32_t tempty_leader[2] = {mapa(smem_u32(&tempty[0]), 0), mapa(smem_u32(&tempty[1]), 0)};
+    int local = 0;
+    for (int t = cid; t < total; t += ncl, ++local) {
+      int m0, n0, split, kt0, kt1;
+      tile_of(t, m0, n0, split, kt0, kt1);
+      const int buf = local & 1;
+      const uint32_t use = static_cast<uint32_t>(local >> 1);
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+      const int m = m0 + static_cast<int>(rank) * kBM + q * 32 + lane;
+      const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf) * ACOLS;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(base + static_cast<uint32_t>(c), r);
+        tmem_ld_wait();
+        if (c + 32 >= BN) {
+          tc_fence_before();
+          mbar_arrive_cluster(tempty_leader[buf]);
+        }
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (n0 + c < args.N) epi_row32(args, m, n0 + c, split, v);
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2(tmem, TCOLS);
   }
 }
 
@@ -505,6 +772,17 @@ CUtensorMap operand_map(const GemmOperand& o, const void* ptr, int es, int rows,
 }
 
 template <int BN, int MATH>
+void launch_inst2(const GemmPlan& p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm2_kernel<BN, MATH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(p.smem));
+    attr = true;
+  }
+  gemm2_kernel<BN, MATH><<<p.grid, 192, p.smem, s>>>(p.ta, p.tb, p.args);
+}
+
+template <int BN, int MATH>
 void launch_inst(const GemmPlan& p, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
@@ -517,6 +795,16 @@ void launch_inst(const GemmPlan& p, cudaStream_t s) {
 
 template <int MATH>
 void launch_math(const GemmPlan& p, cudaStream_t s) {
+  if (p.cta2) {
+    if constexpr (MATH != kMathF32x3) {
+      switch (p.bn) {
+        case 128: launch_inst2<128, MATH>(p, s); return;
+        case 256: launch_inst2<256, MATH>(p, s); return;
+        default: break;
+      }
+    }
+    throw std::runtime_error("gemm: unsupported 2-CTA configuration");
+  }
   switch (p.bn) {
     case 64: launch_inst<64, MATH>(p, s); break;
     case 128: launch_inst<128, MATH>(p, s); break;
@@ -557,6 +845,14 @@ int gemm_choose_splits(int math, int M, int N, int K, int bn) {
   const int es = math == kMathBF16 ? 2 : 4;
   const int kt = cdiv(K, 128 / es);
   const int tiles = cdiv(M, kBM) * cdiv(N, bn);
+  if (math == kMathF32x3) {
+    // Parity mode: the tensor core accumulates with round-toward-zero, so the
+    // error grows with the accumulation chain. Bound each chain to 4 k-tiles
+    // (128 tf32 products); the split partials are summed in fp32 (RN).
+    const int splits = std::max(1, std::min(cdiv(kt, 4), 512));
+    const int kps = cdiv(kt, splits);
+    return cdiv(kt, kps);
+  }
   if (tiles >= 120 || kt < 4) return 1;
   int splits = std::min(cdiv(148, tiles), kt / 2);
   splits = std::max(1, std::min(splits, 64));
@@ -564,16 +860,36 @@ int gemm_choose_splits(int math, int M, int N, int K, int bn) {
   return cdiv(kt, kps);
 }
 
+static bool g_cta2_default = true;
+void gemm_set_cta2_default(bool on) { g_cta2_default = on; }
+
 GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
-                   const Epi& epi, int splits, float* ws, int bn) {
+                   const Epi& epi, int splits, float* ws, int bn, int cta2) {
   if (M <= 0 || N <= 0 || K <= 0) throw std::runtime_error("gemm: empty problem");
   GemmPlan p;
   p.math = math;
-  p.bn = bn > 0 ? bn : gemm_choose_bn(M, N);
   const int es = math == kMathBF16 ? 2 : 4;
   const int BK = 128 / es;
   const int kt = cdiv(K, BK);
-  if (splits <= 0) splits = gemm_choose_splits(math, M, N, K, p.bn);
+  const bool use2 = math != kMathF32x3 && (cta2 == 1 || (cta2 == -1 && g_cta2_default && M >= 256));
+  if (cta2 == 1 && math == kMathF32x3) throw std::runtime_error("gemm: 3xTF32 has no 2-CTA kernel");
+  p.cta2 = use2;
+  if (use2) {
+    if (bn == 128 || bn == 256) {
+      p.bn = bn;
+    } else {
+      // wide tiles unless they waste more than ~20% of the N extent
+      const double w256 = static_cast<double>(N) / (cdiv(N, 256) * 256.0);
+      p.bn = w256 >= 0.8 ? 256 : 128;
+    }
+    if (splits <= 0) {
+      const int tiles2 = cdiv(M, 2 * kBM) * cdiv(N, p.bn);
+      splits = (tiles2 >= 60 || kt < 4) ? 1 : std::max(1, std::min({cdiv(74, tiles2), kt / 2, 64}));
+    }
+  } else {
+    p.bn = bn > 0 ? bn : gemm_choose_bn(M, N);
+    if (splits <= 0) splits = gemm_choose_splits(math, M, N, K, p.bn);
+  }
   const int kps = cdiv(kt, splits);
   splits = cdiv(kt, kps);
   p.splits = splits;
@@ -588,6 +904,7 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   p.args.ws = ws;
   p.args.epi = epi;
   if (splits > 1 && ws == nullptr) throw std::runtime_error("gemm: split-K needs a workspace");
+  const int b_rows = use2 ? p.bn / 2 : p.bn;
   if (a.conv.enabled) {
     if (a.mn_major) throw std::runtime_error("gemm: im2col A must be K-major");
     p.ta = im2col_map(a.ptr, es, a.conv, kBM, false);
@@ -598,12 +915,19 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
     if (!b.mn_major) throw std::runtime_error("gemm: im2col B must be MN-major");
     p.tb = im2col_map(b.ptr, es, b.conv, BK, true);
   } else {
-    p.tb = operand_map(b, b.ptr, es, N, K, p.bn);
+    p.tb = operand_map(b, b.ptr, es, N, K, b_rows);
   }
   p.args.ca = conv_args(a.conv);
   p.args.cb = conv_args(b.conv);
-  p.grid = dim3(cdiv(M, kBM), cdiv(N, p.bn), splits);
-  p.smem = static_cast<size_t>(num_stages(p.bn, math)) * stage_bytes(p.bn, math) + 1024 + 256;
+  if (use2) {
+    const int total = cdiv(M, 2 * kBM) * cdiv(N, p.bn) * splits;
+    p.grid = dim3(2 * std::min(total, 74));
+    p.smem = static_cast<size_t>(num_stages2(p.bn)) * stage_bytes2(p.bn) + 1024 + 256;
+  } else {
+    const int total = cdiv(M, kBM) * cdiv(N, p.bn) * splits;
+    p.grid = dim3(math == kMathF32x3 ? total : std::min(total, 148));
+    p.smem = static_cast<size_t>(num_stages(p.bn, math)) * stage_bytes(p.bn, math) + 1024 + 256;
+  }
   p.valid = true;
   return p;
 }

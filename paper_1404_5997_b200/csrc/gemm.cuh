@@ -83,6 +83,7 @@ struct GemmPlan {
   int math = kMathBF16;
   int bn = 128;
   int splits = 1;
+  bool cta2 = false;  // CTA-pair kernel (M=256 tiles, cta_group::2)
   dim3 grid;
   size_t smem = 0;
   bool valid = false;
@@ -91,7 +92,9 @@ struct GemmPlan {
 // Builds a plan. `splits` <= 0 picks a split-K factor from the tile count.
 // `ws` must hold splits*M*N floats when splits > 1 (query with gemm_ws_floats).
 GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
-                   const Epi& epi, int splits, float* ws, int bn = 0);
+                   const Epi& epi, int splits, float* ws, int bn = 0, int cta2 = -1);
+// cta2: -1 auto (pairs for M >= 256 outside 3xTF32), 0 never, 1 force.
+void gemm_set_cta2_default(bool on);
 int gemm_choose_splits(int math, int M, int N, int K, int bn = 0);
 int gemm_choose_bn(int M, int N);
 void gemm_launch(const GemmPlan& p, cudaStream_t s);

@@ -411,42 +411,75 @@ __global__ void scale_kernel(float* x, long long n, float s) {
 }
 
 // ------------------------------------------------------------------ conv1 im2col from NCHW
+// Block = one (image, output row): the R input rows it needs (all C planes,
+// zero-padded columns) are staged in shared memory with coalesced NCHW reads,
+// then the OW col rows are written as coalesced 16-byte chunks.
 template <class T>
-__global__ void im2col_nchw_kernel(const float* __restrict__ x, T* __restrict__ col, int C, int H,
-                                   int W, int S, int stride, int pad, int OH, int OW, int ldk, int K,
-                                   int P) {
+__global__ void __launch_bounds__(256) im2col_nchw_kernel(const float* __restrict__ x, T* __restrict__ col,
+                                                          int C, int H, int W, int R, int S, int stride,
+                                                          int pad, int OH, int OW, int ldk, int K) {
+  extern __shared__ float smf[];
+  const int Wp = W + 2 * pad + S;          // padded row (extra S keeps every tap in range)
+  float* tile = smf;                       // [C][R][Wp]
+  int* tab = reinterpret_cast<int*>(tile + C * R * Wp);  // k -> c*R*Wp + r*Wp + s, or -1
+  const int oh = blockIdx.x % OH, b = blockIdx.x / OH;
+  const int h0 = oh * stride - pad;
+  for (int k = threadIdx.x; k < ldk; k += blockDim.x) {
+    if (k < K) {
+      const int c = k % C, rs = k / C;
+      tab[k] = (c * R + rs / S) * Wp + rs % S;
+    } else {
+      tab[k] = -1;
+    }
+  }
+  const float* xb = x + static_cast<long long>(b) * C * H * W;
+  for (int e = threadIdx.x; e < C * R * Wp; e += blockDim.x) {
+    const int wp = e % Wp, cr = e / Wp, r = cr % R, c = cr / R;
+    const int h = h0 + r, w = wp - pad;
+    tile[e] = (h >= 0 && h < H && w >= 0 && w < W) ? __ldg(xb + (static_cast<long long>(c) * H + h) * W + w) : 0.f;
+  }
+  __syncthreads();
   constexpr int V = 16 / sizeof(T);
   const int chunks = ldk / V;
-  const int n = P * chunks;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int p = i / chunks;
-    const int k0 = (i - p * chunks) * V;
-    const int ow = p % OW;
-    const int t = p / OW;
-    const int oh = t % OH;
-    const int b = t / OH;
-    int c = k0 % C;
-    int rs = k0 / C;
-    int s = rs % S;
-    int r = rs / S;
+  T* out = col + static_cast<long long>(blockIdx.x) * OW * ldk;
+  for (int e = threadIdx.x; e < OW * chunks; e += blockDim.x) {
+    const int ow = e / chunks, ch = e - ow * chunks;
+    const int base = ow * stride;
     __align__(16) T v[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      float val = 0.f;
-      if (k0 + j < K) {
-        const int h = oh * stride - pad + r, w = ow * stride - pad + s;
-        if (h >= 0 && h < H && w >= 0 && w < W) val = __ldg(x + ((static_cast<long long>(b) * C + c) * H + h) * W + w);
-      }
-      v[j] = from_f<T>(val);
-      if (++c == C) {
-        c = 0;
-        if (++s == S) {
-          s = 0;
-          ++r;
-        }
-      }
+      const int t = tab[ch * V + j];
+      v[j] = from_f<T>(t >= 0 ? tile[t + base] : 0.f);
     }
-    *reinterpret_cast<uint4*>(col + static_cast<long long>(p) * ldk + k0) = *reinterpret_cast<const uint4*>(v);
+    *reinterpret_cast<uint4*>(out + static_cast<long long>(ow) * ldk + ch * V) = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
+// Block = (image, output row); threadIdx.x = output column, threadIdx.y steps
+// k. Every element is one L1-resident load and one coalesced store.
+template <class T>
+__global__ void __launch_bounds__(256) im2col_t_nchw_kernel(const float* __restrict__ x, T* __restrict__ colT,
+                                                            int C, int H, int W, int R, int S, int stride,
+                                                            int pad, int OH, int OW, long long ldp, int K) {
+  extern __shared__ int ktab[];  // k -> (c*H*W + r*W + s) offsets relative to the window origin
+  const int oh = blockIdx.x % OH, b = blockIdx.x / OH;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  for (int k = tid; k < K; k += blockDim.x * blockDim.y) {
+    const int c = k % C, rs = k / C;
+    ktab[2 * k] = c * H * W;
+    ktab[2 * k + 1] = ((rs / S) << 16) | (rs % S);
+  }
+  __syncthreads();
+  const int ow = threadIdx.x;
+  if (ow >= OW) return;
+  const float* xb = x + static_cast<long long>(b) * C * H * W;
+  const long long p = (static_cast<long long>(b) * OH + oh) * OW + ow;
+  const int h0 = oh * stride - pad, w0 = ow * stride - pad;
+  for (int k = threadIdx.y; k < K; k += blockDim.y) {
+    const int off = ktab[2 * k], rsv = ktab[2 * k + 1];
+    const int h = h0 + (rsv >> 16), w = w0 + (rsv & 0xFFFF);
+    const float v = (h >= 0 && h < H && w >= 0 && w < W) ? __ldg(xb + off + h * W + w) : 0.f;
+    colT[static_cast<long long>(k) * ldp + p] = from_f<T>(v);
   }
 }
 
@@ -455,104 +488,188 @@ __device__ __forceinline__ float pow_neg(float d, float beta) {
   return exp2f(-beta * __log2f(d));  // d >= k > 0
 }
 
+// 16-byte channel vectors: V = 8 (bf16) or 4 (fp32) channels per thread, plus
+// a halo of up to LH = 4 channels each side (LRN size <= 9).
+constexpr int LH = 4;
+
 template <class T>
-__global__ void lrn_pool_fwd_kernel(const T* __restrict__ a, T* __restrict__ y,
-                                    uint8_t* __restrict__ widx, int H, int W, int C, int lo, int hi,
-                                    float alpha, float beta, float kk, int pk, int ps, int PH, int PW,
-                                    int n) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int c = i % C;
-    int t = i / C;
-    const int pw = t % PW;
-    t /= PW;
-    const int ph = t % PH;
-    const int b = t / PH;
-    const int j0 = max(0, c - lo), j1 = min(C - 1, c + hi);
-    float best = -INFINITY;
-    int bi = 0;
-    bool done = false;
-    for (int r = 0; r < pk && !done; ++r) {
-      const int h = ph * ps + r;
-      for (int q = 0; q < pk; ++q) {
-        const int w = pw * ps + q;
-        const T* px = a + ((b * H + h) * W + w) * C;
-        float sum = 0.f;
-        for (int j = j0; j <= j1; ++j) {
-          const float v = to_f<T>(px[j]);
-          sum += v * v;
-        }
-        const float v = to_f<T>(px[c]) * pow_neg(kk + alpha * sum, beta);
-        if (v > best || isnan(v)) {
-          best = v;
-          bi = r * pk + q;
-          if (isnan(v)) {
-            done = true;
-            break;
-          }
-        }
-      }
-    }
-    y[i] = from_f<T>(best);
-    widx[i] = static_cast<uint8_t>(bi);
+__device__ __forceinline__ void load_vec(const T* p, float* out);
+template <>
+__device__ __forceinline__ void load_vec<bf16>(const bf16* p, float* out) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const bf16* h = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) out[j] = __bfloat162float(h[j]);
+}
+template <>
+__device__ __forceinline__ void load_vec<float>(const float* p, float* out) {
+  const float4 u = *reinterpret_cast<const float4*>(p);
+  out[0] = u.x;
+  out[1] = u.y;
+  out[2] = u.z;
+  out[3] = u.w;
+}
+template <class T>
+__device__ __forceinline__ void store_vec(T* p, const float* v);
+template <>
+__device__ __forceinline__ void store_vec<bf16>(bf16* p, const float* v) {
+  __align__(16) bf16 h[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) h[j] = __float2bfloat16_rn(v[j]);
+  *reinterpret_cast<uint4*>(p) = *reinterpret_cast<const uint4*>(h);
+}
+template <>
+__device__ __forceinline__ void store_vec<float>(float* p, const float* v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// a[-LH .. V+LH) of one pixel around channel c0 (zeros outside [0, C)).
+template <class T, int V>
+__device__ __forceinline__ void load_window(const T* px, int c0, int C, float* w) {
+  load_vec<T>(px + c0, w + LH);
+#pragma unroll
+  for (int j = 0; j < LH; ++j) {
+    const int cl = c0 - LH + j, cr = c0 + V + j;
+    w[j] = cl >= 0 ? to_f<T>(px[cl]) : 0.f;
+    w[LH + V + j] = cr < C ? to_f<T>(px[cr]) : 0.f;
   }
 }
 
-// Block = PT consecutive pixels x all C channels, staged in shared memory.
+// LRN of channels c0..c0+V-1 from the window w (sum over [c-lo, c+hi]).
+template <int V>
+__device__ __forceinline__ void lrn_vals(const float* w, int lo, int hi, float alpha, float beta,
+                                         float kk, float* out) {
+  float sq[V + 2 * LH];
+#pragma unroll
+  for (int j = 0; j < V + 2 * LH; ++j) sq[j] = w[j] * w[j];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    float sum = 0.f;
+#pragma unroll
+    for (int d = -LH; d <= LH; ++d)
+      if (d >= -lo && d <= hi) sum += sq[LH + i + d];
+    out[i] = w[LH + i] * pow_neg(kk + alpha * sum, beta);
+  }
+}
+
+// Fused LRN + max-pool forward: thread = (pooled pixel, V-channel group).
+template <class T>
+__global__ void __launch_bounds__(256) lrn_pool_fwd_kernel(const T* __restrict__ a, T* __restrict__ y,
+                                                           uint8_t* __restrict__ widx, int H, int W, int C,
+                                                           int lo, int hi, float alpha, float beta, float kk,
+                                                           int pk, int ps, int PH, int PW, int n) {
+  constexpr int V = 16 / sizeof(T);
+  const int groups = C / V;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int g = i % groups, op = i / groups;
+    const int pw = op % PW, t = op / PW, ph = t % PH, b = t / PH;
+    const int c0 = g * V;
+    float best[V];
+    int bi[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      best[j] = -INFINITY;
+      bi[j] = 0;
+    }
+    for (int r = 0; r < pk; ++r) {
+      const T* row = a + (static_cast<long long>(b * H + ph * ps + r) * W + pw * ps) * C;
+      for (int q = 0; q < pk; ++q) {
+        float w[V + 2 * LH], v[V];
+        load_window<T, V>(row + q * C, c0, C, w);
+        lrn_vals<V>(w, lo, hi, alpha, beta, kk, v);
+        const int pos = r * pk + q;
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          if ((v[j] > best[j] || isnan(v[j])) && !isnan(best[j])) {
+            best[j] = v[j];
+            bi[j] = pos;
+          }
+      }
+    }
+    const long long o = static_cast<long long>(op) * C + c0;
+    store_vec<T>(y + o, best);
+    uint32_t lo4 = 0, hi4 = 0;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      if (j < 4) lo4 |= static_cast<uint32_t>(bi[j]) << (8 * j);
+      else hi4 |= static_cast<uint32_t>(bi[j]) << (8 * (j - 4));
+    }
+    if (V == 8) {
+      *reinterpret_cast<uint2*>(widx + o) = make_uint2(lo4, hi4);
+    } else {
+      *reinterpret_cast<uint32_t*>(widx + o) = lo4;
+    }
+  }
+}
+
+// Fused backward: thread = (conv-output pixel, V-channel group).
+//   gb_i = pool backward (sum of gy over windows whose argmax is this pixel)
+//   ga_c = gb_c d_c^-beta - 2 alpha beta a_c sum_{i: c in win(i)} gb_i a_i d_i^(-beta-1)
 template <class TA>
-__global__ void lrn_pool_bwd_kernel(const float* __restrict__ gy, const uint8_t* __restrict__ widx,
-                                    const TA* __restrict__ a, TA* __restrict__ dz, int H, int W,
-                                    int C, int lo, int hi, float alpha, float beta, float kk, int pk,
-                                    int ps, int PH, int PW, int relu_mask, int npix, int PT) {
-  extern __shared__ float sm[];
-  float* sa = sm;                 // a
-  float* sg = sa + PT * C;        // gb (grad wrt LRN output)
-  float* st = sg + PT * C;        // t = gb * a * d^(-beta-1)
-  float* sd = st + PT * C;        // d^(-beta)
-  const int p0 = blockIdx.x * PT;
-  const int np = min(PT, npix - p0);
-  const int tot = np * C;
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-    const int pl = e / C, c = e - pl * C;
-    const int p = p0 + pl;
-    const int w = p % W;
-    const int t = p / W;
-    const int h = t % H;
-    const int b = t / H;
-    sa[e] = to_f<TA>(a[p0 * C + e]);
+__global__ void __launch_bounds__(256) lrn_pool_bwd_kernel(
+    const float* __restrict__ gy, const uint8_t* __restrict__ widx, const TA* __restrict__ a,
+    TA* __restrict__ dz, int H, int W, int C, int lo, int hi, float alpha, float beta, float kk, int pk,
+    int ps, int PH, int PW, int relu_mask, int n) {
+  constexpr int V = 16 / sizeof(TA);
+  constexpr int NA = V + 4 * LH;  // a over [c0-2LH, c0+V+2LH)
+  constexpr int NG = V + 2 * LH;  // gb, d, t over [c0-LH, c0+V+LH)
+  const int groups = C / V;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int g = i % groups, p = i / groups;
+    const int w = p % W, t = p / W, h = t % H, b = t / H;
+    const int c0 = g * V;
+    const TA* px = a + static_cast<long long>(p) * C;
+    float av[NA];
+    load_vec<TA>(px + c0, av + 2 * LH);
+#pragma unroll
+    for (int j = 0; j < 2 * LH; ++j) {
+      const int cl = c0 - 2 * LH + j, cr = c0 + V + j;
+      av[j] = cl >= 0 ? to_f<TA>(px[cl]) : 0.f;
+      av[2 * LH + V + j] = cr < C ? to_f<TA>(px[cr]) : 0.f;
+    }
+    // pool backward for channels [c0-LH, c0+V+LH)
+    float gb[NG];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) gb[j] = 0.f;
     const int oh0 = h - pk + 1 <= 0 ? 0 : (h - pk + ps) / ps;
     const int oh1 = min(PH - 1, h / ps);
     const int ow0 = w - pk + 1 <= 0 ? 0 : (w - pk + ps) / ps;
     const int ow1 = min(PW - 1, w / ps);
-    float g = 0.f;
     for (int oh = oh0; oh <= oh1; ++oh)
       for (int ow = ow0; ow <= ow1; ++ow) {
-        const int o = ((b * PH + oh) * PW + ow) * C + c;
-        if (widx[o] == (h - oh * ps) * pk + (w - ow * ps)) g += gy[o];
+        const int me = (h - oh * ps) * pk + (w - ow * ps);
+        const long long o = (static_cast<long long>(b * PH + oh) * PW + ow) * C;
+#pragma unroll
+        for (int j = 0; j < NG; ++j) {
+          const int c = c0 - LH + j;
+          if (c >= 0 && c < C && (j >= LH - hi && j < LH + V + lo) && widx[o + c] == me) gb[j] += gy[o + c];
+        }
       }
-    sg[e] = g;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-    const int pl = e / C, c = e - pl * C;
-    const float* row = sa + pl * C;
-    const int j0 = max(0, c - lo), j1 = min(C - 1, c + hi);
-    float sum = 0.f;
-    for (int j = j0; j <= j1; ++j) sum += row[j] * row[j];
-    const float d = kk + alpha * sum;
-    const float dn = pow_neg(d, beta);
-    sd[e] = dn;
-    st[e] = sg[e] * sa[e] * __fdividef(dn, d);
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-    const int pl = e / C, c = e - pl * C;
-    const int i0 = max(0, c - hi), i1 = min(C - 1, c + lo);
-    float acc = 0.f;
-    for (int j = i0; j <= i1; ++j) acc += st[pl * C + j];
-    const float av = sa[e];
-    float g = sg[e] * sd[e] - 2.f * alpha * beta * av * acc;
-    if (relu_mask && !(av > 0.f)) g = 0.f;
-    dz[p0 * C + e] = from_f<TA>(g);
+    // d_i, t_i for i in [c0-LH, c0+V+LH)
+    float dn[NG], tt[NG];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+      float sum = 0.f;
+#pragma unroll
+      for (int d = -LH; d <= LH; ++d)
+        if (d >= -lo && d <= hi) sum += av[LH + j + d] * av[LH + j + d];
+      const float dd = kk + alpha * sum;
+      dn[j] = pow_neg(dd, beta);
+      tt[j] = gb[j] * av[LH + j] * __fdividef(dn[j], dd);
+    }
+    float out[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      float acc = 0.f;
+#pragma unroll
+      for (int d = -LH; d <= LH; ++d)
+        if (d >= -hi && d <= lo) acc += tt[LH + k + d];
+      const float ai = av[2 * LH + k];
+      float gval = gb[LH + k] * dn[LH + k] - 2.f * alpha * beta * ai * acc;
+      if (relu_mask && !(ai > 0.f)) gval = 0.f;
+      out[k] = gval;
+    }
+    store_vec<TA>(dz + static_cast<long long>(p) * C + c0, out);
   }
 }
 
@@ -636,22 +753,39 @@ template <class T>
 void launch_im2col_nchw(const float* x, T* col, int B, int C, int H, int W, int R, int S, int stride,
                         int pad, int OH, int OW, long long ldk, cudaStream_t st) {
   constexpr int V = 16 / sizeof(T);
-  if (ldk % V != 0) throw std::runtime_error("im2col_nchw: ldk must be a multiple of 16 bytes");
-  const long long P = static_cast<long long>(B) * OH * OW;
-  const long long n = P * (ldk / V);
-  if (n >= (1LL << 31)) throw std::runtime_error("im2col_nchw: too large for 32-bit indexing");
-  im2col_nchw_kernel<T><<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(x, col, C, H, W, S, stride, pad, OH, OW,
-                                                                    static_cast<int>(ldk), R * S * C,
-                                                                    static_cast<int>(P));
+  const int Wp = W + 2 * pad + S;
+  const size_t smem = static_cast<size_t>(C) * R * Wp * sizeof(float) + static_cast<size_t>(ldk) * sizeof(int);
+  if (ldk % V != 0 || smem > 200 * 1024) throw std::runtime_error("im2col_nchw: unsupported geometry");
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    HP_CUDA(cudaFuncSetAttribute(im2col_nchw_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    attr = smem;
+  }
+  im2col_nchw_kernel<T><<<B * OH, 256, smem, st>>>(x, col, C, H, W, R, S, stride, pad, OH, OW,
+                                                   static_cast<int>(ldk), R * S * C);
+}
+
+template <class T>
+void launch_im2col_t_nchw(const float* x, T* colT, int B, int C, int H, int W, int R, int S,
+                          int stride, int pad, int OH, int OW, long long ldp, cudaStream_t st) {
+  if (OW > 1024 || R >= (1 << 15) || S >= (1 << 16)) throw std::runtime_error("im2col_t: unsupported geometry");
+  const int bx = ((OW + 31) / 32) * 32;
+  const int by = std::max(1, 256 / bx);
+  const int K = R * S * C;
+  im2col_t_nchw_kernel<T><<<B * OH, dim3(bx, by), static_cast<size_t>(K) * 2 * sizeof(int), st>>>(
+      x, colT, C, H, W, R, S, stride, pad, OH, OW, ldp, K);
 }
 
 template <class T>
 void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, int C, int n,
                          float alpha, float beta, float kk, int pk, int ps, int PH, int PW,
                          cudaStream_t st) {
-  const long long total = static_cast<long long>(B) * PH * PW * C;
-  if (static_cast<long long>(B) * H * W * C >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
-  lrn_pool_fwd_kernel<T><<<grid_for(total, 256, 148 * 32), 256, 0, st>>>(
+  constexpr int V = 16 / sizeof(T);
+  if (C % V != 0 || n > 2 * LH + 1) throw std::runtime_error("lrn_pool: C must be a multiple of 16 bytes, size <= 9");
+  const long long total = static_cast<long long>(B) * PH * PW * (C / V);
+  if (static_cast<long long>(B) * H * W >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
+  lrn_pool_fwd_kernel<T><<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(
       a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, static_cast<int>(total));
 }
 
@@ -659,14 +793,13 @@ template <class TA>
 void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* dz, int B, int H,
                          int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
                          int PH, int PW, int relu_mask, cudaStream_t st) {
-  const long long npix = static_cast<long long>(B) * H * W;
-  const int PT = std::max(1, 2048 / C);
-  const size_t smem = static_cast<size_t>(PT) * C * 4 * sizeof(float);
-  const long long blocks = (npix + PT - 1) / PT;
-  if (npix * C >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
-  lrn_pool_bwd_kernel<TA><<<static_cast<unsigned>(blocks), 256, smem, st>>>(
+  constexpr int V = 16 / sizeof(TA);
+  if (C % V != 0 || n > 2 * LH + 1) throw std::runtime_error("lrn_pool: C must be a multiple of 16 bytes, size <= 9");
+  const long long total = static_cast<long long>(B) * H * W * (C / V);
+  if (total >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
+  lrn_pool_bwd_kernel<TA><<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(
       gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, relu_mask,
-      static_cast<int>(npix), PT);
+      static_cast<int>(total));
 }
 
 template <class T>
@@ -692,6 +825,8 @@ void launch_rotate_weights(const float* w, long long ldk, T* wrot, int F, int C,
 }
 
 #define INST_NEW(T)                                                                             \
+  template void launch_im2col_t_nchw<T>(const float*, T*, int, int, int, int, int, int, int, int, int, \
+                                        int, long long, cudaStream_t);                                     \
   template void launch_im2col_nchw<T>(const float*, T*, int, int, int, int, int, int, int, int, int, \
                                       int, long long, cudaStream_t);                            \
   template void launch_lrn_pool_fwd<T>(const T*, T*, uint8_t*, int, int, int, int, int, float,   \

@@ -110,6 +110,13 @@ template <class T>
 void launch_im2col_nchw(const float* x, T* col, int B, int C, int H, int W, int R, int S,
                         int stride, int pad, int OH, int OW, long long ldk, cudaStream_t st);
 
+// Transposed im2col straight from the NCHW fp32 batch: colT [K][P] (pixels
+// contiguous, row stride ldp >= P), k = (r*S+s)*C + c. Consumed as an MN-major A
+// (fprop) / K-major B (wgrad) operand.
+template <class T>
+void launch_im2col_t_nchw(const float* x, T* colT, int B, int C, int H, int W, int R, int S,
+                          int stride, int pad, int OH, int OW, long long ldp, cudaStream_t st);
+
 // Fused cross-channel LRN + overlapping max-pool forward (conv1/conv2 of
 // AlexNet): y = maxpool(lrn(a)); the LRN output and its scale are never
 // written (recomputed in backward). widx = argmax window offset r*k+q.
