@@ -215,6 +215,11 @@ HP_API double hp_cluster_last_gemm_flops(const hp_cluster* c);
 /* Bracket every GEMM with CUDA events on the launching stream (adds event
  * records; off for timed runs). */
 HP_API int hp_cluster_set_profile(hp_cluster* c, int on);
+/* Replay each step as a captured CUDA graph (default on). A graph is keyed by
+ * the step's input pointers, memory kind and scalars; it is captured the second
+ * time a key is seen (the first runs eagerly) and replayed afterwards. Host
+ * inputs are graphed only when they are pinned. */
+HP_API int hp_cluster_set_graphs(hp_cluster* c, int on);
 /* Per-GEMM record of the last profiled step: tag ("conv_fwd", ...), layer,
  * FLOPs and event-timed ms. Returns the count. */
 typedef struct hp_gemm_prof {
@@ -260,6 +265,9 @@ typedef struct hp_gemm_desc {
 /* D = A * B^T on tcgen05 (replaces matmul/_tn/_nt, tensor.cpp:254-305). */
 HP_API int hp_kernel_gemm(const hp_gemm_desc* d, void* stream);
 HP_API int hp_kernel_gemm_splits(const hp_gemm_desc* d);
+/* Dev hook for microbenchmarks: force later auto-configured GEMM plans to
+ * (cta2, bn); (-1, 0) restores the automatic tile choice. */
+HP_API void hp_debug_gemm_force(int cta2, int bn);
 
 /* Implicit-GEMM convolution on tcgen05 with TMA im2col operand loads (no
  * im2col buffer); NHWC activations in the operand type (bf16 for

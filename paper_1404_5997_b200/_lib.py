@@ -129,6 +129,7 @@ def _load() -> C.CDLL:
         "hp_gaussian_fill_f32": ([C.c_uint64, C.c_double, C.POINTER(C.c_float), C.c_int64], None),
         "hp_kernel_gemm": ([C.POINTER(HpGemmDesc), P], C.c_int),
         "hp_kernel_gemm_splits": ([C.POINTER(HpGemmDesc)], C.c_int),
+        "hp_debug_gemm_force": ([C.c_int, C.c_int], None),
         "hp_kernel_conv_fprop": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int,
                                   C.c_int, C.c_int, C.c_int, P, P], C.c_int),
         "hp_kernel_conv_wgrad": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int,
@@ -159,6 +160,7 @@ def _load() -> C.CDLL:
         "hp_cluster_last_step_io": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], None),
         "hp_cluster_last_gemm_flops": ([P], C.c_double),
         "hp_cluster_set_profile": ([P, C.c_int], C.c_int),
+        "hp_cluster_set_graphs": ([P, C.c_int], C.c_int),
         "hp_cluster_gemm_profile": ([P, C.POINTER(HpGemmProf), C.c_int], C.c_int),
     }
     for name, (args, res) in list(sigs.items()) + list(optional.items()):

@@ -370,6 +370,10 @@ class Cluster:
     def last_gemm_flops(self) -> float:
         return lib.hp_cluster_last_gemm_flops(self._h)
 
+    def set_graphs(self, on: bool) -> None:
+        """Replay steps as captured CUDA graphs (default on; see hp_cluster_set_graphs)."""
+        _check(lib.hp_cluster_set_graphs(self._h, int(bool(on))))
+
     def set_profile(self, on: bool) -> None:
         _check(lib.hp_cluster_set_profile(self._h, int(bool(on))))
 

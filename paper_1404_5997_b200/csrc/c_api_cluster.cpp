@@ -137,6 +137,10 @@ HP_API void hp_cluster_last_step_io(const hp_cluster* c, int64_t* h2d, int64_t* 
 
 HP_API double hp_cluster_last_gemm_flops(const hp_cluster* c) { return c->impl->last_gemm_flops; }
 
+HP_API int hp_cluster_set_graphs(hp_cluster* c, int on) {
+  return guarded_c([&] { c->impl->use_graphs = on != 0; });
+}
+
 HP_API int hp_cluster_set_profile(hp_cluster* c, int on) {
   return guarded_c([&] { c->impl->profile = on != 0; });
 }

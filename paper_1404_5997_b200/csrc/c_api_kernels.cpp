@@ -77,6 +77,8 @@ static GemmPlan plan_from_desc(const hp_gemm_desc* d) {
   return gemm_plan(d->math, a, b, d->M, d->N, d->K, e, d->splits, d->ws, d->bn, d->cta2);
 }
 
+HP_API void hp_debug_gemm_force(int cta2, int bn) { gemm_force_config(cta2, bn); }
+
 HP_API int hp_kernel_gemm_splits(const hp_gemm_desc* d) {
   int splits = 1;
   const int rc = guarded([&] {

@@ -21,7 +21,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <string>
+#include <tuple>
 
 #include "cluster.hpp"
 #include "comm.hpp"
@@ -317,6 +319,25 @@ class ClusterImpl final : public ClusterBase {
   void sgd_fc(double lr, float gscale, bool has_gscale, const hp_hyper& hp);
   void sgd_conv(double lr, const hp_hyper& hp);
   void account(int num_sub, hp_step_metrics* out);
+  void enqueue(const float* const* batches, const float* const* targets, int mem_kind,
+               const hp_hyper& hp, double lr);
+  struct GraphKey {
+    std::vector<const void*> ptrs;
+    int mem = 0;
+    std::array<double, 4> scal{};
+    bool operator<(const GraphKey& o) const {
+      return std::tie(ptrs, mem, scal) < std::tie(o.ptrs, o.mem, o.scal);
+    }
+  };
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;
+    double flops = 0.0;
+    int64_t h2d = 0, d2h = 0;
+  };
+  std::map<GraphKey, GraphEntry> graphs_;
+  double* host_parts_ = nullptr;  // pinned: [nlocal][num_sub * xblocks]
+  int* host_bad_ = nullptr;       // pinned: [nlocal]
   void gemm(const GemmPlan& p, const char* tag, int layer);
   void collect_profile();
   // param layout helpers
@@ -474,6 +495,8 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     w.colsum_ws = arena_.make<float>(static_cast<long long>(colsum_ws));
   }
   comm_->reserve(comm_scratch * sizeof(float));
+  HP_CUDA(cudaMallocHost(&host_parts_, sizeof(double) * nl * num_sub_ * xblocks_));
+  HP_CUDA(cudaMallocHost(&host_bad_, sizeof(int) * nl));
   // Plans first with a null workspace to size it, then for real.
   for (auto& w : w_) build_plans(w);
   ws_ = ws_floats_ > 0 ? arena_.make<float>(static_cast<long long>(ws_floats_)) : nullptr;
@@ -487,6 +510,10 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
 template <class TA>
 ClusterImpl<TA>::~ClusterImpl() {
   if (st_) cudaStreamSynchronize(st_);
+  for (auto& kv : graphs_)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  if (host_parts_) cudaFreeHost(host_parts_);
+  if (host_bad_) cudaFreeHost(host_bad_);
   comm_.reset();
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
@@ -536,15 +563,14 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
   };
   auto plan = [&](const GemmOperand& a, const GemmOperand& b, long long M, long long N, long long K,
                   const Epi& e) {
-    const int sp = gemm_choose_splits(math_, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K));
-    if (sp > 1) ws_floats_ = std::max(ws_floats_, static_cast<size_t>(sp * M * N));
-    if (ws_ == nullptr && sp > 1) {
-      // sizing pass: build a throwaway plan against a dummy workspace
-      return gemm_plan(math_, a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e,
-                       sp, reinterpret_cast<float*>(16), 0);
-    }
-    return gemm_plan(math_, a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e, sp,
-                     ws_, 0);
+    // The plan picks its own tile and split-K; the first (sizing) pass runs
+    // against a placeholder workspace and records the largest need.
+    float* ws = ws_ != nullptr ? ws_ : reinterpret_cast<float*>(256);
+    GemmPlan pl = gemm_plan(math_, a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e, 0,
+                            ws, 0);
+    if (pl.splits > 1) ws_floats_ = std::max(ws_floats_, static_cast<size_t>(pl.splits * M * N));
+    else pl.args.ws = ws_;
+    return pl;
   };
   w.conv_fwd.clear();
   w.conv_wgrad.clear();
@@ -1034,32 +1060,14 @@ void ClusterImpl<TA>::sgd_conv(double lr, const hp_hyper& hp) {
 }
 
 // ------------------------------------------------------------------ step
+// All device work of one step, stream-ordered on st_ (eager or captured).
 template <class TA>
-void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* targets, int mem_kind,
-                               const hp_hyper& hp, double lr, hp_step_metrics* out) {
+void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* targets, int mem_kind,
+                              const hp_hyper& hp, double lr) {
   const int nl = comm_->nlocal();
-  if (!batches || !targets) usage_error("run_step: expected " + num(nl) + " batches and targets");
-  for (int i = 0; i < nl; ++i)
-    if (!batches[i] || !targets[i])
-      usage_error("run_step: expected " + num(nl) + " batches and targets, got a null entry");
-  if (mem_kind == HP_MEM_HOST) {
-    // logistic_xent's DomainError (tensor.cpp:600-603), checked before any state change
-    for (int i = 0; i < nl; ++i)
-      for (long long e = 0; e < b_ * L_; ++e) {
-        const double t = targets[i][e];
-        if (t < 0.0 || t > 1.0)
-          domain_error("logistic_xent: target " + std::to_string(t) + " outside [0,1] at flat index " +
-                       num(e % (b_ * L_)));
-      }
-  }
   const double fc_lr = variable_ ? (hp.has_fc_partial_lr ? hp.fc_partial_lr : lr) : lr;
   const auto& in = g_.input;
   const long long xin = b_ * in[0] * in[1] * in[2];
-  launches_ = 0;
-  gemm_flops_ = 0.0;
-  prof_used_ = 0;
-  io_h2d = io_d2h = 0;
-  HP_CUDA(cudaEventRecord(ev0_, st_));
   for (int i = 0; i < nl; ++i) {
     Worker<TA>& w = w_[i];
     const float* src = batches[i];
@@ -1092,7 +1100,6 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
     for (int i = 0; i < nl; ++i) bufs[i] = w_[i].cgr;
     comm_->allreduce_f32(bufs, conv_total_, st_);
     launches_ += 1;
-    if (skip_sync_broadcast) usage_error("set_skip_sync_broadcast: not supported on the B200 path yet");
   }
   if (!variable_) {
     const bool scale = num_sub_ > 1;
@@ -1100,23 +1107,111 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
   }
   sgd_conv(lr, hp);
   for (auto& w : w_) rotate_all(w);
-  HP_CUDA(cudaEventRecord(ev1_, st_));
-
-  // loss = sum_j loss_j * n_j / (K*b) (cluster.cpp:555-556, 710)
-  std::vector<double> parts(static_cast<size_t>(num_sub_) * xblocks_, 0.0);
-  std::vector<int> bad(nl, 0);
+  // loss partials (+ the domain-error flag) to pinned host memory
+  const size_t np = static_cast<size_t>(num_sub_) * xblocks_;
   if (nl == 1 && K_ > 1) {
     std::vector<double*> b{w_[0].loss_parts};
-    comm_->allreduce_f64(b, parts.size(), st_);
+    comm_->allreduce_f64(b, np, st_);
   }
-  std::vector<double> tmp(parts.size());
   for (int i = 0; i < nl; ++i) {
-    HP_CUDA(cudaMemcpyAsync(tmp.data(), w_[i].loss_parts, tmp.size() * sizeof(double),
+    HP_CUDA(cudaMemcpyAsync(host_parts_ + i * np, w_[i].loss_parts, np * sizeof(double),
                             cudaMemcpyDeviceToHost, st_));
-    HP_CUDA(cudaMemcpyAsync(&bad[i], w_[i].bad, sizeof(int), cudaMemcpyDeviceToHost, st_));
-    io_d2h += static_cast<int64_t>(tmp.size() * sizeof(double) + sizeof(int));
-    HP_CUDA(cudaStreamSynchronize(st_));
-    for (size_t e = 0; e < parts.size(); ++e) parts[e] += tmp[e];
+    HP_CUDA(cudaMemcpyAsync(host_bad_ + i, w_[i].bad, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    io_d2h += static_cast<int64_t>(np * sizeof(double) + sizeof(int));
+  }
+}
+
+template <class TA>
+void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* targets, int mem_kind,
+                               const hp_hyper& hp, double lr, hp_step_metrics* out) {
+  const int nl = comm_->nlocal();
+  if (!batches || !targets) usage_error("run_step: expected " + num(nl) + " batches and targets");
+  for (int i = 0; i < nl; ++i)
+    if (!batches[i] || !targets[i])
+      usage_error("run_step: expected " + num(nl) + " batches and targets, got a null entry");
+  if (mem_kind == HP_MEM_HOST) {
+    // logistic_xent's DomainError (tensor.cpp:600-603), checked before any state change
+    for (int i = 0; i < nl; ++i)
+      for (long long e = 0; e < b_ * L_; ++e) {
+        const double t = targets[i][e];
+        if (t < 0.0 || t > 1.0)
+          domain_error("logistic_xent: target " + std::to_string(t) + " outside [0,1] at flat index " +
+                       num(e % (b_ * L_)));
+      }
+  }
+  if (skip_sync_broadcast && K_ > 1)
+    usage_error("set_skip_sync_broadcast: not supported on the B200 path yet");
+
+  // CUDA graph of the whole step, keyed by everything baked into it (input
+  // pointers, memory kind, scalars). Captured on the second occurrence of a
+  // key (the first runs eagerly and warms every kernel), replayed after.
+  bool pinned = mem_kind == HP_MEM_DEVICE;
+  if (!pinned) {
+    pinned = true;
+    for (int i = 0; i < nl && pinned; ++i)
+      for (const float* p : {batches[i], targets[i]}) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess || a.type != cudaMemoryTypeHost) pinned = false;
+      }
+    cudaGetLastError();
+  }
+  GraphKey key;
+  for (int i = 0; i < nl; ++i) {
+    key.ptrs.push_back(batches[i]);
+    key.ptrs.push_back(targets[i]);
+  }
+  key.mem = mem_kind;
+  key.scal = {lr, hp.momentum, hp.weight_decay, hp.has_fc_partial_lr ? hp.fc_partial_lr : -1.0};
+  const bool graphable = use_graphs && !profile && pinned;
+  GraphEntry* ge = nullptr;
+  if (graphable) {
+    auto it = graphs_.find(key);
+    if (it != graphs_.end()) ge = &it->second;
+  }
+  launches_ = 0;
+  gemm_flops_ = 0.0;
+  prof_used_ = 0;
+  io_h2d = io_d2h = 0;
+  if (ge && ge->exec) {
+    HP_CUDA(cudaEventRecord(ev0_, st_));
+    HP_CUDA(cudaGraphLaunch(ge->exec, st_));
+    HP_CUDA(cudaEventRecord(ev1_, st_));
+    launches_ = ge->launches;
+    gemm_flops_ = ge->flops;
+    io_h2d = ge->h2d;
+    io_d2h = ge->d2h;
+  } else if (ge) {
+    // second occurrence: capture
+    if (graphs_.size() > 16) {
+      for (auto& kv : graphs_)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      graphs_.clear();
+      ge = &graphs_[key];
+    }
+    cudaGraph_t g = nullptr;
+    HP_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue(batches, targets, mem_kind, hp, lr);
+    } catch (...) {
+      cudaStreamEndCapture(st_, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    HP_CUDA(cudaStreamEndCapture(st_, &g));
+    HP_CUDA(cudaGraphInstantiate(&ge->exec, g, 0));
+    HP_CUDA(cudaGraphDestroy(g));
+    ge->launches = launches_;
+    ge->flops = gemm_flops_;
+    ge->h2d = io_h2d;
+    ge->d2h = io_d2h;
+    HP_CUDA(cudaEventRecord(ev0_, st_));
+    HP_CUDA(cudaGraphLaunch(ge->exec, st_));
+    HP_CUDA(cudaEventRecord(ev1_, st_));
+  } else {
+    HP_CUDA(cudaEventRecord(ev0_, st_));
+    enqueue(batches, targets, mem_kind, hp, lr);
+    HP_CUDA(cudaEventRecord(ev1_, st_));
+    if (graphable) graphs_[key];  // remember: capture on the next occurrence
   }
   HP_CUDA(cudaStreamSynchronize(st_));
   float ms = 0.f;
@@ -1125,14 +1220,19 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
   last_launches = launches_;
   last_gemm_flops = gemm_flops_;
   if (profile) collect_profile();
-  for (int i = 0; i < nl; ++i)
-    if (bad[i]) domain_error("logistic_xent: target outside [0,1]");
+  const size_t np = static_cast<size_t>(num_sub_) * xblocks_;
+  std::vector<double> parts(np, 0.0);
+  for (int i = 0; i < nl; ++i) {
+    if (host_bad_[i]) domain_error("logistic_xent: target outside [0,1]");
+    for (size_t e = 0; e < np; ++e) parts[e] += host_parts_[i * np + e];
+  }
+  // loss = sum_j loss_j * n_j / (K*b) (cluster.cpp:555-556, 710)
   double loss_weighted = 0.0;
   const double inv_n = 1.0 / static_cast<double>(n_);
   for (int j = 0; j < num_sub_; ++j) {
-    double s = 0.0;
-    for (int k = 0; k < xblocks_; ++k) s += parts[static_cast<size_t>(j) * xblocks_ + k];
-    loss_weighted += (s * inv_n) * static_cast<double>(n_);
+    double sj = 0.0;
+    for (int k = 0; k < xblocks_; ++k) sj += parts[static_cast<size_t>(j) * xblocks_ + k];
+    loss_weighted += (sj * inv_n) * static_cast<double>(n_);
   }
   std::memset(out, 0, sizeof *out);
   out->loss = loss_weighted / static_cast<double>(K_ * b_);

@@ -72,6 +72,7 @@ class ClusterBase {
     float ms;
   };
   bool profile = false;            // bracket every GEMM with CUDA events
+  bool use_graphs = true;          // replay the step as a captured CUDA graph
   std::vector<GemmProf> prof;      // last step, launch order
   double prof_gemm_ms = 0.0;
   double last_gemm_flops = 0.0;    // algorithmic GEMM FLOPs of the last step

@@ -799,6 +799,7 @@ void launch_math(const GemmPlan& p, cudaStream_t s) {
     if constexpr (MATH != kMathF32x3) {
       switch (p.bn) {
         case 128: launch_inst2<128, MATH>(p, s); return;
+        case 192: launch_inst2<192, MATH>(p, s); return;
         case 256: launch_inst2<256, MATH>(p, s); return;
         default: break;
       }
@@ -861,7 +862,49 @@ int gemm_choose_splits(int math, int M, int N, int K, int bn) {
 }
 
 static bool g_cta2_default = true;
+static int g_force_cta2 = -1, g_force_bn = 0;
 void gemm_set_cta2_default(bool on) { g_cta2_default = on; }
+void gemm_force_config(int cta2, int bn) {
+  g_force_cta2 = cta2;
+  g_force_bn = bn;
+}
+
+// Tile choice from measured per-SM efficiency of each kernel shape (bf16,
+// 8192^3: pair/256 1403 TF/s, single/256 1235, single/192 1047, pair/128 805,
+// single/128 852) times N-tile fill and wave quantisation.
+struct TileChoice {
+  bool cta2;
+  int bn;
+};
+static TileChoice choose_tile(int math, const GemmOperand& b, int M, int N) {
+  struct Cand {
+    bool cta2;
+    int bn;
+    double base;
+  };
+  const Cand cands[] = {{true, 256, 1.0}, {true, 192, 0.93}, {false, 256, 0.88}, {false, 192, 0.80},
+                        {true, 128, 0.60}, {false, 128, 0.62}, {false, 64, 0.40}};
+  TileChoice best{false, 128};
+  double best_score = -1.0;
+  for (const Cand& c : cands) {
+    if (c.cta2 && (math == kMathF32x3 || !g_cta2_default || M < 256)) continue;
+    if (c.cta2 && b.mn_major && (c.bn / 2) % (128 / (math == kMathBF16 ? 2 : 4)) != 0) continue;
+    const int mt = c.cta2 ? cdiv(M, 2 * kBM) : cdiv(M, kBM);
+    const int nt = cdiv(N, c.bn);
+    const double nfill = static_cast<double>(N) / (static_cast<double>(nt) * c.bn);
+    const double mfill = static_cast<double>(M) / (static_cast<double>(mt) * (c.cta2 ? 2 * kBM : kBM));
+    const int units = mt * nt;                  // tiles (pairs count as one on two SMs)
+    const int slots = c.cta2 ? 74 : 148;
+    const int waves = cdiv(units, slots);
+    const double wave = units >= slots ? static_cast<double>(units) / (waves * slots) : 1.0;
+    const double score = c.base * nfill * mfill * wave;
+    if (score > best_score + 1e-9) {
+      best_score = score;
+      best = {c.cta2, c.bn};
+    }
+  }
+  return best;
+}
 
 GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
                    const Epi& epi, int splits, float* ws, int bn, int cta2) {
@@ -871,17 +914,21 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   const int es = math == kMathBF16 ? 2 : 4;
   const int BK = 128 / es;
   const int kt = cdiv(K, BK);
-  const bool use2 = math != kMathF32x3 && (cta2 == 1 || (cta2 == -1 && g_cta2_default && M >= 256));
+  if (cta2 == -1 && g_force_cta2 >= 0) cta2 = g_force_cta2;
+  if (bn <= 0 && g_force_bn > 0) bn = g_force_bn;
   if (cta2 == 1 && math == kMathF32x3) throw std::runtime_error("gemm: 3xTF32 has no 2-CTA kernel");
+  bool use2;
+  if (cta2 == -1 && bn <= 0) {
+    const TileChoice tc = choose_tile(math, b, M, N);
+    use2 = tc.cta2;
+    bn = tc.bn;
+  } else {
+    use2 = math != kMathF32x3 && (cta2 == 1 || (cta2 == -1 && g_cta2_default && M >= 256));
+  }
+  if (use2 && b.mn_major && bn == 192) bn = 256;  // MN-major B halves must be whole 128-byte atoms
   p.cta2 = use2;
   if (use2) {
-    if (bn == 128 || bn == 256) {
-      p.bn = bn;
-    } else {
-      // wide tiles unless they waste more than ~20% of the N extent
-      const double w256 = static_cast<double>(N) / (cdiv(N, 256) * 256.0);
-      p.bn = w256 >= 0.8 ? 256 : 128;
-    }
+    p.bn = (bn == 128 || bn == 192 || bn == 256) ? bn : 256;
     if (splits <= 0) {
       const int tiles2 = cdiv(M, 2 * kBM) * cdiv(N, p.bn);
       splits = (tiles2 >= 60 || kt < 4) ? 1 : std::max(1, std::min({cdiv(74, tiles2), kt / 2, 64}));

@@ -95,6 +95,8 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
                    const Epi& epi, int splits, float* ws, int bn = 0, int cta2 = -1);
 // cta2: -1 auto (pairs for M >= 256 outside 3xTF32), 0 never, 1 force.
 void gemm_set_cta2_default(bool on);
+// Dev hook: force every later auto-configured plan to (cta2, bn); -1/0 = auto.
+void gemm_force_config(int cta2, int bn);
 int gemm_choose_splits(int math, int M, int N, int K, int bn = 0);
 int gemm_choose_bn(int M, int N);
 void gemm_launch(const GemmPlan& p, cudaStream_t s);

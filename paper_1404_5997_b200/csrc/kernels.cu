@@ -256,13 +256,18 @@ __global__ void colsum_partial_kernel(const T* __restrict__ x, long long M, int 
   }
 }
 
+// One warp per column: lanes stride the partial rows, then a fixed shuffle
+// tree (deterministic).
 __global__ void colsum_final_kernel(const float* __restrict__ ws, int G, int N,
                                     float* __restrict__ out) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int col = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (col >= N) return;
   float s = 0.f;
-  for (int g = 0; g < G; ++g) s += ws[static_cast<long long>(g) * N + col];
-  out[col] = s;
+  for (int g = lane; g < G; g += 32) s += ws[static_cast<long long>(g) * N + col];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[col] = s;
 }
 
 template <class T>
@@ -602,35 +607,31 @@ __global__ void __launch_bounds__(256) lrn_pool_fwd_kernel(const T* __restrict__
   }
 }
 
-// Fused backward: thread = (conv-output pixel, V-channel group).
-//   gb_i = pool backward (sum of gy over windows whose argmax is this pixel)
+// Fused backward. Block = PT pixels x all C channels; thread = (pixel,
+// V-channel group). Phase 1: each thread loads its own 16-byte vector of a and
+// gathers its own pool gradient gb (vector widx / gy loads) into shared
+// memory. Phase 2: LRN backward with the channel halos read from smem:
 //   ga_c = gb_c d_c^-beta - 2 alpha beta a_c sum_{i: c in win(i)} gb_i a_i d_i^(-beta-1)
 template <class TA>
-__global__ void __launch_bounds__(256) lrn_pool_bwd_kernel(
-    const float* __restrict__ gy, const uint8_t* __restrict__ widx, const TA* __restrict__ a,
-    TA* __restrict__ dz, int H, int W, int C, int lo, int hi, float alpha, float beta, float kk, int pk,
-    int ps, int PH, int PW, int relu_mask, int n) {
+__global__ void lrn_pool_bwd_kernel(const float* __restrict__ gy, const uint8_t* __restrict__ widx,
+                                    const TA* __restrict__ a, TA* __restrict__ dz, int H, int W, int C,
+                                    int lo, int hi, float alpha, float beta, float kk, int pk, int ps,
+                                    int PH, int PW, int relu_mask, int npix, int PT) {
   constexpr int V = 16 / sizeof(TA);
-  constexpr int NA = V + 4 * LH;  // a over [c0-2LH, c0+V+2LH)
-  constexpr int NG = V + 2 * LH;  // gb, d, t over [c0-LH, c0+V+LH)
-  const int groups = C / V;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int g = i % groups, p = i / groups;
+  extern __shared__ float lsm[];
+  float* sa = lsm;            // [PT][C]
+  float* sg = lsm + PT * C;   // [PT][C]
+  const int G = C / V;
+  const int pl = threadIdx.x / G, g = threadIdx.x - pl * G;
+  const int p = blockIdx.x * PT + pl;
+  const bool active = pl < PT && p < npix;
+  const int c0 = g * V;
+  if (active) {
+    float av[V], gb[V];
+    load_vec<TA>(a + static_cast<long long>(p) * C + c0, av);
+#pragma unroll
+    for (int j = 0; j < V; ++j) gb[j] = 0.f;
     const int w = p % W, t = p / W, h = t % H, b = t / H;
-    const int c0 = g * V;
-    const TA* px = a + static_cast<long long>(p) * C;
-    float av[NA];
-    load_vec<TA>(px + c0, av + 2 * LH);
-#pragma unroll
-    for (int j = 0; j < 2 * LH; ++j) {
-      const int cl = c0 - 2 * LH + j, cr = c0 + V + j;
-      av[j] = cl >= 0 ? to_f<TA>(px[cl]) : 0.f;
-      av[2 * LH + V + j] = cr < C ? to_f<TA>(px[cr]) : 0.f;
-    }
-    // pool backward for channels [c0-LH, c0+V+LH)
-    float gb[NG];
-#pragma unroll
-    for (int j = 0; j < NG; ++j) gb[j] = 0.f;
     const int oh0 = h - pk + 1 <= 0 ? 0 : (h - pk + ps) / ps;
     const int oh1 = min(PH - 1, h / ps);
     const int ow0 = w - pk + 1 <= 0 ? 0 : (w - pk + ps) / ps;
@@ -638,39 +639,63 @@ __global__ void __launch_bounds__(256) lrn_pool_bwd_kernel(
     for (int oh = oh0; oh <= oh1; ++oh)
       for (int ow = ow0; ow <= ow1; ++ow) {
         const int me = (h - oh * ps) * pk + (w - ow * ps);
-        const long long o = (static_cast<long long>(b * PH + oh) * PW + ow) * C;
-#pragma unroll
-        for (int j = 0; j < NG; ++j) {
-          const int c = c0 - LH + j;
-          if (c >= 0 && c < C && (j >= LH - hi && j < LH + V + lo) && widx[o + c] == me) gb[j] += gy[o + c];
+        const long long o = (static_cast<long long>(b * PH + oh) * PW + ow) * C + c0;
+        uint8_t wi[V];
+        if (V == 8) {
+          *reinterpret_cast<uint2*>(wi) = *reinterpret_cast<const uint2*>(widx + o);
+        } else {
+          *reinterpret_cast<uint32_t*>(wi) = *reinterpret_cast<const uint32_t*>(widx + o);
         }
-      }
-    // d_i, t_i for i in [c0-LH, c0+V+LH)
-    float dn[NG], tt[NG];
+        float gv[V];
+        load_vec<float>(gy + o, gv);
+        if (V == 8) load_vec<float>(gy + o + 4, gv + 4);
 #pragma unroll
-    for (int j = 0; j < NG; ++j) {
+        for (int j = 0; j < V; ++j)
+          if (wi[j] == me) gb[j] += gv[j];
+      }
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      sa[pl * C + c0 + j] = av[j];
+      sg[pl * C + c0 + j] = gb[j];
+    }
+  }
+  __syncthreads();
+  if (!active) return;
+  const float* ra = sa + pl * C;
+  const float* rg = sg + pl * C;
+  // t_i and d_i^-beta for i in [c0-LH, c0+V+LH)
+  float tt[V + 2 * LH], dn[V];
+#pragma unroll
+  for (int j = 0; j < V + 2 * LH; ++j) {
+    const int i = c0 - LH + j;
+    tt[j] = 0.f;
+    const bool need = (j >= LH - hi && j < LH + V + lo) && i >= 0 && i < C;
+    if (need) {
       float sum = 0.f;
 #pragma unroll
-      for (int d = -LH; d <= LH; ++d)
-        if (d >= -lo && d <= hi) sum += av[LH + j + d] * av[LH + j + d];
+      for (int d = -LH; d <= LH; ++d) {
+        const int q = i + d;
+        if (d >= -lo && d <= hi && q >= 0 && q < C) sum += ra[q] * ra[q];
+      }
       const float dd = kk + alpha * sum;
-      dn[j] = pow_neg(dd, beta);
-      tt[j] = gb[j] * av[LH + j] * __fdividef(dn[j], dd);
+      const float pn = pow_neg(dd, beta);
+      tt[j] = rg[i] * ra[i] * __fdividef(pn, dd);
+      if (j >= LH && j < LH + V) dn[j - LH] = pn;
     }
-    float out[V];
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      float acc = 0.f;
-#pragma unroll
-      for (int d = -LH; d <= LH; ++d)
-        if (d >= -hi && d <= lo) acc += tt[LH + k + d];
-      const float ai = av[2 * LH + k];
-      float gval = gb[LH + k] * dn[LH + k] - 2.f * alpha * beta * ai * acc;
-      if (relu_mask && !(ai > 0.f)) gval = 0.f;
-      out[k] = gval;
-    }
-    store_vec<TA>(dz + static_cast<long long>(p) * C + c0, out);
   }
+  float out[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    float acc = 0.f;
+#pragma unroll
+    for (int d = -LH; d <= LH; ++d)
+      if (d >= -hi && d <= lo) acc += tt[LH + k + d];
+    const float ai = ra[c0 + k];
+    float gval = rg[c0 + k] * dn[k] - 2.f * alpha * beta * ai * acc;
+    if (relu_mask && !(ai > 0.f)) gval = 0.f;
+    out[k] = gval;
+  }
+  store_vec<TA>(dz + static_cast<long long>(p) * C + c0, out);
 }
 
 template <class T>
@@ -794,12 +819,18 @@ void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* 
                          int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
                          int PH, int PW, int relu_mask, cudaStream_t st) {
   constexpr int V = 16 / sizeof(TA);
-  if (C % V != 0 || n > 2 * LH + 1) throw std::runtime_error("lrn_pool: C must be a multiple of 16 bytes, size <= 9");
-  const long long total = static_cast<long long>(B) * H * W * (C / V);
-  if (total >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
-  lrn_pool_bwd_kernel<TA><<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(
+  if (C % V != 0 || n > 2 * LH + 1 || C / V > 256)
+    throw std::runtime_error("lrn_pool: C must be a multiple of 16 bytes, size <= 9");
+  const long long npix = static_cast<long long>(B) * H * W;
+  if (npix * C >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
+  const int G = C / V;
+  const int PT = std::max(1, 256 / G);
+  const int threads = PT * G;
+  const size_t smem = static_cast<size_t>(2) * PT * C * sizeof(float);
+  const long long blocks = (npix + PT - 1) / PT;
+  lrn_pool_bwd_kernel<TA><<<static_cast<unsigned>(blocks), threads, smem, st>>>(
       gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, relu_mask,
-      static_cast<int>(total));
+      static_cast<int>(npix), PT);
 }
 
 template <class T>
@@ -922,7 +953,7 @@ void launch_colsum(const T* x, long long M, int N, long long ldx, float* out, fl
   const long long rows_per = (M + G - 1) / G;
   dim3 grid((N + 31) / 32, static_cast<unsigned>(G));
   colsum_partial_kernel<T><<<grid, dim3(32, 8), 0, st>>>(x, M, N, ldx, rows_per, ws);
-  colsum_final_kernel<<<(N + 127) / 128, 128, 0, st>>>(ws, static_cast<int>(G), N, out);
+  colsum_final_kernel<<<(N * 32 + 255) / 256, 256, 0, st>>>(ws, static_cast<int>(G), N, out);
 }
 
 template <class T>

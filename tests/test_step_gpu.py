@@ -111,3 +111,28 @@ def test_alexnet_bf16_loss_and_io():
     assert h2d == x.nbytes + t.nbytes and d2h > 0
     assert g.last_step_launches() > 20
     assert g.last_gemm_flops() > 5e11  # ~626 GFLOP algorithmic
+
+
+def test_cuda_graph_replay_is_bit_identical():
+    """Eager, first capture and replays produce bit-identical parameters and
+    losses (every kernel is deterministic; the graph bakes the same launches)."""
+    import torch
+    spec = hp.tiny_cnn()
+    res = []
+    for graphs in (False, True):
+        g = hp.Cluster(spec, hp.ClusterConfig(workers=2, per_worker_batch=16, scheme=hp.Scheme.C, seed=3,
+                                              math_mode=hp.MathMode.BF16))
+        g.set_graphs(graphs)
+        bufs = [hp.synthetic_batch(spec, 16, step=s, worker=w) for s in range(2) for w in range(2)]
+        dev = [(torch.from_numpy(x).cuda(), torch.from_numpy(t).cuda()) for x, t in bufs]
+        losses = []
+        for s in range(6):  # each of the 2 input sets: eager, capture, replay
+            k = s % 2
+            xs = [dev[2 * k][0], dev[2 * k + 1][0]]
+            ts = [dev[2 * k][1], dev[2 * k + 1][1]]
+            losses.append(g.run_step(xs, ts, hp.HyperParams(lr=0.01)).metrics.loss)
+        res.append((losses, [g.param(w, which, l) for w in range(2) for which in range(8)
+                             for l in range(3 if (which & 3) < 2 else 2)]))
+    assert res[0][0] == res[1][0]
+    for a, b in zip(res[0][1], res[1][1]):
+        assert np.array_equal(a, b)
