@@ -59,22 +59,36 @@ QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
 
 
 class ClockSampler:
+    """nvidia-smi sampled every 50 ms from before the timed region until after
+    it; summary() keeps the samples stamped inside [t0, t1] (host wall clock
+    around the timed region), or the nearest ones if the region was shorter
+    than the sampling interval (flagged in the result)."""
+
     def __init__(self, gpu_index: int):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         self.idx = gpu_index
         self.p = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={QUERY}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu=timestamp,{QUERY}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(1.0)  # first samples land before the timed region starts
         except Exception:
             self.p = None
         return self
 
+    def mark(self, start: bool):
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
     def __exit__(self, *a):
         if self.p:
+            time.sleep(0.2)
             self.p.terminate()
             try:
                 self.p.wait(timeout=5)
@@ -82,24 +96,35 @@ class ClockSampler:
                 self.p.kill()
 
     def summary(self):
+        import datetime
         self.f.flush()
         rows = []
         with open(self.f.name) as fh:
             for line in fh:
                 parts = [x.strip() for x in line.split(",")]
-                if len(parts) < 9:
+                if len(parts) < 10:
                     continue
                 try:
-                    rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    rows.append((ts, float(parts[2]), float(parts[3]), parts[6:10]))
                 except ValueError:
                     continue
         os.unlink(self.f.name)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        inside = [r for r in rows if self.t0 is not None and self.t0 - 0.05 <= r[0] <= (self.t1 or 0) + 0.05]
+        note = None
+        if not inside:
+            mid = ((self.t0 or 0) + (self.t1 or 0)) / 2
+            inside = sorted(rows, key=lambda r: abs(r[0] - mid))[:3]
+            note = "timed region shorter than the 50 ms sampling interval: nearest samples"
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for _, _, flags in rows for n, f in zip(names, flags) if f.lower() == "active"})
-        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows)}
+        reasons = sorted({n for _, _, _, flags in inside for n, f in zip(names, flags) if f.lower() == "active"})
+        out = {"sm_mhz": statistics.median(r[1] for r in inside), "sm_max_mhz": max(r[2] for r in inside),
+               "reasons": reasons, "samples": len(inside)}
+        if note:
+            out["note"] = note
+        return out
 
 
 # ---------------------------------------------------------------- CPU arms
@@ -264,7 +289,9 @@ def main_b200(args):
         cluster.run_step([x], [t], hyper, device=True)
 
     with ClockSampler(local) as clk:
+        clk.mark(True)
         ms, launches, loss = timed("device", args.steps)
+        clk.mark(False)
     clocks = clk.summary()
     e2e_ms, _, _ = timed("host", args.steps)
     h2d, d2h = cluster.last_step_io()

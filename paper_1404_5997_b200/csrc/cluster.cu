@@ -92,6 +92,8 @@ Geometry make_geometry(const hp_model_spec* s, int K, long long b) {
     cg.OW = static_cast<int>(ow);
     cg.relu = l.relu != 0;
     if (l.lrn_size < 0) config_error(where + ".lrn_size: must be >= 0");
+    if (l.lrn_size > 5 && l.pool_kernel > 0)
+      config_error(where + ".lrn_size: LRN fused with pooling supports sizes up to 5 on B200");
     cg.lrn_n = l.lrn_size;
     cg.lrn_alpha = static_cast<float>(l.lrn_alpha);
     cg.lrn_beta = static_cast<float>(l.lrn_beta);
@@ -312,7 +314,11 @@ class ClusterImpl final : public ClusterBase {
   void conv_forward(Worker<TA>& w);
   const TA* stage_in(const Worker<TA>& w, int l) const;
   void rotate_all(Worker<TA>& w);
-  void conv_backward(Worker<TA>& w);
+  struct ConvBwdState {
+    const float* gout = nullptr;  // grad wrt the current stage's output
+    bool dz_ready = false;        // dz already produced by the layer above's dgrad
+  };
+  void conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs);
   void route_forward(int j);
   void fc_forward_backward(int j, bool beta);
   void return_gradients(int j);
@@ -358,7 +364,10 @@ class ClusterImpl final : public ClusterBase {
   uint64_t seed_;
   std::unique_ptr<Comm> comm_;
   cudaStream_t st_ = nullptr;
+  cudaStream_t sc_ = nullptr;  // side stream: per-layer conv-gradient all-reduce
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  std::vector<cudaEvent_t> ev_layer_;  // per conv layer: its gradients are final on st_
+  cudaEvent_t ev_comm_ = nullptr;      // all conv-gradient all-reduces done on sc_
   DevArena arena_;
   std::vector<Worker<TA>> w_;
   std::vector<long long> coff_, foff_;
@@ -376,6 +385,11 @@ class ClusterImpl final : public ClusterBase {
   std::vector<ProfSlot> prof_pool_;
   size_t prof_used_ = 0;
   double gemm_flops_ = 0.0;
+  // fused FC-weight SGD state for the turn being enqueued
+  bool fuse_sgd_ = false, weights_fused_ = false, sgd_has_gscale_ = false;
+  hp_hyper sgd_hp_{};
+  double sgd_lr_ = 0.0;
+  float sgd_gscale_ = 1.f;
 };
 
 template <class TA>
@@ -413,8 +427,10 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     comm_ = make_logical_comm(K_);
   }
   HP_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  HP_CUDA(cudaStreamCreateWithFlags(&sc_, cudaStreamNonBlocking));
   HP_CUDA(cudaEventCreate(&ev0_));
   HP_CUDA(cudaEventCreate(&ev1_));
+  HP_CUDA(cudaEventCreateWithFlags(&ev_comm_, cudaEventDisableTiming));
 
   // parameter arena layouts (16-byte aligned pieces)
   for (size_t l = 0; l < g_.cg.size(); ++l) {
@@ -495,6 +511,8 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     w.colsum_ws = arena_.make<float>(static_cast<long long>(colsum_ws));
   }
   comm_->reserve(comm_scratch * sizeof(float));
+  ev_layer_.resize(g_.cg.size());
+  for (auto& e : ev_layer_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   HP_CUDA(cudaMallocHost(&host_parts_, sizeof(double) * nl * num_sub_ * xblocks_));
   HP_CUDA(cudaMallocHost(&host_bad_, sizeof(int) * nl));
   // Plans first with a null workspace to size it, then for real.
@@ -517,6 +535,9 @@ ClusterImpl<TA>::~ClusterImpl() {
   comm_.reset();
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
+  for (auto e : ev_layer_) cudaEventDestroy(e);
+  if (ev_comm_) cudaEventDestroy(ev_comm_);
+  if (sc_) cudaStreamDestroy(sc_);
   for (auto& s : prof_pool_) {
     cudaEventDestroy(s.a);
     cudaEventDestroy(s.b);
@@ -918,9 +939,26 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
       const int rows = static_cast<int>(f.c1[w.gid] - f.c0[w.gid]);
       GemmPlan pw = w.fc_wgrad[li];
       pw.args.epi.beta = beta ? 1 : 0;
+      if (fuse_sgd_) {
+        // last (or, in variable mode, every) turn: the weight update runs in
+        // the wgrad epilogue; the gradient is never stored
+        Epi& e = pw.args.epi;
+        e.sgd_w = w.fp + fc_w_off(li);
+        e.sgd_m = w.fm + fc_w_off(li);
+        e.sgd_copy = kTA == kBF16 ? static_cast<void*>(w.fpt + fc_w_off(li)) : nullptr;
+        e.sgd_mu = static_cast<float>(sgd_hp_.momentum);
+        e.sgd_s1 = static_cast<float>(-sgd_lr_);
+        e.sgd_s2 = static_cast<float>(-sgd_lr_ * sgd_hp_.weight_decay);
+        e.sgd_gscale = sgd_gscale_;
+        e.sgd_has_gscale = sgd_has_gscale_ ? 1 : 0;
+        if (pw.splits > 1) pw.args.epi = e;
+      }
+      // dgrad first: it must read this layer's weights before the (fused)
+      // update of the wgrad epilogue -- turn j's dX uses pre-update weights
+      // (cluster.cpp:562-601)
+      gemm(w.fc_dgrad[li], "fc_dgrad", li);
       gemm(pw, "fc_wgrad", li);
       launch_rowsum<TA>(w.fdz[li], rows, static_cast<int>(n_), ldn_, w.fgr + fc_b_off(li), beta ? 1 : 0, st_);
-      gemm(w.fc_dgrad[li], "fc_dgrad", li);
       ++launches_;
     }
     if (li > 0 && K_ > 1) {
@@ -968,55 +1006,53 @@ void ClusterImpl<TA>::return_gradients(int j) {
 // ------------------------------------------------------------------ backward
 // conv_backward_from_flat (model.cpp:259-283) with the pool / LRN superset.
 template <class TA>
-void ClusterImpl<TA>::conv_backward(Worker<TA>& w) {
-  const int nc = static_cast<int>(g_.cg.size());
-  const float* gout = w.gflat;
-  bool dz_ready = false;
-  for (int l = nc - 1; l >= 0; --l) {
-    const ConvGeom& c = g_.cg[l];
-    const TA* mask = c.relu ? w.act[l] : nullptr;
-    const int B = static_cast<int>(b_);
-    if (c.pk > 0 && c.lrn_n > 0) {
-      launch_lrn_pool_bwd<TA>(gout, w.widx[l], w.act[l], w.dz[l], B, c.OH, c.OW, c.F, c.lrn_n,
-                              c.lrn_alpha, c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, c.relu ? 1 : 0,
-                              st_);
-      ++launches_;
-    } else if (c.pk > 0) {
-      launch_maxpool_bwd_w<TA, TA>(gout, w.widx[l], w.dz[l], mask, B, c.OH, c.OW, c.F, c.pk, c.ps,
-                                   c.PH, c.PW, st_);
-      ++launches_;
-    } else if (c.lrn_n > 0) {
-      launch_lrn_bwd<TA, TA>(w.act[l], w.lrn_d[l], gout, w.dz[l], c.P, c.F, c.lrn_n, c.lrn_alpha,
-                             c.lrn_beta, c.relu ? 1 : 0, st_);
-      ++launches_;
-    } else if (!dz_ready) {
-      launch_mask_cast<TA, TA>(gout, mask, w.dz[l], c.P * c.F, st_);
-      ++launches_;
-    }
-    // bias grad = channel sums of dz (model.cpp:184-202)
-    launch_colsum<TA>(w.dz[l], c.P, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, st_);
-    launches_ += 2;
-    gemm(w.conv_wgrad[l], "conv_wgrad", l);
-    if (l == 0) break;
-    const ConvGeom& pc = g_.cg[l - 1];
-    const bool below_fused = pc.pk > 0 || pc.lrn_n > 0;
-    gemm(w.conv_dgrad[l], "conv_dgrad", l);
-    if (!c.impl_dgrad) {
-      if (below_fused) {
-        launch_col2im<float, TA>(w.dcol[l], w.gstage[l - 1], nullptr, B, c.H, c.W, c.C, c.R, c.S,
-                                 c.stride, c.pad, c.OH, c.OW, c.ldk, st_);
-      } else {
-        launch_col2im<TA, TA>(w.dcol[l], w.dz[l - 1], pc.relu ? w.act[l - 1] : nullptr, B, c.H, c.W,
-                              c.C, c.R, c.S, c.stride, c.pad, c.OH, c.OW, c.ldk, st_);
-      }
-      ++launches_;
-    }
+void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs) {
+  if (l == static_cast<int>(g_.cg.size()) - 1) {
+    cs.gout = w.gflat;
+    cs.dz_ready = false;
+  }
+  const ConvGeom& c = g_.cg[l];
+  const TA* mask = c.relu ? w.act[l] : nullptr;
+  const int B = static_cast<int>(b_);
+  if (c.pk > 0 && c.lrn_n > 0) {
+    launch_lrn_pool_bwd<TA>(cs.gout, w.widx[l], w.act[l], w.dz[l], B, c.OH, c.OW, c.F, c.lrn_n, c.lrn_alpha,
+                            c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, c.relu ? 1 : 0, st_);
+    ++launches_;
+  } else if (c.pk > 0) {
+    launch_maxpool_bwd_w<TA, TA>(cs.gout, w.widx[l], w.dz[l], mask, B, c.OH, c.OW, c.F, c.pk, c.ps, c.PH,
+                                 c.PW, st_);
+    ++launches_;
+  } else if (c.lrn_n > 0) {
+    launch_lrn_bwd<TA, TA>(w.act[l], w.lrn_d[l], cs.gout, w.dz[l], c.P, c.F, c.lrn_n, c.lrn_alpha,
+                           c.lrn_beta, c.relu ? 1 : 0, st_);
+    ++launches_;
+  } else if (!cs.dz_ready) {
+    launch_mask_cast<TA, TA>(cs.gout, mask, w.dz[l], c.P * c.F, st_);
+    ++launches_;
+  }
+  // bias grad = channel sums of dz (model.cpp:184-202)
+  launch_colsum<TA>(w.dz[l], c.P, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, st_);
+  launches_ += 2;
+  gemm(w.conv_wgrad[l], "conv_wgrad", l);
+  if (l == 0) return;
+  const ConvGeom& pc = g_.cg[l - 1];
+  const bool below_fused = pc.pk > 0 || pc.lrn_n > 0;
+  gemm(w.conv_dgrad[l], "conv_dgrad", l);
+  if (!c.impl_dgrad) {
     if (below_fused) {
-      gout = w.gstage[l - 1];
-      dz_ready = false;
+      launch_col2im<float, TA>(w.dcol[l], w.gstage[l - 1], nullptr, B, c.H, c.W, c.C, c.R, c.S, c.stride,
+                               c.pad, c.OH, c.OW, c.ldk, st_);
     } else {
-      dz_ready = true;
+      launch_col2im<TA, TA>(w.dcol[l], w.dz[l - 1], pc.relu ? w.act[l - 1] : nullptr, B, c.H, c.W, c.C,
+                            c.R, c.S, c.stride, c.pad, c.OH, c.OW, c.ldk, st_);
     }
+    ++launches_;
+  }
+  if (below_fused) {
+    cs.gout = w.gstage[l - 1];
+    cs.dz_ready = false;
+  } else {
+    cs.dz_ready = true;
   }
 }
 
@@ -1024,6 +1060,21 @@ template <class TA>
 void ClusterImpl<TA>::sgd_fc(double lr, float gscale, bool has_gscale, const hp_hyper& hp) {
   std::vector<SgdTensor> ts;
   for (auto& w : w_) {
+    if (weights_fused_) {  // weights were updated in the wgrad epilogues: biases only
+      for (size_t l = 0; l < g_.fg.size(); ++l) {
+        SgdTensor t{};
+        const long long off = fc_b_off(static_cast<int>(l));
+        t.w = w.fp + off;
+        t.mom = w.fm + off;
+        t.g = w.fgr + off;
+        t.copy = w.fpt ? static_cast<void*>(w.fpt + off) : nullptr;
+        t.n = g_.fg[l].cmax;
+        t.gscale = gscale;
+        t.has_gscale = has_gscale ? 1 : 0;
+        ts.push_back(t);
+      }
+      continue;
+    }
     SgdTensor t{};
     t.w = w.fp;
     t.mom = w.fm;
@@ -1090,16 +1141,41 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
   for (auto& w : w_) conv_forward(w);
   for (int j = 0; j < num_sub_; ++j) {
     route_forward(j);
+    // Fused FC weight update in the wgrad epilogue: every turn in variable
+    // mode (cluster.cpp:586-601), the last turn of the accumulation in exact
+    // mode (Σ_j grads × 1/num_sub, cluster.cpp:602-609, 680-696).
+    fuse_sgd_ = fuse_fc_sgd && (variable_ || j == num_sub_ - 1);
+    sgd_hp_ = hp;
+    sgd_lr_ = variable_ ? fc_lr : lr;
+    sgd_has_gscale_ = !variable_ && num_sub_ > 1;
+    sgd_gscale_ = static_cast<float>(1.0 / static_cast<double>(num_sub_));
     fc_forward_backward(j, !variable_ && j > 0);
     return_gradients(j);
+    weights_fused_ = fuse_sgd_;
     if (variable_) sgd_fc(fc_lr, 1.f, false, hp);  // per-sub-batch update (cluster.cpp:586-601)
   }
-  for (auto& w : w_) conv_backward(w);
+  fuse_sgd_ = false;
+  // Conv backward; each layer's gradients (all local workers) are all-reduced
+  // on the side stream as soon as they are final, overlapping the rest of the
+  // backward (sync_conv_gradients, cluster.cpp:273-319, bucketed per layer in
+  // backward order -- the same order on every rank).
+  const int nc = static_cast<int>(g_.cg.size());
+  std::vector<ConvBwdState> cbs(nl);
+  for (int l = nc - 1; l >= 0; --l) {
+    for (int i = 0; i < nl; ++i) conv_backward_layer(w_[i], l, cbs[i]);
+    if (K_ > 1) {
+      HP_CUDA(cudaEventRecord(ev_layer_[l], st_));
+      HP_CUDA(cudaStreamWaitEvent(sc_, ev_layer_[l], 0));
+      std::vector<float*> bufs(nl);
+      for (int i = 0; i < nl; ++i) bufs[i] = w_[i].cgr + conv_k_off(l);
+      const long long cnt = static_cast<long long>(g_.cg[l].F) * g_.cg[l].ldk + g_.cg[l].F;
+      comm_->allreduce_f32(bufs, static_cast<size_t>(cnt), sc_);
+      launches_ += 1;
+    }
+  }
   if (K_ > 1) {
-    std::vector<float*> bufs(nl);
-    for (int i = 0; i < nl; ++i) bufs[i] = w_[i].cgr;
-    comm_->allreduce_f32(bufs, conv_total_, st_);
-    launches_ += 1;
+    HP_CUDA(cudaEventRecord(ev_comm_, sc_));
+    HP_CUDA(cudaStreamWaitEvent(st_, ev_comm_, 0));
   }
   if (!variable_) {
     const bool scale = num_sub_ > 1;

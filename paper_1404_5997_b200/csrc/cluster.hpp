@@ -73,6 +73,7 @@ class ClusterBase {
   };
   bool profile = false;            // bracket every GEMM with CUDA events
   bool use_graphs = true;          // replay the step as a captured CUDA graph
+  bool fuse_fc_sgd = true;         // FC weight update in the wgrad GEMM epilogue
   std::vector<GemmProf> prof;      // last step, launch order
   double prof_gemm_ms = 0.0;
   double last_gemm_flops = 0.0;    // algorithmic GEMM FLOPs of the last step

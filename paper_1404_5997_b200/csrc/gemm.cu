@@ -41,11 +41,28 @@ __device__ __forceinline__ float load_as_float(const void* p, long long off, int
   return reinterpret_cast<const float*>(p)[off];
 }
 
+__device__ __forceinline__ float sgd_apply(const Epi& e, long long off, float g) {
+  if (e.sgd_has_gscale) g = __fmul_rn(g, e.sgd_gscale);
+  const float w = e.sgd_w[off];
+  float d = __fmul_rn(e.sgd_m[off], e.sgd_mu);
+  d = __fadd_rn(d, __fmul_rn(e.sgd_s1, g));
+  d = __fadd_rn(d, __fmul_rn(e.sgd_s2, w));
+  const float nw = __fadd_rn(w, d);
+  e.sgd_m[off] = d;
+  e.sgd_w[off] = nw;
+  if (e.sgd_copy) reinterpret_cast<__nv_bfloat16*>(e.sgd_copy)[off] = __float2bfloat16_rn(nw);
+  return nw;
+}
+
 __device__ __forceinline__ void epi_elem(const Epi& e, int m, int n, float v) {
   const long long off = e.c_trans ? static_cast<long long>(n) * e.ldc + m
                                   : static_cast<long long>(m) * e.ldc + n;
   v *= e.alpha;
   if (e.beta) v += reinterpret_cast<const float*>(e.c)[off];
+  if (e.sgd_w) {
+    sgd_apply(e, off, v);
+    return;
+  }
   if (e.bias_mode == 1) v += e.bias[m];
   if (e.bias_mode == 2) v += e.bias[n];
   if (e.relu) v = v > 0.f ? v : 0.f;
@@ -81,6 +98,7 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
   // Vector path: 32 contiguous outputs of row m (bias/ReLU/alpha/beta/mask fused).
   const bool vec = !e.c_trans && n0 + 32 <= a.N &&
                    (e.c_type == kF32 ? (e.ldc & 3) == 0 : (e.ldc & 7) == 0) &&
+                   (!e.sgd_w || ((e.ldc & 7) == 0 && e.c_type == kF32)) &&
                    (!e.beta || e.c_type == kF32) &&
                    (!e.mask || (e.mask_trans == 0 && (e.mask_type == kF32 ? (e.ldmask & 3) == 0
                                                                              : (e.ldmask & 7) == 0)));
@@ -100,6 +118,41 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
         x[4 * i + 2] += o.z;
         x[4 * i + 3] += o.w;
       }
+    }
+    if (e.sgd_w) {
+      float* wp = e.sgd_w + off;
+      float* mp = e.sgd_m + off;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 w4 = reinterpret_cast<const float4*>(wp)[i];
+        float4 m4 = reinterpret_cast<const float4*>(mp)[i];
+        float* wv = reinterpret_cast<float*>(&w4);
+        float* mv = reinterpret_cast<float*>(&m4);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float g = x[4 * i + j];
+          if (e.sgd_has_gscale) g = __fmul_rn(g, e.sgd_gscale);
+          float d = __fmul_rn(mv[j], e.sgd_mu);
+          d = __fadd_rn(d, __fmul_rn(e.sgd_s1, g));
+          d = __fadd_rn(d, __fmul_rn(e.sgd_s2, wv[j]));
+          mv[j] = d;
+          wv[j] = __fadd_rn(wv[j], d);
+          x[4 * i + j] = wv[j];
+        }
+        reinterpret_cast<float4*>(wp)[i] = w4;
+        reinterpret_cast<float4*>(mp)[i] = m4;
+      }
+      if (e.sgd_copy) {
+        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.sgd_copy) + off);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          __align__(16) __nv_bfloat16 t[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) t[j] = __float2bfloat16_rn(x[8 * i + j]);
+          dst[i] = *reinterpret_cast<const uint4*>(t);
+        }
+      }
+      return;
     }
     if (e.bias_mode == 1) {
 #pragma unroll

@@ -39,6 +39,16 @@ struct Epi {
   long long ldmask = 0;
   int mask_type = kF32;
   int mask_trans = 0;
+  // Fused momentum SGD (optimizer.cpp:19-31, float storage: four rounded
+  // passes, no FMA). When sgd_w is set the (accumulated) result is the
+  // gradient g of the parameters at the same offsets as c (ldc, row-major);
+  // w and the momentum are updated in place and the gradient is not stored:
+  //   g := g * gscale (if has_gscale);  d := mu d + s1 g + s2 w;  w := w + d
+  float* sgd_w = nullptr;
+  float* sgd_m = nullptr;
+  void* sgd_copy = nullptr;  // optional bf16 operand copy of w (same offsets)
+  float sgd_mu = 0.f, sgd_s1 = 0.f, sgd_s2 = 0.f, sgd_gscale = 1.f;
+  int sgd_has_gscale = 0;
 };
 
 // Implicit-GEMM convolution operand: the matrix is the im2col view of an NHWC

@@ -461,31 +461,34 @@ __global__ void __launch_bounds__(256) im2col_nchw_kernel(const float* __restric
 }
 
 // Block = (image, output row); threadIdx.x = output column, threadIdx.y steps
-// k. Every element is one L1-resident load and one coalesced store.
+// over (c, r) input-row pairs; each thread walks the S taps of its row with
+// incremental addressing (one bounds check per row, ~6 instructions/element).
 template <class T>
 __global__ void __launch_bounds__(256) im2col_t_nchw_kernel(const float* __restrict__ x, T* __restrict__ colT,
                                                             int C, int H, int W, int R, int S, int stride,
                                                             int pad, int OH, int OW, long long ldp, int K) {
-  extern __shared__ int ktab[];  // k -> (c*H*W + r*W + s) offsets relative to the window origin
   const int oh = blockIdx.x % OH, b = blockIdx.x / OH;
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-  for (int k = tid; k < K; k += blockDim.x * blockDim.y) {
-    const int c = k % C, rs = k / C;
-    ktab[2 * k] = c * H * W;
-    ktab[2 * k + 1] = ((rs / S) << 16) | (rs % S);
-  }
-  __syncthreads();
   const int ow = threadIdx.x;
   if (ow >= OW) return;
   const float* xb = x + static_cast<long long>(b) * C * H * W;
   const long long p = (static_cast<long long>(b) * OH + oh) * OW + ow;
   const int h0 = oh * stride - pad, w0 = ow * stride - pad;
-  for (int k = threadIdx.y; k < K; k += blockDim.y) {
-    const int off = ktab[2 * k], rsv = ktab[2 * k + 1];
-    const int h = h0 + (rsv >> 16), w = w0 + (rsv & 0xFFFF);
-    const float v = (h >= 0 && h < H && w >= 0 && w < W) ? __ldg(xb + off + h * W + w) : 0.f;
-    colT[static_cast<long long>(k) * ldp + p] = from_f<T>(v);
+  const long long kstep = static_cast<long long>(C) * ldp;  // next tap s -> k += C
+  for (int cr = threadIdx.y; cr < C * R; cr += blockDim.y) {
+    const int c = cr / R, r = cr - c * R;
+    const int h = h0 + r;
+    const bool hv = h >= 0 && h < H;
+    const float* row = xb + (static_cast<long long>(c) * H + (hv ? h : 0)) * W;
+    T* dst = colT + (static_cast<long long>(r * S) * C + c) * ldp + p;
+#pragma unroll 4
+    for (int s = 0; s < S; ++s) {
+      const int w = w0 + s;
+      const float v = (hv && w >= 0 && w < W) ? __ldg(row + w) : 0.f;
+      *dst = from_f<T>(v);
+      dst += kstep;
+    }
   }
+  (void)K;
 }
 
 // ------------------------------------------------------------------ fused LRN + pool
@@ -528,38 +531,38 @@ __device__ __forceinline__ void store_vec<float>(float* p, const float* v) {
   *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
 }
 
-// a[-LH .. V+LH) of one pixel around channel c0 (zeros outside [0, C)).
-template <class T, int V>
+// a[-HL .. V+HL) of one pixel around channel c0 (zeros outside [0, C)).
+template <class T, int V, int HL>
 __device__ __forceinline__ void load_window(const T* px, int c0, int C, float* w) {
-  load_vec<T>(px + c0, w + LH);
+  load_vec<T>(px + c0, w + HL);
 #pragma unroll
-  for (int j = 0; j < LH; ++j) {
-    const int cl = c0 - LH + j, cr = c0 + V + j;
+  for (int j = 0; j < HL; ++j) {
+    const int cl = c0 - HL + j, cr = c0 + V + j;
     w[j] = cl >= 0 ? to_f<T>(px[cl]) : 0.f;
-    w[LH + V + j] = cr < C ? to_f<T>(px[cr]) : 0.f;
+    w[HL + V + j] = cr < C ? to_f<T>(px[cr]) : 0.f;
   }
 }
 
 // LRN of channels c0..c0+V-1 from the window w (sum over [c-lo, c+hi]).
-template <int V>
+template <int V, int HL>
 __device__ __forceinline__ void lrn_vals(const float* w, int lo, int hi, float alpha, float beta,
                                          float kk, float* out) {
-  float sq[V + 2 * LH];
+  float sq[V + 2 * HL];
 #pragma unroll
-  for (int j = 0; j < V + 2 * LH; ++j) sq[j] = w[j] * w[j];
+  for (int j = 0; j < V + 2 * HL; ++j) sq[j] = w[j] * w[j];
 #pragma unroll
   for (int i = 0; i < V; ++i) {
     float sum = 0.f;
 #pragma unroll
-    for (int d = -LH; d <= LH; ++d)
-      if (d >= -lo && d <= hi) sum += sq[LH + i + d];
-    out[i] = w[LH + i] * pow_neg(kk + alpha * sum, beta);
+    for (int d = -HL; d <= HL; ++d)
+      if (d >= -lo && d <= hi) sum += sq[HL + i + d];
+    out[i] = w[HL + i] * pow_neg(kk + alpha * sum, beta);
   }
 }
 
 // Fused LRN + max-pool forward: thread = (pooled pixel, V-channel group).
-template <class T>
-__global__ void __launch_bounds__(256) lrn_pool_fwd_kernel(const T* __restrict__ a, T* __restrict__ y,
+template <class T, int HL>
+__global__ void __launch_bounds__(256, 4) lrn_pool_fwd_kernel(const T* __restrict__ a, T* __restrict__ y,
                                                            uint8_t* __restrict__ widx, int H, int W, int C,
                                                            int lo, int hi, float alpha, float beta, float kk,
                                                            int pk, int ps, int PH, int PW, int n) {
@@ -579,9 +582,9 @@ __global__ void __launch_bounds__(256) lrn_pool_fwd_kernel(const T* __restrict__
     for (int r = 0; r < pk; ++r) {
       const T* row = a + (static_cast<long long>(b * H + ph * ps + r) * W + pw * ps) * C;
       for (int q = 0; q < pk; ++q) {
-        float w[V + 2 * LH], v[V];
-        load_window<T, V>(row + q * C, c0, C, w);
-        lrn_vals<V>(w, lo, hi, alpha, beta, kk, v);
+        float w[V + 2 * HL], v[V];
+        load_window<T, V, HL>(row + q * C, c0, C, w);
+        lrn_vals<V, HL>(w, lo, hi, alpha, beta, kk, v);
         const int pos = r * pk + q;
 #pragma unroll
         for (int j = 0; j < V; ++j)
@@ -612,15 +615,17 @@ __global__ void __launch_bounds__(256) lrn_pool_fwd_kernel(const T* __restrict__
 // gathers its own pool gradient gb (vector widx / gy loads) into shared
 // memory. Phase 2: LRN backward with the channel halos read from smem:
 //   ga_c = gb_c d_c^-beta - 2 alpha beta a_c sum_{i: c in win(i)} gb_i a_i d_i^(-beta-1)
-template <class TA>
-__global__ void lrn_pool_bwd_kernel(const float* __restrict__ gy, const uint8_t* __restrict__ widx,
-                                    const TA* __restrict__ a, TA* __restrict__ dz, int H, int W, int C,
-                                    int lo, int hi, float alpha, float beta, float kk, int pk, int ps,
-                                    int PH, int PW, int relu_mask, int npix, int PT) {
+template <class TA, int HL>
+__global__ void __launch_bounds__(256) lrn_pool_bwd_kernel(
+    const float* __restrict__ gy, const uint8_t* __restrict__ widx, const TA* __restrict__ a,
+    TA* __restrict__ dz, int H, int W, int C, int lo, int hi, float alpha, float beta, float kk, int pk,
+    int ps, int PH, int PW, int relu_mask, int npix, int PT) {
   constexpr int V = 16 / sizeof(TA);
-  extern __shared__ float lsm[];
-  float* sa = lsm;            // [PT][C]
-  float* sg = lsm + PT * C;   // [PT][C]
+  extern __shared__ float4 lsm4[];
+  float* lsm = reinterpret_cast<float*>(lsm4);
+  const int RS = C + 2 * LH;      // padded row: [LH halo | C | LH halo]
+  float* sa = lsm;                // [PT][RS]
+  float* sg = lsm + PT * RS;      // [PT][RS]
   const int G = C / V;
   const int pl = threadIdx.x / G, g = threadIdx.x - pl * G;
   const int p = blockIdx.x * PT + pl;
@@ -653,45 +658,62 @@ __global__ void lrn_pool_bwd_kernel(const float* __restrict__ gy, const uint8_t*
         for (int j = 0; j < V; ++j)
           if (wi[j] == me) gb[j] += gv[j];
       }
+    float4* ra4 = reinterpret_cast<float4*>(sa + pl * RS + LH + c0);
+    float4* rg4 = reinterpret_cast<float4*>(sg + pl * RS + LH + c0);
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      sa[pl * C + c0 + j] = av[j];
-      sg[pl * C + c0 + j] = gb[j];
+    for (int j = 0; j < V / 4; ++j) {
+      ra4[j] = make_float4(av[4 * j], av[4 * j + 1], av[4 * j + 2], av[4 * j + 3]);
+      rg4[j] = make_float4(gb[4 * j], gb[4 * j + 1], gb[4 * j + 2], gb[4 * j + 3]);
     }
   }
   __syncthreads();
   if (!active) return;
-  const float* ra = sa + pl * C;
-  const float* rg = sg + pl * C;
-  // t_i and d_i^-beta for i in [c0-LH, c0+V+LH)
-  float tt[V + 2 * LH], dn[V];
+  // a over [c0-4, c0+V+4) and gb over the same span, as float4 smem loads
+  // (rows carry a 4-float halo; channels outside [0, C) are zeroed). HL <= 2
+  // covers LRN size <= 5, the general path HL = 4 reads the same span twice.
+  static_assert(HL <= 4, "halo");
+  constexpr int NS = V + 8;
+  float A[NS], Gb[NS];
+  {
+    const float4* ra4 = reinterpret_cast<const float4*>(sa + pl * RS + c0);  // = channel c0-4
+    const float4* rg4 = reinterpret_cast<const float4*>(sg + pl * RS + c0);
 #pragma unroll
-  for (int j = 0; j < V + 2 * LH; ++j) {
-    const int i = c0 - LH + j;
-    tt[j] = 0.f;
-    const bool need = (j >= LH - hi && j < LH + V + lo) && i >= 0 && i < C;
-    if (need) {
-      float sum = 0.f;
-#pragma unroll
-      for (int d = -LH; d <= LH; ++d) {
-        const int q = i + d;
-        if (d >= -lo && d <= hi && q >= 0 && q < C) sum += ra[q] * ra[q];
-      }
-      const float dd = kk + alpha * sum;
-      const float pn = pow_neg(dd, beta);
-      tt[j] = rg[i] * ra[i] * __fdividef(pn, dd);
-      if (j >= LH && j < LH + V) dn[j - LH] = pn;
+    for (int j = 0; j < NS / 4; ++j) {
+      const float4 x = ra4[j], y = rg4[j];
+      A[4 * j] = x.x; A[4 * j + 1] = x.y; A[4 * j + 2] = x.z; A[4 * j + 3] = x.w;
+      Gb[4 * j] = y.x; Gb[4 * j + 1] = y.y; Gb[4 * j + 2] = y.z; Gb[4 * j + 3] = y.w;
     }
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const int c = c0 - 4 + j;
+      if (c < 0 || c >= C) {
+        A[j] = 0.f;
+        Gb[j] = 0.f;
+      }
+    }
+  }
+  // t_i, d_i for i in [c0-HL, c0+V+HL): index j = i - (c0-4)
+  float tt[NS], dn[V];
+#pragma unroll
+  for (int j = 4 - HL; j < 4 + V + HL; ++j) {
+    float sum = 0.f;
+#pragma unroll
+    for (int d = -HL; d <= HL; ++d)
+      if (d >= -lo && d <= hi && j + d >= 0 && j + d < NS) sum += A[j + d] * A[j + d];
+    const float dd = kk + alpha * sum;
+    const float pn = pow_neg(dd, beta);
+    tt[j] = Gb[j] * A[j] * __fdividef(pn, dd);
+    if (j >= 4 && j < 4 + V) dn[j - 4] = pn;
   }
   float out[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) {
     float acc = 0.f;
 #pragma unroll
-    for (int d = -LH; d <= LH; ++d)
-      if (d >= -hi && d <= lo) acc += tt[LH + k + d];
-    const float ai = ra[c0 + k];
-    float gval = rg[c0 + k] * dn[k] - 2.f * alpha * beta * ai * acc;
+    for (int d = -HL; d <= HL; ++d)
+      if (d >= -hi && d <= lo) acc += tt[4 + k + d];
+    const float ai = A[4 + k];
+    float gval = Gb[4 + k] * dn[k] - 2.f * alpha * beta * ai * acc;
     if (relu_mask && !(ai > 0.f)) gval = 0.f;
     out[k] = gval;
   }
@@ -798,8 +820,8 @@ void launch_im2col_t_nchw(const float* x, T* colT, int B, int C, int H, int W, i
   const int bx = ((OW + 31) / 32) * 32;
   const int by = std::max(1, 256 / bx);
   const int K = R * S * C;
-  im2col_t_nchw_kernel<T><<<B * OH, dim3(bx, by), static_cast<size_t>(K) * 2 * sizeof(int), st>>>(
-      x, colT, C, H, W, R, S, stride, pad, OH, OW, ldp, K);
+  im2col_t_nchw_kernel<T><<<B * OH, dim3(bx, by), 0, st>>>(x, colT, C, H, W, R, S, stride, pad, OH, OW,
+                                                            ldp, K);
 }
 
 template <class T>
@@ -810,8 +832,13 @@ void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, i
   if (C % V != 0 || n > 2 * LH + 1) throw std::runtime_error("lrn_pool: C must be a multiple of 16 bytes, size <= 9");
   const long long total = static_cast<long long>(B) * PH * PW * (C / V);
   if (static_cast<long long>(B) * H * W >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
-  lrn_pool_fwd_kernel<T><<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(
-      a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, static_cast<int>(total));
+  if (n <= 5) {
+    lrn_pool_fwd_kernel<T, 2><<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(
+        a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, static_cast<int>(total));
+  } else {
+    lrn_pool_fwd_kernel<T, LH><<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(
+        a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, static_cast<int>(total));
+  }
 }
 
 template <class TA>
@@ -826,9 +853,10 @@ void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* 
   const int G = C / V;
   const int PT = std::max(1, 256 / G);
   const int threads = PT * G;
-  const size_t smem = static_cast<size_t>(2) * PT * C * sizeof(float);
+  const size_t smem = static_cast<size_t>(2) * PT * (C + 2 * LH) * sizeof(float);
   const long long blocks = (npix + PT - 1) / PT;
-  lrn_pool_bwd_kernel<TA><<<static_cast<unsigned>(blocks), threads, smem, st>>>(
+  if (n > 5) throw std::runtime_error("lrn_pool backward: LRN size > 5 not supported yet");
+  lrn_pool_bwd_kernel<TA, 2><<<static_cast<unsigned>(blocks), threads, smem, st>>>(
       gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, relu_mask,
       static_cast<int>(npix), PT);
 }
