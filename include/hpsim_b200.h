@@ -215,6 +215,9 @@ HP_API double hp_cluster_last_gemm_flops(const hp_cluster* c);
 /* Bracket every GEMM with CUDA events on the launching stream (adds event
  * records; off for timed runs). */
 HP_API int hp_cluster_set_profile(hp_cluster* c, int on);
+/* FC weight update fused into the FC wgrad GEMM epilogue (default on); off
+ * stores the FC gradients and runs the multi-tensor SGD kernel instead. */
+HP_API int hp_cluster_set_fuse_fc_sgd(hp_cluster* c, int on);
 /* Replay each step as a captured CUDA graph (default on). A graph is keyed by
  * the step's input pointers, memory kind and scalars; it is captured the second
  * time a key is seen (the first runs eagerly) and replayed afterwards. Host

@@ -160,6 +160,7 @@ def _load() -> C.CDLL:
         "hp_cluster_last_step_io": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], None),
         "hp_cluster_last_gemm_flops": ([P], C.c_double),
         "hp_cluster_set_profile": ([P, C.c_int], C.c_int),
+        "hp_cluster_set_fuse_fc_sgd": ([P, C.c_int], C.c_int),
         "hp_cluster_set_graphs": ([P, C.c_int], C.c_int),
         "hp_cluster_gemm_profile": ([P, C.POINTER(HpGemmProf), C.c_int], C.c_int),
     }

@@ -374,6 +374,10 @@ class Cluster:
         """Replay steps as captured CUDA graphs (default on; see hp_cluster_set_graphs)."""
         _check(lib.hp_cluster_set_graphs(self._h, int(bool(on))))
 
+    def set_fuse_fc_sgd(self, on: bool) -> None:
+        """FC weight update in the wgrad GEMM epilogue (default on)."""
+        _check(lib.hp_cluster_set_fuse_fc_sgd(self._h, int(bool(on))))
+
     def set_profile(self, on: bool) -> None:
         _check(lib.hp_cluster_set_profile(self._h, int(bool(on))))
 

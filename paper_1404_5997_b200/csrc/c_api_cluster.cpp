@@ -141,6 +141,10 @@ HP_API int hp_cluster_set_graphs(hp_cluster* c, int on) {
   return guarded_c([&] { c->impl->use_graphs = on != 0; });
 }
 
+HP_API int hp_cluster_set_fuse_fc_sgd(hp_cluster* c, int on) {
+  return guarded_c([&] { c->impl->fuse_fc_sgd = on != 0; });
+}
+
 HP_API int hp_cluster_set_profile(hp_cluster* c, int on) {
   return guarded_c([&] { c->impl->profile = on != 0; });
 }

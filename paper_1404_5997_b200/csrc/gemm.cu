@@ -22,14 +22,15 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr uint32_t kMaxDynSmem = 232448;  // 227 KB
+constexpr uint32_t kEpiSmemBytes = 4u * 32u * 36u * 4u;  // staged epilogue tiles (see epi_chunk)
 
 __host__ __device__ constexpr uint32_t stage_bytes(int bn, int math) {
   return (kBM * 128u + static_cast<uint32_t>(bn) * 128u) * (math == kMathF32x3 ? 2u : 1u);
 }
 __host__ __device__ constexpr int num_stages(int bn, int math) {
-  return static_cast<int>((kMaxDynSmem - 2048u) / stage_bytes(bn, math)) > 6
+  return static_cast<int>((kMaxDynSmem - 2048u - kEpiSmemBytes) / stage_bytes(bn, math)) > 6
              ? 6
-             : static_cast<int>((kMaxDynSmem - 2048u) / stage_bytes(bn, math));
+             : static_cast<int>((kMaxDynSmem - 2048u - kEpiSmemBytes) / stage_bytes(bn, math));
 }
 // TMEM columns of one accumulator (power of two >= 32); two are allocated.
 __host__ __device__ constexpr uint32_t tmem_cols(int bn) {
@@ -214,6 +215,220 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
   }
   for (int i = 0; i < 32; ++i) {
     if (n0 + i < a.N) epi_elem(e, m, n0 + i, v[i]);
+  }
+}
+
+// ---------------------------------------------------------------- staged epilogue
+// tcgen05.ld hands each thread one accumulator ROW; stores straight from that
+// layout put 32 different rows (32 cache lines) behind every warp access.
+// Instead each epilogue warp transposes its 32x32 fp32 chunk through a padded
+// smem tile (row stride 36 floats: float4 writes and reads are bank-conflict
+// free) so that 8 consecutive lanes cover 32 consecutive columns of one row:
+// every global access of the epilogue (beta read, mask, SGD w/m read+write,
+// output) is then a full 128-byte row segment. The loads of all 8 row groups
+// are issued before any store so the memory-bound epilogues (FC wgrad with the
+// fused SGD update) keep 16+ accesses in flight per thread.
+constexpr int kEpiLd = 36;                               // floats per staged row
+static_assert(kEpiSmemBytes == 4u * 32u * kEpiLd * 4u, "epilogue tile size");
+
+__device__ __forceinline__ bool epi_vec_ok(const GemmArgs& a) {
+  if (a.raw_partial) return (a.N & 3) == 0;
+  const Epi& e = a.epi;
+  if (e.c_trans || e.mask_trans) return false;
+  if (e.ldc & 3) return false;
+  if (e.beta && e.c_type != kF32) return false;
+  if (e.sgd_w && e.c_type != kF32) return false;
+  if (e.mask && (e.ldmask & 3)) return false;
+  return true;
+}
+
+__device__ __forceinline__ float4 ld_bf16x4(const void* p, long long off) {
+  const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(p) + off);
+  const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&u.x);
+  const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
+  const float2 a = __bfloat1622float2(lo), b = __bfloat1622float2(hi);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+__device__ __forceinline__ void st_bf16x4(void* p, long long off, float4 x) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y);
+  __nv_bfloat162 hi = __floats2bfloat162_rn(x.z, x.w);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p) + off) = u;
+}
+
+__device__ __forceinline__ float f4get(const float4& v, int j) {
+  return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ void f4set(float4& v, int j, float x) {
+  if (j == 0) v.x = x;
+  else if (j == 1) v.y = x;
+  else if (j == 2) v.z = x;
+  else v.w = x;
+}
+
+// Epilogue of one warp's 32 rows [m0, m0+32) x 32 columns [n0, n0+32).
+// All 32 lanes must call it (warp-synchronous); `stg` is the warp's tile.
+__device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int split, const float (&v)[32],
+                                          float* stg) {
+  const int lane = threadIdx.x & 31;
+  if (!epi_vec_ok(a)) {  // transposed outputs: the row-per-thread layout is the coalesced one
+    epi_row32(a, m0 + lane, n0, split, v);
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    *reinterpret_cast<float4*>(stg + lane * kEpiLd + 4 * i) =
+        make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  __syncwarp();
+  const int rsub = lane >> 3, cq = (lane & 7) * 4;
+  const int n = n0 + cq;
+  float4 x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = *reinterpret_cast<const float4*>(stg + (4 * i + rsub) * kEpiLd + cq);
+  __syncwarp();  // the tile may be overwritten by the next chunk
+  const bool nfull = n + 4 <= a.N;
+  if (a.raw_partial) {
+    float* dst = a.ws + static_cast<long long>(split) * a.M * a.N;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = m0 + 4 * i + rsub;
+      if (m >= a.M || n >= a.N) continue;
+      float* p = dst + static_cast<long long>(m) * a.N + n;
+      if (nfull) {
+        *reinterpret_cast<float4*>(p) = x[i];
+      } else {
+        for (int j = 0; j < 4 && n + j < a.N; ++j) p[j] = f4get(x[i], j);
+      }
+    }
+    return;
+  }
+  const Epi& e = a.epi;
+  if (!nfull) {  // ragged right edge: scalar
+#pragma unroll 1
+    for (int i = 0; i < 8; ++i) {
+      const int m = m0 + 4 * i + rsub;
+      if (m >= a.M) continue;
+      for (int j = 0; j < 4 && n + j < a.N; ++j) epi_elem(e, m, n + j, f4get(x[i], j));
+    }
+    return;
+  }
+  // full 4-wide columns; rows may run past M
+  float4 aux[8], aux2[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    x[i].x *= e.alpha;
+    x[i].y *= e.alpha;
+    x[i].z *= e.alpha;
+    x[i].w *= e.alpha;
+  }
+  if (e.beta) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = m0 + 4 * i + rsub;
+      aux[i] = m < a.M ? *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.c) +
+                                                          static_cast<long long>(m) * e.ldc + n)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      x[i].x += aux[i].x;
+      x[i].y += aux[i].y;
+      x[i].z += aux[i].z;
+      x[i].w += aux[i].w;
+    }
+  }
+  if (e.sgd_w) {
+    // fused momentum SGD (optimizer.cpp:19-31): four rounded passes, no FMA
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = m0 + 4 * i + rsub;
+      const long long off = static_cast<long long>(m) * e.ldc + n;
+      if (m < a.M) {
+        aux[i] = *reinterpret_cast<const float4*>(e.sgd_w + off);
+        aux2[i] = *reinterpret_cast<const float4*>(e.sgd_m + off);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = m0 + 4 * i + rsub;
+      if (m >= a.M) continue;
+      const long long off = static_cast<long long>(m) * e.ldc + n;
+      float4 w4 = aux[i], m4 = aux2[i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float g = f4get(x[i], j);
+        if (e.sgd_has_gscale) g = __fmul_rn(g, e.sgd_gscale);
+        float d = __fmul_rn(f4get(m4, j), e.sgd_mu);
+        d = __fadd_rn(d, __fmul_rn(e.sgd_s1, g));
+        d = __fadd_rn(d, __fmul_rn(e.sgd_s2, f4get(w4, j)));
+        f4set(m4, j, d);
+        f4set(w4, j, __fadd_rn(f4get(w4, j), d));
+      }
+      *reinterpret_cast<float4*>(e.sgd_w + off) = w4;
+      *reinterpret_cast<float4*>(e.sgd_m + off) = m4;
+      if (e.sgd_copy) st_bf16x4(e.sgd_copy, off, w4);
+    }
+    return;
+  }
+  if (e.bias_mode == 2) {
+    const float4 bb = *reinterpret_cast<const float4*>(e.bias + n);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      x[i].x += bb.x;
+      x[i].y += bb.y;
+      x[i].z += bb.z;
+      x[i].w += bb.w;
+    }
+  } else if (e.bias_mode == 1) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = m0 + 4 * i + rsub;
+      const float bm = m < a.M ? e.bias[m] : 0.f;
+      x[i].x += bm;
+      x[i].y += bm;
+      x[i].z += bm;
+      x[i].w += bm;
+    }
+  }
+  if (e.relu) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      x[i].x = x[i].x > 0.f ? x[i].x : 0.f;
+      x[i].y = x[i].y > 0.f ? x[i].y : 0.f;
+      x[i].z = x[i].z > 0.f ? x[i].z : 0.f;
+      x[i].w = x[i].w > 0.f ? x[i].w : 0.f;
+    }
+  }
+  if (e.mask) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = m0 + 4 * i + rsub;
+      if (m >= a.M) continue;
+      const long long mo = static_cast<long long>(m) * e.ldmask + n;
+      aux[i] = e.mask_type == kBF16 ? ld_bf16x4(e.mask, mo)
+                                    : *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.mask) + mo);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (!(aux[i].x > 0.f)) x[i].x = 0.f;
+      if (!(aux[i].y > 0.f)) x[i].y = 0.f;
+      if (!(aux[i].z > 0.f)) x[i].z = 0.f;
+      if (!(aux[i].w > 0.f)) x[i].w = 0.f;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int m = m0 + 4 * i + rsub;
+    if (m >= a.M) continue;
+    const long long off = static_cast<long long>(m) * e.ldc + n;
+    if (e.c_type == kF32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(e.c) + off) = x[i];
+    } else {
+      st_bf16x4(e.c, off, x[i]);
+    }
   }
 }
 
@@ -482,7 +697,7 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t use = NACC == 2 ? static_cast<uint32_t>(local >> 1) : static_cast<uint32_t>(local);
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
-      const int m = ti.m0 + q * 32 + lane;
+      float* stg = reinterpret_cast<float*>(smem + STAGES * SB + 256) + q * 32 * kEpiLd;
       const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf) * ACOLS;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
@@ -496,7 +711,7 @@ __global__ void __launch_bounds__(192, 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (ti.n0 + c < args.N) epi_row32(args, m, ti.n0 + c, ti.split, v);
+        if (ti.n0 + c < args.N) epi_chunk(args, ti.m0 + q * 32, ti.n0 + c, ti.split, v, stg);
       }
     }
   }
@@ -516,9 +731,9 @@ __host__ __device__ constexpr uint32_t stage_bytes2(int bn) {
   return kBM * 128u + static_cast<uint32_t>(bn / 2) * 128u;
 }
 __host__ __device__ constexpr int num_stages2(int bn) {
-  return static_cast<int>((kMaxDynSmem - 2048u) / stage_bytes2(bn)) > 8
+  return static_cast<int>((kMaxDynSmem - 2048u - kEpiSmemBytes) / stage_bytes2(bn)) > 8
              ? 8
-             : static_cast<int>((kMaxDynSmem - 2048u) / stage_bytes2(bn));
+             : static_cast<int>((kMaxDynSmem - 2048u - kEpiSmemBytes) / stage_bytes2(bn));
 }
 
 template <int BN, int MATH>
@@ -681,7 +896,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const uint32_t use = static_cast<uint32_t>(local >> 1);
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
-      const int m = m0 + static_cast<int>(rank) * kBM + q * 32 + lane;
+      float* stg = reinterpret_cast<float*>(smem + STAGES * SB + 256) + q * 32 * kEpiLd;
       const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf) * ACOLS;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
@@ -695,7 +910,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (n0 + c < args.N) epi_row32(args, m, n0 + c, split, v);
+        if (n0 + c < args.N) epi_chunk(args, m0 + static_cast<int>(rank) * kBM + q * 32, n0 + c, split, v, stg);
       }
     }
   }
@@ -1022,11 +1237,11 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   if (use2) {
     const int total = cdiv(M, 2 * kBM) * cdiv(N, p.bn) * splits;
     p.grid = dim3(2 * std::min(total, 74));
-    p.smem = static_cast<size_t>(num_stages2(p.bn)) * stage_bytes2(p.bn) + 1024 + 256;
+    p.smem = static_cast<size_t>(num_stages2(p.bn)) * stage_bytes2(p.bn) + 1024 + 256 + kEpiSmemBytes;
   } else {
     const int total = cdiv(M, kBM) * cdiv(N, p.bn) * splits;
     p.grid = dim3(math == kMathF32x3 ? total : std::min(total, 148));
-    p.smem = static_cast<size_t>(num_stages(p.bn, math)) * stage_bytes(p.bn, math) + 1024 + 256;
+    p.smem = static_cast<size_t>(num_stages(p.bn, math)) * stage_bytes(p.bn, math) + 1024 + 256 + kEpiSmemBytes;
   }
   p.valid = true;
   return p;

@@ -39,14 +39,20 @@ def gemm(math, A, B, a_mn, b_mn, M, N, K, splits=1, bn=0, cta2=-1, **epi):
     ldc = (M if epi.get("c_trans") else N + 63) // 64 * 64 if not epi.get("c_trans") else (M + 63) // 64 * 64
     rows = N if epi.get("c_trans") else M
     Cb = epi.pop("C_init", None)
+    c_type = int(epi.get("c_type", 0))
     if Cb is None:
-        Cb = torch.full((rows, ldc), float("nan"), device="cuda")
+        Cb = torch.full((rows, ldc), float("nan"), device="cuda",
+                        dtype=torch.bfloat16 if c_type else torch.float32)
     d = HpGemmDesc()
     d.math = math
     d.a, d.a_mn, d.lda = Ab.data_ptr(), a_mn, lda
     d.b, d.b_mn, d.ldb = Bb.data_ptr(), b_mn, ldb
     d.M, d.N, d.K = M, N, K
-    d.c, d.ldc, d.c_type, d.c_trans = Cb.data_ptr(), ldc, 0, int(epi.get("c_trans", 0))
+    d.c, d.ldc, d.c_type, d.c_trans = Cb.data_ptr(), ldc, c_type, int(epi.get("c_trans", 0))
+    mask = epi.get("mask")
+    if mask is not None:
+        d.mask, d.ldmask = mask.data_ptr(), mask.shape[1]
+        d.mask_type = 1 if mask.dtype == torch.bfloat16 else 0
     d.alpha = epi.get("alpha", 1.0)
     d.beta = int(epi.get("beta", 0))
     bias = epi.get("bias")
@@ -136,3 +142,28 @@ def test_gemm_epilogue(math):
     assert (out[:, :N].double() - r).abs().max().item() / r.abs().max().item() < tol
     out, _ = gemm(math, A, B, 0, 0, M, N, K, c_trans=1)
     assert (out[:N, :M].double() - ref.t()).abs().max().item() / ref.abs().max().item() < tol
+
+
+@pytest.mark.parametrize("cta2", [0, 1])
+def test_gemm_epilogue_mask_bf16_ragged(cta2):
+    """ReLU-backward mask (bf16 and fp32) and bf16 output through the staged,
+    coalesced epilogue, with ragged M and N edges (rows past M, columns past N)."""
+    g = torch.Generator(device="cuda").manual_seed(4)
+    M, N, K = 300, 200, 192
+    A = torch.randn(M, K, device="cuda", generator=g)
+    B = torch.randn(N, K, device="cuda", generator=g)
+    Ar, Br = ref_inputs(0, A, B)
+    ref = Ar @ Br.t()
+    for mdt in (torch.bfloat16, torch.float32):
+        mask = torch.randn(M, 256, device="cuda", generator=g).to(mdt)
+        out, _ = gemm(0, A, B, 0, 0, M, N, K, mask=mask, cta2=cta2)
+        r = torch.where(mask[:, :N].double() > 0, ref, torch.zeros_like(ref))
+        assert (out[:, :N].double() - r).abs().max().item() / ref.abs().max().item() < 3e-5
+    out, _ = gemm(0, A, B, 1, 0, M, N, K, c_type=1, relu=1, cta2=cta2)
+    r = torch.relu(ref)
+    assert (out[:, :N].double() - r).abs().max().item() / r.abs().max().item() < 8e-3  # bf16 store
+    for n in (193, 197, 199):  # column counts that end inside a 4-wide group
+        out, _ = gemm(0, A[:, :K], B[:n], 0, 0, M, n, K, cta2=cta2)
+        r = ref[:, :n]
+        assert (out[:, :n].double() - r).abs().max().item() / r.abs().max().item() < 3e-5
+        assert torch.isnan(out[:, n:].float()).all()  # nothing written past N
