@@ -91,7 +91,9 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
       for (int i = 0; i < 32; i += 4)
         *reinterpret_cast<float4*>(dst + n0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
     } else {
-      for (int i = 0; i < 32 && n0 + i < a.N; ++i) dst[n0 + i] = v[i];
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (n0 + i < a.N) dst[n0 + i] = v[i];
     }
     return;
   }
@@ -213,6 +215,7 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
     }
     return;
   }
+#pragma unroll
   for (int i = 0; i < 32; ++i) {
     if (n0 + i < a.N) epi_elem(e, m, n0 + i, v[i]);
   }
@@ -300,18 +303,18 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int
       if (nfull) {
         *reinterpret_cast<float4*>(p) = x[i];
       } else {
-        for (int j = 0; j < 4 && n + j < a.N; ++j) p[j] = f4get(x[i], j);
+        for (int j = 0; j < 4 && n + j < a.N; ++j) p[j] = stg[(4 * i + rsub) * kEpiLd + cq + j];
       }
     }
     return;
   }
   const Epi& e = a.epi;
-  if (!nfull) {  // ragged right edge: scalar
+  if (!nfull) {  // ragged right edge: scalar, straight from the (warp-private) staged tile
 #pragma unroll 1
     for (int i = 0; i < 8; ++i) {
       const int m = m0 + 4 * i + rsub;
       if (m >= a.M) continue;
-      for (int j = 0; j < 4 && n + j < a.N; ++j) epi_elem(e, m, n + j, f4get(x[i], j));
+      for (int j = 0; j < 4 && n + j < a.N; ++j) epi_elem(e, m, n + j, stg[(4 * i + rsub) * kEpiLd + cq + j]);
     }
     return;
   }
@@ -1109,6 +1112,27 @@ int gemm_choose_bn(int M, int N) {
   return best;
 }
 
+// Split-K factor when the tile grid underfills the machine: minimise the
+// critical path, waves x (k-tiles per split + a fixed per-unit cost of ~4
+// k-tiles: pipeline fill, epilogue, partial-sum write), keeping >= 8 k-tiles
+// per split; more splits must win by >3% (partial-sum traffic). Measured on
+// the FC shapes (tests/dev/fc_bench.py): fc6/fc7 fwd pick 4, fc8 8.
+static int split_for_waves(int tiles, int kt, int slots) {
+  if (tiles >= slots * 4 / 5 || kt < 16) return 1;
+  int best = 1;
+  double best_cost = static_cast<double>(cdiv(tiles, slots)) * (kt + 4);
+  for (int s = 2; s <= std::min(64, kt / 8); ++s) {
+    const int kps = cdiv(kt, s);
+    const int real = cdiv(kt, kps);
+    const double cost = static_cast<double>(cdiv(tiles * real, slots)) * (kps + 4);
+    if (cost < best_cost * 0.97) {  // >3% better: more splits cost partial-sum traffic
+      best_cost = cost;
+      best = real;
+    }
+  }
+  return best;
+}
+
 int gemm_choose_splits(int math, int M, int N, int K, int bn) {
   if (bn <= 0) bn = gemm_choose_bn(M, N);
   const int es = math == kMathBF16 ? 2 : 4;
@@ -1122,11 +1146,7 @@ int gemm_choose_splits(int math, int M, int N, int K, int bn) {
     const int kps = cdiv(kt, splits);
     return cdiv(kt, kps);
   }
-  if (tiles >= 120 || kt < 4) return 1;
-  int splits = std::min(cdiv(148, tiles), kt / 2);
-  splits = std::max(1, std::min(splits, 64));
-  const int kps = cdiv(kt, splits);
-  return cdiv(kt, kps);
+  return split_for_waves(tiles, kt, 148);
 }
 
 static bool g_cta2_default = true;
@@ -1199,7 +1219,7 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
     p.bn = (bn == 128 || bn == 192 || bn == 256) ? bn : 256;
     if (splits <= 0) {
       const int tiles2 = cdiv(M, 2 * kBM) * cdiv(N, p.bn);
-      splits = (tiles2 >= 60 || kt < 4) ? 1 : std::max(1, std::min({cdiv(74, tiles2), kt / 2, 64}));
+      splits = split_for_waves(tiles2, kt, 74);
     }
   } else {
     p.bn = bn > 0 ? bn : gemm_choose_bn(M, N);

@@ -496,285 +496,294 @@ __device__ __forceinline__ float pow_neg(float d, float beta) {
   return exp2f(-beta * __log2f(d));  // d >= k > 0
 }
 
-// 16-byte channel vectors: V = 8 (bf16) or 4 (fp32) channels per thread, plus
-// a halo of up to LH = 4 channels each side (LRN size <= 9).
+// LRN channel halo: up to LH = 4 channels each side (LRN size <= 9).
 constexpr int LH = 4;
 
+// 4 channels per thread (C % 4 == 0), 32-bit index math.
 template <class T>
-__device__ __forceinline__ void load_vec(const T* p, float* out);
+__device__ __forceinline__ void ld4(const T* p, float* v);
 template <>
-__device__ __forceinline__ void load_vec<bf16>(const bf16* p, float* out) {
-  const uint4 u = *reinterpret_cast<const uint4*>(p);
-  const bf16* h = reinterpret_cast<const bf16*>(&u);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) out[j] = __bfloat162float(h[j]);
-}
-template <>
-__device__ __forceinline__ void load_vec<float>(const float* p, float* out) {
+__device__ __forceinline__ void ld4<float>(const float* p, float* v) {
   const float4 u = *reinterpret_cast<const float4*>(p);
-  out[0] = u.x;
-  out[1] = u.y;
-  out[2] = u.z;
-  out[3] = u.w;
+  v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
+}
+template <>
+__device__ __forceinline__ void ld4<bf16>(const bf16* p, float* v) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 template <class T>
-__device__ __forceinline__ void store_vec(T* p, const float* v);
+__device__ __forceinline__ void st4(T* p, const float* v);
 template <>
-__device__ __forceinline__ void store_vec<bf16>(bf16* p, const float* v) {
-  __align__(16) bf16 h[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) h[j] = __float2bfloat16_rn(v[j]);
-  *reinterpret_cast<uint4*>(p) = *reinterpret_cast<const uint4*>(h);
-}
-template <>
-__device__ __forceinline__ void store_vec<float>(float* p, const float* v) {
+__device__ __forceinline__ void st4<float>(float* p, const float* v) {
   *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
 }
-
-// a[-HL .. V+HL) of one pixel around channel c0 (zeros outside [0, C)).
-template <class T, int V, int HL>
-__device__ __forceinline__ void load_window(const T* px, int c0, int C, float* w) {
-  load_vec<T>(px + c0, w + HL);
-#pragma unroll
-  for (int j = 0; j < HL; ++j) {
-    const int cl = c0 - HL + j, cr = c0 + V + j;
-    w[j] = cl >= 0 ? to_f<T>(px[cl]) : 0.f;
-    w[HL + V + j] = cr < C ? to_f<T>(px[cr]) : 0.f;
-  }
+template <>
+__device__ __forceinline__ void st4<bf16>(bf16* p, const float* v) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(p) = u;
 }
 
-// LRN of channels c0..c0+V-1 from the window w (sum over [c-lo, c+hi]).
-template <int V, int HL>
-__device__ __forceinline__ void lrn_vals(const float* w, int lo, int hi, float alpha, float beta,
-                                         float kk, float* out) {
-  float sq[V + 2 * HL];
+// Max-pool forward, window argmax as a 1-byte offset r*k+q: first maximum in
+// row-major window order (strict >), a NaN wins and stops the scan.
+template <class T>
+__global__ void __launch_bounds__(256) maxpool_fwd_w_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                            uint8_t* __restrict__ widx, int H, int W, int C,
+                                                            int k, int s, int OH, int OW, int n4) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  const int G = C >> 2;
+  const int g = i % G;
+  int t = i / G;
+  const int ow = t % OW;
+  t /= OW;
+  const int oh = t % OH, b = t / OH;
+  float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  int bi[4] = {0, 0, 0, 0};
+  for (int r = 0; r < k; ++r) {
+    const T* row = x + (static_cast<long long>(b * H + oh * s + r) * W + ow * s) * C + 4 * g;
+    for (int q = 0; q < k; ++q) {
+      float v[4];
+      ld4<T>(row + q * C, v);
 #pragma unroll
-  for (int j = 0; j < V + 2 * HL; ++j) sq[j] = w[j] * w[j];
-#pragma unroll
-  for (int i = 0; i < V; ++i) {
-    float sum = 0.f;
-#pragma unroll
-    for (int d = -HL; d <= HL; ++d)
-      if (d >= -lo && d <= hi) sum += sq[HL + i + d];
-    out[i] = w[HL + i] * pow_neg(kk + alpha * sum, beta);
-  }
-}
-
-// Fused LRN + max-pool forward: thread = (pooled pixel, V-channel group).
-template <class T, int HL>
-__global__ void __launch_bounds__(256, 4) lrn_pool_fwd_kernel(const T* __restrict__ a, T* __restrict__ y,
-                                                           uint8_t* __restrict__ widx, int H, int W, int C,
-                                                           int lo, int hi, float alpha, float beta, float kk,
-                                                           int pk, int ps, int PH, int PW, int n) {
-  constexpr int V = 16 / sizeof(T);
-  const int groups = C / V;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int g = i % groups, op = i / groups;
-    const int pw = op % PW, t = op / PW, ph = t % PH, b = t / PH;
-    const int c0 = g * V;
-    float best[V];
-    int bi[V];
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      best[j] = -INFINITY;
-      bi[j] = 0;
+      for (int j = 0; j < 4; ++j)
+        if ((v[j] > best[j] || isnan(v[j])) && !isnan(best[j])) {
+          best[j] = v[j];
+          bi[j] = r * k + q;
+        }
     }
-    for (int r = 0; r < pk; ++r) {
-      const T* row = a + (static_cast<long long>(b * H + ph * ps + r) * W + pw * ps) * C;
-      for (int q = 0; q < pk; ++q) {
-        float w[V + 2 * HL], v[V];
-        load_window<T, V, HL>(row + q * C, c0, C, w);
-        lrn_vals<V, HL>(w, lo, hi, alpha, beta, kk, v);
-        const int pos = r * pk + q;
+  }
+  const long long o = static_cast<long long>(i) * 4;
+  st4<T>(y + o, best);
+  *reinterpret_cast<uint32_t*>(widx + o) =
+      static_cast<uint32_t>(bi[0]) | (bi[1] << 8) | (bi[2] << 16) | (static_cast<uint32_t>(bi[3]) << 24);
+}
+
+// Max-pool backward as a gather: each input element sums the pooled
+// gradients whose argmax it is (deterministic), optional ReLU mask.
+template <class TO, class TM>
+__global__ void __launch_bounds__(256) maxpool_bwd_w_kernel(const float* __restrict__ gy,
+                                                            const uint8_t* __restrict__ widx,
+                                                            TO* __restrict__ gx, const TM* __restrict__ mask,
+                                                            int H, int W, int C, int k, int s, int OH, int OW,
+                                                            int n4) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  const int G = C >> 2;
+  const int g = i % G;
+  int t = i / G;
+  const int w = t % W;
+  t /= W;
+  const int h = t % H, b = t / H;
+  const int oh0 = h - k + 1 <= 0 ? 0 : (h - k + s) / s;
+  const int oh1 = min(OH - 1, h / s);
+  const int ow0 = w - k + 1 <= 0 ? 0 : (w - k + s) / s;
+  const int ow1 = min(OW - 1, w / s);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int oh = oh0; oh <= oh1; ++oh)
+    for (int ow = ow0; ow <= ow1; ++ow) {
+      const long long o = (static_cast<long long>(b * OH + oh) * OW + ow) * C + 4 * g;
+      const uint32_t wi = *reinterpret_cast<const uint32_t*>(widx + o);
+      const float4 gv = *reinterpret_cast<const float4*>(gy + o);
+      const uint32_t me = static_cast<uint32_t>((h - oh * s) * k + (w - ow * s));
+      if ((wi & 0xff) == me) acc[0] += gv.x;
+      if (((wi >> 8) & 0xff) == me) acc[1] += gv.y;
+      if (((wi >> 16) & 0xff) == me) acc[2] += gv.z;
+      if ((wi >> 24) == me) acc[3] += gv.w;
+    }
+  const long long o = static_cast<long long>(i) * 4;
+  if (mask != nullptr) {
+    float m[4];
+    ld4<TM>(mask + o, m);
 #pragma unroll
-        for (int j = 0; j < V; ++j)
+    for (int j = 0; j < 4; ++j)
+      if (!(m[j] > 0.f)) acc[j] = 0.f;
+  }
+  st4<TO>(gx + o, acc);
+}
+
+// ------------------------------------------------------------------ LRN + pool, v2
+// Forward: block = (image, band of TP pooled rows). Phase 1 computes the LRN of
+// every conv-output pixel the band's windows touch ONCE (4 channels per thread,
+// the +-HL channel halo from the neighbouring 4-channel vectors, L1 hits) into a
+// fp32 smem band; phase 2 max-pools from smem (first max, strict >, NaN wins).
+// Same arithmetic, in the same order, as lrn_pool_fwd_kernel (bit-identical).
+template <class T, int HL>
+__global__ void __launch_bounds__(256) lrn_pool_fwd2_kernel(const T* __restrict__ a, T* __restrict__ y,
+                                                            uint8_t* __restrict__ widx, int H, int W, int C,
+                                                            int lo, int hi, float alpha, float beta, float kk,
+                                                            int pk, int ps, int PH, int PW, int TP) {
+  static_assert(HL <= 4, "halo");
+  extern __shared__ float4 lsm_f4[];
+  float* L = reinterpret_cast<float*>(lsm_f4);
+  const int b = blockIdx.y;
+  const int ph0 = blockIdx.x * TP, ph1 = min(PH, ph0 + TP);
+  const int r0 = ph0 * ps, r1 = (ph1 - 1) * ps + pk;
+  const int G = C >> 2;
+  const int n1 = (r1 - r0) * W * G;
+  const T* base = a + static_cast<long long>(b * H + r0) * W * C;
+  for (int i = threadIdx.x; i < n1; i += blockDim.x) {
+    const int g = i % G, pix = i / G;
+    const T* px = base + static_cast<long long>(pix) * C;
+    const int c0 = 4 * g;
+    float v[12];
+    ld4<T>(px + c0, v + 4);
+    if (c0 >= 4) {
+      ld4<T>(px + c0 - 4, v);
+    } else {
+      v[0] = v[1] = v[2] = v[3] = 0.f;
+    }
+    if (c0 + 4 < C) {
+      ld4<T>(px + c0 + 4, v + 8);
+    } else {
+      v[8] = v[9] = v[10] = v[11] = 0.f;
+    }
+    float sq[12];
+#pragma unroll
+    for (int j = 0; j < 12; ++j) sq[j] = v[j] * v[j];
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float sum = 0.f;
+#pragma unroll
+      for (int d = -HL; d <= HL; ++d)
+        if (d >= -lo && d <= hi) sum += sq[4 + j + d];
+      o[j] = v[4 + j] * pow_neg(kk + alpha * sum, beta);
+    }
+    *reinterpret_cast<float4*>(L + static_cast<long long>(pix) * C + c0) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+  __syncthreads();
+  const int n2 = (ph1 - ph0) * PW * G;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    const int g = i % G, t = i / G;
+    const int pw = t % PW, ph = ph0 + t / PW;
+    const int c0 = 4 * g;
+    float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    int bi[4] = {0, 0, 0, 0};
+    for (int r = 0; r < pk; ++r) {
+      const float* row = L + (static_cast<long long>(ph * ps - r0 + r) * W + pw * ps) * C + c0;
+      for (int q = 0; q < pk; ++q) {
+        const float4 x4 = *reinterpret_cast<const float4*>(row + q * C);
+        const float v[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
           if ((v[j] > best[j] || isnan(v[j])) && !isnan(best[j])) {
             best[j] = v[j];
-            bi[j] = pos;
+            bi[j] = r * pk + q;
           }
       }
     }
-    const long long o = static_cast<long long>(op) * C + c0;
-    store_vec<T>(y + o, best);
-    uint32_t lo4 = 0, hi4 = 0;
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      if (j < 4) lo4 |= static_cast<uint32_t>(bi[j]) << (8 * j);
-      else hi4 |= static_cast<uint32_t>(bi[j]) << (8 * (j - 4));
-    }
-    if (V == 8) {
-      *reinterpret_cast<uint2*>(widx + o) = make_uint2(lo4, hi4);
-    } else {
-      *reinterpret_cast<uint32_t*>(widx + o) = lo4;
-    }
+    const long long o = (static_cast<long long>(b * PH + ph) * PW + pw) * C + c0;
+    st4<T>(y + o, best);
+    *reinterpret_cast<uint32_t*>(widx + o) =
+        static_cast<uint32_t>(bi[0]) | (bi[1] << 8) | (bi[2] << 16) | (static_cast<uint32_t>(bi[3]) << 24);
   }
 }
 
-// Fused backward. Block = PT pixels x all C channels; thread = (pixel,
-// V-channel group). Phase 1: each thread loads its own 16-byte vector of a and
-// gathers its own pool gradient gb (vector widx / gy loads) into shared
-// memory. Phase 2: LRN backward with the channel halos read from smem:
-//   ga_c = gb_c d_c^-beta - 2 alpha beta a_c sum_{i: c in win(i)} gb_i a_i d_i^(-beta-1)
+// Backward: thread = (conv-output pixel, 4 channels), block = PT pixels x C.
+//   gb_c = sum of the pooled gradients whose argmax is this pixel (gather)
+//   d_c = k + alpha sum_{win(c)} a^2,  t_c = gb_c a_c d_c^-beta / d_c
+//   dz_c = gb_c d_c^-beta - 2 alpha beta a_c sum_{i: c in win(i)} t_i  (x ReLU mask)
+// t crosses 4-channel boundaries through a padded smem row. Same arithmetic,
+// same order, as lrn_pool_bwd_kernel.
 template <class TA, int HL>
-__global__ void __launch_bounds__(256) lrn_pool_bwd_kernel(
+__global__ void __launch_bounds__(256) lrn_pool_bwd2_kernel(
     const float* __restrict__ gy, const uint8_t* __restrict__ widx, const TA* __restrict__ a,
     TA* __restrict__ dz, int H, int W, int C, int lo, int hi, float alpha, float beta, float kk, int pk,
     int ps, int PH, int PW, int relu_mask, int npix, int PT) {
-  constexpr int V = 16 / sizeof(TA);
-  extern __shared__ float4 lsm4[];
-  float* lsm = reinterpret_cast<float*>(lsm4);
-  const int RS = C + 2 * LH;      // padded row: [LH halo | C | LH halo]
-  float* sa = lsm;                // [PT][RS]
-  float* sg = lsm + PT * RS;      // [PT][RS]
-  const int G = C / V;
+  static_assert(HL <= 4, "halo");
+  extern __shared__ float4 lsm_b4[];
+  float* T = reinterpret_cast<float*>(lsm_b4);  // [PT][C + 8]: 4-float zero halo each side
+  const int RS = C + 8;
+  const int G = C >> 2;
   const int pl = threadIdx.x / G, g = threadIdx.x - pl * G;
   const int p = blockIdx.x * PT + pl;
   const bool active = pl < PT && p < npix;
-  const int c0 = g * V;
-  if (active) {
-    float av[V], gb[V];
-    load_vec<TA>(a + static_cast<long long>(p) * C + c0, av);
-#pragma unroll
-    for (int j = 0; j < V; ++j) gb[j] = 0.f;
-    const int w = p % W, t = p / W, h = t % H, b = t / H;
-    const int oh0 = h - pk + 1 <= 0 ? 0 : (h - pk + ps) / ps;
-    const int oh1 = min(PH - 1, h / ps);
-    const int ow0 = w - pk + 1 <= 0 ? 0 : (w - pk + ps) / ps;
-    const int ow1 = min(PW - 1, w / ps);
-    for (int oh = oh0; oh <= oh1; ++oh)
-      for (int ow = ow0; ow <= ow1; ++ow) {
-        const int me = (h - oh * ps) * pk + (w - ow * ps);
-        const long long o = (static_cast<long long>(b * PH + oh) * PW + ow) * C + c0;
-        uint8_t wi[V];
-        if (V == 8) {
-          *reinterpret_cast<uint2*>(wi) = *reinterpret_cast<const uint2*>(widx + o);
-        } else {
-          *reinterpret_cast<uint32_t*>(wi) = *reinterpret_cast<const uint32_t*>(widx + o);
-        }
-        float gv[V];
-        load_vec<float>(gy + o, gv);
-        if (V == 8) load_vec<float>(gy + o + 4, gv + 4);
-#pragma unroll
-        for (int j = 0; j < V; ++j)
-          if (wi[j] == me) gb[j] += gv[j];
+  const int c0 = 4 * g;
+  float gp[4] = {0.f, 0.f, 0.f, 0.f}, ac[4] = {0.f, 0.f, 0.f, 0.f};
+  if (pl < PT) {
+    float* row = T + pl * RS;
+    if (g == 0) *reinterpret_cast<float4*>(row) = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (g == G - 1) *reinterpret_cast<float4*>(row + 4 + C) = make_float4(0.f, 0.f, 0.f, 0.f);
+    float tv[4] = {0.f, 0.f, 0.f, 0.f};
+    if (active) {
+      const TA* px = a + static_cast<long long>(p) * C;
+      float v[12];
+      ld4<TA>(px + c0, v + 4);
+      if (c0 >= 4) {
+        ld4<TA>(px + c0 - 4, v);
+      } else {
+        v[0] = v[1] = v[2] = v[3] = 0.f;
       }
-    float4* ra4 = reinterpret_cast<float4*>(sa + pl * RS + LH + c0);
-    float4* rg4 = reinterpret_cast<float4*>(sg + pl * RS + LH + c0);
+      if (c0 + 4 < C) {
+        ld4<TA>(px + c0 + 4, v + 8);
+      } else {
+        v[8] = v[9] = v[10] = v[11] = 0.f;
+      }
+      float gb[4] = {0.f, 0.f, 0.f, 0.f};
+      const int w = p % W, t = p / W, h = t % H, b = t / H;
+      const int oh0 = h - pk + 1 <= 0 ? 0 : (h - pk + ps) / ps;
+      const int oh1 = min(PH - 1, h / ps);
+      const int ow0 = w - pk + 1 <= 0 ? 0 : (w - pk + ps) / ps;
+      const int ow1 = min(PW - 1, w / ps);
+      for (int oh = oh0; oh <= oh1; ++oh)
+        for (int ow = ow0; ow <= ow1; ++ow) {
+          const long long o = (static_cast<long long>(b * PH + oh) * PW + ow) * C + c0;
+          const uint32_t wi = *reinterpret_cast<const uint32_t*>(widx + o);
+          const float4 gv = *reinterpret_cast<const float4*>(gy + o);
+          const uint32_t me = static_cast<uint32_t>((h - oh * ps) * pk + (w - ow * ps));
+          if ((wi & 0xff) == me) gb[0] += gv.x;
+          if (((wi >> 8) & 0xff) == me) gb[1] += gv.y;
+          if (((wi >> 16) & 0xff) == me) gb[2] += gv.z;
+          if ((wi >> 24) == me) gb[3] += gv.w;
+        }
+      float sq[12];
 #pragma unroll
-    for (int j = 0; j < V / 4; ++j) {
-      ra4[j] = make_float4(av[4 * j], av[4 * j + 1], av[4 * j + 2], av[4 * j + 3]);
-      rg4[j] = make_float4(gb[4 * j], gb[4 * j + 1], gb[4 * j + 2], gb[4 * j + 3]);
+      for (int j = 0; j < 12; ++j) sq[j] = v[j] * v[j];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float sum = 0.f;
+#pragma unroll
+        for (int d = -HL; d <= HL; ++d)
+          if (d >= -lo && d <= hi) sum += sq[4 + j + d];
+        const float dd = kk + alpha * sum;
+        const float pn = pow_neg(dd, beta);
+        tv[j] = gb[j] * v[4 + j] * __fdividef(pn, dd);
+        gp[j] = gb[j] * pn;
+        ac[j] = v[4 + j];
+      }
     }
+    *reinterpret_cast<float4*>(row + 4 + c0) = make_float4(tv[0], tv[1], tv[2], tv[3]);
   }
   __syncthreads();
   if (!active) return;
-  // a over [c0-4, c0+V+4) and gb over the same span, as float4 smem loads
-  // (rows carry a 4-float halo; channels outside [0, C) are zeroed). HL <= 2
-  // covers LRN size <= 5, the general path HL = 4 reads the same span twice.
-  static_assert(HL <= 4, "halo");
-  constexpr int NS = V + 8;
-  float A[NS], Gb[NS];
-  {
-    const float4* ra4 = reinterpret_cast<const float4*>(sa + pl * RS + c0);  // = channel c0-4
-    const float4* rg4 = reinterpret_cast<const float4*>(sg + pl * RS + c0);
+  const float* row = T + pl * RS + c0;  // = channel c0 - 4
+  float tt[12];
 #pragma unroll
-    for (int j = 0; j < NS / 4; ++j) {
-      const float4 x = ra4[j], y = rg4[j];
-      A[4 * j] = x.x; A[4 * j + 1] = x.y; A[4 * j + 2] = x.z; A[4 * j + 3] = x.w;
-      Gb[4 * j] = y.x; Gb[4 * j + 1] = y.y; Gb[4 * j + 2] = y.z; Gb[4 * j + 3] = y.w;
-    }
-#pragma unroll
-    for (int j = 0; j < NS; ++j) {
-      const int c = c0 - 4 + j;
-      if (c < 0 || c >= C) {
-        A[j] = 0.f;
-        Gb[j] = 0.f;
-      }
-    }
+  for (int j = 0; j < 3; ++j) {
+    const float4 x = *reinterpret_cast<const float4*>(row + 4 * j);
+    tt[4 * j] = x.x;
+    tt[4 * j + 1] = x.y;
+    tt[4 * j + 2] = x.z;
+    tt[4 * j + 3] = x.w;
   }
-  // t_i, d_i for i in [c0-HL, c0+V+HL): index j = i - (c0-4)
-  float tt[NS], dn[V];
+  float out[4];
 #pragma unroll
-  for (int j = 4 - HL; j < 4 + V + HL; ++j) {
-    float sum = 0.f;
-#pragma unroll
-    for (int d = -HL; d <= HL; ++d)
-      if (d >= -lo && d <= hi && j + d >= 0 && j + d < NS) sum += A[j + d] * A[j + d];
-    const float dd = kk + alpha * sum;
-    const float pn = pow_neg(dd, beta);
-    tt[j] = Gb[j] * A[j] * __fdividef(pn, dd);
-    if (j >= 4 && j < 4 + V) dn[j - 4] = pn;
-  }
-  float out[V];
-#pragma unroll
-  for (int k = 0; k < V; ++k) {
+  for (int k = 0; k < 4; ++k) {
     float acc = 0.f;
 #pragma unroll
     for (int d = -HL; d <= HL; ++d)
       if (d >= -hi && d <= lo) acc += tt[4 + k + d];
-    const float ai = A[4 + k];
-    float gval = Gb[4 + k] * dn[k] - 2.f * alpha * beta * ai * acc;
-    if (relu_mask && !(ai > 0.f)) gval = 0.f;
+    float gval = gp[k] - 2.f * alpha * beta * ac[k] * acc;
+    if (relu_mask && !(ac[k] > 0.f)) gval = 0.f;
     out[k] = gval;
   }
-  store_vec<TA>(dz + static_cast<long long>(p) * C + c0, out);
-}
-
-template <class T>
-__global__ void maxpool_fwd_w_kernel(const T* __restrict__ x, T* __restrict__ y,
-                                     uint8_t* __restrict__ widx, int H, int W, int C, int k, int s,
-                                     int OH, int OW, long long n) {
-  GRID_STRIDE(i, n) {
-    const int c = static_cast<int>(i % C);
-    long long t = i / C;
-    const int ow = static_cast<int>(t % OW);
-    t /= OW;
-    const int oh = static_cast<int>(t % OH);
-    const long long b = t / OH;
-    float best = -INFINITY;
-    int bi = 0;
-    bool done = false;
-    for (int r = 0; r < k && !done; ++r)
-      for (int q = 0; q < k; ++q) {
-        const float v = to_f<T>(x[((b * H + oh * s + r) * W + ow * s + q) * C + c]);
-        if (v > best || isnan(v)) {
-          best = v;
-          bi = r * k + q;
-          if (isnan(v)) {
-            done = true;
-            break;
-          }
-        }
-      }
-    y[i] = from_f<T>(best);
-    widx[i] = static_cast<uint8_t>(bi);
-  }
-}
-
-template <class TO, class TM>
-__global__ void maxpool_bwd_w_kernel(const float* __restrict__ gy, const uint8_t* __restrict__ widx,
-                                     TO* __restrict__ gx, const TM* __restrict__ mask, int H, int W,
-                                     int C, int k, int s, int OH, int OW, long long n) {
-  GRID_STRIDE(i, n) {
-    const int c = static_cast<int>(i % C);
-    long long t = i / C;
-    const int w = static_cast<int>(t % W);
-    t /= W;
-    const int h = static_cast<int>(t % H);
-    const long long b = t / H;
-    const int oh0 = h - k + 1 <= 0 ? 0 : (h - k + s) / s;
-    const int oh1 = min(OH - 1, h / s);
-    const int ow0 = w - k + 1 <= 0 ? 0 : (w - k + s) / s;
-    const int ow1 = min(OW - 1, w / s);
-    float acc = 0.f;
-    for (int oh = oh0; oh <= oh1; ++oh)
-      for (int ow = ow0; ow <= ow1; ++ow) {
-        const long long o = ((b * OH + oh) * OW + ow) * C + c;
-        if (widx[o] == (h - oh * s) * k + (w - ow * s)) acc += gy[o];
-      }
-    if (mask != nullptr && !(to_f<TM>(mask[i]) > 0.f)) acc = 0.f;
-    gx[i] = from_f<TO>(acc);
-  }
+  st4<TA>(dz + static_cast<long long>(p) * C + c0, out);
 }
 
 template <class T>
@@ -828,16 +837,31 @@ template <class T>
 void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, int C, int n,
                          float alpha, float beta, float kk, int pk, int ps, int PH, int PW,
                          cudaStream_t st) {
-  constexpr int V = 16 / sizeof(T);
-  if (C % V != 0 || n > 2 * LH + 1) throw std::runtime_error("lrn_pool: C must be a multiple of 16 bytes, size <= 9");
-  const long long total = static_cast<long long>(B) * PH * PW * (C / V);
-  if (static_cast<long long>(B) * H * W >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
+  if (C % 4 != 0 || n > 2 * LH + 1) throw std::runtime_error("lrn_pool: C must be a multiple of 4, size <= 9");
+  if (static_cast<long long>(B) * H * W * C >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
+  // pooled rows per block: the fp32 LRN band ((TP-1)*ps+pk rows) within ~110 KB
+  const long long row_bytes = static_cast<long long>(W) * C * sizeof(float);
+  int TP = 1;
+  while (TP < PH && (static_cast<long long>(TP) * ps + pk) * row_bytes <= 112 * 1024) ++TP;
+  const size_t smem = static_cast<size_t>(((TP - 1) * ps + pk) * row_bytes);
+  if (smem > 220 * 1024) throw std::runtime_error("lrn_pool: conv row too wide for the smem band");
+  const dim3 grid((PH + TP - 1) / TP, B);
   if (n <= 5) {
-    lrn_pool_fwd_kernel<T, 2><<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(
-        a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, static_cast<int>(total));
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(lrn_pool_fwd2_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      attr = true;
+    }
+    lrn_pool_fwd2_kernel<T, 2><<<grid, 256, smem, st>>>(a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk,
+                                                       pk, ps, PH, PW, TP);
   } else {
-    lrn_pool_fwd_kernel<T, LH><<<grid_for(total, 256, 148 * 16), 256, 0, st>>>(
-        a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, static_cast<int>(total));
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(lrn_pool_fwd2_kernel<T, LH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      attr = true;
+    }
+    lrn_pool_fwd2_kernel<T, LH><<<grid, 256, smem, st>>>(a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta,
+                                                        kk, pk, ps, PH, PW, TP);
   }
 }
 
@@ -845,35 +869,41 @@ template <class TA>
 void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* dz, int B, int H,
                          int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
                          int PH, int PW, int relu_mask, cudaStream_t st) {
-  constexpr int V = 16 / sizeof(TA);
-  if (C % V != 0 || n > 2 * LH + 1 || C / V > 256)
-    throw std::runtime_error("lrn_pool: C must be a multiple of 16 bytes, size <= 9");
+  if (C % 4 != 0 || n > 2 * LH + 1 || C / 4 > 256)
+    throw std::runtime_error("lrn_pool: C must be a multiple of 4 (at most 1024), size <= 9");
   const long long npix = static_cast<long long>(B) * H * W;
   if (npix * C >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
-  const int G = C / V;
+  const int G = C / 4;
   const int PT = std::max(1, 256 / G);
   const int threads = PT * G;
-  const size_t smem = static_cast<size_t>(2) * PT * (C + 2 * LH) * sizeof(float);
+  const size_t smem = static_cast<size_t>(PT) * (C + 8) * sizeof(float);
   const long long blocks = (npix + PT - 1) / PT;
-  if (n > 5) throw std::runtime_error("lrn_pool backward: LRN size > 5 not supported yet");
-  lrn_pool_bwd_kernel<TA, 2><<<static_cast<unsigned>(blocks), threads, smem, st>>>(
-      gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, relu_mask,
-      static_cast<int>(npix), PT);
+  if (n <= 5) {
+    lrn_pool_bwd2_kernel<TA, 2><<<static_cast<unsigned>(blocks), threads, smem, st>>>(
+        gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, relu_mask,
+        static_cast<int>(npix), PT);
+  } else {
+    lrn_pool_bwd2_kernel<TA, LH><<<static_cast<unsigned>(blocks), threads, smem, st>>>(
+        gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, relu_mask,
+        static_cast<int>(npix), PT);
+  }
 }
 
 template <class T>
 void launch_maxpool_fwd_w(const T* x, T* y, uint8_t* widx, int B, int H, int W, int C, int k, int s,
                           int OH, int OW, cudaStream_t st) {
-  const long long n = static_cast<long long>(B) * OH * OW * C;
-  maxpool_fwd_w_kernel<T><<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(x, y, widx, H, W, C, k, s, OH, OW, n);
+  if (C % 4 != 0) throw std::runtime_error("maxpool: channels must be a multiple of 4");
+  const int n4 = static_cast<int>(static_cast<long long>(B) * OH * OW * C / 4);
+  maxpool_fwd_w_kernel<T><<<(n4 + 255) / 256, 256, 0, st>>>(x, y, widx, H, W, C, k, s, OH, OW, n4);
 }
 
 template <class TO, class TM>
 void launch_maxpool_bwd_w(const float* gy, const uint8_t* widx, TO* gx, const TM* mask, int B, int H,
                           int W, int C, int k, int s, int OH, int OW, cudaStream_t st) {
-  const long long n = static_cast<long long>(B) * H * W * C;
-  maxpool_bwd_w_kernel<TO, TM><<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(gy, widx, gx, mask, H, W, C, k,
-                                                                           s, OH, OW, n);
+  if (C % 4 != 0) throw std::runtime_error("maxpool: channels must be a multiple of 4");
+  const int n4 = static_cast<int>(static_cast<long long>(B) * H * W * C / 4);
+  maxpool_bwd_w_kernel<TO, TM><<<(n4 + 255) / 256, 256, 0, st>>>(gy, widx, gx, mask, H, W, C, k, s, OH, OW,
+                                                                 n4);
 }
 
 template <class T>
