@@ -518,8 +518,11 @@ __device__ __forceinline__ TileIdx tile_idx(const GemmArgs& a, int t, int tiles_
   return r;
 }
 
-template <int BN, int MATH>
-__global__ void __launch_bounds__(192, 1)
+// LIGHT: short-K GEMMs whose epilogue is the work (FC wgrad + fused SGD, K =
+// 128): 2 stages, one accumulator, two CTAs per SM -- twice the epilogue warps
+// (memory-level parallelism) per SM.
+template <int BN, int MATH, bool LIGHT>
+__global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                 const GemmArgs args) {
   constexpr bool SPLIT = MATH == kMathF32x3;
@@ -530,8 +533,8 @@ __global__ void __launch_bounds__(192, 1)
   constexpr uint32_t A_BYTES = kBM * 128;
   constexpr uint32_t B_BYTES = BN * 128;
   constexpr uint32_t SB = stage_bytes(BN, MATH);
-  constexpr int STAGES = num_stages(BN, MATH);
-  constexpr int NACC = SPLIT ? 1 : 2;
+  constexpr int STAGES = LIGHT ? 2 : num_stages(BN, MATH);
+  constexpr int NACC = (SPLIT || LIGHT) ? 1 : 2;
   constexpr uint32_t ACOLS = tmem_cols(BN);
   constexpr uint32_t TCOLS = ACOLS * NACC;
 
@@ -1053,15 +1056,15 @@ void launch_inst2(const GemmPlan& p, cudaStream_t s) {
   gemm2_kernel<BN, MATH><<<p.grid, 192, p.smem, s>>>(p.ta, p.tb, p.args);
 }
 
-template <int BN, int MATH>
+template <int BN, int MATH, bool LIGHT>
 void launch_inst(const GemmPlan& p, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_kernel<BN, MATH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(p.smem));
+    cudaFuncSetAttribute(gemm_kernel<BN, MATH, LIGHT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kMaxDynSmem));
     attr = true;
   }
-  gemm_kernel<BN, MATH><<<p.grid, 192, p.smem, s>>>(p.ta, p.tb, p.args);
+  gemm_kernel<BN, MATH, LIGHT><<<p.grid, 192, p.smem, s>>>(p.ta, p.tb, p.args);
 }
 
 template <int MATH>
@@ -1077,11 +1080,20 @@ void launch_math(const GemmPlan& p, cudaStream_t s) {
     }
     throw std::runtime_error("gemm: unsupported 2-CTA configuration");
   }
+  if (p.light) {
+    if constexpr (MATH != kMathF32x3) {
+      if (p.bn == 128) {
+        launch_inst<128, MATH, true>(p, s);
+        return;
+      }
+    }
+    throw std::runtime_error("gemm: unsupported light configuration");
+  }
   switch (p.bn) {
-    case 64: launch_inst<64, MATH>(p, s); break;
-    case 128: launch_inst<128, MATH>(p, s); break;
-    case 192: launch_inst<192, MATH>(p, s); break;
-    case 256: launch_inst<256, MATH>(p, s); break;
+    case 64: launch_inst<64, MATH, false>(p, s); break;
+    case 128: launch_inst<128, MATH, false>(p, s); break;
+    case 192: launch_inst<192, MATH, false>(p, s); break;
+    case 256: launch_inst<256, MATH, false>(p, s); break;
     default: throw std::runtime_error("gemm: unsupported BN");
   }
 }
@@ -1194,6 +1206,8 @@ static TileChoice choose_tile(int math, const GemmOperand& b, int M, int N) {
   return best;
 }
 
+static bool light_ok(int math, int kt, int splits) { return math != kMathF32x3 && kt <= 4 && splits == 1; }
+
 GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
                    const Epi& epi, int splits, float* ws, int bn, int cta2) {
   if (M <= 0 || N <= 0 || K <= 0) throw std::runtime_error("gemm: empty problem");
@@ -1206,7 +1220,9 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   if (bn <= 0 && g_force_bn > 0) bn = g_force_bn;
   if (cta2 == 1 && math == kMathF32x3) throw std::runtime_error("gemm: 3xTF32 has no 2-CTA kernel");
   bool use2;
-  if (cta2 == -1 && bn <= 0) {
+  if (cta2 == -1 && bn <= 0 && light_ok(math, kt, 1)) {
+    use2 = false;  // light single-CTA kernel (below)
+  } else if (cta2 == -1 && bn <= 0) {
     const TileChoice tc = choose_tile(math, b, M, N);
     use2 = tc.cta2;
     bn = tc.bn;
@@ -1224,6 +1240,10 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   } else {
     p.bn = bn > 0 ? bn : gemm_choose_bn(M, N);
     if (splits <= 0) splits = gemm_choose_splits(math, M, N, K, p.bn);
+    // short K (FC wgrad, K = n): the epilogue (gradient store or fused SGD
+    // update) is the work -> the 2-CTA/SM light kernel
+    p.light = light_ok(math, kt, splits) && cta2 != 1 && (bn <= 0 || bn == 128);
+    if (p.light) p.bn = 128;
   }
   const int kps = cdiv(kt, splits);
   splits = cdiv(kt, kps);
@@ -1260,8 +1280,9 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
     p.smem = static_cast<size_t>(num_stages2(p.bn)) * stage_bytes2(p.bn) + 1024 + 256 + kEpiSmemBytes;
   } else {
     const int total = cdiv(M, kBM) * cdiv(N, p.bn) * splits;
-    p.grid = dim3(math == kMathF32x3 ? total : std::min(total, 148));
-    p.smem = static_cast<size_t>(num_stages(p.bn, math)) * stage_bytes(p.bn, math) + 1024 + 256 + kEpiSmemBytes;
+    p.grid = dim3(math == kMathF32x3 ? total : std::min(total, p.light ? 296 : 148));
+    p.smem = static_cast<size_t>(p.light ? 2 : num_stages(p.bn, math)) * stage_bytes(p.bn, math) + 1024 + 256 +
+             kEpiSmemBytes;
   }
   p.valid = true;
   return p;

@@ -94,6 +94,7 @@ struct GemmPlan {
   int bn = 128;
   int splits = 1;
   bool cta2 = false;  // CTA-pair kernel (M=256 tiles, cta_group::2)
+  bool light = false; // 2-stage, 1-accumulator, 2-CTA/SM kernel (short K, fused SGD epilogue)
   dim3 grid;
   size_t smem = 0;
   bool valid = false;

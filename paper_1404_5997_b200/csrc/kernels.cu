@@ -492,8 +492,12 @@ __global__ void __launch_bounds__(256) im2col_t_nchw_kernel(const float* __restr
 }
 
 // ------------------------------------------------------------------ fused LRN + pool
+// d^-beta for d >= k > 0: MUFU lg2 / ex2 (approx, ~2 ulp), no range fix-ups.
 __device__ __forceinline__ float pow_neg(float d, float beta) {
-  return exp2f(-beta * __log2f(d));  // d >= k > 0
+  float l, r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(d));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-beta * l));
+  return r;
 }
 
 // LRN channel halo: up to LH = 4 channels each side (LRN size <= 9).
@@ -607,183 +611,223 @@ __global__ void __launch_bounds__(256) maxpool_bwd_w_kernel(const float* __restr
   st4<TO>(gx + o, acc);
 }
 
-// ------------------------------------------------------------------ LRN + pool, v2
-// Forward: block = (image, band of TP pooled rows). Phase 1 computes the LRN of
-// every conv-output pixel the band's windows touch ONCE (4 channels per thread,
-// the +-HL channel halo from the neighbouring 4-channel vectors, L1 hits) into a
-// fp32 smem band; phase 2 max-pools from smem (first max, strict >, NaN wins).
-// Same arithmetic, in the same order, as lrn_pool_fwd_kernel (bit-identical).
-template <class T, int HL>
-__global__ void __launch_bounds__(256) lrn_pool_fwd2_kernel(const T* __restrict__ a, T* __restrict__ y,
-                                                            uint8_t* __restrict__ widx, int H, int W, int C,
-                                                            int lo, int hi, float alpha, float beta, float kk,
-                                                            int pk, int ps, int PH, int PW, int TP) {
-  static_assert(HL <= 4, "halo");
-  extern __shared__ float4 lsm_f4[];
-  float* L = reinterpret_cast<float*>(lsm_f4);
-  const int b = blockIdx.y;
-  const int ph0 = blockIdx.x * TP, ph1 = min(PH, ph0 + TP);
-  const int r0 = ph0 * ps, r1 = (ph1 - 1) * ps + pk;
-  const int G = C >> 2;
-  const int n1 = (r1 - r0) * W * G;
-  const T* base = a + static_cast<long long>(b * H + r0) * W * C;
-  for (int i = threadIdx.x; i < n1; i += blockDim.x) {
-    const int g = i % G, pix = i / G;
-    const T* px = base + static_cast<long long>(pix) * C;
-    const int c0 = 4 * g;
-    float v[12];
-    ld4<T>(px + c0, v + 4);
-    if (c0 >= 4) {
-      ld4<T>(px + c0 - 4, v);
-    } else {
-      v[0] = v[1] = v[2] = v[3] = 0.f;
-    }
-    if (c0 + 4 < C) {
-      ld4<T>(px + c0 + 4, v + 8);
-    } else {
-      v[8] = v[9] = v[10] = v[11] = 0.f;
-    }
-    float sq[12];
+// ------------------------------------------------------------------ LRN + pool
+// 16-byte channel vectors: V = 8 (bf16) or 4 (fp32) channels per thread.
+template <class T>
+__device__ __forceinline__ void ldv(const T* p, float* v) {
 #pragma unroll
-    for (int j = 0; j < 12; ++j) sq[j] = v[j] * v[j];
-    float o[4];
+  for (int j = 0; j < 16 / static_cast<int>(sizeof(T)); j += 4) ld4<T>(p + j, v + j);
+}
+template <class T>
+__device__ __forceinline__ void stv(T* p, const float* v) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float sum = 0.f;
-#pragma unroll
-      for (int d = -HL; d <= HL; ++d)
-        if (d >= -lo && d <= hi) sum += sq[4 + j + d];
-      o[j] = v[4 + j] * pow_neg(kk + alpha * sum, beta);
-    }
-    *reinterpret_cast<float4*>(L + static_cast<long long>(pix) * C + c0) = make_float4(o[0], o[1], o[2], o[3]);
-  }
-  __syncthreads();
-  const int n2 = (ph1 - ph0) * PW * G;
-  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-    const int g = i % G, t = i / G;
-    const int pw = t % PW, ph = ph0 + t / PW;
-    const int c0 = 4 * g;
-    float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-    int bi[4] = {0, 0, 0, 0};
-    for (int r = 0; r < pk; ++r) {
-      const float* row = L + (static_cast<long long>(ph * ps - r0 + r) * W + pw * ps) * C + c0;
-      for (int q = 0; q < pk; ++q) {
-        const float4 x4 = *reinterpret_cast<const float4*>(row + q * C);
-        const float v[4] = {x4.x, x4.y, x4.z, x4.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if ((v[j] > best[j] || isnan(v[j])) && !isnan(best[j])) {
-            best[j] = v[j];
-            bi[j] = r * pk + q;
-          }
-      }
-    }
-    const long long o = (static_cast<long long>(b * PH + ph) * PW + pw) * C + c0;
-    st4<T>(y + o, best);
-    *reinterpret_cast<uint32_t*>(widx + o) =
-        static_cast<uint32_t>(bi[0]) | (bi[1] << 8) | (bi[2] << 16) | (static_cast<uint32_t>(bi[3]) << 24);
-  }
+  for (int j = 0; j < 16 / static_cast<int>(sizeof(T)); j += 4) st4<T>(p + j, v + j);
 }
 
-// Backward: thread = (conv-output pixel, 4 channels), block = PT pixels x C.
-//   gb_c = sum of the pooled gradients whose argmax is this pixel (gather)
-//   d_c = k + alpha sum_{win(c)} a^2,  t_c = gb_c a_c d_c^-beta / d_c
-//   dz_c = gb_c d_c^-beta - 2 alpha beta a_c sum_{i: c in win(i)} t_i  (x ReLU mask)
-// t crosses 4-channel boundaries through a padded smem row. Same arithmetic,
-// same order, as lrn_pool_bwd_kernel.
-template <class TA, int HL>
-__global__ void __launch_bounds__(256) lrn_pool_bwd2_kernel(
-    const float* __restrict__ gy, const uint8_t* __restrict__ widx, const TA* __restrict__ a,
-    TA* __restrict__ dz, int H, int W, int C, int lo, int hi, float alpha, float beta, float kk, int pk,
-    int ps, int PH, int PW, int relu_mask, int npix, int PT) {
-  static_assert(HL <= 4, "halo");
-  extern __shared__ float4 lsm_b4[];
-  float* T = reinterpret_cast<float*>(lsm_b4);  // [PT][C + 8]: 4-float zero halo each side
-  const int RS = C + 8;
-  const int G = C >> 2;
-  const int pl = threadIdx.x / G, g = threadIdx.x - pl * G;
-  const int p = blockIdx.x * PT + pl;
-  const bool active = pl < PT && p < npix;
-  const int c0 = 4 * g;
-  float gp[4] = {0.f, 0.f, 0.f, 0.f}, ac[4] = {0.f, 0.f, 0.f, 0.f};
-  if (pl < PT) {
-    float* row = T + pl * RS;
-    if (g == 0) *reinterpret_cast<float4*>(row) = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (g == G - 1) *reinterpret_cast<float4*>(row + 4 + C) = make_float4(0.f, 0.f, 0.f, 0.f);
-    float tv[4] = {0.f, 0.f, 0.f, 0.f};
-    if (active) {
-      const TA* px = a + static_cast<long long>(p) * C;
-      float v[12];
-      ld4<TA>(px + c0, v + 4);
+// Forward: block = (band of TP pooled rows, image), threads = (channel
+// vector g, pixel lane). Phase 1 computes the LRN of every conv-output pixel
+// the band's windows touch ONCE into a fp32 smem band (channel halo from the
+// neighbouring vectors, L1 hits); phase 2 max-pools from smem (first max,
+// strict >, NaN wins). No per-thread integer division.
+//   y_c = a_c (k + alpha sum_{i in [c-lo, c+hi]} a_i^2)^-beta
+// NL/PK/PS > 0: LRN size and pool window/stride fixed at compile time (the
+// AlexNet 5 / 3 / 2 fast path); 0: taken from the arguments.
+template <class T, int HL, int NL, int PK, int PS>
+__global__ void __launch_bounds__(1024) lrn_pool_fwd_kernel(const T* __restrict__ a, T* __restrict__ y,
+                                                            uint8_t* __restrict__ widx, int H, int W, int C,
+                                                            int lo_, int hi_, float alpha, float beta, float kk,
+                                                            int pk_, int ps_, int PH, int PW, int TP) {
+  static_assert(HL <= 4 && 2 * HL + 1 >= NL, "halo");
+  const int lo = NL ? NL / 2 : lo_, hi = NL ? (NL - 1) / 2 : hi_;
+  const int pk = PK ? PK : pk_, ps = PS ? PS : ps_;
+  constexpr int V = 16 / sizeof(T);
+  extern __shared__ float4 lsm_f4[];
+  float* L = reinterpret_cast<float*>(lsm_f4);
+  const int g = threadIdx.x, ty = threadIdx.y, NY = blockDim.y;
+  const int c0 = g * V;
+  const int b = blockIdx.y;
+  const int ph0 = blockIdx.x * TP, ph1 = min(PH, ph0 + TP);
+  const int r0 = ph0 * ps, npx = ((ph1 - 1) * ps + pk - r0) * W;
+  const T* base = a + static_cast<long long>(b * H + r0) * W * C + c0;
+  constexpr int U = 2;  // pixels per pass: their loads are in flight together
+  for (int p0 = ty; p0 < npx; p0 += U * NY) {
+    float v[U][V + 8];  // channels [c0-4, c0+V+4)
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int p = p0 + u * NY;
+      if (p >= npx) break;
+      const T* px = base + static_cast<long long>(p) * C;
+      ldv<T>(px, v[u] + 4);
       if (c0 >= 4) {
-        ld4<TA>(px + c0 - 4, v);
+        ld4<T>(px - 4, v[u]);
       } else {
-        v[0] = v[1] = v[2] = v[3] = 0.f;
+        v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0.f;
       }
-      if (c0 + 4 < C) {
-        ld4<TA>(px + c0 + 4, v + 8);
+      if (c0 + V < C) {
+        ld4<T>(px + V, v[u] + 4 + V);
       } else {
-        v[8] = v[9] = v[10] = v[11] = 0.f;
+        v[u][4 + V] = v[u][5 + V] = v[u][6 + V] = v[u][7 + V] = 0.f;
       }
-      float gb[4] = {0.f, 0.f, 0.f, 0.f};
-      const int w = p % W, t = p / W, h = t % H, b = t / H;
-      const int oh0 = h - pk + 1 <= 0 ? 0 : (h - pk + ps) / ps;
-      const int oh1 = min(PH - 1, h / ps);
-      const int ow0 = w - pk + 1 <= 0 ? 0 : (w - pk + ps) / ps;
-      const int ow1 = min(PW - 1, w / ps);
-      for (int oh = oh0; oh <= oh1; ++oh)
-        for (int ow = ow0; ow <= ow1; ++ow) {
-          const long long o = (static_cast<long long>(b * PH + oh) * PW + ow) * C + c0;
-          const uint32_t wi = *reinterpret_cast<const uint32_t*>(widx + o);
-          const float4 gv = *reinterpret_cast<const float4*>(gy + o);
-          const uint32_t me = static_cast<uint32_t>((h - oh * ps) * pk + (w - ow * ps));
-          if ((wi & 0xff) == me) gb[0] += gv.x;
-          if (((wi >> 8) & 0xff) == me) gb[1] += gv.y;
-          if (((wi >> 16) & 0xff) == me) gb[2] += gv.z;
-          if ((wi >> 24) == me) gb[3] += gv.w;
-        }
-      float sq[12];
+    }
 #pragma unroll
-      for (int j = 0; j < 12; ++j) sq[j] = v[j] * v[j];
+    for (int u = 0; u < U; ++u) {
+      const int p = p0 + u * NY;
+      if (p >= npx) break;
+      float sq[V + 8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < V + 8; ++j) sq[j] = v[u][j] * v[u][j];
+      float o[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
         float sum = 0.f;
 #pragma unroll
         for (int d = -HL; d <= HL; ++d)
           if (d >= -lo && d <= hi) sum += sq[4 + j + d];
-        const float dd = kk + alpha * sum;
-        const float pn = pow_neg(dd, beta);
-        tv[j] = gb[j] * v[4 + j] * __fdividef(pn, dd);
-        gp[j] = gb[j] * pn;
-        ac[j] = v[4 + j];
+        o[j] = v[u][4 + j] * pow_neg(kk + alpha * sum, beta);
       }
+      float* dst = L + static_cast<long long>(p) * C + c0;
+#pragma unroll
+      for (int j = 0; j < V; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
     }
-    *reinterpret_cast<float4*>(row + 4 + c0) = make_float4(tv[0], tv[1], tv[2], tv[3]);
   }
   __syncthreads();
-  if (!active) return;
-  const float* row = T + pl * RS + c0;  // = channel c0 - 4
-  float tt[12];
+  for (int ph = ph0; ph < ph1; ++ph)
+    for (int pw = ty; pw < PW; pw += NY) {
+      float best[V];
+      int bi[V];
 #pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    const float4 x = *reinterpret_cast<const float4*>(row + 4 * j);
-    tt[4 * j] = x.x;
-    tt[4 * j + 1] = x.y;
-    tt[4 * j + 2] = x.z;
-    tt[4 * j + 3] = x.w;
+      for (int j = 0; j < V; ++j) {
+        best[j] = -INFINITY;
+        bi[j] = 0;
+      }
+      for (int r = 0; r < pk; ++r) {
+        const float* row = L + (static_cast<long long>(ph * ps - r0 + r) * W + pw * ps) * C + c0;
+        for (int q = 0; q < pk; ++q) {
+          float v[V];
+#pragma unroll
+          for (int j = 0; j < V; j += 4) {
+            const float4 x4 = *reinterpret_cast<const float4*>(row + q * C + j);
+            v[j] = x4.x; v[j + 1] = x4.y; v[j + 2] = x4.z; v[j + 3] = x4.w;
+          }
+#pragma unroll
+          for (int j = 0; j < V; ++j)
+            if ((v[j] > best[j] || isnan(v[j])) && !isnan(best[j])) {
+              best[j] = v[j];
+              bi[j] = r * pk + q;
+            }
+        }
+      }
+      const long long o = (static_cast<long long>(b * PH + ph) * PW + pw) * C + c0;
+      stv<T>(y + o, best);
+#pragma unroll
+      for (int j = 0; j < V; j += 4)
+        *reinterpret_cast<uint32_t*>(widx + o + j) = static_cast<uint32_t>(bi[j]) | (bi[j + 1] << 8) |
+                                                     (bi[j + 2] << 16) | (static_cast<uint32_t>(bi[j + 3]) << 24);
+    }
+}
+
+// Backward: block = one conv-output row (b, h) x all channels, threads =
+// (channel vector g, column w); the pooled-row range is block-uniform.
+//   gb_c = sum of the pooled gradients whose argmax is this pixel (gather)
+//   d_c = k + alpha sum_{win(c)} a^2,  t_c = gb_c a_c d_c^-beta / d_c
+//   dz_c = gb_c d_c^-beta - 2 alpha beta a_c sum_{i: c in win(i)} t_i  (x ReLU mask)
+// a and t cross the vector boundaries through zero-haloed smem rows.
+template <class TA, int HL, int NL, int PK, int PS>
+__global__ void __launch_bounds__(512) lrn_pool_bwd_kernel(
+    const float* __restrict__ gy, const uint8_t* __restrict__ widx, const TA* __restrict__ a,
+    TA* __restrict__ dz, int H, int W, int C, int lo_, int hi_, float alpha, float beta, float kk, int pk_,
+    int ps_, int PH, int PW, int relu_mask) {
+  static_assert(HL <= 4 && 2 * HL + 1 >= NL, "halo");
+  const int lo = NL ? NL / 2 : lo_, hi = NL ? (NL - 1) / 2 : hi_;
+  const int pk = PK ? PK : pk_, ps = PS ? PS : ps_;
+  constexpr int V = 16 / sizeof(TA);
+  extern __shared__ float4 lsm_b4[];
+  const int RS = C + 8;
+  float* sA = reinterpret_cast<float*>(lsm_b4);  // [blockDim.y][RS]: 4-float zero halo each side
+  float* sT = sA + blockDim.y * RS;                // [blockDim.y][RS]
+  const int g = threadIdx.x, G = blockDim.x;
+  const int c0 = g * V;
+  const int nb = gridDim.x;  // column blocks per row
+  const int w = blockIdx.x * blockDim.y + threadIdx.y;
+  const bool live = w < W;  // idle lanes still take part in the barriers
+  const int b = blockIdx.z, h = blockIdx.y;
+  (void)nb;
+  const int px = ((b * H + h) * W + (live ? w : 0)) * C + c0;
+  const int oh0 = h - pk + 1 <= 0 ? 0 : (h - pk + ps) / ps;
+  const int oh1 = min(PH - 1, h / ps);
+  const int ow0 = w - pk + 1 <= 0 ? 0 : (w - pk + ps) / ps;
+  const int ow1 = live ? min(PW - 1, w / ps) : -1;
+  float av[V], gb[V];
+  ldv<TA>(a + px, av);
+#pragma unroll
+  for (int j = 0; j < V; ++j) gb[j] = 0.f;
+  for (int oh = oh0; oh <= oh1; ++oh)
+    for (int ow = ow0; ow <= ow1; ++ow) {
+      const int o = ((b * PH + oh) * PW + ow) * C + c0;
+      const uint32_t me = static_cast<uint32_t>((h - oh * ps) * pk + (w - ow * ps));
+#pragma unroll
+      for (int j = 0; j < V; j += 4) {
+        const uint32_t wi = *reinterpret_cast<const uint32_t*>(widx + o + j);
+        const float4 gv = *reinterpret_cast<const float4*>(gy + o + j);
+        if ((wi & 0xff) == me) gb[j] += gv.x;
+        if (((wi >> 8) & 0xff) == me) gb[j + 1] += gv.y;
+        if (((wi >> 16) & 0xff) == me) gb[j + 2] += gv.z;
+        if ((wi >> 24) == me) gb[j + 3] += gv.w;
+      }
+    }
+  float* ra = sA + threadIdx.y * RS;
+  float* rt = sT + threadIdx.y * RS;
+#pragma unroll
+  for (int j = 0; j < V; j += 4) *reinterpret_cast<float4*>(ra + 4 + c0 + j) = make_float4(av[j], av[j + 1], av[j + 2], av[j + 3]);
+  if (g == 0) {
+    *reinterpret_cast<float4*>(ra) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(rt) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  float out[4];
+  if (g == G - 1) {
+    *reinterpret_cast<float4*>(ra + 4 + C) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(rt + 4 + C) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  float win[V + 8];  // a over channels [c0-4, c0+V+4)
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int j = 0; j < V + 8; j += 4) {
+    const float4 x = *reinterpret_cast<const float4*>(ra + c0 + j);
+    win[j] = x.x; win[j + 1] = x.y; win[j + 2] = x.z; win[j + 3] = x.w;
+  }
+  float gp[V], tv[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    float sum = 0.f;
+#pragma unroll
+    for (int d = -HL; d <= HL; ++d)
+      if (d >= -lo && d <= hi) sum += win[4 + j + d] * win[4 + j + d];
+    const float dd = kk + alpha * sum;
+    const float pn = pow_neg(dd, beta);
+    float rd;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(dd));
+    tv[j] = gb[j] * av[j] * (pn * rd);
+    gp[j] = gb[j] * pn;
+  }
+#pragma unroll
+  for (int j = 0; j < V; j += 4) *reinterpret_cast<float4*>(rt + 4 + c0 + j) = make_float4(tv[j], tv[j + 1], tv[j + 2], tv[j + 3]);
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < V + 8; j += 4) {
+    const float4 x = *reinterpret_cast<const float4*>(rt + c0 + j);
+    win[j] = x.x; win[j + 1] = x.y; win[j + 2] = x.z; win[j + 3] = x.w;
+  }
+  float out[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
     float acc = 0.f;
 #pragma unroll
     for (int d = -HL; d <= HL; ++d)
-      if (d >= -hi && d <= lo) acc += tt[4 + k + d];
-    float gval = gp[k] - 2.f * alpha * beta * ac[k] * acc;
-    if (relu_mask && !(ac[k] > 0.f)) gval = 0.f;
+      if (d >= -hi && d <= lo) acc += win[4 + k + d];
+    float gval = gp[k] - 2.f * alpha * beta * av[k] * acc;
+    if (relu_mask && !(av[k] > 0.f)) gval = 0.f;
     out[k] = gval;
   }
-  st4<TA>(dz + static_cast<long long>(p) * C + c0, out);
+  if (live) stv<TA>(dz + px, out);
 }
 
 template <class T>
@@ -837,31 +881,29 @@ template <class T>
 void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, int C, int n,
                          float alpha, float beta, float kk, int pk, int ps, int PH, int PW,
                          cudaStream_t st) {
-  if (C % 4 != 0 || n > 2 * LH + 1) throw std::runtime_error("lrn_pool: C must be a multiple of 4, size <= 9");
+  constexpr int V = 16 / sizeof(T);
+  if (C % V != 0 || C / V > 384 || n > 2 * LH + 1)
+    throw std::runtime_error("lrn_pool: C must be a multiple of 16 bytes (at most 384 vectors), size <= 9");
   if (static_cast<long long>(B) * H * W * C >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
-  // pooled rows per block: the fp32 LRN band ((TP-1)*ps+pk rows) within ~110 KB
+  // pooled rows per block: the fp32 LRN band ((TP-1)*ps+pk rows) within ~72 KB (3 blocks per SM)
   const long long row_bytes = static_cast<long long>(W) * C * sizeof(float);
   int TP = 1;
-  while (TP < PH && (static_cast<long long>(TP) * ps + pk) * row_bytes <= 112 * 1024) ++TP;
+  while (TP < PH && (static_cast<long long>(TP) * ps + pk) * row_bytes <= 72 * 1024) ++TP;
   const size_t smem = static_cast<size_t>(((TP - 1) * ps + pk) * row_bytes);
   if (smem > 220 * 1024) throw std::runtime_error("lrn_pool: conv row too wide for the smem band");
+  const int G = C / V;
+  const dim3 block(G, std::max(1, 384 / G));
   const dim3 grid((PH + TP - 1) / TP, B);
-  if (n <= 5) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(lrn_pool_fwd2_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-      attr = true;
-    }
-    lrn_pool_fwd2_kernel<T, 2><<<grid, 256, smem, st>>>(a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk,
-                                                       pk, ps, PH, PW, TP);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    kern<<<grid, block, smem, st>>>(a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, TP);
+  };
+  if (n == 5 && pk == 3 && ps == 2) {
+    go(lrn_pool_fwd_kernel<T, 2, 5, 3, 2>);
+  } else if (n <= 5) {
+    go(lrn_pool_fwd_kernel<T, 2, 0, 0, 0>);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(lrn_pool_fwd2_kernel<T, LH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-      attr = true;
-    }
-    lrn_pool_fwd2_kernel<T, LH><<<grid, 256, smem, st>>>(a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta,
-                                                        kk, pk, ps, PH, PW, TP);
+    go(lrn_pool_fwd_kernel<T, LH, 0, 0, 0>);
   }
 }
 
@@ -869,23 +911,28 @@ template <class TA>
 void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* dz, int B, int H,
                          int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
                          int PH, int PW, int relu_mask, cudaStream_t st) {
-  if (C % 4 != 0 || n > 2 * LH + 1 || C / 4 > 256)
-    throw std::runtime_error("lrn_pool: C must be a multiple of 4 (at most 1024), size <= 9");
-  const long long npix = static_cast<long long>(B) * H * W;
-  if (npix * C >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
-  const int G = C / 4;
-  const int PT = std::max(1, 256 / G);
-  const int threads = PT * G;
-  const size_t smem = static_cast<size_t>(PT) * (C + 8) * sizeof(float);
-  const long long blocks = (npix + PT - 1) / PT;
-  if (n <= 5) {
-    lrn_pool_bwd2_kernel<TA, 2><<<static_cast<unsigned>(blocks), threads, smem, st>>>(
-        gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, relu_mask,
-        static_cast<int>(npix), PT);
+  constexpr int V = 16 / sizeof(TA);
+  const int G = C / V;
+  if (C % V != 0 || n > 2 * LH + 1 || G > 1024)
+    throw std::runtime_error("lrn_pool: C must be a multiple of 16 bytes (at most 1024 vectors), size <= 9");
+  if (static_cast<long long>(B) * H * W * C >= (1LL << 31)) throw std::runtime_error("lrn_pool: too large");
+  // columns per block: the whole row when it fits in 1024 threads
+  const int nb = (G * W + 511) / 512;
+  const int WB = (W + nb - 1) / nb;
+  const size_t smem = static_cast<size_t>(2) * WB * (C + 8) * sizeof(float);
+  const dim3 block(G, WB);
+  const dim3 grid(nb, H, B);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    kern<<<grid, block, smem, st>>>(gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW,
+                                    relu_mask);
+  };
+  if (n == 5 && pk == 3 && ps == 2) {
+    go(lrn_pool_bwd_kernel<TA, 2, 5, 3, 2>);
+  } else if (n <= 5) {
+    go(lrn_pool_bwd_kernel<TA, 2, 0, 0, 0>);
   } else {
-    lrn_pool_bwd2_kernel<TA, LH><<<static_cast<unsigned>(blocks), threads, smem, st>>>(
-        gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, relu_mask,
-        static_cast<int>(npix), PT);
+    go(lrn_pool_bwd_kernel<TA, LH, 0, 0, 0>);
   }
 }
 
