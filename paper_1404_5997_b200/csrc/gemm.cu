@@ -928,16 +928,101 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   }
 }
 
-__global__ void epi_apply_kernel(const float* __restrict__ ws, int splits, int M, int N,
-                                 const Epi e) {
-  const long long total = static_cast<long long>(M) * N;
+// One fp32 4-vector (m, n..n+3) through the epilogue (vectorised epi_elem).
+__device__ __forceinline__ void epi_vec4(const Epi& e, int m, int n, float4 x) {
+  const long long off = static_cast<long long>(m) * e.ldc + n;
+  x.x *= e.alpha;
+  x.y *= e.alpha;
+  x.z *= e.alpha;
+  x.w *= e.alpha;
+  if (e.beta) {
+    const float4 o = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.c) + off);
+    x.x += o.x;
+    x.y += o.y;
+    x.z += o.z;
+    x.w += o.w;
+  }
+  if (e.sgd_w) {
+    float4 w4 = *reinterpret_cast<const float4*>(e.sgd_w + off);
+    float4 m4 = *reinterpret_cast<const float4*>(e.sgd_m + off);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float g = f4get(x, j);
+      if (e.sgd_has_gscale) g = __fmul_rn(g, e.sgd_gscale);
+      float d = __fmul_rn(f4get(m4, j), e.sgd_mu);
+      d = __fadd_rn(d, __fmul_rn(e.sgd_s1, g));
+      d = __fadd_rn(d, __fmul_rn(e.sgd_s2, f4get(w4, j)));
+      f4set(m4, j, d);
+      f4set(w4, j, __fadd_rn(f4get(w4, j), d));
+    }
+    *reinterpret_cast<float4*>(e.sgd_w + off) = w4;
+    *reinterpret_cast<float4*>(e.sgd_m + off) = m4;
+    if (e.sgd_copy) st_bf16x4(e.sgd_copy, off, w4);
+    return;
+  }
+  if (e.bias_mode == 1) {
+    const float bm = e.bias[m];
+    x.x += bm;
+    x.y += bm;
+    x.z += bm;
+    x.w += bm;
+  } else if (e.bias_mode == 2) {
+    const float4 bb = *reinterpret_cast<const float4*>(e.bias + n);
+    x.x += bb.x;
+    x.y += bb.y;
+    x.z += bb.z;
+    x.w += bb.w;
+  }
+  if (e.relu) {
+    x.x = x.x > 0.f ? x.x : 0.f;
+    x.y = x.y > 0.f ? x.y : 0.f;
+    x.z = x.z > 0.f ? x.z : 0.f;
+    x.w = x.w > 0.f ? x.w : 0.f;
+  }
+  if (e.mask) {
+    const long long mo = static_cast<long long>(m) * e.ldmask + n;
+    const float4 k = e.mask_type == kBF16 ? ld_bf16x4(e.mask, mo)
+                                          : *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.mask) + mo);
+    if (!(k.x > 0.f)) x.x = 0.f;
+    if (!(k.y > 0.f)) x.y = 0.f;
+    if (!(k.z > 0.f)) x.z = 0.f;
+    if (!(k.w > 0.f)) x.w = 0.f;
+  }
+  if (e.c_type == kF32) {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(e.c) + off) = x;
+  } else {
+    st_bf16x4(e.c, off, x);
+  }
+}
+
+// Split-K reduce (ascending split order) + epilogue. vec: 4 columns per
+// thread (N, ldc, ldmask multiples of 4, untransposed); else one element.
+__global__ void epi_apply_kernel(const float* __restrict__ ws, int splits, int M, int N, const Epi e, int vec) {
   const long long mn = static_cast<long long>(M) * N;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+  if (vec) {
+    const int n4 = N >> 2;
+    const long long total = mn >> 2;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+      float4 acc = reinterpret_cast<const float4*>(ws)[i];
+      for (int s = 1; s < splits; ++s) {
+        const float4 v = reinterpret_cast<const float4*>(ws + s * mn)[i];
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      const int m = static_cast<int>(i / n4);
+      epi_vec4(e, m, 4 * static_cast<int>(i - static_cast<long long>(m) * n4), acc);
+    }
+    return;
+  }
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < mn;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     float acc = ws[i];
     for (int s = 1; s < splits; ++s) acc += ws[s * mn + i];
     const int m = static_cast<int>(i / N);
-    const int n = static_cast<int>(i % N);
+    const int n = static_cast<int>(i - static_cast<long long>(m) * N);
     epi_elem(e, m, n, acc);
   }
 }
@@ -1289,10 +1374,13 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
 }
 
 void epi_apply_launch(const float* ws, int splits, int M, int N, const Epi& e, cudaStream_t s) {
-  const long long total = static_cast<long long>(M) * N;
+  const bool vec = (N & 3) == 0 && !e.c_trans && !e.mask_trans && (e.ldc & 3) == 0 &&
+                   (!e.mask || (e.ldmask & 3) == 0) && (!e.beta || e.c_type == kF32) &&
+                   (!e.sgd_w || e.c_type == kF32);
+  const long long total = static_cast<long long>(M) * N / (vec ? 4 : 1);
   const int threads = 256;
-  const int blocks = static_cast<int>(std::min<long long>((total + threads - 1) / threads, 148LL * 16));
-  epi_apply_kernel<<<blocks, threads, 0, s>>>(ws, splits, M, N, e);
+  const int blocks = static_cast<int>(std::min<long long>((total + threads - 1) / threads, 148LL * 8));
+  epi_apply_kernel<<<blocks, threads, 0, s>>>(ws, splits, M, N, e, vec ? 1 : 0);
 }
 
 void gemm_launch(const GemmPlan& p, cudaStream_t s) {

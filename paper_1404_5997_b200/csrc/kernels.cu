@@ -830,19 +830,29 @@ __global__ void __launch_bounds__(512) lrn_pool_bwd_kernel(
   if (live) stv<TA>(dz + px, out);
 }
 
+// Rotated operand for the implicit dgrad: wr[c][r][s][f] = w[f][R-1-r][S-1-s][c].
+// 32x32 smem transpose tiles (f x k): reads coalesced along k, writes along f.
 template <class T>
-__global__ void rotate_weights_kernel(const float* __restrict__ w, long long ldk, T* __restrict__ wr,
-                                      int F, int C, int R, int S) {
-  const long long n = static_cast<long long>(F) * C * R * S;
-  GRID_STRIDE(i, n) {
-    // output index: [c][r][s][f]
-    const int f = static_cast<int>(i % F);
-    long long t = i / F;
-    const int s = static_cast<int>(t % S);
-    t /= S;
-    const int r = static_cast<int>(t % R);
-    const int c = static_cast<int>(t / R);
-    wr[i] = from_f<T>(w[f * ldk + ((R - 1 - r) * S + (S - 1 - s)) * C + c]);
+__global__ void __launch_bounds__(256) rotate_weights_kernel(const float* __restrict__ w, long long ldk,
+                                                             T* __restrict__ wr, int F, int C, int R, int S) {
+  __shared__ float tile[32][33];
+  const int K = R * S * C;
+  const int k0 = blockIdx.x * 32, f0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int f = f0 + ty + 8 * j, k = k0 + tx;
+    if (f < F && k < K) tile[ty + 8 * j][tx] = w[f * ldk + k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int k = k0 + ty + 8 * j, f = f0 + tx;
+    if (k < K && f < F) {
+      const int rs = k / C, c = k - rs * C;
+      const int r = rs / S, sx = rs - r * S;
+      wr[(static_cast<long long>(c * R + (R - 1 - r)) * S + (S - 1 - sx)) * F + f] = from_f<T>(tile[tx][ty + 8 * j]);
+    }
   }
 }
 
@@ -956,8 +966,8 @@ void launch_maxpool_bwd_w(const float* gy, const uint8_t* widx, TO* gx, const TM
 template <class T>
 void launch_rotate_weights(const float* w, long long ldk, T* wrot, int F, int C, int R, int S,
                            cudaStream_t st) {
-  const long long n = static_cast<long long>(F) * C * R * S;
-  rotate_weights_kernel<T><<<grid_for(n), 256, 0, st>>>(w, ldk, wrot, F, C, R, S);
+  const int K = R * S * C;
+  rotate_weights_kernel<T><<<dim3((K + 31) / 32, (F + 31) / 32), dim3(32, 8), 0, st>>>(w, ldk, wrot, F, C, R, S);
 }
 
 #define INST_NEW(T)                                                                             \

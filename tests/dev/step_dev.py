@@ -50,11 +50,11 @@ if what == "time":
         c.close()
 elif what == "loss":
     for math in (hp.MathMode.BF16, hp.MathMode.F32X3):
-        for lr in (0.01, 0.001, 0.0003):
+        for lr in (0.001, 0.0003, 0.0001):
             c = make(math)
             hyper = hp.HyperParams(momentum=0.9, lr=lr, weight_decay=5e-4)
             ls = []
-            for s in range(60):
+            for s in range(90):
                 x, t = dev[s % 4]
                 r = c.run_step([x], [t], hyper, device=True)
                 ls.append(r.metrics.loss)
