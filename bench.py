@@ -9,7 +9,9 @@ GPU, workers exchanging over NCCL (the C library's own communicator; the
 ncclUniqueId travels over torch.distributed).
 
   value   images/s with inputs already resident in HBM (device pointers)
-  e2e     images/s through the same public API with pinned HOST buffers:
+  e2e     images/s through the same public API with pinned HOST buffers
+          (hp_cluster_prefetch stages step i+1 on the copy stream while step i
+          computes; every step's copy is inside the timed region):
           the H2D copy of each step's images+targets and the D2H loss readback
           are inside the timed region
   --impl reference: the reference's own CPU implementation (oracle/_ref,
@@ -263,11 +265,19 @@ def main_b200(args):
         e0.record(stream)
         launches = 0
         loss = None
+        if kind == "host":
+            x, t = pinned[0]
+            cluster.prefetch([x], [t])
         for s in range(steps):
             if kind == "device":
                 x, t = dev[s % NB]
                 r = cluster.run_step([x], [t], hyper, device=True)
             else:
+                # host arm: this step's pinned batch was staged (H2D on the copy
+                # stream) while the previous step computed; stage the next one
+                if s + 1 < steps:
+                    xn, tn = pinned[(s + 1) % NB]
+                    cluster.prefetch([xn], [tn])
                 x, t = pinned[s % NB]
                 r = cluster.run_step([x], [t], hyper, device=False)
             launches += cluster.last_step_launches()
@@ -283,6 +293,8 @@ def main_b200(args):
     for kind in (dev, pinned):
         for s in range(2 * NB):
             x, t = kind[s % NB]
+            if kind is pinned:
+                cluster.prefetch([x], [t])
             cluster.run_step([x], [t], hyper, device=kind is dev)
     for s in range(args.warmup):
         x, t = dev[s % NB]

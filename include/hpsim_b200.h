@@ -174,6 +174,15 @@ HP_API int hp_cluster_run_step(hp_cluster* c, const float* const* batches,
                                const float* const* targets, int mem_kind, const hp_hyper* hp,
                                double lr, hp_step_metrics* out);
 
+/* B200 extension (no reference counterpart): stage the NEXT step's HOST
+ * batches/targets (same shapes as run_step) into one of two device slots on a
+ * copy stream and return immediately. A later hp_cluster_run_step with
+ * mem_kind HP_MEM_HOST and the same host pointers consumes the slot instead of
+ * copying on the compute stream, so the copy of step i+1 overlaps the compute
+ * of step i. The host buffers must stay valid (and unchanged) until that
+ * run_step returns; pinned memory makes the copy truly asynchronous. */
+HP_API int hp_cluster_prefetch(hp_cluster* c, const float* const* batches, const float* const* targets);
+
 /* Trace of the last step (StepTrace, cluster.hpp:103-109). Returns count. */
 HP_API int hp_cluster_trace(const hp_cluster* c, hp_trace_event* out, int cap);
 /* Cumulative per-worker ByteCounters (cluster.hpp:49-57). */

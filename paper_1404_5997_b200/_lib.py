@@ -141,6 +141,7 @@ def _load() -> C.CDLL:
         "hp_cluster_create": ([C.POINTER(HpModelSpec), C.POINTER(HpClusterConfig), C.POINTER(P)], C.c_int),
         "hp_cluster_destroy": ([P], None),
         "hp_nccl_unique_id": ([C.POINTER(C.c_ubyte * 128)], C.c_int),
+        "hp_cluster_prefetch": ([P, P, P], C.c_int),
         "hp_cluster_run_step": ([P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int,
                                  C.POINTER(HpHyper), C.c_double, C.POINTER(HpStepMetrics)], C.c_int),
         "hp_cluster_trace": ([P, C.POINTER(HpTraceEvent), C.c_int], C.c_int),

@@ -309,6 +309,17 @@ class Cluster:
         return StepResult(StepMetrics(m.loss, m.fc_update_count, m.conv_update_count, list(m.bytes_sent)),
                           self.trace())
 
+    def prefetch(self, batches: Sequence, targets: Sequence) -> None:
+        """Stage the next step's HOST batches (numpy or pinned CPU tensors) on the
+        copy stream; a following run_step with the same buffers consumes them
+        (double-buffered H2D overlapping the current step's compute)."""
+        n = len(batches)
+        if len(targets) != n:
+            raise UsageError(f"prefetch: expected {n} batches and targets, got {n} / {len(targets)}")
+        bp = (C.c_void_p * n)(*[_ptr(x) for x in batches])
+        tp = (C.c_void_p * n)(*[_ptr(t) for t in targets])
+        _check(lib.hp_cluster_prefetch(self._h, bp, tp))
+
     def trace(self) -> List[TraceEvent]:
         ev = (HpTraceEvent * 512)()
         k = lib.hp_cluster_trace(self._h, ev, 512)

@@ -60,6 +60,13 @@ HP_API int hp_cluster_run_step(hp_cluster* c, const float* const* batches, const
   });
 }
 
+HP_API int hp_cluster_prefetch(hp_cluster* c, const float* const* batches, const float* const* targets) {
+  return guarded_c([&] {
+    if (!c) usage_error("prefetch: null cluster");
+    c->impl->prefetch(batches, targets);
+  });
+}
+
 HP_API int hp_cluster_trace(const hp_cluster* c, hp_trace_event* out, int cap) {
   const auto& t = c->impl->trace;
   for (int i = 0; i < static_cast<int>(t.size()) && i < cap; ++i) out[i] = t[i];

@@ -265,6 +265,8 @@ struct Worker {
   int gid = 0;
   // inputs
   float* x_nchw = nullptr;  // staging for host batches
+  float* xin[2] = {nullptr, nullptr};  // prefetch slots: images
+  float* tin[2] = {nullptr, nullptr};  // prefetch slots: targets
   TA* x0 = nullptr;         // [b][H][W][C]
   float* targets = nullptr; // [b][L]
   // conv stack
@@ -299,6 +301,7 @@ class ClusterImpl final : public ClusterBase {
   ClusterImpl(const hp_model_spec* spec, const hp_cluster_config* cfg);
   ~ClusterImpl() override;
   void* stream() const override { return st_; }
+  void prefetch(const float* const* batches, const float* const* targets) override;
   void run_step(const float* const* batches, const float* const* targets, int mem_kind,
                 const hp_hyper& hp, double lr, hp_step_metrics* out) override;
   int64_t param_size(int worker, int which, int layer) const override;
@@ -368,6 +371,16 @@ class ClusterImpl final : public ClusterBase {
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   std::vector<cudaEvent_t> ev_layer_;  // per conv layer: its gradients are final on st_
   cudaEvent_t ev_comm_ = nullptr;      // all conv-gradient all-reduces done on sc_
+  cudaStream_t sx_ = nullptr;          // copy stream: prefetch H2D
+  struct PrefSlot {
+    std::vector<const float*> x, t;  // host pointers staged in this slot
+    bool valid = false;
+    int64_t bytes = 0;
+    cudaEvent_t ready = nullptr;  // copies done (sx_)
+    cudaEvent_t used = nullptr;   // the step that consumed the slot is done reading it (st_)
+  };
+  PrefSlot pref_[2];
+  int next_slot_ = 0;
   DevArena arena_;
   std::vector<Worker<TA>> w_;
   std::vector<long long> coff_, foff_;
@@ -431,6 +444,11 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   HP_CUDA(cudaEventCreate(&ev0_));
   HP_CUDA(cudaEventCreate(&ev1_));
   HP_CUDA(cudaEventCreateWithFlags(&ev_comm_, cudaEventDisableTiming));
+  HP_CUDA(cudaStreamCreateWithFlags(&sx_, cudaStreamNonBlocking));
+  for (auto& ps : pref_) {
+    HP_CUDA(cudaEventCreateWithFlags(&ps.ready, cudaEventDisableTiming));
+    HP_CUDA(cudaEventCreateWithFlags(&ps.used, cudaEventDisableTiming));
+  }
 
   // parameter arena layouts (16-byte aligned pieces)
   for (size_t l = 0; l < g_.cg.size(); ++l) {
@@ -465,6 +483,10 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     Worker<TA>& w = w_[i];
     w.gid = comm_->first() + i;
     w.x_nchw = arena_.make<float>(b_ * in[0] * in[1] * in[2]);
+    for (int k = 0; k < 2; ++k) {
+      w.xin[k] = arena_.make<float>(b_ * in[0] * in[1] * in[2]);
+      w.tin[k] = arena_.make<float>(b_ * L_);
+    }
     w.x0 = g_.cg[0].impl_fwd ? arena_.make<TA>(b_ * in[0] * in[1] * in[2]) : nullptr;
     w.targets = arena_.make<float>(b_ * L_);
     for (int l = 0; l < nc; ++l) {
@@ -538,6 +560,12 @@ ClusterImpl<TA>::~ClusterImpl() {
   for (auto e : ev_layer_) cudaEventDestroy(e);
   if (ev_comm_) cudaEventDestroy(ev_comm_);
   if (sc_) cudaStreamDestroy(sc_);
+  if (sx_) cudaStreamSynchronize(sx_);
+  for (auto& ps : pref_) {
+    if (ps.ready) cudaEventDestroy(ps.ready);
+    if (ps.used) cudaEventDestroy(ps.used);
+  }
+  if (sx_) cudaStreamDestroy(sx_);
   for (auto& s : prof_pool_) {
     cudaEventDestroy(s.a);
     cudaEventDestroy(s.b);
@@ -1198,9 +1226,60 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
 }
 
 template <class TA>
+void ClusterImpl<TA>::prefetch(const float* const* batches, const float* const* targets) {
+  const int nl = comm_->nlocal();
+  if (!batches || !targets) usage_error("prefetch: expected " + num(nl) + " batches and targets");
+  for (int i = 0; i < nl; ++i)
+    if (!batches[i] || !targets[i]) usage_error("prefetch: null batch or target");
+  PrefSlot& ps = pref_[next_slot_];
+  next_slot_ ^= 1;
+  const auto& in = g_.input;
+  const long long xin = b_ * in[0] * in[1] * in[2];
+  HP_CUDA(cudaStreamWaitEvent(sx_, ps.used, 0));  // the slot's previous consumer is done
+  ps.x.assign(batches, batches + nl);
+  ps.t.assign(targets, targets + nl);
+  ps.bytes = 0;
+  const int slot = static_cast<int>(&ps - pref_);
+  for (int i = 0; i < nl; ++i) {
+    HP_CUDA(cudaMemcpyAsync(w_[i].xin[slot], batches[i], xin * sizeof(float), cudaMemcpyHostToDevice, sx_));
+    HP_CUDA(cudaMemcpyAsync(w_[i].tin[slot], targets[i], b_ * L_ * sizeof(float), cudaMemcpyHostToDevice, sx_));
+    ps.bytes += (xin + b_ * L_) * static_cast<int64_t>(sizeof(float));
+  }
+  HP_CUDA(cudaEventRecord(ps.ready, sx_));
+  ps.valid = true;
+}
+
+template <class TA>
 void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* targets, int mem_kind,
                                const hp_hyper& hp, double lr, hp_step_metrics* out) {
   const int nl = comm_->nlocal();
+  if (mem_kind == HP_MEM_HOST && batches && targets) {
+    // consume a prefetched slot holding exactly these host buffers
+    for (auto& ps : pref_) {
+      if (!ps.valid || static_cast<int>(ps.x.size()) != nl) continue;
+      bool same = true;
+      for (int i = 0; i < nl && same; ++i) same = ps.x[i] == batches[i] && ps.t[i] == targets[i];
+      if (!same) continue;
+      for (int i = 0; i < nl; ++i)
+        for (long long e = 0; e < b_ * L_; ++e) {
+          const double t = targets[i][e];
+          if (t < 0.0 || t > 1.0)
+            domain_error("logistic_xent: target " + std::to_string(t) + " outside [0,1] at flat index " + num(e));
+        }
+      const int slot = static_cast<int>(&ps - pref_);
+      std::vector<const float*> xb(nl), tb(nl);
+      for (int i = 0; i < nl; ++i) {
+        xb[i] = w_[i].xin[slot];
+        tb[i] = w_[i].tin[slot];
+      }
+      ps.valid = false;
+      HP_CUDA(cudaStreamWaitEvent(st_, ps.ready, 0));
+      run_step(xb.data(), tb.data(), HP_MEM_DEVICE, hp, lr, out);
+      HP_CUDA(cudaEventRecord(ps.used, st_));
+      io_h2d = ps.bytes;
+      return;
+    }
+  }
   if (!batches || !targets) usage_error("run_step: expected " + num(nl) + " batches and targets");
   for (int i = 0; i < nl; ++i)
     if (!batches[i] || !targets[i])

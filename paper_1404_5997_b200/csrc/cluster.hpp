@@ -64,6 +64,11 @@ class ClusterBase {
                             float* const* fb) = 0;
 
   virtual void* stream() const = 0;
+  // Stage the NEXT step's host batches/targets into a device slot on the copy
+  // stream (async); a later run_step with the same host pointers consumes the
+  // slot instead of copying on the compute stream (double buffering: the copy
+  // of step i+1 overlaps the compute of step i).
+  virtual void prefetch(const float* const* batches, const float* const* targets) = 0;
 
   struct GemmProf {
     const char* tag;

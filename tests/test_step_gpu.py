@@ -136,3 +136,37 @@ def test_cuda_graph_replay_is_bit_identical():
     assert res[0][0] == res[1][0]
     for a, b in zip(res[0][1], res[1][1]):
         assert np.array_equal(a, b)
+
+
+def test_prefetch_double_buffer_matches_plain_host_steps():
+    """hp_cluster_prefetch: host batches staged on the copy stream (two slots,
+    overlapping the previous step) give bit-identical results to plain host
+    steps; the H2D bytes are still charged to the consuming step; a run_step
+    on different host buffers ignores the staged slot."""
+    import torch
+    spec = hp.tiny_cnn()
+    host = [hp.synthetic_batch(spec, 16, step=s, worker=w) for s in range(3) for w in range(2)]
+    pinned = [(torch.from_numpy(x).pin_memory(), torch.from_numpy(t).pin_memory()) for x, t in host]
+    res = []
+    for pre in (False, True):
+        g = hp.Cluster(spec, hp.ClusterConfig(workers=2, per_worker_batch=16, scheme=hp.Scheme.B, seed=5,
+                                              math_mode=hp.MathMode.BF16))
+        losses, io = [], []
+        order = [0, 1, 2, 0, 1, 2, 1]
+        if pre:
+            k = order[0]
+            g.prefetch([pinned[2 * k][0], pinned[2 * k + 1][0]], [pinned[2 * k][1], pinned[2 * k + 1][1]])
+        for i, k in enumerate(order):
+            if pre and i + 1 < len(order) and i != 3:  # step 4 runs without a staged slot
+                kn = order[i + 1]
+                g.prefetch([pinned[2 * kn][0], pinned[2 * kn + 1][0]], [pinned[2 * kn][1], pinned[2 * kn + 1][1]])
+            xs = [pinned[2 * k][0], pinned[2 * k + 1][0]]
+            ts = [pinned[2 * k][1], pinned[2 * k + 1][1]]
+            losses.append(g.run_step(xs, ts, hp.HyperParams(lr=0.01), device=False).metrics.loss)
+            io.append(g.last_step_io()[0])
+        res.append((losses, io, [g.param(w, which, l) for w in range(2) for which in range(8)
+                                 for l in range(3 if (which & 3) < 2 else 2)]))
+    assert res[0][0] == res[1][0]
+    assert res[0][1] == res[1][1]
+    for a, b in zip(res[0][2], res[1][2]):
+        assert np.array_equal(a, b)
