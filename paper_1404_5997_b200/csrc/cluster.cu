@@ -274,6 +274,9 @@ struct Worker {
   std::vector<float*> lrn_d, dcol, gstage;
   std::vector<uint8_t*> widx;  // pool argmax as window offset
   std::vector<TA*> wrot;        // rotated kernels [C][R][S][F] (implicit dgrad)
+  TA* z = nullptr;              // s2d layer 0: space-to-depth input [b][Zh][Zw][Cz]
+  TA* wz = nullptr;             // s2d layer 0: kernels [F][Rq][Rq][Cz] (operand type)
+  float* dwz = nullptr;         // s2d layer 0: wgrad in the s2d layout
   const float* x_src = nullptr; // this step's NCHW batch (device)
   // conv params: [kernels F x ldk | bias F] per layer, one arena
   float *cp = nullptr, *cm = nullptr, *cgr = nullptr;
@@ -467,6 +470,16 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   for (size_t l = 0; l < g_.cg.size(); ++l) {
     ConvGeom& c = g_.cg[l];
     c.impl_fwd = c.C % atom == 0;
+    // strided first layer with few channels (AlexNet conv1: C=3, s=4 -> 48 of 64
+    // channels, 3x3 taps): space-to-depth + implicit GEMM instead of an im2col buffer
+    const int cz = static_cast<int>(round_up(static_cast<long long>(c.C) * c.stride * c.stride, atom));
+    c.s2d = l == 0 && !c.impl_fwd && c.stride >= 2 && cz <= 2 * atom;
+    if (c.s2d) {
+      c.Cz = cz;
+      c.Rq = (c.R + c.stride - 1) / c.stride;
+      c.Zh = c.OH + c.Rq - 1;
+      c.Zw = c.OW + c.Rq - 1;
+    }
     c.impl_dgrad = l > 0 && c.stride == 1 && c.F % atom == 0 && c.pad <= c.R - 1 &&
                    c.H == c.OH + c.R - 1 - 2 * c.pad && c.W == c.OW + c.S - 1 - 2 * c.pad;
   }
@@ -493,7 +506,12 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
       const ConvGeom& c = g_.cg[l];
       const bool lrn_only = c.lrn_n > 0 && c.pk == 0;  // fused LRN+pool keeps no LRN output
       // layer 0 explicit: transposed colT [Kc][P]; other explicit layers: col [P][ldk]
-      w.col.push_back(c.impl_fwd ? nullptr
+      if (c.s2d) {
+        w.z = arena_.make<TA>(b_ * c.Zh * c.Zw * c.Cz);
+        w.wz = arena_.make<TA>(static_cast<long long>(c.F) * c.Rq * c.Rq * c.Cz);
+        w.dwz = arena_.make<float>(static_cast<long long>(c.F) * c.Rq * c.Rq * c.Cz);
+      }
+      w.col.push_back(c.impl_fwd || c.s2d ? nullptr
                                  : (l == 0 ? arena_.make<TA>(static_cast<long long>(c.Kc) * c.ldp)
                                            : arena_.make<TA>(c.P * c.ldk)));
       w.act.push_back(arena_.make<TA>(c.P * c.F));
@@ -647,7 +665,15 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       xa = op(in, 0, 0);
       xa.conv = view;
     }
-    w.conv_fwd.push_back(plan(xa, op(kw, 0, c.ldk), c.P, c.F, c.Kc, e));
+    const long long Kz = static_cast<long long>(c.Rq) * c.Rq * c.Cz;
+    const Im2col zview{1, static_cast<int>(b_), c.Zh, c.Zw, c.Cz, c.Rq, c.Rq, 1, 0, c.OH, c.OW};
+    if (c.s2d) {
+      xa = op(w.z, 0, 0);
+      xa.conv = zview;
+      w.conv_fwd.push_back(plan(xa, op(w.wz, 0, Kz), c.P, c.F, Kz, e));
+    } else {
+      w.conv_fwd.push_back(plan(xa, op(kw, 0, c.ldk), c.P, c.F, c.Kc, e));
+    }
     // wgrad: dW[F][Kc] = dz^T[F][P] . im2col(x)[P][Kc]
     Epi eg;
     eg.c = w.cgr + conv_k_off(l);
@@ -657,7 +683,15 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       xb = op(in, 1, 0);
       xb.conv = view;
     }
-    w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, c.Kc, c.P, eg));
+    if (c.s2d) {
+      eg.c = w.dwz;
+      eg.ldc = Kz;
+      xb = op(w.z, 1, 0);
+      xb.conv = zview;
+      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, Kz, c.P, eg));
+    } else {
+      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, c.Kc, c.P, eg));
+    }
     if (l == 0) {
       w.conv_dgrad.push_back(GemmPlan{});
       continue;
@@ -858,7 +892,10 @@ void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
   const int B = static_cast<int>(b_);
   for (int l = 0; l < nc; ++l) {
     const ConvGeom& c = g_.cg[l];
-    if (!c.impl_fwd) {
+    if (c.s2d) {
+      launch_s2d_input<TA>(w.x_src, w.z, B, c.C, c.H, c.W, c.stride, c.pad, c.Zh, c.Zw, c.Cz, st_);
+      ++launches_;
+    } else if (!c.impl_fwd) {
       if (l == 0) {
         launch_im2col_t_nchw<TA>(w.x_src, w.col[0], B, c.C, c.H, c.W, c.R, c.S, c.stride, c.pad, c.OH,
                                  c.OW, c.ldp, st_);
@@ -889,6 +926,11 @@ template <class TA>
 void ClusterImpl<TA>::rotate_all(Worker<TA>& w) {
   for (size_t l = 0; l < g_.cg.size(); ++l) {
     const ConvGeom& c = g_.cg[l];
+    if (c.s2d) {  // the s2d operand copy of the (just updated) master kernels
+      launch_s2d_weights<TA>(w.cp + conv_k_off(static_cast<int>(l)), c.ldk, w.wz, c.F, c.C, c.R, c.S, c.stride, c.Rq,
+                             c.Cz, st_);
+      ++launches_;
+    }
     if (!c.impl_dgrad) continue;
     launch_rotate_weights<TA>(w.cp + conv_k_off(static_cast<int>(l)), c.ldk, w.wrot[l], c.F, c.C, c.R,
                               c.S, st_);
@@ -1062,6 +1104,10 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
   launch_colsum<TA>(w.dz[l], c.P, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, st_);
   launches_ += 2;
   gemm(w.conv_wgrad[l], "conv_wgrad", l);
+  if (c.s2d) {
+    launch_s2d_wgrad_gather(w.dwz, w.cgr + conv_k_off(l), c.ldk, c.F, c.C, c.R, c.S, c.stride, c.Rq, c.Cz, st_);
+    ++launches_;
+  }
   if (l == 0) return;
   const ConvGeom& pc = g_.cg[l - 1];
   const bool below_fused = pc.pk > 0 || pc.lrn_n > 0;

@@ -24,6 +24,8 @@ struct ConvGeom {
   int Kc;                      // R*S*C (im2col width)
   bool impl_fwd = false;       // fprop + wgrad as implicit GEMM (TMA im2col), no col buffer
   bool impl_dgrad = false;     // stride-1 dgrad as a conv over dY with rotated weights
+  bool s2d = false;            // strided first layer as a stride-1 conv over its space-to-depth input
+  int Rq = 0, Zh = 0, Zw = 0, Cz = 0;  // s2d: taps, z extents, padded z channels
   long long ldk;               // padded row stride of col / kernels (16-byte multiple)
   long long P;                 // b*OH*OW rows per worker
   long long PP;                // b*PH*PW

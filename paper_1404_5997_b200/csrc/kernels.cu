@@ -856,6 +856,70 @@ __global__ void __launch_bounds__(256) rotate_weights_kernel(const float* __rest
   }
 }
 
+// Space-to-depth (see kernels.cuh): thread = (pixel (b,i,j), 8-channel group),
+// one 16-byte (bf16) / 2x16-byte (fp32) store per thread.
+template <class T>
+__global__ void __launch_bounds__(256) s2d_input_kernel(const float* __restrict__ x, T* __restrict__ z, int C,
+                                                        int H, int W, int s, int pad, int Zh, int Zw, int Cz,
+                                                        int total) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  const int G = Cz >> 3;
+  const int q = t % G;
+  const int pix = t / G;
+  const int j = pix % Zw, r = pix / Zw;
+  const int i = r % Zh, b = r / Zh;
+  const int real = s * s * C;
+  const float* xb = x + static_cast<long long>(b) * C * H * W;
+  float v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int ch = q * 8 + k;
+    float val = 0.f;
+    if (ch < real) {
+      const int c = ch % C, d = ch / C;
+      const int dr = d / s, dc = d - dr * s;
+      const int h = s * i + dr - pad, w = s * j + dc - pad;
+      if (h >= 0 && h < H && w >= 0 && w < W) val = __ldg(xb + (static_cast<long long>(c) * H + h) * W + w);
+    }
+    v[k] = val;
+  }
+  T* dst = z + static_cast<long long>(pix) * Cz + q * 8;
+  st4<T>(dst, v);
+  st4<T>(dst + 4, v + 4);
+}
+
+template <class T>
+__global__ void s2d_weights_kernel(const float* __restrict__ w, long long ldk, T* __restrict__ wz, int F, int C,
+                                   int R, int S, int s, int Rq, int Cz) {
+  const int Kz = Rq * Rq * Cz;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= F * Kz) return;
+  const int f = t / Kz, k = t - f * Kz;
+  const int ab = k / Cz, ch = k - ab * Cz;
+  const int a = ab / Rq, bq = ab - a * Rq;
+  float val = 0.f;
+  if (ch < s * s * C) {
+    const int c = ch % C, d = ch / C;
+    const int dr = d / s, dc = d - dr * s;
+    const int r = s * a + dr, q = s * bq + dc;
+    if (r < R && q < S) val = w[f * ldk + (r * S + q) * C + c];
+  }
+  wz[t] = from_f<T>(val);
+}
+
+__global__ void s2d_wgrad_gather_kernel(const float* __restrict__ dwz, float* __restrict__ dw, long long ldk,
+                                        int F, int C, int R, int S, int s, int Rq, int Cz) {
+  const int K = R * S * C;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= F * K) return;
+  const int f = t / K, k = t - f * K;
+  const int rq = k / C, c = k - rq * C;
+  const int r = rq / S, q = rq - r * S;
+  const int kz = ((r / s) * Rq + q / s) * Cz + ((r % s) * s + q % s) * C + c;
+  dw[f * ldk + k] = dwz[static_cast<long long>(f) * Rq * Rq * Cz + kz];
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -970,7 +1034,34 @@ void launch_rotate_weights(const float* w, long long ldk, T* wrot, int F, int C,
   rotate_weights_kernel<T><<<dim3((K + 31) / 32, (F + 31) / 32), dim3(32, 8), 0, st>>>(w, ldk, wrot, F, C, R, S);
 }
 
+template <class T>
+void launch_s2d_input(const float* x, T* z, int B, int C, int H, int W, int s, int pad, int Zh, int Zw, int Cz,
+                      cudaStream_t st) {
+  if (Cz % 8 != 0) throw std::runtime_error("s2d: padded channels must be a multiple of 8");
+  const long long total = static_cast<long long>(B) * Zh * Zw * (Cz / 8);
+  if (total >= (1LL << 31)) throw std::runtime_error("s2d: too large");
+  s2d_input_kernel<T><<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(x, z, C, H, W, s, pad, Zh, Zw, Cz,
+                                                                               static_cast<int>(total));
+}
+
+template <class T>
+void launch_s2d_weights(const float* w, long long ldk, T* wz, int F, int C, int R, int S, int s, int Rq, int Cz,
+                        cudaStream_t st) {
+  const int n = F * Rq * Rq * Cz;
+  s2d_weights_kernel<T><<<(n + 255) / 256, 256, 0, st>>>(w, ldk, wz, F, C, R, S, s, Rq, Cz);
+}
+
+void launch_s2d_wgrad_gather(const float* dwz, float* dw, long long ldk, int F, int C, int R, int S, int s, int Rq,
+                             int Cz, cudaStream_t st) {
+  const int n = F * R * S * C;
+  s2d_wgrad_gather_kernel<<<(n + 255) / 256, 256, 0, st>>>(dwz, dw, ldk, F, C, R, S, s, Rq, Cz);
+}
+
 #define INST_NEW(T)                                                                             \
+  template void launch_s2d_input<T>(const float*, T*, int, int, int, int, int, int, int, int, int, \
+                                    cudaStream_t);                                              \
+  template void launch_s2d_weights<T>(const float*, long long, T*, int, int, int, int, int, int, \
+                                      int, cudaStream_t);                                       \
   template void launch_im2col_t_nchw<T>(const float*, T*, int, int, int, int, int, int, int, int, int, \
                                         int, long long, cudaStream_t);                                     \
   template void launch_im2col_nchw<T>(const float*, T*, int, int, int, int, int, int, int, int, int, \

@@ -143,6 +143,25 @@ template <class T>
 void launch_rotate_weights(const float* w, long long ldk, T* wrot, int F, int C, int R, int S,
                            cudaStream_t st);
 
+// Space-to-depth for a strided first layer (AlexNet conv1, stride s): the
+// stride-s RxS conv over the NCHW fp32 batch equals a stride-1 Rq x Rq conv
+// (Rq = ceil(R/s)) over z[b][i][j][ch], ch = (dr*s + dc)*C + c < s*s*C (zero up
+// to Cz), z = xpad[b][c][s*i + dr][s*j + dc] (xpad: x shifted by pad, zero
+// outside). Zh x Zw = (OH + Rq - 1) x (OW + Rq - 1). The implicit-GEMM path
+// then runs conv1 like any other layer (TMA im2col over z, no col buffer).
+template <class T>
+void launch_s2d_input(const float* x, T* z, int B, int C, int H, int W, int s, int pad, int Zh, int Zw,
+                      int Cz, cudaStream_t st);
+// wz[f][(a*Rq + b)*Cz + ch] = w[f][((s*a+dr)*S + (s*b+dc))*C + c] (zero where
+// s*a+dr >= R, s*b+dc >= S or ch >= s*s*C); w rows of stride ldk.
+template <class T>
+void launch_s2d_weights(const float* w, long long ldk, T* wz, int F, int C, int R, int S, int s, int Rq,
+                        int Cz, cudaStream_t st);
+// Inverse map of the s2d weight gradient back to the reference layout:
+// dw[f][(r*S + q)*C + c] = dwz[f][((r/s)*Rq + q/s)*Cz + ((r%s)*s + q%s)*C + c].
+void launch_s2d_wgrad_gather(const float* dwz, float* dw, long long ldk, int F, int C, int R, int S, int s,
+                             int Rq, int Cz, cudaStream_t st);
+
 // Scale in place (fp32).
 void launch_scale(float* x, long long n, float s, cudaStream_t st);
 
