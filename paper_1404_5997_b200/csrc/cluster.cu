@@ -483,6 +483,36 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     c.impl_dgrad = l > 0 && c.stride == 1 && c.F % atom == 0 && c.pad <= c.R - 1 &&
                    c.H == c.OH + c.R - 1 - 2 * c.pad && c.W == c.OW + c.S - 1 - 2 * c.pad;
   }
+  {
+    // q-layout per layer (stride-1 same convs whose producers/consumers support it)
+    const int n = static_cast<int>(g_.cg.size());
+    for (int l = 1; l < n; ++l) {
+      ConvGeom& c = g_.cg[l];
+      const ConvGeom& pc = g_.cg[l - 1];
+      c.in_q = c.impl_fwd && c.impl_dgrad && c.stride == 1 && 2 * c.pad == c.R - 1 && c.R == c.S &&
+               c.OH == c.H && c.OW == c.W && !(pc.lrn_n > 0 && pc.pk == 0);
+      // dz without pool/LRN above: written by mask_cast (last layer, unsupported)
+      if (c.pk == 0 && c.lrn_n == 0 && l == n - 1) c.in_q = false;
+    }
+    // a layer without pool/LRN shares one layout between its output (= next
+    // input, the ReLU mask of its dz) and its dz: both q with equal pads or neither
+    for (bool changed = true; changed;) {
+      changed = false;
+      for (int l = 1; l + 1 < n; ++l) {
+        ConvGeom& c = g_.cg[l];
+        ConvGeom& nx = g_.cg[l + 1];
+        if (c.pk == 0 && c.lrn_n == 0 && (c.in_q != nx.in_q || (c.in_q && c.pad != nx.pad))) {
+          if (c.in_q || nx.in_q) changed = true;
+          c.in_q = nx.in_q = false;
+        }
+      }
+    }
+    for (auto& c : g_.cg) {
+      c.Hq = c.in_q ? c.H + c.pad : c.H;
+      c.Wq = c.in_q ? c.W + c.pad : c.W;
+      c.Pq = c.in_q ? b_ * c.Hq * c.Wq : c.P;
+    }
+  }
   const auto& in = g_.input;
   const long long A = g_.A;
   const int nc = static_cast<int>(g_.cg.size()), nf = static_cast<int>(g_.fg.size());
@@ -490,7 +520,7 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   for (int l = 0; l < nf; ++l) (void)l;
   xblocks_ = xent_blocks(static_cast<int>(g_.fg.back().cmax), static_cast<int>(n_));
   size_t colsum_ws = 0;
-  for (const auto& cg : g_.cg) colsum_ws = std::max(colsum_ws, colsum_ws_floats(cg.P, cg.F));
+  for (const auto& cg : g_.cg) colsum_ws = std::max(colsum_ws, colsum_ws_floats(cg.Pq, cg.F));
   size_t comm_scratch = 0;
   for (int i = 0; i < nl; ++i) {
     Worker<TA>& w = w_[i];
@@ -514,12 +544,14 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
       w.col.push_back(c.impl_fwd || c.s2d ? nullptr
                                  : (l == 0 ? arena_.make<TA>(static_cast<long long>(c.Kc) * c.ldp)
                                            : arena_.make<TA>(c.P * c.ldk)));
-      w.act.push_back(arena_.make<TA>(c.P * c.F));
+      const bool next_q = l + 1 < nc && g_.cg[l + 1].in_q;
+      const long long out_rows = next_q ? g_.cg[l + 1].Pq : -1;  // stage output in the next layer's q-layout
+      w.act.push_back(arena_.make<TA>((c.pk == 0 && c.lrn_n == 0 && next_q ? out_rows : c.P) * c.F));
       w.lrn.push_back(lrn_only ? arena_.make<TA>(c.P * c.F) : nullptr);
       w.lrn_d.push_back(lrn_only ? arena_.make<float>(c.P * c.F) : nullptr);
-      w.pool.push_back(c.pk > 0 ? arena_.make<TA>(c.PP * c.F) : nullptr);
+      w.pool.push_back(c.pk > 0 ? arena_.make<TA>((next_q ? out_rows : c.PP) * c.F) : nullptr);
       w.widx.push_back(c.pk > 0 ? arena_.make<uint8_t>(c.PP * c.F) : nullptr);
-      w.dz.push_back(arena_.make<TA>(c.P * c.F));
+      w.dz.push_back(arena_.make<TA>(c.Pq * c.F));
       w.dcol.push_back(l > 0 && !c.impl_dgrad ? arena_.make<float>(c.P * c.ldk) : nullptr);
       w.wrot.push_back(c.impl_dgrad ? arena_.make<TA>(static_cast<long long>(c.F) * c.Kc) : nullptr);
       // grad wrt this stage's output, needed when the stage ends in pool/LRN
@@ -651,7 +683,15 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     const ConvGeom& c = g_.cg[l];
     const char* kw = static_cast<const char*>(cweights) + conv_k_off(l) * es;
     const void* in = l == 0 ? static_cast<const void*>(w.x0) : stage_in(w, l);
-    const Im2col view{1, static_cast<int>(b_), c.H, c.W, c.C, c.R, c.S, c.stride, c.pad, c.OH, c.OW};
+    Im2col view{1, static_cast<int>(b_), c.H, c.W, c.C, c.R, c.S, c.stride, c.pad, c.OH, c.OW};
+    if (c.in_q) {  // x in q-layout: the padding is in memory; walk the valid outputs
+      view.H = c.Hq;
+      view.W = c.Wq;
+      view.corners = 1;
+      view.lo = 0;
+      view.hi = -c.pad;
+    }
+    const bool next_q = l + 1 < nc && g_.cg[l + 1].in_q;
     // fprop: Y[P][F] = im2col(x)[P][Kc] . W[F][Kc]^T (+bias, ReLU)
     Epi e;
     e.c = w.act[l];
@@ -660,6 +700,10 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     e.bias = w.cp + conv_b_off(l);
     e.bias_mode = 2;
     e.relu = c.relu;
+    if (next_q && c.pk == 0 && c.lrn_n == 0) {  // conv output = next layer's q-layout input
+      const ConvGeom& nx = g_.cg[l + 1];
+      e.rows = RowMap{1, c.OH, c.OW, c.OH, c.OW, nx.Hq, nx.Wq, nx.pad};
+    }
     GemmOperand xa = l == 0 ? op(w.col[0], 1, c.ldp) : op(w.col[l], 0, c.ldk);
     if (c.impl_fwd) {
       xa = op(in, 0, 0);
@@ -682,6 +726,12 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     if (c.impl_fwd) {
       xb = op(in, 1, 0);
       xb.conv = view;
+      if (c.in_q) {  // K = every stored q position (dz is zero on the border)
+        xb.conv.lo = -c.pad;
+        xb.conv.hi = -c.pad;
+        xb.conv.OH = c.Hq;
+        xb.conv.OW = c.Wq;
+      }
     }
     if (c.s2d) {
       eg.c = w.dwz;
@@ -690,7 +740,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       xb.conv = zview;
       w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, Kz, c.P, eg));
     } else {
-      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, c.Kc, c.P, eg));
+      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, c.Kc, c.Pq, eg));
     }
     if (l == 0) {
       w.conv_dgrad.push_back(GemmPlan{});
@@ -712,10 +762,18 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
           ed.ldmask = c.C;
           ed.mask_type = kTA;
         }
+        if (pc.in_q) ed.rows = RowMap{1, c.H, c.W, c.H, c.W, pc.Hq, pc.Wq, pc.pad};  // dz (and mask) q-layout
       }
       ed.ldc = c.C;
       GemmOperand dy = op(w.dz[l], 0, 0);
       dy.conv = Im2col{1, static_cast<int>(b_), c.OH, c.OW, c.F, c.R, c.S, 1, c.R - 1 - c.pad, c.H, c.W};
+      if (c.in_q) {  // dz in q-layout: same geometry as x (same conv)
+        dy.conv.H = c.Hq;
+        dy.conv.W = c.Wq;
+        dy.conv.corners = 1;
+        dy.conv.lo = 0;
+        dy.conv.hi = -c.pad;
+      }
       const long long kd = static_cast<long long>(c.R) * c.S * c.F;  // dgrad reduces over (r, s, f)
       w.conv_dgrad.push_back(plan(dy, op(w.wrot[l], 0, kd), b_ * c.H * c.W, c.C, kd, ed));
     } else {
@@ -906,9 +964,11 @@ void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
       ++launches_;
     }
     gemm(w.conv_fwd[l], "conv_fwd", l);
+    OutLayout yl{};  // stage output in the next layer's q-layout
+    if (l + 1 < nc && g_.cg[l + 1].in_q) yl = OutLayout{g_.cg[l + 1].Hq, g_.cg[l + 1].Wq, g_.cg[l + 1].pad};
     if (c.lrn_n > 0 && c.pk > 0) {
       launch_lrn_pool_fwd<TA>(w.act[l], w.pool[l], w.widx[l], B, c.OH, c.OW, c.F, c.lrn_n, c.lrn_alpha,
-                              c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, st_);
+                              c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, st_, yl);
       ++launches_;
     } else if (c.lrn_n > 0) {
       launch_lrn_fwd<TA>(w.act[l], w.lrn[l], w.lrn_d[l], c.P, c.F, c.lrn_n, c.lrn_alpha, c.lrn_beta,
@@ -916,7 +976,7 @@ void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
       ++launches_;
     } else if (c.pk > 0) {
       launch_maxpool_fwd_w<TA>(w.act[l], w.pool[l], w.widx[l], B, c.OH, c.OW, c.F, c.pk, c.ps, c.PH,
-                               c.PW, st_);
+                               c.PW, st_, yl);
       ++launches_;
     }
   }
@@ -1084,13 +1144,14 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
   const ConvGeom& c = g_.cg[l];
   const TA* mask = c.relu ? w.act[l] : nullptr;
   const int B = static_cast<int>(b_);
+  const OutLayout zl = c.in_q ? OutLayout{c.Hq, c.Wq, c.pad} : OutLayout{};  // dz layout
   if (c.pk > 0 && c.lrn_n > 0) {
     launch_lrn_pool_bwd<TA>(cs.gout, w.widx[l], w.act[l], w.dz[l], B, c.OH, c.OW, c.F, c.lrn_n, c.lrn_alpha,
-                            c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, c.relu ? 1 : 0, st_);
+                            c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, c.relu ? 1 : 0, st_, zl);
     ++launches_;
   } else if (c.pk > 0) {
     launch_maxpool_bwd_w<TA, TA>(cs.gout, w.widx[l], w.dz[l], mask, B, c.OH, c.OW, c.F, c.pk, c.ps, c.PH,
-                                 c.PW, st_);
+                                 c.PW, st_, zl);
     ++launches_;
   } else if (c.lrn_n > 0) {
     launch_lrn_bwd<TA, TA>(w.act[l], w.lrn_d[l], cs.gout, w.dz[l], c.P, c.F, c.lrn_n, c.lrn_alpha,
@@ -1101,7 +1162,7 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
     ++launches_;
   }
   // bias grad = channel sums of dz (model.cpp:184-202)
-  launch_colsum<TA>(w.dz[l], c.P, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, st_);
+  launch_colsum<TA>(w.dz[l], c.Pq, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, st_);
   launches_ += 2;
   gemm(w.conv_wgrad[l], "conv_wgrad", l);
   if (c.s2d) {

@@ -26,6 +26,12 @@ struct ConvGeom {
   bool impl_dgrad = false;     // stride-1 dgrad as a conv over dY with rotated weights
   bool s2d = false;            // strided first layer as a stride-1 conv over its space-to-depth input
   int Rq = 0, Zh = 0, Zw = 0, Cz = 0;  // s2d: taps, z extents, padded z channels
+  // q-layout (see RowMap, gemm.cuh): this layer's input x and its dz are
+  // stored as (H+pad) x (W+pad) row slots per image with a shared zero border
+  // (stride-1 "same" convs): the conv is a flat shift of the row index.
+  bool in_q = false;
+  int Hq = 0, Wq = 0;
+  long long Pq = 0;  // b*Hq*Wq (rows of x / dz when in_q)
   long long ldk;               // padded row stride of col / kernels (16-byte multiple)
   long long P;                 // b*OH*OW rows per worker
   long long PP;                // b*PH*PW

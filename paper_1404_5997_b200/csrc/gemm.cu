@@ -55,7 +55,22 @@ __device__ __forceinline__ float sgd_apply(const Epi& e, long long off, float g)
   return nw;
 }
 
+// Output row of GEMM row m under e.rows (-1: not stored).
+__device__ __forceinline__ int map_row(const RowMap& r, int m) {
+  if (!r.enabled) return m;
+  const int plane = r.sH * r.sW;
+  const int b = m / plane, rem = m - b * plane;
+  const int y = rem / r.sW, x = rem - y * r.sW;
+  if (y >= r.vH || x >= r.vW) return -1;
+  return (b * r.dH + y + r.dp) * r.dW + x + r.dp;
+}
+
 __device__ __forceinline__ void epi_elem(const Epi& e, int m, int n, float v) {
+  const int gm = m;  // GEMM row (per-row bias)
+  if (e.rows.enabled) {
+    m = map_row(e.rows, m);
+    if (m < 0) return;
+  }
   const long long off = e.c_trans ? static_cast<long long>(n) * e.ldc + m
                                   : static_cast<long long>(m) * e.ldc + n;
   v *= e.alpha;
@@ -64,7 +79,7 @@ __device__ __forceinline__ void epi_elem(const Epi& e, int m, int n, float v) {
     sgd_apply(e, off, v);
     return;
   }
-  if (e.bias_mode == 1) v += e.bias[m];
+  if (e.bias_mode == 1) v += e.bias[gm];
   if (e.bias_mode == 2) v += e.bias[n];
   if (e.relu) v = v > 0.f ? v : 0.f;
   if (e.mask) {
@@ -99,7 +114,7 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
   }
   const Epi& e = a.epi;
   // Vector path: 32 contiguous outputs of row m (bias/ReLU/alpha/beta/mask fused).
-  const bool vec = !e.c_trans && n0 + 32 <= a.N &&
+  const bool vec = !e.rows.enabled && !e.c_trans && n0 + 32 <= a.N &&
                    (e.c_type == kF32 ? (e.ldc & 3) == 0 : (e.ldc & 7) == 0) &&
                    (!e.sgd_w || ((e.ldc & 7) == 0 && e.c_type == kF32)) &&
                    (!e.beta || e.c_type == kF32) &&
@@ -309,7 +324,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int
     return;
   }
   const Epi& e = a.epi;
-  if (!nfull) {  // ragged right edge: scalar, straight from the (warp-private) staged tile
+  if (!nfull) {  // ragged right edge: scalar, straight from the (warp-private) staged tile (epi_elem maps rows)
 #pragma unroll 1
     for (int i = 0; i < 8; ++i) {
       const int m = m0 + 4 * i + rsub;
@@ -318,7 +333,15 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int
     }
     return;
   }
-  // full 4-wide columns; rows may run past M
+  // full 4-wide columns; rows may run past M. mrow[i]: output row of GEMM row
+  // m0 + 4i + rsub (-1: past M or dropped by the row map); bias_mode 1 uses the
+  // GEMM row.
+  int mrow[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int m = m0 + 4 * i + rsub;
+    mrow[i] = m < a.M ? map_row(e.rows, m) : -1;
+  }
   float4 aux[8], aux2[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -330,10 +353,10 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int
   if (e.beta) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int m = m0 + 4 * i + rsub;
-      aux[i] = m < a.M ? *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.c) +
-                                                          static_cast<long long>(m) * e.ldc + n)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      const int m = mrow[i];
+      aux[i] = m >= 0 ? *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.c) +
+                                                         static_cast<long long>(m) * e.ldc + n)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -347,17 +370,17 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int
     // fused momentum SGD (optimizer.cpp:19-31): four rounded passes, no FMA
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int m = m0 + 4 * i + rsub;
+      const int m = mrow[i];
       const long long off = static_cast<long long>(m) * e.ldc + n;
-      if (m < a.M) {
+      if (m >= 0) {
         aux[i] = *reinterpret_cast<const float4*>(e.sgd_w + off);
         aux2[i] = *reinterpret_cast<const float4*>(e.sgd_m + off);
       }
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int m = m0 + 4 * i + rsub;
-      if (m >= a.M) continue;
+      const int m = mrow[i];
+      if (m < 0) continue;
       const long long off = static_cast<long long>(m) * e.ldc + n;
       float4 w4 = aux[i], m4 = aux2[i];
 #pragma unroll
@@ -408,8 +431,8 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int
   if (e.mask) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int m = m0 + 4 * i + rsub;
-      if (m >= a.M) continue;
+      const int m = mrow[i];
+      if (m < 0) continue;
       const long long mo = static_cast<long long>(m) * e.ldmask + n;
       aux[i] = e.mask_type == kBF16 ? ld_bf16x4(e.mask, mo)
                                     : *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.mask) + mo);
@@ -424,8 +447,8 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const int m = m0 + 4 * i + rsub;
-    if (m >= a.M) continue;
+    const int m = mrow[i];
+    if (m < 0) continue;
     const long long off = static_cast<long long>(m) * e.ldc + n;
     if (e.c_type == kF32) {
       *reinterpret_cast<float4*>(reinterpret_cast<float*>(e.c) + off) = x[i];
@@ -930,6 +953,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 
 // One fp32 4-vector (m, n..n+3) through the epilogue (vectorised epi_elem).
 __device__ __forceinline__ void epi_vec4(const Epi& e, int m, int n, float4 x) {
+  const int gm = m;  // GEMM row (per-row bias)
+  m = map_row(e.rows, m);
+  if (m < 0) return;
   const long long off = static_cast<long long>(m) * e.ldc + n;
   x.x *= e.alpha;
   x.y *= e.alpha;
@@ -961,7 +987,7 @@ __device__ __forceinline__ void epi_vec4(const Epi& e, int m, int n, float4 x) {
     return;
   }
   if (e.bias_mode == 1) {
-    const float bm = e.bias[m];
+    const float bm = e.bias[gm];
     x.x += bm;
     x.y += bm;
     x.z += bm;
@@ -1095,6 +1121,10 @@ CUtensorMap im2col_map(const void* ptr, int es, const Im2col& g, int pixels, boo
                            static_cast<cuuint64_t>(g.H) * g.W * g.C * es};
   int lower[2] = {-g.pad, -g.pad};                    // {W, H}
   int upper[2] = {g.pad - (g.S - 1), g.pad - (g.R - 1)};
+  if (g.corners) {
+    lower[0] = lower[1] = g.lo;
+    upper[0] = upper[1] = g.hi;
+  }
   cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(g.stride), static_cast<cuuint32_t>(g.stride), 1};
   CUresult r = encode_im2col_fn()(&m, es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                                   4, const_cast<void*>(ptr), dims, strides, lower, upper,
@@ -1117,8 +1147,8 @@ ConvArgs conv_args(const Im2col& g) {
   c.OH = g.OH;
   c.OW = g.OW;
   c.stride = g.stride;
-  c.lo_w = -g.pad;
-  c.lo_h = -g.pad;
+  c.lo_w = g.corners ? g.lo : -g.pad;
+  c.lo_h = g.corners ? g.lo : -g.pad;
   return c;
 }
 

@@ -25,6 +25,18 @@ enum MathMode : int {
   kMathF32x3 = 2,  // fp32 operands, 3xTF32 hi/lo split
 };
 
+// Epilogue row remap (im2col / q-layout outputs). GEMM row m is the pixel
+// (b, y, x) of a source grid sH x sW (m = (b*sH + y)*sW + x); it is stored
+// only if y < vH && x < vW, at row (b*dH + y + dp)*dW + x + dp of the output
+// (and of the mask). q-layout: an HxW image with pad p stored as (H+p) x (W+p)
+// row slots per image, pixel (h, w) at slot (h+p, w+p), zeros elsewhere -- the
+// zero border of one row/image doubles as the next one's, so a stride-1 conv
+// reads it as a flat shift of the row index.
+struct RowMap {
+  int enabled = 0;
+  int sH = 0, sW = 0, vH = 0, vW = 0, dH = 0, dW = 0, dp = 0;
+};
+
 struct Epi {
   void* c = nullptr;  // output
   long long ldc = 0;
@@ -49,6 +61,7 @@ struct Epi {
   void* sgd_copy = nullptr;  // optional bf16 operand copy of w (same offsets)
   float sgd_mu = 0.f, sgd_s1 = 0.f, sgd_s2 = 0.f, sgd_gscale = 1.f;
   int sgd_has_gscale = 0;
+  RowMap rows;  // rows.enabled: remap output (and mask) rows; not with c_trans / sgd
 };
 
 // Implicit-GEMM convolution operand: the matrix is the im2col view of an NHWC
@@ -62,7 +75,14 @@ struct Im2col {
   int N = 0, H = 0, W = 0, C = 0;  // activation tensor
   int R = 0, S = 0, stride = 1, pad = 0;
   int OH = 0, OW = 0;              // output pixels enumerated by the GEMM
+  // corners != 0: explicit im2col bounding box (both spatial dims) instead of
+  // the one implied by pad: base pixels lo .. extent-1+hi (stride 1). Used on
+  // zero-bordered "q-layout" tensors (see RowMap), where the padding is in
+  // memory and the box walks either the valid outputs (lo 0, hi -p) or every
+  // stored position (lo -p, hi -p).
+  int corners = 0, lo = 0, hi = 0;
 };
+
 
 struct GemmOperand {
   const void* ptr = nullptr;

@@ -538,7 +538,8 @@ __device__ __forceinline__ void st4<bf16>(bf16* p, const float* v) {
 template <class T>
 __global__ void __launch_bounds__(256) maxpool_fwd_w_kernel(const T* __restrict__ x, T* __restrict__ y,
                                                             uint8_t* __restrict__ widx, int H, int W, int C,
-                                                            int k, int s, int OH, int OW, int n4) {
+                                                            int k, int s, int OH, int OW, int n4, int YH, int YW,
+                                                            int yp) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n4) return;
   const int G = C >> 2;
@@ -563,7 +564,7 @@ __global__ void __launch_bounds__(256) maxpool_fwd_w_kernel(const T* __restrict_
     }
   }
   const long long o = static_cast<long long>(i) * 4;
-  st4<T>(y + o, best);
+  st4<T>(y + (static_cast<long long>(b * YH + oh + yp) * YW + ow + yp) * C + 4 * g, best);
   *reinterpret_cast<uint32_t*>(widx + o) =
       static_cast<uint32_t>(bi[0]) | (bi[1] << 8) | (bi[2] << 16) | (static_cast<uint32_t>(bi[3]) << 24);
 }
@@ -575,7 +576,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_w_kernel(const float* __restr
                                                             const uint8_t* __restrict__ widx,
                                                             TO* __restrict__ gx, const TM* __restrict__ mask,
                                                             int H, int W, int C, int k, int s, int OH, int OW,
-                                                            int n4) {
+                                                            int n4, int ZH, int ZW, int zp) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n4) return;
   const int G = C >> 2;
@@ -608,7 +609,7 @@ __global__ void __launch_bounds__(256) maxpool_bwd_w_kernel(const float* __restr
     for (int j = 0; j < 4; ++j)
       if (!(m[j] > 0.f)) acc[j] = 0.f;
   }
-  st4<TO>(gx + o, acc);
+  st4<TO>(gx + (static_cast<long long>(b * ZH + h + zp) * ZW + w + zp) * C + 4 * g, acc);
 }
 
 // ------------------------------------------------------------------ LRN + pool
@@ -636,7 +637,8 @@ template <class T, int HL, int NL, int PK, int PS>
 __global__ void __launch_bounds__(1024) lrn_pool_fwd_kernel(const T* __restrict__ a, T* __restrict__ y,
                                                             uint8_t* __restrict__ widx, int H, int W, int C,
                                                             int lo_, int hi_, float alpha, float beta, float kk,
-                                                            int pk_, int ps_, int PH, int PW, int TP) {
+                                                            int pk_, int ps_, int PH, int PW, int TP, int YH,
+                                                            int YW, int yp) {
   static_assert(HL <= 4 && 2 * HL + 1 >= NL, "halo");
   const int lo = NL ? NL / 2 : lo_, hi = NL ? (NL - 1) / 2 : hi_;
   const int pk = PK ? PK : pk_, ps = PS ? PS : ps_;
@@ -718,7 +720,7 @@ __global__ void __launch_bounds__(1024) lrn_pool_fwd_kernel(const T* __restrict_
         }
       }
       const long long o = (static_cast<long long>(b * PH + ph) * PW + pw) * C + c0;
-      stv<T>(y + o, best);
+      stv<T>(y + (static_cast<long long>(b * YH + ph + yp) * YW + pw + yp) * C + c0, best);
 #pragma unroll
       for (int j = 0; j < V; j += 4)
         *reinterpret_cast<uint32_t*>(widx + o + j) = static_cast<uint32_t>(bi[j]) | (bi[j + 1] << 8) |
@@ -736,7 +738,7 @@ template <class TA, int HL, int NL, int PK, int PS>
 __global__ void __launch_bounds__(512) lrn_pool_bwd_kernel(
     const float* __restrict__ gy, const uint8_t* __restrict__ widx, const TA* __restrict__ a,
     TA* __restrict__ dz, int H, int W, int C, int lo_, int hi_, float alpha, float beta, float kk, int pk_,
-    int ps_, int PH, int PW, int relu_mask) {
+    int ps_, int PH, int PW, int relu_mask, int ZH, int ZW, int zp) {
   static_assert(HL <= 4 && 2 * HL + 1 >= NL, "halo");
   const int lo = NL ? NL / 2 : lo_, hi = NL ? (NL - 1) / 2 : hi_;
   const int pk = PK ? PK : pk_, ps = PS ? PS : ps_;
@@ -827,7 +829,7 @@ __global__ void __launch_bounds__(512) lrn_pool_bwd_kernel(
     if (relu_mask && !(av[k] > 0.f)) gval = 0.f;
     out[k] = gval;
   }
-  if (live) stv<TA>(dz + px, out);
+  if (live) stv<TA>(dz + ((b * ZH + h + zp) * ZW + w + zp) * C + c0, out);
 }
 
 // Rotated operand for the implicit dgrad: wr[c][r][s][f] = w[f][R-1-r][S-1-s][c].
@@ -954,7 +956,8 @@ void launch_im2col_t_nchw(const float* x, T* colT, int B, int C, int H, int W, i
 template <class T>
 void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, int C, int n,
                          float alpha, float beta, float kk, int pk, int ps, int PH, int PW,
-                         cudaStream_t st) {
+                         cudaStream_t st, OutLayout yl) {
+  if (yl.H == 0) yl = OutLayout{PH, PW, 0};
   constexpr int V = 16 / sizeof(T);
   if (C % V != 0 || C / V > 384 || n > 2 * LH + 1)
     throw std::runtime_error("lrn_pool: C must be a multiple of 16 bytes (at most 384 vectors), size <= 9");
@@ -970,7 +973,8 @@ void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, i
   const dim3 grid((PH + TP - 1) / TP, B);
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    kern<<<grid, block, smem, st>>>(a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, TP);
+    kern<<<grid, block, smem, st>>>(a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, TP,
+                                    yl.H, yl.W, yl.p);
   };
   if (n == 5 && pk == 3 && ps == 2) {
     go(lrn_pool_fwd_kernel<T, 2, 5, 3, 2>);
@@ -984,7 +988,8 @@ void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, i
 template <class TA>
 void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* dz, int B, int H,
                          int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
-                         int PH, int PW, int relu_mask, cudaStream_t st) {
+                         int PH, int PW, int relu_mask, cudaStream_t st, OutLayout zl) {
+  if (zl.H == 0) zl = OutLayout{H, W, 0};
   constexpr int V = 16 / sizeof(TA);
   const int G = C / V;
   if (C % V != 0 || n > 2 * LH + 1 || G > 1024)
@@ -999,7 +1004,7 @@ void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* 
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     kern<<<grid, block, smem, st>>>(gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW,
-                                    relu_mask);
+                                    relu_mask, zl.H, zl.W, zl.p);
   };
   if (n == 5 && pk == 3 && ps == 2) {
     go(lrn_pool_bwd_kernel<TA, 2, 5, 3, 2>);
@@ -1012,19 +1017,22 @@ void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* 
 
 template <class T>
 void launch_maxpool_fwd_w(const T* x, T* y, uint8_t* widx, int B, int H, int W, int C, int k, int s,
-                          int OH, int OW, cudaStream_t st) {
+                          int OH, int OW, cudaStream_t st, OutLayout yl) {
+  if (yl.H == 0) yl = OutLayout{OH, OW, 0};
   if (C % 4 != 0) throw std::runtime_error("maxpool: channels must be a multiple of 4");
   const int n4 = static_cast<int>(static_cast<long long>(B) * OH * OW * C / 4);
-  maxpool_fwd_w_kernel<T><<<(n4 + 255) / 256, 256, 0, st>>>(x, y, widx, H, W, C, k, s, OH, OW, n4);
+  maxpool_fwd_w_kernel<T><<<(n4 + 255) / 256, 256, 0, st>>>(x, y, widx, H, W, C, k, s, OH, OW, n4, yl.H, yl.W,
+                                                             yl.p);
 }
 
 template <class TO, class TM>
 void launch_maxpool_bwd_w(const float* gy, const uint8_t* widx, TO* gx, const TM* mask, int B, int H,
-                          int W, int C, int k, int s, int OH, int OW, cudaStream_t st) {
+                          int W, int C, int k, int s, int OH, int OW, cudaStream_t st, OutLayout zl) {
+  if (zl.H == 0) zl = OutLayout{H, W, 0};
   if (C % 4 != 0) throw std::runtime_error("maxpool: channels must be a multiple of 4");
   const int n4 = static_cast<int>(static_cast<long long>(B) * H * W * C / 4);
   maxpool_bwd_w_kernel<TO, TM><<<(n4 + 255) / 256, 256, 0, st>>>(gy, widx, gx, mask, H, W, C, k, s, OH, OW,
-                                                                 n4);
+                                                                 n4, zl.H, zl.W, zl.p);
 }
 
 template <class T>
@@ -1067,12 +1075,12 @@ void launch_s2d_wgrad_gather(const float* dwz, float* dw, long long ldk, int F, 
   template void launch_im2col_nchw<T>(const float*, T*, int, int, int, int, int, int, int, int, int, \
                                       int, long long, cudaStream_t);                            \
   template void launch_lrn_pool_fwd<T>(const T*, T*, uint8_t*, int, int, int, int, int, float,   \
-                                       float, float, int, int, int, int, cudaStream_t);         \
+                                       float, float, int, int, int, int, cudaStream_t, OutLayout); \
   template void launch_lrn_pool_bwd<T>(const float*, const uint8_t*, const T*, T*, int, int, int, \
                                        int, int, float, float, float, int, int, int, int, int,  \
-                                       cudaStream_t);                                           \
+                                       cudaStream_t, OutLayout);                                \
   template void launch_maxpool_fwd_w<T>(const T*, T*, uint8_t*, int, int, int, int, int, int, int, \
-                                        int, cudaStream_t);                                     \
+                                        int, cudaStream_t, OutLayout);                          \
   template void launch_rotate_weights<T>(const float*, long long, T*, int, int, int, int,       \
                                          cudaStream_t);
 
@@ -1081,7 +1089,7 @@ INST_NEW(bf16)
 
 #define INST_MPB(TO, TM)                                                                        \
   template void launch_maxpool_bwd_w<TO, TM>(const float*, const uint8_t*, TO*, const TM*, int,  \
-                                             int, int, int, int, int, int, int, cudaStream_t);
+                                             int, int, int, int, int, int, int, cudaStream_t, OutLayout);
 INST_MPB(float, float)
 INST_MPB(float, bf16)
 INST_MPB(bf16, bf16)

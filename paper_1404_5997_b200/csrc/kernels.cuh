@@ -10,6 +10,13 @@
 
 namespace hp {
 
+// Where a pooling kernel stores its per-pixel output: an H x W grid of rows with
+// the image at offset (p, p) (q-layout, see RowMap in gemm.cuh). {0,0,0}: the
+// dense output grid.
+struct OutLayout {
+  int H = 0, W = 0, p = 0;
+};
+
 using bf16 = __nv_bfloat16;
 
 // Reference batch layout NCHW fp32 -> device NHWC T.
@@ -123,19 +130,19 @@ void launch_im2col_t_nchw(const float* x, T* colT, int B, int C, int H, int W, i
 template <class T>
 void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, int C, int n,
                          float alpha, float beta, float kk, int pk, int ps, int PH, int PW,
-                         cudaStream_t st);
+                         cudaStream_t st, OutLayout yl = {});
 // Fused backward: dz = relu_mask(a) * lrn_bwd(a, pool_bwd(gy, widx)).
 template <class TA>
 void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* dz, int B, int H,
                          int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
-                         int PH, int PW, int relu_mask, cudaStream_t st);
+                         int PH, int PW, int relu_mask, cudaStream_t st, OutLayout zl = {});
 // Max-pool forward / backward with window-offset argmax (no LRN).
 template <class T>
 void launch_maxpool_fwd_w(const T* x, T* y, uint8_t* widx, int B, int H, int W, int C, int k, int s,
-                          int OH, int OW, cudaStream_t st);
+                          int OH, int OW, cudaStream_t st, OutLayout yl = {});
 template <class TO, class TM>
 void launch_maxpool_bwd_w(const float* gy, const uint8_t* widx, TO* gx, const TM* mask, int B, int H,
-                          int W, int C, int k, int s, int OH, int OW, cudaStream_t st);
+                          int W, int C, int k, int s, int OH, int OW, cudaStream_t st, OutLayout zl = {});
 
 // wrot[c][r][s][f] = w[f][R-1-r][S-1-s][c] (w rows of stride ldk), cast to T:
 // the stride-1 dgrad as a convolution over dY.
