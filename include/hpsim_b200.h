@@ -227,6 +227,9 @@ HP_API int hp_cluster_set_profile(hp_cluster* c, int on);
 /* FC weight update fused into the FC wgrad GEMM epilogue (default on); off
  * stores the FC gradients and runs the multi-tensor SGD kernel instead. */
 HP_API int hp_cluster_set_fuse_fc_sgd(hp_cluster* c, int on);
+/* bf16 stride-1 convs through the flat-shift kernel (default on); off uses the
+ * TMA-im2col implicit GEMM for them (A/B comparisons; rebuilds the plans). */
+HP_API int hp_cluster_set_shift_conv(hp_cluster* c, int on);
 /* Replay each step as a captured CUDA graph (default on). A graph is keyed by
  * the step's input pointers, memory kind and scalars; it is captured the second
  * time a key is seen (the first runs eagerly) and replayed afterwards. Host
@@ -298,6 +301,14 @@ HP_API int hp_kernel_conv_wgrad(int math, const void* x, int B, int H, int W, in
 HP_API int hp_kernel_conv_dgrad(int math, const void* dy, int B, int OH, int OW, int F,
                                 const void* wrot, int C, int R, int S, int pad, float* dx,
                                 void* stream);
+/* Stride-1 conv as a flat-shift implicit GEMM on tcgen05 (bf16, CTA pairs):
+ * y[rows][N] fp32 = sum_{r,s} x[row + r*wq + s][0..C) . w[N][(r*S+s)*C + c],
+ * one smem halo per 64-channel block reused by all R*S taps. x is a
+ * zero-bordered "q-layout" activation (or any [rows][C] bf16 matrix); border
+ * and wrap-around rows of y are garbage. C % 64 == 0, 128 + (R-1)*wq + S-1 <= 256.
+ * Replaces conv2d_forward / the stride-1 conv2d_backward dgrad (tensor.cpp:419-516). */
+HP_API int hp_kernel_conv_shift(const void* x, int64_t rows, int C, int R, int S, int wq, const void* w,
+                                int N, float* y, int boff_mode, void* stream);
 
 #ifdef __cplusplus
 }

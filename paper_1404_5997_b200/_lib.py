@@ -128,6 +128,8 @@ def _load() -> C.CDLL:
         "hp_gaussian_fill": ([C.c_uint64, C.POINTER(C.c_double), C.c_int64], None),
         "hp_gaussian_fill_f32": ([C.c_uint64, C.c_double, C.POINTER(C.c_float), C.c_int64], None),
         "hp_kernel_gemm": ([C.POINTER(HpGemmDesc), P], C.c_int),
+        "hp_kernel_conv_shift": ([P, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, P, C.c_int, P],
+                                 C.c_int),
         "hp_kernel_gemm_splits": ([C.POINTER(HpGemmDesc)], C.c_int),
         "hp_debug_gemm_force": ([C.c_int, C.c_int], None),
         "hp_kernel_conv_fprop": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int,
@@ -162,6 +164,7 @@ def _load() -> C.CDLL:
         "hp_cluster_last_gemm_flops": ([P], C.c_double),
         "hp_cluster_set_profile": ([P, C.c_int], C.c_int),
         "hp_cluster_set_fuse_fc_sgd": ([P, C.c_int], C.c_int),
+        "hp_cluster_set_shift_conv": ([P, C.c_int], C.c_int),
         "hp_cluster_set_graphs": ([P, C.c_int], C.c_int),
         "hp_cluster_gemm_profile": ([P, C.POINTER(HpGemmProf), C.c_int], C.c_int),
     }

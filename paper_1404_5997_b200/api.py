@@ -389,6 +389,10 @@ class Cluster:
         """FC weight update in the wgrad GEMM epilogue (default on)."""
         _check(lib.hp_cluster_set_fuse_fc_sgd(self._h, int(bool(on))))
 
+    def set_shift_conv(self, on: bool) -> None:
+        """bf16 stride-1 convs via the flat-shift kernel (default on) or TMA im2col."""
+        _check(lib.hp_cluster_set_shift_conv(self._h, int(bool(on))))
+
     def set_profile(self, on: bool) -> None:
         _check(lib.hp_cluster_set_profile(self._h, int(bool(on))))
 

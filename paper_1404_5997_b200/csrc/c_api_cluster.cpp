@@ -152,6 +152,13 @@ HP_API int hp_cluster_set_fuse_fc_sgd(hp_cluster* c, int on) {
   return guarded_c([&] { c->impl->fuse_fc_sgd = on != 0; });
 }
 
+HP_API int hp_cluster_set_shift_conv(hp_cluster* c, int on) {
+  return guarded_c([&] {
+    c->impl->use_shift = on != 0;
+    c->impl->rebuild_plans();
+  });
+}
+
 HP_API int hp_cluster_set_profile(hp_cluster* c, int on) {
   return guarded_c([&] { c->impl->profile = on != 0; });
 }

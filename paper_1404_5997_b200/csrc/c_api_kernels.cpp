@@ -161,4 +161,21 @@ HP_API int hp_kernel_conv_dgrad(int math, const void* dy, int B, int OH, int OW,
   });
 }
 
+/* Flat-shift implicit-GEMM conv (bf16, see conv_shift_plan): y[rows][N] (fp32,
+ * every row position; border rows hold garbage) = sum over taps of
+ * x[row + r*wq + s][C] . w[N][(r*S+s)*C + c]. Returns HP_ERR_CONFIG when the
+ * shape is unsupported. boff_mode: descriptor base-offset convention (dev). */
+HP_API int hp_kernel_conv_shift(const void* x, int64_t rows, int C, int R, int S, int wq, const void* w, int N,
+                                float* y, int boff_mode, void* stream) {
+  return guarded([&] {
+    Epi e;
+    e.c = y;
+    e.ldc = N;
+    GemmPlan p = conv_shift_plan(x, rows, C, R, S, wq, w, static_cast<long long>(R) * S * C, N, e, boff_mode);
+    if (!p.valid) config_error("conv_shift: unsupported shape");
+    gemm_launch(p, static_cast<cudaStream_t>(stream));
+    HP_CUDA(cudaGetLastError());
+  });
+}
+
 }  // extern "C"

@@ -305,6 +305,13 @@ class ClusterImpl final : public ClusterBase {
   ~ClusterImpl() override;
   void* stream() const override { return st_; }
   void prefetch(const float* const* batches, const float* const* targets) override;
+  void rebuild_plans() override {
+    HP_CUDA(cudaStreamSynchronize(st_));
+    for (auto& kv : graphs_)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    graphs_.clear();
+    for (auto& w : w_) build_plans(w);
+  }
   void run_step(const float* const* batches, const float* const* targets, int mem_kind,
                 const hp_hyper& hp, double lr, hp_step_metrics* out) override;
   int64_t param_size(int worker, int which, int layer) const override;
@@ -587,8 +594,14 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   for (auto& e : ev_layer_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   HP_CUDA(cudaMallocHost(&host_parts_, sizeof(double) * nl * num_sub_ * xblocks_));
   HP_CUDA(cudaMallocHost(&host_bad_, sizeof(int) * nl));
-  // Plans first with a null workspace to size it, then for real.
-  for (auto& w : w_) build_plans(w);
+  // Plans first with a null workspace to size it (for both conv kernel
+  // families, so rebuild_plans can switch), then for real.
+  const bool shift = use_shift;
+  for (bool sh : {false, true}) {
+    use_shift = sh;
+    for (auto& w : w_) build_plans(w);
+  }
+  use_shift = shift;
   ws_ = ws_floats_ > 0 ? arena_.make<float>(static_cast<long long>(ws_floats_)) : nullptr;
   for (auto& w : w_) build_plans(w);
   init_params();
@@ -711,7 +724,23 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     }
     const long long Kz = static_cast<long long>(c.Rq) * c.Rq * c.Cz;
     const Im2col zview{1, static_cast<int>(b_), c.Zh, c.Zw, c.Cz, c.Rq, c.Rq, 1, 0, c.OH, c.OW};
-    if (c.s2d) {
+    // bf16 stride-1 convs over zero-bordered rows: the flat-shift kernel (one
+    // smem halo per channel block for all taps); output rows are the stored
+    // grid, the RowMap keeps the valid ones
+    // Measured on B200 (tests/dev/step_dev.py): the shift kernel wins on the
+    // 3x3 layers (fewer, wider K blocks per halo); the TMA-im2col kernel is as
+    // fast or faster on the 5x5 / space-to-depth layers with 64-wide operands.
+    const bool shift_fwd = bf && use_shift && !c.s2d && c.R <= 3 && c.in_q &&
+                           conv_shift_supported(c.C, c.R, c.S, c.Wq, c.F);
+    if (shift_fwd) {
+      Epi es = e;
+      const int gH = c.s2d ? c.Zh : c.Hq, gW = c.s2d ? c.Zw : c.Wq;
+      es.rows = e.rows.enabled ? RowMap{1, gH, gW, c.OH, c.OW, e.rows.dH, e.rows.dW, e.rows.dp}
+                               : RowMap{1, gH, gW, c.OH, c.OW, c.OH, c.OW, 0};
+      GemmPlan pl = c.s2d ? conv_shift_plan(w.z, b_ * gH * gW, c.Cz, c.Rq, c.Rq, gW, w.wz, Kz, c.F, es)
+                          : conv_shift_plan(in, c.Pq, c.C, c.R, c.S, gW, kw, c.ldk, c.F, es);
+      w.conv_fwd.push_back(pl);
+    } else if (c.s2d) {
       xa = op(w.z, 0, 0);
       xa.conv = zview;
       w.conv_fwd.push_back(plan(xa, op(w.wz, 0, Kz), c.P, c.F, Kz, e));
@@ -775,7 +804,14 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
         dy.conv.hi = -c.pad;
       }
       const long long kd = static_cast<long long>(c.R) * c.S * c.F;  // dgrad reduces over (r, s, f)
-      w.conv_dgrad.push_back(plan(dy, op(w.wrot[l], 0, kd), b_ * c.H * c.W, c.C, kd, ed));
+      if (bf && use_shift && c.in_q && c.R <= 3 && conv_shift_supported(c.F, c.R, c.S, c.Wq, c.C)) {
+        // dX over the stored q grid of dz: rows (b, h, w) valid for h < H, w < W
+        ed.rows = ed.rows.enabled ? RowMap{1, c.Hq, c.Wq, c.H, c.W, ed.rows.dH, ed.rows.dW, ed.rows.dp}
+                                  : RowMap{1, c.Hq, c.Wq, c.H, c.W, c.H, c.W, 0};
+        w.conv_dgrad.push_back(conv_shift_plan(w.dz[l], c.Pq, c.F, c.R, c.S, c.Wq, w.wrot[l], kd, c.C, ed));
+      } else {
+        w.conv_dgrad.push_back(plan(dy, op(w.wrot[l], 0, kd), b_ * c.H * c.W, c.C, kd, ed));
+      }
     } else {
       // dcol[P][Kc] = dz[P][F] . W[F][Kc], then col2im
       Epi ed;

@@ -72,6 +72,7 @@ class ClusterBase {
                             float* const* fb) = 0;
 
   virtual void* stream() const = 0;
+  virtual void rebuild_plans() = 0;  // after a kernel-choice toggle (drops captured graphs)
   // Stage the NEXT step's host batches/targets into a device slot on the copy
   // stream (async); a later run_step with the same host pointers consumes the
   // slot instead of copying on the compute stream (double buffering: the copy
@@ -87,6 +88,7 @@ class ClusterBase {
   bool profile = false;            // bracket every GEMM with CUDA events
   bool use_graphs = true;          // replay the step as a captured CUDA graph
   bool fuse_fc_sgd = true;         // FC weight update in the wgrad GEMM epilogue
+  bool use_shift = true;           // bf16 stride-1 convs via the flat-shift kernel (else TMA im2col)
   std::vector<GemmProf> prof;      // last step, launch order
   double prof_gemm_ms = 0.0;
   double last_gemm_flops = 0.0;    // algorithmic GEMM FLOPs of the last step

@@ -287,26 +287,50 @@ __device__ __forceinline__ void f4set(float4& v, int j, float x) {
   else v.w = x;
 }
 
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a)
+               : "memory");
+  return v;
+}
+
+// Output rows of the 8 GEMM rows m0 + 4i + (lane >> 3) a thread stores in
+// epi_chunk (-1: past M or dropped by the RowMap). Depends only on the tile
+// and the thread, so the kernels compute it once per tile.
+__device__ __forceinline__ void epi_rows(const GemmArgs& a, int m0, int (&mrow)[8]) {
+  const int rsub = (threadIdx.x & 31) >> 3;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int m = m0 + 4 * i + rsub;
+    mrow[i] = m < a.M ? map_row(a.epi.rows, m) : -1;
+  }
+}
+
 // Epilogue of one warp's 32 rows [m0, m0+32) x 32 columns [n0, n0+32).
 // All 32 lanes must call it (warp-synchronous); `stg` is the warp's tile.
 __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int split, const float (&v)[32],
-                                          float* stg) {
+                                          float* stg, const int (&mrow)[8]) {
   const int lane = threadIdx.x & 31;
   if (!epi_vec_ok(a)) {  // transposed outputs: the row-per-thread layout is the coalesced one
     epi_row32(a, m0 + lane, n0, split, v);
     return;
   }
+  const uint32_t sbase = smem_u32(stg);
+  __syncwarp();  // the previous chunk's reads of the tile are done
 #pragma unroll
   for (int i = 0; i < 8; ++i)
-    *reinterpret_cast<float4*>(stg + lane * kEpiLd + 4 * i) =
-        make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    sts128(sbase + (lane * kEpiLd + 4 * i) * 4, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
   __syncwarp();
   const int rsub = lane >> 3, cq = (lane & 7) * 4;
   const int n = n0 + cq;
   float4 x[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) x[i] = *reinterpret_cast<const float4*>(stg + (4 * i + rsub) * kEpiLd + cq);
-  __syncwarp();  // the tile may be overwritten by the next chunk
+  for (int i = 0; i < 8; ++i) x[i] = lds128(sbase + ((4 * i + rsub) * kEpiLd + cq) * 4);
+  // (the next chunk's entry __syncwarp orders these reads before its writes)
   const bool nfull = n + 4 <= a.N;
   if (a.raw_partial) {
     float* dst = a.ws + static_cast<long long>(split) * a.M * a.N;
@@ -333,15 +357,8 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int
     }
     return;
   }
-  // full 4-wide columns; rows may run past M. mrow[i]: output row of GEMM row
-  // m0 + 4i + rsub (-1: past M or dropped by the row map); bias_mode 1 uses the
-  // GEMM row.
-  int mrow[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int m = m0 + 4 * i + rsub;
-    mrow[i] = m < a.M ? map_row(e.rows, m) : -1;
-  }
+  // full 4-wide columns; mrow[i]: output row of GEMM row m0 + 4i + rsub (-1:
+  // past M or dropped by the row map); bias_mode 1 uses the GEMM row.
   float4 aux[8], aux2[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -728,6 +745,8 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
       tc_fence_after();
       float* stg = reinterpret_cast<float*>(smem + STAGES * SB + 256) + q * 32 * kEpiLd;
       const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf) * ACOLS;
+      int mrow[8];
+      epi_rows(args, ti.m0 + q * 32, mrow);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
@@ -740,7 +759,7 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (ti.n0 + c < args.N) epi_chunk(args, ti.m0 + q * 32, ti.n0 + c, ti.split, v, stg);
+        if (ti.n0 + c < args.N) epi_chunk(args, ti.m0 + q * 32, ti.n0 + c, ti.split, v, stg, mrow);
       }
     }
   }
@@ -927,6 +946,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       tc_fence_after();
       float* stg = reinterpret_cast<float*>(smem + STAGES * SB + 256) + q * 32 * kEpiLd;
       const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf) * ACOLS;
+      int mrow[8];
+      epi_rows(args, m0 + static_cast<int>(rank) * kBM + q * 32, mrow);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
@@ -939,7 +960,199 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (n0 + c < args.N) epi_chunk(args, m0 + static_cast<int>(rank) * kBM + q * 32, n0 + c, split, v, stg);
+        if (n0 + c < args.N) epi_chunk(args, m0 + static_cast<int>(rank) * kBM + q * 32, n0 + c, split, v, stg, mrow);
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2(tmem, TCOLS);
+  }
+}
+
+// ---------------------------------------------------------------- shift conv
+// See conv_shift_plan (gemm.cuh). Warp roles as gemm2_kernel; per tile the
+// K loop is (channel block cb) x (tap r, s): one halo TMA per cb (both CTAs,
+// own 128 rows + halo), one weight-tile TMA per (tap, cb), 4 MMAs per tap whose
+// A descriptor starts (r*wq + s) rows into the halo.
+constexpr uint32_t kHaloBytes = 256u * 128u;
+__host__ __device__ constexpr uint32_t shift_b_bytes(int bn) { return static_cast<uint32_t>(bn / 2) * 128u; }
+__host__ __device__ constexpr int shift_stages(int bn) {
+  return static_cast<int>((kMaxDynSmem - 2304u - kEpiSmemBytes - 2u * kHaloBytes) / shift_b_bytes(bn)) > 12
+             ? 12
+             : static_cast<int>((kMaxDynSmem - 2304u - kEpiSmemBytes - 2u * kHaloBytes) / shift_b_bytes(bn));
+}
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    conv_shift_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                      const GemmArgs args) {
+  constexpr int BNH = BN / 2;
+  constexpr uint32_t B_BYTES = shift_b_bytes(BN);
+  constexpr int STAGES = shift_stages(BN);
+  constexpr uint32_t ACOLS = tmem_cols(BN);
+  constexpr uint32_t TCOLS = ACOLS * 2;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* halo = smem;                       // [2][256 rows][128 B]
+  uint8_t* bst = smem + 2 * kHaloBytes;       // [STAGES][BNH rows][128 B]
+  uint64_t* full = reinterpret_cast<uint64_t*>(bst + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* hfull = empty + STAGES;  // [2]
+  uint64_t* hempty = hfull + 2;      // [2]
+  uint64_t* tfull = hempty + 2;      // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stg_base = reinterpret_cast<float*>(bst + STAGES * B_BYTES + 512);  // barriers: < 512 B
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int cid = blockIdx.x >> 1;
+  const int ncl = gridDim.x >> 1;
+  const int tiles_m = (args.M + 2 * kBM - 1) / (2 * kBM);
+  const int tiles_n = (args.N + BN - 1) / BN;
+  const int total = tiles_m * tiles_n;
+  const int cblocks = args.sh_C / 64;
+  const int taps = args.sh_R * args.sh_S;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&hfull[i], 1);
+      mbar_init(&hempty[i], 1);
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 256);  // both CTAs' epilogue threads (leader's copy is used)
+    }
+    fence_barrier_init();
+    tma_prefetch(&ta);
+    tma_prefetch(&tb);
+  }
+  if (warp == 1) tmem_alloc2(tslot, TCOLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0, hb = 0;
+      uint32_t phase = 0, hphase = 0;
+      const uint32_t halo_tx = static_cast<uint32_t>(args.sh_halo) * 128u;
+      for (int t = cid; t < total; t += ncl) {
+        const int mb = t / tiles_n;
+        const int m0 = mb * 2 * kBM, n0 = (t - mb * tiles_n) * BN;
+        const int am = m0 + static_cast<int>(rank) * kBM;
+        const int bn0 = n0 + static_cast<int>(rank) * BNH;
+        for (int cb = 0; cb < cblocks; ++cb) {
+          mbar_wait(&hempty[hb], hphase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&hfull[hb], 2 * halo_tx);
+          tma_load_2d_2sm(halo + hb * kHaloBytes, &ta, &hfull[hb], cb * 64, am);
+          if (++hb == 2) {
+            hb = 0;
+            hphase ^= 1;
+          }
+          for (int tap = 0; tap < taps; ++tap) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * B_BYTES);
+            tma_load_2d_2sm(bst + stage * B_BYTES, &tb, &full[stage], tap * args.sh_C + cb * 64, bn0);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                             (static_cast<uint32_t>((2 * kBM) >> 4) << 24);
+      int stage = 0, hb = 0, local = 0;
+      uint32_t phase = 0, hphase = 0;
+      const uint32_t halo0 = smem_u32(halo);
+      for (int t = cid; t < total; t += ncl, ++local) {
+        const int buf = local & 1;
+        const uint32_t use = static_cast<uint32_t>(local >> 1);
+        mbar_wait(&tempty[buf], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + static_cast<uint32_t>(buf) * ACOLS;
+        uint32_t acc = 0;
+        for (int cb = 0; cb < cblocks; ++cb) {
+          mbar_wait(&hfull[hb], hphase);
+          tc_fence_after();
+          const uint32_t hbase = halo0 + static_cast<uint32_t>(hb) * kHaloBytes;
+          for (int r = 0; r < args.sh_R; ++r)
+            for (int sx = 0; sx < args.sh_S; ++sx) {
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              const uint32_t a0 = hbase + static_cast<uint32_t>(r * args.sh_wq + sx) * 128u;
+              const uint32_t sb = smem_u32(bst + stage * B_BYTES);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint32_t aa = a0 + k * 32;
+                // The 128B swizzle is a function of the ABSOLUTE smem address bits
+                // (TMA wrote the halo 1024-aligned), so a descriptor starting any
+                // whole row into the halo reads rows aa.. correctly with the
+                // descriptor base offset left 0 (measured: setting it to
+                // (aa >> 7) & 7 double-applies the phase).
+                uint64_t ad = umma_desc_sw128(aa, 16, 1024, 2);
+                if (args.sh_boff) ad |= static_cast<uint64_t>((aa >> 7) & 7u) << 49;
+                const uint64_t bd = umma_desc_sw128(sb + k * 32, 16, 1024, 2);
+                mma_f16_2sm(d, ad, bd, idesc, acc);
+                acc = 1;
+              }
+              mma_commit_2sm(&empty[stage]);
+              if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+              }
+            }
+          mma_commit_2sm(&hempty[hb]);
+          if (++hb == 2) {
+            hb = 0;
+            hphase ^= 1;
+          }
+        }
+        mma_commit_2sm(&tfull[buf]);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    const uint32_t tempty_leader[2] = {mapa(smem_u32(&tempty[0]), 0), mapa(smem_u32(&tempty[1]), 0)};
+    float* stg = stg_base + q * 32 * kEpiLd;
+    int local = 0;
+    for (int t = cid; t < total; t += ncl, ++local) {
+      const int mb = t / tiles_n;
+      const int m0 = mb * 2 * kBM, n0 = (t - mb * tiles_n) * BN;
+      const int buf = local & 1;
+      const uint32_t use = static_cast<uint32_t>(local >> 1);
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+      const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf) * ACOLS;
+      int mrow[8];
+      epi_rows(args, m0 + static_cast<int>(rank) * kBM + q * 32, mrow);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(base + static_cast<uint32_t>(c), r);
+        tmem_ld_wait();
+        if (c + 32 >= BN) {
+          tc_fence_before();
+          mbar_arrive_cluster(tempty_leader[buf]);
+        }
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (n0 + c < args.N) epi_chunk(args, m0 + static_cast<int>(rank) * kBM + q * 32, n0 + c, 0, v, stg, mrow);
       }
     }
   }
@@ -1413,8 +1626,77 @@ void epi_apply_launch(const float* ws, int splits, int M, int N, const Epi& e, c
   epi_apply_kernel<<<blocks, threads, 0, s>>>(ws, splits, M, N, e, vec ? 1 : 0);
 }
 
+
+bool conv_shift_supported(int C, int R, int S, int wq, int N) {
+  return C % 64 == 0 && R >= 1 && S >= 1 && 128 + (R - 1) * wq + (S - 1) <= 256 && N >= 16;
+}
+
+GemmPlan conv_shift_plan(const void* x, long long rows, int C, int R, int S, int wq, const void* w, long long ldw,
+                         int N, const Epi& epi, int boff_mode) {
+  GemmPlan p;
+  if (!conv_shift_supported(C, R, S, wq, N) || rows >= (1LL << 31)) return p;
+  p.math = kMathBF16;
+  p.shift = true;
+  p.cta2 = true;
+  // N tile: widest of 256/192/128/64 with the least padding
+  int best = 256;
+  double best_fill = -1.0;
+  for (int bn : {256, 192, 128, 64}) {
+    const int nt = cdiv(N, bn);
+    const double fill = static_cast<double>(N) / (static_cast<double>(nt) * bn);
+    if (fill > best_fill + 1e-9) {
+      best_fill = fill;
+      best = bn;
+    }
+  }
+  p.bn = best;
+  p.splits = 1;
+  const int halo = 128 + (R - 1) * wq + (S - 1);
+  p.args.M = static_cast<int>(rows);
+  p.args.N = N;
+  p.args.K = R * S * C;
+  p.args.k_tiles_total = R * S * (C / 64);
+  p.args.k_tiles_per_split = p.args.k_tiles_total;
+  p.args.epi = epi;
+  p.args.sh_R = R;
+  p.args.sh_S = S;
+  p.args.sh_wq = wq;
+  p.args.sh_C = C;
+  p.args.sh_halo = halo;
+  p.args.sh_boff = boff_mode;
+  p.ta = make_map(x, 2, C, rows, C, 64, halo, CU_TENSOR_MAP_SWIZZLE_128B);
+  p.tb = make_map(w, 2, static_cast<long long>(R) * S * C, N, ldw, 64, p.bn / 2, CU_TENSOR_MAP_SWIZZLE_128B);
+  const int total = cdiv(rows, 2 * kBM) * cdiv(N, p.bn);
+  p.grid = dim3(2 * std::min(total, 74));
+  p.smem = 2 * kHaloBytes + static_cast<size_t>(shift_stages(p.bn)) * shift_b_bytes(p.bn) + 1024 + 512 +
+           kEpiSmemBytes;
+  p.valid = true;
+  return p;
+}
+
+template <int BN>
+void launch_shift(const GemmPlan& p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(conv_shift_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kMaxDynSmem));
+    attr = true;
+  }
+  conv_shift_kernel<BN><<<p.grid, 192, p.smem, s>>>(p.ta, p.tb, p.args);
+}
+
 void gemm_launch(const GemmPlan& p, cudaStream_t s) {
   if (!p.valid) throw std::runtime_error("gemm: invalid plan");
+  if (p.shift) {
+    switch (p.bn) {
+      case 64: launch_shift<64>(p, s); break;
+      case 128: launch_shift<128>(p, s); break;
+      case 192: launch_shift<192>(p, s); break;
+      case 256: launch_shift<256>(p, s); break;
+      default: throw std::runtime_error("conv_shift: unsupported BN");
+    }
+    return;
+  }
   switch (p.math) {
     case kMathBF16: launch_math<kMathBF16>(p, s); break;
     case kMathTF32: launch_math<kMathTF32>(p, s); break;

@@ -104,6 +104,9 @@ struct GemmArgs {
   float* ws;
   Epi epi;
   ConvArgs ca, cb;  // im2col bookkeeping for A / B
+  // shift conv (conv_shift_plan): taps R x S, flat row shift r*wq + s, C
+  // channels per tap (64-channel blocks), halo rows per CTA, base-offset mode
+  int sh_R, sh_S, sh_wq, sh_C, sh_halo, sh_boff;
 };
 
 // A fully prepared GEMM launch (tensor maps encoded once, reused every step).
@@ -115,6 +118,7 @@ struct GemmPlan {
   int splits = 1;
   bool cta2 = false;  // CTA-pair kernel (M=256 tiles, cta_group::2)
   bool light = false; // 2-stage, 1-accumulator, 2-CTA/SM kernel (short K, fused SGD epilogue)
+  bool shift = false; // stride-1 conv as flat row shifts of one smem halo per channel block
   dim3 grid;
   size_t smem = 0;
   bool valid = false;
@@ -131,6 +135,20 @@ void gemm_force_config(int cta2, int bn);
 int gemm_choose_splits(int math, int M, int N, int K, int bn = 0);
 int gemm_choose_bn(int M, int N);
 void gemm_launch(const GemmPlan& p, cudaStream_t s);
+
+// Stride-1 convolution as a flat-shift implicit GEMM (bf16, CTA pairs): the
+// input x is a [rows][C] bf16 matrix in which output row o reads rows
+// o + r*wq + s for the R x S taps (q-layout or a pad-free grid such as conv1's
+// space-to-depth input). Per 64-channel block each CTA stages ONE halo of
+// 128 + (R-1)*wq + (S-1) rows (<= 256) in swizzled smem and every tap's A
+// operand is a row-shifted UMMA descriptor into it (no per-tap re-load). B is
+// the [N][R*S*C] K-major kernel matrix (k = (r*S+s)*C + c). Output rows are the
+// M = rows positions (the epilogue's RowMap drops the border / garbage rows);
+// w rows have stride ldw >= R*S*C.
+// Returns an invalid plan (valid = false) when the shape is unsupported.
+GemmPlan conv_shift_plan(const void* x, long long rows, int C, int R, int S, int wq, const void* w, long long ldw,
+                         int N, const Epi& epi, int boff_mode = 0);
+bool conv_shift_supported(int C, int R, int S, int wq, int N);
 
 // Applies an Epi elementwise to a fp32 [M][N] source (used after split-K and
 // by the kernel tests).

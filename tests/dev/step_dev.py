@@ -19,9 +19,10 @@ batches = [hp.synthetic_batch(spec, 128, step=s) for s in range(4)]
 dev = [(torch.from_numpy(x).cuda(), torch.from_numpy(t).cuda()) for x, t in batches]
 
 if what == "time":
-    for fuse in (True, False):
+    for fuse, shift in ((True, True), (True, False)):
         c = make()
         c.set_fuse_fc_sgd(fuse)
+        c.set_shift_conv(shift)
         hyper = hp.HyperParams(momentum=0.9, lr=0.001, weight_decay=5e-4)
         for s in range(12):
             x, t = dev[s % 4]
@@ -43,7 +44,7 @@ if what == "time":
                 a[1] += pms / 3
         c.set_profile(False)
         tot = sum(v[1] for v in per.values())
-        print(f"fuse={fuse}: step {np.median(ms):.3f} ms (min {min(ms):.3f}), gemm {tot:.3f} ms, "
+        print(f"fuse={fuse} shift={shift}: step {np.median(ms):.3f} ms (min {min(ms):.3f}), gemm {tot:.3f} ms, "
               f"{128 / np.median(ms) * 1e3:.0f} img/s")
         for k, (f, t) in sorted(per.items(), key=lambda kv: -kv[1][1]):
             print(f"   {k:16s} {t:7.3f} ms {f / 1e9:7.2f} GF {f / t / 1e9:7.1f} TF/s")

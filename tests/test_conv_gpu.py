@@ -71,3 +71,44 @@ def test_fprop_wgrad_dgrad(math, shape):
         torch.cuda.synchronize()
         rdx = xt.grad.permute(0, 2, 3, 1).reshape(B * H * H, Cc)
         assert (dx.double() - rdx).abs().max().item() / rdx.abs().max().item() < tol
+
+
+def to_q(x, p):
+    """NHWC [B][H][W][C] -> q-layout rows [(B*(H+p)*(W+p))][C]: pixel (h, w) at
+    slot (h+p, w+p) of its image's (H+p) x (W+p) block, zeros elsewhere."""
+    B, H, W, C = x.shape
+    q = torch.zeros(B, H + p, W + p, C, dtype=x.dtype, device=x.device)
+    q[:, p:, p:, :] = x
+    return q.reshape(-1, C).contiguous()
+
+
+SHIFT_SHAPES = [  # B, C, H, F, R (stride 1, same padding)
+    (2, 64, 27, 192, 5),    # AlexNet conv2 fprop
+    (2, 192, 13, 384, 3),   # conv3
+    (3, 384, 13, 256, 3),   # conv5
+    (2, 192, 27, 64, 5),    # conv2 dgrad shape (N = 64)
+    (1, 128, 9, 128, 1),    # 1x1
+]
+
+
+@pytest.mark.parametrize("shape", SHIFT_SHAPES)
+def test_conv_shift_q_layout(shape):
+    """Flat-shift implicit GEMM (one smem halo per channel block, row-shifted
+    UMMA descriptors per tap) on a q-layout input == torch conv2d (fp64 on the
+    bf16-rounded operands) at every valid output position."""
+    B, C, H, Fo, R = shape
+    p = (R - 1) // 2
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randn(B, H, H, C, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(Fo, R, R, C, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    xq = to_q(x, p)
+    rows = xq.shape[0]
+    y = torch.full((rows, Fo), float("nan"), device="cuda")
+    rc = lib.hp_kernel_conv_shift(xq.data_ptr(), rows, C, R, R, H + p, w.data_ptr(), Fo, y.data_ptr(), 0, None)
+    assert rc == 0, last_error()
+    torch.cuda.synchronize()
+    ref = F.conv2d(x.double().permute(0, 3, 1, 2), w.double().permute(0, 3, 1, 2), padding=p)
+    ref = ref.permute(0, 2, 3, 1)  # B, H, W, F
+    got = y.reshape(B, H + p, H + p, Fo)[:, :H, :H, :].double()
+    err = (got - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 2e-5, err
