@@ -204,6 +204,28 @@ def run_reference_arm(args):
     print(json.dumps(line))
 
 
+def algorithmic_gemm_flops(spec, b: int, world: int) -> float:
+    """Algorithmic GEMM FLOPs of one step on one GPU (SURVEY.md 8(d)/App. B):
+    conv fprop + wgrad + dgrad (conv1 dgrad excluded: the reference discards
+    it), 2 FLOPs per MAC on the useful problem (no padded channels, taps or
+    border rows); the FC stack's 3 GEMMs over K*b examples split K ways."""
+    c, h, w = spec.input_shape
+    total = 0.0
+    for i, l in enumerate(spec.conv_layers):
+        def od(x):
+            return (x + 2 * l.pad - l.kernel) // l.stride + 1
+        oh, ow = od(h), od(w)
+        macs = b * oh * ow * l.out_channels * l.kernel * l.kernel * l.in_channels
+        total += 2.0 * macs * (2 if i == 0 else 3)
+        c, h, w = l.out_channels, oh, ow
+        if l.pool_kernel:
+            h = (h - l.pool_kernel) // l.pool_stride + 1
+            w = (w - l.pool_kernel) // l.pool_stride + 1
+    for f in spec.fc_layers:
+        total += 3 * 2.0 * b * f.in_dim * f.out_dim  # (K*b examples) x (out/K columns)
+    return total
+
+
 # ---------------------------------------------------------------- B200 arm
 def main_b200(args):
     import numpy as np
@@ -339,8 +361,17 @@ def main_b200(args):
     if args.math != "bf16":
         peak = peak / 2.0  # tf32 dense rate is half of bf16 (nominal); not separately measured
         peak_src += " / 2 (tf32)"
-    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    # achieved = ALGORITHMIC GEMM FLOPs of the step (useful work only; the
+    # kernels' padded problems are larger) / the GEMM launches' event-timed time
+    alg_flops = algorithmic_gemm_flops(spec, b, world)
+    achieved = alg_flops * prof_steps / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
     step_ms = ms / args.steps
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
+            traffic = json.load(fh)["gemm_dram_bytes_per_step"]
+    except Exception:
+        pass
     gemm_share = (gemm_ms / prof_steps) / step_ms if step_ms > 0 else None
 
     if args.profile_out and rank == 0:
@@ -386,9 +417,11 @@ def main_b200(args):
                    "final_loss": loss},
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (all conv fprop/dgrad/wgrad + fc launches)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per step, all GEMM launches (ncu, profiles/r1_traffic.json)",
                      "peak_source": peak_src, "gemm_share_of_step": gemm_share,
-                     "algorithmic_gflop_per_step": gemm_flops / prof_steps / 1e9},
+                     "algorithmic_gflop_per_step": alg_flops / 1e9,
+                     "executed_gflop_per_step": gemm_flops / prof_steps / 1e9},
         "cpu_baseline": cpu,
         "e2e": {"value": images / (e2e_ms / 1e3), "unit": "images/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
