@@ -283,6 +283,9 @@ HP_API int hp_kernel_gemm_splits(const hp_gemm_desc* d);
 /* Dev hook for microbenchmarks: force later auto-configured GEMM plans to
  * (cta2, bn); (-1, 0) restores the automatic tile choice. */
 HP_API void hp_debug_gemm_force(int cta2, int bn);
+/* Dev hook: flags for later plans; bit 0 skips the epilogue's global traffic
+ * (mainloop-only timing; results are garbage). */
+HP_API void hp_debug_gemm_flags(int flags);
 
 /* Implicit-GEMM convolution on tcgen05 with TMA im2col operand loads (no
  * im2col buffer); NHWC activations in the operand type (bf16 for

@@ -132,6 +132,7 @@ def _load() -> C.CDLL:
                                  C.c_int),
         "hp_kernel_gemm_splits": ([C.POINTER(HpGemmDesc)], C.c_int),
         "hp_debug_gemm_force": ([C.c_int, C.c_int], None),
+        "hp_debug_gemm_flags": ([C.c_int], None),
         "hp_kernel_conv_fprop": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int,
                                   C.c_int, C.c_int, C.c_int, P, P], C.c_int),
         "hp_kernel_conv_wgrad": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int,

@@ -78,6 +78,7 @@ static GemmPlan plan_from_desc(const hp_gemm_desc* d) {
 }
 
 HP_API void hp_debug_gemm_force(int cta2, int bn) { gemm_force_config(cta2, bn); }
+HP_API void hp_debug_gemm_flags(int flags) { gemm_debug_flags(flags); }
 
 HP_API int hp_kernel_gemm_splits(const hp_gemm_desc* d) {
   int splits = 1;

@@ -95,8 +95,9 @@ __device__ __forceinline__ void epi_elem(const Epi& e, int m, int n, float v) {
 }
 
 // Epilogue for 32 consecutive columns [n0, n0+32) of row m.
+// mo: the output row of GEMM row m under the epilogue RowMap (-1: dropped).
 __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int split,
-                                          const float (&v)[32]) {
+                                          const float (&v)[32], int mo) {
   if (m >= a.M) return;
   if (a.raw_partial) {
     float* dst = a.ws + static_cast<long long>(split) * a.M * a.N +
@@ -114,7 +115,8 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
   }
   const Epi& e = a.epi;
   // Vector path: 32 contiguous outputs of row m (bias/ReLU/alpha/beta/mask fused).
-  const bool vec = !e.rows.enabled && !e.c_trans && n0 + 32 <= a.N &&
+  if (mo < 0) return;
+  const bool vec = !e.c_trans && n0 + 32 <= a.N &&
                    (e.c_type == kF32 ? (e.ldc & 3) == 0 : (e.ldc & 7) == 0) &&
                    (!e.sgd_w || ((e.ldc & 7) == 0 && e.c_type == kF32)) &&
                    (!e.beta || e.c_type == kF32) &&
@@ -125,7 +127,7 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
     const float bm = e.bias_mode == 1 ? e.bias[m] : 0.f;
 #pragma unroll
     for (int i = 0; i < 32; ++i) x[i] = v[i] * e.alpha;
-    const long long off = static_cast<long long>(m) * e.ldc + n0;
+    const long long off = static_cast<long long>(mo) * e.ldc + n0;
     if (e.beta) {
       const float4* old = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.c) + off);
 #pragma unroll
@@ -191,9 +193,9 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
       for (int i = 0; i < 32; ++i) x[i] = x[i] > 0.f ? x[i] : 0.f;
     }
     if (e.mask) {
-      const long long mo = static_cast<long long>(m) * e.ldmask + n0;
+      const long long mko = static_cast<long long>(mo) * e.ldmask + n0;
       if (e.mask_type == kBF16) {
-        const uint4* mp = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(e.mask) + mo);
+        const uint4* mp = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(e.mask) + mko);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           uint4 u = mp[i];
@@ -203,7 +205,7 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
             if (!(__bfloat162float(h[j]) > 0.f)) x[8 * i + j] = 0.f;
         }
       } else {
-        const float4* mp = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.mask) + mo);
+        const float4* mp = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.mask) + mko);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const float4 o = mp[i];
@@ -301,7 +303,9 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
 // Output rows of the 8 GEMM rows m0 + 4i + (lane >> 3) a thread stores in
 // epi_chunk (-1: past M or dropped by the RowMap). Depends only on the tile
 // and the thread, so the kernels compute it once per tile.
-__device__ __forceinline__ void epi_rows(const GemmArgs& a, int m0, int (&mrow)[8]) {
+__device__ __forceinline__ void epi_rows(const GemmArgs& a, int m0, int (&mrow)[8], int& mself) {
+  const int ms = m0 + (threadIdx.x & 31);
+  mself = ms < a.M ? map_row(a.epi.rows, ms) : -1;
   const int rsub = (threadIdx.x & 31) >> 3;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -313,10 +317,16 @@ __device__ __forceinline__ void epi_rows(const GemmArgs& a, int m0, int (&mrow)[
 // Epilogue of one warp's 32 rows [m0, m0+32) x 32 columns [n0, n0+32).
 // All 32 lanes must call it (warp-synchronous); `stg` is the warp's tile.
 __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int split, const float (&v)[32],
-                                          float* stg, const int (&mrow)[8]) {
+                                          float* stg, const int (&mrow)[8], int mself) {
   const int lane = threadIdx.x & 31;
-  if (!epi_vec_ok(a)) {  // transposed outputs: the row-per-thread layout is the coalesced one
-    epi_row32(a, m0 + lane, n0, split, v);
+  if (a.dbg & 1) return;  // dev: mainloop-only timing
+  // Store-only epilogues (no beta / mask / SGD reads) and transposed outputs
+  // write straight from the row-per-thread layout: 32 contiguous outputs per
+  // thread, no smem round trip (the staged transpose costs shared-memory
+  // bandwidth the MMAs need; it pays only when the epilogue also reads HBM).
+  const bool direct = !(a.dbg & 2) && (a.raw_partial || (!a.epi.beta && !a.epi.mask && !a.epi.sgd_w));
+  if (direct || !epi_vec_ok(a)) {
+    epi_row32(a, m0 + lane, n0, split, v, mself);
     return;
   }
   const uint32_t sbase = smem_u32(stg);
@@ -745,8 +755,8 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
       tc_fence_after();
       float* stg = reinterpret_cast<float*>(smem + STAGES * SB + 256) + q * 32 * kEpiLd;
       const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf) * ACOLS;
-      int mrow[8];
-      epi_rows(args, ti.m0 + q * 32, mrow);
+      int mrow[8], mself;
+      epi_rows(args, ti.m0 + q * 32, mrow, mself);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
@@ -759,7 +769,7 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (ti.n0 + c < args.N) epi_chunk(args, ti.m0 + q * 32, ti.n0 + c, ti.split, v, stg, mrow);
+        if (ti.n0 + c < args.N) epi_chunk(args, ti.m0 + q * 32, ti.n0 + c, ti.split, v, stg, mrow, mself);
       }
     }
   }
@@ -946,8 +956,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       tc_fence_after();
       float* stg = reinterpret_cast<float*>(smem + STAGES * SB + 256) + q * 32 * kEpiLd;
       const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf) * ACOLS;
-      int mrow[8];
-      epi_rows(args, m0 + static_cast<int>(rank) * kBM + q * 32, mrow);
+      int mrow[8], mself;
+      epi_rows(args, m0 + static_cast<int>(rank) * kBM + q * 32, mrow, mself);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
@@ -960,7 +970,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (n0 + c < args.N) epi_chunk(args, m0 + static_cast<int>(rank) * kBM + q * 32, n0 + c, split, v, stg, mrow);
+        if (n0 + c < args.N) epi_chunk(args, m0 + static_cast<int>(rank) * kBM + q * 32, n0 + c, split, v, stg, mrow, mself);
       }
     }
   }
@@ -1138,8 +1148,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
       const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf) * ACOLS;
-      int mrow[8];
-      epi_rows(args, m0 + static_cast<int>(rank) * kBM + q * 32, mrow);
+      int mrow[8], mself;
+      epi_rows(args, m0 + static_cast<int>(rank) * kBM + q * 32, mrow, mself);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
@@ -1152,7 +1162,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (n0 + c < args.N) epi_chunk(args, m0 + static_cast<int>(rank) * kBM + q * 32, n0 + c, 0, v, stg, mrow);
+        if (n0 + c < args.N) epi_chunk(args, m0 + static_cast<int>(rank) * kBM + q * 32, n0 + c, 0, v, stg, mrow, mself);
       }
     }
   }
@@ -1490,7 +1500,8 @@ int gemm_choose_splits(int math, int M, int N, int K, int bn) {
 }
 
 static bool g_cta2_default = true;
-static int g_force_cta2 = -1, g_force_bn = 0;
+static int g_force_cta2 = -1, g_force_bn = 0, g_dbg_flags = 0;
+void gemm_debug_flags(int flags) { g_dbg_flags = flags; }
 void gemm_set_cta2_default(bool on) { g_cta2_default = on; }
 void gemm_force_config(int cta2, int bn) {
   g_force_cta2 = cta2;
@@ -1584,6 +1595,7 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   p.args.a_mn = a.mn_major;
   p.args.b_mn = b.mn_major;
   p.args.raw_partial = splits > 1 ? 1 : 0;
+  p.args.dbg = g_dbg_flags;
   p.args.ws = ws;
   p.args.epi = epi;
   if (splits > 1 && ws == nullptr) throw std::runtime_error("gemm: split-K needs a workspace");
@@ -1664,6 +1676,7 @@ GemmPlan conv_shift_plan(const void* x, long long rows, int C, int R, int S, int
   p.args.sh_C = C;
   p.args.sh_halo = halo;
   p.args.sh_boff = boff_mode;
+  p.args.dbg = g_dbg_flags;
   p.ta = make_map(x, 2, C, rows, C, 64, halo, CU_TENSOR_MAP_SWIZZLE_128B);
   p.tb = make_map(w, 2, static_cast<long long>(R) * S * C, N, ldw, 64, p.bn / 2, CU_TENSOR_MAP_SWIZZLE_128B);
   const int total = cdiv(rows, 2 * kBM) * cdiv(N, p.bn);

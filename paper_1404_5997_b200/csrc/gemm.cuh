@@ -107,6 +107,7 @@ struct GemmArgs {
   // shift conv (conv_shift_plan): taps R x S, flat row shift r*wq + s, C
   // channels per tap (64-channel blocks), halo rows per CTA, base-offset mode
   int sh_R, sh_S, sh_wq, sh_C, sh_halo, sh_boff;
+  int dbg;  // dev flags (gemm_debug_flags): bit 0 = skip the epilogue's global traffic
 };
 
 // A fully prepared GEMM launch (tensor maps encoded once, reused every step).
@@ -132,6 +133,8 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
 void gemm_set_cta2_default(bool on);
 // Dev hook: force every later auto-configured plan to (cta2, bn); -1/0 = auto.
 void gemm_force_config(int cta2, int bn);
+// Dev hook: flags copied into every later plan (GemmArgs::dbg).
+void gemm_debug_flags(int flags);
 int gemm_choose_splits(int math, int M, int N, int K, int bn = 0);
 int gemm_choose_bn(int M, int N);
 void gemm_launch(const GemmPlan& p, cudaStream_t s);

@@ -33,6 +33,36 @@ __device__ __forceinline__ bf16 from_f<bf16>(float v) {
   return __float2bfloat16_rn(v);
 }
 
+// 4-element vector load / store as fp32 (float4 or 4 x bf16).
+template <class T>
+__device__ __forceinline__ void ld4(const T* p, float* v);
+template <>
+__device__ __forceinline__ void ld4<float>(const float* p, float* v) {
+  const float4 u = *reinterpret_cast<const float4*>(p);
+  v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
+}
+template <>
+__device__ __forceinline__ void ld4<bf16>(const bf16* p, float* v) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+template <class T>
+__device__ __forceinline__ void st4(T* p, const float* v);
+template <>
+__device__ __forceinline__ void st4<float>(float* p, const float* v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+template <>
+__device__ __forceinline__ void st4<bf16>(bf16* p, const float* v) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+
 int grid_for(long long n, int threads = 256, int max_blocks = 148 * 16) {
   long long b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -237,27 +267,43 @@ __global__ void lrn_bwd_kernel(const TA* __restrict__ a, const float* __restrict
 }
 
 // ------------------------------------------------------------------ reductions
+// Column sums of x[M][N] (conv bias gradient, model.cpp:184-202), deterministic,
+// two passes: block (x, g) sums rows [g*rows_per, ...) of 8-column vectors
+// (16-byte loads) into ws[g][N]; then one warp per column adds the G partials
+// (lane l: l, l+32, ...; fixed xor-shuffle tree).
 template <class T>
-__global__ void colsum_partial_kernel(const T* __restrict__ x, long long M, int N, long long ldx,
-                                      long long rows_per, float* __restrict__ ws) {
-  __shared__ float red[8][33];
-  const int col = blockIdx.x * 32 + threadIdx.x;
+__global__ void __launch_bounds__(256) colsum_partial_kernel(const T* __restrict__ x, long long M, int N,
+                                                             long long ldx, long long rows_per,
+                                                             float* __restrict__ ws) {
+  __shared__ float red[256][9];
+  const int tx = threadIdx.x, ty = threadIdx.y, TX = blockDim.x, TY = blockDim.y;
+  const int c0 = 8 * (blockIdx.x * TX + tx);
   const long long r0 = blockIdx.y * rows_per;
   const long long r1 = min(M, r0 + rows_per);
-  float acc = 0.f;
-  if (col < N)
-    for (long long r = r0 + threadIdx.y; r < r1; r += 8) acc += to_f<T>(x[r * ldx + col]);
-  red[threadIdx.y][threadIdx.x] = acc;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c0 < N) {
+    for (long long r = r0 + ty; r < r1; r += TY) {
+      float v[8];
+      ld4<T>(x + r * ldx + c0, v);
+      ld4<T>(x + r * ldx + c0 + 4, v + 4);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += v[j];
+    }
+  }
+  const int t = ty * TX + tx;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) red[t][j] = acc[j];
   __syncthreads();
-  if (threadIdx.y == 0 && col < N) {
-    float s = 0.f;
-    for (int y = 0; y < 8; ++y) s += red[y][threadIdx.x];
-    ws[static_cast<long long>(blockIdx.y) * N + col] = s;
+  if (ty == 0 && c0 < N) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float sum = 0.f;
+      for (int y = 0; y < TY; ++y) sum += red[y * TX + tx][j];
+      ws[static_cast<long long>(blockIdx.y) * N + c0 + j] = sum;
+    }
   }
 }
 
-// One warp per column: lanes stride the partial rows, then a fixed shuffle
-// tree (deterministic).
 __global__ void colsum_final_kernel(const float* __restrict__ ws, int G, int N,
                                     float* __restrict__ out) {
   const int col = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -502,36 +548,6 @@ __device__ __forceinline__ float pow_neg(float d, float beta) {
 
 // LRN channel halo: up to LH = 4 channels each side (LRN size <= 9).
 constexpr int LH = 4;
-
-// 4 channels per thread (C % 4 == 0), 32-bit index math.
-template <class T>
-__device__ __forceinline__ void ld4(const T* p, float* v);
-template <>
-__device__ __forceinline__ void ld4<float>(const float* p, float* v) {
-  const float4 u = *reinterpret_cast<const float4*>(p);
-  v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
-}
-template <>
-__device__ __forceinline__ void ld4<bf16>(const bf16* p, float* v) {
-  const uint2 u = *reinterpret_cast<const uint2*>(p);
-  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-}
-template <class T>
-__device__ __forceinline__ void st4(T* p, const float* v);
-template <>
-__device__ __forceinline__ void st4<float>(float* p, const float* v) {
-  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-}
-template <>
-__device__ __forceinline__ void st4<bf16>(bf16* p, const float* v) {
-  __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
-  uint2 u;
-  u.x = *reinterpret_cast<uint32_t*>(&a);
-  u.y = *reinterpret_cast<uint32_t*>(&b);
-  *reinterpret_cast<uint2*>(p) = u;
-}
 
 // Max-pool forward, window argmax as a 1-byte offset r*k+q: first maximum in
 // row-major window order (strict >), a NaN wins and stops the scan.
@@ -858,37 +874,55 @@ __global__ void __launch_bounds__(256) rotate_weights_kernel(const float* __rest
   }
 }
 
-// Space-to-depth (see kernels.cuh): thread = (pixel (b,i,j), 8-channel group),
-// one 16-byte (bf16) / 2x16-byte (fp32) store per thread.
+// Space-to-depth (see kernels.cuh): block = one z row (b, i). Phase 1 stages
+// the C*s input rows it needs (zero where outside the image, x shifted by pad)
+// in smem with coalesced (float4 when W % 4 == 0) loads; phase 2 writes the
+// Zw x Cz bf16 row, one 8-channel 16-byte vector per thread.
 template <class T>
 __global__ void __launch_bounds__(256) s2d_input_kernel(const float* __restrict__ x, T* __restrict__ z, int C,
-                                                        int H, int W, int s, int pad, int Zh, int Zw, int Cz,
-                                                        int total) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= total) return;
-  const int G = Cz >> 3;
-  const int q = t % G;
-  const int pix = t / G;
-  const int j = pix % Zw, r = pix / Zw;
-  const int i = r % Zh, b = r / Zh;
+                                                        int H, int W, int s, int pad, int Zh, int Zw, int Cz) {
+  extern __shared__ float sx[];  // [C][s][s*Zw]
+  const int b = blockIdx.y, i = blockIdx.x;
+  const int SW = s * Zw;
+  const int nrows = C * s;
+  for (int rr = threadIdx.y; rr < nrows; rr += blockDim.y) {
+    const int c = rr / s, dr = rr - c * s;
+    const int h = s * i + dr - pad;
+    float* dst = sx + rr * SW;
+    const bool hv = h >= 0 && h < H;
+    const float* src = x + ((static_cast<long long>(b) * C + c) * H + (hv ? h : 0)) * W;
+    for (int q = threadIdx.x; q < SW; q += blockDim.x) {
+      const int w = q - pad;
+      dst[q] = (hv && w >= 0 && w < W) ? __ldg(src + w) : 0.f;
+    }
+  }
+  __shared__ int choff[256];  // smem offset of channel ch at j = 0 (-1: zero channel)
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
   const int real = s * s * C;
-  const float* xb = x + static_cast<long long>(b) * C * H * W;
-  float v[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int ch = q * 8 + k;
-    float val = 0.f;
+  for (int ch = tid; ch < Cz; ch += nt) {
+    int off = -1;
     if (ch < real) {
       const int c = ch % C, d = ch / C;
       const int dr = d / s, dc = d - dr * s;
-      const int h = s * i + dr - pad, w = s * j + dc - pad;
-      if (h >= 0 && h < H && w >= 0 && w < W) val = __ldg(xb + (static_cast<long long>(c) * H + h) * W + w);
+      off = (c * s + dr) * SW + dc;
     }
-    v[k] = val;
+    choff[ch] = off;
   }
-  T* dst = z + static_cast<long long>(pix) * Cz + q * 8;
-  st4<T>(dst, v);
-  st4<T>(dst + 4, v + 4);
+  __syncthreads();
+  const int G = Cz >> 3;
+  T* zrow = z + (static_cast<long long>(b) * Zh + i) * Zw * Cz;
+  for (int t = tid; t < Zw * G; t += nt) {
+    const int j = t / G, q = t - j * G;
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int off = choff[q * 8 + k];
+      v[k] = off >= 0 ? sx[off + s * j] : 0.f;
+    }
+    T* dst = zrow + static_cast<long long>(j) * Cz + q * 8;
+    st4<T>(dst, v);
+    st4<T>(dst + 4, v + 4);
+  }
 }
 
 template <class T>
@@ -1046,10 +1080,11 @@ template <class T>
 void launch_s2d_input(const float* x, T* z, int B, int C, int H, int W, int s, int pad, int Zh, int Zw, int Cz,
                       cudaStream_t st) {
   if (Cz % 8 != 0) throw std::runtime_error("s2d: padded channels must be a multiple of 8");
-  const long long total = static_cast<long long>(B) * Zh * Zw * (Cz / 8);
-  if (total >= (1LL << 31)) throw std::runtime_error("s2d: too large");
-  s2d_input_kernel<T><<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(x, z, C, H, W, s, pad, Zh, Zw, Cz,
-                                                                               static_cast<int>(total));
+  if (static_cast<long long>(B) * Zh * Zw * Cz >= (1LL << 31)) throw std::runtime_error("s2d: too large");
+  const size_t smem = static_cast<size_t>(C) * s * s * Zw * sizeof(float);
+  if (smem > 200 * 1024 || Cz > 256) throw std::runtime_error("s2d: input rows too wide for smem");
+  cudaFuncSetAttribute(s2d_input_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  s2d_input_kernel<T><<<dim3(Zh, B), dim3(64, 4), smem, st>>>(x, z, C, H, W, s, pad, Zh, Zw, Cz);
 }
 
 template <class T>
@@ -1163,10 +1198,13 @@ size_t colsum_ws_floats(long long M, int N) {
 template <class T>
 void launch_colsum(const T* x, long long M, int N, long long ldx, float* out, float* ws,
                    cudaStream_t st) {
+  if (N % 8 != 0 || ldx % 8 != 0) throw std::runtime_error("colsum: N and ldx must be multiples of 8");
   const long long G = std::min<long long>(std::max<long long>(1, (M + 255) / 256), 512);
   const long long rows_per = (M + G - 1) / G;
-  dim3 grid((N + 31) / 32, static_cast<unsigned>(G));
-  colsum_partial_kernel<T><<<grid, dim3(32, 8), 0, st>>>(x, M, N, ldx, rows_per, ws);
+  const int vec = N / 8;
+  const int TX = std::min(vec, 32), TY = 256 / TX;
+  colsum_partial_kernel<T><<<dim3((vec + TX - 1) / TX, static_cast<unsigned>(G)), dim3(TX, TY), 0, st>>>(
+      x, M, N, ldx, rows_per, ws);
   colsum_final_kernel<<<(N * 32 + 255) / 256, 256, 0, st>>>(ws, static_cast<int>(G), N, out);
 }
 
