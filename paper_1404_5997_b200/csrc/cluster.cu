@@ -280,6 +280,7 @@ struct Worker {
   const float* x_src = nullptr; // this step's NCHW batch (device)
   // conv params: [kernels F x ldk | bias F] per layer, one arena
   float *cp = nullptr, *cm = nullptr, *cgr = nullptr;
+  float* cgr_local = nullptr;  // skip_sync_broadcast: this worker's pre-all-reduce conv gradients
   TA* cpt = nullptr;  // operand copy (bf16 mode)
   // fc stack
   TA* xb = nullptr;        // [n][A] boundary input
@@ -568,6 +569,7 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     w.cp = arena_.make<float>(conv_total_);
     w.cm = arena_.make<float>(conv_total_);
     w.cgr = arena_.make<float>(conv_total_);
+    w.cgr_local = K_ > 1 ? arena_.make<float>(conv_total_) : nullptr;
     w.cpt = std::is_same<TA, float>::value ? nullptr : arena_.make<TA>(conv_total_);
     w.xb = arena_.make<TA>(n_ * A);
     w.tb = arena_.make<float>(n_ * L_);
@@ -1271,9 +1273,10 @@ void ClusterImpl<TA>::sgd_conv(double lr, const hp_hyper& hp) {
     t.g = w.cgr;
     t.copy = w.cpt;
     t.n = conv_total_;
-    // mean.scale(1/K) of sync_conv_gradients (cluster.cpp:293-295)
+    // mean.scale(1/K) of sync_conv_gradients (cluster.cpp:293-295); already
+    // applied to the owned shard by the skip-broadcast fix-up
     t.gscale = static_cast<float>(1.0 / static_cast<double>(K_));
-    t.has_gscale = K_ > 1 ? 1 : 0;
+    t.has_gscale = K_ > 1 && !skip_sync_broadcast ? 1 : 0;
     ts.push_back(t);
   }
   launch_sgd(ts.data(), static_cast<int>(ts.size()), kTA == kBF16 ? 1 : 0, lr, hp.momentum,
@@ -1334,6 +1337,12 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
   std::vector<ConvBwdState> cbs(nl);
   for (int l = nc - 1; l >= 0; --l) {
     for (int i = 0; i < nl; ++i) conv_backward_layer(w_[i], l, cbs[i]);
+    if (K_ > 1 && skip_sync_broadcast) {  // keep the local gradients for the negative control
+      const long long cnt = static_cast<long long>(g_.cg[l].F) * g_.cg[l].ldk + g_.cg[l].F;
+      for (int i = 0; i < nl; ++i)
+        HP_CUDA(cudaMemcpyAsync(w_[i].cgr_local + conv_k_off(l), w_[i].cgr + conv_k_off(l), cnt * sizeof(float),
+                                cudaMemcpyDeviceToDevice, st_));
+    }
     if (K_ > 1) {
       HP_CUDA(cudaEventRecord(ev_layer_[l], st_));
       HP_CUDA(cudaStreamWaitEvent(sc_, ev_layer_[l], 0));
@@ -1347,6 +1356,25 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
   if (K_ > 1) {
     HP_CUDA(cudaEventRecord(ev_comm_, sc_));
     HP_CUDA(cudaStreamWaitEvent(st_, ev_comm_, 0));
+  }
+  if (K_ > 1 && skip_sync_broadcast) {
+    // sync_conv_gradients(skip_broadcast) (cluster.cpp:306-314): owners keep the
+    // mean of their shard of the reference-flattened gradient, everything else
+    // stays local; the mean's 1/K is applied here, so sgd_conv skips it
+    long long G = 0;
+    for (const auto& c : g_.cg) G += static_cast<long long>(c.F) * c.Kc + c.F;
+    for (auto& w : w_) {
+      long long b0, b1;
+      shard(G, K_, w.gid, &b0, &b1);
+      long long base = 0;
+      for (size_t l = 0; l < g_.cg.size(); ++l) {
+        const ConvGeom& c = g_.cg[l];
+        launch_skip_sync_fixup(w.cgr + conv_k_off(static_cast<int>(l)), w.cgr_local + conv_k_off(static_cast<int>(l)),
+                               c.F, c.C, c.R, c.S, c.ldk, base, b0, b1, static_cast<float>(1.0 / K_), st_);
+        ++launches_;
+        base += static_cast<long long>(c.F) * c.Kc + c.F;
+      }
+    }
   }
   if (!variable_) {
     const bool scale = num_sub_ > 1;
@@ -1437,8 +1465,6 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
                        num(e % (b_ * L_)));
       }
   }
-  if (skip_sync_broadcast && K_ > 1)
-    usage_error("set_skip_sync_broadcast: not supported on the B200 path yet");
 
   // CUDA graph of the whole step, keyed by everything baked into it (input
   // pointers, memory kind, scalars). Captured on the second occurrence of a
@@ -1460,6 +1486,7 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
   }
   key.mem = mem_kind;
   key.scal = {lr, hp.momentum, hp.weight_decay, hp.has_fc_partial_lr ? hp.fc_partial_lr : -1.0};
+  key.mem += skip_sync_broadcast ? 16 : 0;  // a different step (fix-up launches)
   const bool graphable = use_graphs && !profile && pinned;
   GraphEntry* ge = nullptr;
   if (graphable) {

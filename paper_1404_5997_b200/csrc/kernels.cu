@@ -956,6 +956,26 @@ __global__ void s2d_wgrad_gather_kernel(const float* __restrict__ dwz, float* __
   dw[f * ldk + k] = dwz[static_cast<long long>(f) * Rq * Rq * Cz + kz];
 }
 
+__global__ void skip_sync_fixup_kernel(float* __restrict__ g, const float* __restrict__ local, int F, int C,
+                                       int R, int S, long long ldk, long long base, long long own_b,
+                                       long long own_e, float inv_k) {
+  const long long kern = static_cast<long long>(F) * ldk;
+  const long long n = kern + F;
+  GRID_STRIDE(i, n) {
+    long long ref;
+    if (i < kern) {
+      const int f = static_cast<int>(i / ldk), k = static_cast<int>(i - static_cast<long long>(f) * ldk);
+      if (k >= R * S * C) continue;  // row padding
+      const int rs = k / C, c = k - rs * C;
+      const int r = rs / S, q = rs - r * S;
+      ref = base + ((static_cast<long long>(f) * C + c) * R + r) * S + q;
+    } else {
+      ref = base + static_cast<long long>(F) * C * R * S + (i - kern);
+    }
+    g[i] = (ref >= own_b && ref < own_e) ? __fmul_rn(g[i], inv_k) : local[i];
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -1098,6 +1118,12 @@ void launch_s2d_wgrad_gather(const float* dwz, float* dw, long long ldk, int F, 
                              int Cz, cudaStream_t st) {
   const int n = F * R * S * C;
   s2d_wgrad_gather_kernel<<<(n + 255) / 256, 256, 0, st>>>(dwz, dw, ldk, F, C, R, S, s, Rq, Cz);
+}
+
+void launch_skip_sync_fixup(float* g, const float* local, int F, int C, int R, int S, long long ldk,
+                            long long base, long long own_b, long long own_e, float inv_k, cudaStream_t st) {
+  const long long n = static_cast<long long>(F) * ldk + F;
+  skip_sync_fixup_kernel<<<grid_for(n), 256, 0, st>>>(g, local, F, C, R, S, ldk, base, own_b, own_e, inv_k);
 }
 
 #define INST_NEW(T)                                                                             \

@@ -169,6 +169,15 @@ void launch_s2d_weights(const float* w, long long ldk, T* wz, int F, int C, int 
 void launch_s2d_wgrad_gather(const float* dwz, float* dw, long long ldk, int F, int C, int R, int S, int s,
                              int Rq, int Cz, cudaStream_t st);
 
+// Cluster::set_skip_sync_broadcast negative control (cluster.cpp:306-314): after
+// the all-reduce (g = sum over workers), worker-owned entries -- reference flat
+// index (kernels [F][C][R][S] then bias, per layer from `base`) inside
+// [own_b, own_e) -- become sum * inv_k; every other entry reverts to the
+// worker's local gradient. Device layout of one layer: kernels [F][ldk] with
+// k = (r*S + s)*C + c, then bias[F].
+void launch_skip_sync_fixup(float* g, const float* local, int F, int C, int R, int S, long long ldk,
+                            long long base, long long own_b, long long own_e, float inv_k, cudaStream_t st);
+
 // Scale in place (fp32).
 void launch_scale(float* x, long long n, float s, cudaStream_t st);
 

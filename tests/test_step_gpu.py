@@ -28,12 +28,15 @@ TOL = {hp.MathMode.F32X3: (2e-3, 2e-5, 2e-5), hp.MathMode.TF32: (8e-2, 1e-4, 1e-
        hp.MathMode.BF16: (3e-1, 5e-4, 1e-4)}
 
 
-def compare(spec, K, scheme, var, math, b, steps=2, lr=0.05, wscale=1.0, seed=1):
+def compare(spec, K, scheme, var, math, b, steps=2, lr=0.05, wscale=1.0, seed=1, skip=False):
     cfg = hp.ClusterConfig(workers=K, per_worker_batch=b, scheme=hp.Scheme.from_string(scheme),
                            variable_batch=var, seed=seed, math_mode=math)
     g = hp.Cluster(spec, cfg)
     o = O.OracleCluster(spec, workers=K, per_worker_batch=b, scheme=scheme, variable_batch=var,
                         precision="single", seed=seed)
+    if skip:
+        g.set_skip_sync_broadcast(True)
+        o.set_skip_sync_broadcast(True)
     nl = lambda which: len(spec.conv_layers) if (which & 3) < 2 else len(spec.fc_layers)
     for w in range(K):  # identical initial parameters (GaussianSampler replay + layout permutations)
         for which in range(4):
@@ -62,10 +65,11 @@ def compare(spec, K, scheme, var, math, b, steps=2, lr=0.05, wscale=1.0, seed=1)
                 e = rel_err(g.param(w, which, l), o.param(w, which, l))
                 # biases start at zero, so (like momenta) they are pure gradient history
                 assert e <= (mt if (which >= 4 or which in (1, 3)) else wt), (w, which, l, e)
-    # replica consistency: conv replicas identical across workers
+    # replica consistency: conv replicas identical across workers (unless the
+    # negative control skipped the broadcast)
     for w in range(1, K):
         for l in range(len(spec.conv_layers)):
-            assert np.array_equal(g.param(w, 0, l), g.param(0, 0, l))
+            assert np.array_equal(g.param(w, 0, l), g.param(0, 0, l)) != skip
     return g, o
 
 
@@ -170,3 +174,11 @@ def test_prefetch_double_buffer_matches_plain_host_steps():
     assert res[0][1] == res[1][1]
     for a, b in zip(res[0][2], res[1][2]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("math", [hp.MathMode.F32X3, hp.MathMode.BF16])
+def test_skip_sync_broadcast_negative_control(math):
+    """Cluster::set_skip_sync_broadcast (cluster.cpp:306-314): each worker keeps
+    the mean only on its own shard of the flattened conv gradient, so replicas
+    diverge exactly as the oracle's do."""
+    compare(hp.tiny_cnn(), 4, "B", False, math, 8, skip=True)
