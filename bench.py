@@ -411,7 +411,9 @@ def main_b200(args):
                    + (" variable" if args.variable else " exact") + " SGD (configs[2])",
                    "per_gpu_batch": b, "global_batch": b * world, "image": [3, 224, 224],
                    "scheme": args.scheme.upper(), "variant": "approximate" if args.variable else "exact",
-                   "math": args.math, "parallelism": f"conv dp{world} + fc mp{world}",
+                   "math": args.math,
+                   "parallelism": (f"dp{world} (conv + replicated fc, fc gradients all-reduced)"
+                                   if args.scheme.upper() in ("DP", "D") else f"conv dp{world} + fc mp{world}"),
                    "l2": "no flush; per-step working set (~3 GB im2col/activations) >> 126 MB L2; 4 rotating input batches",
                    "cuda_graphs": True, "graph_prime_steps": 2 * NB * 2,
                    "final_loss": loss},

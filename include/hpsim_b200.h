@@ -49,7 +49,12 @@ enum {
   HP_ERR_NCCL = 6
 };
 
-enum { HP_SCHEME_A = 0, HP_SCHEME_B = 1, HP_SCHEME_C = 2 }; /* cluster.hpp:36 */
+enum { HP_SCHEME_A = 0, HP_SCHEME_B = 1, HP_SCHEME_C = 2, /* cluster.hpp:36 */
+       /* B200 extension (BASELINE config 5 comparison, no reference
+        * counterpart): pure data parallelism -- every worker holds the whole FC
+        * stack, runs it on its own b examples, and the FC gradients are
+        * all-reduced with the conv gradients (one exact update per step). */
+       HP_SCHEME_DP = 3 };
 enum { HP_PRECISION_SINGLE = 0, HP_PRECISION_DOUBLE = 1 };  /* tensor.hpp:28 */
 enum {
   HP_MATH_BF16 = 0,  /* bf16 operands, fp32 accumulate (throughput mode) */

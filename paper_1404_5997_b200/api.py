@@ -66,6 +66,7 @@ class Scheme(enum.IntEnum):
     A = 0
     B = 1
     C = 2
+    DP = 3  # B200 extension: pure data parallelism (FC replicated, gradients all-reduced)
 
     @staticmethod
     def from_string(s: str) -> "Scheme":  # cluster.cpp:31-36
@@ -75,6 +76,8 @@ class Scheme(enum.IntEnum):
             return Scheme.B
         if s in ("C", "c"):
             return Scheme.C
+        if s in ("DP", "dp", "D", "d"):
+            return Scheme.DP
         raise ConfigError(f"unknown scheme '{s}' (expected A|B|C)")
 
 

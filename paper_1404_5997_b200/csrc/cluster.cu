@@ -160,6 +160,41 @@ void step_accounting(const Geometry& g_, int K, long long b, int scheme_,
                      std::vector<std::array<int64_t, 4>>& received, std::vector<hp_trace_event>& trace,
                      int64_t* bytes_sent) {
   const long long elt = 4, row_bytes = g_.A * elt;
+  if (scheme_ == HP_SCHEME_DP) {
+    // Pure data parallelism (no reference counterpart): no boundary exchange,
+    // no FC-internal traffic; the conv and FC gradient vectors are each
+    // all-reduced, charged with the reference's sync formula
+    // (G - s_i)*e + (K-1)*s_i*e (cluster.cpp:296-304).
+    long long Gc = 0, Gf = 0;
+    for (const auto& c : g_.cg) Gc += static_cast<long long>(c.F) * c.Kc + c.F;
+    for (const auto& f : g_.fg) Gf += f.in * f.out + f.out;
+    long long total = 0, mx = 0;
+    for (int i = 0; i < K; ++i) {
+      long long sc = 0, sf = 0;
+      if (K > 1) {
+        long long s0, s1;
+        shard(Gc, K, i, &s0, &s1);
+        sc = (Gc - (s1 - s0)) * elt + (K - 1) * (s1 - s0) * elt;
+        shard(Gf, K, i, &s0, &s1);
+        sf = (Gf - (s1 - s0)) * elt + (K - 1) * (s1 - s0) * elt;
+      }
+      sent[i][HP_MSG_CONV_SYNC] += sc;
+      received[i][HP_MSG_CONV_SYNC] += sc;
+      sent[i][HP_MSG_FC_GRADIENTS] += sf;
+      received[i][HP_MSG_FC_GRADIENTS] += sf;
+      bytes_sent[HP_MSG_CONV_SYNC] += sc;
+      bytes_sent[HP_MSG_FC_GRADIENTS] += sf;
+      total += sc + sf;
+      mx = std::max(mx, sc + sf);
+    }
+    trace.clear();
+    trace.push_back({HP_PHASE_CONV_FWD, -1, -1, 0, 0});
+    trace.push_back({HP_PHASE_FC_FWD, 0, -1, 0, 0});
+    trace.push_back({HP_PHASE_FC_BWD, 0, -1, 0, 0});
+    trace.push_back({HP_PHASE_CONV_BWD, -1, -1, 0, 0});
+    trace.push_back({HP_PHASE_SYNC, -1, -1, total, mx});
+    return;
+  }
   const int num_sub = scheme_ == HP_SCHEME_A ? 1 : K;
   const long long n_ = scheme_ == HP_SCHEME_A ? K * b : b;
   auto charge = [&](int i, int cls, long long s, long long r) {
@@ -372,6 +407,9 @@ class ClusterImpl final : public ClusterBase {
 
   Geometry g_;
   int K_, math_, scheme_;
+  bool dp_ = false;  // HP_SCHEME_DP: FC stack replicated (one shard), gradients all-reduced
+  int fcK_ = 1;      // FC shards (K_, or 1 under DP)
+  int sid(int gid) const { return dp_ ? 0 : gid; }  // FC shard index of a worker
   bool variable_;
   long long b_, n_, ldn_;
   int num_sub_, L_;
@@ -382,6 +420,7 @@ class ClusterImpl final : public ClusterBase {
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   std::vector<cudaEvent_t> ev_layer_;  // per conv layer: its gradients are final on st_
   cudaEvent_t ev_comm_ = nullptr;      // all conv-gradient all-reduces done on sc_
+  cudaEvent_t ev0_fc_ = nullptr;       // DP: FC gradients final on st_
   cudaStream_t sx_ = nullptr;          // copy stream: prefetch H2D
   struct PrefSlot {
     std::vector<const float*> x, t;  // host pointers staged in this slot
@@ -421,10 +460,12 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   // ClusterConfig::validate (cluster.cpp:50-67)
   if (cfg->workers < 1) config_error("cluster.workers: must be >= 1");
   if (cfg->per_worker_batch < 1) config_error("cluster.per_worker_batch: must be >= 1");
-  if (cfg->scheme < 0 || cfg->scheme > 2) config_error("cluster.scheme: expected A|B|C");
+  if (cfg->scheme < 0 || cfg->scheme > 3) config_error("cluster.scheme: expected A|B|C (or DP)");
   if (cfg->scheme == HP_SCHEME_C && cfg->per_worker_batch % cfg->workers != 0)
     config_error("cluster.per_worker_batch: scheme C scatters b/K examples per worker per turn; " +
                  num(cfg->per_worker_batch) + " is not divisible by " + num(cfg->workers));
+  if (cfg->variable_batch && cfg->scheme == HP_SCHEME_DP)
+    config_error("cluster.variable_batch: pure data parallelism has a single fc pass per step");
   if (cfg->variable_batch && cfg->scheme == HP_SCHEME_A)
     config_error("cluster.variable_batch: scheme A has a single fc pass per step; per-sub-batch "
                  "updates require scheme B or C");
@@ -437,9 +478,11 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   variable_ = cfg->variable_batch != 0;
   math_ = cfg->math_mode;
   seed_ = cfg->seed;
-  g_ = make_geometry(spec, K_, b_);
+  dp_ = scheme_ == HP_SCHEME_DP;
+  fcK_ = dp_ ? 1 : K_;
+  g_ = make_geometry(spec, fcK_, b_);
   L_ = static_cast<int>(g_.num_classes);
-  num_sub_ = scheme_ == HP_SCHEME_A ? 1 : K_;
+  num_sub_ = (scheme_ == HP_SCHEME_A || scheme_ == HP_SCHEME_DP) ? 1 : K_;
   n_ = scheme_ == HP_SCHEME_A ? K_ * b_ : b_;
   ldn_ = round_up(n_, 8);
 
@@ -455,6 +498,7 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   HP_CUDA(cudaEventCreate(&ev0_));
   HP_CUDA(cudaEventCreate(&ev1_));
   HP_CUDA(cudaEventCreateWithFlags(&ev_comm_, cudaEventDisableTiming));
+  HP_CUDA(cudaEventCreateWithFlags(&ev0_fc_, cudaEventDisableTiming));
   HP_CUDA(cudaStreamCreateWithFlags(&sx_, cudaStreamNonBlocking));
   for (auto& ps : pref_) {
     HP_CUDA(cudaEventCreateWithFlags(&ps.ready, cudaEventDisableTiming));
@@ -624,6 +668,7 @@ ClusterImpl<TA>::~ClusterImpl() {
   if (ev1_) cudaEventDestroy(ev1_);
   for (auto e : ev_layer_) cudaEventDestroy(e);
   if (ev_comm_) cudaEventDestroy(ev_comm_);
+  if (ev0_fc_) cudaEventDestroy(ev0_fc_);
   if (sc_) cudaStreamDestroy(sc_);
   if (sx_) cudaStreamSynchronize(sx_);
   for (auto& ps : pref_) {
@@ -825,7 +870,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
   const void* fweights = bf ? static_cast<const void*>(w.fpt) : static_cast<const void*>(w.fp);
   for (int l = 0; l < nf; ++l) {
     const FcGeom& f = g_.fg[l];
-    const long long rows = f.c1[w.gid] - f.c0[w.gid];
+    const long long rows = f.c1[sid(w.gid)] - f.c0[sid(w.gid)];
     const char* fwp = static_cast<const char*>(fweights) + fc_w_off(l) * es;
     const bool last = l + 1 == nf;
     // fwd: Z^T[rows][n] = W[rows][Ip] . X^T
@@ -834,7 +879,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       e.c = w.logits;
       e.c_type = kF32;
     } else {
-      e.c = static_cast<TA*>(w.fx[l + 1]) + static_cast<long long>(w.gid) * f.cmax * ldn_;
+      e.c = static_cast<TA*>(w.fx[l + 1]) + static_cast<long long>(sid(w.gid)) * f.cmax * ldn_;
       e.c_type = kTA;
     }
     e.ldc = ldn_;
@@ -852,7 +897,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     // dgrad
     if (l > 0) {
       Epi ed;
-      if (K_ == 1) {
+      if (fcK_ == 1) {
         ed.c = w.fdz[l - 1];
         ed.c_type = kTA;
       } else {
@@ -867,7 +912,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       w.fc_dgrad.push_back(plan(op(fwp, 1, f.Ip), op(w.fdz[l], 1, ldn_), f.Ip, n_, rows, ed));
     } else {
       Epi ed;
-      ed.c = K_ == 1 ? w.gflat : w.fdpart[0];
+      ed.c = fcK_ == 1 ? w.gflat : w.fdpart[0];
       ed.ldc = g_.A;
       w.fc_dgrad.push_back(plan(op(w.fdz[0], 1, ldn_), op(fwp, 1, f.Ip), n_, g_.A, rows, ed));
     }
@@ -923,7 +968,7 @@ long long ClusterImpl<TA>::fc_col(int l, long long i) const {
     return p * c.F + ch;
   }
   const FcGeom& prev = g_.fg[l - 1];
-  for (int q = 0; q < K_; ++q)
+  for (int q = 0; q < fcK_; ++q)
     if (i >= prev.c0[q] && i < prev.c1[q]) return q * prev.cmax + (i - prev.c0[q]);
   return -1;
 }
@@ -956,7 +1001,7 @@ void ClusterImpl<TA>::init_params() {
       for (long long o = 0; o < f.out; ++o) {
         const float v = static_cast<float>(0.01 * gs.next());
         for (size_t wi = 0; wi < w_.size(); ++wi) {
-          const int gid = w_[wi].gid;
+          const int gid = sid(w_[wi].gid);
           if (o >= f.c0[gid] && o < f.c1[gid])
             fcs[wi][fc_w_off(static_cast<int>(l)) + (o - f.c0[gid]) * f.Ip + col[i]] = v;
         }
@@ -1053,7 +1098,12 @@ void ClusterImpl<TA>::route_forward(int j) {
     ra[i] = w_[i].xb;
     rt[i] = w_[i].tb;
   }
-  if (scheme_ == HP_SCHEME_A) {
+  if (dp_) {  // own examples only
+    for (int i = 0; i < nl; ++i) {
+      HP_CUDA(cudaMemcpyAsync(ra[i], sa[i], b_ * A * es, cudaMemcpyDeviceToDevice, st_));
+      HP_CUDA(cudaMemcpyAsync(rt[i], stt[i], b_ * L_ * sizeof(float), cudaMemcpyDeviceToDevice, st_));
+    }
+  } else if (scheme_ == HP_SCHEME_A) {
     comm_->allgather(sa, ra, b_ * A * es, st_);
     comm_->allgather(stt, rt, b_ * L_ * sizeof(float), st_);
   } else if (scheme_ == HP_SCHEME_B) {
@@ -1086,7 +1136,7 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
     for (auto& w : w_) {
       gemm(w.fc_fwd[l], "fc_fwd", l);
     }
-    if (l + 1 < nf && K_ > 1) {
+    if (l + 1 < nf && fcK_ > 1) {
       std::vector<void*> bufs(nl);
       for (int i = 0; i < nl; ++i) bufs[i] = w_[i].fx[l + 1];
       comm_->allgather_inplace(bufs, g_.fg[l].cmax * ldn_ * sizeof(TA), st_);
@@ -1096,15 +1146,15 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
   // output units are independent).
   const FcGeom& fl = g_.fg.back();
   for (auto& w : w_) {
-    const int rows = static_cast<int>(fl.c1[w.gid] - fl.c0[w.gid]);
-    launch_xent<TA>(w.logits, ldn_, w.tb, L_, static_cast<int>(fl.c0[w.gid]), rows, static_cast<int>(n_),
+    const int rows = static_cast<int>(fl.c1[sid(w.gid)] - fl.c0[sid(w.gid)]);
+    launch_xent<TA>(w.logits, ldn_, w.tb, L_, static_cast<int>(fl.c0[sid(w.gid)]), rows, static_cast<int>(n_),
                     w.fdz[nf - 1], ldn_, w.loss_parts + static_cast<long long>(j) * xblocks_, w.bad, st_);
     ++launches_;
   }
   for (int li = nf - 1; li >= 0; --li) {
     const FcGeom& f = g_.fg[li];
     for (auto& w : w_) {
-      const int rows = static_cast<int>(f.c1[w.gid] - f.c0[w.gid]);
+      const int rows = static_cast<int>(f.c1[sid(w.gid)] - f.c0[sid(w.gid)]);
       GemmPlan pw = w.fc_wgrad[li];
       pw.args.epi.beta = beta ? 1 : 0;
       if (fuse_sgd_) {
@@ -1129,7 +1179,7 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
       launch_rowsum<TA>(w.fdz[li], rows, static_cast<int>(n_), ldn_, w.fgr + fc_b_off(li), beta ? 1 : 0, st_);
       ++launches_;
     }
-    if (li > 0 && K_ > 1) {
+    if (li > 0 && fcK_ > 1) {
       std::vector<const float*> send(nl);
       std::vector<void*> recv(nl);
       for (int i = 0; i < nl; ++i) {
@@ -1146,7 +1196,7 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
 // back to the worker whose example it is, summed over the fc shards.
 template <class TA>
 void ClusterImpl<TA>::return_gradients(int j) {
-  if (K_ == 1) return;  // dgrad wrote gflat directly
+  if (fcK_ == 1) return;  // dgrad wrote gflat directly
   const int nl = comm_->nlocal();
   const long long A = g_.A;
   std::vector<const float*> send(nl);
@@ -1318,7 +1368,7 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
     // Fused FC weight update in the wgrad epilogue: every turn in variable
     // mode (cluster.cpp:586-601), the last turn of the accumulation in exact
     // mode (Σ_j grads × 1/num_sub, cluster.cpp:602-609, 680-696).
-    fuse_sgd_ = fuse_fc_sgd && (variable_ || j == num_sub_ - 1);
+    fuse_sgd_ = fuse_fc_sgd && !dp_ && (variable_ || j == num_sub_ - 1);
     sgd_hp_ = hp;
     sgd_lr_ = variable_ ? fc_lr : lr;
     sgd_has_gscale_ = !variable_ && num_sub_ > 1;
@@ -1329,6 +1379,14 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
     if (variable_) sgd_fc(fc_lr, 1.f, false, hp);  // per-sub-batch update (cluster.cpp:586-601)
   }
   fuse_sgd_ = false;
+  if (dp_ && K_ > 1) {  // pure DP: the FC gradients are all-reduced first (overlapping the conv backward)
+    HP_CUDA(cudaEventRecord(ev0_fc_, st_));
+    HP_CUDA(cudaStreamWaitEvent(sc_, ev0_fc_, 0));
+    std::vector<float*> bufs(nl);
+    for (int i = 0; i < nl; ++i) bufs[i] = w_[i].fgr;
+    comm_->allreduce_f32(bufs, static_cast<size_t>(fc_total_), sc_);
+    launches_ += 1;
+  }
   // Conv backward; each layer's gradients (all local workers) are all-reduced
   // on the side stream as soon as they are final, overlapping the rest of the
   // backward (sync_conv_gradients, cluster.cpp:273-319, bucketed per layer in
@@ -1376,7 +1434,9 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
       }
     }
   }
-  if (!variable_) {
+  if (dp_) {
+    sgd_fc(lr, static_cast<float>(1.0 / static_cast<double>(K_)), K_ > 1, hp);  // mean over workers
+  } else if (!variable_) {
     const bool scale = num_sub_ > 1;
     sgd_fc(lr, static_cast<float>(1.0 / static_cast<double>(num_sub_)), scale, hp);
   }
@@ -1587,7 +1647,7 @@ int64_t ClusterImpl<TA>::param_size(int worker, int which, int layer) const {
   }
   if (layer < 0 || layer >= static_cast<int>(g_.fg.size())) return -1;
   const FcGeom& f = g_.fg[layer];
-  const int64_t ns = f.c1[worker] - f.c0[worker];
+  const int64_t ns = f.c1[sid(worker)] - f.c0[sid(worker)];
   return base == 2 ? f.in * ns : ns;
 }
 
@@ -1618,7 +1678,7 @@ void ClusterImpl<TA>::read_param(int worker, int which, int layer, float* dst, i
     return;
   }
   const FcGeom& f = g_.fg[layer];
-  const long long ns = f.c1[worker] - f.c0[worker];
+  const long long ns = f.c1[sid(worker)] - f.c0[sid(worker)];
   std::vector<float> h(static_cast<size_t>(f.cmax * f.Ip + f.cmax));
   HP_CUDA(cudaMemcpy(h.data(), (mom ? w.fm : w.fp) + fc_w_off(layer), h.size() * sizeof(float),
                      cudaMemcpyDeviceToHost));
@@ -1660,7 +1720,7 @@ void ClusterImpl<TA>::write_param(int worker, int which, int layer, const float*
     }
   } else {
     const FcGeom& f = g_.fg[layer];
-    const long long ns = f.c1[worker] - f.c0[worker];
+    const long long ns = f.c1[sid(worker)] - f.c0[sid(worker)];
     dbase = (mom ? w.fm : w.fp) + fc_w_off(layer);
     h.resize(static_cast<size_t>(f.cmax * f.Ip + f.cmax));
     HP_CUDA(cudaMemcpy(h.data(), dbase, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
@@ -1695,7 +1755,7 @@ void ClusterImpl<TA>::gather_model(float* const* ck, float* const* cb, float* co
   if (comm_->nlocal() != K_) usage_error("gather_model: NCCL transport gathers via hp_cluster_read_param per rank");
   for (size_t l = 0; l < g_.fg.size(); ++l) {
     const FcGeom& f = g_.fg[l];
-    for (int k = 0; k < K_; ++k) {
+    for (int k = 0; k < fcK_; ++k) {
       const long long ns = f.c1[k] - f.c0[k];
       std::vector<float> shard(static_cast<size_t>(f.in * ns));
       read_param(k, 2, static_cast<int>(l), shard.data(), static_cast<int64_t>(shard.size()));

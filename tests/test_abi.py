@@ -94,3 +94,27 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".cuh", ".hpp", "Makefile")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "hpsim_oracle" not in txt and "libhpsim_ref" not in txt, f
+
+
+def test_pure_dp_accounting():
+    """Scheme DP (B200 extension, BASELINE config 5): no boundary / FC-internal
+    traffic; the conv and FC gradient vectors are each all-reduced and charged
+    with the reference's sync formula (G - s_i)*4 + (K-1)*s_i*4 (cluster.cpp:296-304)."""
+    spec = hp.alexnet_1col()
+    K = 8
+    bs, trace, per = hp.step_accounting(spec, hp.ClusterConfig(workers=K, per_worker_batch=128,
+                                                               scheme=hp.Scheme.DP))
+    Gc = sum(l.out_channels * l.in_channels * l.kernel ** 2 + l.out_channels for l in spec.conv_layers)
+    Gf = sum(f.in_dim * f.out_dim + f.out_dim for f in spec.fc_layers)
+    assert Gc == 3_207_104 and Gc + Gf == 61_838_248  # SURVEY 8(d)/(e)
+
+    def charge(G, i):
+        s0, s1 = hp.shard_range(G, K, i)
+        return (G - (s1 - s0)) * 4 + (K - 1) * (s1 - s0) * 4
+    assert bs[0] == 0 and bs[2] == 0  # fc activations / fc internal (MsgClass order, cluster.hpp)
+    assert bs[1] == sum(charge(Gf, i) for i in range(K))
+    assert bs[3] == sum(charge(Gc, i) for i in range(K))
+    assert [e[0] for e in trace] == [0, 1, 2, 3, 4]
+    assert trace[-1][3] == bs[1] + bs[3]
+    for i, (sent, recv) in enumerate(per):
+        assert sent == [0, charge(Gf, i), 0, charge(Gc, i)] and recv == sent

@@ -182,3 +182,39 @@ def test_skip_sync_broadcast_negative_control(math):
     the mean only on its own shard of the flattened conv gradient, so replicas
     diverge exactly as the oracle's do."""
     compare(hp.tiny_cnn(), 4, "B", False, math, 8, skip=True)
+
+
+@pytest.mark.parametrize("math,K", [(hp.MathMode.F32X3, 2), (hp.MathMode.F32X3, 3), (hp.MathMode.BF16, 2)])
+def test_pure_data_parallel_matches_scheme_a(math, K):
+    """Scheme DP (BASELINE config 5's pure-data-parallel comparison): each worker
+    runs the replicated FC stack on its own examples and the FC gradients are
+    all-reduced -- the same exact-SGD update as scheme A on the K*b batch, so
+    the oracle's scheme-A run is the reference; every worker's FC copy matches it."""
+    spec = hp.tiny_cnn()
+    b = 8
+    g = hp.Cluster(spec, hp.ClusterConfig(workers=K, per_worker_batch=b, scheme=hp.Scheme.DP, seed=1,
+                                          math_mode=math))
+    o = O.OracleCluster(spec, workers=K, per_worker_batch=b, scheme="A", precision="single", seed=1)
+    hpg = hp.HyperParams(momentum=0.9, lr=0.05, weight_decay=5e-4)
+    hpo = O.make_hyper_c(0.9, 0.05, 5e-4)
+    mt, wt, lt = TOL[math]
+    for s in range(2):
+        xs, ts = zip(*[hp.synthetic_batch(spec, b, step=s, worker=w) for w in range(K)])
+        r = g.run_step(list(xs), list(ts), hpg)
+        m = o.run_step([x.astype(np.float64) for x in xs], [t.astype(np.float64) for t in ts], hpo)
+        assert abs(r.metrics.loss - m.loss) <= lt * abs(m.loss), (r.metrics.loss, m.loss)
+        assert [e.phase for e in r.trace] == [0, 1, 2, 3, 4]
+    gm = g.gathered_model()
+    om = o.gathered_model() if hasattr(o, "gathered_model") else None
+    for w in range(K):
+        for l in range(len(spec.conv_layers)):
+            for which in (0, 1):
+                e = rel_err(g.param(w, which, l), o.param(0, which, l))
+                assert e <= (mt if which == 1 else wt), (w, which, l, e)
+        for l in range(len(spec.fc_layers)):
+            fin = spec.fc_layers[l].in_dim
+            full_w = np.concatenate([o.param(k, 2, l).reshape(fin, -1) for k in range(K)], axis=1).ravel()
+            full_b = np.concatenate([o.param(k, 3, l) for k in range(K)])
+            assert rel_err(g.param(w, 2, l).ravel(), full_w) <= wt, (w, l)
+            assert rel_err(g.param(w, 3, l), full_b) <= mt, (w, l)
+    del gm, om
