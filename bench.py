@@ -204,28 +204,6 @@ def run_reference_arm(args):
     print(json.dumps(line))
 
 
-def algorithmic_gemm_flops(spec, b: int, world: int) -> float:
-    """Algorithmic GEMM FLOPs of one step on one GPU (SURVEY.md 8(d)/App. B):
-    conv fprop + wgrad + dgrad (conv1 dgrad excluded: the reference discards
-    it), 2 FLOPs per MAC on the useful problem (no padded channels, taps or
-    border rows); the FC stack's 3 GEMMs over K*b examples split K ways."""
-    c, h, w = spec.input_shape
-    total = 0.0
-    for i, l in enumerate(spec.conv_layers):
-        def od(x):
-            return (x + 2 * l.pad - l.kernel) // l.stride + 1
-        oh, ow = od(h), od(w)
-        macs = b * oh * ow * l.out_channels * l.kernel * l.kernel * l.in_channels
-        total += 2.0 * macs * (2 if i == 0 else 3)
-        c, h, w = l.out_channels, oh, ow
-        if l.pool_kernel:
-            h = (h - l.pool_kernel) // l.pool_stride + 1
-            w = (w - l.pool_kernel) // l.pool_stride + 1
-    for f in spec.fc_layers:
-        total += 3 * 2.0 * b * f.in_dim * f.out_dim  # (K*b examples) x (out/K columns)
-    return total
-
-
 # ---------------------------------------------------------------- B200 arm
 def main_b200(args):
     import numpy as np
@@ -363,6 +341,7 @@ def main_b200(args):
         peak_src += " / 2 (tf32)"
     # achieved = ALGORITHMIC GEMM FLOPs of the step (useful work only; the
     # kernels' padded problems are larger) / the GEMM launches' event-timed time
+    from paper_1404_5997_b200.specs import algorithmic_gemm_flops
     alg_flops = algorithmic_gemm_flops(spec, b, world)
     achieved = alg_flops * prof_steps / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
     step_ms = ms / args.steps

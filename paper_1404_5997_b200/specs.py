@@ -91,3 +91,25 @@ def synthetic_batch(spec: ModelSpec, b: int, step: int = 0, worker: int = 0, see
     t = np.zeros((b, spec.num_classes), dtype=np.float32)
     t[np.arange(b), labels] = 1.0
     return x, t
+
+
+def algorithmic_gemm_flops(spec: ModelSpec, b: int, workers: int = 1) -> float:
+    """Algorithmic GEMM FLOPs of one step on one worker:
+    conv fprop + wgrad + dgrad (conv1 dgrad excluded: the reference discards it),
+    2 FLOPs per MAC on the useful problem (no padded channels, taps or border
+    rows); the FC stack's 3 GEMMs over K*b examples split K ways."""
+    c, h, w = spec.input_shape
+    total = 0.0
+    for i, l in enumerate(spec.conv_layers):
+        def od(x):
+            return (x + 2 * l.pad - l.kernel) // l.stride + 1
+        oh, ow = od(h), od(w)
+        macs = b * oh * ow * l.out_channels * l.kernel * l.kernel * l.in_channels
+        total += 2.0 * macs * (2 if i == 0 else 3)
+        c, h, w = l.out_channels, oh, ow
+        if l.pool_kernel:
+            h = (h - l.pool_kernel) // l.pool_stride + 1
+            w = (w - l.pool_kernel) // l.pool_stride + 1
+    for f in spec.fc_layers:
+        total += 3 * 2.0 * b * f.in_dim * f.out_dim
+    return total
