@@ -809,11 +809,25 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
         xb.conv.OW = c.Wq;
       }
     }
+    // Orientation: dW[F][Kc] = dz^T . im2col(x) (M = F), or its transpose
+    // dW^T[Kc][F] = im2col(x)^T . dz (M = Kc, stored transposed) when the F-side
+    // 256-row CTA-pair tiles are badly filled and F makes one wide N tile.
+    // Measured (tests/dev/step_dev.py): conv2 (F=192) 0.151 -> 0.108 ms; conv1
+    // (F=64, N=64 too narrow) and conv3/4 (F=384: two N tiles, MN-major im2col
+    // A loads) are faster unswapped.
+    auto mfill = [](long long m) { return static_cast<double>(m) / (((m + 255) / 256) * 256); };
+    const long long Kw = c.s2d ? Kz : c.Kc;
+    const bool swap = (c.impl_fwd || c.s2d) && c.F >= 128 && c.F <= 256 && mfill(Kw) > mfill(c.F) + 0.1;
     if (c.s2d) {
       eg.c = w.dwz;
       eg.ldc = Kz;
       xb = op(w.z, 1, 0);
       xb.conv = zview;
+    }
+    if (swap) {
+      eg.c_trans = 1;  // element (m = k, n = f) -> dW[f][k]
+      w.conv_wgrad.push_back(plan(xb, op(w.dz[l], 1, c.F), Kw, c.F, c.s2d ? c.P : c.Pq, eg));
+    } else if (c.s2d) {
       w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, Kz, c.P, eg));
     } else {
       w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, c.Kc, c.Pq, eg));

@@ -635,7 +635,9 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
           uint8_t* sa = smem + stage * SB;
           uint8_t* sb = sa + A_BYTES;
           mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
-          if (args.ca.enabled) {
+          if (args.ca.enabled && args.a_mn) {  // wgrad with im2col(x)^T as A: K = pixels
+            load_b_im2col<false, BK, ATOM>(sa, &ta, &full[stage], args.ca, ti.m0, kBM, kt);
+          } else if (args.ca.enabled) {
             load_a_im2col<false, ATOM>(sa, &ta, &full[stage], args.ca, ti.m0, kt);
           } else {
             load_tile_t<false, BK, ATOM>(sa, &ta, &full[stage], args.a_mn, ti.m0, kBM, kt * BK);
@@ -873,7 +875,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           uint8_t* sa = smem + stage * SB;
           uint8_t* sb = sa + A_BYTES;
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * SB);
-          if (args.ca.enabled) {
+          if (args.ca.enabled && args.a_mn) {
+            load_b_im2col<true, BK, ATOM>(sa, &ta, &full[stage], args.ca, am, kBM, kt);
+          } else if (args.ca.enabled) {
             load_a_im2col<true, ATOM>(sa, &ta, &full[stage], args.ca, am, kt);
           } else {
             load_tile_t<true, BK, ATOM>(sa, &ta, &full[stage], args.a_mn, am, kBM, kt * BK);
@@ -1601,8 +1605,9 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   if (splits > 1 && ws == nullptr) throw std::runtime_error("gemm: split-K needs a workspace");
   const int b_rows = use2 ? p.bn / 2 : p.bn;
   if (a.conv.enabled) {
-    if (a.mn_major) throw std::runtime_error("gemm: im2col A must be K-major");
-    p.ta = im2col_map(a.ptr, es, a.conv, kBM, false);
+    // K-major: rows = output pixels (fprop / dgrad); MN-major: K = output
+    // pixels, M = (tap, channel) (wgrad as im2col(x)^T . dY)
+    p.ta = a.mn_major ? im2col_map(a.ptr, es, a.conv, BK, true) : im2col_map(a.ptr, es, a.conv, kBM, false);
   } else {
     p.ta = operand_map(a, a.ptr, es, M, K, kBM);
   }
