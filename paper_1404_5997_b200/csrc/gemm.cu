@@ -1414,6 +1414,7 @@ void launch_math(const GemmPlan& p, cudaStream_t s) {
   if (p.cta2) {
     if constexpr (MATH != kMathF32x3) {
       switch (p.bn) {
+        case 64: launch_inst2<64, MATH>(p, s); return;
         case 128: launch_inst2<128, MATH>(p, s); return;
         case 192: launch_inst2<192, MATH>(p, s); return;
         case 256: launch_inst2<256, MATH>(p, s); return;
@@ -1526,7 +1527,7 @@ static TileChoice choose_tile(int math, const GemmOperand& b, int M, int N) {
     double base;
   };
   const Cand cands[] = {{true, 256, 1.0}, {true, 192, 0.93}, {false, 256, 0.88}, {false, 192, 0.80},
-                        {true, 128, 0.60}, {false, 128, 0.62}, {false, 64, 0.40}};
+                        {true, 128, 0.60}, {false, 128, 0.62}, {true, 64, 0.45}, {false, 64, 0.40}};
   TileChoice best{false, 128};
   double best_score = -1.0;
   for (const Cand& c : cands) {
@@ -1575,7 +1576,7 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   if (use2 && b.mn_major && bn == 192) bn = 256;  // MN-major B halves must be whole 128-byte atoms
   p.cta2 = use2;
   if (use2) {
-    p.bn = (bn == 128 || bn == 192 || bn == 256) ? bn : 256;
+    p.bn = (bn == 64 || bn == 128 || bn == 192 || bn == 256) ? bn : 256;
     if (splits <= 0) {
       const int tiles2 = cdiv(M, 2 * kBM) * cdiv(N, p.bn);
       splits = split_for_waves(tiles2, kt, 74);
