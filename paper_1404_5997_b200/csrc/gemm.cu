@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp: warp-uniform loop (uniform-register descriptors), one elected issuer
       constexpr uint32_t fmt = MATH == kMathBF16 ? 1u : 2u;
       const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
                              (static_cast<uint32_t>(args.a_mn) << 15) |
@@ -693,26 +693,31 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
             const uint64_t bd = umma_desc_sw128(sb + k * b_kstep, b_lbo, b_sbo, b_lay);
             const uint32_t acc = (kt > ti.kt0 || k > 0) ? 1u : 0u;
             if (MATH == kMathBF16) {
-              mma_f16(d, ad, bd, idesc, acc);
+              if (elect_one()) mma_f16(d, ad, bd, idesc, acc);
             } else {
-              mma_tf32(d, ad, bd, idesc, acc);
+              if (elect_one()) mma_tf32(d, ad, bd, idesc, acc);
               if (SPLIT) {
                 const uint64_t ad2 =
                     umma_desc_sw128(sb + B_BYTES + k * a_kstep, a_lbo, a_sbo, a_lay);
                 const uint64_t bd2 =
                     umma_desc_sw128(sb + B_BYTES + A_BYTES + k * b_kstep, b_lbo, b_sbo, b_lay);
-                mma_tf32(d, ad, bd2, idesc, 1u);
-                mma_tf32(d, ad2, bd, idesc, 1u);
+                if (elect_one()) {
+                  mma_tf32(d, ad, bd2, idesc, 1u);
+                  mma_tf32(d, ad2, bd, idesc, 1u);
+                }
               }
             }
+            __syncwarp();
           }
-          mma_commit(&empty[stage]);
+          if (elect_one()) mma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull[buf]);
+        if (elect_one()) mma_commit(&tfull[buf]);
+        __syncwarp();
       }
     }
     __syncwarp();
@@ -895,7 +900,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // leader's whole warp: warp-uniform loop, one elected issuer
       constexpr uint32_t fmt = MATH == kMathBF16 ? 1u : 2u;
       const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
                              (static_cast<uint32_t>(args.a_mn) << 15) |
@@ -931,19 +936,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
             const uint64_t ad = umma_desc_sw128(sa + k * a_kstep, a_lbo, a_sbo, a_lay);
             const uint64_t bd = umma_desc_sw128(sb + k * b_kstep, b_lbo, b_sbo, b_lay);
             const uint32_t acc = (kt > kt0 || k > 0) ? 1u : 0u;
-            if (MATH == kMathBF16) {
-              mma_f16_2sm(d, ad, bd, idesc, acc);
-            } else {
-              mma_tf32_2sm(d, ad, bd, idesc, acc);
+            if (elect_one()) {
+              if (MATH == kMathBF16) {
+                mma_f16_2sm(d, ad, bd, idesc, acc);
+              } else {
+                mma_tf32_2sm(d, ad, bd, idesc, acc);
+              }
             }
+            __syncwarp();
           }
-          mma_commit_2sm(&empty[stage]);
+          if (elect_one()) mma_commit_2sm(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit_2sm(&tfull[buf]);
+        if (elect_one()) mma_commit_2sm(&tfull[buf]);
+        __syncwarp();
       }
     }
     __syncwarp();
@@ -1086,7 +1096,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // leader's whole warp: warp-uniform loop, one elected issuer
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
                              (static_cast<uint32_t>((2 * kBM) >> 4) << 24);
       int stage = 0, hb = 0, local = 0;
@@ -1120,22 +1130,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                 uint64_t ad = umma_desc_sw128(aa, 16, 1024, 2);
                 if (args.sh_boff) ad |= static_cast<uint64_t>((aa >> 7) & 7u) << 49;
                 const uint64_t bd = umma_desc_sw128(sb + k * 32, 16, 1024, 2);
-                mma_f16_2sm(d, ad, bd, idesc, acc);
+                if (elect_one()) mma_f16_2sm(d, ad, bd, idesc, acc);
+                __syncwarp();
                 acc = 1;
               }
-              mma_commit_2sm(&empty[stage]);
+              if (elect_one()) mma_commit_2sm(&empty[stage]);
+              __syncwarp();
               if (++stage == STAGES) {
                 stage = 0;
                 phase ^= 1;
               }
             }
-          mma_commit_2sm(&hempty[hb]);
+          if (elect_one()) mma_commit_2sm(&hempty[hb]);
+          __syncwarp();
           if (++hb == 2) {
             hb = 0;
             hphase ^= 1;
           }
         }
-        mma_commit_2sm(&tfull[buf]);
+        if (elect_one()) mma_commit_2sm(&tfull[buf]);
+        __syncwarp();
       }
     }
     __syncwarp();

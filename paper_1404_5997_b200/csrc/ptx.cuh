@@ -175,6 +175,17 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
 }
 
 // ---------------------------------------------------------------- tcgen05
+// One lane of a fully converged warp (the same lane every call): lets the MMA
+// warp run its loop warp-uniformly, so descriptors live in uniform registers,
+// while exactly one thread issues each tcgen05.mma / commit.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(p));
+  return p != 0;
+}
+
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
