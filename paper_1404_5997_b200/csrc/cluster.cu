@@ -393,7 +393,7 @@ class ClusterImpl final : public ClusterBase {
   std::map<GraphKey, GraphEntry> graphs_;
   double* host_parts_ = nullptr;  // pinned: [nlocal][num_sub * xblocks]
   int* host_bad_ = nullptr;       // pinned: [nlocal]
-  void gemm(const GemmPlan& p, const char* tag, int layer);
+  void gemm(const GemmPlan& p, const char* tag, int layer, cudaStream_t s = nullptr);
   void collect_profile();
   // param layout helpers
   long long conv_k_off(int l) const { return coff_[l]; }
@@ -435,8 +435,13 @@ class ClusterImpl final : public ClusterBase {
   std::vector<Worker<TA>> w_;
   std::vector<long long> coff_, foff_;
   long long conv_total_ = 0, fc_total_ = 0;
-  float* ws_ = nullptr;  // shared split-K workspace (one stream)
+  float* ws_ = nullptr;  // split-K workspace of the compute-stream GEMMs
   size_t ws_floats_ = 0;
+  float* ws2_ = nullptr;  // split-K workspace of the conv wgrad GEMMs (side stream sw_)
+  size_t ws2_floats_ = 0;
+  cudaStream_t sw_ = nullptr;          // side stream: conv bias/weight gradients (off the dgrad chain)
+  std::vector<cudaEvent_t> ev_dz_;     // per conv layer: dz final on st_
+  std::vector<cudaEvent_t> ev_wg_;     // per conv layer: its weight + bias gradients final on sw_
   int xblocks_ = 0;
   int64_t launches_ = 0;
   struct ProfSlot {
@@ -500,6 +505,7 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   HP_CUDA(cudaEventCreateWithFlags(&ev_comm_, cudaEventDisableTiming));
   HP_CUDA(cudaEventCreateWithFlags(&ev0_fc_, cudaEventDisableTiming));
   HP_CUDA(cudaStreamCreateWithFlags(&sx_, cudaStreamNonBlocking));
+  HP_CUDA(cudaStreamCreateWithFlags(&sw_, cudaStreamNonBlocking));
   for (auto& ps : pref_) {
     HP_CUDA(cudaEventCreateWithFlags(&ps.ready, cudaEventDisableTiming));
     HP_CUDA(cudaEventCreateWithFlags(&ps.used, cudaEventDisableTiming));
@@ -638,6 +644,10 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   comm_->reserve(comm_scratch * sizeof(float));
   ev_layer_.resize(g_.cg.size());
   for (auto& e : ev_layer_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  ev_dz_.resize(g_.cg.size());
+  ev_wg_.resize(g_.cg.size());
+  for (auto& e : ev_dz_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : ev_wg_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   HP_CUDA(cudaMallocHost(&host_parts_, sizeof(double) * nl * num_sub_ * xblocks_));
   HP_CUDA(cudaMallocHost(&host_bad_, sizeof(int) * nl));
   // Plans first with a null workspace to size it (for both conv kernel
@@ -649,6 +659,7 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   }
   use_shift = shift;
   ws_ = ws_floats_ > 0 ? arena_.make<float>(static_cast<long long>(ws_floats_)) : nullptr;
+  ws2_ = ws2_floats_ > 0 ? arena_.make<float>(static_cast<long long>(ws2_floats_)) : nullptr;
   for (auto& w : w_) build_plans(w);
   init_params();
   sent.assign(K_, {0, 0, 0, 0});
@@ -667,6 +678,12 @@ ClusterImpl<TA>::~ClusterImpl() {
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   for (auto e : ev_layer_) cudaEventDestroy(e);
+  for (auto e : ev_dz_) cudaEventDestroy(e);
+  for (auto e : ev_wg_) cudaEventDestroy(e);
+  if (sw_) {
+    cudaStreamSynchronize(sw_);
+    cudaStreamDestroy(sw_);
+  }
   if (ev_comm_) cudaEventDestroy(ev_comm_);
   if (ev0_fc_) cudaEventDestroy(ev0_fc_);
   if (sc_) cudaStreamDestroy(sc_);
@@ -721,14 +738,18 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     return o;
   };
   auto plan = [&](const GemmOperand& a, const GemmOperand& b, long long M, long long N, long long K,
-                  const Epi& e) {
+                  const Epi& e, bool side = false) {
     // The plan picks its own tile and split-K; the first (sizing) pass runs
-    // against a placeholder workspace and records the largest need.
-    float* ws = ws_ != nullptr ? ws_ : reinterpret_cast<float*>(256);
+    // against a placeholder workspace and records the largest need. Side-stream
+    // (wgrad) plans get their own workspace: they run concurrently with the
+    // compute stream's GEMMs.
+    float* real = side ? ws2_ : ws_;
+    size_t& need = side ? ws2_floats_ : ws_floats_;
+    float* ws = real != nullptr ? real : reinterpret_cast<float*>(256);
     GemmPlan pl = gemm_plan(math_, a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e, 0,
                             ws, 0);
-    if (pl.splits > 1) ws_floats_ = std::max(ws_floats_, static_cast<size_t>(pl.splits * M * N));
-    else pl.args.ws = ws_;
+    if (pl.splits > 1) need = std::max(need, static_cast<size_t>(pl.splits * M * N));
+    else pl.args.ws = real;
     return pl;
   };
   w.conv_fwd.clear();
@@ -826,11 +847,11 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     }
     if (swap) {
       eg.c_trans = 1;  // element (m = k, n = f) -> dW[f][k]
-      w.conv_wgrad.push_back(plan(xb, op(w.dz[l], 1, c.F), Kw, c.F, c.s2d ? c.P : c.Pq, eg));
+      w.conv_wgrad.push_back(plan(xb, op(w.dz[l], 1, c.F), Kw, c.F, c.s2d ? c.P : c.Pq, eg, true));
     } else if (c.s2d) {
-      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, Kz, c.P, eg));
+      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, Kz, c.P, eg, true));
     } else {
-      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, c.Kc, c.Pq, eg));
+      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, c.Kc, c.Pq, eg, true));
     }
     if (l == 0) {
       w.conv_dgrad.push_back(GemmPlan{});
@@ -936,7 +957,8 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
 // Every tcgen05 GEMM of the step goes through here: launch, count, and (when
 // profiling) bracket with CUDA events on the launching stream.
 template <class TA>
-void ClusterImpl<TA>::gemm(const GemmPlan& p, const char* tag, int layer) {
+void ClusterImpl<TA>::gemm(const GemmPlan& p, const char* tag, int layer, cudaStream_t stream) {
+  cudaStream_t st = stream ? stream : st_;
   const double flops = 2.0 * p.args.M * static_cast<double>(p.args.N) * p.args.K;
   if (profile) {
     if (prof_used_ == prof_pool_.size()) {
@@ -949,11 +971,11 @@ void ClusterImpl<TA>::gemm(const GemmPlan& p, const char* tag, int layer) {
     s.tag = tag;
     s.layer = layer;
     s.flops = flops;
-    HP_CUDA(cudaEventRecord(s.a, st_));
-    gemm_launch(p, st_);
-    HP_CUDA(cudaEventRecord(s.b, st_));
+    HP_CUDA(cudaEventRecord(s.a, st));
+    gemm_launch(p, st);
+    HP_CUDA(cudaEventRecord(s.b, st));
   } else {
-    gemm_launch(p, st_);
+    gemm_launch(p, st);
   }
   launches_ += p.splits > 1 ? 2 : 1;
   gemm_flops_ += flops;
@@ -1263,14 +1285,29 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
     launch_mask_cast<TA, TA>(cs.gout, mask, w.dz[l], c.P * c.F, st_);
     ++launches_;
   }
+  // Weight and bias gradients of this layer only feed the update (and the
+  // all-reduce), not the backward chain: they run on the side stream sw_,
+  // overlapping this layer's dgrad and the layers below (serialised on st_ when
+  // profiling, for clean per-GEMM times).
+  cudaStream_t ws = profile ? st_ : sw_;
+  if (ws != st_) {
+    HP_CUDA(cudaEventRecord(ev_dz_[l], st_));
+    HP_CUDA(cudaStreamWaitEvent(ws, ev_dz_[l], 0));
+  }
   // bias grad = channel sums of dz (model.cpp:184-202)
-  launch_colsum<TA>(w.dz[l], c.Pq, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, st_);
+  launch_colsum<TA>(w.dz[l], c.Pq, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, ws);
   launches_ += 2;
-  gemm(w.conv_wgrad[l], "conv_wgrad", l);
+  gemm(w.conv_wgrad[l], "conv_wgrad", l, ws);
   if (c.s2d) {
-    launch_s2d_wgrad_gather(w.dwz, w.cgr + conv_k_off(l), c.ldk, c.F, c.C, c.R, c.S, c.stride, c.Rq, c.Cz, st_);
+    launch_s2d_wgrad_gather(w.dwz, w.cgr + conv_k_off(l), c.ldk, c.F, c.C, c.R, c.S, c.stride, c.Rq, c.Cz, ws);
     ++launches_;
   }
+  if (K_ > 1 && skip_sync_broadcast) {  // keep the local gradients for the negative control
+    const long long cnt = static_cast<long long>(c.F) * c.ldk + c.F;
+    HP_CUDA(cudaMemcpyAsync(w.cgr_local + conv_k_off(l), w.cgr + conv_k_off(l), cnt * sizeof(float),
+                            cudaMemcpyDeviceToDevice, ws));
+  }
+  HP_CUDA(cudaEventRecord(ev_wg_[l], ws));
   if (l == 0) return;
   const ConvGeom& pc = g_.cg[l - 1];
   const bool below_fused = pc.pk > 0 || pc.lrn_n > 0;
@@ -1409,15 +1446,9 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
   std::vector<ConvBwdState> cbs(nl);
   for (int l = nc - 1; l >= 0; --l) {
     for (int i = 0; i < nl; ++i) conv_backward_layer(w_[i], l, cbs[i]);
-    if (K_ > 1 && skip_sync_broadcast) {  // keep the local gradients for the negative control
-      const long long cnt = static_cast<long long>(g_.cg[l].F) * g_.cg[l].ldk + g_.cg[l].F;
-      for (int i = 0; i < nl; ++i)
-        HP_CUDA(cudaMemcpyAsync(w_[i].cgr_local + conv_k_off(l), w_[i].cgr + conv_k_off(l), cnt * sizeof(float),
-                                cudaMemcpyDeviceToDevice, st_));
-    }
     if (K_ > 1) {
-      HP_CUDA(cudaEventRecord(ev_layer_[l], st_));
-      HP_CUDA(cudaStreamWaitEvent(sc_, ev_layer_[l], 0));
+      // ev_wg_[l]: the last local worker's gradients of layer l (sw_ is in order)
+      HP_CUDA(cudaStreamWaitEvent(sc_, ev_wg_[l], 0));
       std::vector<float*> bufs(nl);
       for (int i = 0; i < nl; ++i) bufs[i] = w_[i].cgr + conv_k_off(l);
       const long long cnt = static_cast<long long>(g_.cg[l].F) * g_.cg[l].ldk + g_.cg[l].F;
@@ -1425,6 +1456,7 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
       launches_ += 1;
     }
   }
+  HP_CUDA(cudaStreamWaitEvent(st_, ev_wg_[0], 0));  // join sw_ (layer 0 is its last work)
   if (K_ > 1) {
     HP_CUDA(cudaEventRecord(ev_comm_, sc_));
     HP_CUDA(cudaStreamWaitEvent(st_, ev_comm_, 0));
