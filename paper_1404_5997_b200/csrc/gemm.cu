@@ -915,6 +915,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const uint32_t b_lay = (ES == 4 && args.b_mn) ? 1 : 2;
       const uint32_t a_kstep = args.a_mn ? UK * 128 : UK * ES;
       const uint32_t b_kstep = args.b_mn ? UK * 128 : UK * ES;
+      const uint32_t ahi = umma_desc_hi(a_sbo, a_lay), bhi = umma_desc_hi(b_sbo, b_lay);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -931,18 +932,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * SB);
           const uint32_t sb = sa + A_BYTES;
+          const uint32_t alo = (sa >> 4) | ((a_lbo >> 4) << 16), blo = (sb >> 4) | ((b_lbo >> 4) << 16);
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k) {
-            const uint64_t ad = umma_desc_sw128(sa + k * a_kstep, a_lbo, a_sbo, a_lay);
-            const uint64_t bd = umma_desc_sw128(sb + k * b_kstep, b_lbo, b_sbo, b_lay);
             const uint32_t acc = (kt > kt0 || k > 0) ? 1u : 0u;
-            if (elect_one()) {
-              if (MATH == kMathBF16) {
-                mma_f16_2sm(d, ad, bd, idesc, acc);
-              } else {
-                mma_tf32_2sm(d, ad, bd, idesc, acc);
-              }
-            }
+            if (elect_one())
+              mma_2sm_lohi<MATH != kMathBF16>(d, alo + k * (a_kstep >> 4), ahi, blo + k * (b_kstep >> 4), bhi,
+                                              idesc, acc);
             __syncwarp();
           }
           if (elect_one()) mma_commit_2sm(&empty[stage]);
@@ -1102,6 +1098,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       int stage = 0, hb = 0, local = 0;
       uint32_t phase = 0, hphase = 0;
       const uint32_t halo0 = smem_u32(halo);
+      constexpr uint32_t hi0 = umma_desc_hi(1024, 2);
       for (int t = cid; t < total; t += ncl, ++local) {
         const int buf = local & 1;
         const uint32_t use = static_cast<uint32_t>(local >> 1);
@@ -1119,18 +1116,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
               tc_fence_after();
               const uint32_t a0 = hbase + static_cast<uint32_t>(r * args.sh_wq + sx) * 128u;
               const uint32_t sb = smem_u32(bst + stage * B_BYTES);
+              // The 128B swizzle is a function of the ABSOLUTE smem address bits
+              // (TMA wrote the halo 1024-aligned), so a descriptor starting any
+              // whole row into the halo reads rows a0.. correctly with the
+              // descriptor base offset left 0 (measured: setting it to
+              // (a0 >> 7) & 7 double-applies the phase).
+              const uint32_t ahi = args.sh_boff ? (hi0 | (((a0 >> 7) & 7u) << 17)) : hi0;
+              const uint32_t alo = (a0 >> 4) | (1u << 16), blo = (sb >> 4) | (1u << 16);
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
-                const uint32_t aa = a0 + k * 32;
-                // The 128B swizzle is a function of the ABSOLUTE smem address bits
-                // (TMA wrote the halo 1024-aligned), so a descriptor starting any
-                // whole row into the halo reads rows aa.. correctly with the
-                // descriptor base offset left 0 (measured: setting it to
-                // (aa >> 7) & 7 double-applies the phase).
-                uint64_t ad = umma_desc_sw128(aa, 16, 1024, 2);
-                if (args.sh_boff) ad |= static_cast<uint64_t>((aa >> 7) & 7u) << 49;
-                const uint64_t bd = umma_desc_sw128(sb + k * 32, 16, 1024, 2);
-                if (elect_one()) mma_f16_2sm(d, ad, bd, idesc, acc);
+                if (elect_one()) mma_2sm_lohi<false>(d, alo + 2 * k, ahi, blo + 2 * k, hi0, idesc, acc);
                 __syncwarp();
                 acc = 1;
               }
