@@ -687,29 +687,26 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * SB);
           const uint32_t sb = sa + A_BYTES;
+          if (elect_one()) {  // the stage's MMAs back to back, then the commit
 #pragma unroll
-          for (int k = 0; k < BK / UK; ++k) {
-            const uint64_t ad = umma_desc_sw128(sa + k * a_kstep, a_lbo, a_sbo, a_lay);
-            const uint64_t bd = umma_desc_sw128(sb + k * b_kstep, b_lbo, b_sbo, b_lay);
-            const uint32_t acc = (kt > ti.kt0 || k > 0) ? 1u : 0u;
-            if (MATH == kMathBF16) {
-              if (elect_one()) mma_f16(d, ad, bd, idesc, acc);
-            } else {
-              if (elect_one()) mma_tf32(d, ad, bd, idesc, acc);
-              if (SPLIT) {
-                const uint64_t ad2 =
-                    umma_desc_sw128(sb + B_BYTES + k * a_kstep, a_lbo, a_sbo, a_lay);
-                const uint64_t bd2 =
-                    umma_desc_sw128(sb + B_BYTES + A_BYTES + k * b_kstep, b_lbo, b_sbo, b_lay);
-                if (elect_one()) {
+            for (int k = 0; k < BK / UK; ++k) {
+              const uint64_t ad = umma_desc_sw128(sa + k * a_kstep, a_lbo, a_sbo, a_lay);
+              const uint64_t bd = umma_desc_sw128(sb + k * b_kstep, b_lbo, b_sbo, b_lay);
+              const uint32_t acc = (kt > ti.kt0 || k > 0) ? 1u : 0u;
+              if (MATH == kMathBF16) {
+                mma_f16(d, ad, bd, idesc, acc);
+              } else {
+                mma_tf32(d, ad, bd, idesc, acc);
+                if (SPLIT) {
+                  const uint64_t ad2 = umma_desc_sw128(sb + B_BYTES + k * a_kstep, a_lbo, a_sbo, a_lay);
+                  const uint64_t bd2 = umma_desc_sw128(sb + B_BYTES + A_BYTES + k * b_kstep, b_lbo, b_sbo, b_lay);
                   mma_tf32(d, ad, bd2, idesc, 1u);
                   mma_tf32(d, ad2, bd, idesc, 1u);
                 }
               }
             }
-            __syncwarp();
+            mma_commit(&empty[stage]);
           }
-          if (elect_one()) mma_commit(&empty[stage]);
           __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
@@ -933,15 +930,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           const uint32_t sa = smem_u32(smem + stage * SB);
           const uint32_t sb = sa + A_BYTES;
           const uint32_t alo = (sa >> 4) | ((a_lbo >> 4) << 16), blo = (sb >> 4) | ((b_lbo >> 4) << 16);
+          // one elected thread issues the stage's MMAs back to back (descriptors
+          // in uniform registers; bf16 hi words are immediates) and the commit
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / UK; ++k) {
-            const uint32_t acc = (kt > kt0 || k > 0) ? 1u : 0u;
-            if (elect_one())
-              mma_2sm_lohi<MATH != kMathBF16>(d, alo + k * (a_kstep >> 4), ahi, blo + k * (b_kstep >> 4), bhi,
-                                              idesc, acc);
-            __syncwarp();
+            for (int k = 0; k < BK / UK; ++k) {
+              const uint32_t acc = (kt > kt0 || k > 0) ? 1u : 0u;
+              if (MATH == kMathBF16) {
+                constexpr uint64_t H = umma_desc_hi(1024, 2);
+                mma_f16_2sm_lo<H, H>(d, alo + k * (a_kstep >> 4), blo + k * (b_kstep >> 4), idesc, acc);
+              } else {
+                mma_2sm_lohi<true>(d, alo + k * (a_kstep >> 4), ahi, blo + k * (b_kstep >> 4), bhi, idesc, acc);
+              }
+            }
+            mma_commit_2sm(&empty[stage]);
           }
-          if (elect_one()) mma_commit_2sm(&empty[stage]);
           __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
@@ -1121,16 +1124,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
               // whole row into the halo reads rows a0.. correctly with the
               // descriptor base offset left 0 (measured: setting it to
               // (a0 >> 7) & 7 double-applies the phase).
-              const uint32_t ahi = args.sh_boff ? (hi0 | (((a0 >> 7) & 7u) << 17)) : hi0;
               const uint32_t alo = (a0 >> 4) | (1u << 16), blo = (sb >> 4) | (1u << 16);
+              if (elect_one()) {  // the tap's MMAs back to back, then the commit
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                if (elect_one()) mma_2sm_lohi<false>(d, alo + 2 * k, ahi, blo + 2 * k, hi0, idesc, acc);
-                __syncwarp();
-                acc = 1;
+                for (int k = 0; k < 4; ++k) mma_f16_2sm_lo<hi0, hi0>(d, alo + 2 * k, blo + 2 * k, idesc, acc | (k > 0));
+                mma_commit_2sm(&empty[stage]);
               }
-              if (elect_one()) mma_commit_2sm(&empty[stage]);
               __syncwarp();
+              acc = 1;
               if (++stage == STAGES) {
                 stage = 0;
                 phase ^= 1;

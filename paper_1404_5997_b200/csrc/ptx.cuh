@@ -179,6 +179,20 @@ __device__ __forceinline__ void mma_2sm_lohi(uint32_t d, uint32_t alo, uint32_t 
         : "memory");
   }
 }
+// Variant with compile-time hi words (immediates: only the lo words are
+// registers that need moving into the uniform datapath).
+template <uint64_t AHI, uint64_t BHI>
+__device__ __forceinline__ void mma_f16_2sm_lo(uint32_t d, uint32_t alo, uint32_t blo, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+      "cvt.u64.u32 da, %1;\n\tor.b64 da, da, %5;\n\t"
+      "cvt.u64.u32 db, %2;\n\tor.b64 db, db, %6;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(d),
+      "r"(alo), "r"(blo), "r"(idesc), "r"(accumulate), "n"(AHI << 32), "n"(BHI << 32)
+      : "memory");
+}
 // hi word of umma_desc_sw128 (SBO, version bit 46, layout bits 61-63)
 __host__ __device__ constexpr uint32_t umma_desc_hi(uint32_t sbo, uint32_t layout) {
   return ((sbo >> 4) & 0x3FFFu) | (1u << 14) | (layout << 29);
