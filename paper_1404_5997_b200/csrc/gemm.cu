@@ -324,7 +324,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int
   // write straight from the row-per-thread layout: 32 contiguous outputs per
   // thread, no smem round trip (the staged transpose costs shared-memory
   // bandwidth the MMAs need; it pays only when the epilogue also reads HBM).
-  const bool direct = !(a.dbg & 2) && (a.raw_partial || (!a.epi.beta && !a.epi.mask && !a.epi.sgd_w));
+  const bool direct = !(a.dbg & 2) && (a.raw_partial || (!a.epi.beta && !a.epi.sgd_w));
   if (direct || !epi_vec_ok(a)) {
     epi_row32(a, m0 + lane, n0, split, v, mself);
     return;
