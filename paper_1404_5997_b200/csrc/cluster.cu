@@ -795,11 +795,11 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     // bf16 stride-1 convs over zero-bordered rows: the flat-shift kernel (one
     // smem halo per channel block for all taps); output rows are the stored
     // grid, the RowMap keeps the valid ones
-    // Measured on B200 (tests/dev/step_dev.py): the shift kernel wins on the
-    // 3x3 layers (fewer, wider K blocks per halo); the TMA-im2col kernel is as
-    // fast or faster on the 5x5 / space-to-depth layers with 64-wide operands.
-    const bool shift_fwd = bf && use_shift && !c.s2d && c.R <= 3 && c.in_q &&
-                           conv_shift_supported(c.C, c.R, c.S, c.Wq, c.F);
+    // Measured on B200 (tests/dev/step_dev.py): the shift kernel wins on every
+    // q-layout layer (conv2-5 fprop and dgrad).
+    // (conv1's space-to-depth input -- 64 channels, 9 taps, N = 64 -- measures
+    // faster on the TMA-im2col kernel: 0.092 vs 0.099 ms)
+    const bool shift_fwd = bf && use_shift && !c.s2d && c.in_q && conv_shift_supported(c.C, c.R, c.S, c.Wq, c.F);
     if (shift_fwd) {
       Epi es = e;
       const int gH = c.s2d ? c.Zh : c.Hq, gW = c.s2d ? c.Zw : c.Wq;
@@ -886,7 +886,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
         dy.conv.hi = -c.pad;
       }
       const long long kd = static_cast<long long>(c.R) * c.S * c.F;  // dgrad reduces over (r, s, f)
-      if (bf && use_shift && c.in_q && c.R <= 3 && conv_shift_supported(c.F, c.R, c.S, c.Wq, c.C)) {
+      if (bf && use_shift && c.in_q && conv_shift_supported(c.F, c.R, c.S, c.Wq, c.C)) {
         // dX over the stored q grid of dz: rows (b, h, w) valid for h < H, w < W
         ed.rows = ed.rows.enabled ? RowMap{1, c.Hq, c.Wq, c.H, c.W, ed.rows.dH, ed.rows.dW, ed.rows.dp}
                                   : RowMap{1, c.Hq, c.Wq, c.H, c.W, c.H, c.W, 0};
