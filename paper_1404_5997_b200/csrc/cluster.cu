@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -833,9 +834,9 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     // Orientation: dW[F][Kc] = dz^T . im2col(x) (M = F), or its transpose
     // dW^T[Kc][F] = im2col(x)^T . dz (M = Kc, stored transposed) when the F-side
     // 256-row CTA-pair tiles are badly filled and F makes one wide N tile.
-    // Measured (tests/dev/step_dev.py): conv2 (F=192) 0.151 -> 0.108 ms; conv1
-    // (F=64, N=64 too narrow) and conv3/4 (F=384: two N tiles, MN-major im2col
-    // A loads) are faster unswapped.
+    // Measured (tests/dev/step_dev.py, after the MMA-issue rework): conv2
+    // (F=192) 0.157 -> 0.110 ms swapped; conv1 (F=64) 0.107 vs 0.118, conv3
+    // 0.067 vs 0.071, conv4 (F=384) 0.114 vs 0.120 faster unswapped.
     auto mfill = [](long long m) { return static_cast<double>(m) / (((m + 255) / 256) * 256); };
     const long long Kw = c.s2d ? Kz : c.Kc;
     const bool swap = (c.impl_fwd || c.s2d) && c.F >= 128 && c.F <= 256 && mfill(Kw) > mfill(c.F) + 0.1;
