@@ -39,15 +39,16 @@ def conv_shift(B, Cin, H, F, R):
         assert lib.hp_kernel_conv_shift(x.data_ptr(), rows, Cin, R, R, H + p, w.data_ptr(), F, y.data_ptr(), 0, None) == 0, last_error()
     return f, (x, w, y), 2.0 * rows * F * R * R * Cin
 
-for flags in (0, 1):
-    lib.hp_debug_gemm_flags(flags)
-    for (M, N, K) in [(8192, 8192, 8192), (93312, 192, 1600), (21632, 384, 3456)]:
-        for cta2, bn in ((1, 256), (1, 192), (0, 256)):
-            f, keep = gemm_fn(M, N, K, bn, cta2)
-            t = timeit(f)
-            print(f"flags={flags} gemm {str((M,N,K)):22s} cta2={cta2} bn={bn}: {t:.4f} ms {2*M*N*K/t/1e9:7.0f} TF/s", flush=True)
-    for args in [(128, 384, 13, 384, 3), (128, 192, 13, 384, 3), (128, 64, 27, 192, 5)]:
-        f, keep, fl = conv_shift(*args)
-        t = timeit(f)
-        print(f"flags={flags} shift {str(args):22s}: {t:.4f} ms {fl/t/1e9:7.0f} TF/s", flush=True)
-lib.hp_debug_gemm_flags(0)
+if __name__ == "__main__":
+  for flags in (0, 1):
+      lib.hp_debug_gemm_flags(flags)
+      for (M, N, K) in [(8192, 8192, 8192), (93312, 192, 1600), (21632, 384, 3456)]:
+          for cta2, bn in ((1, 256), (1, 192), (0, 256)):
+              f, keep = gemm_fn(M, N, K, bn, cta2)
+              t = timeit(f)
+              print(f"flags={flags} gemm {str((M,N,K)):22s} cta2={cta2} bn={bn}: {t:.4f} ms {2*M*N*K/t/1e9:7.0f} TF/s", flush=True)
+      for args in [(128, 384, 13, 384, 3), (128, 192, 13, 384, 3), (128, 64, 27, 192, 5)]:
+          f, keep, fl = conv_shift(*args)
+          t = timeit(f)
+          print(f"flags={flags} shift {str(args):22s}: {t:.4f} ms {fl/t/1e9:7.0f} TF/s", flush=True)
+  lib.hp_debug_gemm_flags(0)
