@@ -829,6 +829,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
         xb.conv.hi = -c.pad;
         xb.conv.OH = c.Hq;
         xb.conv.OW = c.Wq;
+        xb.conv.shift = 1;  // tiled boxes at shifted rows of the flat q-layout x
       }
     }
     // Orientation: dW[F][Kc] = dz^T . im2col(x) (M = F), or its transpose

@@ -546,6 +546,19 @@ __device__ __forceinline__ void load_b_im2col(uint8_t* dst, const CUtensorMap* t
   }
 }
 
+// Shift-mode MN-major conv operand (wgrad over q-layout x): `rows` columns =
+// rows/ATOM channel blocks, each at its own tap, as tiled boxes at shifted rows.
+template <bool TWO, int BK, int ATOM>
+__device__ __forceinline__ void load_mn_shift(uint8_t* dst, const CUtensorMap* tm, uint64_t* bar, const ConvArgs& c,
+                                              int n0, int rows, int kt) {
+  for (int a = 0; a < rows / ATOM; ++a) {
+    const int col = n0 + a * ATOM;
+    const int tap = col / c.C, ch = col - tap * c.C;
+    const int r = tap / c.S, s = tap - r * c.S;
+    tma2d<TWO>(dst + a * (BK * 128), tm, bar, ch, kt * BK + r * c.wq + s + c.base_off);
+  }
+}
+
 // Persistent tile loop. Tiles t = blockIdx.x, blockIdx.x + gridDim.x, ... in
 // (split, m, n) order with n fastest, so co-resident CTAs share A tiles in L2.
 // Two TMEM accumulators: the epilogue of tile i overlaps the MMAs of tile i+1.
@@ -635,14 +648,18 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
           uint8_t* sa = smem + stage * SB;
           uint8_t* sb = sa + A_BYTES;
           mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
-          if (args.ca.enabled && args.a_mn) {  // wgrad with im2col(x)^T as A: K = pixels
+          if (args.ca.enabled && args.a_mn && args.ca.shift) {
+            load_mn_shift<false, BK, ATOM>(sa, &ta, &full[stage], args.ca, ti.m0, kBM, kt);
+          } else if (args.ca.enabled && args.a_mn) {  // wgrad with im2col(x)^T as A: K = pixels
             load_b_im2col<false, BK, ATOM>(sa, &ta, &full[stage], args.ca, ti.m0, kBM, kt);
           } else if (args.ca.enabled) {
             load_a_im2col<false, ATOM>(sa, &ta, &full[stage], args.ca, ti.m0, kt);
           } else {
             load_tile_t<false, BK, ATOM>(sa, &ta, &full[stage], args.a_mn, ti.m0, kBM, kt * BK);
           }
-          if (args.cb.enabled) {
+          if (args.cb.enabled && args.cb.shift) {
+            load_mn_shift<false, BK, ATOM>(sb, &tb, &full[stage], args.cb, ti.n0, BN, kt);
+          } else if (args.cb.enabled) {
             load_b_im2col<false, BK, ATOM>(sb, &tb, &full[stage], args.cb, ti.n0, BN, kt);
           } else {
             load_tile_t<false, BK, ATOM>(sb, &tb, &full[stage], args.b_mn, ti.n0, BN, kt * BK);
@@ -877,14 +894,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           uint8_t* sa = smem + stage * SB;
           uint8_t* sb = sa + A_BYTES;
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * SB);
-          if (args.ca.enabled && args.a_mn) {
+          if (args.ca.enabled && args.a_mn && args.ca.shift) {
+            load_mn_shift<true, BK, ATOM>(sa, &ta, &full[stage], args.ca, am, kBM, kt);
+          } else if (args.ca.enabled && args.a_mn) {
             load_b_im2col<true, BK, ATOM>(sa, &ta, &full[stage], args.ca, am, kBM, kt);
           } else if (args.ca.enabled) {
             load_a_im2col<true, ATOM>(sa, &ta, &full[stage], args.ca, am, kt);
           } else {
             load_tile_t<true, BK, ATOM>(sa, &ta, &full[stage], args.a_mn, am, kBM, kt * BK);
           }
-          if (args.cb.enabled) {
+          if (args.cb.enabled && args.cb.shift) {
+            load_mn_shift<true, BK, ATOM>(sb, &tb, &full[stage], args.cb, bn0, BNH, kt);
+          } else if (args.cb.enabled) {
             load_b_im2col<true, BK, ATOM>(sb, &tb, &full[stage], args.cb, bn0, BNH, kt);
           } else {
             load_tile_t<true, BK, ATOM>(sb, &tb, &full[stage], args.b_mn, bn0, BNH, kt * BK);
@@ -1386,6 +1407,9 @@ ConvArgs conv_args(const Im2col& g) {
   c.stride = g.stride;
   c.lo_w = g.corners ? g.lo : -g.pad;
   c.lo_h = g.corners ? g.lo : -g.pad;
+  c.shift = g.shift;
+  c.wq = g.W;
+  c.base_off = -(g.pad * g.W + g.pad);
   return c;
 }
 
@@ -1618,11 +1642,21 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   if (a.conv.enabled) {
     // K-major: rows = output pixels (fprop / dgrad); MN-major: K = output
     // pixels, M = (tap, channel) (wgrad as im2col(x)^T . dY)
-    p.ta = a.mn_major ? im2col_map(a.ptr, es, a.conv, BK, true) : im2col_map(a.ptr, es, a.conv, kBM, false);
+    if (a.conv.shift) {
+      if (!a.mn_major) throw std::runtime_error("gemm: shift-mode A must be MN-major");
+      p.ta = make_map(a.ptr, es, a.conv.C, static_cast<long long>(a.conv.N) * a.conv.H * a.conv.W, a.conv.C, 128 / es,
+                      BK, es == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B);
+    } else {
+      p.ta = a.mn_major ? im2col_map(a.ptr, es, a.conv, BK, true) : im2col_map(a.ptr, es, a.conv, kBM, false);
+    }
   } else {
     p.ta = operand_map(a, a.ptr, es, M, K, kBM);
   }
-  if (b.conv.enabled) {
+  if (b.conv.enabled && b.conv.shift) {
+    if (!b.mn_major) throw std::runtime_error("gemm: shift-mode B must be MN-major");
+    p.tb = make_map(b.ptr, es, b.conv.C, static_cast<long long>(b.conv.N) * b.conv.H * b.conv.W, b.conv.C, 128 / es,
+                    BK, es == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B);
+  } else if (b.conv.enabled) {
     if (!b.mn_major) throw std::runtime_error("gemm: im2col B must be MN-major");
     p.tb = im2col_map(b.ptr, es, b.conv, BK, true);
   } else {

@@ -81,6 +81,11 @@ struct Im2col {
   // memory and the box walks either the valid outputs (lo 0, hi -p) or every
   // stored position (lo -p, hi -p).
   int corners = 0, lo = 0, hi = 0;
+  // shift = 1 (MN-major operands, wgrad): x is a plain [N*H*W][C] q-layout
+  // matrix and the K index is a stored q position; the (tap r, s) column block
+  // of k-tile kt is the tiled TMA box at rows kt*BK + r*W + s - (pad*W + pad)
+  // (zero fill outside) -- plain tiled loads instead of TMA im2col.
+  int shift = 0;
 };
 
 
@@ -93,6 +98,7 @@ struct GemmOperand {
 
 struct ConvArgs {            // device-side im2col bookkeeping (see Im2col)
   int enabled, C, S, OH, OW, stride, lo_w, lo_h;
+  int shift, wq, base_off;   // Im2col::shift mode
 };
 
 struct GemmArgs {
