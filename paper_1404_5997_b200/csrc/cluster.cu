@@ -441,6 +441,11 @@ class ClusterImpl final : public ClusterBase {
   float* ws2_ = nullptr;  // split-K workspace of the conv wgrad GEMMs (side stream sw_)
   size_t ws2_floats_ = 0;
   cudaStream_t sw_ = nullptr;          // side stream: conv bias/weight gradients (off the dgrad chain)
+  cudaStream_t sf_ = nullptr;          // side stream: FC weight gradients + fused update (off the backward chain)
+  cudaEvent_t ev_fcd_ = nullptr;       // FC dgrad of the current layer done (st_)
+  cudaEvent_t ev_fcw_ = nullptr;       // all FC wgrads of the turn done (sf_)
+  float* ws3_ = nullptr;               // split-K workspace of the FC wgrad GEMMs (sf_)
+  size_t ws3_floats_ = 0;
   std::vector<cudaEvent_t> ev_dz_;     // per conv layer: dz final on st_
   std::vector<cudaEvent_t> ev_wg_;     // per conv layer: its weight + bias gradients final on sw_
   int xblocks_ = 0;
@@ -507,6 +512,9 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   HP_CUDA(cudaEventCreateWithFlags(&ev0_fc_, cudaEventDisableTiming));
   HP_CUDA(cudaStreamCreateWithFlags(&sx_, cudaStreamNonBlocking));
   HP_CUDA(cudaStreamCreateWithFlags(&sw_, cudaStreamNonBlocking));
+  HP_CUDA(cudaStreamCreateWithFlags(&sf_, cudaStreamNonBlocking));
+  HP_CUDA(cudaEventCreateWithFlags(&ev_fcd_, cudaEventDisableTiming));
+  HP_CUDA(cudaEventCreateWithFlags(&ev_fcw_, cudaEventDisableTiming));
   for (auto& ps : pref_) {
     HP_CUDA(cudaEventCreateWithFlags(&ps.ready, cudaEventDisableTiming));
     HP_CUDA(cudaEventCreateWithFlags(&ps.used, cudaEventDisableTiming));
@@ -661,6 +669,7 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   use_shift = shift;
   ws_ = ws_floats_ > 0 ? arena_.make<float>(static_cast<long long>(ws_floats_)) : nullptr;
   ws2_ = ws2_floats_ > 0 ? arena_.make<float>(static_cast<long long>(ws2_floats_)) : nullptr;
+  ws3_ = ws3_floats_ > 0 ? arena_.make<float>(static_cast<long long>(ws3_floats_)) : nullptr;
   for (auto& w : w_) build_plans(w);
   init_params();
   sent.assign(K_, {0, 0, 0, 0});
@@ -685,6 +694,12 @@ ClusterImpl<TA>::~ClusterImpl() {
     cudaStreamSynchronize(sw_);
     cudaStreamDestroy(sw_);
   }
+  if (sf_) {
+    cudaStreamSynchronize(sf_);
+    cudaStreamDestroy(sf_);
+  }
+  if (ev_fcd_) cudaEventDestroy(ev_fcd_);
+  if (ev_fcw_) cudaEventDestroy(ev_fcw_);
   if (ev_comm_) cudaEventDestroy(ev_comm_);
   if (ev0_fc_) cudaEventDestroy(ev0_fc_);
   if (sc_) cudaStreamDestroy(sc_);
@@ -739,13 +754,13 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     return o;
   };
   auto plan = [&](const GemmOperand& a, const GemmOperand& b, long long M, long long N, long long K,
-                  const Epi& e, bool side = false) {
+                  const Epi& e, int side = 0) {
     // The plan picks its own tile and split-K; the first (sizing) pass runs
     // against a placeholder workspace and records the largest need. Side-stream
     // (wgrad) plans get their own workspace: they run concurrently with the
     // compute stream's GEMMs.
-    float* real = side ? ws2_ : ws_;
-    size_t& need = side ? ws2_floats_ : ws_floats_;
+    float* real = side == 1 ? ws2_ : side == 2 ? ws3_ : ws_;
+    size_t& need = side == 1 ? ws2_floats_ : side == 2 ? ws3_floats_ : ws_floats_;
     float* ws = real != nullptr ? real : reinterpret_cast<float*>(256);
     GemmPlan pl = gemm_plan(math_, a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e, 0,
                             ws, 0);
@@ -849,11 +864,11 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     }
     if (swap) {
       eg.c_trans = 1;  // element (m = k, n = f) -> dW[f][k]
-      w.conv_wgrad.push_back(plan(xb, op(w.dz[l], 1, c.F), Kw, c.F, c.s2d ? c.P : c.Pq, eg, true));
+      w.conv_wgrad.push_back(plan(xb, op(w.dz[l], 1, c.F), Kw, c.F, c.s2d ? c.P : c.Pq, eg, 1));
     } else if (c.s2d) {
-      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, Kz, c.P, eg, true));
+      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, Kz, c.P, eg, 1));
     } else {
-      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, c.Kc, c.Pq, eg, true));
+      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, c.Kc, c.Pq, eg, 1));
     }
     if (l == 0) {
       w.conv_dgrad.push_back(GemmPlan{});
@@ -930,7 +945,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     eg.c = w.fgr + fc_w_off(l);
     eg.ldc = f.Ip;
     const GemmOperand xw = l == 0 ? op(w.xb, 1, g_.A) : op(w.fx[l], 0, ldn_);
-    w.fc_wgrad.push_back(plan(op(w.fdz[l], 0, ldn_), xw, rows, f.Ip, n_, eg));
+    w.fc_wgrad.push_back(plan(op(w.fdz[l], 0, ldn_), xw, rows, f.Ip, n_, eg, 2));
     // dgrad
     if (l > 0) {
       Epi ed;
@@ -1213,8 +1228,16 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
       // update of the wgrad epilogue -- turn j's dX uses pre-update weights
       // (cluster.cpp:562-601)
       gemm(w.fc_dgrad[li], "fc_dgrad", li);
-      gemm(pw, "fc_wgrad", li);
-      launch_rowsum<TA>(w.fdz[li], rows, static_cast<int>(n_), ldn_, w.fgr + fc_b_off(li), beta ? 1 : 0, st_);
+      // The weight gradient (and the fused update) feeds nothing downstream in
+      // this step: it runs on sf_, overlapping the rest of the backward
+      // (serialised when profiling).
+      cudaStream_t fs = profile ? st_ : sf_;
+      if (fs != st_) {
+        HP_CUDA(cudaEventRecord(ev_fcd_, st_));
+        HP_CUDA(cudaStreamWaitEvent(fs, ev_fcd_, 0));
+      }
+      gemm(pw, "fc_wgrad", li, fs);
+      launch_rowsum<TA>(w.fdz[li], rows, static_cast<int>(n_), ldn_, w.fgr + fc_b_off(li), beta ? 1 : 0, fs);
       ++launches_;
     }
     if (li > 0 && fcK_ > 1) {
@@ -1228,6 +1251,7 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
       launches_ += nl;
     }
   }
+  HP_CUDA(cudaEventRecord(ev_fcw_, profile ? st_ : sf_));
 }
 
 // return_gradients (cluster.cpp:196-269): each boundary-gradient row goes
@@ -1417,6 +1441,9 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
   }
   for (auto& w : w_) conv_forward(w);
   for (int j = 0; j < num_sub_; ++j) {
+    // turn j overwrites the FC activations / gradients the previous turn's
+    // wgrads (sf_) read
+    if (j > 0) HP_CUDA(cudaStreamWaitEvent(st_, ev_fcw_, 0));
     route_forward(j);
     // Fused FC weight update in the wgrad epilogue: every turn in variable
     // mode (cluster.cpp:586-601), the last turn of the accumulation in exact
@@ -1429,12 +1456,14 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
     fc_forward_backward(j, !variable_ && j > 0);
     return_gradients(j);
     weights_fused_ = fuse_sgd_;
-    if (variable_) sgd_fc(fc_lr, 1.f, false, hp);  // per-sub-batch update (cluster.cpp:586-601)
+    if (variable_) {  // per-sub-batch update (cluster.cpp:586-601)
+      HP_CUDA(cudaStreamWaitEvent(st_, ev_fcw_, 0));
+      sgd_fc(fc_lr, 1.f, false, hp);
+    }
   }
   fuse_sgd_ = false;
   if (dp_ && K_ > 1) {  // pure DP: the FC gradients are all-reduced first (overlapping the conv backward)
-    HP_CUDA(cudaEventRecord(ev0_fc_, st_));
-    HP_CUDA(cudaStreamWaitEvent(sc_, ev0_fc_, 0));
+    HP_CUDA(cudaStreamWaitEvent(sc_, ev_fcw_, 0));
     std::vector<float*> bufs(nl);
     for (int i = 0; i < nl; ++i) bufs[i] = w_[i].fgr;
     comm_->allreduce_f32(bufs, static_cast<size_t>(fc_total_), sc_);
@@ -1459,6 +1488,7 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
     }
   }
   HP_CUDA(cudaStreamWaitEvent(st_, ev_wg_[0], 0));  // join sw_ (layer 0 is its last work)
+  HP_CUDA(cudaStreamWaitEvent(st_, ev_fcw_, 0));    // join sf_
   if (K_ > 1) {
     HP_CUDA(cudaEventRecord(ev_comm_, sc_));
     HP_CUDA(cudaStreamWaitEvent(st_, ev_comm_, 0));
