@@ -216,6 +216,15 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
       : "memory");
 }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialization may start (prologue: barriers, TMEM, descriptor prefetch)
+// while its predecessor drains; pdl_wait() blocks until the predecessor grid
+// has completed and its memory is visible -- call it before the first global
+// access. pdl_trigger(): this CTA no longer holds back the next kernel's launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- tcgen05
 // One lane of a fully converged warp (the same lane every call): lets the MMA
 // warp run its loop warp-uniformly, so descriptors live in uniform registers,
