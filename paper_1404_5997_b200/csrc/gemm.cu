@@ -1734,17 +1734,21 @@ GemmPlan conv_shift_plan(const void* x, long long rows, int C, int R, int S, int
   p.math = kMathBF16;
   p.shift = true;
   p.cta2 = true;
-  // N tile: widest of 256/192/128/64 with the least padding
+  // N tile: minimise rounds of pair tiles on the 74 pairs x the tile's cost
+  // (MMA time ~ BN plus a fixed per-tap share), preferring wider tiles on ties
+  static const int force_bn = getenv("HP_DEV_SHIFT_BN") ? atoi(getenv("HP_DEV_SHIFT_BN")) : 0;
   int best = 256;
-  double best_fill = -1.0;
+  double best_cost = 1e30;
+  const long long mt = (rows + 2 * kBM - 1) / (2 * kBM);
   for (int bn : {256, 192, 128, 64}) {
-    const int nt = cdiv(N, bn);
-    const double fill = static_cast<double>(N) / (static_cast<double>(nt) * bn);
-    if (fill > best_fill + 1e-9) {
-      best_fill = fill;
+    const long long tiles = mt * cdiv(N, bn);
+    const double cost = static_cast<double>((tiles + 73) / 74) * (bn + 64);
+    if (cost < best_cost * 0.97) {
+      best_cost = cost;
       best = bn;
     }
   }
+  if (force_bn) best = force_bn;
   p.bn = best;
   p.splits = 1;
   const int halo = 128 + (R - 1) * wq + (S - 1);
