@@ -54,6 +54,18 @@ bool out_dim(long long in, int k, int s, int p, bool floor_mode, long long* out)
 
 std::string num(long long v) { return std::to_string(v); }
 
+// logistic_xent's DomainError (tensor.cpp:600-603) on host targets: a
+// branch-free (vectorisable) scan first, the exact message only on failure.
+void check_targets(const float* t, long long n) {
+  int bad = 0;
+  for (long long e = 0; e < n; ++e) bad |= static_cast<int>(t[e] < 0.f) | static_cast<int>(t[e] > 1.f);
+  if (!bad) return;
+  for (long long e = 0; e < n; ++e)
+    if (t[e] < 0.f || t[e] > 1.f)
+      domain_error("logistic_xent: target " + std::to_string(static_cast<double>(t[e])) +
+                   " outside [0,1] at flat index " + num(e));
+}
+
 }  // namespace
 
 Geometry make_geometry(const hp_model_spec* s, int K, long long b) {
@@ -1569,12 +1581,7 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
       bool same = true;
       for (int i = 0; i < nl && same; ++i) same = ps.x[i] == batches[i] && ps.t[i] == targets[i];
       if (!same) continue;
-      for (int i = 0; i < nl; ++i)
-        for (long long e = 0; e < b_ * L_; ++e) {
-          const double t = targets[i][e];
-          if (t < 0.0 || t > 1.0)
-            domain_error("logistic_xent: target " + std::to_string(t) + " outside [0,1] at flat index " + num(e));
-        }
+      for (int i = 0; i < nl; ++i) check_targets(targets[i], b_ * L_);
       const int slot = static_cast<int>(&ps - pref_);
       std::vector<const float*> xb(nl), tb(nl);
       for (int i = 0; i < nl; ++i) {
@@ -1595,13 +1602,7 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
       usage_error("run_step: expected " + num(nl) + " batches and targets, got a null entry");
   if (mem_kind == HP_MEM_HOST) {
     // logistic_xent's DomainError (tensor.cpp:600-603), checked before any state change
-    for (int i = 0; i < nl; ++i)
-      for (long long e = 0; e < b_ * L_; ++e) {
-        const double t = targets[i][e];
-        if (t < 0.0 || t > 1.0)
-          domain_error("logistic_xent: target " + std::to_string(t) + " outside [0,1] at flat index " +
-                       num(e % (b_ * L_)));
-      }
+    for (int i = 0; i < nl; ++i) check_targets(targets[i], b_ * L_);
   }
 
   // CUDA graph of the whole step, keyed by everything baked into it (input
