@@ -25,12 +25,19 @@ failure. `HPSIM_OUTPUT_DIR` overrides output_dir. Config: JSON, one file:
    "data": {"seed_data": 100, "seed_label": 200},
    "steps": 5, "output_dir": "out"}
 
-cost-report / scale-hparams (SPEC cost_model / hparam_scaling) are host math
-outside the hot path and are not provided here.
+  python -m paper_1404_5997_b200.cli cost-report --config run.json [--json]
+      analytical step model (cost_model.py): per-phase table,
+      timeline CSV (<output_dir>/timeline.csv: worker,t0,t1,kind,label) and the
+      speedup summary vs K=1. Config "cost": {"machine": "b200"|"paper",
+      "measured_step_ms": <1-GPU step to calibrate compute to, or null>, plus any
+      CostParams field to override}.
+  python -m paper_1404_5997_b200.cli scale-hparams --eps 0.01 --omega 0.0005 --k 8
+      [--rule theory_sqrt|heuristic_linear] [--json].
 """
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import csv
 import json
 import os
@@ -63,7 +70,8 @@ def default_config() -> Dict[str, Any]:
                         "math_mode": "bf16"},
             "hyper": {"momentum": 0.9, "lr": 0.01, "weight_decay": 0.0005, "fc_partial_lr": None},
             "data": {"seed_data": 100, "seed_label": 200},
-            "steps": 5, "output_dir": "out"}
+            "steps": 5, "output_dir": "out",
+            "cost": {"machine": "b200", "measured_step_ms": None}}
 
 
 def load_config(path: str) -> Dict[str, Any]:
@@ -73,6 +81,11 @@ def load_config(path: str) -> Dict[str, Any]:
     except (OSError, json.JSONDecodeError) as e:
         raise ValidationError(f"config: cannot read {path}: {e}") from e
     return normalize_config(raw)
+
+
+def _cost_fields():
+    from .cost_model import CostParams
+    return {f.name for f in dataclasses.fields(CostParams)}
 
 
 def normalize_config(raw: Dict[str, Any]) -> Dict[str, Any]:
@@ -85,7 +98,7 @@ def normalize_config(raw: Dict[str, Any]) -> Dict[str, Any]:
         raise ValidationError(f"config: unknown field(s) {sorted(unknown)}")
     for k, v in raw.items():
         if isinstance(cfg[k], dict) and isinstance(v, dict):
-            extra = set(v) - set(cfg[k])
+            extra = set(v) - set(cfg[k]) - (_cost_fields() if k == "cost" else set())
             if extra:
                 raise ValidationError(f"config.{k}: unknown field(s) {sorted(extra)}")
             cfg[k].update(v)
@@ -146,6 +159,25 @@ def validate(cfg) -> None:
         raise ValidationError(str(e)) from e
     except HpsimError as e:
         raise ValidationError(str(e)) from e
+
+
+def cost_params(cfg):
+    from . import cost_model as cm
+    c = dict(cfg.get("cost") or {})
+    machine = str(c.pop("machine", "b200")).lower()
+    c.pop("measured_step_ms", None)
+    K = cfg["cluster"]["workers"]
+    if machine == "paper":
+        params, topo = cm.PAPER, cm.paper_topology(K)
+    elif machine == "b200":
+        params, topo = cm.b200_params(), cm.b200_topology(K)
+    else:
+        raise ValidationError(f"config.cost.machine: expected b200|paper, got {machine!r}")
+    try:
+        params = dataclasses.replace(params, **c)
+    except (TypeError, ValueError) as e:
+        raise ValidationError(f"config.cost: {e}") from e
+    return params, topo
 
 
 # ---------------------------------------------------------------- checkpoint
@@ -299,10 +331,65 @@ def cmd_verify_equivalence(cfg, tol: float = 2e-5, skip_broadcast: bool = False,
     return EXIT_OK
 
 
+def cmd_cost_report(cfg, as_json: bool = False, out=None) -> int:
+    """per-phase table + timeline CSV + speedup summary."""
+    from . import cost_model as cm
+    out = out or sys.stdout
+    validate(cfg)
+    spec, cl = model_spec(cfg), cluster_config(cfg)
+    params, topo = cost_params(cfg)
+    meas = (cfg.get("cost") or {}).get("measured_step_ms")
+    scale = cm.calibrate(spec, cl.per_worker_batch, params, meas * 1e-3) if meas else 1.0
+    r = cm.speedup(spec, cl, topo, params, compute_scale=scale)
+    tl = r.pop("timeline")
+    odir = os.environ.get("HPSIM_OUTPUT_DIR", cfg["output_dir"])
+    os.makedirs(odir, exist_ok=True)
+    with open(os.path.join(odir, "timeline.csv"), "w") as fh:
+        fh.write(tl.csv())
+    summary = {"workers": cl.workers, "per_worker_batch": cl.per_worker_batch, "scheme": cl.scheme.name,
+               "compute_scale": scale, "phases_s": tl.phase_table(), "internal_s": tl.internal_s,
+               "sync_s": tl.sync_s, "sync_exposed_s": tl.sync_exposed_s, **r}
+    if as_json:
+        print(json.dumps(summary, sort_keys=True), file=out)
+        return EXIT_OK
+    print(f"cost-report: K={cl.workers} b={cl.per_worker_batch} scheme={cl.scheme.name} "
+          f"flops/s={params.flops_per_sec:.4g}x{scale:.3f} link={params.link_bandwidth:.4g} B/s", file=out)
+    print(f"{'phase':<12}{'seconds':>14}", file=out)
+    for k, v in tl.phase_table().items():
+        print(f"{k:<12}{v:>14.6e}", file=out)
+    h = r["hidden_comm_fraction"]
+    print(f"step_time_s={r['step_time_K']:.6e} speedup={r['speedup']:.4f} images/s={r['images_per_s']:.1f} "
+          f"hidden_comm_fraction={'n/a' if h is None else f'{h:.6f}'}", file=out)
+    return EXIT_OK
+
+
+def cmd_scale_hparams(eps: float, omega: float, k: float, rule: str, as_json: bool = False, out=None) -> int:
+    from .hparams import make_scale_plan
+    out = out or sys.stdout
+    try:
+        p = make_scale_plan(eps, omega, k, rule)
+    except ValueError as e:
+        raise ValidationError(str(e)) from e
+    d = dataclasses.asdict(p)
+    if as_json:
+        print(json.dumps(d, sort_keys=True), file=out)
+    else:
+        for key in ("k", "rule", "eps", "omega", "eps_new", "omega_exact", "omega_approx", "omega_practical"):
+            v = d[key]
+            print(f"{key:<16}{v:.10g}" if isinstance(v, float) else f"{key:<16}{v}", file=out)
+    return EXIT_OK
+
+
 def main(argv=None) -> int:
     p = argparse.ArgumentParser(prog="python -m paper_1404_5997_b200.cli")
     sub = p.add_subparsers(dest="cmd", required=True)
-    for name in ("train", "verify-equivalence"):
+    sh = sub.add_parser("scale-hparams")
+    sh.add_argument("--eps", type=float, required=True)
+    sh.add_argument("--omega", type=float, required=True)
+    sh.add_argument("--k", type=float, required=True)
+    sh.add_argument("--rule", choices=("theory_sqrt", "heuristic_linear"), default="theory_sqrt")
+    sh.add_argument("--json", action="store_true")
+    for name in ("train", "verify-equivalence", "cost-report"):
         s = sub.add_parser(name)
         s.add_argument("--config", required=True)
         s.add_argument("--seed", type=int, default=None)
@@ -312,11 +399,15 @@ def main(argv=None) -> int:
             s.add_argument("--skip-broadcast", action="store_true")
     a = p.parse_args(argv)
     try:
+        if a.cmd == "scale-hparams":
+            return cmd_scale_hparams(a.eps, a.omega, a.k, a.rule, a.json)
         cfg = load_config(a.config)
         if a.seed is not None:
             cfg["cluster"]["seed"] = a.seed
         if a.cmd == "train":
             return cmd_train(cfg)
+        if a.cmd == "cost-report":
+            return cmd_cost_report(cfg, a.json)
         return cmd_verify_equivalence(cfg, tol=a.tol, skip_broadcast=a.skip_broadcast)
     except ValidationError as e:
         print(f"error: {e}", file=sys.stderr)
