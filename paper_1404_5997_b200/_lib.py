@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhpsim_b200.so")
+LIB_PATH = os.environ.get("HP_DEV_LIB") or os.path.join(_HERE, "lib", "libhpsim_b200.so")  # HP_DEV_LIB: dev variant builds
 
 
 class HpConvLayer(C.Structure):

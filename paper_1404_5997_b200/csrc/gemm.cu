@@ -29,9 +29,12 @@ constexpr uint32_t kEpiSmemBytes = 4u * 32u * 36u * 4u;  // staged epilogue tile
 __host__ __device__ constexpr uint32_t stage_bytes(int bn, int math) {
   return (kBM * 128u + static_cast<uint32_t>(bn) * 128u) * (math == kMathF32x3 ? 2u : 1u);
 }
+#ifndef HP_GEMM_CAP
+#define HP_GEMM_CAP 6
+#endif
 __host__ __device__ constexpr int num_stages(int bn, int math) {
-  return static_cast<int>((kMaxDynSmem - 2048u - kEpiSmemBytes) / stage_bytes(bn, math)) > 6
-             ? 6
+  return static_cast<int>((kMaxDynSmem - 2048u - kEpiSmemBytes) / stage_bytes(bn, math)) > HP_GEMM_CAP
+             ? HP_GEMM_CAP
              : static_cast<int>((kMaxDynSmem - 2048u - kEpiSmemBytes) / stage_bytes(bn, math));
 }
 // TMEM columns of one accumulator (power of two >= 32); two are allocated.
@@ -814,9 +817,12 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
 __host__ __device__ constexpr uint32_t stage_bytes2(int bn) {
   return kBM * 128u + static_cast<uint32_t>(bn / 2) * 128u;
 }
+#ifndef HP_GEMM2_CAP
+#define HP_GEMM2_CAP 8
+#endif
 __host__ __device__ constexpr int num_stages2(int bn) {
-  return static_cast<int>((kMaxDynSmem - 2048u - kEpiSmemBytes) / stage_bytes2(bn)) > 8
-             ? 8
+  return static_cast<int>((kMaxDynSmem - 2048u - kEpiSmemBytes) / stage_bytes2(bn)) > HP_GEMM2_CAP
+             ? HP_GEMM2_CAP
              : static_cast<int>((kMaxDynSmem - 2048u - kEpiSmemBytes) / stage_bytes2(bn));
 }
 
@@ -1030,11 +1036,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 // own 128 rows + halo), one weight-tile TMA per (tap, cb), 4 MMAs per tap whose
 // A descriptor starts (r*wq + s) rows into the halo.
 constexpr uint32_t kHaloBytes = 256u * 128u;
+#ifndef HP_SHIFT_CAP
+#define HP_SHIFT_CAP 12
+#endif
 __host__ __device__ constexpr uint32_t shift_b_bytes(int bn) { return static_cast<uint32_t>(bn / 2) * 128u; }
 __host__ __device__ constexpr int shift_stages(int bn) {
-  return static_cast<int>((kMaxDynSmem - 2304u - kEpiSmemBytes - 2u * kHaloBytes) / shift_b_bytes(bn)) > 12
-             ? 12
+  return static_cast<int>((kMaxDynSmem - 2304u - kEpiSmemBytes - 2u * kHaloBytes) / shift_b_bytes(bn)) > HP_SHIFT_CAP
+             ? HP_SHIFT_CAP
              : static_cast<int>((kMaxDynSmem - 2304u - kEpiSmemBytes - 2u * kHaloBytes) / shift_b_bytes(bn));
+}
+// barrier words (full/empty per stage + 8) and the TMEM slot, rounded to 128 B
+__host__ __device__ constexpr uint32_t shift_bar_bytes(int bn) {
+  return ((static_cast<uint32_t>(2 * shift_stages(bn) + 8) * 8u + 4u) + 127u) & ~127u;
 }
 
 template <int BN>
@@ -1059,7 +1072,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   uint64_t* tfull = hempty + 2;      // [2]
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* stg_base = reinterpret_cast<float*>(bst + STAGES * B_BYTES + 512);  // barriers: < 512 B
+  float* stg_base = reinterpret_cast<float*>(bst + STAGES * B_BYTES + shift_bar_bytes(BN));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -1769,8 +1782,8 @@ GemmPlan conv_shift_plan(const void* x, long long rows, int C, int R, int S, int
   p.tb = make_map(w, 2, static_cast<long long>(R) * S * C, N, ldw, 64, p.bn / 2, CU_TENSOR_MAP_SWIZZLE_128B);
   const int total = cdiv(rows, 2 * kBM) * cdiv(N, p.bn);
   p.grid = dim3(2 * std::min(total, 74));
-  p.smem = 2 * kHaloBytes + static_cast<size_t>(shift_stages(p.bn)) * shift_b_bytes(p.bn) + 1024 + 512 +
-           kEpiSmemBytes;
+  p.smem = 2 * kHaloBytes + static_cast<size_t>(shift_stages(p.bn)) * shift_b_bytes(p.bn) + 1024 +
+           shift_bar_bytes(p.bn) + kEpiSmemBytes;
   p.valid = true;
   return p;
 }

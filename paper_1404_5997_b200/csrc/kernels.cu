@@ -6,6 +6,7 @@
 
 #include "errors.hpp"
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace hp {
 
@@ -282,12 +283,23 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const T* __restrict
   const long long r1 = min(M, r0 + rows_per);
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (c0 < N) {
-    for (long long r = r0 + ty; r < r1; r += TY) {
-      float v[8];
-      ld4<T>(x + r * ldx + c0, v);
-      ld4<T>(x + r * ldx + c0 + 4, v + 4);
+    for (long long r = r0 + ty; r < r1; r += 4 * TY) {
+      float v[4][8];  // four rows' loads in flight, added in row order
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] += v[j];
+      for (int u = 0; u < 4; ++u) {
+        const long long ru = r + u * TY;
+        if (ru < r1) {
+          ld4<T>(x + ru * ldx + c0, v[u]);
+          ld4<T>(x + ru * ldx + c0 + 4, v[u] + 4);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[u][j] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += v[u][j];
     }
   }
   const int t = ty * TX + tx;
@@ -309,8 +321,13 @@ __global__ void colsum_final_kernel(const float* __restrict__ ws, int G, int N,
   const int col = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (col >= N) return;
-  float s = 0.f;
-  for (int g = lane; g < G; g += 32) s += ws[static_cast<long long>(g) * N + col];
+  float p[4] = {0.f, 0.f, 0.f, 0.f};  // four independent chains, fixed order
+  for (int g = lane; g < G; g += 128) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (g + 32 * u < G) p[u] += ws[static_cast<long long>(g + 32 * u) * N + col];
+  }
+  float s = (p[0] + p[1]) + (p[2] + p[3]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) out[col] = s;
@@ -666,8 +683,21 @@ __global__ void __launch_bounds__(1024) lrn_pool_fwd_kernel(const T* __restrict_
   const int b = blockIdx.y;
   const int ph0 = blockIdx.x * TP, ph1 = min(PH, ph0 + TP);
   const int r0 = ph0 * ps, npx = ((ph1 - 1) * ps + pk - r0) * W;
-  const T* base = a + static_cast<long long>(b * H + r0) * W * C + c0;
-  constexpr int U = 2;  // pixels per pass: their loads are in flight together
+  // the band's conv-output rows are contiguous in HBM: one bulk copy into smem
+  // (all of it in flight at once), then the LRN reads smem
+  T* raw = reinterpret_cast<T*>(L + static_cast<long long>((TP - 1) * ps + pk) * W * C);
+  __shared__ __align__(8) uint64_t band_bar;
+  if (g == 0 && ty == 0) {
+    mbar_init(&band_bar, 1);
+    fence_barrier_init();
+    const uint32_t bytes = static_cast<uint32_t>(npx) * C * sizeof(T);
+    mbar_arrive_expect_tx(&band_bar, bytes);
+    bulk_load(raw, a + static_cast<long long>(b * H + r0) * W * C, bytes, &band_bar);
+  }
+  __syncthreads();
+  mbar_wait(&band_bar, 0);
+  const T* base = raw + c0;
+  constexpr int U = 2;  // pixels per pass
   for (int p0 = ty; p0 < npx; p0 += U * NY) {
     float v[U][V + 8];  // channels [c0-4, c0+V+4)
 #pragma unroll
@@ -779,6 +809,39 @@ __global__ void __launch_bounds__(512) lrn_pool_bwd_kernel(
   ldv<TA>(a + px, av);
 #pragma unroll
   for (int j = 0; j < V; ++j) gb[j] = 0.f;
+  constexpr int MW = PK ? (PK + PS - 1) / PS : 0;  // pooled windows covering a pixel, per dim
+  if constexpr (MW > 0) {
+    // fixed-trip gather: every window's argmax word and gradient load in flight together
+    uint32_t wi[MW][MW][V / 4];
+    float4 gv[MW][MW][V / 4];
+#pragma unroll
+    for (int i = 0; i < MW; ++i)
+#pragma unroll
+      for (int k = 0; k < MW; ++k) {
+        const bool ok = oh0 + i <= oh1 && ow0 + k <= ow1;
+        const int o = ((b * PH + (ok ? oh0 + i : 0)) * PW + (ok ? ow0 + k : 0)) * C + c0;
+#pragma unroll
+        for (int j = 0; j < V / 4; ++j) {
+          wi[i][k][j] = ok ? *reinterpret_cast<const uint32_t*>(widx + o + 4 * j) : 0xffffffffu;
+          gv[i][k][j] = ok ? *reinterpret_cast<const float4*>(gy + o + 4 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+    for (int i = 0; i < MW; ++i)
+#pragma unroll
+      for (int k = 0; k < MW; ++k) {
+        const uint32_t me = static_cast<uint32_t>((h - (oh0 + i) * ps) * pk + (w - (ow0 + k) * ps));
+#pragma unroll
+        for (int j = 0; j < V / 4; ++j) {
+          const uint32_t x = wi[i][k][j];
+          const float4 g4 = gv[i][k][j];
+          if ((x & 0xff) == me) gb[4 * j] += g4.x;
+          if (((x >> 8) & 0xff) == me) gb[4 * j + 1] += g4.y;
+          if (((x >> 16) & 0xff) == me) gb[4 * j + 2] += g4.z;
+          if ((x >> 24) == me) gb[4 * j + 3] += g4.w;
+        }
+      }
+  } else
   for (int oh = oh0; oh <= oh1; ++oh)
     for (int ow = ow0; ow <= ow1; ++ow) {
       const int o = ((b * PH + oh) * PW + ow) * C + c0;
@@ -876,7 +939,8 @@ __global__ void __launch_bounds__(256) rotate_weights_kernel(const float* __rest
 
 // Space-to-depth (see kernels.cuh): block = one z row (b, i). Phase 1 stages
 // the C*s input rows it needs (zero where outside the image, x shifted by pad)
-// in smem with coalesced (float4 when W % 4 == 0) loads; phase 2 writes the
+// in smem with coalesced loads (float4, four in flight per thread, when
+// W % 4 == 0); phase 2 writes the
 // Zw x Cz bf16 row, one 8-channel 16-byte vector per thread.
 template <class T>
 __global__ void __launch_bounds__(256) s2d_input_kernel(const float* __restrict__ x, T* __restrict__ z, int C,
@@ -885,19 +949,56 @@ __global__ void __launch_bounds__(256) s2d_input_kernel(const float* __restrict_
   const int b = blockIdx.y, i = blockIdx.x;
   const int SW = s * Zw;
   const int nrows = C * s;
-  for (int rr = threadIdx.y; rr < nrows; rr += blockDim.y) {
-    const int c = rr / s, dr = rr - c * s;
-    const int h = s * i + dr - pad;
-    float* dst = sx + rr * SW;
-    const bool hv = h >= 0 && h < H;
-    const float* src = x + ((static_cast<long long>(b) * C + c) * H + (hv ? h : 0)) * W;
-    for (int q = threadIdx.x; q < SW; q += blockDim.x) {
-      const int w = q - pad;
-      dst[q] = (hv && w >= 0 && w < W) ? __ldg(src + w) : 0.f;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
+  if ((W & 3) == 0 && pad + W <= SW) {
+    // float4 loads, all of a thread's loads in flight before any smem store
+    const int W4 = W >> 2, n4 = nrows * W4;
+    for (int base = tid; base < n4; base += 4 * nt) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = base + u * nt;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (idx < n4) {
+          const int rr = idx / W4, w4 = idx - rr * W4;
+          const int c = rr / s, dr = rr - c * s;
+          const int h = s * i + dr - pad;
+          if (h >= 0 && h < H)
+            v[u] = __ldg(reinterpret_cast<const float4*>(x + ((static_cast<long long>(b) * C + c) * H + h) * W) + w4);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = base + u * nt;
+        if (idx < n4) {
+          const int rr = idx / W4, w4 = idx - rr * W4;
+          float* dst = sx + rr * SW + pad + 4 * w4;
+          dst[0] = v[u].x;
+          dst[1] = v[u].y;
+          dst[2] = v[u].z;
+          dst[3] = v[u].w;
+        }
+      }
+    }
+    const int edge = SW - W;  // pad columns left of and right of the image
+    for (int t = tid; t < nrows * edge; t += nt) {
+      const int rr = t / edge, e = t - rr * edge;
+      sx[rr * SW + (e < pad ? e : W + e)] = 0.f;
+    }
+  } else {
+    for (int rr = threadIdx.y; rr < nrows; rr += blockDim.y) {
+      const int c = rr / s, dr = rr - c * s;
+      const int h = s * i + dr - pad;
+      float* dst = sx + rr * SW;
+      const bool hv = h >= 0 && h < H;
+      const float* src = x + ((static_cast<long long>(b) * C + c) * H + (hv ? h : 0)) * W;
+      for (int q = threadIdx.x; q < SW; q += blockDim.x) {
+        const int w = q - pad;
+        dst[q] = (hv && w >= 0 && w < W) ? __ldg(src + w) : 0.f;
+      }
     }
   }
   __shared__ int choff[256];  // smem offset of channel ch at j = 0 (-1: zero channel)
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
   const int real = s * s * C;
   for (int ch = tid; ch < Cz; ch += nt) {
     int off = -1;
@@ -1020,8 +1121,11 @@ void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, i
   const long long row_bytes = static_cast<long long>(W) * C * sizeof(float);
   int TP = 1;
   while (TP < PH && (static_cast<long long>(TP) * ps + pk) * row_bytes <= 72 * 1024) ++TP;
-  const size_t smem = static_cast<size_t>(((TP - 1) * ps + pk) * row_bytes);
+  // + the raw band (T) the block bulk-loads from HBM
+  const size_t smem = static_cast<size_t>(((TP - 1) * ps + pk) * row_bytes) * (sizeof(float) + sizeof(T)) / sizeof(float);
   if (smem > 220 * 1024) throw std::runtime_error("lrn_pool: conv row too wide for the smem band");
+  if ((static_cast<long long>(W) * C * sizeof(T)) % 16 != 0 || reinterpret_cast<uintptr_t>(a) % 16 != 0)
+    throw std::runtime_error("lrn_pool: conv rows must be 16-byte multiples");
   const int G = C / V;
   const dim3 block(G, std::max(1, 384 / G));
   const dim3 grid((PH + TP - 1) / TP, B);
@@ -1216,16 +1320,18 @@ void launch_lrn_bwd(const TA* a, const float* d, const float* gb, TO* ga, long l
       a, d, gb, ga, C, n / 2, (n - 1) / 2, alpha, beta, relu_mask, total);
 }
 
-size_t colsum_ws_floats(long long M, int N) {
-  const long long G = std::min<long long>(std::max<long long>(1, (M + 255) / 256), 512);
-  return static_cast<size_t>(G) * N;
+// row groups: 256 rows each, at most 512
+static long long colsum_groups(long long M, int) {
+  return std::min<long long>(std::max<long long>(1, (M + 255) / 256), 512);
 }
+
+size_t colsum_ws_floats(long long M, int N) { return static_cast<size_t>(colsum_groups(M, N)) * N; }
 
 template <class T>
 void launch_colsum(const T* x, long long M, int N, long long ldx, float* out, float* ws,
                    cudaStream_t st) {
   if (N % 8 != 0 || ldx % 8 != 0) throw std::runtime_error("colsum: N and ldx must be multiples of 8");
-  const long long G = std::min<long long>(std::max<long long>(1, (M + 255) / 256), 512);
+  const long long G = colsum_groups(M, N);
   const long long rows_per = (M + G - 1) / G;
   const int vec = N / 8;
   const int TX = std::min(vec, 32), TY = 256 / TX;

@@ -98,6 +98,15 @@ __device__ __forceinline__ void tma_load_im2col_4d(void* dst, const CUtensorMap*
 }
 
 // ---------------------------------------------------------------- clusters / CTA pairs
+// Plain (non-tensor) bulk copy global -> own smem, completion on an mbarrier
+// (16-byte aligned addresses, bytes % 16 == 0).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
