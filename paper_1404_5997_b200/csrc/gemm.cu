@@ -99,15 +99,77 @@ __device__ __forceinline__ void epi_elem(const Epi& e, int m, int n, float v) {
   }
 }
 
+// 256-bit global accesses (sm_100): one request per 32 contiguous bytes of a
+// row -- the row-per-thread epilogue's stores touch a different line per lane,
+// so request count, not bytes, is what they cost.
+__device__ __forceinline__ void st256(void* p, const uint32_t (&u)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(u[0]), "r"(u[1]),
+               "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7])
+               : "memory");
+}
+__device__ __forceinline__ void ld256(const void* p, uint32_t (&u)[8]) {
+  asm volatile("ld.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7])
+               : "l"(p));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// The row-per-thread vector path applies (32 contiguous outputs of one row).
+__device__ __forceinline__ bool epi_row_vec(const GemmArgs& a, int n0) {
+  const Epi& e = a.epi;
+  return !e.c_trans && n0 + 32 <= a.N && (e.c_type == kF32 ? (e.ldc & 3) == 0 : (e.ldc & 7) == 0) &&
+         (!e.sgd_w || ((e.ldc & 7) == 0 && e.c_type == kF32)) && (!e.beta || e.c_type == kF32) &&
+         (!e.mask ||
+          (e.mask_trans == 0 && (e.mask_type == kF32 ? (e.ldmask & 3) == 0 : (e.ldmask & 7) == 0)));
+}
+
+// bf16 ReLU-mask words of one row's 32 columns, loaded a chunk ahead so the
+// load latency hides behind the previous chunk's epilogue.
+struct MaskPre {
+  uint4 v[4];
+  bool ok = false;
+};
+__device__ __forceinline__ void epi_mask_load(const GemmArgs& a, int mo, int n0, MaskPre& p) {
+  p.ok = false;
+  const Epi& e = a.epi;
+  if (!e.mask || e.mask_type != kBF16 || a.raw_partial || mo < 0 || (a.dbg & 16) || !epi_row_vec(a, n0)) return;
+  const __nv_bfloat16* mp = reinterpret_cast<const __nv_bfloat16*>(e.mask) + static_cast<long long>(mo) * e.ldmask + n0;
+  if ((reinterpret_cast<uintptr_t>(mp) & 31) == 0) {
+    uint32_t u[8];
+    ld256(mp, u);
+    p.v[0] = make_uint4(u[0], u[1], u[2], u[3]);
+    p.v[1] = make_uint4(u[4], u[5], u[6], u[7]);
+    ld256(mp + 16, u);
+    p.v[2] = make_uint4(u[0], u[1], u[2], u[3]);
+    p.v[3] = make_uint4(u[4], u[5], u[6], u[7]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) p.v[i] = reinterpret_cast<const uint4*>(mp)[i];
+  }
+  p.ok = true;
+}
+
 // Epilogue for 32 consecutive columns [n0, n0+32) of row m.
 // mo: the output row of GEMM row m under the epilogue RowMap (-1: dropped).
 __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int split,
-                                          const float (&v)[32], int mo) {
+                                          const float (&v)[32], int mo, const float* sbias = nullptr,
+                                          const MaskPre* mpre = nullptr) {
   if (m >= a.M) return;
   if (a.raw_partial) {
     float* dst = a.ws + static_cast<long long>(split) * a.M * a.N +
                  static_cast<long long>(m) * a.N;
-    if (n0 + 32 <= a.N && (a.N & 3) == 0) {
+    if (n0 + 32 <= a.N && (reinterpret_cast<uintptr_t>(dst + n0) & 31) == 0) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint32_t u[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) u[j] = __float_as_uint(v[i + j]);
+        st256(dst + n0 + i, u);
+      }
+    } else if (n0 + 32 <= a.N && (a.N & 3) == 0) {
 #pragma unroll
       for (int i = 0; i < 32; i += 4)
         *reinterpret_cast<float4*>(dst + n0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
@@ -121,12 +183,7 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
   const Epi& e = a.epi;
   // Vector path: 32 contiguous outputs of row m (bias/ReLU/alpha/beta/mask fused).
   if (mo < 0) return;
-  const bool vec = !e.c_trans && n0 + 32 <= a.N &&
-                   (e.c_type == kF32 ? (e.ldc & 3) == 0 : (e.ldc & 7) == 0) &&
-                   (!e.sgd_w || ((e.ldc & 7) == 0 && e.c_type == kF32)) &&
-                   (!e.beta || e.c_type == kF32) &&
-                   (!e.mask || (e.mask_trans == 0 && (e.mask_type == kF32 ? (e.ldmask & 3) == 0
-                                                                             : (e.ldmask & 7) == 0)));
+  const bool vec = epi_row_vec(a, n0);
   if (vec) {
     float x[32];
     const float bm = e.bias_mode == 1 ? e.bias[m] : 0.f;
@@ -182,8 +239,8 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
     if (e.bias_mode == 1) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) x[i] += bm;
-    } else if (e.bias_mode == 2) {
-      const float4* bb = reinterpret_cast<const float4*>(e.bias + n0);
+    } else if (e.bias_mode == 2 && !(a.dbg & 4)) {  // dbg 4: skip the bias loads (dev)
+      const float4* bb = reinterpret_cast<const float4*>((sbias ? sbias : e.bias) + n0);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const float4 o = bb[i];
@@ -197,13 +254,13 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
 #pragma unroll
       for (int i = 0; i < 32; ++i) x[i] = x[i] > 0.f ? x[i] : 0.f;
     }
-    if (e.mask) {
+    if (e.mask && !(a.dbg & 16)) {  // dbg 16: skip the mask loads (dev)
       const long long mko = static_cast<long long>(mo) * e.ldmask + n0;
       if (e.mask_type == kBF16) {
         const uint4* mp = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(e.mask) + mko);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          uint4 u = mp[i];
+          uint4 u = (mpre && mpre->ok) ? mpre->v[i] : mp[i];
           const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
@@ -221,18 +278,45 @@ __device__ __forceinline__ void epi_row32(const GemmArgs& a, int m, int n0, int 
         }
       }
     }
-    if (e.c_type == kF32) {
-      float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.c) + off);
+    if (a.dbg & 8) {  // dev: skip the stores (keep the values live)
+      float acc = 0.f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) dst[i] = make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
+      for (int i = 0; i < 32; ++i) acc += x[i];
+      if (acc == 12345.678f) reinterpret_cast<float*>(e.c)[off] = acc;
+    } else if (e.c_type == kF32) {
+      float* dst = reinterpret_cast<float*>(e.c) + off;
+      if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint32_t u[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) u[j] = __float_as_uint(x[i + j]);
+          st256(dst + i, u);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          reinterpret_cast<float4*>(dst)[i] = make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
+      }
     } else {
-      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.c) + off);
+      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(e.c) + off;
+      if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        __align__(16) __nv_bfloat16 t[8];
+        for (int i = 0; i < 32; i += 16) {
+          uint32_t u[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) t[j] = __float2bfloat16_rn(x[8 * i + j]);
-        dst[i] = *reinterpret_cast<const uint4*>(t);
+          for (int j = 0; j < 8; ++j) u[j] = pack_bf16x2(x[i + 2 * j], x[i + 2 * j + 1]);
+          st256(dst + i, u);
+        }
+      } else {
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          __align__(16) __nv_bfloat16 t[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) t[j] = __float2bfloat16_rn(x[8 * i + j]);
+          d4[i] = *reinterpret_cast<const uint4*>(t);
+        }
       }
     }
     return;
@@ -305,6 +389,19 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
   return v;
 }
 
+// Direct (row-per-thread) epilogues with per-column bias read it from smem:
+// every lane needs the same 32 values per chunk, and a global load there is a
+// full L2 round trip on the epilogue's critical path (measured: ~1/8 of conv
+// fprop time). The epilogue warps (threads 64..191) copy bias[0, N) into the
+// staging area the direct path does not use; returns it, or nullptr.
+__device__ __forceinline__ const float* epi_stage_bias(const GemmArgs& a, float* base) {
+  const bool direct = !(a.dbg & 2) && !a.raw_partial && !a.epi.beta && !a.epi.sgd_w;
+  if (!direct || a.epi.bias_mode != 2 || a.epi.c_trans || a.N > static_cast<int>(kEpiSmemBytes / 4)) return nullptr;
+  for (int i = static_cast<int>(threadIdx.x) - 64; i < a.N; i += 128) base[i] = a.epi.bias[i];
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  return base;
+}
+
 // Output rows of the 8 GEMM rows m0 + 4i + (lane >> 3) a thread stores in
 // epi_chunk (-1: past M or dropped by the RowMap). Depends only on the tile
 // and the thread, so the kernels compute it once per tile.
@@ -322,7 +419,8 @@ __device__ __forceinline__ void epi_rows(const GemmArgs& a, int m0, int (&mrow)[
 // Epilogue of one warp's 32 rows [m0, m0+32) x 32 columns [n0, n0+32).
 // All 32 lanes must call it (warp-synchronous); `stg` is the warp's tile.
 __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int split, const float (&v)[32],
-                                          float* stg, const int (&mrow)[8], int mself) {
+                                          float* stg, const int (&mrow)[8], int mself,
+                                          const float* sbias = nullptr, const MaskPre* mpre = nullptr) {
   const int lane = threadIdx.x & 31;
   if (a.dbg & 1) return;  // dev: mainloop-only timing
   // Store-only epilogues (no beta / mask / SGD reads) and transposed outputs
@@ -331,7 +429,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int
   // bandwidth the MMAs need; it pays only when the epilogue also reads HBM).
   const bool direct = !(a.dbg & 2) && (a.raw_partial || (!a.epi.beta && !a.epi.sgd_w));
   if (direct || !epi_vec_ok(a)) {
-    epi_row32(a, m0 + lane, n0, split, v, mself);
+    epi_row32(a, m0 + lane, n0, split, v, mself, sbias, mpre);
     return;
   }
   const uint32_t sbase = smem_u32(stg);
@@ -744,6 +842,7 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
     __syncwarp();
   } else {
     const int q = warp & 3;
+    const float* sbias = epi_stage_bias(args, reinterpret_cast<float*>(smem + STAGES * SB + 256));
     int cstage = 0;
     uint32_t cphase = 0;
     int local = 0;
@@ -785,10 +884,13 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
       const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf) * ACOLS;
       int mrow[8], mself;
       epi_rows(args, ti.m0 + q * 32, mrow, mself);
+      MaskPre mcur, mnext;  // (not in the LIGHT kernel: FC wgrad has no mask, and registers are tight)
+      if (!LIGHT) epi_mask_load(args, mself, ti.n0, mcur);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld32(base + static_cast<uint32_t>(c), r);
+        if (!LIGHT && c + 32 < BN) epi_mask_load(args, mself, ti.n0 + c + 32, mnext);
         tmem_ld_wait();
         if (c + 32 >= BN) {  // accumulator fully in registers: hand it back to the MMA warp
           tc_fence_before();
@@ -797,7 +899,8 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (ti.n0 + c < args.N) epi_chunk(args, ti.m0 + q * 32, ti.n0 + c, ti.split, v, stg, mrow, mself);
+        if (ti.n0 + c < args.N) epi_chunk(args, ti.m0 + q * 32, ti.n0 + c, ti.split, v, stg, mrow, mself, sbias, &mcur);
+        mcur = mnext;
       }
     }
   }
@@ -993,6 +1096,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   } else {
     const int q = warp & 3;
     const uint32_t tempty_leader[2] = {mapa(smem_u32(&tempty[0]), 0), mapa(smem_u32(&tempty[1]), 0)};
+    const float* sbias = epi_stage_bias(args, reinterpret_cast<float*>(smem + STAGES * SB + 256));
     int local = 0;
     for (int t = cid; t < total; t += ncl, ++local) {
       int m0, n0, split, kt0, kt1;
@@ -1005,10 +1109,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf) * ACOLS;
       int mrow[8], mself;
       epi_rows(args, m0 + static_cast<int>(rank) * kBM + q * 32, mrow, mself);
+      MaskPre mcur, mnext;
+      epi_mask_load(args, mself, n0, mcur);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld32(base + static_cast<uint32_t>(c), r);
+        if (c + 32 < BN) epi_mask_load(args, mself, n0 + c + 32, mnext);
         tmem_ld_wait();
         if (c + 32 >= BN) {
           tc_fence_before();
@@ -1017,7 +1124,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (n0 + c < args.N) epi_chunk(args, m0 + static_cast<int>(rank) * kBM + q * 32, n0 + c, split, v, stg, mrow, mself);
+        if (n0 + c < args.N)
+          epi_chunk(args, m0 + static_cast<int>(rank) * kBM + q * 32, n0 + c, split, v, stg, mrow, mself, sbias, &mcur);
+        mcur = mnext;
       }
     }
   }
@@ -1197,6 +1306,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     const int q = warp & 3;
     const uint32_t tempty_leader[2] = {mapa(smem_u32(&tempty[0]), 0), mapa(smem_u32(&tempty[1]), 0)};
     float* stg = stg_base + q * 32 * kEpiLd;
+    const float* sbias = epi_stage_bias(args, stg_base);
     int local = 0;
     for (int t = cid; t < total; t += ncl, ++local) {
       const int mb = t / tiles_n;
@@ -1208,10 +1318,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf) * ACOLS;
       int mrow[8], mself;
       epi_rows(args, m0 + static_cast<int>(rank) * kBM + q * 32, mrow, mself);
+      MaskPre mcur, mnext;
+      epi_mask_load(args, mself, n0, mcur);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld32(base + static_cast<uint32_t>(c), r);
+        if (c + 32 < BN) epi_mask_load(args, mself, n0 + c + 32, mnext);
         tmem_ld_wait();
         if (c + 32 >= BN) {
           tc_fence_before();
@@ -1220,7 +1333,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (n0 + c < args.N) epi_chunk(args, m0 + static_cast<int>(rank) * kBM + q * 32, n0 + c, 0, v, stg, mrow, mself);
+        if (n0 + c < args.N)
+          epi_chunk(args, m0 + static_cast<int>(rank) * kBM + q * 32, n0 + c, 0, v, stg, mrow, mself, sbias, &mcur);
+        mcur = mnext;
       }
     }
   }

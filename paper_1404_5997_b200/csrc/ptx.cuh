@@ -121,8 +121,12 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
+// Default .release.cta semantics: orders this thread's tcgen05.ld (after
+// tcgen05.fence::before_thread_sync) before the arrive without the gpu-scope
+// MEMBAR a .cluster release emits, which would drain every outstanding
+// epilogue global store first (measured: ~1/3 of conv fprop time).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-SM TMA: issued by both CTAs of a pair; bytes complete on the LEADER's
 // barrier (peer bit 24 of the shared::cluster address cleared).
