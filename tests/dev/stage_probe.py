@@ -34,7 +34,7 @@ shapes = {  # name: (H(out), pad, C, R, F)
     "conv4 fwd": (13, 1, 384, 3, 384), "conv5 fwd": (13, 1, 384, 3, 256), "conv5 dgrad": (13, 1, 256, 3, 384)}
 tot = 0.0
 for name, (H, p, Cin, R, F) in shapes.items():
-    wq = H + 2 * p
+    wq = H + p  # q-layout: one shared zero border per row and column
     t, tf = run(b * wq * wq, Cin, R, R, wq, F, b * H * H)
     tot += t
     print(f"{name:12s} {t*1e3:7.1f} us  {tf:6.0f} TF/s (useful)", flush=True)
