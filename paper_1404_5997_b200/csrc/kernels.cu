@@ -1,6 +1,7 @@
 // Memory-bound kernels of the step. See kernels.cuh.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <stdexcept>
 
@@ -306,12 +307,15 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const T* __restrict
 #pragma unroll
   for (int j = 0; j < 8; ++j) red[t][j] = acc[j];
   __syncthreads();
-  if (ty == 0 && c0 < N) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
+  // one thread per output column (TX*8 of them), rows summed in y order: the
+  // same sums as one thread per 8 columns, 8x shorter serial tail
+  if (t < TX * 8) {
+    const int ox = t >> 3, oj = t & 7;
+    const int col = 8 * (blockIdx.x * TX + ox) + oj;
+    if (col < N) {
       float sum = 0.f;
-      for (int y = 0; y < TY; ++y) sum += red[y * TX + tx][j];
-      ws[static_cast<long long>(blockIdx.y) * N + c0 + j] = sum;
+      for (int y = 0; y < TY; ++y) sum += red[y * TX + ox][oj];
+      ws[static_cast<long long>(blockIdx.y) * N + col] = sum;
     }
   }
 }
@@ -911,6 +915,115 @@ __global__ void __launch_bounds__(512) lrn_pool_bwd_kernel(
   if (live) stv<TA>(dz + ((b * ZH + h + zp) * ZW + w + zp) * C + c0, out);
 }
 
+// Backward, flat form (AlexNet 5/3/2 fast path, C/V <= 32 vectors): thread =
+// (conv pixel, channel vector), P = next power of two >= C/V lanes per pixel.
+// The +-2-channel LRN halos of a and t come from the neighbouring lanes by
+// segmented shuffles, so there is no shared memory and no block barrier: every
+// thread issues its activation, argmax and pooled-gradient loads at once.
+// Same arithmetic, in the same order, as lrn_pool_bwd_kernel (bit-identical).
+template <class TA, int P>
+__global__ void __launch_bounds__(256) lrn_pool_bwd_flat_kernel(
+    const float* __restrict__ gy, const uint8_t* __restrict__ widx, const TA* __restrict__ a,
+    TA* __restrict__ dz, int B, int H, int W, int C, float alpha, float beta, float kk, int PH, int PW,
+    int relu_mask, int ZH, int ZW, int zp) {
+  constexpr int V = 16 / sizeof(TA);
+  constexpr int HL = 2, PK = 3, PS = 2, MW = 2;
+  const int G = C / V;
+  const int g = threadIdx.x & (P - 1);
+  const int pix = blockIdx.x * (blockDim.x / P) + threadIdx.x / P;  // B*H*W < 2^31 (launcher)
+  const bool live = g < G && pix < B * H * W;
+  const int bh = live ? pix / W : 0;
+  const int w = live ? pix - bh * W : 0;
+  const int b = bh / H, h = bh - b * H;
+  const int c0 = g * V;
+  float av[V], gb[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    av[j] = 0.f;
+    gb[j] = 0.f;
+  }
+  uint32_t wi[MW][MW][V / 4];
+  float4 gv[MW][MW][V / 4];
+  const int oh0 = h - PK + 1 <= 0 ? 0 : (h - PK + PS) / PS;
+  const int oh1 = min(PH - 1, h / PS);
+  const int ow0 = w - PK + 1 <= 0 ? 0 : (w - PK + PS) / PS;
+  const int ow1 = min(PW - 1, w / PS);
+  if (live) {
+    ldv<TA>(a + ((static_cast<long long>(b) * H + h) * W + w) * C + c0, av);
+#pragma unroll
+    for (int i = 0; i < MW; ++i)
+#pragma unroll
+      for (int k = 0; k < MW; ++k) {
+        const bool ok = oh0 + i <= oh1 && ow0 + k <= ow1;
+        const long long o = ((static_cast<long long>(b) * PH + (ok ? oh0 + i : 0)) * PW + (ok ? ow0 + k : 0)) * C + c0;
+#pragma unroll
+        for (int j = 0; j < V / 4; ++j) {
+          wi[i][k][j] = ok ? *reinterpret_cast<const uint32_t*>(widx + o + 4 * j) : 0xffffffffu;
+          gv[i][k][j] = ok ? *reinterpret_cast<const float4*>(gy + o + 4 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+    for (int i = 0; i < MW; ++i)
+#pragma unroll
+      for (int k = 0; k < MW; ++k) {
+        const uint32_t me = static_cast<uint32_t>((h - (oh0 + i) * PS) * PK + (w - (ow0 + k) * PS));
+#pragma unroll
+        for (int j = 0; j < V / 4; ++j) {
+          const uint32_t x = wi[i][k][j];
+          const float4 g4 = gv[i][k][j];
+          if ((x & 0xff) == me) gb[4 * j] += g4.x;
+          if (((x >> 8) & 0xff) == me) gb[4 * j + 1] += g4.y;
+          if (((x >> 16) & 0xff) == me) gb[4 * j + 2] += g4.z;
+          if ((x >> 24) == me) gb[4 * j + 3] += g4.w;
+        }
+      }
+  }
+  // a over channels [c0-2, c0+V+2): halo from the neighbouring lanes (zero at the channel ends)
+  float win[V + 2 * HL];
+#pragma unroll
+  for (int j = 0; j < V; ++j) win[HL + j] = av[j];
+#pragma unroll
+  for (int d = 0; d < HL; ++d) {
+    const float l = __shfl_up_sync(0xffffffffu, av[V - HL + d], 1, P);
+    const float r = __shfl_down_sync(0xffffffffu, av[d], 1, P);
+    win[d] = g > 0 ? l : 0.f;
+    win[HL + V + d] = g + 1 < G ? r : 0.f;
+  }
+  float gp[V], tv[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    float sum = 0.f;
+#pragma unroll
+    for (int d = -HL; d <= HL; ++d) sum += win[HL + j + d] * win[HL + j + d];
+    const float dd = kk + alpha * sum;
+    const float pn = pow_neg(dd, beta);
+    float rd;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(dd));
+    tv[j] = gb[j] * av[j] * (pn * rd);
+    gp[j] = gb[j] * pn;
+  }
+#pragma unroll
+  for (int j = 0; j < V; ++j) win[HL + j] = tv[j];
+#pragma unroll
+  for (int d = 0; d < HL; ++d) {
+    const float l = __shfl_up_sync(0xffffffffu, tv[V - HL + d], 1, P);
+    const float r = __shfl_down_sync(0xffffffffu, tv[d], 1, P);
+    win[d] = g > 0 ? l : 0.f;
+    win[HL + V + d] = g + 1 < G ? r : 0.f;
+  }
+  float out[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    float acc = 0.f;
+#pragma unroll
+    for (int d = -HL; d <= HL; ++d) acc += win[HL + k + d];
+    float gval = gp[k] - 2.f * alpha * beta * av[k] * acc;
+    if (relu_mask && !(av[k] > 0.f)) gval = 0.f;
+    out[k] = gval;
+  }
+  if (live) stv<TA>(dz + ((static_cast<long long>(b) * ZH + h + zp) * ZW + w + zp) * C + c0, out);
+}
+
 // Rotated operand for the implicit dgrad: wr[c][r][s][f] = w[f][R-1-r][S-1-s][c].
 // 32x32 smem transpose tiles (f x k): reads coalesced along k, writes along f.
 template <class T>
@@ -1164,7 +1277,21 @@ void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* 
     kern<<<grid, block, smem, st>>>(gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW,
                                     relu_mask, zl.H, zl.W, zl.p);
   };
-  if (n == 5 && pk == 3 && ps == 2) {
+  static const bool flat_off = getenv("HP_DEV_LRN_BWD_SMEM") != nullptr;  // dev: the block-per-row kernel
+  // (only when the vectors fill the lane groups: padded lanes measured slower than the smem kernel)
+  if (n == 5 && pk == 3 && ps == 2 && (G == 4 || G == 8 || G == 16 || G == 32) && !flat_off) {
+    const int P = G <= 4 ? 4 : G <= 8 ? 8 : G <= 16 ? 16 : 32;
+    const long long threads = static_cast<long long>(B) * H * W * P;
+    const int blocks = static_cast<int>((threads + 255) / 256);
+    auto fl = [&](auto kern) {
+      kern<<<blocks, 256, 0, st>>>(gy, widx, a, dz, B, H, W, C, alpha, beta, kk, PH, PW, relu_mask, zl.H, zl.W,
+                                   zl.p);
+    };
+    if (P == 4) fl(lrn_pool_bwd_flat_kernel<TA, 4>);
+    else if (P == 8) fl(lrn_pool_bwd_flat_kernel<TA, 8>);
+    else if (P == 16) fl(lrn_pool_bwd_flat_kernel<TA, 16>);
+    else fl(lrn_pool_bwd_flat_kernel<TA, 32>);
+  } else if (n == 5 && pk == 3 && ps == 2) {
     go(lrn_pool_bwd_kernel<TA, 2, 5, 3, 2>);
   } else if (n <= 5) {
     go(lrn_pool_bwd_kernel<TA, 2, 0, 0, 0>);
