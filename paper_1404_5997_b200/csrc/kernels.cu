@@ -572,11 +572,14 @@ constexpr int LH = 4;
 
 // Max-pool forward, window argmax as a 1-byte offset r*k+q: first maximum in
 // row-major window order (strict >), a NaN wins and stops the scan.
-template <class T>
+// KK/SS > 0: window and stride compiled in (the AlexNet 3/2 path: every
+// window load unrolled and in flight together); 0: taken from the arguments.
+template <class T, int KK, int SS>
 __global__ void __launch_bounds__(256) maxpool_fwd_w_kernel(const T* __restrict__ x, T* __restrict__ y,
                                                             uint8_t* __restrict__ widx, int H, int W, int C,
-                                                            int k, int s, int OH, int OW, int n4, int YH, int YW,
+                                                            int k_, int s_, int OH, int OW, int n4, int YH, int YW,
                                                             int yp) {
+  const int k = KK ? KK : k_, s = SS ? SS : s_;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n4) return;
   const int G = C >> 2;
@@ -587,9 +590,11 @@ __global__ void __launch_bounds__(256) maxpool_fwd_w_kernel(const T* __restrict_
   const int oh = t % OH, b = t / OH;
   float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
   int bi[4] = {0, 0, 0, 0};
-  for (int r = 0; r < k; ++r) {
+#pragma unroll
+  for (int r = 0; r < (KK ? KK : k); ++r) {
     const T* row = x + (static_cast<long long>(b * H + oh * s + r) * W + ow * s) * C + 4 * g;
-    for (int q = 0; q < k; ++q) {
+#pragma unroll
+    for (int q = 0; q < (KK ? KK : k); ++q) {
       float v[4];
       ld4<T>(row + q * C, v);
 #pragma unroll
@@ -608,12 +613,13 @@ __global__ void __launch_bounds__(256) maxpool_fwd_w_kernel(const T* __restrict_
 
 // Max-pool backward as a gather: each input element sums the pooled
 // gradients whose argmax it is (deterministic), optional ReLU mask.
-template <class TO, class TM>
+template <class TO, class TM, int KK, int SS>
 __global__ void __launch_bounds__(256) maxpool_bwd_w_kernel(const float* __restrict__ gy,
                                                             const uint8_t* __restrict__ widx,
                                                             TO* __restrict__ gx, const TM* __restrict__ mask,
-                                                            int H, int W, int C, int k, int s, int OH, int OW,
+                                                            int H, int W, int C, int k_, int s_, int OH, int OW,
                                                             int n4, int ZH, int ZW, int zp) {
+  const int k = KK ? KK : k_, s = SS ? SS : s_;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n4) return;
   const int G = C >> 2;
@@ -627,6 +633,32 @@ __global__ void __launch_bounds__(256) maxpool_bwd_w_kernel(const float* __restr
   const int ow0 = w - k + 1 <= 0 ? 0 : (w - k + s) / s;
   const int ow1 = min(OW - 1, w / s);
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  constexpr int MW = KK ? (KK + SS - 1) / SS : 0;  // windows covering a pixel, per dim
+  if constexpr (MW > 0) {
+    // fixed trip count: every window's argmax word and gradient in flight at once
+    uint32_t wi[MW][MW];
+    float4 gv[MW][MW];
+#pragma unroll
+    for (int a = 0; a < MW; ++a)
+#pragma unroll
+      for (int c = 0; c < MW; ++c) {
+        const bool ok = oh0 + a <= oh1 && ow0 + c <= ow1;
+        const long long o = (static_cast<long long>(b * OH + (ok ? oh0 + a : 0)) * OW + (ok ? ow0 + c : 0)) * C + 4 * g;
+        wi[a][c] = ok ? *reinterpret_cast<const uint32_t*>(widx + o) : 0xffffffffu;
+        gv[a][c] = ok ? *reinterpret_cast<const float4*>(gy + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+    for (int a = 0; a < MW; ++a)
+#pragma unroll
+      for (int c = 0; c < MW; ++c) {
+        const uint32_t me = static_cast<uint32_t>((h - (oh0 + a) * s) * k + (w - (ow0 + c) * s));
+        const uint32_t x = wi[a][c];
+        if ((x & 0xff) == me) acc[0] += gv[a][c].x;
+        if (((x >> 8) & 0xff) == me) acc[1] += gv[a][c].y;
+        if (((x >> 16) & 0xff) == me) acc[2] += gv[a][c].z;
+        if ((x >> 24) == me) acc[3] += gv[a][c].w;
+      }
+  } else
   for (int oh = oh0; oh <= oh1; ++oh)
     for (int ow = ow0; ow <= ow1; ++ow) {
       const long long o = (static_cast<long long>(b * OH + oh) * OW + ow) * C + 4 * g;
@@ -1306,8 +1338,13 @@ void launch_maxpool_fwd_w(const T* x, T* y, uint8_t* widx, int B, int H, int W, 
   if (yl.H == 0) yl = OutLayout{OH, OW, 0};
   if (C % 4 != 0) throw std::runtime_error("maxpool: channels must be a multiple of 4");
   const int n4 = static_cast<int>(static_cast<long long>(B) * OH * OW * C / 4);
-  maxpool_fwd_w_kernel<T><<<(n4 + 255) / 256, 256, 0, st>>>(x, y, widx, H, W, C, k, s, OH, OW, n4, yl.H, yl.W,
-                                                             yl.p);
+  if (k == 3 && s == 2) {
+    maxpool_fwd_w_kernel<T, 3, 2><<<(n4 + 255) / 256, 256, 0, st>>>(x, y, widx, H, W, C, k, s, OH, OW, n4, yl.H,
+                                                                    yl.W, yl.p);
+  } else {
+    maxpool_fwd_w_kernel<T, 0, 0><<<(n4 + 255) / 256, 256, 0, st>>>(x, y, widx, H, W, C, k, s, OH, OW, n4, yl.H,
+                                                                    yl.W, yl.p);
+  }
 }
 
 template <class TO, class TM>
@@ -1316,8 +1353,13 @@ void launch_maxpool_bwd_w(const float* gy, const uint8_t* widx, TO* gx, const TM
   if (zl.H == 0) zl = OutLayout{H, W, 0};
   if (C % 4 != 0) throw std::runtime_error("maxpool: channels must be a multiple of 4");
   const int n4 = static_cast<int>(static_cast<long long>(B) * H * W * C / 4);
-  maxpool_bwd_w_kernel<TO, TM><<<(n4 + 255) / 256, 256, 0, st>>>(gy, widx, gx, mask, H, W, C, k, s, OH, OW,
-                                                                 n4, zl.H, zl.W, zl.p);
+  if (k == 3 && s == 2) {
+    maxpool_bwd_w_kernel<TO, TM, 3, 2><<<(n4 + 255) / 256, 256, 0, st>>>(gy, widx, gx, mask, H, W, C, k, s, OH,
+                                                                         OW, n4, zl.H, zl.W, zl.p);
+  } else {
+    maxpool_bwd_w_kernel<TO, TM, 0, 0><<<(n4 + 255) / 256, 256, 0, st>>>(gy, widx, gx, mask, H, W, C, k, s, OH,
+                                                                         OW, n4, zl.H, zl.W, zl.p);
+  }
 }
 
 template <class T>
