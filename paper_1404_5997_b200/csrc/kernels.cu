@@ -953,12 +953,12 @@ __global__ void __launch_bounds__(512) lrn_pool_bwd_kernel(
 // segmented shuffles, so there is no shared memory and no block barrier: every
 // thread issues its activation, argmax and pooled-gradient loads at once.
 // Same arithmetic, in the same order, as lrn_pool_bwd_kernel (bit-identical).
-template <class TA, int P>
+template <class TA, int P, int V>
 __global__ void __launch_bounds__(256) lrn_pool_bwd_flat_kernel(
     const float* __restrict__ gy, const uint8_t* __restrict__ widx, const TA* __restrict__ a,
     TA* __restrict__ dz, int B, int H, int W, int C, float alpha, float beta, float kk, int PH, int PW,
     int relu_mask, int ZH, int ZW, int zp) {
-  constexpr int V = 16 / sizeof(TA);
+  static_assert(V % 4 == 0, "channel vectors of 4");
   constexpr int HL = 2, PK = 3, PS = 2, MW = 2;
   const int G = C / V;
   const int g = threadIdx.x & (P - 1);
@@ -981,7 +981,8 @@ __global__ void __launch_bounds__(256) lrn_pool_bwd_flat_kernel(
   const int ow0 = w - PK + 1 <= 0 ? 0 : (w - PK + PS) / PS;
   const int ow1 = min(PW - 1, w / PS);
   if (live) {
-    ldv<TA>(a + ((static_cast<long long>(b) * H + h) * W + w) * C + c0, av);
+#pragma unroll
+    for (int j = 0; j < V; j += 4) ld4<TA>(a + ((static_cast<long long>(b) * H + h) * W + w) * C + c0 + j, av + j);
 #pragma unroll
     for (int i = 0; i < MW; ++i)
 #pragma unroll
@@ -1053,7 +1054,10 @@ __global__ void __launch_bounds__(256) lrn_pool_bwd_flat_kernel(
     if (relu_mask && !(av[k] > 0.f)) gval = 0.f;
     out[k] = gval;
   }
-  if (live) stv<TA>(dz + ((static_cast<long long>(b) * ZH + h + zp) * ZW + w + zp) * C + c0, out);
+  if (live) {
+#pragma unroll
+    for (int j = 0; j < V; j += 4) st4<TA>(dz + ((static_cast<long long>(b) * ZH + h + zp) * ZW + w + zp) * C + c0 + j, out + j);
+  }
 }
 
 // Rotated operand for the implicit dgrad: wr[c][r][s][f] = w[f][R-1-r][S-1-s][c].
@@ -1155,7 +1159,9 @@ __global__ void __launch_bounds__(256) s2d_input_kernel(const float* __restrict_
     choff[ch] = off;
   }
   __syncthreads();
-  const int G = Cz >> 3;
+  // only the 8-channel vectors holding real channels: the all-padding ones
+  // (AlexNet: 48 real of 64) stay as the allocation zeroed them
+  const int G = (real + 7) >> 3;
   T* zrow = z + (static_cast<long long>(b) * Zh + i) * Zw * Cz;
   for (int t = tid; t < Zw * G; t += nt) {
     const int j = t / G, q = t - j * G;
@@ -1310,19 +1316,31 @@ void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* 
                                     relu_mask, zl.H, zl.W, zl.p);
   };
   static const bool flat_off = getenv("HP_DEV_LRN_BWD_SMEM") != nullptr;  // dev: the block-per-row kernel
-  // (only when the vectors fill the lane groups: padded lanes measured slower than the smem kernel)
-  if (n == 5 && pk == 3 && ps == 2 && (G == 4 || G == 8 || G == 16 || G == 32) && !flat_off) {
-    const int P = G <= 4 ? 4 : G <= 8 ? 8 : G <= 16 ? 16 : 32;
+  // Flat kernel when the channel vectors fill power-of-two lane groups: 16-byte
+  // vectors (conv1: 8 of 8 bf16 channels), else 12-channel vectors (conv2: 192
+  // channels = 16 x 12); padded lane groups measured slower than the smem kernel.
+  auto pow2 = [](int g) { return g == 4 || g == 8 || g == 16 || g == 32; };
+  const int Vf = pow2(G) ? V : (C % 12 == 0 && pow2(C / 12) ? 12 : 0);
+  if (n == 5 && pk == 3 && ps == 2 && Vf > 0 && !flat_off) {
+    const int P = C / Vf;
     const long long threads = static_cast<long long>(B) * H * W * P;
     const int blocks = static_cast<int>((threads + 255) / 256);
     auto fl = [&](auto kern) {
       kern<<<blocks, 256, 0, st>>>(gy, widx, a, dz, B, H, W, C, alpha, beta, kk, PH, PW, relu_mask, zl.H, zl.W,
                                    zl.p);
     };
-    if (P == 4) fl(lrn_pool_bwd_flat_kernel<TA, 4>);
-    else if (P == 8) fl(lrn_pool_bwd_flat_kernel<TA, 8>);
-    else if (P == 16) fl(lrn_pool_bwd_flat_kernel<TA, 16>);
-    else fl(lrn_pool_bwd_flat_kernel<TA, 32>);
+    constexpr int V0 = 16 / sizeof(TA);
+    if (Vf == V0) {
+      if (P == 4) fl(lrn_pool_bwd_flat_kernel<TA, 4, V0>);
+      else if (P == 8) fl(lrn_pool_bwd_flat_kernel<TA, 8, V0>);
+      else if (P == 16) fl(lrn_pool_bwd_flat_kernel<TA, 16, V0>);
+      else fl(lrn_pool_bwd_flat_kernel<TA, 32, V0>);
+    } else {
+      if (P == 4) fl(lrn_pool_bwd_flat_kernel<TA, 4, 12>);
+      else if (P == 8) fl(lrn_pool_bwd_flat_kernel<TA, 8, 12>);
+      else if (P == 16) fl(lrn_pool_bwd_flat_kernel<TA, 16, 12>);
+      else fl(lrn_pool_bwd_flat_kernel<TA, 32, 12>);
+    }
   } else if (n == 5 && pk == 3 && ps == 2) {
     go(lrn_pool_bwd_kernel<TA, 2, 5, 3, 2>);
   } else if (n <= 5) {
