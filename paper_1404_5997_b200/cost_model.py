@@ -34,6 +34,8 @@ class CostParams:
     cross_subset_penalty: float = 0.5    # throughput multiplier across subsets
     host_hop_latency: float = 10e-6      # seconds, cross-subset only (SPEC: arbitrary default)
     link_latency: float = 0.0            # seconds per transfer, any pair (B200: NCCL launch + NVSwitch hop)
+    hbm_bandwidth: float = 0.0           # bytes/s for the FC weight streams and update (0: FLOPs only, as SPEC)
+    fc_update_bytes: float = 18.0        # per FC parameter per step: fp32 w + momentum read/write, bf16 copy
     overlap_sync: bool = False           # B200 path: conv-gradient all-reduce overlaps conv backward
     sync_algorithm_factor: float = 1.0   # multiplier on 2(K-1)G/K (NVLS in-switch reduction ~0.5)
 
@@ -71,12 +73,16 @@ def paper_topology(K: int) -> Topology:
     return Topology(K, [list(range(i, min(i + 4, K))) for i in range(0, K, 4)])
 
 
-def b200_params(gemm_efficiency: float = 0.31, element_size: int = 2) -> CostParams:
+def b200_params(gemm_efficiency: float = 0.31, element_size: int = 2, hbm_efficiency: float = 0.75) -> CostParams:
     """NVLink 5 / NVSwitch: every GPU pair at 900 GB/s per direction (one subset),
     bf16 activations, the measured sustained bf16 rate x this repo's measured
-    GEMM efficiency (bench.py roofline.frac)."""
+    GEMM efficiency (bench.py roofline.frac). The FC layers are HBM-bound on
+    B200 (tests/dev/cost_validate.py: 28% of the GEMM time for 7% of its
+    FLOPs), so their time is max(FLOPs, weight bytes) at the measured copy
+    bandwidth x the fused update's measured efficiency (fc6: 75%)."""
     return CostParams(flops_per_sec=1.406e15 * gemm_efficiency, link_bandwidth=900e9, element_size=element_size,
-                      cross_subset_penalty=1.0, host_hop_latency=0.0, link_latency=10e-6, overlap_sync=True)
+                      cross_subset_penalty=1.0, host_hop_latency=0.0, link_latency=10e-6, overlap_sync=True,
+                      hbm_bandwidth=6.5456e12 * hbm_efficiency)
 
 
 def b200_topology(K: int) -> Topology:
@@ -222,13 +228,20 @@ def scheme_step_model(spec, cluster, topo: Topology, params: CostParams,
     ev: List[Event] = [Event(0, 0.0, t_conv_f, "compute", "conv_fwd")]
     t = t_conv_f
     tl = Timeline(ev, 0.0)
+    # FC weights this worker holds: the whole stack (K = 1, pure DP) or a 1/K
+    # column shard; streamed twice per pass (fwd, dgrad; bf16) and updated once
+    # per step when hbm_bandwidth is set
+    P = sum(f.in_dim * f.out_dim for f in spec.fc_layers) / (1 if (K == 1 or s == Scheme.DP) else K)
+    hbm = params.hbm_bandwidth
+    fc_pass = lambda f: max(ct(f), 2 * 2 * P / hbm if hbm > 0 else 0.0)
+    fc_upd = params.fc_update_bytes * P / hbm if hbm > 0 else 0.0
     if K == 1 or s == Scheme.DP:
-        fc = ct(3 * sum(fl["fc_fwd"]) * b)
+        fc = fc_pass(3 * sum(fl["fc_fwd"]) * b)
         ev.append(Event(0, t, t + fc, "compute", "fc"))
         t += fc
     else:
         n = x["rows"]
-        fc = ct(3 * sum(fl["fc_fwd"]) * n / K)  # n examples over out/K columns
+        fc = fc_pass(3 * sum(fl["fc_fwd"]) * n / K)  # n examples over out/K columns
         # model-parallel internals per turn: forward all-gather of each layer's column
         # shard, backward reduce-scatter of the input partials above the first layer
         internal = sum(_flow_time((K - 1) * n * f.out_dim / K, K - 1, params, topo) for f in spec.fc_layers) + \
@@ -266,6 +279,9 @@ def scheme_step_model(spec, cluster, topo: Topology, params: CostParams,
             t = max(t, link_back)
             tl.boundary_total = K * (ta + tg)
         tl.internal_s = x["turns"] * internal
+    if fc_upd > 0:
+        ev.append(Event(0, t, t + fc_upd, "compute", "fc_update"))
+        t += fc_upd
     ev.append(Event(0, t, t + t_conv_b, "compute", "conv_bwd"))
     t_end = t + t_conv_b
     if K > 1:
@@ -296,7 +312,19 @@ def speedup(spec, cluster, topo: Topology, params: CostParams, compute_scale: fl
 
 
 def calibrate(spec, b: int, params: CostParams, measured_step_s: float) -> float:
-    """compute_scale such that the K=1 model equals a measured 1-GPU step."""
+    """compute_scale such that the K=1 model equals a measured 1-GPU step (the
+    step time is non-decreasing in the scale; HBM-bound phases do not scale)."""
     from .api import ClusterConfig
-    t = scheme_step_model(spec, ClusterConfig(workers=1, per_worker_batch=b), Topology(1), params).step_time
-    return measured_step_s / t
+    cl = ClusterConfig(workers=1, per_worker_batch=b)
+    f = lambda sc: scheme_step_model(spec, cl, Topology(1), params, sc).step_time
+    lo, hi = 0.0, 1.0
+    while f(hi) < measured_step_s:
+        hi *= 2.0
+        if hi > 1e9:
+            raise ValueError("calibrate: measured step unreachable")
+    if f(lo) > measured_step_s:
+        raise ValueError("calibrate: measured step below the model's memory-bound floor")
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        lo, hi = (mid, hi) if f(mid) < measured_step_s else (lo, mid)
+    return 0.5 * (lo + hi)
