@@ -220,3 +220,22 @@ def test_cli_scale_hparams(capsys):
     assert d["eps_new"] == pytest.approx(0.0282843, abs=1e-7)
     assert abs(d["omega_exact"] - 0.0014141888) <= 1e-9 and abs(d["omega_approx"] - 0.0014142136) <= 1e-10
     assert cli.main(["scale-hparams", "--eps", "2", "--omega", "0.6", "--k", "8"]) == cli.EXIT_VALIDATION
+
+
+def test_fc_hbm_term_shards_with_model_parallelism():
+    """B200 parameter set: FC passes are max(FLOPs, bf16 weight reads) and the
+    fused update streams 18 B per parameter a worker holds (1/K shard under
+    the hybrid schemes, all of it under pure DP)."""
+    spec = alexnet_1col()
+    p = cm.b200_params()
+    P = sum(f.in_dim * f.out_dim for f in spec.fc_layers)
+    t1 = cm.scheme_step_model(spec, hp.ClusterConfig(workers=1, per_worker_batch=128), cm.Topology(1), p)
+    assert t1.phase_table()["fc_update"] == pytest.approx(18 * P / p.hbm_bandwidth)
+    assert t1.phase_table()["fc"] >= 4 * P / p.hbm_bandwidth
+    for s, share in ((hp.Scheme.A, 1 / 8), (hp.Scheme.B, 1 / 8), (hp.Scheme.DP, 1.0)):
+        tk = cm.scheme_step_model(spec, hp.ClusterConfig(workers=8, per_worker_batch=128, scheme=s),
+                                  cm.b200_topology(8), p)
+        assert tk.phase_table()["fc_update"] == pytest.approx(18 * P * share / p.hbm_bandwidth)
+    # the paper machine keeps the SPEC's FLOPs-only FC phase
+    assert "fc_update" not in cm.scheme_step_model(spec, hp.ClusterConfig(workers=1, per_worker_batch=128),
+                                                   cm.Topology(1), cm.PAPER).phase_table()
