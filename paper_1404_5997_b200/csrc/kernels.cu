@@ -810,6 +810,85 @@ __global__ void __launch_bounds__(1024) lrn_pool_fwd_kernel(const T* __restrict_
     }
 }
 
+// Forward, flat form (AlexNet 5/3/2 fast path, vectors filling power-of-two
+// lane groups): thread = (pooled pixel, channel vector); it computes the LRN of
+// the 3x3 window's conv pixels itself (+-2-channel halos by segmented shuffles)
+// and max-pools in registers -- no smem band, no barriers; each conv pixel's
+// LRN is recomputed by up to 4 windows. Same values, order and argmax rule as
+// lrn_pool_fwd_kernel (bit-identical).
+template <class T, int P, int V>
+__global__ void __launch_bounds__(256) lrn_pool_fwd_flat_kernel(const T* __restrict__ a, T* __restrict__ y,
+                                                                 uint8_t* __restrict__ widx, int B, int H, int W,
+                                                                 int C, float alpha, float beta, float kk, int PH,
+                                                                 int PW, int YH, int YW, int yp) {
+  static_assert(V % 4 == 0, "channel vectors of 4");
+  constexpr int HL = 2, PK = 3, PS = 2;
+  const int G = C / V;
+  const int g = threadIdx.x & (P - 1);
+  const int pix = blockIdx.x * (blockDim.x / P) + threadIdx.x / P;  // B*PH*PW < 2^31 (launcher)
+  const bool live = g < G && pix < B * PH * PW;
+  const int bph = live ? pix / PW : 0;
+  const int pw = live ? pix - bph * PW : 0;
+  const int b = bph / PH, ph = bph - b * PH;
+  const int c0 = g * V;
+  float best[V];
+  int bi[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    best[j] = -INFINITY;
+    bi[j] = 0;
+  }
+#pragma unroll 1
+  for (int r = 0; r < PK; ++r) {
+    float v[PK][V];
+#pragma unroll
+    for (int q = 0; q < PK; ++q) {
+      const T* px = a + ((static_cast<long long>(b) * H + ph * PS + r) * W + pw * PS + q) * C + c0;
+#pragma unroll
+      for (int j = 0; j < V; j += 4) {
+        if (live) {
+          ld4<T>(px + j, v[q] + j);
+        } else {
+          v[q][j] = v[q][j + 1] = v[q][j + 2] = v[q][j + 3] = 0.f;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PK; ++q) {
+      float sq[V + 2 * HL];
+#pragma unroll
+      for (int j = 0; j < V; ++j) sq[HL + j] = v[q][j] * v[q][j];
+#pragma unroll
+      for (int d = 0; d < HL; ++d) {
+        const float l = __shfl_up_sync(0xffffffffu, v[q][V - HL + d], 1, P);
+        const float rr = __shfl_down_sync(0xffffffffu, v[q][d], 1, P);
+        sq[d] = g > 0 ? l * l : 0.f;
+        sq[HL + V + d] = g + 1 < G ? rr * rr : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        float sum = 0.f;
+#pragma unroll
+        for (int d = -HL; d <= HL; ++d) sum += sq[HL + j + d];
+        const float o = v[q][j] * pow_neg(kk + alpha * sum, beta);
+        if ((o > best[j] || isnan(o)) && !isnan(best[j])) {
+          best[j] = o;
+          bi[j] = r * PK + q;
+        }
+      }
+    }
+  }
+  if (!live) return;
+#pragma unroll
+  for (int j = 0; j < V; j += 4)
+    st4<T>(y + (static_cast<long long>(b * YH + ph + yp) * YW + pw + yp) * C + c0 + j, best + j);
+  const long long o = (static_cast<long long>(b * PH + ph) * PW + pw) * C + c0;
+#pragma unroll
+  for (int j = 0; j < V; j += 4)
+    *reinterpret_cast<uint32_t*>(widx + o + j) = static_cast<uint32_t>(bi[j]) | (bi[j + 1] << 8) |
+                                                 (bi[j + 2] << 16) | (static_cast<uint32_t>(bi[j + 3]) << 24);
+}
+
 // Backward: block = one conv-output row (b, h) x all channels, threads =
 // (channel vector g, column w); the pooled-row range is block-uniform.
 //   gb_c = sum of the pooled gradients whose argmax is this pixel (gather)
@@ -1285,7 +1364,28 @@ void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, i
     kern<<<grid, block, smem, st>>>(a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, TP,
                                     yl.H, yl.W, yl.p);
   };
-  if (n == 5 && pk == 3 && ps == 2) {
+  static const bool flat_off = getenv("HP_DEV_LRN_FWD_SMEM") != nullptr;  // dev: the smem-band kernel
+  auto pow2 = [](int g) { return g == 4 || g == 8 || g == 16 || g == 32; };
+  const int Vf = pow2(G) ? V : (C % 12 == 0 && pow2(C / 12) ? 12 : 0);
+  if (n == 5 && pk == 3 && ps == 2 && Vf > 0 && !flat_off) {
+    const int P = C / Vf;
+    const long long threads = static_cast<long long>(B) * PH * PW * P;
+    const int blocks = static_cast<int>((threads + 255) / 256);
+    auto fl = [&](auto kern) {
+      kern<<<blocks, 256, 0, st>>>(a, y, widx, B, H, W, C, alpha, beta, kk, PH, PW, yl.H, yl.W, yl.p);
+    };
+    if (Vf == V) {
+      if (P == 4) fl(lrn_pool_fwd_flat_kernel<T, 4, V>);
+      else if (P == 8) fl(lrn_pool_fwd_flat_kernel<T, 8, V>);
+      else if (P == 16) fl(lrn_pool_fwd_flat_kernel<T, 16, V>);
+      else fl(lrn_pool_fwd_flat_kernel<T, 32, V>);
+    } else {
+      if (P == 4) fl(lrn_pool_fwd_flat_kernel<T, 4, 12>);
+      else if (P == 8) fl(lrn_pool_fwd_flat_kernel<T, 8, 12>);
+      else if (P == 16) fl(lrn_pool_fwd_flat_kernel<T, 16, 12>);
+      else fl(lrn_pool_fwd_flat_kernel<T, 32, 12>);
+    }
+  } else if (n == 5 && pk == 3 && ps == 2) {
     go(lrn_pool_fwd_kernel<T, 2, 5, 3, 2>);
   } else if (n <= 5) {
     go(lrn_pool_fwd_kernel<T, 2, 0, 0, 0>);

@@ -1,7 +1,7 @@
 """Kernel variants that must agree bit for bit (GPU). The flat shuffle-halo
-LRN+pool backward (conv1: 8-channel vectors, conv2: 12-channel vectors) is the
-default; HP_DEV_LRN_BWD_SMEM=1 selects the block-per-row smem kernel it
-replaced. The switch is read once per process, so each variant runs an
+LRN+pool kernels (conv1: 8-channel vectors, conv2: 12-channel vectors) are the
+default; HP_DEV_LRN_BWD_SMEM=1 / HP_DEV_LRN_FWD_SMEM=1 select the smem kernels
+they replaced. The switch is read once per process, so each variant runs an
 AlexNet-1col bf16 step sequence in its own subprocess and the parameter bytes
 are compared."""
 import os
@@ -40,7 +40,7 @@ def run(env_extra, math):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("math", ["BF16", "F32X3"])
-def test_flat_lrn_backward_matches_smem_kernel(math):
+def test_flat_lrn_kernels_match_smem_kernels(math):
     flat = run({}, math)
-    smem = run({"HP_DEV_LRN_BWD_SMEM": "1"}, math)
-    assert flat == smem
+    assert flat == run({"HP_DEV_LRN_BWD_SMEM": "1"}, math)
+    assert flat == run({"HP_DEV_LRN_FWD_SMEM": "1"}, math)
