@@ -1636,7 +1636,7 @@ void launch_rowsum(const T* x, int R, int n, long long ldx, float* out, int beta
 
 int xent_blocks(int Ls, int n) {
   const long long total = static_cast<long long>(Ls) * n;
-  return static_cast<int>(std::min<long long>(std::max<long long>(1, (total + 255) / 256), 128));
+  return static_cast<int>(std::min<long long>(std::max<long long>(1, (total + 255) / 256), 512));
 }
 
 template <class TO>
