@@ -1607,9 +1607,15 @@ void launch_lrn_bwd(const TA* a, const float* d, const float* gb, TO* ga, long l
       a, d, gb, ga, C, n / 2, (n - 1) / 2, alpha, beta, relu_mask, total);
 }
 
-// row groups: 256 rows each, at most 512
-static long long colsum_groups(long long M, int) {
-  return std::min<long long>(std::max<long long>(1, (M + 255) / 256), 512);
+// row groups: 256 rows each (at most 512), but at least ~384 blocks over the
+// column blocks while groups keep >= 64 rows (the 13x13 layers had 98-196
+// blocks: 13-16% of the warp slots busy; more groups cost the final pass)
+static long long colsum_groups(long long M, int N) {
+  const int vec = N / 8, TX = std::min(vec, 32);
+  const long long xb = (vec + TX - 1) / TX;
+  const long long g256 = std::min<long long>(std::max<long long>(1, (M + 255) / 256), 512);
+  const long long fill = std::min<long long>((384 + xb - 1) / xb, std::max<long long>(1, M / 64));
+  return std::max(g256, fill);
 }
 
 size_t colsum_ws_floats(long long M, int N) { return static_cast<size_t>(colsum_groups(M, N)) * N; }
