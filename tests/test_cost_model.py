@@ -239,3 +239,21 @@ def test_fc_hbm_term_shards_with_model_parallelism():
     # the paper machine keeps the SPEC's FLOPs-only FC phase
     assert "fc_update" not in cm.scheme_step_model(spec, hp.ClusterConfig(workers=1, per_worker_batch=128),
                                                    cm.Topology(1), cm.PAPER).phase_table()
+
+
+def test_cli_cost_report_b200_calibrated(tmp_path, capsys):
+    """machine b200 + measured_step_ms: the K=1 model reproduces the measured
+    step, and the report carries the FC update phase (HBM term)."""
+    c = {"model": "alexnet_1col", "cluster": {"workers": 1, "per_worker_batch": 128, "scheme": "B"},
+         "output_dir": str(tmp_path / "o"), "cost": {"machine": "b200", "measured_step_ms": 1.6}}
+    p = tmp_path / "c.json"
+    p.write_text(json.dumps(c))
+    assert cli.main(["cost-report", "--config", str(p), "--json"]) == 0
+    r = json.loads(capsys.readouterr().out)
+    assert r["step_time_K"] == pytest.approx(1.6e-3, rel=1e-9)
+    assert "fc_update" in r["phases_s"] and r["speedup"] == pytest.approx(1.0)
+    c["cluster"].update(workers=8, scheme="A")
+    p.write_text(json.dumps(c))
+    assert cli.main(["cost-report", "--config", str(p), "--json"]) == 0
+    r8 = json.loads(capsys.readouterr().out)
+    assert r8["phases_s"]["fc_update"] == pytest.approx(r["phases_s"]["fc_update"] / 8, rel=1e-9)
