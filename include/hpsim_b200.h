@@ -249,6 +249,16 @@ typedef struct hp_gemm_prof {
   double ms;
 } hp_gemm_prof;
 HP_API int hp_cluster_gemm_profile(const hp_cluster* c, hp_gemm_prof* out, int cap);
+/* Debug (graph-structure tests): capture one step WITHOUT running it, with a
+ * 1-thread tagged marker kernel at each turn boundary -- 100+j / 200+j around
+ * turn j's boundary exchange (stream sr), 300+j / 400+j around turn j's FC
+ * forward+backward (compute stream), 500+j / 600+j around turn j's gradient
+ * return -- and report reach[i*n+k] = 1 when marker k is reachable from
+ * marker i in the captured dependency DAG. tags/reach: cap and cap*cap. */
+HP_API int hp_cluster_debug_marker_graph(hp_cluster* c, const float* const* batches,
+                                         const float* const* targets, int mem_kind, const hp_hyper* hp,
+                                         double lr, int32_t* tags, uint8_t* reach, int cap,
+                                         int* n_markers);
 
 /* ---- host-side helpers shared with the reference ------------------------ */
 /* Analytic byte counters + phase trace of `steps` steps (cluster.cpp:466-673)
@@ -317,6 +327,30 @@ HP_API int hp_kernel_conv_dgrad(int math, const void* dy, int B, int OH, int OW,
  * Replaces conv2d_forward / the stride-1 conv2d_backward dgrad (tensor.cpp:419-516). */
 HP_API int hp_kernel_conv_shift(const void* x, int64_t rows, int C, int R, int S, int wq, const void* w,
                                 int N, float* y, int boff_mode, void* stream);
+
+/* Fused LRN + overlapping max-pool of one conv stage (the AlexNet superset;
+ * no reference counterpart -- parity pinned by the oracle's torch-checked
+ * restatement, oracle/hpsim_oracle.c or_lrn_* / or_maxpool_*). The same
+ * launch the step makes. math: HP_MATH_BF16 (a, y, dz bf16) or fp32.
+ * a [B][H][W][C] conv output (post-ReLU), y [B][PH][PW][C] with
+ * PH = (H - pk) / ps + 1, widx [B][PH][PW][C] uint8 window offset r*pk + q of
+ * the FIRST maximum in row-major window order (strict >, NaN wins), gy fp32
+ * [B][PH][PW][C], dz [B][H][W][C] (x ReLU mask of a when relu_mask).
+ * LRN (Krizhevsky 2012): b_c = a_c (k + alpha sum_{|i-c|<=n/2} a_i^2)^-beta,
+ * alpha NOT divided by n. lrn_size 0: max-pool only. */
+HP_API int hp_kernel_lrn_pool_fwd(int math, const void* a, int B, int H, int W, int C, int lrn_size,
+                                  float alpha, float beta, float k, int pk, int ps, void* y,
+                                  uint8_t* widx, void* stream);
+HP_API int hp_kernel_lrn_pool_bwd(int math, const float* gy, const uint8_t* widx, const void* a, int B,
+                                  int H, int W, int C, int lrn_size, float alpha, float beta, float k,
+                                  int pk, int ps, int relu_mask, void* dz, void* stream);
+/* The step's momentum SGD (momentum_update, optimizer.cpp:19-31) on one fp32
+ * tensor: g *= gscale (if has_gscale), delta = mu*delta; delta += -lr*g;
+ * delta += -lr*wd*w; w += delta -- four rounded passes, scalars formed in
+ * double and rounded to float once (tensor.cpp:195-229). bf16_copy: optional
+ * bf16 copy of the updated w. */
+HP_API int hp_kernel_sgd(float* w, float* mom, const float* g, int64_t n, double lr, double momentum,
+                         double weight_decay, float gscale, int has_gscale, void* bf16_copy, void* stream);
 
 #ifdef __cplusplus
 }

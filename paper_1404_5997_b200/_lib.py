@@ -137,6 +137,12 @@ def _load() -> C.CDLL:
                                   C.c_int, C.c_int, C.c_int, P, P], C.c_int),
         "hp_kernel_conv_wgrad": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int,
                                   C.c_int, C.c_int, C.c_int, P, P, C.c_int64, P], C.c_int),
+        "hp_kernel_lrn_pool_fwd": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float,
+                                    C.c_float, C.c_float, C.c_int, C.c_int, P, P, P], C.c_int),
+        "hp_kernel_lrn_pool_bwd": ([C.c_int, P, P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float,
+                                    C.c_float, C.c_float, C.c_int, C.c_int, C.c_int, P, P], C.c_int),
+        "hp_kernel_sgd": ([P, P, P, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_float, C.c_int, P, P],
+                          C.c_int),
         "hp_kernel_conv_dgrad": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int,
                                   C.c_int, C.c_int, P, P], C.c_int),
     }
@@ -168,6 +174,9 @@ def _load() -> C.CDLL:
         "hp_cluster_set_shift_conv": ([P, C.c_int], C.c_int),
         "hp_cluster_set_graphs": ([P, C.c_int], C.c_int),
         "hp_cluster_gemm_profile": ([P, C.POINTER(HpGemmProf), C.c_int], C.c_int),
+        "hp_cluster_debug_marker_graph": ([P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int,
+                                           C.POINTER(HpHyper), C.c_double, C.POINTER(C.c_int32),
+                                           C.POINTER(C.c_uint8), C.c_int, C.POINTER(C.c_int)], C.c_int),
     }
     for name, (args, res) in list(sigs.items()) + list(optional.items()):
         fn = getattr(lib, name, None)

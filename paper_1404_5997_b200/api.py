@@ -239,12 +239,23 @@ def nccl_unique_id() -> bytes:
 
 
 def _ptr(x) -> int:
-    """Address of a host numpy array or a device tensor (anything with data_ptr())."""
+    """Address of a host numpy array or a torch tensor (float32, contiguous)."""
     if isinstance(x, np.ndarray):
         if x.dtype != np.float32 or not x.flags["C_CONTIGUOUS"]:
             raise DimensionError("host tensors must be C-contiguous float32")
         return x.ctypes.data
+    if str(getattr(x, "dtype", "")) != "torch.float32" or not x.is_contiguous():
+        raise DimensionError("tensors must be contiguous float32")
     return int(x.data_ptr())
+
+
+def _on_device(x) -> bool:
+    """HP_MEM_DEVICE for CUDA tensors; numpy arrays and (pinned) CPU tensors are host memory."""
+    return bool(getattr(x, "is_cuda", False))
+
+
+def _shape_str(shape) -> str:  # shape_string (tensor.cpp:57-66)
+    return "[" + "x".join(str(int(d)) for d in shape) + "]"
 
 
 class Cluster:
@@ -295,14 +306,17 @@ class Cluster:
         targets[i]: [b][L]; host numpy arrays or device tensors (all the same kind)."""
         lr = hp.lr if lr is None else lr
         n = len(batches)
-        if len(targets) != n:
-            raise UsageError(f"run_step: expected {n} batches and targets, got {n} / {len(targets)}")
+        k = 1 if self.config.transport == Transport.NCCL else self.config.workers
+        if n != k or len(targets) != k:  # cluster.cpp:444-450
+            raise UsageError(f"run_step: expected {k} batches and targets, got {n} / {len(targets)}")
+        self._check_inputs(batches, targets, "run_step")
+        kinds = {_on_device(x) for x in list(batches) + list(targets)}
+        if len(kinds) != 1:
+            raise UsageError("run_step: batches and targets must all be host or all be device memory")
         if device is None:
-            device = not isinstance(batches[0], np.ndarray)
-        b = self.config.per_worker_batch
-        for i, (x, t) in enumerate(zip(batches, targets)):
-            if x.shape[0] != b or t.shape[0] != b:
-                raise UsageError(f"run_step: worker {i} batch must hold exactly {b} examples")
+            device = kinds.pop()
+        elif bool(device) != kinds.pop():
+            raise UsageError("run_step: device= does not match where the tensors live")
         bp = (C.c_void_p * n)(*[_ptr(x) for x in batches])
         tp = (C.c_void_p * n)(*[_ptr(t) for t in targets])
         h = HpHyper(hp.momentum, hp.lr, hp.weight_decay, 0 if hp.fc_partial_lr is None else 1,
@@ -312,6 +326,23 @@ class Cluster:
         return StepResult(StepMetrics(m.loss, m.fc_update_count, m.conv_update_count, list(m.bytes_sent)),
                           self.trace())
 
+    def _check_inputs(self, batches: Sequence, targets: Sequence, fn: str) -> None:
+        """Full shapes before any native call: rows (UsageError, cluster.cpp:451-457),
+        then [b][C][H][W] (DimensionError, model.cpp:204-214) and [b][L]
+        (logistic_xent's shape check, tensor.cpp:172-182). The native side reads
+        exactly b*C*H*W and b*L floats per worker."""
+        b = self.config.per_worker_batch
+        C_, H, W = self.spec.input_shape
+        L = self.spec.num_classes
+        for i, (x, t) in enumerate(zip(batches, targets)):
+            if x.shape[0] != b or t.shape[0] != b:
+                raise UsageError(f"{fn}: worker {i} batch must hold exactly {b} examples")
+            if len(x.shape) != 4 or tuple(x.shape[1:]) != (C_, H, W):
+                raise DimensionError(f"forward: batch shape {_shape_str(x.shape)} does not match model input "
+                                     f"[Bx{C_}x{H}x{W}]")
+            if tuple(t.shape) != (b, L):
+                raise DimensionError(f"logistic_xent: shape mismatch {_shape_str((b, L))} vs {_shape_str(t.shape)}")
+
     def prefetch(self, batches: Sequence, targets: Sequence) -> None:
         """Stage the next step's HOST batches (numpy or pinned CPU tensors) on the
         copy stream; a following run_step with the same buffers consumes them
@@ -319,6 +350,9 @@ class Cluster:
         n = len(batches)
         if len(targets) != n:
             raise UsageError(f"prefetch: expected {n} batches and targets, got {n} / {len(targets)}")
+        self._check_inputs(batches, targets, "prefetch")
+        if any(_on_device(x) for x in list(batches) + list(targets)):
+            raise UsageError("prefetch: stages host buffers only")
         bp = (C.c_void_p * n)(*[_ptr(x) for x in batches])
         tp = (C.c_void_p * n)(*[_ptr(t) for t in targets])
         _check(lib.hp_cluster_prefetch(self._h, bp, tp))
@@ -398,6 +432,28 @@ class Cluster:
 
     def set_profile(self, on: bool) -> None:
         _check(lib.hp_cluster_set_profile(self._h, int(bool(on))))
+
+    def marker_graph(self, batches: Sequence, targets: Sequence, hp: HyperParams, lr: Optional[float] = None):
+        """Debug: (tags, reach) of one captured-but-not-run step; reach[i][k] is
+        True when marker tags[k] is reachable from tags[i] in the step graph
+        (see hp_cluster_debug_marker_graph for the tag scheme)."""
+        lr = hp.lr if lr is None else lr
+        n = len(batches)
+        self._check_inputs(batches, targets, "marker_graph")
+        device = _on_device(batches[0])
+        bp = (C.c_void_p * n)(*[_ptr(x) for x in batches])
+        tp = (C.c_void_p * n)(*[_ptr(t) for t in targets])
+        h = HpHyper(hp.momentum, hp.lr, hp.weight_decay, 0 if hp.fc_partial_lr is None else 1,
+                    0.0 if hp.fc_partial_lr is None else hp.fc_partial_lr)
+        cap = 1024
+        tags = (C.c_int32 * cap)()
+        reach = (C.c_uint8 * (cap * cap))()
+        nm = C.c_int()
+        _check(lib.hp_cluster_debug_marker_graph(self._h, bp, tp, 1 if device else 0, C.byref(h), lr, tags,
+                                                 reach, cap, C.byref(nm)))
+        m = nm.value
+        r = np.frombuffer(reach, dtype=np.uint8, count=m * m).reshape(m, m).astype(bool)
+        return list(tags[:m]), r
 
     def gemm_profile(self):
         """[(tag, layer, flops, ms)] for the last profiled step, launch order."""

@@ -4,6 +4,7 @@
 
 #include "errors.hpp"
 #include "gemm.cuh"
+#include "kernels.cuh"
 #include "hpsim_b200.h"
 #include "rng.hpp"
 
@@ -175,6 +176,70 @@ HP_API int hp_kernel_conv_shift(const void* x, int64_t rows, int C, int R, int S
     GemmPlan p = conv_shift_plan(x, rows, C, R, S, wq, w, static_cast<long long>(R) * S * C, N, e, boff_mode);
     if (!p.valid) config_error("conv_shift: unsupported shape");
     gemm_launch(p, static_cast<cudaStream_t>(stream));
+    HP_CUDA(cudaGetLastError());
+  });
+}
+
+// Fused LRN + max-pool of one conv stage, exactly the launch the step makes
+// (kernels.cu launch_lrn_pool_* / launch_maxpool_*_w); lrn_size 0: pool only.
+HP_API int hp_kernel_lrn_pool_fwd(int math, const void* a, int B, int H, int W, int C, int lrn_size, float alpha,
+                                  float beta, float k, int pk, int ps, void* y, uint8_t* widx, void* stream) {
+  return guarded([&] {
+    if (!a || !y || !widx) usage_error("lrn_pool_fwd: null pointer");
+    if (pk < 1 || ps < 1 || pk > 16 || H < pk || W < pk) config_error("lrn_pool_fwd: bad pool window");
+    const int PH = (H - pk) / ps + 1, PW = (W - pk) / ps + 1;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto go = [&](auto tag) {
+      using T = decltype(tag);
+      if (lrn_size > 0)
+        launch_lrn_pool_fwd<T>(static_cast<const T*>(a), static_cast<T*>(y), widx, B, H, W, C, lrn_size, alpha, beta,
+                               k, pk, ps, PH, PW, st);
+      else
+        launch_maxpool_fwd_w<T>(static_cast<const T*>(a), static_cast<T*>(y), widx, B, H, W, C, pk, ps, PH, PW, st);
+    };
+    if (math == HP_MATH_BF16) go(bf16{});
+    else go(float{});
+    HP_CUDA(cudaGetLastError());
+  });
+}
+
+HP_API int hp_kernel_lrn_pool_bwd(int math, const float* gy, const uint8_t* widx, const void* a, int B, int H, int W,
+                                  int C, int lrn_size, float alpha, float beta, float k, int pk, int ps, int relu_mask,
+                                  void* dz, void* stream) {
+  return guarded([&] {
+    if (!gy || !widx || !a || !dz) usage_error("lrn_pool_bwd: null pointer");
+    if (pk < 1 || ps < 1 || pk > 16 || H < pk || W < pk) config_error("lrn_pool_bwd: bad pool window");
+    const int PH = (H - pk) / ps + 1, PW = (W - pk) / ps + 1;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto go = [&](auto tag) {
+      using T = decltype(tag);
+      if (lrn_size > 0)
+        launch_lrn_pool_bwd<T>(gy, widx, static_cast<const T*>(a), static_cast<T*>(dz), B, H, W, C, lrn_size, alpha,
+                               beta, k, pk, ps, PH, PW, relu_mask, st);
+      else
+        launch_maxpool_bwd_w<T, T>(gy, widx, static_cast<T*>(dz), relu_mask ? static_cast<const T*>(a) : nullptr, B,
+                                   H, W, C, pk, ps, PH, PW, st);
+    };
+    if (math == HP_MATH_BF16) go(bf16{});
+    else go(float{});
+    HP_CUDA(cudaGetLastError());
+  });
+}
+
+// The step's momentum SGD kernel on one fp32 tensor (optimizer.cpp:19-31).
+HP_API int hp_kernel_sgd(float* w, float* mom, const float* g, int64_t n, double lr, double momentum,
+                         double weight_decay, float gscale, int has_gscale, void* bf16_copy, void* stream) {
+  return guarded([&] {
+    if (!w || !mom || !g) usage_error("sgd: null pointer");
+    SgdTensor t{};
+    t.w = w;
+    t.mom = mom;
+    t.g = g;
+    t.copy = bf16_copy;
+    t.n = n;
+    t.gscale = gscale;
+    t.has_gscale = has_gscale;
+    launch_sgd(&t, 1, bf16_copy ? 1 : 0, lr, momentum, weight_decay, static_cast<cudaStream_t>(stream));
     HP_CUDA(cudaGetLastError());
   });
 }

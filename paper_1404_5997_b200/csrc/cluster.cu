@@ -22,7 +22,9 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <chrono>
 #include <map>
+#include <thread>
 #include <string>
 #include <tuple>
 
@@ -331,8 +333,11 @@ struct Worker {
   float* cgr_local = nullptr;  // skip_sync_broadcast: this worker's pre-all-reduce conv gradients
   TA* cpt = nullptr;  // operand copy (bf16 mode)
   // fc stack
-  TA* xb = nullptr;        // [n][A] boundary input
-  float* tb = nullptr;     // [n][L] routed targets
+  // boundary buffers, double-buffered by turn parity: turn j+1's exchange
+  // fills slot (j+1)&1 while turn j's FC compute reads slot j&1
+  TA* xb[2] = {nullptr, nullptr};     // [n][A] boundary input
+  float* tb[2] = {nullptr, nullptr};  // [n][L] routed targets
+  float* fd0[2] = {nullptr, nullptr}; // [n][A] partial boundary gradient (fc0 dgrad -> return)
   std::vector<TA*> fx;     // fx[l] (l>=1): [K*cmax(l-1)][ldn]
   float* logits = nullptr; // [cmax_last][ldn]
   std::vector<TA*> fdz;    // [cmax_l][ldn]
@@ -345,6 +350,7 @@ struct Worker {
   float* colsum_ws = nullptr;
   // GEMM plans
   std::vector<GemmPlan> conv_fwd, conv_wgrad, conv_dgrad, fc_fwd, fc_wgrad, fc_dgrad;
+  GemmPlan fc0_slot1[3];  // fc layer 0 {fwd, wgrad, dgrad} over boundary slot 1 (slot 0: the vectors)
 };
 
 template <class TA>
@@ -363,6 +369,9 @@ class ClusterImpl final : public ClusterBase {
   }
   void run_step(const float* const* batches, const float* const* targets, int mem_kind,
                 const hp_hyper& hp, double lr, hp_step_metrics* out) override;
+  void marker_graph(const float* const* batches, const float* const* targets, int mem_kind,
+                    const hp_hyper& hp, double lr, std::vector<int>& tags,
+                    std::vector<uint8_t>& reach) override;
   int64_t param_size(int worker, int which, int layer) const override;
   void read_param(int worker, int which, int layer, float* dst, int64_t n) override;
   void write_param(int worker, int which, int layer, const float* src, int64_t n) override;
@@ -381,9 +390,14 @@ class ClusterImpl final : public ClusterBase {
     bool dz_ready = false;        // dz already produced by the layer above's dgrad
   };
   void conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs);
-  void route_forward(int j);
-  void fc_forward_backward(int j, bool beta);
-  void return_gradients(int j);
+  void route_forward(int j, int slot, cudaStream_t s);
+  void fc_forward_backward(int j, bool beta, int slot);
+  void return_gradients(int j, int slot, cudaStream_t s);
+  void marker(int tag, cudaStream_t s) {
+    if (!markers) return;
+    launch_marker(tag, s);
+    ++launches_;
+  }
   void sgd_fc(double lr, float gscale, bool has_gscale, const hp_hyper& hp);
   void sgd_conv(double lr, const hp_hyper& hp);
   void account(int num_sub, hp_step_metrics* out);
@@ -427,7 +441,21 @@ class ClusterImpl final : public ClusterBase {
   long long b_, n_, ldn_;
   int num_sub_, L_;
   uint64_t seed_;
-  std::unique_ptr<Comm> comm_;
+  // One transport per concurrent stream (NCCL: one communicator each, split
+  // from the first, so no two streams ever drive the same communicator):
+  // comm_ FC-internal gathers/scatters + loss on st_, comm_x_ the boundary
+  // exchange / gradient return on sr_, comm_s_ the conv-gradient all-reduce on sc_.
+  std::unique_ptr<Comm> comm_, comm_x_, comm_s_;
+  cudaStream_t sr_ = nullptr;  // boundary exchange + gradient return (overlaps the FC compute)
+  cudaEvent_t ev_conv_ = nullptr;          // conv tops + targets final on st_
+  cudaEvent_t ev_xready_[2] = {nullptr, nullptr};  // boundary slot filled (sr_)
+  cudaEvent_t ev_fd0_ = nullptr;           // this turn's fc0 dgrad partial written (st_)
+  cudaEvent_t ev_ret_[2] = {nullptr, nullptr};     // slot's gradient return done (sr_)
+  cudaEvent_t ev_sr_ = nullptr;            // all of the step's sr_ work done
+  void wait_step();  // synchronise st_, polling the transports for asynchronous errors
+  void check_device_targets(const float* const* targets);
+  bool nccl_ = false;
+  bool targets_checked_ = false;  // this step's targets were validated on the host already
   cudaStream_t st_ = nullptr;
   cudaStream_t sc_ = nullptr;  // side stream: per-layer conv-gradient all-reduce
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
@@ -513,10 +541,16 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   if (cfg->transport == HP_TRANSPORT_NCCL) {
     if (cfg->rank < 0 || cfg->rank >= K_) usage_error("cluster.rank: out of range");
     comm_ = make_nccl_comm(K_, cfg->rank, cfg->nccl_id);
+    nccl_ = true;
   } else {
     comm_ = make_logical_comm(K_);
   }
+  comm_x_ = comm_->split();
+  comm_s_ = comm_->split();
   HP_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  HP_CUDA(cudaStreamCreateWithFlags(&sr_, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&ev_conv_, &ev_xready_[0], &ev_xready_[1], &ev_fd0_, &ev_ret_[0], &ev_ret_[1], &ev_sr_})
+    HP_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   HP_CUDA(cudaStreamCreateWithFlags(&sc_, cudaStreamNonBlocking));
   HP_CUDA(cudaEventCreate(&ev0_));
   HP_CUDA(cudaEventCreate(&ev1_));
@@ -642,14 +676,17 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     w.cgr = arena_.make<float>(conv_total_);
     w.cgr_local = K_ > 1 ? arena_.make<float>(conv_total_) : nullptr;
     w.cpt = std::is_same<TA, float>::value ? nullptr : arena_.make<TA>(conv_total_);
-    w.xb = arena_.make<TA>(n_ * A);
-    w.tb = arena_.make<float>(n_ * L_);
+    for (int s = 0; s < 2; ++s) {
+      w.xb[s] = arena_.make<TA>(n_ * A);
+      w.tb[s] = arena_.make<float>(n_ * L_);
+      w.fd0[s] = fcK_ > 1 ? arena_.make<float>(n_ * A) : nullptr;
+    }
     w.fx.assign(nf, nullptr);
     for (int l = 1; l < nf; ++l) w.fx[l] = arena_.make<TA>(g_.fg[l].Ip * ldn_);
     w.logits = arena_.make<float>(g_.fg.back().cmax * ldn_);
     for (int l = 0; l < nf; ++l) {
       w.fdz.push_back(arena_.make<TA>(g_.fg[l].cmax * ldn_));
-      w.fdpart.push_back(l > 0 ? arena_.make<float>(g_.fg[l].Ip * ldn_) : arena_.make<float>(n_ * A));
+      w.fdpart.push_back(l > 0 ? arena_.make<float>(g_.fg[l].Ip * ldn_) : w.fd0[0]);
       if (l > 0) comm_scratch = std::max(comm_scratch, static_cast<size_t>(g_.fg[l - 1].cmax * ldn_));
     }
     comm_scratch = std::max(comm_scratch, static_cast<size_t>(b_ * A));
@@ -663,6 +700,7 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     w.colsum_ws = arena_.make<float>(static_cast<long long>(colsum_ws));
   }
   comm_->reserve(comm_scratch * sizeof(float));
+  comm_x_->reserve(static_cast<size_t>(b_ * A) * sizeof(float));
   ev_layer_.resize(g_.cg.size());
   for (auto& e : ev_layer_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   ev_dz_.resize(g_.cg.size());
@@ -696,7 +734,14 @@ ClusterImpl<TA>::~ClusterImpl() {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (host_parts_) cudaFreeHost(host_parts_);
   if (host_bad_) cudaFreeHost(host_bad_);
+  if (sr_) cudaStreamSynchronize(sr_);
+  if (sc_) cudaStreamSynchronize(sc_);
+  comm_s_.reset();
+  comm_x_.reset();
   comm_.reset();
+  for (cudaEvent_t e : {ev_conv_, ev_xready_[0], ev_xready_[1], ev_fd0_, ev_ret_[0], ev_ret_[1], ev_sr_})
+    if (e) cudaEventDestroy(e);
+  if (sr_) cudaStreamDestroy(sr_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   for (auto e : ev_layer_) cudaEventDestroy(e);
@@ -950,14 +995,16 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     e.bias = w.fp + fc_b_off(l);
     e.bias_mode = 1;
     e.relu = f.relu;
-    const GemmOperand xin = l == 0 ? op(w.xb, 0, g_.A) : op(w.fx[l], 1, ldn_);
+    const GemmOperand xin = l == 0 ? op(w.xb[0], 0, g_.A) : op(w.fx[l], 1, ldn_);
     w.fc_fwd.push_back(plan(op(fwp, 0, f.Ip), xin, rows, n_, f.Ip, e));
+    if (l == 0) w.fc0_slot1[0] = plan(op(fwp, 0, f.Ip), op(w.xb[1], 0, g_.A), rows, n_, f.Ip, e);
     // wgrad: dW[rows][Ip] (+)= dZ[rows][n] . X[n][Ip]
     Epi eg;
     eg.c = w.fgr + fc_w_off(l);
     eg.ldc = f.Ip;
-    const GemmOperand xw = l == 0 ? op(w.xb, 1, g_.A) : op(w.fx[l], 0, ldn_);
+    const GemmOperand xw = l == 0 ? op(w.xb[0], 1, g_.A) : op(w.fx[l], 0, ldn_);
     w.fc_wgrad.push_back(plan(op(w.fdz[l], 0, ldn_), xw, rows, f.Ip, n_, eg, 2));
+    if (l == 0) w.fc0_slot1[1] = plan(op(w.fdz[l], 0, ldn_), op(w.xb[1], 1, g_.A), rows, f.Ip, n_, eg, 2);
     // dgrad
     if (l > 0) {
       Epi ed;
@@ -976,9 +1023,11 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       w.fc_dgrad.push_back(plan(op(fwp, 1, f.Ip), op(w.fdz[l], 1, ldn_), f.Ip, n_, rows, ed));
     } else {
       Epi ed;
-      ed.c = fcK_ == 1 ? w.gflat : w.fdpart[0];
+      ed.c = fcK_ == 1 ? w.gflat : w.fd0[0];
       ed.ldc = g_.A;
       w.fc_dgrad.push_back(plan(op(w.fdz[0], 1, ldn_), op(fwp, 1, f.Ip), n_, g_.A, rows, ed));
+      ed.c = fcK_ == 1 ? w.gflat : w.fd0[1];
+      w.fc0_slot1[2] = plan(op(w.fdz[0], 1, ldn_), op(fwp, 1, f.Ip), n_, g_.A, rows, ed);
     }
   }
 }
@@ -1149,7 +1198,7 @@ void ClusterImpl<TA>::rotate_all(Worker<TA>& w) {
 // Boundary exchange for turn j (exchange_activations / assemble_rows,
 // cluster.cpp:113-194), targets routed with their examples.
 template <class TA>
-void ClusterImpl<TA>::route_forward(int j) {
+void ClusterImpl<TA>::route_forward(int j, int slot, cudaStream_t st) {
   const int nl = comm_->nlocal();
   const long long A = g_.A;
   const size_t es = sizeof(TA);
@@ -1160,25 +1209,26 @@ void ClusterImpl<TA>::route_forward(int j) {
     const TA* top = stage_out_of(w_[i], g_.cg[last], last);
     sa[i] = top;
     stt[i] = w_[i].targets;
-    ra[i] = w_[i].xb;
-    rt[i] = w_[i].tb;
+    ra[i] = w_[i].xb[slot];
+    rt[i] = w_[i].tb[slot];
   }
+  Comm& cx = *comm_x_;
   if (dp_) {  // own examples only
     for (int i = 0; i < nl; ++i) {
-      HP_CUDA(cudaMemcpyAsync(ra[i], sa[i], b_ * A * es, cudaMemcpyDeviceToDevice, st_));
-      HP_CUDA(cudaMemcpyAsync(rt[i], stt[i], b_ * L_ * sizeof(float), cudaMemcpyDeviceToDevice, st_));
+      HP_CUDA(cudaMemcpyAsync(ra[i], sa[i], b_ * A * es, cudaMemcpyDeviceToDevice, st));
+      HP_CUDA(cudaMemcpyAsync(rt[i], stt[i], b_ * L_ * sizeof(float), cudaMemcpyDeviceToDevice, st));
     }
   } else if (scheme_ == HP_SCHEME_A) {
-    comm_->allgather(sa, ra, b_ * A * es, st_);
-    comm_->allgather(stt, rt, b_ * L_ * sizeof(float), st_);
+    cx.allgather(sa, ra, b_ * A * es, st);
+    cx.allgather(stt, rt, b_ * L_ * sizeof(float), st);
   } else if (scheme_ == HP_SCHEME_B) {
     for (int i = 0; i < nl; ++i)
       if (w_[i].gid == j) {
-        HP_CUDA(cudaMemcpyAsync(ra[i], sa[i], b_ * A * es, cudaMemcpyDeviceToDevice, st_));
-        HP_CUDA(cudaMemcpyAsync(rt[i], stt[i], b_ * L_ * sizeof(float), cudaMemcpyDeviceToDevice, st_));
+        HP_CUDA(cudaMemcpyAsync(ra[i], sa[i], b_ * A * es, cudaMemcpyDeviceToDevice, st));
+        HP_CUDA(cudaMemcpyAsync(rt[i], stt[i], b_ * L_ * sizeof(float), cudaMemcpyDeviceToDevice, st));
       }
-    comm_->broadcast(ra, b_ * A * es, j, st_);
-    comm_->broadcast(rt, b_ * L_ * sizeof(float), j, st_);
+    cx.broadcast(ra, b_ * A * es, j, st);
+    cx.broadcast(rt, b_ * L_ * sizeof(float), j, st);
   } else {
     const long long slice = b_ / K_;
     std::vector<const void*> sa2(nl), st2(nl);
@@ -1186,20 +1236,20 @@ void ClusterImpl<TA>::route_forward(int j) {
       sa2[i] = static_cast<const char*>(sa[i]) + j * slice * A * es;
       st2[i] = static_cast<const char*>(stt[i]) + j * slice * L_ * sizeof(float);
     }
-    comm_->allgather(sa2, ra, slice * A * es, st_);
-    comm_->allgather(st2, rt, slice * L_ * sizeof(float), st_);
+    cx.allgather(sa2, ra, slice * A * es, st);
+    cx.allgather(st2, rt, slice * L_ * sizeof(float), st);
   }
 }
 
 // Model-parallel fc forward, loss and backward for one sub-batch
 // (cluster.cpp:534-584).
 template <class TA>
-void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
+void ClusterImpl<TA>::fc_forward_backward(int j, bool beta, int slot) {
   const int nf = static_cast<int>(g_.fg.size());
   const int nl = comm_->nlocal();
   for (int l = 0; l < nf; ++l) {
     for (auto& w : w_) {
-      gemm(w.fc_fwd[l], "fc_fwd", l);
+      gemm(l == 0 && slot == 1 ? w.fc0_slot1[0] : w.fc_fwd[l], "fc_fwd", l);
     }
     if (l + 1 < nf && fcK_ > 1) {
       std::vector<void*> bufs(nl);
@@ -1212,15 +1262,16 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
   const FcGeom& fl = g_.fg.back();
   for (auto& w : w_) {
     const int rows = static_cast<int>(fl.c1[sid(w.gid)] - fl.c0[sid(w.gid)]);
-    launch_xent<TA>(w.logits, ldn_, w.tb, L_, static_cast<int>(fl.c0[sid(w.gid)]), rows, static_cast<int>(n_),
-                    w.fdz[nf - 1], ldn_, w.loss_parts + static_cast<long long>(j) * xblocks_, w.bad, st_);
+    launch_xent<TA>(w.logits, ldn_, w.tb[slot], L_, static_cast<int>(fl.c0[sid(w.gid)]), rows, static_cast<int>(n_),
+                    w.fdz[nf - 1], ldn_, w.loss_parts + static_cast<long long>(j) * xblocks_, w.bad,
+                    fl.relu ? 1 : 0, xblocks_, st_);
     ++launches_;
   }
   for (int li = nf - 1; li >= 0; --li) {
     const FcGeom& f = g_.fg[li];
     for (auto& w : w_) {
       const int rows = static_cast<int>(f.c1[sid(w.gid)] - f.c0[sid(w.gid)]);
-      GemmPlan pw = w.fc_wgrad[li];
+      GemmPlan pw = li == 0 && slot == 1 ? w.fc0_slot1[1] : w.fc_wgrad[li];
       pw.args.epi.beta = beta ? 1 : 0;
       if (fuse_sgd_) {
         // last (or, in variable mode, every) turn: the weight update runs in
@@ -1239,7 +1290,7 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
       // dgrad first: it must read this layer's weights before the (fused)
       // update of the wgrad epilogue -- turn j's dX uses pre-update weights
       // (cluster.cpp:562-601)
-      gemm(w.fc_dgrad[li], "fc_dgrad", li);
+      gemm(li == 0 && slot == 1 ? w.fc0_slot1[2] : w.fc_dgrad[li], "fc_dgrad", li);
       // The weight gradient (and the fused update) feeds nothing downstream in
       // this step: it runs on sf_, overlapping the rest of the backward
       // (serialised when profiling).
@@ -1264,33 +1315,35 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta) {
     }
   }
   HP_CUDA(cudaEventRecord(ev_fcw_, profile ? st_ : sf_));
+  HP_CUDA(cudaEventRecord(ev_fd0_, st_));
 }
 
 // return_gradients (cluster.cpp:196-269): each boundary-gradient row goes
 // back to the worker whose example it is, summed over the fc shards.
 template <class TA>
-void ClusterImpl<TA>::return_gradients(int j) {
+void ClusterImpl<TA>::return_gradients(int j, int slot, cudaStream_t st) {
   if (fcK_ == 1) return;  // dgrad wrote gflat directly
   const int nl = comm_->nlocal();
   const long long A = g_.A;
+  Comm& cx = *comm_x_;
   std::vector<const float*> send(nl);
-  for (int i = 0; i < nl; ++i) send[i] = w_[i].fdpart[0];
+  for (int i = 0; i < nl; ++i) send[i] = w_[i].fd0[slot];
   if (scheme_ == HP_SCHEME_A) {
     std::vector<void*> recv(nl);
     for (int i = 0; i < nl; ++i) recv[i] = w_[i].gflat;
     // own.scale(K): the big batch's 1/(K*b) scale -> per-worker mean (cluster.cpp:650-652)
-    comm_->reduce_scatter(send, recv, b_ * A, kF32, static_cast<float>(K_), st_);
+    cx.reduce_scatter(send, recv, b_ * A, kF32, static_cast<float>(K_), st);
   } else if (scheme_ == HP_SCHEME_B) {
     void* root_buf = nullptr;
     for (int i = 0; i < nl; ++i)
       if (w_[i].gid == j) root_buf = w_[i].gflat;
     if (!root_buf) root_buf = w_[0].gflat;  // ignored on non-root ranks
-    comm_->reduce(send, root_buf, b_ * A, j, kF32, 1.f, st_);
+    cx.reduce(send, root_buf, b_ * A, j, kF32, 1.f, st);
   } else {
     const long long slice = b_ / K_;
     std::vector<void*> recv(nl);
     for (int i = 0; i < nl; ++i) recv[i] = w_[i].gflat + j * slice * A;
-    comm_->reduce_scatter(send, recv, slice * A, kF32, 1.f, st_);
+    cx.reduce_scatter(send, recv, slice * A, kF32, 1.f, st);
   }
   launches_ += nl;
 }
@@ -1452,11 +1505,38 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
     }
   }
   for (auto& w : w_) conv_forward(w);
+  // The turns (cluster.cpp:507-614). The boundary exchange and the gradient
+  // return run on their own stream sr_ with double-buffered boundary slots:
+  // turn j+1's exchange is issued BEFORE turn j's FC compute and depends only
+  // on the conv tops and on turn j-1 having released its slot, so it overlaps
+  // turn j's FC GEMMs ((K-1)/K of the exchange is hidden);
+  // turn j's return overlaps turn j+1's FC compute the same way. The FC
+  // compute of consecutive turns stays serialised on st_: it reuses the FC
+  // activation buffers, and in variable mode turn j+1 reads the weights turn
+  // j updated (cluster.cpp:586-601).
+  cudaStream_t xs = profile ? st_ : sr_;  // serialised when profiling
+  HP_CUDA(cudaEventRecord(ev_conv_, st_));
+  HP_CUDA(cudaStreamWaitEvent(xs, ev_conv_, 0));
+  marker(100, xs);
+  route_forward(0, 0, xs);
+  marker(200, xs);
+  HP_CUDA(cudaEventRecord(ev_xready_[0], xs));
   for (int j = 0; j < num_sub_; ++j) {
+    const int slot = j & 1;
+    if (j + 1 < num_sub_) {
+      // slot (j+1)&1 was last read by turn j-1: its fc0 forward / xent on st_
+      // and its fc0 wgrad on sf_, all before turn j-1's ev_fcw_ record
+      if (j >= 1) HP_CUDA(cudaStreamWaitEvent(xs, ev_fcw_, 0));
+      marker(100 + j + 1, xs);
+      route_forward(j + 1, slot ^ 1, xs);
+      marker(200 + j + 1, xs);
+      HP_CUDA(cudaEventRecord(ev_xready_[slot ^ 1], xs));
+    }
     // turn j overwrites the FC activations / gradients the previous turn's
     // wgrads (sf_) read
     if (j > 0) HP_CUDA(cudaStreamWaitEvent(st_, ev_fcw_, 0));
-    route_forward(j);
+    HP_CUDA(cudaStreamWaitEvent(st_, ev_xready_[slot], 0));
+    if (j >= 2) HP_CUDA(cudaStreamWaitEvent(st_, ev_ret_[slot], 0));  // fd0[slot] returned by turn j-2
     // Fused FC weight update in the wgrad epilogue: every turn in variable
     // mode (cluster.cpp:586-601), the last turn of the accumulation in exact
     // mode (Σ_j grads × 1/num_sub, cluster.cpp:602-609, 680-696).
@@ -1465,8 +1545,14 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
     sgd_lr_ = variable_ ? fc_lr : lr;
     sgd_has_gscale_ = !variable_ && num_sub_ > 1;
     sgd_gscale_ = static_cast<float>(1.0 / static_cast<double>(num_sub_));
-    fc_forward_backward(j, !variable_ && j > 0);
-    return_gradients(j);
+    marker(300 + j, st_);
+    fc_forward_backward(j, !variable_ && j > 0, slot);
+    marker(400 + j, st_);
+    HP_CUDA(cudaStreamWaitEvent(xs, ev_fd0_, 0));
+    marker(500 + j, xs);
+    return_gradients(j, slot, xs);
+    marker(600 + j, xs);
+    HP_CUDA(cudaEventRecord(ev_ret_[slot], xs));
     weights_fused_ = fuse_sgd_;
     if (variable_) {  // per-sub-batch update (cluster.cpp:586-601)
       HP_CUDA(cudaStreamWaitEvent(st_, ev_fcw_, 0));
@@ -1474,11 +1560,13 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
     }
   }
   fuse_sgd_ = false;
+  HP_CUDA(cudaEventRecord(ev_sr_, xs));
+  HP_CUDA(cudaStreamWaitEvent(st_, ev_sr_, 0));  // every boundary gradient returned
   if (dp_ && K_ > 1) {  // pure DP: the FC gradients are all-reduced first (overlapping the conv backward)
     HP_CUDA(cudaStreamWaitEvent(sc_, ev_fcw_, 0));
     std::vector<float*> bufs(nl);
     for (int i = 0; i < nl; ++i) bufs[i] = w_[i].fgr;
-    comm_->allreduce_f32(bufs, static_cast<size_t>(fc_total_), sc_);
+    comm_s_->allreduce_f32(bufs, static_cast<size_t>(fc_total_), sc_);
     launches_ += 1;
   }
   // Conv backward; each layer's gradients (all local workers) are all-reduced
@@ -1495,7 +1583,7 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
       std::vector<float*> bufs(nl);
       for (int i = 0; i < nl; ++i) bufs[i] = w_[i].cgr + conv_k_off(l);
       const long long cnt = static_cast<long long>(g_.cg[l].F) * g_.cg[l].ldk + g_.cg[l].F;
-      comm_->allreduce_f32(bufs, static_cast<size_t>(cnt), sc_);
+      comm_s_->allreduce_f32(bufs, static_cast<size_t>(cnt), sc_);
       launches_ += 1;
     }
   }
@@ -1590,7 +1678,14 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
       }
       ps.valid = false;
       HP_CUDA(cudaStreamWaitEvent(st_, ps.ready, 0));
-      run_step(xb.data(), tb.data(), HP_MEM_DEVICE, hp, lr, out);
+      targets_checked_ = true;
+      try {
+        run_step(xb.data(), tb.data(), HP_MEM_DEVICE, hp, lr, out);
+      } catch (...) {
+        targets_checked_ = false;
+        throw;
+      }
+      targets_checked_ = false;
       HP_CUDA(cudaEventRecord(ps.used, st_));
       io_h2d = ps.bytes;
       return;
@@ -1600,9 +1695,13 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
   for (int i = 0; i < nl; ++i)
     if (!batches[i] || !targets[i])
       usage_error("run_step: expected " + num(nl) + " batches and targets, got a null entry");
+  // logistic_xent's DomainError (tensor.cpp:600-603), checked before any state
+  // change: the reference throws inside the loss, before the conv update (and,
+  // in exact mode, before any FC update), so no parameter may move.
   if (mem_kind == HP_MEM_HOST) {
-    // logistic_xent's DomainError (tensor.cpp:600-603), checked before any state change
     for (int i = 0; i < nl; ++i) check_targets(targets[i], b_ * L_);
+  } else if (!targets_checked_) {
+    check_device_targets(targets);
   }
 
   // CUDA graph of the whole step, keyed by everything baked into it (input
@@ -1677,7 +1776,7 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
     HP_CUDA(cudaEventRecord(ev1_, st_));
     if (graphable) graphs_[key];  // remember: capture on the next occurrence
   }
-  HP_CUDA(cudaStreamSynchronize(st_));
+  wait_step();
   float ms = 0.f;
   HP_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
   last_ms = ms;
@@ -1703,6 +1802,119 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
   out->fc_update_count = variable_ ? num_sub_ : 1;
   out->conv_update_count = 1;
   account(num_sub_, out);
+}
+
+template <class TA>
+void ClusterImpl<TA>::wait_step() {
+  if (!nccl_) {
+    HP_CUDA(cudaStreamSynchronize(st_));
+    return;
+  }
+  // NCCL: poll, so that a failed peer surfaces as HP_ERR_NCCL (communicators
+  // aborted) instead of a hang in cudaStreamSynchronize
+  for (int spin = 0;; ++spin) {
+    const cudaError_t r = cudaStreamQuery(st_);
+    if (r == cudaSuccess) break;
+    if (r != cudaErrorNotReady) HP_CUDA(r);
+    if (spin % 64 == 63) {
+      comm_->check_async();
+      comm_x_->check_async();
+      comm_s_->check_async();
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(spin < 256 ? 2 : 50));
+  }
+  comm_->check_async();
+  comm_x_->check_async();
+  comm_s_->check_async();
+}
+
+template <class TA>
+void ClusterImpl<TA>::check_device_targets(const float* const* targets) {
+  const int nl = comm_->nlocal();
+  for (int i = 0; i < nl; ++i) {
+    HP_CUDA(cudaMemsetAsync(w_[i].bad, 0, sizeof(int), st_));
+    launch_target_check(targets[i], b_ * L_, w_[i].bad, st_);
+    HP_CUDA(cudaMemcpyAsync(host_bad_ + i, w_[i].bad, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  }
+  HP_CUDA(cudaStreamSynchronize(st_));
+  for (int i = 0; i < nl; ++i) {
+    if (!host_bad_[i]) continue;
+    std::vector<float> h(static_cast<size_t>(b_ * L_));
+    HP_CUDA(cudaMemcpy(h.data(), targets[i], h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    check_targets(h.data(), b_ * L_);  // the reference's exact message
+    domain_error("logistic_xent: target outside [0,1]");
+  }
+}
+
+// Captures one step with marker kernels (never launched: nothing changes) and
+// reports marker-to-marker reachability in the graph's dependency DAG.
+template <class TA>
+void ClusterImpl<TA>::marker_graph(const float* const* batches, const float* const* targets, int mem_kind,
+                                   const hp_hyper& hp, double lr, std::vector<int>& tags,
+                                   std::vector<uint8_t>& reach) {
+  HP_CUDA(cudaStreamSynchronize(st_));
+  const bool pm = markers, pp = profile;
+  markers = true;
+  profile = false;
+  const int64_t keep_launches = launches_;
+  const int64_t kh = io_h2d, kd = io_d2h;
+  cudaGraph_t g = nullptr;
+  HP_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+  try {
+    enqueue(batches, targets, mem_kind, hp, lr);
+  } catch (...) {
+    cudaStreamEndCapture(st_, &g);
+    if (g) cudaGraphDestroy(g);
+    markers = pm;
+    profile = pp;
+    throw;
+  }
+  HP_CUDA(cudaStreamEndCapture(st_, &g));
+  markers = pm;
+  profile = pp;
+  launches_ = keep_launches;
+  io_h2d = kh;
+  io_d2h = kd;
+  size_t nn = 0, ne = 0;
+  HP_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  HP_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+  HP_CUDA(cudaGraphGetEdges(g, nullptr, nullptr, &ne));
+  std::vector<cudaGraphNode_t> from(ne), to(ne);
+  HP_CUDA(cudaGraphGetEdges(g, from.data(), to.data(), &ne));
+  std::map<cudaGraphNode_t, int> id;
+  for (size_t i = 0; i < nn; ++i) id[nodes[i]] = static_cast<int>(i);
+  std::vector<std::vector<int>> adj(nn);
+  for (size_t e = 0; e < ne; ++e) adj[id[from[e]]].push_back(id[to[e]]);
+  std::vector<int> mnode;
+  tags.clear();
+  for (size_t i = 0; i < nn; ++i) {
+    cudaGraphNodeType t;
+    HP_CUDA(cudaGraphNodeGetType(nodes[i], &t));
+    if (t != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams p{};
+    HP_CUDA(cudaGraphKernelNodeGetParams(nodes[i], &p));
+    if (!is_marker_kernel(p.func)) continue;
+    tags.push_back(*static_cast<int*>(p.kernelParams[0]));
+    mnode.push_back(static_cast<int>(i));
+  }
+  const size_t m = mnode.size();
+  reach.assign(m * m, 0);
+  for (size_t a = 0; a < m; ++a) {
+    std::vector<uint8_t> seen(nn, 0);
+    std::vector<int> stack{mnode[a]};
+    while (!stack.empty()) {
+      const int v = stack.back();
+      stack.pop_back();
+      for (int u : adj[v])
+        if (!seen[u]) {
+          seen[u] = 1;
+          stack.push_back(u);
+        }
+    }
+    for (size_t b = 0; b < m; ++b) reach[a * m + b] = seen[mnode[b]];
+  }
+  HP_CUDA(cudaGraphDestroy(g));
 }
 
 // Analytic byte counters and phase trace, exactly as the reference charges
@@ -1817,30 +2029,55 @@ void ClusterImpl<TA>::write_param(int worker, int which, int layer, const float*
   HP_CUDA(cudaStreamSynchronize(st_));
 }
 
+// gathered_model (cluster.cpp:417-437): conv from a local replica (identical
+// on every worker after the all-reduce), FC shards pasted back by column.
+// NCCL transport: a collective -- every rank calls it; the FC shard arenas
+// (same padded layout on every rank) are all-gathered over the library's
+// communicator and every rank unpacks the full model.
 template <class TA>
 void ClusterImpl<TA>::gather_model(float* const* ck, float* const* cb, float* const* fw,
                                    float* const* fb) {
   const int first = w_[0].gid;
   for (size_t l = 0; l < g_.cg.size(); ++l) {
-    if (first == 0) {
-      read_param(0, 0, static_cast<int>(l), ck[l], param_size(0, 0, static_cast<int>(l)));
-      read_param(0, 1, static_cast<int>(l), cb[l], param_size(0, 1, static_cast<int>(l)));
-    } else {
-      // every replica is bit-identical after the all-reduce; read ours
-      read_param(first, 0, static_cast<int>(l), ck[l], param_size(first, 0, static_cast<int>(l)));
-      read_param(first, 1, static_cast<int>(l), cb[l], param_size(first, 1, static_cast<int>(l)));
-    }
+    read_param(first, 0, static_cast<int>(l), ck[l], param_size(first, 0, static_cast<int>(l)));
+    read_param(first, 1, static_cast<int>(l), cb[l], param_size(first, 1, static_cast<int>(l)));
   }
-  if (comm_->nlocal() != K_) usage_error("gather_model: NCCL transport gathers via hp_cluster_read_param per rank");
+  std::vector<float> all;
+  if (nccl_ && fcK_ > 1) {
+    float* tmp = nullptr;
+    HP_CUDA(cudaStreamSynchronize(st_));
+    HP_CUDA(cudaMalloc(&tmp, static_cast<size_t>(fc_total_) * K_ * sizeof(float)));
+    try {
+      comm_->allgather(std::vector<const void*>{w_[0].fp}, std::vector<void*>{tmp},
+                       static_cast<size_t>(fc_total_) * sizeof(float), st_);
+      wait_step();
+      all.resize(static_cast<size_t>(fc_total_) * K_);
+      HP_CUDA(cudaMemcpy(all.data(), tmp, all.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    } catch (...) {
+      cudaFree(tmp);
+      throw;
+    }
+    HP_CUDA(cudaFree(tmp));
+  }
   for (size_t l = 0; l < g_.fg.size(); ++l) {
     const FcGeom& f = g_.fg[l];
     for (int k = 0; k < fcK_; ++k) {
       const long long ns = f.c1[k] - f.c0[k];
+      if (!all.empty()) {  // unpack worker k's all-gathered arena (layout as read_param)
+        const float* base = all.data() + static_cast<size_t>(k) * fc_total_ + fc_w_off(static_cast<int>(l));
+        for (long long i = 0; i < f.in; ++i) {
+          const long long col = fc_col(static_cast<int>(l), i);
+          for (long long o = 0; o < ns; ++o) fw[l][i * f.out + f.c0[k] + o] = base[o * f.Ip + col];
+        }
+        for (long long o = 0; o < ns; ++o) fb[l][f.c0[k] + o] = base[f.cmax * f.Ip + o];
+        continue;
+      }
+      const int wk = fcK_ == 1 ? first : k;  // DP: every worker holds the whole (replicated) FC stack
       std::vector<float> shard(static_cast<size_t>(f.in * ns));
-      read_param(k, 2, static_cast<int>(l), shard.data(), static_cast<int64_t>(shard.size()));
+      read_param(wk, 2, static_cast<int>(l), shard.data(), static_cast<int64_t>(shard.size()));
       for (long long i = 0; i < f.in; ++i)
         for (long long o = 0; o < ns; ++o) fw[l][i * f.out + f.c0[k] + o] = shard[i * ns + o];
-      read_param(k, 3, static_cast<int>(l), fb[l] + f.c0[k], ns);
+      read_param(wk, 3, static_cast<int>(l), fb[l] + f.c0[k], ns);
     }
   }
 }

@@ -78,6 +78,12 @@ class ClusterBase {
   // slot instead of copying on the compute stream (double buffering: the copy
   // of step i+1 overlaps the compute of step i).
   virtual void prefetch(const float* const* batches, const float* const* targets) = 0;
+  // Debug: capture one step (never executed) with marker kernels at the turn
+  // boundaries and report, for every pair of markers (tags[i], tags[j]),
+  // whether j is reachable from i in the captured graph's dependency DAG.
+  virtual void marker_graph(const float* const* batches, const float* const* targets, int mem_kind,
+                            const hp_hyper& hp, double lr, std::vector<int>& tags,
+                            std::vector<uint8_t>& reach) = 0;
 
   struct GemmProf {
     const char* tag;
@@ -86,6 +92,7 @@ class ClusterBase {
     float ms;
   };
   bool profile = false;            // bracket every GEMM with CUDA events
+  bool markers = false;            // debug: tagged 1-thread marker kernels at the turn boundaries
   bool use_graphs = true;          // replay the step as a captured CUDA graph
   bool fuse_fc_sgd = true;         // FC weight update in the wgrad GEMM epilogue
   bool use_shift = true;           // bf16 stride-1 convs via the flat-shift kernel (else TMA im2col)

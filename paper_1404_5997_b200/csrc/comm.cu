@@ -90,6 +90,7 @@ class LogicalComm final : public Comm {
     usage_error("allreduce_f64: not used with the logical transport");
   }
   void reserve(size_t) override {}
+  std::unique_ptr<Comm> split() override { return std::make_unique<LogicalComm>(K_); }
 
  private:
   int K_;
@@ -103,6 +104,7 @@ class NcclComm final : public Comm {
     std::memcpy(uid.internal, id, 128);
     HP_NCCL(ncclCommInitRank(&comm_, K, uid, rank));
   }
+  NcclComm(int K, int rank, ncclComm_t c) : K_(K), rank_(rank), comm_(c) {}
   ~NcclComm() override {
     if (comm_) ncclCommDestroy(comm_);
     if (scratch_) cudaFree(scratch_);
@@ -112,23 +114,28 @@ class NcclComm final : public Comm {
   int first() const override { return rank_; }
 
   void allgather_inplace(const std::vector<void*>& bufs, size_t bytes, cudaStream_t s) override {
+    live();
     char* b = static_cast<char*>(bufs[0]);
     HP_NCCL(ncclAllGather(b + rank_ * bytes, b, bytes, ncclUint8, comm_, s));
   }
   void allgather(const std::vector<const void*>& send, const std::vector<void*>& recv, size_t bytes,
                  cudaStream_t s) override {
+    live();
     HP_NCCL(ncclAllGather(send[0], recv[0], bytes, ncclUint8, comm_, s));
   }
   void broadcast(const std::vector<void*>& bufs, size_t bytes, int root, cudaStream_t s) override {
+    live();
     HP_NCCL(ncclBroadcast(bufs[0], bufs[0], bytes, ncclUint8, root, comm_, s));
   }
   void reduce_scatter(const std::vector<const float*>& send, const std::vector<void*>& recv,
                       size_t count, int out_type, float alpha, cudaStream_t s) override {
     if (out_type == 0 && alpha == 1.f) {
-      HP_NCCL(ncclReduceScatter(send[0], recv[0], count, ncclFloat32, ncclSum, comm_, s));
+      live();
+    HP_NCCL(ncclReduceScatter(send[0], recv[0], count, ncclFloat32, ncclSum, comm_, s));
       return;
     }
     need(count * sizeof(float));
+    live();
     HP_NCCL(ncclReduceScatter(send[0], scratch_, count, ncclFloat32, ncclSum, comm_, s));
     finish_f32(static_cast<const float*>(scratch_), recv[0], count, out_type, alpha, s);
   }
@@ -137,18 +144,40 @@ class NcclComm final : public Comm {
     const bool direct = out_type == 0 && alpha == 1.f;
     if (!direct) need(count * sizeof(float));
     void* dst = direct ? recv_root : scratch_;
+    live();
     HP_NCCL(ncclReduce(send[0], dst, count, ncclFloat32, ncclSum, root, comm_, s));
     if (!direct && rank_ == root) finish_f32(static_cast<const float*>(scratch_), recv_root, count, out_type, alpha, s);
   }
   void allreduce_f32(const std::vector<float*>& bufs, size_t count, cudaStream_t s) override {
+    live();
     HP_NCCL(ncclAllReduce(bufs[0], bufs[0], count, ncclFloat32, ncclSum, comm_, s));
   }
   void allreduce_f64(const std::vector<double*>& bufs, size_t count, cudaStream_t s) override {
+    live();
     HP_NCCL(ncclAllReduce(bufs[0], bufs[0], count, ncclFloat64, ncclSum, comm_, s));
   }
   void reserve(size_t bytes) override { need(bytes); }
+  std::unique_ptr<Comm> split() override {
+    ncclComm_t c = nullptr;
+    live();
+    HP_NCCL(ncclCommSplit(comm_, 0, rank_, &c, nullptr));
+    return std::make_unique<NcclComm>(K_, rank_, c);
+  }
+  void check_async() override {
+    if (!comm_) return;
+    ncclResult_t st = ncclSuccess;
+    HP_NCCL(ncclCommGetAsyncError(comm_, &st));
+    if (st == ncclSuccess || st == ncclInProgress) return;
+    ncclCommAbort(comm_);
+    comm_ = nullptr;
+    throw Error(HP_ERR_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(st) +
+                                 " (communicator aborted)");
+  }
 
  private:
+  void live() const {
+    if (!comm_) throw Error(HP_ERR_NCCL, "NCCL communicator was aborted after an asynchronous error");
+  }
   void need(size_t bytes) {
     if (bytes <= scratch_bytes_) return;
     if (scratch_) {

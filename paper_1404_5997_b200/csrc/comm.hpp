@@ -47,6 +47,13 @@ class Comm {
   virtual void allreduce_f64(const std::vector<double*>& bufs, size_t count, cudaStream_t s) = 0;
   // Scratch reservation for fp32 staging (NCCL reduce -> cast).
   virtual void reserve(size_t bytes) = 0;
+  // A transport over the same workers for use on another stream (NCCL: a new
+  // communicator from ncclCommSplit, so concurrent streams never share one).
+  virtual std::unique_ptr<Comm> split() = 0;
+  // Throws HP_ERR_NCCL if the transport saw an asynchronous failure (a peer
+  // died, a network error); the communicator is aborted first so pending
+  // collectives return instead of hanging.
+  virtual void check_async() {}
 };
 
 std::unique_ptr<Comm> make_logical_comm(int K);

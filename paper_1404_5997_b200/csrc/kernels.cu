@@ -356,7 +356,7 @@ template <class TO>
 __global__ void xent_kernel(const float* __restrict__ z, long long ldzin,
                             const float* __restrict__ t, int L, int c0, int Ls, int n,
                             TO* __restrict__ dz, long long ldz, double* __restrict__ partial,
-                            int* __restrict__ bad) {
+                            int* __restrict__ bad, int relu_mask) {
   __shared__ double red[256];
   const long long total = static_cast<long long>(Ls) * n;
   const double inv_b = 1.0 / static_cast<double>(n);
@@ -369,7 +369,12 @@ __global__ void xent_kernel(const float* __restrict__ z, long long ldzin,
     const double softplus_neg = fmax(-zi, 0.0) + log1p(exp(-fabs(zi)));
     loss += softplus_neg + (1.0 - ti) * zi;
     const double sigma = zi >= 0.0 ? 1.0 / (1.0 + exp(-zi)) : exp(zi) / (1.0 + exp(zi));
-    dz[o * ldz + i] = from_f<TO>(__double2float_rn(inv_b * (sigma - ti)));
+    float g = __double2float_rn(inv_b * (sigma - ti));
+    // last fc layer with ReLU: relu_backward on the logit grad (model.cpp:302,
+    // cluster.cpp:569); the stored logits are post-ReLU, > 0 exactly when the
+    // pre-activation is
+    if (relu_mask && !(zi > 0.0)) g = 0.f;
+    dz[o * ldz + i] = from_f<TO>(g);
   }
   red[threadIdx.x] = loss;
   __syncthreads();
@@ -1640,6 +1645,27 @@ void launch_rowsum(const T* x, int R, int n, long long ldx, float* out, int beta
   rowsum_kernel<T><<<static_cast<int>(blocks), threads, 0, st>>>(x, R, n, ldx, out, beta);
 }
 
+__global__ void marker_kernel(int tag) {
+  if (tag < 0) asm volatile("trap;");  // never: keeps the argument live
+}
+
+void launch_marker(int tag, cudaStream_t st) { marker_kernel<<<1, 1, 0, st>>>(tag); }
+bool is_marker_kernel(const void* func) { return func == reinterpret_cast<const void*>(&marker_kernel); }
+
+__global__ void target_check_kernel(const float* __restrict__ t, long long n, int* __restrict__ bad) {
+  int b = 0;
+  GRID_STRIDE(e, n) {
+    const float v = t[e];
+    b |= (v < 0.f) | (v > 1.f);  // the reference's test: NaN passes
+  }
+  if (__syncthreads_or(b) && threadIdx.x == 0) atomicExch(bad, 1);
+}
+
+void launch_target_check(const float* t, long long n, int* bad, cudaStream_t st) {
+  const int blocks = static_cast<int>(std::min<long long>(std::max<long long>(1, (n + 255) / 256), 1184));
+  target_check_kernel<<<blocks, 256, 0, st>>>(t, n, bad);
+}
+
 int xent_blocks(int Ls, int n) {
   const long long total = static_cast<long long>(Ls) * n;
   return static_cast<int>(std::min<long long>(std::max<long long>(1, (total + 255) / 256), 512));
@@ -1647,9 +1673,10 @@ int xent_blocks(int Ls, int n) {
 
 template <class TO>
 int launch_xent(const float* z, long long ldzin, const float* t, int L, int c0, int Ls, int n,
-                TO* dz, long long ldz, double* partial, int* bad_target, cudaStream_t st) {
-  const int blocks = xent_blocks(Ls, n);
-  xent_kernel<TO><<<blocks, 256, 0, st>>>(z, ldzin, t, L, c0, Ls, n, dz, ldz, partial, bad_target);
+                TO* dz, long long ldz, double* partial, int* bad_target, int relu_mask, int blocks,
+                cudaStream_t st) {
+  if (blocks <= 0) blocks = xent_blocks(Ls, n);
+  xent_kernel<TO><<<blocks, 256, 0, st>>>(z, ldzin, t, L, c0, Ls, n, dz, ldz, partial, bad_target, relu_mask);
   return blocks;
 }
 
@@ -1718,7 +1745,7 @@ void launch_scale(float* x, long long n, float s, cudaStream_t st) {
                                  cudaStream_t);                                                \
   template void launch_rowsum<T>(const T*, int, int, long long, float*, int, cudaStream_t);    \
   template int launch_xent<T>(const float*, long long, const float*, int, int, int, int, T*,   \
-                              long long, double*, int*, cudaStream_t);                         \
+                              long long, double*, int*, int, int, cudaStream_t);               \
   template void launch_cast<T>(const float*, T*, long long, cudaStream_t);                     \
   template void launch_sum_k<T>(PtrList, int, T*, long long, float, cudaStream_t);
 

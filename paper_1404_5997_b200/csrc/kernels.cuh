@@ -63,11 +63,22 @@ void launch_rowsum(const T* x, int R, int n, long long ldx, float* out, int beta
 
 // Logistic cross-entropy on a feature-major logit shard z [Ls][n] (fp32):
 // targets t [n][L] (columns c0..c0+Ls), grad -> dz [Ls][ldz], per-block
-// double loss partials -> partial[nblocks]. Returns nblocks.
+// double loss partials -> partial[nblocks]. relu_mask: zero the gradient where
+// the (post-ReLU) logit is not > 0. blocks <= 0: xent_blocks(Ls, n); callers
+// that combine partials across ranks pass one count for all (every entry of
+// partial[0..blocks) is rewritten). Returns nblocks.
 template <class TO>
 int launch_xent(const float* z, long long ldzin, const float* t, int L, int c0, int Ls, int n,
-                TO* dz, long long ldz, double* partial, int* bad_target, cudaStream_t st);
+                TO* dz, long long ldz, double* partial, int* bad_target, int relu_mask, int blocks,
+                cudaStream_t st);
 int xent_blocks(int Ls, int n);
+
+// Debug marker: a 1-thread kernel carrying an integer tag (graph-structure tests).
+void launch_marker(int tag, cudaStream_t st);
+bool is_marker_kernel(const void* func);
+// Device-resident targets: bad |= any t outside [0,1] (logistic_xent's
+// DomainError, tensor.cpp:600-603, checked before a step changes any state).
+void launch_target_check(const float* t, long long n, int* bad, cudaStream_t st);
 
 // Momentum SGD over a list of tensors (optimizer.cpp:19-31, float storage:
 // scalars rounded to float once, four separate rounded passes, no FMA).

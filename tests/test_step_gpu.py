@@ -15,6 +15,8 @@ init many pre-activations sit within fp32 error of zero, and conv1's gradient
 collects every flip below it -- bounding the accumulation chains did not move
 the worst case.)
 Integer outputs (byte counters, trace, update counts) must be identical."""
+import os
+
 import numpy as np
 import pytest
 
@@ -63,6 +65,8 @@ def compare(spec, K, scheme, var, math, b, steps=2, lr=0.05, wscale=1.0, seed=1,
         for which in range(8):
             for l in range(nl(which)):
                 e = rel_err(g.param(w, which, l), o.param(w, which, l))
+                if os.environ.get("HP_TOL_REPORT"):
+                    print(f"TOL {math.name} K={K} {scheme} var={var} b={b} ws={wscale} w{w} p{which} l{l} {e:.3e}")
                 # biases start at zero, so (like momenta) they are pure gradient history
                 assert e <= (mt if (which >= 4 or which in (1, 3)) else wt), (w, which, l, e)
     # replica consistency: conv replicas identical across workers (unless the
@@ -102,6 +106,37 @@ def test_active_relus():
 def test_alexnet_small_batch(K, scheme, var):
     """AlexNet-1col (LRN, overlapping pool, floor-mode conv1) at b=2 per worker in 3xTF32."""
     compare(hp.alexnet_1col(), K, scheme, var, hp.MathMode.F32X3, 2, steps=1, lr=0.01)
+
+
+def test_last_fc_layer_relu():
+    """A spec whose LAST fc layer has a ReLU: the logit gradient is masked by
+    relu_backward(pre, grad) (model.cpp:302, cluster.cpp:569) before the fc
+    backward and the boundary return."""
+    spec = hp.tiny_cnn()
+    spec.fc_layers[-1].relu = True
+    compare(spec, 2, "C", False, hp.MathMode.F32X3, 8, steps=2, lr=0.001, wscale=30.0)
+    compare(spec, 1, "B", False, hp.MathMode.BF16, 16, steps=1)
+
+
+def test_device_target_domain_error_before_any_update():
+    """logistic_xent's DomainError (tensor.cpp:600-603) for DEVICE-resident
+    targets is raised before the step changes any parameter or momentum."""
+    import torch
+    spec = hp.tiny_cnn()
+    g = hp.Cluster(spec, hp.ClusterConfig(workers=2, per_worker_batch=8, scheme=hp.Scheme.B, seed=1,
+                                          math_mode=hp.MathMode.BF16))
+    xs, ts = zip(*[hp.synthetic_batch(spec, 8, worker=w) for w in range(2)])
+    dx = [torch.from_numpy(x).cuda() for x in xs]
+    dt = [torch.from_numpy(t).cuda() for t in ts]
+    g.run_step(dx, dt, hp.HyperParams(lr=0.01))
+    before = [g.param(w, which, l) for w in range(2) for which in range(8) for l in range(3 if (which & 3) < 2 else 2)]
+    bad = dt[1].clone()
+    bad[3, 2] = 1.5
+    with pytest.raises(hp.DomainError, match="outside"):
+        g.run_step(dx, [dt[0], bad], hp.HyperParams(lr=0.01))
+    after = [g.param(w, which, l) for w in range(2) for which in range(8) for l in range(3 if (which & 3) < 2 else 2)]
+    assert all(np.array_equal(a, b) for a, b in zip(before, after))
+    g.run_step(dx, dt, hp.HyperParams(lr=0.01))  # still usable
 
 
 def test_alexnet_bf16_loss_and_io():
