@@ -202,6 +202,17 @@ enum { HP_P_CONV_K = 0, HP_P_CONV_B = 1, HP_P_FC_W = 2, HP_P_FC_B = 3, HP_P_MOME
 HP_API int64_t hp_cluster_param_size(const hp_cluster* c, int worker, int which, int layer);
 HP_API int hp_cluster_read_param(hp_cluster* c, int worker, int which, int layer, float* dst,
                                  int64_t n);
+/* Parity / debug (no reference counterpart): the last step's discrete forward
+ * decisions in the reference layouts -- kind 0: conv layer ReLU mask, uint8
+ * [b][F][OH][OW]; kind 1: conv pool argmax, int32 [b][F][PH][PW] as the index
+ * h*OW+w in the conv output plane; kind 2: fc layer ReLU mask, uint8 [n][out]
+ * of the last sub-batch (K == 1 or scheme DP). dst NULL: returns the count.
+ * Returns the element count, or -1 (hp_last_error). */
+/* Debug capture of every turn's fc ReLU masks for hp_cluster_debug_decisions
+ * (synchronises inside the step; disables graph replay while on). */
+HP_API int hp_cluster_set_debug_capture(hp_cluster* c, int on);
+HP_API int64_t hp_cluster_debug_decisions(hp_cluster* c, int worker, int kind, int layer, void* dst,
+                                          int64_t n);
 HP_API int hp_cluster_write_param(hp_cluster* c, int worker, int which, int layer,
                                   const float* src, int64_t n);
 
@@ -335,7 +346,9 @@ HP_API int hp_kernel_conv_shift(const void* x, int64_t rows, int C, int R, int S
  * a [B][H][W][C] conv output (post-ReLU), y [B][PH][PW][C] with
  * PH = (H - pk) / ps + 1, widx [B][PH][PW][C] uint8 window offset r*pk + q of
  * the FIRST maximum in row-major window order (strict >, NaN wins), gy fp32
- * [B][PH][PW][C], dz [B][H][W][C] (x ReLU mask of a when relu_mask).
+ * [B][PH][PW][C], dz [B][H][W][C] (x ReLU mask of a when relu_mask); bias_grad (optional,
+ * LRN stages) [C] = channel sums of the stored dz (model.cpp:184-202), fused into the
+ * backward like the step does.
  * LRN (Krizhevsky 2012): b_c = a_c (k + alpha sum_{|i-c|<=n/2} a_i^2)^-beta,
  * alpha NOT divided by n. lrn_size 0: max-pool only. */
 HP_API int hp_kernel_lrn_pool_fwd(int math, const void* a, int B, int H, int W, int C, int lrn_size,
@@ -343,7 +356,7 @@ HP_API int hp_kernel_lrn_pool_fwd(int math, const void* a, int B, int H, int W, 
                                   uint8_t* widx, void* stream);
 HP_API int hp_kernel_lrn_pool_bwd(int math, const float* gy, const uint8_t* widx, const void* a, int B,
                                   int H, int W, int C, int lrn_size, float alpha, float beta, float k,
-                                  int pk, int ps, int relu_mask, void* dz, void* stream);
+                                  int pk, int ps, int relu_mask, void* dz, float* bias_grad, void* stream);
 /* The step's momentum SGD (momentum_update, optimizer.cpp:19-31) on one fp32
  * tensor: g *= gscale (if has_gscale), delta = mu*delta; delta += -lr*g;
  * delta += -lr*wd*w; w += delta -- four rounded passes, scalars formed in

@@ -114,6 +114,10 @@ def _load_oracle() -> C.CDLL:
     lib.or_cluster_read_param.argtypes = [P, C.c_int, C.c_int, C.c_int, _D, C.c_int64]
     lib.or_cluster_write_param.argtypes = [P, C.c_int, C.c_int, C.c_int, _D, C.c_int64]
     lib.or_cluster_set_skip_sync_broadcast.argtypes = [P, C.c_int]
+    lib.or_cluster_set_storage_rounding.argtypes = [P, C.c_int]
+    lib.or_cluster_force_decisions.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64]
+    lib.or_cluster_decision_stats.argtypes = [P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64),
+                                              C.POINTER(C.c_double)]
     lib.or_set_threads.argtypes = [C.c_int]
     lib.or_gaussian_fill.argtypes = [C.c_uint64, _D, C.c_int64]
     lib.or_uniform_u64.argtypes = [C.c_uint64, C.POINTER(C.c_uint64), C.c_int64]
@@ -322,6 +326,27 @@ class _ClusterBase:
 
 
 class OracleCluster(_ClusterBase):
+    def set_storage_rounding(self, mode: str):
+        """'double' (the reference restatement) or 'bf16' (round stored tensors
+        where the B200 bf16 math mode stores them; see hpsim_oracle.c)."""
+        self._check(self.lib.or_cluster_set_storage_rounding(self.h, {"double": 0, "bf16": 1}[mode]))
+
+    def force_decisions(self, worker: int, kind: int, layer: int, values):
+        """Replay these ReLU masks (kind 0 conv, 2 fc; uint8) / pool argmax
+        (kind 1, int32 plane index) in the next step; None clears."""
+        if values is None:
+            self._check(self.lib.or_cluster_force_decisions(self.h, worker, kind, layer, None, 0))
+            return
+        v = np.ascontiguousarray(values, dtype=np.int32 if kind == 1 else np.uint8)
+        self._check(self.lib.or_cluster_force_decisions(self.h, worker, kind, layer, v.ctypes.data, v.size))
+
+    def decision_stats(self, worker: int, kind: int, layer: int):
+        """(mismatches, max_gap) of the last step's forced decisions against the
+        oracle's own: ReLU -- |z| / rms(z); pool -- relative value gap."""
+        m, g = C.c_int64(0), C.c_double(0.0)
+        self._check(self.lib.or_cluster_decision_stats(self.h, worker, kind, layer, C.byref(m), C.byref(g)))
+        return m.value, g.value
+
     prefix = "or_"
 
     @staticmethod

@@ -498,6 +498,8 @@ typedef struct {
 
 typedef struct {
   double* input;
+  int input_owned;
+  const uint8_t** mask; /* forced ReLU masks (NULL: pre > 0) */
   double** pre;
   double** act;
   double** lrn;
@@ -514,10 +516,24 @@ struct or_cluster {
   geom_t* g;
   int64_t flat;
   int skip_sync_broadcast;
+  int storage_bf16; /* test-only: round stored tensors to bf16 where the B200 bf16 path stores them */
+  /* test-only decision replay (or_cluster_force_decisions): per worker x conv
+   * layer ReLU masks / pool argmax, per fc layer ReLU masks (K == 1); and the
+   * last step's disagreement statistics against the oracle's own decisions */
+  uint8_t** f_cmask;
+  int32_t** f_pidx;
+  uint8_t** f_fmask;
+  int64_t* st_mis;  /* [3][K * max(nc, nf)] */
+  double* st_gap;
   worker_t* w;
   or_trace_event* events;
   int n_events, cap_events;
 };
+
+static int stat_layers(const or_cluster* c) {
+  const int a = c->spec.n_conv, b = c->cfg.workers * c->spec.n_fc;
+  return a > b ? a : b;
+}
 
 static double* dalloc(int64_t n) { return calloc((size_t)(n > 0 ? n : 1), sizeof(double)); }
 
@@ -642,6 +658,14 @@ or_cluster* or_cluster_create(const or_model_spec* spec, const or_cluster_config
   free(mw);
   c->cap_events = 8 + 2 * K;
   c->events = calloc((size_t)c->cap_events, sizeof(or_trace_event));
+  {
+    const int L = nc > K * nf ? nc : K * nf;
+    c->f_cmask = calloc((size_t)(K * nc + 1), sizeof(uint8_t*));
+    c->f_pidx = calloc((size_t)(K * nc + 1), sizeof(int32_t*));
+    c->f_fmask = calloc((size_t)(K * nf + 1), sizeof(uint8_t*));
+    c->st_mis = calloc((size_t)(3 * K * L + 1), sizeof(int64_t));
+    c->st_gap = calloc((size_t)(3 * K * L + 1), sizeof(double));
+  }
   return c;
 }
 
@@ -657,19 +681,183 @@ void or_cluster_destroy(or_cluster* c) {
     }
     free(w->conv); free(w->conv_m); free(w->fc); free(w->fc_m);
   }
+  for (int t = 0; t < c->cfg.workers * c->spec.n_conv; ++t) { free(c->f_cmask[t]); free(c->f_pidx[t]); }
+  for (int t = 0; t < c->cfg.workers * c->spec.n_fc; ++t) free(c->f_fmask[t]);
+  free(c->f_cmask); free(c->f_pidx); free(c->f_fmask); free(c->st_mis); free(c->st_gap);
   free(c->w); free(c->conv); free(c->fc); free(c->g); free(c->events);
   free(c);
 }
 
 void or_cluster_set_skip_sync_broadcast(or_cluster* c, int v) { c->skip_sync_broadcast = v; }
 
+/* ---- bf16 storage emulation (test infrastructure; not in the reference) ----
+ * The B200 bf16 math mode keeps fp32 master weights / momenta and accumulates
+ * every GEMM, LRN and reduction in fp32, but STORES operands as bf16: the input
+ * batch, the conv / fc operand copies of the weights, every post-ReLU
+ * activation and stage output (pooled LRN output), the logit gradient, the
+ * fc-internal input gradients and every conv-layer dz / dgrad output. The
+ * logits and the boundary gradient stay fp32. A forward decision taken on a
+ * bf16-rounded value (pool argmax, ReLU mask) differs from the all-double one
+ * whenever rounding reorders or ties two window values, which changes whole
+ * gradient entries, not just their low bits. With storage_bf16 set, this
+ * oracle rounds (to nearest even, via float like the GPU's fp32 -> bf16 store)
+ * at exactly those points and computes everything else in double, so the GPU
+ * step is compared with the same decisions; the pure-double mode stays the
+ * reference restatement. */
+static double q_bf16(double v) {
+  float f = (float)v;
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) {
+    u += 0x7fffu + ((u >> 16) & 1u);
+    u &= 0xffff0000u;
+  }
+  memcpy(&f, &u, 4);
+  return (double)f;
+}
+static void q_arr(const or_cluster* c, double* a, int64_t n) {
+  if (c->storage_bf16 != 1) return;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) a[i] = q_bf16(a[i]);
+}
+static void f_arr(const or_cluster* c, double* a, int64_t n) { /* fp32 storage */
+  if (c->storage_bf16 != 1) return;
+  for (int64_t i = 0; i < n; ++i) a[i] = (double)(float)a[i];
+}
+/* Operand copy (bf16 mode) or the array itself. Caller frees when != src. */
+static const double* q_copy(const or_cluster* c, const double* src, int64_t n) {
+  if (c->storage_bf16 != 1) return src;
+  double* d = dalloc(n);
+  memcpy(d, src, sizeof(double) * (size_t)n);
+  q_arr(c, d, n);
+  return d;
+}
+/* bf16 mode: the LRN scale in fp32 with the B200 kernels' pinned arithmetic
+ * (lrn_pool_fwd_kernel: s = fma(a_j, a_j, s) over the window in ascending
+ * channel order from s = 0, d = fma(alpha, s, k)), then b = a * d^-beta in
+ * double. The scale decides pool ties: at AlexNet's k = 2 most pixels have
+ * alpha * sum below half an fp32 ulp of 2, so d is exactly 2.0f on the GPU and
+ * two pixels with the same bf16 activation tie (first maximum wins), where the
+ * all-double scale would break the tie. */
+static void lrn_forward_f32_scale(const double* a, int64_t B, int64_t C, int64_t HW, int n, double alpha,
+                                  double beta, double k, double* b) {
+  const int lo = n / 2, hi = (n - 1) / 2;
+  const float af = (float)alpha, kf = (float)k;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int64_t bb = 0; bb < B; ++bb)
+    for (int64_t c = 0; c < C; ++c) {
+      const int64_t j0 = c - lo < 0 ? 0 : c - lo;
+      const int64_t j1 = c + hi > C - 1 ? C - 1 : c + hi;
+      for (int64_t p = 0; p < HW; ++p) {
+        float sum = 0.f;
+        for (int64_t j = j0; j <= j1; ++j) {
+          const float v = (float)a[(bb * C + j) * HW + p];
+          sum = fmaf(v, v, sum);
+        }
+        const float d = fmaf(af, sum, kf);
+        const int64_t at = (bb * C + c) * HW + p;
+        b[at] = a[at] * pow((double)d, -beta);
+      }
+    }
+}
+
+/* Decision replay (test infrastructure): the next run_step takes these ReLU
+ * masks / pool argmax instead of its own (kind 0: conv ReLU mask uint8
+ * [b][F][OH][OW]; kind 1: conv pool argmax int32 [b][F][PH][PW], plane index;
+ * kind 2: fc ReLU mask uint8 [n][out] of turn j, layer = j * n_fc + l, the
+ * gathered activation's mask -- worker i uses its shard's columns) and records, per forced
+ * decision set, how many differ from its own and by how much. src NULL clears. */
+int or_cluster_force_decisions(or_cluster* c, int worker, int kind, int layer, const void* src, int64_t n) {
+  const int nc = c->spec.n_conv, nf = c->spec.n_fc, K = c->cfg.workers;
+  const int64_t b = c->cfg.per_worker_batch;
+  if (worker < 0 || worker >= K || kind < 0 || kind > 2) return fail(4, "force_decisions: bad worker/kind");
+  if (kind < 2 && (layer < 0 || layer >= nc)) return fail(4, "force_decisions: bad conv layer");
+  const int nsub = c->cfg.scheme == 0 ? 1 : K;
+  if (kind == 2 && (layer < 0 || layer >= nsub * nf)) return fail(4, "force_decisions: bad fc turn/layer");
+  int64_t want;
+  void** slot;
+  size_t es;
+  if (kind == 0) {
+    want = b * c->g[layer].f * c->g[layer].ho * c->g[layer].wo;
+    slot = (void**)&c->f_cmask[worker * nc + layer];
+    es = 1;
+  } else if (kind == 1) {
+    if (c->conv[layer].pool_kernel <= 0) return fail(4, "force_decisions: layer has no pool");
+    want = b * c->g[layer].f * c->g[layer].hp * c->g[layer].wp;
+    slot = (void**)&c->f_pidx[worker * nc + layer];
+    es = 4;
+  } else {
+    const int64_t rows = c->cfg.scheme == 0 ? (int64_t)K * b : b;
+    want = rows * c->fc[layer % nf].out_dim;
+    slot = (void**)&c->f_fmask[layer];
+    es = 1;
+  }
+  free(*slot);
+  *slot = NULL;
+  if (!src) return 0;
+  if (n != want) return fail(2, "force_decisions: size %lld, expected %lld", (long long)n, (long long)want);
+  *slot = malloc((size_t)n * es);
+  memcpy(*slot, src, (size_t)n * es);
+  return 0;
+}
+
+int or_cluster_decision_stats(const or_cluster* c, int worker, int kind, int layer, int64_t* mismatches,
+                              double* max_gap) {
+  const int L = stat_layers(c);
+  if (worker < 0 || worker >= c->cfg.workers || kind < 0 || kind > 2 || layer < 0 || layer >= L)
+    return fail(4, "decision_stats: bad worker/kind/layer");
+  const int64_t at = ((int64_t)kind * c->cfg.workers + worker) * L + layer;
+  *mismatches = c->st_mis[at];
+  *max_gap = c->st_gap[at];
+  return 0;
+}
+
+int or_cluster_set_storage_rounding(or_cluster* c, int mode) {
+  if (mode < 0 || mode > 1) return fail(4, "storage rounding: mode must be 0 (double) or 1 (bf16)");
+  c->storage_bf16 = mode;
+  return 0;
+}
+
 /* conv_forward (model.cpp:225-243) + add_channel_bias (:166-182) + relu
  * (tensor.cpp:556-564), then the LRN / pool superset. */
+static void decision_stat(const or_cluster* c, int kind, int worker, int layer, int64_t mis, double gap) {
+  const int L = stat_layers(c);
+  const int64_t at = ((int64_t)kind * c->cfg.workers + worker) * L + layer;
+  c->st_mis[at] = mis;
+  c->st_gap[at] = gap;
+}
+
+/* ReLU with an optional forced mask: out = mask ? z : 0; records the
+ * disagreements with the oracle's own decision (z > 0) and the largest |z| /
+ * rms(z) among them. */
+static void relu_forced(const or_cluster* c, int kind, int worker, int layer, const double* z, double* a,
+                        int64_t n, const uint8_t* mask) {
+  if (!mask) {
+    for (int64_t i = 0; i < n; ++i) a[i] = z[i] > 0.0 ? z[i] : 0.0;
+    return;
+  }
+  int64_t mis = 0;
+  double gap = 0.0, ss = 0.0;
+  for (int64_t i = 0; i < n; ++i) ss += z[i] * z[i];
+  const double rms = sqrt(ss / (double)(n > 0 ? n : 1));
+  for (int64_t i = 0; i < n; ++i) {
+    a[i] = mask[i] ? z[i] : 0.0;
+    if ((mask[i] != 0) != (z[i] > 0.0)) {
+      ++mis;
+      const double g = fabs(z[i]) / (rms > 0.0 ? rms : 1.0);
+      if (g > gap) gap = g;
+    }
+  }
+  decision_stat(c, kind, worker, layer, mis, gap);
+}
+
 static void conv_forward(const or_cluster* c, const conv_p* p, const double* batch, int64_t B,
-                         cache_t* cache) {
+                         cache_t* cache, int worker) {
   const int nc = c->spec.n_conv;
-  cache->input = (double*)batch;
+  cache->input = (double*)q_copy(c, batch, B * c->g[0].c * c->g[0].h * c->g[0].w);
+  cache->input_owned = cache->input != batch;
   cache->pre = calloc((size_t)nc, sizeof(double*));
+  cache->mask = calloc((size_t)nc, sizeof(uint8_t*));
   cache->act = calloc((size_t)nc, sizeof(double*));
   cache->lrn = calloc((size_t)nc, sizeof(double*));
   cache->lrn_d = calloc((size_t)nc, sizeof(double*));
@@ -681,14 +869,23 @@ static void conv_forward(const or_cluster* c, const conv_p* p, const double* bat
     const geom_t* g = &c->g[l];
     const int64_t hw = g->ho * g->wo, n = B * g->f * hw;
     double* z = dalloc(n);
-    conv_fwd(x, p[l].k, z, B, g->c, g->h, g->w, g->f, L->kernel, L->kernel, g->ho, g->wo,
+    const double* kq = q_copy(c, p[l].k, conv_k_size(c, l));
+    conv_fwd(l == 0 ? cache->input : x, kq, z, B, g->c, g->h, g->w, g->f, L->kernel, L->kernel, g->ho, g->wo,
              L->stride, L->pad);
+    if (kq != p[l].k) free((void*)kq);
     for (int64_t b = 0; b < B; ++b)
       for (int64_t f = 0; f < g->f; ++f)
         for (int64_t q = 0; q < hw; ++q) z[(b * g->f + f) * hw + q] += p[l].b[f];
     cache->pre[l] = z;
     double* a = dalloc(n);
-    for (int64_t i = 0; i < n; ++i) a[i] = L->relu ? (z[i] > 0.0 ? z[i] : 0.0) : z[i];
+    const uint8_t* fm = c->f_cmask[worker * nc + l];
+    if (L->relu) {
+      relu_forced(c, 0, worker, l, z, a, n, fm);
+      cache->mask[l] = fm;
+    } else {
+      for (int64_t i = 0; i < n; ++i) a[i] = z[i];
+    }
+    q_arr(c, a, n);
     cache->act[l] = a;
     const double* out = a;
     if (L->lrn_size > 0) {
@@ -696,6 +893,9 @@ static void conv_forward(const or_cluster* c, const conv_p* p, const double* bat
       cache->lrn_d[l] = dalloc(n);
       or_lrn_forward(a, B, g->f, hw, L->lrn_size, L->lrn_alpha, L->lrn_beta, L->lrn_k,
                      cache->lrn[l], cache->lrn_d[l]);
+      if (c->storage_bf16 == 1)
+        lrn_forward_f32_scale(a, B, g->f, hw, L->lrn_size, L->lrn_alpha, L->lrn_beta, L->lrn_k,
+                              cache->lrn[l]);
       out = cache->lrn[l];
     }
     if (L->pool_kernel > 0) {
@@ -704,7 +904,30 @@ static void conv_forward(const or_cluster* c, const conv_p* p, const double* bat
       cache->pidx[l] = calloc((size_t)np, sizeof(int32_t));
       or_maxpool_forward(out, B, g->f, g->ho, g->wo, L->pool_kernel, L->pool_stride,
                          cache->pool[l], cache->pidx[l]);
+      const int32_t* fi = c->f_pidx[worker * nc + l];
+      if (fi) { /* replay the forced argmax; record the near-tie gaps where it differs */
+        int64_t mis = 0;
+        double gap = 0.0, ss = 0.0;
+        const int64_t plane = g->ho * g->wo, pp = g->hp * g->wp;
+        for (int64_t t = 0; t < n; ++t) ss += out[t] * out[t];
+        const double rms = sqrt(ss / (double)(n > 0 ? n : 1));
+        for (int64_t o = 0; o < np; ++o) {
+          const double* xp = out + (o / pp) * plane;
+          const double own = cache->pool[l][o], forced = xp[fi[o]];
+          if (fi[o] != cache->pidx[l][o]) { /* gap: the value given up, in units of the layer's rms */
+            ++mis;
+            const double gg = fabs(own - forced) / (rms > 0.0 ? rms : 1.0);
+            if (gg > gap) gap = gg;
+          }
+          cache->pool[l][o] = forced;
+          cache->pidx[l][o] = fi[o];
+        }
+        decision_stat(c, 1, worker, l, mis, gap);
+      }
       out = cache->pool[l];
+      q_arr(c, cache->pool[l], np);
+    } else if (L->lrn_size > 0) {
+      q_arr(c, cache->lrn[l], n);
     }
     x = out;
   }
@@ -721,8 +944,9 @@ static void cache_free(const or_cluster* c, cache_t* cache) {
     free(cache->pre[l]); free(cache->act[l]); free(cache->lrn[l]); free(cache->lrn_d[l]);
     free(cache->pool[l]); free(cache->pidx[l]);
   }
-  free(cache->pre); free(cache->act); free(cache->lrn); free(cache->lrn_d); free(cache->pool);
+  free(cache->pre); free((void*)cache->mask); free(cache->act); free(cache->lrn); free(cache->lrn_d); free(cache->pool);
   free(cache->pidx);
+  if (cache->input_owned) free(cache->input);
 }
 
 /* conv_backward_from_flat (model.cpp:259-283) + channel_sums (:184-202) +
@@ -751,17 +975,23 @@ static void conv_backward(const or_cluster* c, const conv_p* p, const cache_t* c
       free(grad);
       grad = ga;
     }
-    if (L->relu)
+    if (L->relu) {
+      const uint8_t* fm = cache->mask[l];
       for (int64_t i = 0; i < n; ++i)
-        if (!(cache->pre[l][i] > 0.0)) grad[i] = 0.0;
+        if (fm ? !fm[i] : !(cache->pre[l][i] > 0.0)) grad[i] = 0.0;
+    }
+    q_arr(c, grad, n);
     for (int64_t f = 0; f < g->f; ++f) grads[l].b[f] = 0.0;
     for (int64_t b = 0; b < B; ++b)
       for (int64_t f = 0; f < g->f; ++f)
         for (int64_t q = 0; q < hw; ++q) grads[l].b[f] += grad[(b * g->f + f) * hw + q];
     const double* input = l == 0 ? cache->input : stage_out(c, cache, l - 1);
     double* gx = l > 0 ? dalloc(B * g->c * g->h * g->w) : NULL;
-    conv_bwd(input, p[l].k, grad, gx, grads[l].k, B, g->c, g->h, g->w, g->f, L->kernel, L->kernel,
+    const double* kq = q_copy(c, p[l].k, conv_k_size(c, l));
+    conv_bwd(input, kq, grad, gx, grads[l].k, B, g->c, g->h, g->w, g->f, L->kernel, L->kernel,
              g->ho, g->wo, L->stride, L->pad);
+    if (kq != p[l].k) free((void*)kq);
+    if (gx) q_arr(c, gx, B * g->c * g->h * g->w);
     free(grad);
     grad = gx;
   }
@@ -801,7 +1031,7 @@ int or_cluster_run_step(or_cluster* c, const double* const* batches, const doubl
   } while (0)
 
   cache_t* caches = calloc((size_t)K, sizeof(cache_t));
-  for (int i = 0; i < K; ++i) conv_forward(c, c->w[i].conv, batches[i], b, &caches[i]);
+  for (int i = 0; i < K; ++i) conv_forward(c, c->w[i].conv, batches[i], b, &caches[i], i);
 
   /* exchange_activations / assemble_rows (cluster.cpp:113-194) */
   const int num_sub = scheme == 0 ? 1 : K;
@@ -883,24 +1113,42 @@ int or_cluster_run_step(or_cluster* c, const double* const* batches, const doubl
         const fc_p* p = &c->w[i].fc[l];
         const int64_t ns = p->c1 - p->c0;
         double* z = dalloc(n * ns);
-        or_matmul(x, p->w, z, n, in, ns); /* fc_affine model.cpp:219-223 */
+        const double* wq = q_copy(c, p->w, in * ns);
+        or_matmul(x, wq, z, n, in, ns); /* fc_affine model.cpp:219-223 */
+        if (wq != p->w) free((void*)wq);
         for (int64_t r = 0; r < n; ++r)
           for (int64_t q = 0; q < ns; ++q) z[r * ns + q] += p->b[q];
-        for (int64_t r = 0; r < n; ++r)
-          for (int64_t q = 0; q < ns; ++q) {
-            const double v = z[r * ns + q];
-            gathered[r * outd + p->c0 + q] = c->fc[l].relu ? (v > 0.0 ? v : 0.0) : v;
-          }
+        const uint8_t* fg = c->f_fmask[j * nf + l];
+        if (fg && c->fc[l].relu) { /* forced: this shard's columns of the turn's gathered mask */
+          uint8_t* fm = malloc((size_t)(n * ns));
+          for (int64_t r = 0; r < n; ++r)
+            for (int64_t q = 0; q < ns; ++q) fm[r * ns + q] = fg[r * outd + p->c0 + q];
+          double* a = dalloc(n * ns);
+          relu_forced(c, 2, i, j * nf + l, z, a, n * ns, fm);
+          for (int64_t r = 0; r < n; ++r)
+            for (int64_t q = 0; q < ns; ++q) gathered[r * outd + p->c0 + q] = a[r * ns + q];
+          free(a);
+          free(fm);
+        } else {
+          for (int64_t r = 0; r < n; ++r)
+            for (int64_t q = 0; q < ns; ++q) {
+              const double v = z[r * ns + q];
+              gathered[r * outd + p->c0 + q] = c->fc[l].relu ? (v > 0.0 ? v : 0.0) : v;
+            }
+        }
         pre[l * K + i] = z;
         const int64_t shard_bytes = n * ns * elt;
         CHARGE(i, 2, (K - 1) * shard_bytes, n * (outd - ns) * elt);
       }
+      if (l + 1 < nf) q_arr(c, gathered, n * outd);
+      else f_arr(c, gathered, n * outd);
       x = gathered;
     }
     double* grad = dalloc(n * L);
     double loss = 0.0;
     int rc = or_logistic_xent(x, sub_t[j], n, L, grad, &loss);
     if (rc) return rc; /* DomainError propagates (test-only oracle: leaks on error) */
+    q_arr(c, grad, n * L);
     loss_weighted += loss * (double)n;
     free(x);
     /* fc backward (cluster.cpp:562-584) */
@@ -913,15 +1161,20 @@ int or_cluster_run_step(or_cluster* c, const double* const* batches, const doubl
         double* dz = dalloc(n * ns);
         for (int64_t r = 0; r < n; ++r)
           for (int64_t q = 0; q < ns; ++q) dz[r * ns + q] = grad[r * outd + p->c0 + q];
-        if (c->fc[li].relu)
-          for (int64_t t = 0; t < n * ns; ++t)
-            if (!(pre[li * K + i][t] > 0.0)) dz[t] = 0.0;
+        if (c->fc[li].relu) {
+          const uint8_t* fg = c->f_fmask[j * nf + li];
+          for (int64_t r = 0; r < n; ++r)
+            for (int64_t q = 0; q < ns; ++q)
+              if (fg ? !fg[r * outd + p->c0 + q] : !(pre[li * K + i][r * ns + q] > 0.0)) dz[r * ns + q] = 0.0;
+        }
         or_matmul_tn(layer_in[li], dz, pass[i][li].w, n, in, ns);
         for (int64_t q = 0; q < ns; ++q) pass[i][li].b[q] = 0.0;
         for (int64_t r = 0; r < n; ++r)
           for (int64_t q = 0; q < ns; ++q) pass[i][li].b[q] += dz[r * ns + q];
         double* partial = dalloc(n * in);
-        or_matmul_nt(dz, p->w, partial, n, ns, in);
+        const double* wq = q_copy(c, p->w, in * ns);
+        or_matmul_nt(dz, wq, partial, n, ns, in);
+        if (wq != p->w) free((void*)wq);
         for (int64_t t = 0; t < n * in; ++t) dx[t] += partial[t];
         free(partial);
         free(dz);
@@ -931,6 +1184,8 @@ int or_cluster_run_step(or_cluster* c, const double* const* batches, const doubl
         }
       }
       free(grad);
+      if (li > 0) q_arr(c, dx, n * in);
+      else f_arr(c, dx, n * in);
       grad = dx;
     }
     boundary[j] = grad;

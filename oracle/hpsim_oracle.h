@@ -96,6 +96,13 @@ int or_cluster_read_param(const or_cluster* c, int worker, int which, int layer,
 int or_cluster_write_param(or_cluster* c, int worker, int which, int layer, const double* src,
                            int64_t n);
 void or_cluster_set_skip_sync_broadcast(or_cluster* c, int v);
+/* test-only: 0 = all double (the reference restatement), 1 = bf16 storage
+ * emulation of the B200 bf16 math mode (see hpsim_oracle.c). */
+int or_cluster_set_storage_rounding(or_cluster* c, int mode);
+/* test-only decision replay: see hpsim_oracle.c */
+int or_cluster_force_decisions(or_cluster* c, int worker, int kind, int layer, const void* src, int64_t n);
+int or_cluster_decision_stats(const or_cluster* c, int worker, int kind, int layer, int64_t* mismatches,
+                              double* max_gap);
 void or_set_threads(int n);
 
 /* Primitives (tensor.cpp / model.cpp restated, plus the extensions). */

@@ -140,7 +140,7 @@ def _load() -> C.CDLL:
         "hp_kernel_lrn_pool_fwd": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float,
                                     C.c_float, C.c_float, C.c_int, C.c_int, P, P, P], C.c_int),
         "hp_kernel_lrn_pool_bwd": ([C.c_int, P, P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float,
-                                    C.c_float, C.c_float, C.c_int, C.c_int, C.c_int, P, P], C.c_int),
+                                    C.c_float, C.c_float, C.c_int, C.c_int, C.c_int, P, P, P], C.c_int),
         "hp_kernel_sgd": ([P, P, P, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_float, C.c_int, P, P],
                           C.c_int),
         "hp_kernel_conv_dgrad": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int,
@@ -158,6 +158,8 @@ def _load() -> C.CDLL:
         "hp_cluster_param_size": ([P, C.c_int, C.c_int, C.c_int], C.c_int64),
         "hp_cluster_read_param": ([P, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64], C.c_int),
         "hp_cluster_write_param": ([P, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64], C.c_int),
+        "hp_cluster_debug_decisions": ([P, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64], C.c_int64),
+        "hp_cluster_set_debug_capture": ([P, C.c_int], C.c_int),
         "hp_cluster_gather_model": ([P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                      C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)], C.c_int),
         "hp_cluster_set_skip_sync_broadcast": ([P, C.c_int], C.c_int),

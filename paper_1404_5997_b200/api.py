@@ -379,6 +379,23 @@ class Cluster:
         _check(lib.hp_cluster_read_param(self._h, worker, which, layer, out.ctypes.data, n))
         return out
 
+    def decisions(self, worker: int, kind: int, layer: int) -> np.ndarray:
+        """The last step's discrete forward decisions (parity tests): kind 0 conv
+        ReLU mask uint8 [b*F*OH*OW], 1 conv pool argmax int32 (plane index h*OW+w),
+        2 fc ReLU mask uint8 [n*out] with layer = turn * n_fc + fc layer (earlier
+        turns need set_debug_capture(True)). See hp_cluster_debug_decisions."""
+        n = lib.hp_cluster_debug_decisions(self._h, worker, kind, layer, None, 0)
+        if n < 0:
+            _check(4)
+        out = np.empty(n, dtype=np.int32 if kind == 1 else np.uint8)
+        if lib.hp_cluster_debug_decisions(self._h, worker, kind, layer, out.ctypes.data, n) < 0:
+            _check(4)
+        return out
+
+    def set_debug_capture(self, on: bool) -> None:
+        """Keep every turn's fc ReLU masks for decisions() (no graph replay while on)."""
+        _check(lib.hp_cluster_set_debug_capture(self._h, int(bool(on))))
+
     def write_param(self, worker: int, which: int, layer: int, values) -> None:
         v = np.ascontiguousarray(values, dtype=np.float32).ravel()
         _check(lib.hp_cluster_write_param(self._h, worker, which, layer, v.ctypes.data, v.size))

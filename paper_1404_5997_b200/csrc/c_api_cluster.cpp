@@ -117,6 +117,15 @@ HP_API int hp_cluster_read_param(hp_cluster* c, int worker, int which, int layer
   });
 }
 
+HP_API int64_t hp_cluster_debug_decisions(hp_cluster* c, int worker, int kind, int layer, void* dst, int64_t n) {
+  int64_t r = -1;
+  const int rc = guarded_c([&] {
+    need(c, "hp_cluster_debug_decisions");
+    r = c->impl->read_decisions(worker, kind, layer, dst, n);
+  });
+  return rc == 0 ? r : -1;
+}
+
 HP_API int hp_cluster_write_param(hp_cluster* c, int worker, int which, int layer, const float* src,
                                   int64_t n) {
   return guarded_c([&] {
@@ -185,6 +194,10 @@ HP_API double hp_cluster_last_gemm_flops(const hp_cluster* c) {
 
 HP_API int hp_cluster_set_graphs(hp_cluster* c, int on) {
   return guarded_c([&] { need(c, "hp_cluster_set_graphs").impl->use_graphs = on != 0; });
+}
+
+HP_API int hp_cluster_set_debug_capture(hp_cluster* c, int on) {
+  return guarded_c([&] { need(c, "hp_cluster_set_debug_capture").impl->capture_fc = on != 0; });
 }
 
 HP_API int hp_cluster_set_fuse_fc_sgd(hp_cluster* c, int on) {

@@ -205,7 +205,7 @@ HP_API int hp_kernel_lrn_pool_fwd(int math, const void* a, int B, int H, int W, 
 
 HP_API int hp_kernel_lrn_pool_bwd(int math, const float* gy, const uint8_t* widx, const void* a, int B, int H, int W,
                                   int C, int lrn_size, float alpha, float beta, float k, int pk, int ps, int relu_mask,
-                                  void* dz, void* stream) {
+                                  void* dz, float* bias_grad, void* stream) {
   return guarded([&] {
     if (!gy || !widx || !a || !dz) usage_error("lrn_pool_bwd: null pointer");
     if (pk < 1 || ps < 1 || pk > 16 || H < pk || W < pk) config_error("lrn_pool_bwd: bad pool window");
@@ -213,12 +213,31 @@ HP_API int hp_kernel_lrn_pool_bwd(int math, const float* gy, const uint8_t* widx
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     auto go = [&](auto tag) {
       using T = decltype(tag);
-      if (lrn_size > 0)
-        launch_lrn_pool_bwd<T>(gy, widx, static_cast<const T*>(a), static_cast<T*>(dz), B, H, W, C, lrn_size, alpha,
-                               beta, k, pk, ps, PH, PW, relu_mask, st);
-      else
+      if (lrn_size > 0) {
+        // the step's launch: the row-streaming kernel writes the bias partials too
+        const int rows = lrn_pool_bwd_partial_rows(B, H, W, C, PH, PW, sizeof(T));
+        float* part = nullptr;
+        if (rows > 0) HP_CUDA(cudaMalloc(&part, sizeof(float) * static_cast<size_t>(rows) * C));
+        const int got = launch_lrn_pool_bwd<T>(gy, widx, static_cast<const T*>(a), static_cast<T*>(dz), B, H, W, C,
+                                               lrn_size, alpha, beta, k, pk, ps, PH, PW, relu_mask, st, OutLayout{},
+                                               part);
+        if (bias_grad && got > 0) launch_bias_partials_reduce(part, got, C, bias_grad, st);
+        if (part) {
+          HP_CUDA(cudaStreamSynchronize(st));
+          HP_CUDA(cudaFree(part));
+        }
+        if (bias_grad && got == 0) {
+          float* ws = nullptr;
+          const long long M = static_cast<long long>(B) * H * W;
+          HP_CUDA(cudaMalloc(&ws, sizeof(float) * colsum_ws_floats(M, C)));
+          launch_colsum<T>(static_cast<const T*>(dz), M, C, C, bias_grad, ws, st);
+          HP_CUDA(cudaStreamSynchronize(st));
+          HP_CUDA(cudaFree(ws));
+        }
+      } else {
         launch_maxpool_bwd_w<T, T>(gy, widx, static_cast<T*>(dz), relu_mask ? static_cast<const T*>(a) : nullptr, B,
                                    H, W, C, pk, ps, PH, PW, st);
+      }
     };
     if (math == HP_MATH_BF16) go(bf16{});
     else go(float{});

@@ -348,6 +348,7 @@ struct Worker {
   double* loss_parts = nullptr;
   int* bad = nullptr;
   float* colsum_ws = nullptr;
+  float* bias_part = nullptr;  // LRN+pool backward's per-block bias-gradient partial rows
   // GEMM plans
   std::vector<GemmPlan> conv_fwd, conv_wgrad, conv_dgrad, fc_fwd, fc_wgrad, fc_dgrad;
   GemmPlan fc0_slot1[3];  // fc layer 0 {fwd, wgrad, dgrad} over boundary slot 1 (slot 0: the vectors)
@@ -374,6 +375,10 @@ class ClusterImpl final : public ClusterBase {
                     std::vector<uint8_t>& reach) override;
   int64_t param_size(int worker, int which, int layer) const override;
   void read_param(int worker, int which, int layer, float* dst, int64_t n) override;
+  int64_t read_decisions(int worker, int kind, int layer, void* dst, int64_t n) override;
+  void fc_mask_now(int l, std::vector<uint8_t>& m);
+  void capture_fc_masks(int j);
+  std::vector<std::vector<uint8_t>> cap_fc_;  // debug capture: [turn * nf + layer] -> [n][out]
   void write_param(int worker, int which, int layer, const float* src, int64_t n) override;
   void gather_model(float* const* ck, float* const* cb, float* const* fw, float* const* fb) override;
 
@@ -449,6 +454,7 @@ class ClusterImpl final : public ClusterBase {
   cudaStream_t sr_ = nullptr;  // boundary exchange + gradient return (overlaps the FC compute)
   cudaEvent_t ev_conv_ = nullptr;          // conv tops + targets final on st_
   cudaEvent_t ev_xready_[2] = {nullptr, nullptr};  // boundary slot filled (sr_)
+  std::vector<long long> bias_off_;        // per conv layer: offset of its bias partial rows in bias_part
   cudaEvent_t ev_fd0_ = nullptr;           // this turn's fc0 dgrad partial written (st_)
   cudaEvent_t ev_ret_[2] = {nullptr, nullptr};     // slot's gradient return done (sr_)
   cudaEvent_t ev_sr_ = nullptr;            // all of the step's sr_ work done
@@ -632,8 +638,16 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   xblocks_ = 0;
   for (int l = 0; l < nf; ++l) (void)l;
   xblocks_ = xent_blocks(static_cast<int>(g_.fg.back().cmax), static_cast<int>(n_));
-  size_t colsum_ws = 0;
-  for (const auto& cg : g_.cg) colsum_ws = std::max(colsum_ws, colsum_ws_floats(cg.Pq, cg.F));
+  size_t colsum_ws = 0, bias_part = 0;
+  bias_off_.assign(nc, 0);
+  for (int l = 0; l < nc; ++l) {  // one region per layer: layer l's reduce (side stream) may trail layer l-1's write
+    const ConvGeom& cg = g_.cg[l];
+    colsum_ws = std::max(colsum_ws, colsum_ws_floats(cg.Pq, cg.F));
+    bias_off_[l] = static_cast<long long>(bias_part);
+    if (cg.lrn_n > 0 && cg.pk > 0)
+      bias_part += static_cast<size_t>(lrn_pool_bwd_partial_rows(static_cast<int>(b_), cg.OH, cg.OW, cg.F, cg.PH,
+                                                                 cg.PW, sizeof(TA))) * cg.F;
+  }
   size_t comm_scratch = 0;
   for (int i = 0; i < nl; ++i) {
     Worker<TA>& w = w_[i];
@@ -698,6 +712,7 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     w.loss_parts = arena_.make<double>(static_cast<long long>(num_sub_) * xblocks_);
     w.bad = arena_.make<int>(1);
     w.colsum_ws = arena_.make<float>(static_cast<long long>(colsum_ws));
+    if (bias_part) w.bias_part = arena_.make<float>(static_cast<long long>(bias_part));
   }
   comm_->reserve(comm_scratch * sizeof(float));
   comm_x_->reserve(static_cast<size_t>(b_ * A) * sizeof(float));
@@ -1257,6 +1272,7 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta, int slot) {
       comm_->allgather_inplace(bufs, g_.fg[l].cmax * ldn_ * sizeof(TA), st_);
     }
   }
+  if (capture_fc) capture_fc_masks(j);
   // logistic cross-entropy on each worker's logit shard (no logit gather:
   // output units are independent).
   const FcGeom& fl = g_.fg.back();
@@ -1360,9 +1376,11 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
   const TA* mask = c.relu ? w.act[l] : nullptr;
   const int B = static_cast<int>(b_);
   const OutLayout zl = c.in_q ? OutLayout{c.Hq, c.Wq, c.pad} : OutLayout{};  // dz layout
+  int bias_rows = 0;  // > 0: the LRN+pool backward also wrote the bias-gradient partials
   if (c.pk > 0 && c.lrn_n > 0) {
-    launch_lrn_pool_bwd<TA>(cs.gout, w.widx[l], w.act[l], w.dz[l], B, c.OH, c.OW, c.F, c.lrn_n, c.lrn_alpha,
-                            c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, c.relu ? 1 : 0, st_, zl);
+    bias_rows = launch_lrn_pool_bwd<TA>(cs.gout, w.widx[l], w.act[l], w.dz[l], B, c.OH, c.OW, c.F, c.lrn_n,
+                                        c.lrn_alpha, c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, c.relu ? 1 : 0,
+                                        st_, zl, w.bias_part ? w.bias_part + bias_off_[l] : nullptr);
     ++launches_;
   } else if (c.pk > 0) {
     launch_maxpool_bwd_w<TA, TA>(cs.gout, w.widx[l], w.dz[l], mask, B, c.OH, c.OW, c.F, c.pk, c.ps, c.PH,
@@ -1386,8 +1404,13 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
     HP_CUDA(cudaStreamWaitEvent(ws, ev_dz_[l], 0));
   }
   // bias grad = channel sums of dz (model.cpp:184-202)
-  launch_colsum<TA>(w.dz[l], c.Pq, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, ws);
-  launches_ += 2;
+  if (bias_rows > 0) {
+    launch_bias_partials_reduce(w.bias_part + bias_off_[l], bias_rows, c.F, w.cgr + conv_b_off(l), ws);
+    ++launches_;
+  } else {
+    launch_colsum<TA>(w.dz[l], c.Pq, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, ws);
+    launches_ += 2;
+  }
   gemm(w.conv_wgrad[l], "conv_wgrad", l, ws);
   if (c.s2d) {
     launch_s2d_wgrad_gather(w.dwz, w.cgr + conv_k_off(l), c.ldk, c.F, c.C, c.R, c.S, c.stride, c.Rq, c.Cz, ws);
@@ -1725,7 +1748,7 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
   key.mem = mem_kind;
   key.scal = {lr, hp.momentum, hp.weight_decay, hp.has_fc_partial_lr ? hp.fc_partial_lr : -1.0};
   key.mem += skip_sync_broadcast ? 16 : 0;  // a different step (fix-up launches)
-  const bool graphable = use_graphs && !profile && pinned;
+  const bool graphable = use_graphs && !profile && !capture_fc && pinned;
   GraphEntry* ge = nullptr;
   if (graphable) {
     auto it = graphs_.find(key);
@@ -1981,6 +2004,107 @@ void ClusterImpl<TA>::read_param(int worker, int which, int layer, float* dst, i
     const long long col = fc_col(layer, i);
     for (long long o = 0; o < ns; ++o) dst[i * ns + o] = h[o * f.Ip + col];
   }
+}
+
+// The last step's discrete forward decisions in the reference layouts (the
+// parity tests replay them in the oracle, hpsim_oracle.c or_cluster_force_decisions):
+//   kind 0: conv layer ReLU mask, uint8 [b][F][OH][OW] (stored activation > 0)
+//   kind 1: conv layer pool argmax, int32 [b][F][PH][PW], index h*OW + w in the
+//           conv output plane (or_maxpool_forward's convention)
+//   kind 2: fc layer ReLU mask, uint8 [n][out] of the last sub-batch (one fc
+//           shard: K == 1 or the DP scheme)
+// dst == nullptr: returns the element count only.
+template <class TA>
+int64_t ClusterImpl<TA>::read_decisions(int worker, int kind, int layer, void* dst, int64_t n) {
+  Worker<TA>& w = local(worker);
+  const int nc = static_cast<int>(g_.cg.size()), nf = static_cast<int>(g_.fg.size());
+  auto pos = [](const TA& v) { return static_cast<float>(v) > 0.f; };
+  if (kind == 0 || kind == 1) {
+    if (layer < 0 || layer >= nc) usage_error("read_decisions: bad conv layer");
+    const ConvGeom& c = g_.cg[layer];
+    if (kind == 1 && c.pk == 0) usage_error("read_decisions: layer has no pool");
+    const int64_t want = kind == 0 ? b_ * c.F * c.OH * c.OW : b_ * c.F * c.PH * c.PW;
+    if (!dst) return want;
+    if (n != want) dimension_error("read_decisions: size " + num(n) + ", expected " + num(want));
+    HP_CUDA(cudaStreamSynchronize(st_));
+    if (kind == 0) {
+      const bool next_q = layer + 1 < nc && g_.cg[layer + 1].in_q && c.pk == 0 && c.lrn_n == 0;
+      const long long H = next_q ? g_.cg[layer + 1].Hq : c.OH, W = next_q ? g_.cg[layer + 1].Wq : c.OW;
+      const long long p = next_q ? g_.cg[layer + 1].pad : 0;
+      std::vector<TA> h(static_cast<size_t>((next_q ? g_.cg[layer + 1].Pq : c.P) * c.F));
+      HP_CUDA(cudaMemcpy(h.data(), w.act[layer], h.size() * sizeof(TA), cudaMemcpyDeviceToHost));
+      uint8_t* m = static_cast<uint8_t*>(dst);
+      for (long long b = 0; b < b_; ++b)
+        for (long long f = 0; f < c.F; ++f)
+          for (long long y = 0; y < c.OH; ++y)
+            for (long long x = 0; x < c.OW; ++x)
+              m[((b * c.F + f) * c.OH + y) * c.OW + x] = pos(h[((b * H + y + p) * W + x + p) * c.F + f]) ? 1 : 0;
+    } else {
+      std::vector<uint8_t> h(static_cast<size_t>(c.PP * c.F));
+      HP_CUDA(cudaMemcpy(h.data(), w.widx[layer], h.size(), cudaMemcpyDeviceToHost));
+      int32_t* o = static_cast<int32_t*>(dst);
+      for (long long b = 0; b < b_; ++b)
+        for (long long f = 0; f < c.F; ++f)
+          for (long long y = 0; y < c.PH; ++y)
+            for (long long x = 0; x < c.PW; ++x) {
+              const int off = h[((b * c.PH + y) * c.PW + x) * c.F + f];
+              o[((b * c.F + f) * c.PH + y) * c.PW + x] =
+                  static_cast<int32_t>((y * c.ps + off / c.pk) * c.OW + x * c.ps + off % c.pk);
+            }
+    }
+    return want;
+  }
+  // kind 2: layer = turn * nf + fc layer
+  if (kind != 2 || layer < 0 || layer >= num_sub_ * nf) usage_error("read_decisions: bad kind/layer");
+  const int j = layer / nf, l = layer % nf;
+  const int64_t want = n_ * g_.fg[l].out;
+  if (!dst) return want;
+  if (n != want) dimension_error("read_decisions: size " + num(n) + ", expected " + num(want));
+  if (static_cast<int>(cap_fc_.size()) == num_sub_ * nf && !cap_fc_[layer].empty()) {
+    std::memcpy(dst, cap_fc_[layer].data(), static_cast<size_t>(want));
+    return want;
+  }
+  if (j != num_sub_ - 1) usage_error("read_decisions: earlier turns need hp_cluster_set_debug_capture");
+  HP_CUDA(cudaStreamSynchronize(st_));
+  std::vector<uint8_t> m;
+  fc_mask_now(l, m);
+  std::memcpy(dst, m.data(), static_cast<size_t>(want));
+  return want;
+}
+
+// The current turn's fc layer-l ReLU mask [n][out] (gathered activation > 0;
+// the last layer: the local workers' logit shards). Stream must be idle.
+template <class TA>
+void ClusterImpl<TA>::fc_mask_now(int l, std::vector<uint8_t>& m) {
+  const int nf = static_cast<int>(g_.fg.size());
+  const FcGeom& f = g_.fg[l];
+  m.assign(static_cast<size_t>(n_ * f.out), 0);
+  if (l + 1 < nf) {
+    std::vector<TA> h(static_cast<size_t>(g_.fg[l + 1].Ip * ldn_));
+    HP_CUDA(cudaMemcpy(h.data(), w_[0].fx[l + 1], h.size() * sizeof(TA), cudaMemcpyDeviceToHost));
+    for (long long o = 0; o < f.out; ++o) {
+      const long long row = fc_col(l + 1, o);
+      for (long long i = 0; i < n_; ++i) m[i * f.out + o] = static_cast<float>(h[row * ldn_ + i]) > 0.f ? 1 : 0;
+    }
+    return;
+  }
+  std::vector<float> h(static_cast<size_t>(f.cmax * ldn_));
+  for (auto& w : w_) {
+    HP_CUDA(cudaMemcpy(h.data(), w.logits, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    const long long c0 = f.c0[sid(w.gid)], c1 = f.c1[sid(w.gid)];
+    for (long long o = c0; o < c1; ++o)
+      for (long long i = 0; i < n_; ++i) m[i * f.out + o] = h[(o - c0) * ldn_ + i] > 0.f ? 1 : 0;
+  }
+}
+
+// Debug capture (hp_cluster_set_debug_capture): every turn's fc ReLU masks,
+// taken right after the turn's forward (stream synchronised; graphs off).
+template <class TA>
+void ClusterImpl<TA>::capture_fc_masks(int j) {
+  const int nf = static_cast<int>(g_.fg.size());
+  if (static_cast<int>(cap_fc_.size()) != num_sub_ * nf) cap_fc_.assign(num_sub_ * nf, {});
+  HP_CUDA(cudaStreamSynchronize(st_));
+  for (int l = 0; l < nf; ++l) fc_mask_now(l, cap_fc_[j * nf + l]);
 }
 
 template <class TA>

@@ -68,6 +68,8 @@ class ClusterBase {
   virtual int64_t param_size(int worker, int which, int layer) const = 0;
   virtual void read_param(int worker, int which, int layer, float* dst, int64_t n) = 0;
   virtual void write_param(int worker, int which, int layer, const float* src, int64_t n) = 0;
+  // Debug / parity: the last step's ReLU masks and pool argmax (see cluster.cu).
+  virtual int64_t read_decisions(int worker, int kind, int layer, void* dst, int64_t n) = 0;
   virtual void gather_model(float* const* ck, float* const* cb, float* const* fw,
                             float* const* fb) = 0;
 
@@ -96,6 +98,7 @@ class ClusterBase {
   bool use_graphs = true;          // replay the step as a captured CUDA graph
   bool fuse_fc_sgd = true;         // FC weight update in the wgrad GEMM epilogue
   bool use_shift = true;           // bf16 stride-1 convs via the flat-shift kernel (else TMA im2col)
+  bool capture_fc = false;         // debug: keep every turn's fc ReLU masks (read_decisions kind 2; no graphs)
   std::vector<GemmProf> prof;      // last step, launch order
   double prof_gemm_ms = 0.0;
   double last_gemm_flops = 0.0;    // algorithmic GEMM FLOPs of the last step

@@ -572,6 +572,23 @@ __device__ __forceinline__ float pow_neg(float d, float beta) {
   return r;
 }
 
+// LRN scale with pinned arithmetic (the oracle's bf16 mode mirrors it, and the
+// argmax ties depend on it): s = fma(a_j, a_j, s) over channels c-2..c+2
+// ascending from 0, d = fma(alpha, s, k).
+__device__ __forceinline__ float lrn_scale5(const float* v, float alpha, float kk) {
+  float s = __fmul_rn(v[0], v[0]);
+  s = __fmaf_rn(v[1], v[1], s);
+  s = __fmaf_rn(v[2], v[2], s);
+  s = __fmaf_rn(v[3], v[3], s);
+  s = __fmaf_rn(v[4], v[4], s);
+  return __fmaf_rn(alpha, s, kk);
+}
+
+// dz_c = gp_c - 2 alpha beta a_c acc_c, pinned the same way in every LRN backward kernel.
+__device__ __forceinline__ float lrn_bwd_out(float gp, float a, float acc, float alpha, float beta) {
+  return __fmaf_rn(-(2.f * alpha * beta) * a, acc, gp);
+}
+
 // LRN channel halo: up to LH = 4 channels each side (LRN size <= 9).
 constexpr int LH = 4;
 
@@ -768,11 +785,15 @@ __global__ void __launch_bounds__(1024) lrn_pool_fwd_kernel(const T* __restrict_
       float o[V];
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        float sum = 0.f;
+        if (NL == 5) {
+          o[j] = v[u][4 + j] * pow_neg(lrn_scale5(v[u] + 2 + j, alpha, kk), beta);
+        } else {
+          float sum = 0.f;
 #pragma unroll
-        for (int d = -HL; d <= HL; ++d)
-          if (d >= -lo && d <= hi) sum += sq[4 + j + d];
-        o[j] = v[u][4 + j] * pow_neg(kk + alpha * sum, beta);
+          for (int d = -HL; d <= HL; ++d)
+            if (d >= -lo && d <= hi) sum += sq[4 + j + d];
+          o[j] = v[u][4 + j] * pow_neg(kk + alpha * sum, beta);
+        }
       }
       float* dst = L + static_cast<long long>(p) * C + c0;
 #pragma unroll
@@ -813,85 +834,6 @@ __global__ void __launch_bounds__(1024) lrn_pool_fwd_kernel(const T* __restrict_
         *reinterpret_cast<uint32_t*>(widx + o + j) = static_cast<uint32_t>(bi[j]) | (bi[j + 1] << 8) |
                                                      (bi[j + 2] << 16) | (static_cast<uint32_t>(bi[j + 3]) << 24);
     }
-}
-
-// Forward, flat form (AlexNet 5/3/2 fast path, vectors filling power-of-two
-// lane groups): thread = (pooled pixel, channel vector); it computes the LRN of
-// the 3x3 window's conv pixels itself (+-2-channel halos by segmented shuffles)
-// and max-pools in registers -- no smem band, no barriers; each conv pixel's
-// LRN is recomputed by up to 4 windows. Same values, order and argmax rule as
-// lrn_pool_fwd_kernel (bit-identical).
-template <class T, int P, int V>
-__global__ void __launch_bounds__(256) lrn_pool_fwd_flat_kernel(const T* __restrict__ a, T* __restrict__ y,
-                                                                 uint8_t* __restrict__ widx, int B, int H, int W,
-                                                                 int C, float alpha, float beta, float kk, int PH,
-                                                                 int PW, int YH, int YW, int yp) {
-  static_assert(V % 4 == 0, "channel vectors of 4");
-  constexpr int HL = 2, PK = 3, PS = 2;
-  const int G = C / V;
-  const int g = threadIdx.x & (P - 1);
-  const int pix = blockIdx.x * (blockDim.x / P) + threadIdx.x / P;  // B*PH*PW < 2^31 (launcher)
-  const bool live = g < G && pix < B * PH * PW;
-  const int bph = live ? pix / PW : 0;
-  const int pw = live ? pix - bph * PW : 0;
-  const int b = bph / PH, ph = bph - b * PH;
-  const int c0 = g * V;
-  float best[V];
-  int bi[V];
-#pragma unroll
-  for (int j = 0; j < V; ++j) {
-    best[j] = -INFINITY;
-    bi[j] = 0;
-  }
-#pragma unroll 1
-  for (int r = 0; r < PK; ++r) {
-    float v[PK][V];
-#pragma unroll
-    for (int q = 0; q < PK; ++q) {
-      const T* px = a + ((static_cast<long long>(b) * H + ph * PS + r) * W + pw * PS + q) * C + c0;
-#pragma unroll
-      for (int j = 0; j < V; j += 4) {
-        if (live) {
-          ld4<T>(px + j, v[q] + j);
-        } else {
-          v[q][j] = v[q][j + 1] = v[q][j + 2] = v[q][j + 3] = 0.f;
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < PK; ++q) {
-      float sq[V + 2 * HL];
-#pragma unroll
-      for (int j = 0; j < V; ++j) sq[HL + j] = v[q][j] * v[q][j];
-#pragma unroll
-      for (int d = 0; d < HL; ++d) {
-        const float l = __shfl_up_sync(0xffffffffu, v[q][V - HL + d], 1, P);
-        const float rr = __shfl_down_sync(0xffffffffu, v[q][d], 1, P);
-        sq[d] = g > 0 ? l * l : 0.f;
-        sq[HL + V + d] = g + 1 < G ? rr * rr : 0.f;
-      }
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        float sum = 0.f;
-#pragma unroll
-        for (int d = -HL; d <= HL; ++d) sum += sq[HL + j + d];
-        const float o = v[q][j] * pow_neg(kk + alpha * sum, beta);
-        if ((o > best[j] || isnan(o)) && !isnan(best[j])) {
-          best[j] = o;
-          bi[j] = r * PK + q;
-        }
-      }
-    }
-  }
-  if (!live) return;
-#pragma unroll
-  for (int j = 0; j < V; j += 4)
-    st4<T>(y + (static_cast<long long>(b * YH + ph + yp) * YW + pw + yp) * C + c0 + j, best + j);
-  const long long o = (static_cast<long long>(b * PH + ph) * PW + pw) * C + c0;
-#pragma unroll
-  for (int j = 0; j < V; j += 4)
-    *reinterpret_cast<uint32_t*>(widx + o + j) = static_cast<uint32_t>(bi[j]) | (bi[j + 1] << 8) |
-                                                 (bi[j + 2] << 16) | (static_cast<uint32_t>(bi[j + 3]) << 24);
 }
 
 // Backward: block = one conv-output row (b, h) x all channels, threads =
@@ -998,11 +940,16 @@ __global__ void __launch_bounds__(512) lrn_pool_bwd_kernel(
   float gp[V], tv[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) {
-    float sum = 0.f;
+    float dd;
+    if (NL == 5) {
+      dd = lrn_scale5(win + 2 + j, alpha, kk);
+    } else {
+      float sum = 0.f;
 #pragma unroll
-    for (int d = -HL; d <= HL; ++d)
-      if (d >= -lo && d <= hi) sum += win[4 + j + d] * win[4 + j + d];
-    const float dd = kk + alpha * sum;
+      for (int d = -HL; d <= HL; ++d)
+        if (d >= -lo && d <= hi) sum += win[4 + j + d] * win[4 + j + d];
+      dd = kk + alpha * sum;
+    }
     const float pn = pow_neg(dd, beta);
     float rd;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(dd));
@@ -1024,124 +971,381 @@ __global__ void __launch_bounds__(512) lrn_pool_bwd_kernel(
 #pragma unroll
     for (int d = -HL; d <= HL; ++d)
       if (d >= -hi && d <= lo) acc += win[4 + k + d];
-    float gval = gp[k] - 2.f * alpha * beta * av[k] * acc;
+    float gval = lrn_bwd_out(gp[k], av[k], acc, alpha, beta);
     if (relu_mask && !(av[k] > 0.f)) gval = 0.f;
     out[k] = gval;
   }
   if (live) stv<TA>(dz + ((b * ZH + h + zp) * ZW + w + zp) * C + c0, out);
 }
 
-// Backward, flat form (AlexNet 5/3/2 fast path, C/V <= 32 vectors): thread =
-// (conv pixel, channel vector), P = next power of two >= C/V lanes per pixel.
-// The +-2-channel LRN halos of a and t come from the neighbouring lanes by
-// segmented shuffles, so there is no shared memory and no block barrier: every
-// thread issues its activation, argmax and pooled-gradient loads at once.
-// Same arithmetic, in the same order, as lrn_pool_bwd_kernel (bit-identical).
-template <class TA, int P, int V>
-__global__ void __launch_bounds__(256) lrn_pool_bwd_flat_kernel(
-    const float* __restrict__ gy, const uint8_t* __restrict__ widx, const TA* __restrict__ a,
-    TA* __restrict__ dz, int B, int H, int W, int C, float alpha, float beta, float kk, int PH, int PW,
-    int relu_mask, int ZH, int ZW, int zp) {
-  static_assert(V % 4 == 0, "channel vectors of 4");
-  constexpr int HL = 2, PK = 3, PS = 2, MW = 2;
+// ------------------------------------------------------------------ LRN + pool, row-streaming
+// AlexNet 5 / 3 / 2 path. Block = (image b, band of rows); the band's conv
+// rows stream HBM -> smem through a ring of TMA bulk copies (thread 0 keeps
+// NR rows in flight), so the memory pipe never waits on the arithmetic. Each
+// conv pixel's LRN is computed ONCE per row (fp32, into a double-buffered smem
+// row), then pooled: the 3-wide horizontal max from smem, the 3-high vertical
+// max in registers across rows (row-major first maximum, strict >, first NaN
+// wins -- the order of a 3x3 row-major scan). One block barrier per row.
+// Loads V channels [c0, c0+V) of one pixel plus 2 halo channels on each side
+// (zero outside [0, C)) as fp32: out[0..V+4) = channels c0-2 .. c0+V+1.
+template <class T, int V>
+__device__ __forceinline__ void load_halo5(const T* px, int c0, int C, float* out) {
+  ldv<T>(px + c0, out + 2);
+  if constexpr (sizeof(T) == 2) {
+    if (c0 > 0) {
+      const float2 l = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(px + c0 - 2));
+      out[0] = l.x;
+      out[1] = l.y;
+    } else {
+      out[0] = out[1] = 0.f;
+    }
+    if (c0 + V < C) {
+      const float2 r = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(px + c0 + V));
+      out[V + 2] = r.x;
+      out[V + 3] = r.y;
+    } else {
+      out[V + 2] = out[V + 3] = 0.f;
+    }
+  } else {
+    if (c0 > 0) {
+      const float2 l = *reinterpret_cast<const float2*>(px + c0 - 2);
+      out[0] = l.x;
+      out[1] = l.y;
+    } else {
+      out[0] = out[1] = 0.f;
+    }
+    if (c0 + V < C) {
+      const float2 r = *reinterpret_cast<const float2*>(px + c0 + V);
+      out[V + 2] = r.x;
+      out[V + 3] = r.y;
+    } else {
+      out[V + 2] = out[V + 3] = 0.f;
+    }
+  }
+}
+
+// The fp32 row halo (t in the backward): same as load_halo5 on float rows.
+template <int V>
+__device__ __forceinline__ void load_halo5_f(const float* px, int c0, int C, float* out) {
+#pragma unroll
+  for (int j = 0; j < V; j += 4) {
+    const float4 x = *reinterpret_cast<const float4*>(px + c0 + j);
+    out[2 + j] = x.x; out[3 + j] = x.y; out[4 + j] = x.z; out[5 + j] = x.w;
+  }
+  if (c0 > 0) {
+    const float2 l = *reinterpret_cast<const float2*>(px + c0 - 2);
+    out[0] = l.x;
+    out[1] = l.y;
+  } else {
+    out[0] = out[1] = 0.f;
+  }
+  if (c0 + V < C) {
+    const float2 r = *reinterpret_cast<const float2*>(px + c0 + V);
+    out[V + 2] = r.x;
+    out[V + 3] = r.y;
+  } else {
+    out[V + 2] = out[V + 3] = 0.f;
+  }
+}
+
+__device__ __forceinline__ bool takes_max(float v, float best) { return (v > best || isnan(v)) && !isnan(best); }
+
+
+// KI: (pixel, channel-vector) items per thread (W*G <= KI * blockDim.x).
+template <class T, int KI>
+__global__ void __launch_bounds__(1024) lrn_pool_fwd_rows_kernel(const T* __restrict__ a, T* __restrict__ y,
+                                                                 uint8_t* __restrict__ widx, int H, int W, int C,
+                                                                 float alpha, float beta, float kk, int PH, int PW,
+                                                                 int TP, int YH, int YW, int yp, int NR) {
+  constexpr int V = 16 / sizeof(T);
   const int G = C / V;
-  const int g = threadIdx.x & (P - 1);
-  const int pix = blockIdx.x * (blockDim.x / P) + threadIdx.x / P;  // B*H*W < 2^31 (launcher)
-  const bool live = g < G && pix < B * H * W;
-  const int bh = live ? pix / W : 0;
-  const int w = live ? pix - bh * W : 0;
-  const int b = bh / H, h = bh - b * H;
-  const int c0 = g * V;
-  float av[V], gb[V];
-#pragma unroll
-  for (int j = 0; j < V; ++j) {
-    av[j] = 0.f;
-    gb[j] = 0.f;
+  extern __shared__ __align__(128) unsigned char lrn_rows_sm[];
+  const long long row_elems = static_cast<long long>(W) * C;
+  T* raw = reinterpret_cast<T*>(lrn_rows_sm);
+  float* ybuf = reinterpret_cast<float*>(lrn_rows_sm + NR * row_elems * sizeof(T));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ybuf + 2 * row_elems);
+  const int b = blockIdx.y;
+  const int ph0 = blockIdx.x * TP, ph1 = min(PH, ph0 + TP) - 1;
+  const int nrows = 2 * (ph1 - ph0) + 3;  // conv rows 2*ph0 .. 2*ph1+2
+  const T* src = a + (static_cast<long long>(b) * H + 2 * ph0) * row_elems;
+  const uint32_t row_bytes = static_cast<uint32_t>(row_elems * sizeof(T));
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  if (tid == 0) {
+    for (int s = 0; s < NR; ++s) mbar_init(&bars[s], 1);
+    fence_barrier_init();
+    for (int s = 0; s < min(NR, nrows); ++s) {
+      mbar_arrive_expect_tx(&bars[s], row_bytes);
+      bulk_load(raw + s * row_elems, src + s * row_elems, row_bytes, &bars[s]);
+    }
   }
-  uint32_t wi[MW][MW][V / 4];
-  float4 gv[MW][MW][V / 4];
-  const int oh0 = h - PK + 1 <= 0 ? 0 : (h - PK + PS) / PS;
-  const int oh1 = min(PH - 1, h / PS);
-  const int ow0 = w - PK + 1 <= 0 ? 0 : (w - PK + PS) / PS;
-  const int ow1 = min(PW - 1, w / PS);
-  if (live) {
+  // items: LRN (w, g) over W*G, pool (pw, g) over PW*G; at most KI each
+  int lw[KI], lg[KI], pw_[KI], pg[KI];
 #pragma unroll
-    for (int j = 0; j < V; j += 4) ld4<TA>(a + ((static_cast<long long>(b) * H + h) * W + w) * C + c0 + j, av + j);
+  for (int k = 0; k < KI; ++k) {
+    const int it = tid + k * nthr;
+    lw[k] = it < W * G ? it / G : -1;
+    lg[k] = it < W * G ? it - lw[k] * G : 0;
+    pw_[k] = it < PW * G ? it / G : -1;
+    pg[k] = it < PW * G ? it - pw_[k] * G : 0;
+  }
+  float best[KI][V];
+  int bi[KI][V];
+  __syncthreads();
+  for (int i = 0; i < nrows; ++i) {
+    const int slot = i % NR;
+    mbar_wait(&bars[slot], static_cast<uint32_t>((i / NR) & 1));
+    const T* row = raw + slot * row_elems;
+    float* yb = ybuf + (i & 1) * row_elems;
 #pragma unroll
-    for (int i = 0; i < MW; ++i)
+    for (int k = 0; k < KI; ++k) {
+      if (lw[k] < 0) continue;
+      const int c0 = lg[k] * V;
+      float v[V + 4];
+      load_halo5<T, V>(row + static_cast<long long>(lw[k]) * C, c0, C, v);
+      float o[V];
 #pragma unroll
-      for (int k = 0; k < MW; ++k) {
-        const bool ok = oh0 + i <= oh1 && ow0 + k <= ow1;
-        const long long o = ((static_cast<long long>(b) * PH + (ok ? oh0 + i : 0)) * PW + (ok ? ow0 + k : 0)) * C + c0;
+      for (int j = 0; j < V; ++j) o[j] = v[j + 2] * pow_neg(lrn_scale5(v + j, alpha, kk), beta);
+      float* dst = yb + static_cast<long long>(lw[k]) * C + c0;
 #pragma unroll
-        for (int j = 0; j < V / 4; ++j) {
-          wi[i][k][j] = ok ? *reinterpret_cast<const uint32_t*>(widx + o + 4 * j) : 0xffffffffu;
-          gv[i][k][j] = ok ? *reinterpret_cast<const float4*>(gy + o + 4 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+      for (int j = 0; j < V; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+    }
+    __syncthreads();
+    if (tid == 0 && i + NR < nrows) {  // every thread is done with this slot: refill it
+      mbar_arrive_expect_tx(&bars[slot], row_bytes);
+      bulk_load(raw + slot * row_elems, src + (i + NR) * row_elems, row_bytes, &bars[slot]);
+    }
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+      if (pw_[k] < 0) continue;
+      const int c0 = pg[k] * V;
+      float hv[V];
+      int hq[V];
+      const float* p0 = yb + static_cast<long long>(2 * pw_[k]) * C + c0;
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        hv[j] = -INFINITY;
+        hq[j] = 0;
       }
 #pragma unroll
-    for (int i = 0; i < MW; ++i)
+      for (int q = 0; q < 3; ++q) {
 #pragma unroll
-      for (int k = 0; k < MW; ++k) {
-        const uint32_t me = static_cast<uint32_t>((h - (oh0 + i) * PS) * PK + (w - (ow0 + k) * PS));
+        for (int j = 0; j < V; j += 4) {
+          const float4 x = *reinterpret_cast<const float4*>(p0 + q * C + j);
+          const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-        for (int j = 0; j < V / 4; ++j) {
-          const uint32_t x = wi[i][k][j];
-          const float4 g4 = gv[i][k][j];
-          if ((x & 0xff) == me) gb[4 * j] += g4.x;
-          if (((x >> 8) & 0xff) == me) gb[4 * j + 1] += g4.y;
-          if (((x >> 16) & 0xff) == me) gb[4 * j + 2] += g4.z;
-          if ((x >> 24) == me) gb[4 * j + 3] += g4.w;
+          for (int u = 0; u < 4; ++u)
+            if (takes_max(xv[u], hv[j + u])) {
+              hv[j + u] = xv[u];
+              hq[j + u] = q;
+            }
         }
       }
+      if ((i & 1) == 0) {
+        if (i > 0) {  // last row (r = 2) of window ph0 + i/2 - 1: finish and store it
+#pragma unroll
+          for (int j = 0; j < V; ++j)
+            if (takes_max(hv[j], best[k][j])) {
+              best[k][j] = hv[j];
+              bi[k][j] = 6 + hq[j];
+            }
+          const int ph = ph0 + i / 2 - 1, pw = pw_[k];
+#pragma unroll
+          for (int j = 0; j < V; j += 4)
+            st4<T>(y + (static_cast<long long>(b * YH + ph + yp) * YW + pw + yp) * C + c0 + j, best[k] + j);
+          const long long o = (static_cast<long long>(b * PH + ph) * PW + pw) * C + c0;
+#pragma unroll
+          for (int j = 0; j < V; j += 4)
+            *reinterpret_cast<uint32_t*>(widx + o + j) = static_cast<uint32_t>(bi[k][j]) | (bi[k][j + 1] << 8) |
+                                                         (bi[k][j + 2] << 16) |
+                                                         (static_cast<uint32_t>(bi[k][j + 3]) << 24);
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) {  // first row (r = 0) of window ph0 + i/2
+          best[k][j] = hv[j];
+          bi[k][j] = hq[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+          if (takes_max(hv[j], best[k][j])) {
+            best[k][j] = hv[j];
+            bi[k][j] = 3 + hq[j];
+          }
+      }
+    }
   }
-  // a over channels [c0-2, c0+V+2): halo from the neighbouring lanes (zero at the channel ends)
-  float win[V + 2 * HL];
-#pragma unroll
-  for (int j = 0; j < V; ++j) win[HL + j] = av[j];
-#pragma unroll
-  for (int d = 0; d < HL; ++d) {
-    const float l = __shfl_up_sync(0xffffffffu, av[V - HL + d], 1, P);
-    const float r = __shfl_down_sync(0xffffffffu, av[d], 1, P);
-    win[d] = g > 0 ? l : 0.f;
-    win[HL + V + d] = g + 1 < G ? r : 0.f;
+}
+
+// Backward: block = (image b, band of conv rows). Conv rows and the pooled
+// rows (gradient + argmax bytes) they draw from stream in through two TMA
+// rings. Per conv row: gather gb (every window containing the pixel whose
+// argmax is it), d, t = gb a d^-beta / d into a double-buffered fp32 smem row
+// (the +-2-channel t halo), then
+//   dz_c = gb_c d_c^-beta - 2 alpha beta a_c sum_{i in c-2..c+2} t_i   (x ReLU mask)
+// stored as TA; the bias gradient (model.cpp:184-202, channel sums of the
+// STORED dz) is accumulated per block in registers and written as one fp32
+// partial row per block (reduced in ascending block order by
+// bias_partials_reduce_kernel: deterministic).
+template <class TA, int KI>
+__global__ void __launch_bounds__(1024) lrn_pool_bwd_rows_kernel(
+    const float* __restrict__ gy, const uint8_t* __restrict__ widx, const TA* __restrict__ a,
+    TA* __restrict__ dz, float* __restrict__ bias_part, int H, int W, int C, float alpha, float beta, float kk,
+    int PH, int PW, int relu_mask, int ZH, int ZW, int zp, int TH, int NR, int NP) {
+  constexpr int V = 16 / sizeof(TA);
+  const int G = C / V;
+  extern __shared__ __align__(128) unsigned char lrn_rows_sm[];
+  const long long row_elems = static_cast<long long>(W) * C, prow_elems = static_cast<long long>(PW) * C;
+  TA* raw = reinterpret_cast<TA*>(lrn_rows_sm);
+  float* pg_ring = reinterpret_cast<float*>(lrn_rows_sm + NR * row_elems * sizeof(TA));
+  uint8_t* pi_ring = reinterpret_cast<uint8_t*>(pg_ring + NP * prow_elems);
+  float* tbuf = reinterpret_cast<float*>(pi_ring + NP * prow_elems);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tbuf + 2 * row_elems);  // NR conv rows, then NP pooled rows
+  const int b = blockIdx.y;
+  const int h0 = blockIdx.x * TH, h1 = min(H, h0 + TH) - 1;
+  const int nrows = h1 - h0 + 1;
+  const int pr0 = h0 <= 1 ? 0 : (h0 - 1) / 2;
+  const int pr1 = min(PH - 1, h1 / 2);
+  const TA* src = a + (static_cast<long long>(b) * H + h0) * row_elems;
+  const float* gsrc = gy + static_cast<long long>(b) * PH * prow_elems;
+  const uint8_t* isrc = widx + static_cast<long long>(b) * PH * prow_elems;
+  const uint32_t row_bytes = static_cast<uint32_t>(row_elems * sizeof(TA));
+  const uint32_t pg_bytes = static_cast<uint32_t>(prow_elems * sizeof(float)), pi_bytes = static_cast<uint32_t>(prow_elems);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  auto load_pooled = [&](int ph) {
+    const int s = (ph - pr0) % NP;
+    mbar_arrive_expect_tx(&bars[NR + s], pg_bytes + pi_bytes);
+    bulk_load(pg_ring + s * prow_elems, gsrc + ph * prow_elems, pg_bytes, &bars[NR + s]);
+    bulk_load(pi_ring + s * prow_elems, isrc + ph * prow_elems, pi_bytes, &bars[NR + s]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < NR + NP; ++s) mbar_init(&bars[s], 1);
+    fence_barrier_init();
+    for (int s = 0; s < min(NR, nrows); ++s) {
+      mbar_arrive_expect_tx(&bars[s], row_bytes);
+      bulk_load(raw + s * row_elems, src + s * row_elems, row_bytes, &bars[s]);
+    }
+    for (int ph = pr0; ph <= min(pr1, pr0 + NP - 1); ++ph) load_pooled(ph);
   }
-  float gp[V], tv[V];
+  int lw[KI], lg[KI];
+  float bsum[KI][V];
 #pragma unroll
-  for (int j = 0; j < V; ++j) {
-    float sum = 0.f;
+  for (int k = 0; k < KI; ++k) {
+    const int it = tid + k * nthr;
+    lw[k] = it < W * G ? it / G : -1;
+    lg[k] = it < W * G ? it - lw[k] * G : 0;
 #pragma unroll
-    for (int d = -HL; d <= HL; ++d) sum += win[HL + j + d] * win[HL + j + d];
-    const float dd = kk + alpha * sum;
-    const float pn = pow_neg(dd, beta);
-    float rd;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(dd));
-    tv[j] = gb[j] * av[j] * (pn * rd);
-    gp[j] = gb[j] * pn;
+    for (int j = 0; j < V; ++j) bsum[k][j] = 0.f;
   }
+  __syncthreads();
+  int waited = pr0 - 1;  // pooled rows this thread has waited for
+  for (int i = 0; i < nrows; ++i) {
+    const int h = h0 + i;
+    const int slot = i % NR;
+    const int plo = h <= 1 ? 0 : (h - 1) / 2, phi = min(PH - 1, h / 2);
+    while (waited < phi) {
+      ++waited;
+      mbar_wait(&bars[NR + (waited - pr0) % NP], static_cast<uint32_t>(((waited - pr0) / NP) & 1));
+    }
+    mbar_wait(&bars[slot], static_cast<uint32_t>((i / NR) & 1));
+    const TA* row = raw + slot * row_elems;
+    float* tb = tbuf + (i & 1) * row_elems;
+    float av[KI][V + 4], gp[KI][V];
 #pragma unroll
-  for (int j = 0; j < V; ++j) win[HL + j] = tv[j];
+    for (int k = 0; k < KI; ++k) {
+      if (lw[k] < 0) continue;
+      const int w = lw[k], c0 = lg[k] * V;
+      load_halo5<TA, V>(row + static_cast<long long>(w) * C, c0, C, av[k]);
+      float gb[V];
 #pragma unroll
-  for (int d = 0; d < HL; ++d) {
-    const float l = __shfl_up_sync(0xffffffffu, tv[V - HL + d], 1, P);
-    const float r = __shfl_down_sync(0xffffffffu, tv[d], 1, P);
-    win[d] = g > 0 ? l : 0.f;
-    win[HL + V + d] = g + 1 < G ? r : 0.f;
+      for (int j = 0; j < V; ++j) gb[j] = 0.f;
+      const int qlo = w <= 1 ? 0 : (w - 1) / 2, qhi = min(PW - 1, w / 2);
+      for (int ph = plo; ph <= phi; ++ph) {
+        const int ps_ = (ph - pr0) % NP;
+        const float* gr = pg_ring + ps_ * prow_elems;
+        const uint8_t* ir = pi_ring + ps_ * prow_elems;
+        for (int pw = qlo; pw <= qhi; ++pw) {
+          const uint32_t me = static_cast<uint32_t>((h - 2 * ph) * 3 + (w - 2 * pw));
+#pragma unroll
+          for (int j = 0; j < V; j += 4) {
+            const uint32_t x = *reinterpret_cast<const uint32_t*>(ir + pw * C + c0 + j);
+            const float4 g4 = *reinterpret_cast<const float4*>(gr + pw * C + c0 + j);
+            if ((x & 0xff) == me) gb[j] += g4.x;
+            if (((x >> 8) & 0xff) == me) gb[j + 1] += g4.y;
+            if (((x >> 16) & 0xff) == me) gb[j + 2] += g4.z;
+            if ((x >> 24) == me) gb[j + 3] += g4.w;
+          }
+        }
+      }
+      float tv[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const float dd = lrn_scale5(av[k] + j, alpha, kk);
+        const float pn = pow_neg(dd, beta);
+        float rd;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(dd));
+        tv[j] = gb[j] * av[k][j + 2] * (pn * rd);
+        gp[k][j] = gb[j] * pn;
+      }
+      float* dst = tb + static_cast<long long>(w) * C + c0;
+#pragma unroll
+      for (int j = 0; j < V; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(tv[j], tv[j + 1], tv[j + 2], tv[j + 3]);
+    }
+    __syncthreads();
+    if (tid == 0) {  // every thread is done with conv slot i and with the pooled rows finished by row h
+      if (i + NR < nrows) {
+        mbar_arrive_expect_tx(&bars[slot], row_bytes);
+        bulk_load(raw + slot * row_elems, src + (i + NR) * row_elems, row_bytes, &bars[slot]);
+      }
+      if ((h & 1) == 0 && h >= 2) {
+        const int done = (h - 2) / 2;  // its last conv row was h
+        if (done >= pr0 && done + NP <= pr1) load_pooled(done + NP);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KI; ++k) {
+      if (lw[k] < 0) continue;
+      const int w = lw[k], c0 = lg[k] * V;
+      float tw[V + 4];
+      load_halo5_f<V>(tb + static_cast<long long>(w) * C, c0, C, tw);
+      float out[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const float acc = (((tw[j] + tw[j + 1]) + tw[j + 2]) + tw[j + 3]) + tw[j + 4];
+        float gval = lrn_bwd_out(gp[k][j], av[k][j + 2], acc, alpha, beta);
+        if (relu_mask && !(av[k][j + 2] > 0.f)) gval = 0.f;
+        out[j] = to_f<TA>(from_f<TA>(gval));
+        bsum[k][j] += out[j];
+      }
+      stv<TA>(dz + (static_cast<long long>(b * ZH + h + zp) * ZW + w + zp) * C + c0, out);
+    }
   }
-  float out[V];
+  // per-block bias partial: sum the items' registers over w in ascending order
+  __syncthreads();
+  float* red = tbuf;  // [W][C]
 #pragma unroll
-  for (int k = 0; k < V; ++k) {
-    float acc = 0.f;
+  for (int k = 0; k < KI; ++k) {
+    if (lw[k] < 0) continue;
+    float* dst = red + static_cast<long long>(lw[k]) * C + lg[k] * V;
 #pragma unroll
-    for (int d = -HL; d <= HL; ++d) acc += win[HL + k + d];
-    float gval = gp[k] - 2.f * alpha * beta * av[k] * acc;
-    if (relu_mask && !(av[k] > 0.f)) gval = 0.f;
-    out[k] = gval;
+    for (int j = 0; j < V; j += 4)
+      *reinterpret_cast<float4*>(dst + j) = make_float4(bsum[k][j], bsum[k][j + 1], bsum[k][j + 2], bsum[k][j + 3]);
   }
-  if (live) {
-#pragma unroll
-    for (int j = 0; j < V; j += 4) st4<TA>(dz + ((static_cast<long long>(b) * ZH + h + zp) * ZW + w + zp) * C + c0 + j, out + j);
+  __syncthreads();
+  float* part = bias_part + (static_cast<long long>(b) * gridDim.x + blockIdx.x) * C;
+  for (int c = tid; c < C; c += nthr) {
+    float s = 0.f;
+    for (int w = 0; w < W; ++w) s += red[static_cast<long long>(w) * C + c];
+    part[c] = s;
   }
+}
+
+// out[c] = sum over partial rows in ascending order (deterministic bias grads).
+__global__ void bias_partials_reduce_kernel(const float* __restrict__ part, int rows, int C, float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  float s = 0.f;
+  for (int r = 0; r < rows; ++r) s += part[static_cast<long long>(r) * C + c];
+  out[c] = s;
 }
 
 // Rotated operand for the implicit dgrad: wr[c][r][s][f] = w[f][R-1-r][S-1-s][c].
@@ -1343,6 +1547,57 @@ void launch_im2col_t_nchw(const float* x, T* colT, int B, int C, int H, int W, i
                                                             ldp, K);
 }
 
+// Launch plan of the row-streaming LRN+pool kernels (5/3/2): block =
+// (band of rows, image), threads = the row's (pixel, channel-vector) items (at
+// most 2 per thread), smem = the TMA rings + the fp32 double row. The band
+// length minimises waves x rows per band at the occupancy the smem allows.
+struct LrnRowsPlan {
+  bool ok = false;
+  int threads = 0, ki = 1, band = 0, bands = 0, nr = 0, np = 0;
+  size_t smem = 0;
+};
+LrnRowsPlan lrn_rows_plan(bool bwd, int B, int H, int W, int C, int PH, int PW, int elem) {
+  LrnRowsPlan p;
+  const int V = 16 / elem;
+  if (C % V != 0 || C < 2 * V) return p;
+  const int G = C / V;
+  const long long items = static_cast<long long>(W) * G;
+  const long long row = static_cast<long long>(W) * C * elem, prow = static_cast<long long>(PW) * C;
+  if (items > 2048 || row % 16 != 0 || prow % 16 != 0 || (prow * 4) % 16 != 0) return p;
+  p.threads = static_cast<int>(std::min<long long>(1024, (items + 31) / 32 * 32));
+  p.ki = items > p.threads ? 2 : 1;
+  const size_t fixed = static_cast<size_t>(2) * W * C * sizeof(float);
+  const size_t budget = 220 * 1024;
+  for (int nr = 4; nr >= 2; --nr) {
+    const int np = bwd ? 3 : 0;
+    const size_t sm = nr * row + np * prow * 5 + fixed + (nr + np) * 8;
+    if (sm <= budget) {
+      p.nr = nr;
+      p.np = np;
+      p.smem = sm;
+      break;
+    }
+  }
+  if (p.nr == 0) return p;
+  const int per_sm = std::max(1, std::min(static_cast<int>((227 * 1024) / (p.smem + 1024)), 2048 / p.threads));
+  const int slots = 148 * per_sm;
+  const int units = bwd ? H : PH;  // conv rows (bwd) / pooled rows (fwd) per image
+  double best = 1e30;
+  for (int t = 1; t <= units; ++t) {
+    const int bands = (units + t - 1) / t;
+    const int waves = (B * bands + slots - 1) / slots;
+    const double rows = bwd ? t + 1.0 : 2.0 * t + 1.0;  // + the ramp of the ring
+    const double cost = waves * rows;
+    if (cost < best - 1e-9) {
+      best = cost;
+      p.band = t;
+      p.bands = bands;
+    }
+  }
+  p.ok = true;
+  return p;
+}
+
 template <class T>
 void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, int C, int n,
                          float alpha, float beta, float kk, int pk, int ps, int PH, int PW,
@@ -1369,27 +1624,16 @@ void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, i
     kern<<<grid, block, smem, st>>>(a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, TP,
                                     yl.H, yl.W, yl.p);
   };
-  static const bool flat_off = getenv("HP_DEV_LRN_FWD_SMEM") != nullptr;  // dev: the smem-band kernel
-  auto pow2 = [](int g) { return g == 4 || g == 8 || g == 16 || g == 32; };
-  const int Vf = pow2(G) ? V : (C % 12 == 0 && pow2(C / 12) ? 12 : 0);
-  if (n == 5 && pk == 3 && ps == 2 && Vf > 0 && !flat_off) {
-    const int P = C / Vf;
-    const long long threads = static_cast<long long>(B) * PH * PW * P;
-    const int blocks = static_cast<int>((threads + 255) / 256);
-    auto fl = [&](auto kern) {
-      kern<<<blocks, 256, 0, st>>>(a, y, widx, B, H, W, C, alpha, beta, kk, PH, PW, yl.H, yl.W, yl.p);
+  static const bool rows_off = getenv("HP_DEV_LRN_FWD_SMEM") != nullptr;  // dev: the smem-band kernel
+  const LrnRowsPlan rp = lrn_rows_plan(false, B, H, W, C, PH, PW, sizeof(T));
+  if (n == 5 && pk == 3 && ps == 2 && rp.ok && !rows_off) {
+    auto rk = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rp.smem));
+      kern<<<dim3(rp.bands, B), rp.threads, rp.smem, st>>>(a, y, widx, H, W, C, alpha, beta, kk, PH, PW, rp.band,
+                                                           yl.H, yl.W, yl.p, rp.nr);
     };
-    if (Vf == V) {
-      if (P == 4) fl(lrn_pool_fwd_flat_kernel<T, 4, V>);
-      else if (P == 8) fl(lrn_pool_fwd_flat_kernel<T, 8, V>);
-      else if (P == 16) fl(lrn_pool_fwd_flat_kernel<T, 16, V>);
-      else fl(lrn_pool_fwd_flat_kernel<T, 32, V>);
-    } else {
-      if (P == 4) fl(lrn_pool_fwd_flat_kernel<T, 4, 12>);
-      else if (P == 8) fl(lrn_pool_fwd_flat_kernel<T, 8, 12>);
-      else if (P == 16) fl(lrn_pool_fwd_flat_kernel<T, 16, 12>);
-      else fl(lrn_pool_fwd_flat_kernel<T, 32, 12>);
-    }
+    if (rp.ki == 1) rk(lrn_pool_fwd_rows_kernel<T, 1>);
+    else rk(lrn_pool_fwd_rows_kernel<T, 2>);
   } else if (n == 5 && pk == 3 && ps == 2) {
     go(lrn_pool_fwd_kernel<T, 2, 5, 3, 2>);
   } else if (n <= 5) {
@@ -1400,9 +1644,9 @@ void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, i
 }
 
 template <class TA>
-void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* dz, int B, int H,
-                         int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
-                         int PH, int PW, int relu_mask, cudaStream_t st, OutLayout zl) {
+int launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* dz, int B, int H,
+                        int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
+                        int PH, int PW, int relu_mask, cudaStream_t st, OutLayout zl, float* bias_part) {
   if (zl.H == 0) zl = OutLayout{H, W, 0};
   constexpr int V = 16 / sizeof(TA);
   const int G = C / V;
@@ -1420,32 +1664,17 @@ void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* 
     kern<<<grid, block, smem, st>>>(gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW,
                                     relu_mask, zl.H, zl.W, zl.p);
   };
-  static const bool flat_off = getenv("HP_DEV_LRN_BWD_SMEM") != nullptr;  // dev: the block-per-row kernel
-  // Flat kernel when the channel vectors fill power-of-two lane groups: 16-byte
-  // vectors (conv1: 8 of 8 bf16 channels), else 12-channel vectors (conv2: 192
-  // channels = 16 x 12); padded lane groups measured slower than the smem kernel.
-  auto pow2 = [](int g) { return g == 4 || g == 8 || g == 16 || g == 32; };
-  const int Vf = pow2(G) ? V : (C % 12 == 0 && pow2(C / 12) ? 12 : 0);
-  if (n == 5 && pk == 3 && ps == 2 && Vf > 0 && !flat_off) {
-    const int P = C / Vf;
-    const long long threads = static_cast<long long>(B) * H * W * P;
-    const int blocks = static_cast<int>((threads + 255) / 256);
-    auto fl = [&](auto kern) {
-      kern<<<blocks, 256, 0, st>>>(gy, widx, a, dz, B, H, W, C, alpha, beta, kk, PH, PW, relu_mask, zl.H, zl.W,
-                                   zl.p);
+  static const bool rows_off = getenv("HP_DEV_LRN_BWD_SMEM") != nullptr;  // dev: the block-per-row kernel
+  const LrnRowsPlan rp = lrn_rows_plan(true, B, H, W, C, PH, PW, sizeof(TA));
+  if (n == 5 && pk == 3 && ps == 2 && rp.ok && !rows_off && bias_part != nullptr) {
+    auto rk = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rp.smem));
+      kern<<<dim3(rp.bands, B), rp.threads, rp.smem, st>>>(gy, widx, a, dz, bias_part, H, W, C, alpha, beta, kk, PH,
+                                                           PW, relu_mask, zl.H, zl.W, zl.p, rp.band, rp.nr, rp.np);
     };
-    constexpr int V0 = 16 / sizeof(TA);
-    if (Vf == V0) {
-      if (P == 4) fl(lrn_pool_bwd_flat_kernel<TA, 4, V0>);
-      else if (P == 8) fl(lrn_pool_bwd_flat_kernel<TA, 8, V0>);
-      else if (P == 16) fl(lrn_pool_bwd_flat_kernel<TA, 16, V0>);
-      else fl(lrn_pool_bwd_flat_kernel<TA, 32, V0>);
-    } else {
-      if (P == 4) fl(lrn_pool_bwd_flat_kernel<TA, 4, 12>);
-      else if (P == 8) fl(lrn_pool_bwd_flat_kernel<TA, 8, 12>);
-      else if (P == 16) fl(lrn_pool_bwd_flat_kernel<TA, 16, 12>);
-      else fl(lrn_pool_bwd_flat_kernel<TA, 32, 12>);
-    }
+    if (rp.ki == 1) rk(lrn_pool_bwd_rows_kernel<TA, 1>);
+    else rk(lrn_pool_bwd_rows_kernel<TA, 2>);
+    return rp.bands * B;
   } else if (n == 5 && pk == 3 && ps == 2) {
     go(lrn_pool_bwd_kernel<TA, 2, 5, 3, 2>);
   } else if (n <= 5) {
@@ -1453,6 +1682,16 @@ void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* 
   } else {
     go(lrn_pool_bwd_kernel<TA, LH, 0, 0, 0>);
   }
+  return 0;
+}
+
+void launch_bias_partials_reduce(const float* part, int rows, int C, float* out, cudaStream_t st) {
+  bias_partials_reduce_kernel<<<(C + 127) / 128, 128, 0, st>>>(part, rows, C, out);
+}
+
+int lrn_pool_bwd_partial_rows(int B, int H, int W, int C, int PH, int PW, int elem_bytes) {
+  const LrnRowsPlan rp = lrn_rows_plan(true, B, H, W, C, PH, PW, elem_bytes);
+  return rp.ok ? rp.bands * B : 0;
 }
 
 template <class T>
@@ -1533,9 +1772,9 @@ void launch_skip_sync_fixup(float* g, const float* local, int F, int C, int R, i
                                       int, long long, cudaStream_t);                            \
   template void launch_lrn_pool_fwd<T>(const T*, T*, uint8_t*, int, int, int, int, int, float,   \
                                        float, float, int, int, int, int, cudaStream_t, OutLayout); \
-  template void launch_lrn_pool_bwd<T>(const float*, const uint8_t*, const T*, T*, int, int, int, \
-                                       int, int, float, float, float, int, int, int, int, int,  \
-                                       cudaStream_t, OutLayout);                                \
+  template int launch_lrn_pool_bwd<T>(const float*, const uint8_t*, const T*, T*, int, int, int, \
+                                      int, int, float, float, float, int, int, int, int, int,  \
+                                      cudaStream_t, OutLayout, float*);                        \
   template void launch_maxpool_fwd_w<T>(const T*, T*, uint8_t*, int, int, int, int, int, int, int, \
                                         int, cudaStream_t, OutLayout);                          \
   template void launch_rotate_weights<T>(const float*, long long, T*, int, int, int, int,       \

@@ -8,7 +8,10 @@ AlexNet-1col training step at the bench's own shapes:
   k1b  K=1, scheme B, exact SGD, b=128          (configs[2] at N=1 -- bench.py's step)
   k2c  K=2, scheme C, approximate (variable), b=128 per worker  (configs[3]'s mode)
 
-on the same seeded synthetic inputs the product generates (specs.synthetic_batch,
+each with the oracle in plain double (the reference restatement) and in
+bf16-storage mode (k1bq / k2cq: tensors rounded to bf16 exactly where the
+B200 bf16 math mode stores them, so pool argmax and ReLU decisions are taken on
+the same values -- see oracle/hpsim_oracle.c), on the same seeded synthetic inputs the product generates (specs.synthetic_batch,
 GaussianSampler replay) and the same initial weights (init_model replay). A full
 AlexNet step costs the oracle minutes of CPU, so the result is committed: per
 parameter tensor, the max |value| over the FULL tensor and the values at a fixed
@@ -33,7 +36,8 @@ import paper_1404_5997_b200 as hp  # noqa: E402
 SAMPLE = 131072
 PRIME = 2654435761  # > every tensor size here, so the strided sample has no repeats
 HYPER = (0.9, 0.01, 5e-4)  # momentum, lr, weight decay
-CASES = {"k1b": (1, "B", False), "k2c": (2, "C", True)}
+CASES = {"k1b": (1, "B", False, "double"), "k2c": (2, "C", True, "double"),
+         "k1bq": (1, "B", False, "bf16"), "k2cq": (2, "C", True, "bf16")}
 B = 128
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "alexnet_step1.npz")
 
@@ -49,12 +53,13 @@ def main(only=None):
     out = dict(np.load(OUT)) if os.path.exists(OUT) else {}
     out["hyper"] = np.array(HYPER)
     out["b"] = np.array([B])
-    for name, (K, scheme, var) in CASES.items():
+    for name, (K, scheme, var, storage) in CASES.items():
         if only and name not in only:
             continue
         t0 = time.time()
         o = O.OracleCluster(spec, workers=K, per_worker_batch=B, scheme=scheme, variable_batch=var,
                             precision="single", seed=1)
+        o.set_storage_rounding(storage)
         xs, ts = zip(*[hp.synthetic_batch(spec, B, step=0, worker=w) for w in range(K)])
         m = o.run_step([x.astype(np.float64) for x in xs], [t.astype(np.float64) for t in ts],
                        O.make_hyper_c(*HYPER))

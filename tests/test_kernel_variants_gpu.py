@@ -1,32 +1,39 @@
-"""Kernel variants that must agree bit for bit (GPU). The flat shuffle-halo
-LRN+pool kernels (conv1: 8-channel vectors, conv2: 12-channel vectors) are the
-default; HP_DEV_LRN_BWD_SMEM=1 / HP_DEV_LRN_FWD_SMEM=1 select the smem kernels
-they replaced. The switch is read once per process, so each variant runs an
-AlexNet-1col bf16 step sequence in its own subprocess and the parameter bytes
-are compared."""
+"""Kernel variants that must agree (GPU). The row-streaming LRN+pool kernels
+(TMA row rings, LRN computed once per pixel, the bias gradient fused into the
+backward) are the default; HP_DEV_LRN_BWD_SMEM=1 / HP_DEV_LRN_FWD_SMEM=1 select
+the smem-band kernels (same pinned LRN arithmetic, kernels.cu lrn_scale5 /
+lrn_bwd_out). The switch is read once per process, so each variant runs one
+AlexNet-1col step in its own subprocess and the parameters are compared: every
+weight tensor and fc bias bit for bit; the conv biases of the LRN stages to
+fp32 summation order (the smem path sums dz with the separate colsum kernel,
+the row path per block in the backward)."""
+import json
 import os
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 SCRIPT = r"""
-import hashlib, sys
+import hashlib, json, sys
 sys.path.insert(0, {root!r})
 import numpy as np
 import paper_1404_5997_b200 as hp
 spec = hp.alexnet_1col()
 c = hp.Cluster(spec, hp.ClusterConfig(workers=1, per_worker_batch=32, seed=5, math_mode=hp.MathMode.{math}))
-for s in range(2):
-    x, t = hp.synthetic_batch(spec, 32, step=s)
-    r = c.run_step([x], [t], hp.HyperParams(momentum=0.9, lr=1e-3, weight_decay=5e-4))
-h = hashlib.sha256()
+x, t = hp.synthetic_batch(spec, 32, step=0)
+r = c.run_step([x], [t], hp.HyperParams(momentum=0.9, lr=1e-3, weight_decay=5e-4))
+out = {{"loss": r.metrics.loss, "hash": {{}}, "conv_b": {{}}}}
 for which in range(4):
     for l in range(len(spec.conv_layers) if which < 2 else len(spec.fc_layers)):
-        h.update(np.ascontiguousarray(c.param(0, which, l)).tobytes())
-print(repr(r.metrics.loss), h.hexdigest())
+        v = np.ascontiguousarray(c.param(0, which, l))
+        out["hash"][f"{{which}}_{{l}}"] = hashlib.sha256(v.tobytes()).hexdigest()
+        if which == 1:
+            out["conv_b"][str(l)] = v.astype(float).tolist()
+print(json.dumps(out))
 """
 
 
@@ -35,12 +42,19 @@ def run(env_extra, math):
     out = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, math=math)], env=env,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
-    return out.stdout.strip().splitlines()[-1]
+    return json.loads(out.stdout.strip().splitlines()[-1])
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("math", ["BF16", "F32X3"])
-def test_flat_lrn_kernels_match_smem_kernels(math):
-    flat = run({}, math)
-    assert flat == run({"HP_DEV_LRN_BWD_SMEM": "1"}, math)
-    assert flat == run({"HP_DEV_LRN_FWD_SMEM": "1"}, math)
+def test_row_lrn_kernels_match_smem_kernels(math):
+    rows = run({}, math)
+    for env in ({"HP_DEV_LRN_FWD_SMEM": "1"}, {"HP_DEV_LRN_BWD_SMEM": "1"}):
+        alt = run(env, math)
+        assert alt["loss"] == rows["loss"], env
+        for k, h in rows["hash"].items():
+            if k in ("1_0", "1_1") and "HP_DEV_LRN_BWD_SMEM" in env:
+                a, b = np.array(rows["conv_b"][k[2:]]), np.array(alt["conv_b"][k[2:]])
+                assert np.abs(a - b).max() <= 1e-6 * np.abs(a).max(), (env, k)
+            else:
+                assert alt["hash"][k] == h, (env, k)

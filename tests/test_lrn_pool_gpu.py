@@ -111,7 +111,7 @@ def test_pool_argmax_bit_exact(math, shape):
     """Identity LRN (alpha=0, k=1) and pool-only: the GPU pools exactly the
     oracle's values, so every window's argmax must be identical -- ties
     (first maximum, strict >), ReLU zeros and NaN (first NaN wins) included.
-    Shapes: AlexNet conv1 / conv2 (flat kernels), conv5 (pool-only kernel), and
+    Shapes: AlexNet conv1 / conv2 (row-streaming kernels), conv5 (pool-only kernel), and
     an odd one (smem-band kernel)."""
     B, H, W, Cc = shape
     for n in (5, 0):
@@ -148,10 +148,14 @@ def test_lrn_pool_forward_backward(math, shape):
     gy = rng.normal(size=(B, PH, PW, Cc))
     gyd = torch.from_numpy(gy.astype(np.float32)).cuda()
     dz = torch.empty_like(ad)
+    bias = torch.full((Cc,), float("nan"), device="cuda")
     rc = lib.hp_kernel_lrn_pool_bwd(math, gyd.data_ptr(), widx.data_ptr(), ad.data_ptr(), B, H, W, Cc, n, alpha,
-                                    beta, k, pk, ps, 1, dz.data_ptr(), None)
+                                    beta, k, pk, ps, 1, dz.data_ptr(), bias.data_ptr(), None)
     assert rc == 0
     torch.cuda.synchronize()
+    # fused bias gradient = channel sums of the STORED dz (fp32 sums vs double)
+    dsum = _host(dz).astype(np.float64).sum(axis=(0, 1, 2))
+    assert np.abs(bias.cpu().numpy() - dsum).max() <= 1e-5 * np.abs(_host(dz)).sum(axis=(0, 1, 2)).max()
     gb = np.zeros_like(a_nchw)
     gyo = np.ascontiguousarray(gy.astype(np.float32).astype(np.float64).transpose(0, 3, 1, 2))
     O.oracle_lib().or_maxpool_backward(O._dp(gyo), np.ascontiguousarray(gi).ctypes.data_as(C.POINTER(C.c_int32)),
@@ -176,7 +180,7 @@ def test_maxpool_backward_routes_exactly(math):
     gyd = torch.from_numpy(gy).cuda()
     dz = torch.empty_like(ad)
     assert lib.hp_kernel_lrn_pool_bwd(math, gyd.data_ptr(), widx.data_ptr(), ad.data_ptr(), B, H, W, Cc, 0, 0.0,
-                                      0.75, 1.0, 3, 2, 1, dz.data_ptr(), None) == 0
+                                      0.75, 1.0, 3, 2, 1, dz.data_ptr(), None, None) == 0
     torch.cuda.synchronize()
     gx = np.zeros_like(a_nchw)
     O.oracle_lib().or_maxpool_backward(O._dp(np.ascontiguousarray(gy.astype(np.float64).transpose(0, 3, 1, 2))),

@@ -76,6 +76,8 @@ def test_alexnet_k8_scheme_c_variable_runs():
     assert r.metrics.fc_update_count == K and r.metrics.conv_update_count == 1
     bs, trace, _ = hp.step_accounting(spec, cfg)
     assert list(r.metrics.bytes_sent) == bs
-    assert len(r.trace) == 2 + 2 * K
+    # conv_fwd, (fc_fwd j, fc_bwd j) x K, conv_bwd, sync -- the host accounting's events
+    assert [(e.phase, e.sub_batch, e.worker, e.bytes_total, e.bytes_max_sender) for e in r.trace] == trace
+    assert len(r.trace) == 3 + 2 * K
     for w in range(1, K):
         assert np.array_equal(g.param(w, 0, 4), g.param(0, 0, 4))

@@ -60,6 +60,7 @@ def compare(spec, K, scheme, var, math, b, steps=2, lr=0.05, wscale=1.0, seed=1,
         assert [(e.phase, e.sub_batch, e.worker, e.bytes_total, e.bytes_max_sender) for e in r.trace] == o.trace()
         assert r.metrics.fc_update_count == m.fc_update_count
         assert r.metrics.conv_update_count == m.conv_update_count
+    bad = []
     for w in range(K):
         assert g.worker_bytes(w) == o.worker_bytes(w)
         for which in range(8):
@@ -68,7 +69,9 @@ def compare(spec, K, scheme, var, math, b, steps=2, lr=0.05, wscale=1.0, seed=1,
                 if os.environ.get("HP_TOL_REPORT"):
                     print(f"TOL {math.name} K={K} {scheme} var={var} b={b} ws={wscale} w{w} p{which} l{l} {e:.3e}")
                 # biases start at zero, so (like momenta) they are pure gradient history
-                assert e <= (mt if (which >= 4 or which in (1, 3)) else wt), (w, which, l, e)
+                if e > (mt if (which >= 4 or which in (1, 3)) else wt):
+                    bad.append((w, which, l, e))
+    assert not bad, bad
     # replica consistency: conv replicas identical across workers (unless the
     # negative control skipped the broadcast)
     for w in range(1, K):
@@ -114,7 +117,10 @@ def test_last_fc_layer_relu():
     backward and the boundary return."""
     spec = hp.tiny_cnn()
     spec.fc_layers[-1].relu = True
-    compare(spec, 2, "C", False, hp.MathMode.F32X3, 8, steps=2, lr=0.001, wscale=30.0)
+    # weights x10: logits well away from 0 (x30 makes step 2 chaotic -- the same
+    # 1e-2 divergence appears with or without the ReLU, tests/dev/relu_probe.py)
+    compare(spec, 2, "C", False, hp.MathMode.F32X3, 8, steps=2, lr=0.001, wscale=10.0)
+    compare(spec, 2, "A", False, hp.MathMode.F32X3, 8, steps=2, lr=0.001, wscale=10.0)
     compare(spec, 1, "B", False, hp.MathMode.BF16, 16, steps=1)
 
 
