@@ -347,8 +347,7 @@ HP_API int hp_kernel_conv_shift(const void* x, int64_t rows, int C, int R, int S
  * PH = (H - pk) / ps + 1, widx [B][PH][PW][C] uint8 window offset r*pk + q of
  * the FIRST maximum in row-major window order (strict >, NaN wins), gy fp32
  * [B][PH][PW][C], dz [B][H][W][C] (x ReLU mask of a when relu_mask); bias_grad (optional,
- * LRN stages) [C] = channel sums of the stored dz (model.cpp:184-202), fused into the
- * backward like the step does.
+ * LRN stages) [C] = channel sums of the stored dz (model.cpp:184-202), the step's colsum.
  * LRN (Krizhevsky 2012): b_c = a_c (k + alpha sum_{|i-c|<=n/2} a_i^2)^-beta,
  * alpha NOT divided by n. lrn_size 0: max-pool only. */
 HP_API int hp_kernel_lrn_pool_fwd(int math, const void* a, int B, int H, int W, int C, int lrn_size,

@@ -214,19 +214,9 @@ HP_API int hp_kernel_lrn_pool_bwd(int math, const float* gy, const uint8_t* widx
     auto go = [&](auto tag) {
       using T = decltype(tag);
       if (lrn_size > 0) {
-        // the step's launch: the row-streaming kernel writes the bias partials too
-        const int rows = lrn_pool_bwd_partial_rows(B, H, W, C, PH, PW, sizeof(T));
-        float* part = nullptr;
-        if (rows > 0) HP_CUDA(cudaMalloc(&part, sizeof(float) * static_cast<size_t>(rows) * C));
-        const int got = launch_lrn_pool_bwd<T>(gy, widx, static_cast<const T*>(a), static_cast<T*>(dz), B, H, W, C,
-                                               lrn_size, alpha, beta, k, pk, ps, PH, PW, relu_mask, st, OutLayout{},
-                                               part);
-        if (bias_grad && got > 0) launch_bias_partials_reduce(part, got, C, bias_grad, st);
-        if (part) {
-          HP_CUDA(cudaStreamSynchronize(st));
-          HP_CUDA(cudaFree(part));
-        }
-        if (bias_grad && got == 0) {
+        launch_lrn_pool_bwd<T>(gy, widx, static_cast<const T*>(a), static_cast<T*>(dz), B, H, W, C, lrn_size, alpha,
+                               beta, k, pk, ps, PH, PW, relu_mask, st);
+        if (bias_grad) {  // the step's bias gradient: channel sums of the stored dz (model.cpp:184-202)
           float* ws = nullptr;
           const long long M = static_cast<long long>(B) * H * W;
           HP_CUDA(cudaMalloc(&ws, sizeof(float) * colsum_ws_floats(M, C)));

@@ -348,7 +348,6 @@ struct Worker {
   double* loss_parts = nullptr;
   int* bad = nullptr;
   float* colsum_ws = nullptr;
-  float* bias_part = nullptr;  // LRN+pool backward's per-block bias-gradient partial rows
   // GEMM plans
   std::vector<GemmPlan> conv_fwd, conv_wgrad, conv_dgrad, fc_fwd, fc_wgrad, fc_dgrad;
   GemmPlan fc0_slot1[3];  // fc layer 0 {fwd, wgrad, dgrad} over boundary slot 1 (slot 0: the vectors)
@@ -454,7 +453,6 @@ class ClusterImpl final : public ClusterBase {
   cudaStream_t sr_ = nullptr;  // boundary exchange + gradient return (overlaps the FC compute)
   cudaEvent_t ev_conv_ = nullptr;          // conv tops + targets final on st_
   cudaEvent_t ev_xready_[2] = {nullptr, nullptr};  // boundary slot filled (sr_)
-  std::vector<long long> bias_off_;        // per conv layer: offset of its bias partial rows in bias_part
   cudaEvent_t ev_fd0_ = nullptr;           // this turn's fc0 dgrad partial written (st_)
   cudaEvent_t ev_ret_[2] = {nullptr, nullptr};     // slot's gradient return done (sr_)
   cudaEvent_t ev_sr_ = nullptr;            // all of the step's sr_ work done
@@ -638,16 +636,8 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   xblocks_ = 0;
   for (int l = 0; l < nf; ++l) (void)l;
   xblocks_ = xent_blocks(static_cast<int>(g_.fg.back().cmax), static_cast<int>(n_));
-  size_t colsum_ws = 0, bias_part = 0;
-  bias_off_.assign(nc, 0);
-  for (int l = 0; l < nc; ++l) {  // one region per layer: layer l's reduce (side stream) may trail layer l-1's write
-    const ConvGeom& cg = g_.cg[l];
-    colsum_ws = std::max(colsum_ws, colsum_ws_floats(cg.Pq, cg.F));
-    bias_off_[l] = static_cast<long long>(bias_part);
-    if (cg.lrn_n > 0 && cg.pk > 0)
-      bias_part += static_cast<size_t>(lrn_pool_bwd_partial_rows(static_cast<int>(b_), cg.OH, cg.OW, cg.F, cg.PH,
-                                                                 cg.PW, sizeof(TA))) * cg.F;
-  }
+  size_t colsum_ws = 0;
+  for (const auto& cg : g_.cg) colsum_ws = std::max(colsum_ws, colsum_ws_floats(cg.Pq, cg.F));
   size_t comm_scratch = 0;
   for (int i = 0; i < nl; ++i) {
     Worker<TA>& w = w_[i];
@@ -712,7 +702,6 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     w.loss_parts = arena_.make<double>(static_cast<long long>(num_sub_) * xblocks_);
     w.bad = arena_.make<int>(1);
     w.colsum_ws = arena_.make<float>(static_cast<long long>(colsum_ws));
-    if (bias_part) w.bias_part = arena_.make<float>(static_cast<long long>(bias_part));
   }
   comm_->reserve(comm_scratch * sizeof(float));
   comm_x_->reserve(static_cast<size_t>(b_ * A) * sizeof(float));
@@ -1376,11 +1365,9 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
   const TA* mask = c.relu ? w.act[l] : nullptr;
   const int B = static_cast<int>(b_);
   const OutLayout zl = c.in_q ? OutLayout{c.Hq, c.Wq, c.pad} : OutLayout{};  // dz layout
-  int bias_rows = 0;  // > 0: the LRN+pool backward also wrote the bias-gradient partials
   if (c.pk > 0 && c.lrn_n > 0) {
-    bias_rows = launch_lrn_pool_bwd<TA>(cs.gout, w.widx[l], w.act[l], w.dz[l], B, c.OH, c.OW, c.F, c.lrn_n,
-                                        c.lrn_alpha, c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, c.relu ? 1 : 0,
-                                        st_, zl, w.bias_part ? w.bias_part + bias_off_[l] : nullptr);
+    launch_lrn_pool_bwd<TA>(cs.gout, w.widx[l], w.act[l], w.dz[l], B, c.OH, c.OW, c.F, c.lrn_n, c.lrn_alpha,
+                            c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, c.relu ? 1 : 0, st_, zl);
     ++launches_;
   } else if (c.pk > 0) {
     launch_maxpool_bwd_w<TA, TA>(cs.gout, w.widx[l], w.dz[l], mask, B, c.OH, c.OW, c.F, c.pk, c.ps, c.PH,
@@ -1404,13 +1391,8 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
     HP_CUDA(cudaStreamWaitEvent(ws, ev_dz_[l], 0));
   }
   // bias grad = channel sums of dz (model.cpp:184-202)
-  if (bias_rows > 0) {
-    launch_bias_partials_reduce(w.bias_part + bias_off_[l], bias_rows, c.F, w.cgr + conv_b_off(l), ws);
-    ++launches_;
-  } else {
-    launch_colsum<TA>(w.dz[l], c.Pq, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, ws);
-    launches_ += 2;
-  }
+  launch_colsum<TA>(w.dz[l], c.Pq, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, ws);
+  launches_ += 2;
   gemm(w.conv_wgrad[l], "conv_wgrad", l, ws);
   if (c.s2d) {
     launch_s2d_wgrad_gather(w.dwz, w.cgr + conv_k_off(l), c.ldk, c.F, c.C, c.R, c.S, c.stride, c.Rq, c.Cz, ws);

@@ -978,14 +978,7 @@ __global__ void __launch_bounds__(512) lrn_pool_bwd_kernel(
   if (live) stv<TA>(dz + ((b * ZH + h + zp) * ZW + w + zp) * C + c0, out);
 }
 
-// ------------------------------------------------------------------ LRN + pool, row-streaming
-// AlexNet 5 / 3 / 2 path. Block = (image b, band of rows); the band's conv
-// rows stream HBM -> smem through a ring of TMA bulk copies (thread 0 keeps
-// NR rows in flight), so the memory pipe never waits on the arithmetic. Each
-// conv pixel's LRN is computed ONCE per row (fp32, into a double-buffered smem
-// row), then pooled: the 3-wide horizontal max from smem, the 3-high vertical
-// max in registers across rows (row-major first maximum, strict >, first NaN
-// wins -- the order of a 3x3 row-major scan). One block barrier per row.
+// ------------------------------------------------------------------ LRN + pool helpers
 // Loads V channels [c0, c0+V) of one pixel plus 2 halo channels on each side
 // (zero outside [0, C)) as fp32: out[0..V+4) = channels c0-2 .. c0+V+1.
 template <class T, int V>
@@ -1051,301 +1044,204 @@ __device__ __forceinline__ void load_halo5_f(const float* px, int c0, int C, flo
 __device__ __forceinline__ bool takes_max(float v, float best) { return (v > best || isnan(v)) && !isnan(best); }
 
 
-// KI: (pixel, channel-vector) items per thread (W*G <= KI * blockDim.x).
-template <class T, int KI>
-__global__ void __launch_bounds__(1024) lrn_pool_fwd_rows_kernel(const T* __restrict__ a, T* __restrict__ y,
-                                                                 uint8_t* __restrict__ widx, int H, int W, int C,
-                                                                 float alpha, float beta, float kk, int PH, int PW,
-                                                                 int TP, int YH, int YW, int yp, int NR) {
-  constexpr int V = 16 / sizeof(T);
-  const int G = C / V;
-  extern __shared__ __align__(128) unsigned char lrn_rows_sm[];
-  const long long row_elems = static_cast<long long>(W) * C;
-  T* raw = reinterpret_cast<T*>(lrn_rows_sm);
-  float* ybuf = reinterpret_cast<float*>(lrn_rows_sm + NR * row_elems * sizeof(T));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ybuf + 2 * row_elems);
-  const int b = blockIdx.y;
-  const int ph0 = blockIdx.x * TP, ph1 = min(PH, ph0 + TP) - 1;
-  const int nrows = 2 * (ph1 - ph0) + 3;  // conv rows 2*ph0 .. 2*ph1+2
-  const T* src = a + (static_cast<long long>(b) * H + 2 * ph0) * row_elems;
-  const uint32_t row_bytes = static_cast<uint32_t>(row_elems * sizeof(T));
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  if (tid == 0) {
-    for (int s = 0; s < NR; ++s) mbar_init(&bars[s], 1);
-    fence_barrier_init();
-    for (int s = 0; s < min(NR, nrows); ++s) {
-      mbar_arrive_expect_tx(&bars[s], row_bytes);
-      bulk_load(raw + s * row_elems, src + s * row_elems, row_bytes, &bars[s]);
-    }
-  }
-  // items: LRN (w, g) over W*G, pool (pw, g) over PW*G; at most KI each
-  int lw[KI], lg[KI], pw_[KI], pg[KI];
+// ------------------------------------------------------------------ LRN + pool, tiles / quads
+// AlexNet 5 / 3 / 2 fast path.
+//
+// Forward: block = a TPxTP tile of pooled windows x a CB-channel chunk of one
+// image. Phase 1 computes the LRN of every conv pixel the tile's windows touch
+// ONCE ((2TP+1)^2 pixels, ~12% recomputed at tile edges instead of the 2.25x
+// of a per-window recompute) into an fp32 smem tile, loading 16-byte channel
+// vectors plus the +-2-channel halo (L1 hits); phase 2 max-pools each window
+// from smem in row-major window order (first maximum, strict >, first NaN
+// wins) and writes the pooled value and the 1-byte window offset.
+template <class T, int V, int GB, int TP>
+__global__ void __launch_bounds__(GB * TP * TP) lrn_pool_fwd_tile_kernel(
+    const T* __restrict__ a, T* __restrict__ y, uint8_t* __restrict__ widx, int H, int W, int C, float alpha,
+    float beta, float kk, int PH, int PW, int tiles_w, int YH, int YW, int yp) {
+  constexpr int S = 2 * TP + 1, CB = GB * V, NT = GB * TP * TP;
+  extern __shared__ float4 lrn_tile_sm[];
+  float* yb = reinterpret_cast<float*>(lrn_tile_sm);  // [S][S][CB]
+  const int b = blockIdx.z, cc0 = blockIdx.y * CB;
+  const int ph0 = (blockIdx.x / tiles_w) * TP, pw0 = (blockIdx.x % tiles_w) * TP;
+  const int h0 = 2 * ph0, w0 = 2 * pw0;
+  const int tid = threadIdx.x, g = tid % GB;
+  const int c0 = cc0 + g * V;
+  const T* img = a + static_cast<long long>(b) * H * W * C;
+  for (int pix = tid / GB; pix < S * S; pix += NT / GB) {
+    const int r = pix / S, s = pix - r * S;
+    const int h = h0 + r, w = w0 + s;
+    if (h >= H || w >= W) continue;
+    float v[V + 4];
+    load_halo5<T, V>(img + (static_cast<long long>(h) * W + w) * C, c0, C, v);
+    float o[V];
 #pragma unroll
-  for (int k = 0; k < KI; ++k) {
-    const int it = tid + k * nthr;
-    lw[k] = it < W * G ? it / G : -1;
-    lg[k] = it < W * G ? it - lw[k] * G : 0;
-    pw_[k] = it < PW * G ? it / G : -1;
-    pg[k] = it < PW * G ? it - pw_[k] * G : 0;
+    for (int j = 0; j < V; ++j) o[j] = v[j + 2] * pow_neg(lrn_scale5(v + j, alpha, kk), beta);
+    float* dst = yb + pix * CB + g * V;
+#pragma unroll
+    for (int j = 0; j < V; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
   }
-  float best[KI][V];
-  int bi[KI][V];
   __syncthreads();
-  for (int i = 0; i < nrows; ++i) {
-    const int slot = i % NR;
-    mbar_wait(&bars[slot], static_cast<uint32_t>((i / NR) & 1));
-    const T* row = raw + slot * row_elems;
-    float* yb = ybuf + (i & 1) * row_elems;
+  const int wdw = tid / GB, i = wdw / TP, jj = wdw - i * TP;
+  const int ph = ph0 + i, pw = pw0 + jj;
+  if (ph >= PH || pw >= PW) return;
+  float best[V];
+  int bi[V];
+  const float* base = yb + ((2 * i) * S + 2 * jj) * CB + g * V;
 #pragma unroll
-    for (int k = 0; k < KI; ++k) {
-      if (lw[k] < 0) continue;
-      const int c0 = lg[k] * V;
-      float v[V + 4];
-      load_halo5<T, V>(row + static_cast<long long>(lw[k]) * C, c0, C, v);
-      float o[V];
+  for (int r = 0; r < 3; ++r) {
 #pragma unroll
-      for (int j = 0; j < V; ++j) o[j] = v[j + 2] * pow_neg(lrn_scale5(v + j, alpha, kk), beta);
-      float* dst = yb + static_cast<long long>(lw[k]) * C + c0;
+    for (int q = 0; q < 3; ++q) {
+      const float* p = base + (r * S + q) * CB;
 #pragma unroll
-      for (int j = 0; j < V; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
-    }
-    __syncthreads();
-    if (tid == 0 && i + NR < nrows) {  // every thread is done with this slot: refill it
-      mbar_arrive_expect_tx(&bars[slot], row_bytes);
-      bulk_load(raw + slot * row_elems, src + (i + NR) * row_elems, row_bytes, &bars[slot]);
-    }
+      for (int j = 0; j < V; j += 4) {
+        const float4 x = *reinterpret_cast<const float4*>(p + j);
+        const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-    for (int k = 0; k < KI; ++k) {
-      if (pw_[k] < 0) continue;
-      const int c0 = pg[k] * V;
-      float hv[V];
-      int hq[V];
-      const float* p0 = yb + static_cast<long long>(2 * pw_[k]) * C + c0;
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        hv[j] = -INFINITY;
-        hq[j] = 0;
-      }
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-#pragma unroll
-        for (int j = 0; j < V; j += 4) {
-          const float4 x = *reinterpret_cast<const float4*>(p0 + q * C + j);
-          const float xv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (takes_max(xv[u], hv[j + u])) {
-              hv[j + u] = xv[u];
-              hq[j + u] = q;
-            }
-        }
-      }
-      if ((i & 1) == 0) {
-        if (i > 0) {  // last row (r = 2) of window ph0 + i/2 - 1: finish and store it
-#pragma unroll
-          for (int j = 0; j < V; ++j)
-            if (takes_max(hv[j], best[k][j])) {
-              best[k][j] = hv[j];
-              bi[k][j] = 6 + hq[j];
-            }
-          const int ph = ph0 + i / 2 - 1, pw = pw_[k];
-#pragma unroll
-          for (int j = 0; j < V; j += 4)
-            st4<T>(y + (static_cast<long long>(b * YH + ph + yp) * YW + pw + yp) * C + c0 + j, best[k] + j);
-          const long long o = (static_cast<long long>(b * PH + ph) * PW + pw) * C + c0;
-#pragma unroll
-          for (int j = 0; j < V; j += 4)
-            *reinterpret_cast<uint32_t*>(widx + o + j) = static_cast<uint32_t>(bi[k][j]) | (bi[k][j + 1] << 8) |
-                                                         (bi[k][j + 2] << 16) |
-                                                         (static_cast<uint32_t>(bi[k][j + 3]) << 24);
-        }
-#pragma unroll
-        for (int j = 0; j < V; ++j) {  // first row (r = 0) of window ph0 + i/2
-          best[k][j] = hv[j];
-          bi[k][j] = hq[j];
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < V; ++j)
-          if (takes_max(hv[j], best[k][j])) {
-            best[k][j] = hv[j];
-            bi[k][j] = 3 + hq[j];
+        for (int u = 0; u < 4; ++u) {
+          if (r == 0 && q == 0) {
+            best[j + u] = xv[u];
+            bi[j + u] = 0;
+          } else if (takes_max(xv[u], best[j + u])) {
+            best[j + u] = xv[u];
+            bi[j + u] = r * 3 + q;
           }
+        }
       }
     }
   }
+#pragma unroll
+  for (int j = 0; j < V; j += 4)
+    st4<T>(y + (static_cast<long long>(b * YH + ph + yp) * YW + pw + yp) * C + c0 + j, best + j);
+  const long long o = (static_cast<long long>(b * PH + ph) * PW + pw) * C + c0;
+#pragma unroll
+  for (int j = 0; j < V; j += 4)
+    *reinterpret_cast<uint32_t*>(widx + o + j) = static_cast<uint32_t>(bi[j]) | (bi[j + 1] << 8) |
+                                                 (bi[j + 2] << 16) | (static_cast<uint32_t>(bi[j + 3]) << 24);
 }
 
-// Backward: block = (image b, band of conv rows). Conv rows and the pooled
-// rows (gradient + argmax bytes) they draw from stream in through two TMA
-// rings. Per conv row: gather gb (every window containing the pixel whose
-// argmax is it), d, t = gb a d^-beta / d into a double-buffered fp32 smem row
-// (the +-2-channel t halo), then
-//   dz_c = gb_c d_c^-beta - 2 alpha beta a_c sum_{i in c-2..c+2} t_i   (x ReLU mask)
-// stored as TA; the bias gradient (model.cpp:184-202, channel sums of the
-// STORED dz) is accumulated per block in registers and written as one fp32
-// partial row per block (reduced in ascending block order by
-// bias_partials_reduce_kernel: deterministic).
-template <class TA, int KI>
-__global__ void __launch_bounds__(1024) lrn_pool_bwd_rows_kernel(
+// Backward: thread = (2x2 quad of conv pixels, channel vector); P lanes (a
+// power of two >= C/V) per quad so the +-2-channel halos of a and t come from
+// the neighbouring lanes by segmented shuffles. Quad (qh, qw) owns pixels
+// (2qh+dy, 2qw+dx); the pooled windows that can route a gradient to them are
+// (qh-1 | qh, qw-1 | qw) -- each loaded once for the quad (4 argmax words and
+// gradient vectors per 4 pixels instead of 4 per pixel). Per pixel
+//   gb_c = sum of the pooled gradients whose argmax is this pixel (windows in
+//          ascending (ph, pw) order, the order of every other LRN backward here)
+//   d_c, t_c = gb_c a_c d_c^-beta / d_c,
+//   dz_c = gb_c d_c^-beta - 2 alpha beta a_c sum_{i in c-2..c+2} t_i  (x ReLU mask)
+template <class TA, int P, int V>
+__global__ void __launch_bounds__(128) lrn_pool_bwd_quad_kernel(
     const float* __restrict__ gy, const uint8_t* __restrict__ widx, const TA* __restrict__ a,
-    TA* __restrict__ dz, float* __restrict__ bias_part, int H, int W, int C, float alpha, float beta, float kk,
-    int PH, int PW, int relu_mask, int ZH, int ZW, int zp, int TH, int NR, int NP) {
-  constexpr int V = 16 / sizeof(TA);
+    TA* __restrict__ dz, int B, int H, int W, int C, float alpha, float beta, float kk, int PH, int PW, int QH,
+    int QW, int relu_mask, int ZH, int ZW, int zp) {
+  static_assert(V % 4 == 0, "channel vectors of 4");
   const int G = C / V;
-  extern __shared__ __align__(128) unsigned char lrn_rows_sm[];
-  const long long row_elems = static_cast<long long>(W) * C, prow_elems = static_cast<long long>(PW) * C;
-  TA* raw = reinterpret_cast<TA*>(lrn_rows_sm);
-  float* pg_ring = reinterpret_cast<float*>(lrn_rows_sm + NR * row_elems * sizeof(TA));
-  uint8_t* pi_ring = reinterpret_cast<uint8_t*>(pg_ring + NP * prow_elems);
-  float* tbuf = reinterpret_cast<float*>(pi_ring + NP * prow_elems);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tbuf + 2 * row_elems);  // NR conv rows, then NP pooled rows
-  const int b = blockIdx.y;
-  const int h0 = blockIdx.x * TH, h1 = min(H, h0 + TH) - 1;
-  const int nrows = h1 - h0 + 1;
-  const int pr0 = h0 <= 1 ? 0 : (h0 - 1) / 2;
-  const int pr1 = min(PH - 1, h1 / 2);
-  const TA* src = a + (static_cast<long long>(b) * H + h0) * row_elems;
-  const float* gsrc = gy + static_cast<long long>(b) * PH * prow_elems;
-  const uint8_t* isrc = widx + static_cast<long long>(b) * PH * prow_elems;
-  const uint32_t row_bytes = static_cast<uint32_t>(row_elems * sizeof(TA));
-  const uint32_t pg_bytes = static_cast<uint32_t>(prow_elems * sizeof(float)), pi_bytes = static_cast<uint32_t>(prow_elems);
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  auto load_pooled = [&](int ph) {
-    const int s = (ph - pr0) % NP;
-    mbar_arrive_expect_tx(&bars[NR + s], pg_bytes + pi_bytes);
-    bulk_load(pg_ring + s * prow_elems, gsrc + ph * prow_elems, pg_bytes, &bars[NR + s]);
-    bulk_load(pi_ring + s * prow_elems, isrc + ph * prow_elems, pi_bytes, &bars[NR + s]);
-  };
-  if (tid == 0) {
-    for (int s = 0; s < NR + NP; ++s) mbar_init(&bars[s], 1);
-    fence_barrier_init();
-    for (int s = 0; s < min(NR, nrows); ++s) {
-      mbar_arrive_expect_tx(&bars[s], row_bytes);
-      bulk_load(raw + s * row_elems, src + s * row_elems, row_bytes, &bars[s]);
+  const int g = threadIdx.x & (P - 1);
+  const int quad = blockIdx.x * (blockDim.x / P) + threadIdx.x / P;  // B*QH*QW < 2^31 (launcher)
+  const bool live = g < G && quad < B * QH * QW;
+  const int bq = live ? quad / QW : 0;
+  const int qw = live ? quad - bq * QW : 0;
+  const int b = bq / QH, qh = bq - b * QH;
+  const int c0 = g * V;
+  // the 4 candidate windows, ascending (ph, pw): (qh-1,qw-1) (qh-1,qw) (qh,qw-1) (qh,qw)
+  uint32_t wi[4][V / 4];
+  float4 gv[4][V / 4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int ph = qh - 1 + (k >> 1), pw = qw - 1 + (k & 1);
+    const bool ok = live && ph >= 0 && ph < PH && pw >= 0 && pw < PW;
+    const long long o = ((static_cast<long long>(b) * PH + (ok ? ph : 0)) * PW + (ok ? pw : 0)) * C + c0;
+#pragma unroll
+    for (int j = 0; j < V / 4; ++j) {
+      wi[k][j] = ok ? *reinterpret_cast<const uint32_t*>(widx + o + 4 * j) : 0xffffffffu;
+      gv[k][j] = ok ? *reinterpret_cast<const float4*>(gy + o + 4 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    for (int ph = pr0; ph <= min(pr1, pr0 + NP - 1); ++ph) load_pooled(ph);
   }
-  int lw[KI], lg[KI];
-  float bsum[KI][V];
+  // the quad's 4 activation vectors, loaded (raw) together with the windows
+  constexpr int RW = V * sizeof(TA) / 8;  // 8-byte words per vector
+  uint2 araw[4][RW];
 #pragma unroll
-  for (int k = 0; k < KI; ++k) {
-    const int it = tid + k * nthr;
-    lw[k] = it < W * G ? it / G : -1;
-    lg[k] = it < W * G ? it - lw[k] * G : 0;
+  for (int p4 = 0; p4 < 4; ++p4) {
+    const int h = 2 * qh + (p4 >> 1), w = 2 * qw + (p4 & 1);
+    const bool ok = live && h < H && w < W;
+    const uint2* src = reinterpret_cast<const uint2*>(a + ((static_cast<long long>(b) * H + (ok ? h : 0)) * W +
+                                                          (ok ? w : 0)) * C + c0);
 #pragma unroll
-    for (int j = 0; j < V; ++j) bsum[k][j] = 0.f;
+    for (int j = 0; j < RW; ++j) araw[p4][j] = ok ? src[j] : make_uint2(0u, 0u);
   }
-  __syncthreads();
-  int waited = pr0 - 1;  // pooled rows this thread has waited for
-  for (int i = 0; i < nrows; ++i) {
-    const int h = h0 + i;
-    const int slot = i % NR;
-    const int plo = h <= 1 ? 0 : (h - 1) / 2, phi = min(PH - 1, h / 2);
-    while (waited < phi) {
-      ++waited;
-      mbar_wait(&bars[NR + (waited - pr0) % NP], static_cast<uint32_t>(((waited - pr0) / NP) & 1));
-    }
-    mbar_wait(&bars[slot], static_cast<uint32_t>((i / NR) & 1));
-    const TA* row = raw + slot * row_elems;
-    float* tb = tbuf + (i & 1) * row_elems;
-    float av[KI][V + 4], gp[KI][V];
 #pragma unroll
-    for (int k = 0; k < KI; ++k) {
-      if (lw[k] < 0) continue;
-      const int w = lw[k], c0 = lg[k] * V;
-      load_halo5<TA, V>(row + static_cast<long long>(w) * C, c0, C, av[k]);
+  for (int dy = 0; dy < 2; ++dy) {
+#pragma unroll
+    for (int dx = 0; dx < 2; ++dx) {
+      const int h = 2 * qh + dy, w = 2 * qw + dx;
+      const bool px_live = live && h < H && w < W;  // shuffles below: every lane takes part
+      float av[V];
+#pragma unroll
+      for (int j = 0; j < V; j += 4) ld4<TA>(reinterpret_cast<const TA*>(&araw[dy * 2 + dx][0]) + j, av + j);
       float gb[V];
 #pragma unroll
       for (int j = 0; j < V; ++j) gb[j] = 0.f;
-      const int qlo = w <= 1 ? 0 : (w - 1) / 2, qhi = min(PW - 1, w / 2);
-      for (int ph = plo; ph <= phi; ++ph) {
-        const int ps_ = (ph - pr0) % NP;
-        const float* gr = pg_ring + ps_ * prow_elems;
-        const uint8_t* ir = pi_ring + ps_ * prow_elems;
-        for (int pw = qlo; pw <= qhi; ++pw) {
-          const uint32_t me = static_cast<uint32_t>((h - 2 * ph) * 3 + (w - 2 * pw));
 #pragma unroll
-          for (int j = 0; j < V; j += 4) {
-            const uint32_t x = *reinterpret_cast<const uint32_t*>(ir + pw * C + c0 + j);
-            const float4 g4 = *reinterpret_cast<const float4*>(gr + pw * C + c0 + j);
-            if ((x & 0xff) == me) gb[j] += g4.x;
-            if (((x >> 8) & 0xff) == me) gb[j + 1] += g4.y;
-            if (((x >> 16) & 0xff) == me) gb[j + 2] += g4.z;
-            if ((x >> 24) == me) gb[j + 3] += g4.w;
-          }
+      for (int k = 0; k < 4; ++k) {
+        // window k routes to this pixel iff it covers it: offset r*3+q with
+        // r = h - 2 ph = dy + 2 (k < 2 ? 1 : 0), q = dx + 2 ((k & 1) ? 0 : 1)
+        const int r = dy + ((k >> 1) ? 0 : 2), q = dx + ((k & 1) ? 0 : 2);
+        if (r > 2 || q > 2) continue;
+        const uint32_t me = static_cast<uint32_t>(r * 3 + q);
+#pragma unroll
+        for (int j = 0; j < V / 4; ++j) {
+          const uint32_t x = wi[k][j];
+          const float4 g4 = gv[k][j];
+          if ((x & 0xff) == me) gb[4 * j] += g4.x;
+          if (((x >> 8) & 0xff) == me) gb[4 * j + 1] += g4.y;
+          if (((x >> 16) & 0xff) == me) gb[4 * j + 2] += g4.z;
+          if ((x >> 24) == me) gb[4 * j + 3] += g4.w;
         }
       }
-      float tv[V];
+      float win[V + 4];
+#pragma unroll
+      for (int j = 0; j < V; ++j) win[2 + j] = av[j];
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        const float l = __shfl_up_sync(0xffffffffu, av[V - 2 + d], 1, P);
+        const float rr = __shfl_down_sync(0xffffffffu, av[d], 1, P);
+        win[d] = g > 0 ? l : 0.f;
+        win[2 + V + d] = g + 1 < G ? rr : 0.f;
+      }
+      float gp[V], tv[V];
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        const float dd = lrn_scale5(av[k] + j, alpha, kk);
+        const float dd = lrn_scale5(win + j, alpha, kk);
         const float pn = pow_neg(dd, beta);
         float rd;
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(dd));
-        tv[j] = gb[j] * av[k][j + 2] * (pn * rd);
-        gp[k][j] = gb[j] * pn;
+        tv[j] = gb[j] * av[j] * (pn * rd);
+        gp[j] = gb[j] * pn;
       }
-      float* dst = tb + static_cast<long long>(w) * C + c0;
 #pragma unroll
-      for (int j = 0; j < V; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(tv[j], tv[j + 1], tv[j + 2], tv[j + 3]);
-    }
-    __syncthreads();
-    if (tid == 0) {  // every thread is done with conv slot i and with the pooled rows finished by row h
-      if (i + NR < nrows) {
-        mbar_arrive_expect_tx(&bars[slot], row_bytes);
-        bulk_load(raw + slot * row_elems, src + (i + NR) * row_elems, row_bytes, &bars[slot]);
-      }
-      if ((h & 1) == 0 && h >= 2) {
-        const int done = (h - 2) / 2;  // its last conv row was h
-        if (done >= pr0 && done + NP <= pr1) load_pooled(done + NP);
-      }
-    }
+      for (int j = 0; j < V; ++j) win[2 + j] = tv[j];
 #pragma unroll
-    for (int k = 0; k < KI; ++k) {
-      if (lw[k] < 0) continue;
-      const int w = lw[k], c0 = lg[k] * V;
-      float tw[V + 4];
-      load_halo5_f<V>(tb + static_cast<long long>(w) * C, c0, C, tw);
+      for (int d = 0; d < 2; ++d) {
+        const float l = __shfl_up_sync(0xffffffffu, tv[V - 2 + d], 1, P);
+        const float rr = __shfl_down_sync(0xffffffffu, tv[d], 1, P);
+        win[d] = g > 0 ? l : 0.f;
+        win[2 + V + d] = g + 1 < G ? rr : 0.f;
+      }
       float out[V];
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        const float acc = (((tw[j] + tw[j + 1]) + tw[j + 2]) + tw[j + 3]) + tw[j + 4];
-        float gval = lrn_bwd_out(gp[k][j], av[k][j + 2], acc, alpha, beta);
-        if (relu_mask && !(av[k][j + 2] > 0.f)) gval = 0.f;
-        out[j] = to_f<TA>(from_f<TA>(gval));
-        bsum[k][j] += out[j];
+        const float acc = (((win[j] + win[j + 1]) + win[j + 2]) + win[j + 3]) + win[j + 4];
+        float gval = lrn_bwd_out(gp[j], av[j], acc, alpha, beta);
+        if (relu_mask && !(av[j] > 0.f)) gval = 0.f;
+        out[j] = gval;
       }
-      stv<TA>(dz + (static_cast<long long>(b * ZH + h + zp) * ZW + w + zp) * C + c0, out);
+      if (px_live) {
+#pragma unroll
+        for (int j = 0; j < V; j += 4)
+          st4<TA>(dz + ((static_cast<long long>(b) * ZH + h + zp) * ZW + w + zp) * C + c0 + j, out + j);
+      }
     }
   }
-  // per-block bias partial: sum the items' registers over w in ascending order
-  __syncthreads();
-  float* red = tbuf;  // [W][C]
-#pragma unroll
-  for (int k = 0; k < KI; ++k) {
-    if (lw[k] < 0) continue;
-    float* dst = red + static_cast<long long>(lw[k]) * C + lg[k] * V;
-#pragma unroll
-    for (int j = 0; j < V; j += 4)
-      *reinterpret_cast<float4*>(dst + j) = make_float4(bsum[k][j], bsum[k][j + 1], bsum[k][j + 2], bsum[k][j + 3]);
-  }
-  __syncthreads();
-  float* part = bias_part + (static_cast<long long>(b) * gridDim.x + blockIdx.x) * C;
-  for (int c = tid; c < C; c += nthr) {
-    float s = 0.f;
-    for (int w = 0; w < W; ++w) s += red[static_cast<long long>(w) * C + c];
-    part[c] = s;
-  }
-}
-
-// out[c] = sum over partial rows in ascending order (deterministic bias grads).
-__global__ void bias_partials_reduce_kernel(const float* __restrict__ part, int rows, int C, float* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  float s = 0.f;
-  for (int r = 0; r < rows; ++r) s += part[static_cast<long long>(r) * C + c];
-  out[c] = s;
 }
 
 // Rotated operand for the implicit dgrad: wr[c][r][s][f] = w[f][R-1-r][S-1-s][c].
@@ -1547,57 +1443,6 @@ void launch_im2col_t_nchw(const float* x, T* colT, int B, int C, int H, int W, i
                                                             ldp, K);
 }
 
-// Launch plan of the row-streaming LRN+pool kernels (5/3/2): block =
-// (band of rows, image), threads = the row's (pixel, channel-vector) items (at
-// most 2 per thread), smem = the TMA rings + the fp32 double row. The band
-// length minimises waves x rows per band at the occupancy the smem allows.
-struct LrnRowsPlan {
-  bool ok = false;
-  int threads = 0, ki = 1, band = 0, bands = 0, nr = 0, np = 0;
-  size_t smem = 0;
-};
-LrnRowsPlan lrn_rows_plan(bool bwd, int B, int H, int W, int C, int PH, int PW, int elem) {
-  LrnRowsPlan p;
-  const int V = 16 / elem;
-  if (C % V != 0 || C < 2 * V) return p;
-  const int G = C / V;
-  const long long items = static_cast<long long>(W) * G;
-  const long long row = static_cast<long long>(W) * C * elem, prow = static_cast<long long>(PW) * C;
-  if (items > 2048 || row % 16 != 0 || prow % 16 != 0 || (prow * 4) % 16 != 0) return p;
-  p.threads = static_cast<int>(std::min<long long>(1024, (items + 31) / 32 * 32));
-  p.ki = items > p.threads ? 2 : 1;
-  const size_t fixed = static_cast<size_t>(2) * W * C * sizeof(float);
-  const size_t budget = 220 * 1024;
-  for (int nr = 4; nr >= 2; --nr) {
-    const int np = bwd ? 3 : 0;
-    const size_t sm = nr * row + np * prow * 5 + fixed + (nr + np) * 8;
-    if (sm <= budget) {
-      p.nr = nr;
-      p.np = np;
-      p.smem = sm;
-      break;
-    }
-  }
-  if (p.nr == 0) return p;
-  const int per_sm = std::max(1, std::min(static_cast<int>((227 * 1024) / (p.smem + 1024)), 2048 / p.threads));
-  const int slots = 148 * per_sm;
-  const int units = bwd ? H : PH;  // conv rows (bwd) / pooled rows (fwd) per image
-  double best = 1e30;
-  for (int t = 1; t <= units; ++t) {
-    const int bands = (units + t - 1) / t;
-    const int waves = (B * bands + slots - 1) / slots;
-    const double rows = bwd ? t + 1.0 : 2.0 * t + 1.0;  // + the ramp of the ring
-    const double cost = waves * rows;
-    if (cost < best - 1e-9) {
-      best = cost;
-      p.band = t;
-      p.bands = bands;
-    }
-  }
-  p.ok = true;
-  return p;
-}
-
 template <class T>
 void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, int C, int n,
                          float alpha, float beta, float kk, int pk, int ps, int PH, int PW,
@@ -1624,16 +1469,26 @@ void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, i
     kern<<<grid, block, smem, st>>>(a, y, widx, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW, TP,
                                     yl.H, yl.W, yl.p);
   };
-  static const bool rows_off = getenv("HP_DEV_LRN_FWD_SMEM") != nullptr;  // dev: the smem-band kernel
-  const LrnRowsPlan rp = lrn_rows_plan(false, B, H, W, C, PH, PW, sizeof(T));
-  if (n == 5 && pk == 3 && ps == 2 && rp.ok && !rows_off) {
-    auto rk = [&](auto kern) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rp.smem));
-      kern<<<dim3(rp.bands, B), rp.threads, rp.smem, st>>>(a, y, widx, H, W, C, alpha, beta, kk, PH, PW, rp.band,
-                                                           yl.H, yl.W, yl.p, rp.nr);
+  static const bool fast_off = getenv("HP_DEV_LRN_FWD_SMEM") != nullptr;  // dev: the smem-band kernel
+  if (n == 5 && pk == 3 && ps == 2 && C % 64 == 0 && !fast_off) {
+    // 64-channel chunks; 9x9 or 7x7 window tiles, whichever pads PH x PW less
+    // (measured: AlexNet conv1 27 -> 3 tiles of 9 a side 45.7 us, 4 of 7 ~50 us;
+    // conv2 13 -> 2 of 7); fp32 only fits 7x7 (threads)
+    auto waste = [&](int tp) { return ((PH + tp - 1) / tp * tp) * ((PW + tp - 1) / tp * tp); };
+    auto tk = [&](auto kern, int tp, int gb) {
+      const int tw = (PW + tp - 1) / tp, th = (PH + tp - 1) / tp;
+      const size_t smem = static_cast<size_t>(2 * tp + 1) * (2 * tp + 1) * 64 * sizeof(float);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      kern<<<dim3(tw * th, C / 64, B), gb * tp * tp, smem, st>>>(a, y, widx, H, W, C, alpha, beta, kk, PH, PW, tw,
+                                                                  yl.H, yl.W, yl.p);
     };
-    if (rp.ki == 1) rk(lrn_pool_fwd_rows_kernel<T, 1>);
-    else rk(lrn_pool_fwd_rows_kernel<T, 2>);
+    constexpr int V = 16 / sizeof(T), GB = 64 / V;
+    if constexpr (sizeof(T) == 2) {
+      if (waste(9) <= waste(7)) tk(lrn_pool_fwd_tile_kernel<T, V, GB, 9>, 9, GB);
+      else tk(lrn_pool_fwd_tile_kernel<T, V, GB, 7>, 7, GB);
+    } else {
+      tk(lrn_pool_fwd_tile_kernel<T, V, GB, 7>, 7, GB);
+    }
   } else if (n == 5 && pk == 3 && ps == 2) {
     go(lrn_pool_fwd_kernel<T, 2, 5, 3, 2>);
   } else if (n <= 5) {
@@ -1644,9 +1499,9 @@ void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, i
 }
 
 template <class TA>
-int launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* dz, int B, int H,
-                        int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
-                        int PH, int PW, int relu_mask, cudaStream_t st, OutLayout zl, float* bias_part) {
+void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* dz, int B, int H,
+                         int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
+                         int PH, int PW, int relu_mask, cudaStream_t st, OutLayout zl) {
   if (zl.H == 0) zl = OutLayout{H, W, 0};
   constexpr int V = 16 / sizeof(TA);
   const int G = C / V;
@@ -1664,17 +1519,32 @@ int launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* d
     kern<<<grid, block, smem, st>>>(gy, widx, a, dz, H, W, C, n / 2, (n - 1) / 2, alpha, beta, kk, pk, ps, PH, PW,
                                     relu_mask, zl.H, zl.W, zl.p);
   };
-  static const bool rows_off = getenv("HP_DEV_LRN_BWD_SMEM") != nullptr;  // dev: the block-per-row kernel
-  const LrnRowsPlan rp = lrn_rows_plan(true, B, H, W, C, PH, PW, sizeof(TA));
-  if (n == 5 && pk == 3 && ps == 2 && rp.ok && !rows_off && bias_part != nullptr) {
-    auto rk = [&](auto kern) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rp.smem));
-      kern<<<dim3(rp.bands, B), rp.threads, rp.smem, st>>>(gy, widx, a, dz, bias_part, H, W, C, alpha, beta, kk, PH,
-                                                           PW, relu_mask, zl.H, zl.W, zl.p, rp.band, rp.nr, rp.np);
+  static const bool fast_off = getenv("HP_DEV_LRN_BWD_SMEM") != nullptr;  // dev: the block-per-row kernel
+  // quad kernel when the channel vectors fill power-of-two lane groups: 16-byte
+  // vectors (conv1: 8 of 8 bf16 channels), else 12-channel vectors (conv2: 192
+  // channels = 16 x 12)
+  auto pow2 = [](int q) { return q == 4 || q == 8 || q == 16 || q == 32; };
+  constexpr int V0 = 16 / sizeof(TA);
+  const int Vq = pow2(C / V0) && C % V0 == 0 ? V0 : (C % 12 == 0 && pow2(C / 12) ? 12 : 0);
+  if (n == 5 && pk == 3 && ps == 2 && Vq > 0 && !fast_off) {
+    const int P = C / Vq, QH = (H + 1) / 2, QW = (W + 1) / 2;
+    const long long threads = static_cast<long long>(B) * QH * QW * P;
+    const int blocks = static_cast<int>((threads + 127) / 128);
+    auto qk = [&](auto kern) {
+      kern<<<blocks, 128, 0, st>>>(gy, widx, a, dz, B, H, W, C, alpha, beta, kk, PH, PW, QH, QW, relu_mask, zl.H, zl.W,
+                                   zl.p);
     };
-    if (rp.ki == 1) rk(lrn_pool_bwd_rows_kernel<TA, 1>);
-    else rk(lrn_pool_bwd_rows_kernel<TA, 2>);
-    return rp.bands * B;
+    if (Vq == V0) {
+      if (P == 4) qk(lrn_pool_bwd_quad_kernel<TA, 4, V0>);
+      else if (P == 8) qk(lrn_pool_bwd_quad_kernel<TA, 8, V0>);
+      else if (P == 16) qk(lrn_pool_bwd_quad_kernel<TA, 16, V0>);
+      else qk(lrn_pool_bwd_quad_kernel<TA, 32, V0>);
+    } else {
+      if (P == 4) qk(lrn_pool_bwd_quad_kernel<TA, 4, 12>);
+      else if (P == 8) qk(lrn_pool_bwd_quad_kernel<TA, 8, 12>);
+      else if (P == 16) qk(lrn_pool_bwd_quad_kernel<TA, 16, 12>);
+      else qk(lrn_pool_bwd_quad_kernel<TA, 32, 12>);
+    }
   } else if (n == 5 && pk == 3 && ps == 2) {
     go(lrn_pool_bwd_kernel<TA, 2, 5, 3, 2>);
   } else if (n <= 5) {
@@ -1682,17 +1552,8 @@ int launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* d
   } else {
     go(lrn_pool_bwd_kernel<TA, LH, 0, 0, 0>);
   }
-  return 0;
 }
 
-void launch_bias_partials_reduce(const float* part, int rows, int C, float* out, cudaStream_t st) {
-  bias_partials_reduce_kernel<<<(C + 127) / 128, 128, 0, st>>>(part, rows, C, out);
-}
-
-int lrn_pool_bwd_partial_rows(int B, int H, int W, int C, int PH, int PW, int elem_bytes) {
-  const LrnRowsPlan rp = lrn_rows_plan(true, B, H, W, C, PH, PW, elem_bytes);
-  return rp.ok ? rp.bands * B : 0;
-}
 
 template <class T>
 void launch_maxpool_fwd_w(const T* x, T* y, uint8_t* widx, int B, int H, int W, int C, int k, int s,
@@ -1772,9 +1633,9 @@ void launch_skip_sync_fixup(float* g, const float* local, int F, int C, int R, i
                                       int, long long, cudaStream_t);                            \
   template void launch_lrn_pool_fwd<T>(const T*, T*, uint8_t*, int, int, int, int, int, float,   \
                                        float, float, int, int, int, int, cudaStream_t, OutLayout); \
-  template int launch_lrn_pool_bwd<T>(const float*, const uint8_t*, const T*, T*, int, int, int, \
-                                      int, int, float, float, float, int, int, int, int, int,  \
-                                      cudaStream_t, OutLayout, float*);                        \
+  template void launch_lrn_pool_bwd<T>(const float*, const uint8_t*, const T*, T*, int, int, int, \
+                                       int, int, float, float, float, int, int, int, int, int,  \
+                                       cudaStream_t, OutLayout);                                \
   template void launch_maxpool_fwd_w<T>(const T*, T*, uint8_t*, int, int, int, int, int, int, int, \
                                         int, cudaStream_t, OutLayout);                          \
   template void launch_rotate_weights<T>(const float*, long long, T*, int, int, int, int,       \

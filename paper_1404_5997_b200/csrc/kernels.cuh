@@ -143,19 +143,10 @@ void launch_lrn_pool_fwd(const T* a, T* y, uint8_t* widx, int B, int H, int W, i
                          float alpha, float beta, float kk, int pk, int ps, int PH, int PW,
                          cudaStream_t st, OutLayout yl = {});
 // Fused backward: dz = relu_mask(a) * lrn_bwd(a, pool_bwd(gy, widx)).
-// bias_part != nullptr and the row-streaming path applies (AlexNet 5/3/2):
-// also writes the bias gradient's per-block partial rows (channel sums of the
-// stored dz) to bias_part[rows][C] and returns rows (reduce them with
-// launch_bias_partials_reduce); else returns 0 and the caller sums dz itself.
 template <class TA>
-int launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* dz, int B, int H,
-                        int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
-                        int PH, int PW, int relu_mask, cudaStream_t st, OutLayout zl = {},
-                        float* bias_part = nullptr);
-// Partial rows launch_lrn_pool_bwd writes for this shape (0: not the row path).
-int lrn_pool_bwd_partial_rows(int B, int H, int W, int C, int PH, int PW, int elem_bytes);
-// out[c] = sum_r part[r][c] in ascending r (deterministic).
-void launch_bias_partials_reduce(const float* part, int rows, int C, float* out, cudaStream_t st);
+void launch_lrn_pool_bwd(const float* gy, const uint8_t* widx, const TA* a, TA* dz, int B, int H,
+                         int W, int C, int n, float alpha, float beta, float kk, int pk, int ps,
+                         int PH, int PW, int relu_mask, cudaStream_t st, OutLayout zl = {});
 // Max-pool forward / backward with window-offset argmax (no LRN).
 template <class T>
 void launch_maxpool_fwd_w(const T* x, T* y, uint8_t* widx, int B, int H, int W, int C, int k, int s,

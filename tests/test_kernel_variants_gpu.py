@@ -1,18 +1,16 @@
-"""Kernel variants that must agree (GPU). The row-streaming LRN+pool kernels
-(TMA row rings, LRN computed once per pixel, the bias gradient fused into the
-backward) are the default; HP_DEV_LRN_BWD_SMEM=1 / HP_DEV_LRN_FWD_SMEM=1 select
-the smem-band kernels (same pinned LRN arithmetic, kernels.cu lrn_scale5 /
-lrn_bwd_out). The switch is read once per process, so each variant runs one
-AlexNet-1col step in its own subprocess and the parameters are compared: every
-weight tensor and fc bias bit for bit; the conv biases of the LRN stages to
-fp32 summation order (the smem path sums dz with the separate colsum kernel,
-the row path per block in the backward)."""
+"""Kernel variants that must agree bit for bit (GPU). The window-tile LRN+pool
+forward (LRN once per conv pixel into an smem tile, pooled from smem) and the
+quad backward (2x2 conv pixels per thread sharing their 4 candidate windows)
+are the default; HP_DEV_LRN_FWD_SMEM=1 / HP_DEV_LRN_BWD_SMEM=1 select the
+smem-band kernels, which use the same pinned LRN arithmetic (kernels.cu
+lrn_scale5 / lrn_bwd_out) and window order. The switch is read once per
+process, so each variant runs one AlexNet-1col step in its own subprocess and
+every parameter tensor is compared bit for bit."""
 import json
 import os
 import subprocess
 import sys
 
-import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -47,14 +45,10 @@ def run(env_extra, math):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("math", ["BF16", "F32X3"])
-def test_row_lrn_kernels_match_smem_kernels(math):
+def test_tile_quad_lrn_kernels_match_smem_kernels(math):
     rows = run({}, math)
     for env in ({"HP_DEV_LRN_FWD_SMEM": "1"}, {"HP_DEV_LRN_BWD_SMEM": "1"}):
         alt = run(env, math)
         assert alt["loss"] == rows["loss"], env
         for k, h in rows["hash"].items():
-            if k in ("1_0", "1_1") and "HP_DEV_LRN_BWD_SMEM" in env:
-                a, b = np.array(rows["conv_b"][k[2:]]), np.array(alt["conv_b"][k[2:]])
-                assert np.abs(a - b).max() <= 1e-6 * np.abs(a).max(), (env, k)
-            else:
-                assert alt["hash"][k] == h, (env, k)
+            assert alt["hash"][k] == h, (env, k)
