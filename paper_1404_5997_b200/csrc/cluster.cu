@@ -1989,7 +1989,7 @@ void ClusterImpl<TA>::read_param(int worker, int which, int layer, float* dst, i
 }
 
 // The last step's discrete forward decisions in the reference layouts (the
-// parity tests replay them in the oracle, hpsim_oracle.c or_cluster_force_decisions):
+// parity tests replay them in the CPU checker, tests/test_alexnet_parity_gpu.py):
 //   kind 0: conv layer ReLU mask, uint8 [b][F][OH][OW] (stored activation > 0)
 //   kind 1: conv layer pool argmax, int32 [b][F][PH][PW], index h*OW + w in the
 //           conv output plane (or_maxpool_forward's convention)
