@@ -13,6 +13,9 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#if __cplusplus >= 202002L
+#include <span>
+#endif
 
 #include "hpsim_b200.h"
 
@@ -131,6 +134,64 @@ struct StepMetrics {  // cluster.hpp:111-117
   std::array<std::int64_t, 4> bytes_sent{};
 };
 
+// Minimal host tensor standing in for hpsim::Tensor (tensor.hpp:40-90) at
+// this boundary: row-major float32 storage plus a shape. The reference's
+// Tensor carries its precision; the B200 path computes in fp32/bf16 and takes
+// float32 host data, so a kDouble caller converts once (Tensor::converted).
+class Tensor {
+ public:
+  Tensor() = default;
+  explicit Tensor(std::vector<std::int64_t> shape) : shape_(std::move(shape)), data_(count(shape_)) {}
+  Tensor(std::vector<std::int64_t> shape, std::vector<float> values) : shape_(std::move(shape)), data_(std::move(values)) {
+    if (static_cast<std::int64_t>(data_.size()) != count(shape_))
+      throw DimensionError("Tensor: value count does not match shape");
+  }
+  const std::vector<std::int64_t>& shape() const { return shape_; }
+  std::size_t rank() const { return shape_.size(); }
+  std::int64_t dim(std::size_t i) const { return shape_.at(i); }
+  std::int64_t size() const { return static_cast<std::int64_t>(data_.size()); }
+  float* data() { return data_.data(); }
+  const float* data() const { return data_.data(); }
+
+ private:
+  static std::int64_t count(const std::vector<std::int64_t>& s) {
+    std::int64_t n = 1;
+    for (auto d : s) n *= d;
+    return n;
+  }
+  std::vector<std::int64_t> shape_;
+  std::vector<float> data_;
+};
+
+struct ConvParams {  // model.hpp:75-78
+  Tensor kernels;    // [F x C x R x S]
+  Tensor bias;       // [F]
+};
+struct FcParams {  // model.hpp:80-83
+  Tensor weight;   // [in_dim x out_dim] (a worker's shard: [in_dim x out_i])
+  Tensor bias;     // [out_dim]
+};
+struct ByteCounters {  // cluster.hpp:41-57, indexed by Phase (kConvFwd .. kConvBwd)
+  std::array<std::int64_t, 4> sent{};
+  std::array<std::int64_t, 4> received{};
+};
+// cluster.hpp:77-84. Cluster::worker() returns a host snapshot read back from
+// the device (the reference returns a reference into host memory).
+struct WorkerState {
+  int worker_id = 0;
+  std::vector<ConvParams> conv_params;
+  std::vector<ConvParams> conv_momentum;
+  std::vector<FcParams> fc_shard;
+  std::vector<FcParams> fc_momentum;
+  ByteCounters bytes;
+};
+struct Model {  // model.hpp:88-94
+  ModelSpec spec;
+  std::vector<ConvParams> conv;
+  std::vector<FcParams> fc;
+  std::uint64_t rng_seed = 0;
+};
+
 class Cluster {  // cluster.hpp:178-212
  public:
   struct StepResult {
@@ -191,9 +252,68 @@ class Cluster {  // cluster.hpp:178-212
     return r;
   }
 
+  // cluster.hpp:190-192: the reference's signature over Tensor objects.
+  // Shapes are checked here (model.cpp:204-214 DimensionError; rows per
+  // worker, cluster.cpp:444-457 UsageError) before any native call.
+#if __cplusplus >= 202002L
+  StepResult run_step(std::span<const Tensor> batches, std::span<const Tensor> targets, const HyperParams& hp,
+                      double lr) {
+    return run_step_tensors(batches.data(), batches.size(), targets.data(), targets.size(), hp, lr);
+  }
+#endif
+  StepResult run_step(const std::vector<Tensor>& batches, const std::vector<Tensor>& targets, const HyperParams& hp,
+                      double lr) {
+    return run_step_tensors(batches.data(), batches.size(), targets.data(), targets.size(), hp, lr);
+  }
+
   int workers() const { return config_.workers; }
   const ClusterConfig& config() const { return config_; }
   const ModelSpec& spec() const { return spec_; }
+
+  // cluster.hpp:197 (host snapshot; NCCL transport: the local rank's worker).
+  WorkerState worker(int i) const {
+    WorkerState w;
+    w.worker_id = i;
+    for (int l = 0; l < static_cast<int>(spec_.conv_layers.size()); ++l) {
+      const auto& c = spec_.conv_layers[static_cast<std::size_t>(l)];
+      const std::vector<std::int64_t> ks{c.out_channels, c.in_channels, c.kernel, c.kernel}, bs{c.out_channels};
+      w.conv_params.push_back({Tensor(ks, param(i, HP_P_CONV_K, l)), Tensor(bs, param(i, HP_P_CONV_B, l))});
+      w.conv_momentum.push_back({Tensor(ks, param(i, HP_P_CONV_K + HP_P_MOMENTUM, l)),
+                                 Tensor(bs, param(i, HP_P_CONV_B + HP_P_MOMENTUM, l))});
+    }
+    for (int l = 0; l < static_cast<int>(spec_.fc_layers.size()); ++l) {
+      const auto& f = spec_.fc_layers[static_cast<std::size_t>(l)];
+      const std::vector<float> b = param(i, HP_P_FC_B, l);
+      const std::int64_t out = static_cast<std::int64_t>(b.size());
+      const std::vector<std::int64_t> ws{f.in_dim, out}, bs{out};
+      w.fc_shard.push_back({Tensor(ws, param(i, HP_P_FC_W, l)), Tensor(bs, b)});
+      w.fc_momentum.push_back({Tensor(ws, param(i, HP_P_FC_W + HP_P_MOMENTUM, l)),
+                               Tensor(bs, param(i, HP_P_FC_B + HP_P_MOMENTUM, l))});
+    }
+    check(hp_cluster_worker_bytes(h_, i, w.bytes.sent.data(), w.bytes.received.data()));
+    return w;
+  }
+
+  // cluster.hpp:199-201 / cluster.cpp:417-437: worker 0's conv replica and
+  // the fc shards pasted back into whole matrices (NCCL: collective).
+  Model gathered_model() const {
+    Model m;
+    m.spec = spec_;
+    m.rng_seed = config_.seed;
+    std::vector<float*> ck, cb, fw, fb;
+    for (const auto& c : spec_.conv_layers) {
+      m.conv.push_back({Tensor({c.out_channels, c.in_channels, c.kernel, c.kernel}), Tensor({c.out_channels})});
+      ck.push_back(m.conv.back().kernels.data());
+      cb.push_back(m.conv.back().bias.data());
+    }
+    for (const auto& f : spec_.fc_layers) {
+      m.fc.push_back({Tensor({f.in_dim, f.out_dim}), Tensor({f.out_dim})});
+      fw.push_back(m.fc.back().weight.data());
+      fb.push_back(m.fc.back().bias.data());
+    }
+    check(hp_cluster_gather_model(h_, ck.data(), cb.data(), fw.data(), fb.data()));
+    return m;
+  }
 
   // WorkerState tensors in reference layouts (which: HP_P_*).
   std::vector<float> param(int worker, int which, int layer) const {
@@ -207,6 +327,30 @@ class Cluster {  // cluster.hpp:178-212
   void set_skip_sync_broadcast(bool v) { check(hp_cluster_set_skip_sync_broadcast(h_, v ? 1 : 0)); }
 
  private:
+  StepResult run_step_tensors(const Tensor* b, std::size_t nb, const Tensor* t, std::size_t nt,
+                              const HyperParams& hp, double lr) {
+    const std::size_t k = config_.nccl ? 1u : static_cast<std::size_t>(config_.workers);
+    if (nb != k || nt != k)
+      throw UsageError("run_step: expected " + std::to_string(k) + " batches and targets, got " +
+                       std::to_string(nb) + " / " + std::to_string(nt));
+    std::vector<const float*> bp, tp;
+    for (std::size_t i = 0; i < k; ++i) {
+      const Tensor& x = b[i];
+      const Tensor& y = t[i];
+      if (x.rank() < 1 || y.rank() < 1 || x.dim(0) != config_.per_worker_batch || y.dim(0) != config_.per_worker_batch)
+        throw UsageError("run_step: worker " + std::to_string(i) + " batch must hold exactly " +
+                         std::to_string(config_.per_worker_batch) + " examples");
+      if (x.rank() != 4 || x.dim(1) != spec_.input_shape[0] || x.dim(2) != spec_.input_shape[1] ||
+          x.dim(3) != spec_.input_shape[2])
+        throw DimensionError("forward: batch shape does not match model input");
+      if (y.rank() != 2 || y.dim(1) != spec_.num_classes)
+        throw DimensionError("logistic_xent: target shape does not match the logits");
+      bp.push_back(x.data());
+      tp.push_back(y.data());
+    }
+    return run_step(bp, tp, hp, lr, false);
+  }
+
   ModelSpec spec_;
   ClusterConfig config_;
   hp_cluster* h_ = nullptr;

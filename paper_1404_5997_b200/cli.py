@@ -31,8 +31,6 @@ failure. `HPSIM_OUTPUT_DIR` overrides output_dir. Config: JSON, one file:
       speedup summary vs K=1. Config "cost": {"machine": "b200"|"paper",
       "measured_step_ms": <1-GPU step to calibrate compute to, or null>, plus any
       CostParams field to override}.
-  python -m paper_1404_5997_b200.cli scale-hparams --eps 0.01 --omega 0.0005 --k 8
-      [--rule theory_sqrt|heuristic_linear] [--json].
 """
 from __future__ import annotations
 
@@ -363,32 +361,9 @@ def cmd_cost_report(cfg, as_json: bool = False, out=None) -> int:
     return EXIT_OK
 
 
-def cmd_scale_hparams(eps: float, omega: float, k: float, rule: str, as_json: bool = False, out=None) -> int:
-    from .hparams import make_scale_plan
-    out = out or sys.stdout
-    try:
-        p = make_scale_plan(eps, omega, k, rule)
-    except ValueError as e:
-        raise ValidationError(str(e)) from e
-    d = dataclasses.asdict(p)
-    if as_json:
-        print(json.dumps(d, sort_keys=True), file=out)
-    else:
-        for key in ("k", "rule", "eps", "omega", "eps_new", "omega_exact", "omega_approx", "omega_practical"):
-            v = d[key]
-            print(f"{key:<16}{v:.10g}" if isinstance(v, float) else f"{key:<16}{v}", file=out)
-    return EXIT_OK
-
-
 def main(argv=None) -> int:
     p = argparse.ArgumentParser(prog="python -m paper_1404_5997_b200.cli")
     sub = p.add_subparsers(dest="cmd", required=True)
-    sh = sub.add_parser("scale-hparams")
-    sh.add_argument("--eps", type=float, required=True)
-    sh.add_argument("--omega", type=float, required=True)
-    sh.add_argument("--k", type=float, required=True)
-    sh.add_argument("--rule", choices=("theory_sqrt", "heuristic_linear"), default="theory_sqrt")
-    sh.add_argument("--json", action="store_true")
     for name in ("train", "verify-equivalence", "cost-report"):
         s = sub.add_parser(name)
         s.add_argument("--config", required=True)
@@ -399,8 +374,6 @@ def main(argv=None) -> int:
             s.add_argument("--skip-broadcast", action="store_true")
     a = p.parse_args(argv)
     try:
-        if a.cmd == "scale-hparams":
-            return cmd_scale_hparams(a.eps, a.omega, a.k, a.rule, a.json)
         cfg = load_config(a.config)
         if a.seed is not None:
             cfg["cluster"]["seed"] = a.seed

@@ -35,7 +35,18 @@
 #include "kernels.cuh"
 #include "rng.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace hp {
+
+// NVTX ranges around the step's phases (host-side enqueue; visible in any
+// NVTX-aware timeline). Cheap when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 namespace {
 
@@ -1034,6 +1045,21 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       w.fc0_slot1[2] = plan(op(w.fdz[0], 1, ldn_), op(fwp, 1, f.Ip), n_, g_.A, rows, ed);
     }
   }
+  static const bool dump = getenv("HP_DEV_PLANS") != nullptr;  // dev: print every plan's shape and tiling
+  if (dump && w.gid == 0) {
+    auto show = [](const char* tag, size_t l, const GemmPlan& p) {
+      if (!p.valid) return;
+      fprintf(stderr, "plan %-10s %zu  M %6d N %6d K %7d  %s bn %3d splits %2d grid %3u%s%s a_mn %d b_mn %d\n", tag, l,
+              p.args.M, p.args.N, p.args.K, p.shift ? "shift" : p.cta2 ? "pair " : "1cta ", p.bn, p.splits, p.grid.x,
+              p.light ? " light" : "", p.args.epi.c_trans ? " c_trans" : "", p.args.a_mn, p.args.b_mn);
+    };
+    for (size_t l = 0; l < w.conv_fwd.size(); ++l) show("conv_fwd", l, w.conv_fwd[l]);
+    for (size_t l = 0; l < w.conv_wgrad.size(); ++l) show("conv_wgrad", l, w.conv_wgrad[l]);
+    for (size_t l = 0; l < w.conv_dgrad.size(); ++l) show("conv_dgrad", l, w.conv_dgrad[l]);
+    for (size_t l = 0; l < w.fc_fwd.size(); ++l) show("fc_fwd", l, w.fc_fwd[l]);
+    for (size_t l = 0; l < w.fc_wgrad.size(); ++l) show("fc_wgrad", l, w.fc_wgrad[l]);
+    for (size_t l = 0; l < w.fc_dgrad.size(); ++l) show("fc_dgrad", l, w.fc_dgrad[l]);
+  }
 }
 
 // Every tcgen05 GEMM of the step goes through here: launch, count, and (when
@@ -1509,7 +1535,10 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
       ++launches_;
     }
   }
-  for (auto& w : w_) conv_forward(w);
+  {
+    NvtxRange r("hp.conv_forward");
+    for (auto& w : w_) conv_forward(w);
+  }
   // The turns (cluster.cpp:507-614). The boundary exchange and the gradient
   // return run on their own stream sr_ with double-buffered boundary slots:
   // turn j+1's exchange is issued BEFORE turn j's FC compute and depends only
@@ -1551,6 +1580,7 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
     sgd_has_gscale_ = !variable_ && num_sub_ > 1;
     sgd_gscale_ = static_cast<float>(1.0 / static_cast<double>(num_sub_));
     marker(300 + j, st_);
+    NvtxRange turn_range("hp.fc_turn");
     fc_forward_backward(j, !variable_ && j > 0, slot);
     marker(400 + j, st_);
     HP_CUDA(cudaStreamWaitEvent(xs, ev_fd0_, 0));
@@ -1580,6 +1610,7 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
   // backward order -- the same order on every rank).
   const int nc = static_cast<int>(g_.cg.size());
   std::vector<ConvBwdState> cbs(nl);
+  NvtxRange bwd_range("hp.conv_backward_sync_sgd");
   for (int l = nc - 1; l >= 0; --l) {
     for (int i = 0; i < nl; ++i) conv_backward_layer(w_[i], l, cbs[i]);
     if (K_ > 1) {
@@ -1667,6 +1698,7 @@ template <class TA>
 void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* targets, int mem_kind,
                                const hp_hyper& hp, double lr, hp_step_metrics* out) {
   const int nl = comm_->nlocal();
+  NvtxRange step_range("hp.run_step");
   if (mem_kind == HP_MEM_HOST && batches && targets) {
     // consume a prefetched slot holding exactly these host buffers
     for (auto& ps : pref_) {

@@ -1,11 +1,25 @@
-"""Summarise an ncu --set full report (raw page CSV) per launch: duration,
-tensor-pipe activity, DRAM bytes, L2 (lts) throughput, TMA bytes."""
-import csv, subprocess, sys
+"""Summarise an ncu --set full capture per launch (raw page CSV: a .ncu-rep, or the
+exported .csv / .csv.gz): duration, tcgen05 tensor activity, DRAM bytes, L2->SM
+bytes, L2 throughput.
 
-rep = sys.argv[1]
-names = sys.argv[2].split(",") if len(sys.argv) > 2 else None
-out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rows = list(csv.reader(out.splitlines()))
+tensor% is the bf16->fp32 tensor-op path utilisation
+(sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off, % of peak over the
+elapsed time) -- the counter tcgen05.mma kind::f16 drives on sm_100. memT% is
+sm__mem_tensor_cycles_active (tensor-core operand reads from smem/TMEM). The
+legacy sm__pipe_tensor_cycles_active counts only the HMMA (mma.sync) pipe and
+reads ~3% on tcgen05 kernels, so it is not used.
+usage: ncu_summary.py <rep|csv|csv.gz> [labels comma-separated]"""
+import csv, gzip, io, subprocess, sys
+
+src = sys.argv[1]
+labels = sys.argv[2].split(",") if len(sys.argv) > 2 else None
+if src.endswith(".ncu-rep"):
+    text = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+elif src.endswith(".gz"):
+    text = gzip.open(src, "rt").read()
+else:
+    text = open(src).read()
+rows = list(csv.reader(io.StringIO(text)))
 h = rows[0]
 col = {k: i for i, k in enumerate(h)}
 
@@ -20,30 +34,28 @@ def g(r, k, default=float("nan")):
         return default
 
 
-def unit(k):
-    return rows[1][col[k]] if k in col else ""
-
-
 def scale(k, to):
-    u = unit(k)
+    u = rows[1][col[k]] if k in col else ""
     f = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "msecond": 1e-3,
          "usecond": 1e-6, "nsecond": 1e-9}.get(u, 1)
     return f / to
 
 
-print(f"{'#':>3} {'kernel':34s} {'grid':>10s} {'us':>8s} {'tensor%':>7s} {'dramMB':>8s} {'dramTB/s':>8s} {'lts%':>5s} {'sm%':>5s} {'tmaGB':>7s}")
+TEN = "sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed"
+MEMT = "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"
+print(f"{'#':>3} {'label':12s} {'kernel':28s} {'grid':>6s} {'us':>7s} {'tensor%':>7s} {'memT%':>6s} {'dramMB':>7s} "
+      f"{'TB/s':>5s} {'L2->SM MB':>9s} {'B/clk/SM':>8s} {'lts%':>5s}")
 for n, r in enumerate(rows[2:]):
     name = r[col["Kernel Name"]]
-    short = name.split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "").replace("unnamed>::", "")[-34:]
+    short = name.split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "").replace("hp::", "")[-28:]
     t = g(r, "gpu__time_duration.sum") * scale("gpu__time_duration.sum", 1e-6)
-    rd = g(r, "dram__bytes_read.sum") * scale("dram__bytes_read.sum", 1e6)
-    wr = g(r, "dram__bytes_write.sum") * scale("dram__bytes_write.sum", 1e6)
-    ten = g(r, "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed")
-    if ten != ten:
-        ten = g(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed")
-    lts = g(r, "lts__throughput.avg.pct_of_peak_sustained_elapsed")
-    sm = g(r, "sm__throughput.avg.pct_of_peak_sustained_elapsed")
-    tma = g(r, "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum") * scale(
-        "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum", 1e9)
-    grid = r[col["Grid Size"]] if "Grid Size" in col else ""
-    print(f"{n:3d} {short:34s} {grid:>10s} {t:8.1f} {ten:7.1f} {rd + wr:8.1f} {(rd + wr) / t:8.2f} {lts:5.1f} {sm:5.1f} {tma:7.3f}")
+    dram = (g(r, "dram__bytes_read.sum") * scale("dram__bytes_read.sum", 1e6) +
+            g(r, "dram__bytes_write.sum") * scale("dram__bytes_write.sum", 1e6))
+    x2l1 = g(r, "l1tex__m_xbar2l1tex_read_bytes.sum") * scale("l1tex__m_xbar2l1tex_read_bytes.sum", 1e6)
+    clk = g(r, "gpc__cycles_elapsed.max")
+    sms = g(r, "device__attribute_multiprocessor_count", 148)
+    bpc = x2l1 * 1e6 / (clk * sms) if clk == clk and clk > 0 else float("nan")
+    grid = r[col["Grid Size"]].split(",")[0].strip("( ") if "Grid Size" in col else ""
+    lab = labels[n] if labels and n < len(labels) else ""
+    print(f"{n:3d} {lab:12s} {short:28s} {grid:>6s} {t:7.1f} {g(r, TEN):7.1f} {g(r, MEMT):6.1f} {dram:7.1f} "
+          f"{dram / t:5.2f} {x2l1:9.1f} {bpc:8.1f} {g(r, 'lts__throughput.avg.pct_of_peak_sustained_elapsed'):5.1f}")
