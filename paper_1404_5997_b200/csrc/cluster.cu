@@ -116,6 +116,7 @@ Geometry make_geometry(const hp_model_spec* s, int K, long long b) {
                    num(l.kernel) + ")/" + num(l.stride) + "+1 is not a positive integer");
     cg.OH = static_cast<int>(oh);
     cg.OW = static_cast<int>(ow);
+    cg.OWs = cg.OW;
     cg.relu = l.relu != 0;
     if (l.lrn_size < 0) config_error(where + ".lrn_size: must be >= 0");
     if (l.lrn_size > 5 && l.pool_kernel > 0)
@@ -338,6 +339,7 @@ struct Worker {
   TA* z = nullptr;              // s2d layer 0: space-to-depth input [b][Zh][Zw][Cz]
   TA* wz = nullptr;             // s2d layer 0: kernels [F][Rq][Rq][Cz] (operand type)
   float* dwz = nullptr;         // s2d layer 0: wgrad in the s2d layout
+  float* bias2 = nullptr;       // s2d pixel pairs: conv1 bias twice (the 2F GEMM columns)
   const float* x_src = nullptr; // this step's NCHW batch (device)
   // conv params: [kernels F x ldk | bias F] per layer, one arena
   float *cp = nullptr, *cm = nullptr, *cgr = nullptr;
@@ -605,8 +607,13 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     if (c.s2d) {
       c.Cz = cz;
       c.Rq = (c.R + c.stride - 1) / c.stride;
+      static const bool no_pairs = getenv("HP_DEV_NO_PAIRS") != nullptr;  // dev: the N = F s2d GEMMs
+      // (the pool -- the only consumer -- reads the stored width; LRN-only / no-pool
+      // layers keep the plain layout)
+      c.pairs = !std::is_same<TA, float>::value && 2 * c.F <= 256 && (2 * c.F) % 64 == 0 && c.pk > 0 && !no_pairs;
+      c.OWs = c.pairs ? (c.OW + 1) / 2 * 2 : c.OW;
       c.Zh = c.OH + c.Rq - 1;
-      c.Zw = c.OW + c.Rq - 1;
+      c.Zw = c.OWs + c.Rq - 1;  // pairs: pair u reads z columns 2u .. 2u + Rq
     }
     c.impl_dgrad = l > 0 && c.stride == 1 && c.F % atom == 0 && c.pad <= c.R - 1 &&
                    c.H == c.OH + c.R - 1 - 2 * c.pad && c.W == c.OW + c.S - 1 - 2 * c.pad;
@@ -638,7 +645,7 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     for (auto& c : g_.cg) {
       c.Hq = c.in_q ? c.H + c.pad : c.H;
       c.Wq = c.in_q ? c.W + c.pad : c.W;
-      c.Pq = c.in_q ? b_ * c.Hq * c.Wq : c.P;
+      c.Pq = c.in_q ? b_ * c.Hq * c.Wq : b_ * c.OH * c.OWs;
     }
   }
   const auto& in = g_.input;
@@ -665,16 +672,18 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
       const bool lrn_only = c.lrn_n > 0 && c.pk == 0;  // fused LRN+pool keeps no LRN output
       // layer 0 explicit: transposed colT [Kc][P]; other explicit layers: col [P][ldk]
       if (c.s2d) {
+        const long long kz = static_cast<long long>(c.pairs ? 2 : 1) * c.F * c.Rq * (c.Rq + (c.pairs ? 1 : 0)) * c.Cz;
         w.z = arena_.make<TA>(b_ * c.Zh * c.Zw * c.Cz);
-        w.wz = arena_.make<TA>(static_cast<long long>(c.F) * c.Rq * c.Rq * c.Cz);
-        w.dwz = arena_.make<float>(static_cast<long long>(c.F) * c.Rq * c.Rq * c.Cz);
+        w.wz = arena_.make<TA>(kz);
+        w.dwz = arena_.make<float>(kz);
+        w.bias2 = c.pairs ? arena_.make<float>(2LL * c.F) : nullptr;
       }
       w.col.push_back(c.impl_fwd || c.s2d ? nullptr
                                  : (l == 0 ? arena_.make<TA>(static_cast<long long>(c.Kc) * c.ldp)
                                            : arena_.make<TA>(c.P * c.ldk)));
       const bool next_q = l + 1 < nc && g_.cg[l + 1].in_q;
       const long long out_rows = next_q ? g_.cg[l + 1].Pq : -1;  // stage output in the next layer's q-layout
-      w.act.push_back(arena_.make<TA>((c.pk == 0 && c.lrn_n == 0 && next_q ? out_rows : c.P) * c.F));
+      w.act.push_back(arena_.make<TA>((c.pk == 0 && c.lrn_n == 0 && next_q ? out_rows : c.pairs ? c.Pq : c.P) * c.F));
       w.lrn.push_back(lrn_only ? arena_.make<TA>(c.P * c.F) : nullptr);
       w.lrn_d.push_back(lrn_only ? arena_.make<float>(c.P * c.F) : nullptr);
       w.pool.push_back(c.pk > 0 ? arena_.make<TA>((next_q ? out_rows : c.PP) * c.F) : nullptr);
@@ -826,7 +835,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     return o;
   };
   auto plan = [&](const GemmOperand& a, const GemmOperand& b, long long M, long long N, long long K,
-                  const Epi& e, int side = 0) {
+                  const Epi& e, int side = 0, int bn = 0, int cta2 = -1) {
     // The plan picks its own tile and split-K; the first (sizing) pass runs
     // against a placeholder workspace and records the largest need. Side-stream
     // (wgrad) plans get their own workspace: they run concurrently with the
@@ -835,7 +844,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     size_t& need = side == 1 ? ws2_floats_ : side == 2 ? ws3_floats_ : ws_floats_;
     float* ws = real != nullptr ? real : reinterpret_cast<float*>(256);
     GemmPlan pl = gemm_plan(math_, a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e, 0,
-                            ws, 0);
+                            ws, bn, cta2);
     if (pl.splits > 1) need = std::max(need, static_cast<size_t>(pl.splits * M * N));
     else pl.args.ws = real;
     return pl;
@@ -878,8 +887,14 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       xa = op(in, 0, 0);
       xa.conv = view;
     }
-    const long long Kz = static_cast<long long>(c.Rq) * c.Rq * c.Cz;
-    const Im2col zview{1, static_cast<int>(b_), c.Zh, c.Zw, c.Cz, c.Rq, c.Rq, 1, 0, c.OH, c.OW};
+    // s2d: im2col over z. Pixel pairs: one GEMM row per pair (W walked with
+    // stride 2), Rq+1 tap columns, N = 2F (see launch_s2d_weights)
+    const int sq = c.Rq + (c.pairs ? 1 : 0);
+    const long long Kz = static_cast<long long>(c.Rq) * sq * c.Cz;
+    Im2col zview{1, static_cast<int>(b_), c.Zh, c.Zw, c.Cz, c.Rq, sq, c.pairs ? 2 : 1, 0, c.OH, c.OWs / (c.pairs ? 2 : 1)};
+    zview.stride_h = 1;
+    const long long zrows = b_ * c.OH * (c.OWs / (c.pairs ? 2 : 1));  // GEMM rows (pixels or pairs)
+    const int zn = c.pairs ? 2 * c.F : c.F;                              // GEMM columns
     // bf16 stride-1 convs over zero-bordered rows: the flat-shift kernel (one
     // smem halo per channel block for all taps); output rows are the stored
     // grid, the RowMap keeps the valid ones
@@ -899,7 +914,15 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     } else if (c.s2d) {
       xa = op(w.z, 0, 0);
       xa.conv = zview;
-      w.conv_fwd.push_back(plan(xa, op(w.wz, 0, Kz), c.P, c.F, Kz, e));
+      if (c.pairs) {  // row = pixel pair: its 2F outputs are the two pixels' contiguous channel rows
+        e.ldc = zn;
+        e.bias = w.bias2;
+      }
+      // dev: HP_DEV_C1F=<cta2>,<bn> forces conv1's tile
+      static const char* c1f = getenv("HP_DEV_C1F");
+      int f_cta2 = -1, f_bn = 0;
+      if (c1f) sscanf(c1f, "%d,%d", &f_cta2, &f_bn);
+      w.conv_fwd.push_back(plan(xa, op(w.wz, 0, Kz), zrows, zn, Kz, e, 0, f_bn, f_cta2));
     } else {
       w.conv_fwd.push_back(plan(xa, op(kw, 0, c.ldk), c.P, c.F, c.Kc, e));
     }
@@ -927,7 +950,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     // 0.067 vs 0.071, conv4 (F=384) 0.114 vs 0.120 faster unswapped.
     auto mfill = [](long long m) { return static_cast<double>(m) / (((m + 255) / 256) * 256); };
     const long long Kw = c.s2d ? Kz : c.Kc;
-    const bool swap = (c.impl_fwd || c.s2d) && c.F >= 128 && c.F <= 256 && mfill(Kw) > mfill(c.F) + 0.1;
+    const bool swap = (c.impl_fwd || c.s2d) && !c.pairs && c.F >= 128 && c.F <= 256 && mfill(Kw) > mfill(c.F) + 0.1;
     if (c.s2d) {
       eg.c = w.dwz;
       eg.ldc = Kz;
@@ -938,7 +961,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       eg.c_trans = 1;  // element (m = k, n = f) -> dW[f][k]
       w.conv_wgrad.push_back(plan(xb, op(w.dz[l], 1, c.F), Kw, c.F, c.s2d ? c.P : c.Pq, eg, 1));
     } else if (c.s2d) {
-      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, Kz, c.P, eg, 1));
+      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, zn), xb, zn, Kz, zrows, eg, 1));
     } else {
       w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, c.Kc, c.Pq, eg, 1));
     }
@@ -1194,7 +1217,7 @@ void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
     OutLayout yl{};  // stage output in the next layer's q-layout
     if (l + 1 < nc && g_.cg[l + 1].in_q) yl = OutLayout{g_.cg[l + 1].Hq, g_.cg[l + 1].Wq, g_.cg[l + 1].pad};
     if (c.lrn_n > 0 && c.pk > 0) {
-      launch_lrn_pool_fwd<TA>(w.act[l], w.pool[l], w.widx[l], B, c.OH, c.OW, c.F, c.lrn_n, c.lrn_alpha,
+      launch_lrn_pool_fwd<TA>(w.act[l], w.pool[l], w.widx[l], B, c.OH, c.OWs, c.F, c.lrn_n, c.lrn_alpha,
                               c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, st_, yl);
       ++launches_;
     } else if (c.lrn_n > 0) {
@@ -1202,7 +1225,7 @@ void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
                          c.lrn_k, st_);
       ++launches_;
     } else if (c.pk > 0) {
-      launch_maxpool_fwd_w<TA>(w.act[l], w.pool[l], w.widx[l], B, c.OH, c.OW, c.F, c.pk, c.ps, c.PH,
+      launch_maxpool_fwd_w<TA>(w.act[l], w.pool[l], w.widx[l], B, c.OH, c.OWs, c.F, c.pk, c.ps, c.PH,
                                c.PW, st_, yl);
       ++launches_;
     }
@@ -1215,7 +1238,7 @@ void ClusterImpl<TA>::rotate_all(Worker<TA>& w) {
     const ConvGeom& c = g_.cg[l];
     if (c.s2d) {  // the s2d operand copy of the (just updated) master kernels
       launch_s2d_weights<TA>(w.cp + conv_k_off(static_cast<int>(l)), c.ldk, w.wz, c.F, c.C, c.R, c.S, c.stride, c.Rq,
-                             c.Cz, st_);
+                             c.Cz, st_, c.pairs ? w.cp + conv_b_off(static_cast<int>(l)) : nullptr, w.bias2);
       ++launches_;
     }
     if (!c.impl_dgrad) continue;
@@ -1392,11 +1415,11 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
   const int B = static_cast<int>(b_);
   const OutLayout zl = c.in_q ? OutLayout{c.Hq, c.Wq, c.pad} : OutLayout{};  // dz layout
   if (c.pk > 0 && c.lrn_n > 0) {
-    launch_lrn_pool_bwd<TA>(cs.gout, w.widx[l], w.act[l], w.dz[l], B, c.OH, c.OW, c.F, c.lrn_n, c.lrn_alpha,
+    launch_lrn_pool_bwd<TA>(cs.gout, w.widx[l], w.act[l], w.dz[l], B, c.OH, c.OWs, c.F, c.lrn_n, c.lrn_alpha,
                             c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, c.relu ? 1 : 0, st_, zl);
     ++launches_;
   } else if (c.pk > 0) {
-    launch_maxpool_bwd_w<TA, TA>(cs.gout, w.widx[l], w.dz[l], mask, B, c.OH, c.OW, c.F, c.pk, c.ps, c.PH,
+    launch_maxpool_bwd_w<TA, TA>(cs.gout, w.widx[l], w.dz[l], mask, B, c.OH, c.OWs, c.F, c.pk, c.ps, c.PH,
                                  c.PW, st_, zl);
     ++launches_;
   } else if (c.lrn_n > 0) {
@@ -1421,7 +1444,8 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
   launches_ += 2;
   gemm(w.conv_wgrad[l], "conv_wgrad", l, ws);
   if (c.s2d) {
-    launch_s2d_wgrad_gather(w.dwz, w.cgr + conv_k_off(l), c.ldk, c.F, c.C, c.R, c.S, c.stride, c.Rq, c.Cz, ws);
+    launch_s2d_wgrad_gather(w.dwz, w.cgr + conv_k_off(l), c.ldk, c.F, c.C, c.R, c.S, c.stride, c.Rq, c.Cz, ws,
+                            c.pairs ? 1 : 0);
     ++launches_;
   }
   if (K_ > 1 && skip_sync_broadcast) {  // keep the local gradients for the negative control
@@ -2043,9 +2067,9 @@ int64_t ClusterImpl<TA>::read_decisions(int worker, int kind, int layer, void* d
     HP_CUDA(cudaStreamSynchronize(st_));
     if (kind == 0) {
       const bool next_q = layer + 1 < nc && g_.cg[layer + 1].in_q && c.pk == 0 && c.lrn_n == 0;
-      const long long H = next_q ? g_.cg[layer + 1].Hq : c.OH, W = next_q ? g_.cg[layer + 1].Wq : c.OW;
+      const long long H = next_q ? g_.cg[layer + 1].Hq : c.OH, W = next_q ? g_.cg[layer + 1].Wq : c.OWs;
       const long long p = next_q ? g_.cg[layer + 1].pad : 0;
-      std::vector<TA> h(static_cast<size_t>((next_q ? g_.cg[layer + 1].Pq : c.P) * c.F));
+      std::vector<TA> h(static_cast<size_t>((next_q ? g_.cg[layer + 1].Pq : b_ * c.OH * c.OWs) * c.F));
       HP_CUDA(cudaMemcpy(h.data(), w.act[layer], h.size() * sizeof(TA), cudaMemcpyDeviceToHost));
       uint8_t* m = static_cast<uint8_t*>(dst);
       for (long long b = 0; b < b_; ++b)

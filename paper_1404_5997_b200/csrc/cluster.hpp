@@ -26,6 +26,13 @@ struct ConvGeom {
   bool impl_dgrad = false;     // stride-1 dgrad as a conv over dY with rotated weights
   bool s2d = false;            // strided first layer as a stride-1 conv over its space-to-depth input
   int Rq = 0, Zh = 0, Zw = 0, Cz = 0;  // s2d: taps, z extents, padded z channels
+  // s2d pixel pairs (bf16, 2F <= 256): the conv1 GEMM takes one row per pair of
+  // horizontally adjacent output pixels and N = 2F columns (F = 64 alone is a
+  // shared-memory-bound N); the output and its gradient are
+  // stored OWs = OW rounded up to even wide (the extra column never feeds the
+  // pool, its gradient stays zero).
+  bool pairs = false;
+  int OWs = 0;                 // stored conv-output width (OW, or even for pairs)
   // q-layout (see RowMap, gemm.cuh): this layer's input x and its dz are
   // stored as (H+pad) x (W+pad) row slots per image with a shared zero border
   // (stride-1 "same" convs): the conv is a flat shift of the row index.

@@ -627,7 +627,7 @@ __device__ __forceinline__ void load_a_im2col(uint8_t* dst, const CUtensorMap* t
   const int ohw = c.OH * c.OW;
   const int n = m0 / ohw, rem = m0 - n * ohw;
   const int oh = rem / c.OW, ow = rem - oh * c.OW;
-  tma_im2col<TWO>(dst, tm, bar, cb * ATOM, c.lo_w + ow * c.stride, c.lo_h + oh * c.stride, n,
+  tma_im2col<TWO>(dst, tm, bar, cb * ATOM, c.lo_w + ow * c.stride, c.lo_h + oh * c.stride_h, n,
                   static_cast<uint16_t>(s), static_cast<uint16_t>(r));
 }
 
@@ -644,7 +644,7 @@ __device__ __forceinline__ void load_b_im2col(uint8_t* dst, const CUtensorMap* t
     const int col = n0 + a * ATOM;
     const int rs = col / c.C, ch = col - rs * c.C;
     const int r = rs / c.S, s = rs - r * c.S;
-    tma_im2col<TWO>(dst + a * (BK * 128), tm, bar, ch, c.lo_w + ow * c.stride, c.lo_h + oh * c.stride, n,
+    tma_im2col<TWO>(dst + a * (BK * 128), tm, bar, ch, c.lo_w + ow * c.stride, c.lo_h + oh * c.stride_h, n,
                     static_cast<uint16_t>(s), static_cast<uint16_t>(r));
   }
 }
@@ -1523,7 +1523,8 @@ CUtensorMap im2col_map(const void* ptr, int es, const Im2col& g, int pixels, boo
     lower[0] = lower[1] = g.lo;
     upper[0] = upper[1] = g.hi;
   }
-  cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(g.stride), static_cast<cuuint32_t>(g.stride), 1};
+  const int sh = g.stride_h > 0 ? g.stride_h : g.stride;
+  cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(g.stride), static_cast<cuuint32_t>(sh), 1};
   CUresult r = encode_im2col_fn()(&m, es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                                   4, const_cast<void*>(ptr), dims, strides, lower, upper,
                                   static_cast<cuuint32_t>(atom), static_cast<cuuint32_t>(pixels), estr,
@@ -1545,6 +1546,7 @@ ConvArgs conv_args(const Im2col& g) {
   c.OH = g.OH;
   c.OW = g.OW;
   c.stride = g.stride;
+  c.stride_h = g.stride_h > 0 ? g.stride_h : g.stride;
   c.lo_w = g.corners ? g.lo : -g.pad;
   c.lo_h = g.corners ? g.lo : -g.pad;
   c.shift = g.shift;

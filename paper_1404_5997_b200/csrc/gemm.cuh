@@ -86,6 +86,10 @@ struct Im2col {
   // of k-tile kt is the tiled TMA box at rows kt*BK + r*W + s - (pad*W + pad)
   // (zero fill outside) -- plain tiled loads instead of TMA im2col.
   int shift = 0;
+  // vertical traversal stride when it differs from `stride` (0: same). The
+  // s2d conv1 pixel-pair GEMM walks W with stride 2 (one row per output pixel
+  // pair) and H with stride 1.
+  int stride_h = 0;
 };
 
 
@@ -99,6 +103,7 @@ struct GemmOperand {
 struct ConvArgs {            // device-side im2col bookkeeping (see Im2col)
   int enabled, C, S, OH, OW, stride, lo_w, lo_h;
   int shift, wq, base_off;   // Im2col::shift mode
+  int stride_h;              // vertical stride (Im2col::stride_h, resolved)
 };
 
 struct GemmArgs {

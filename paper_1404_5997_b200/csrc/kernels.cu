@@ -1361,16 +1361,27 @@ __global__ void __launch_bounds__(256) s2d_input_kernel(const float* __restrict_
   }
 }
 
+// pairs = 0: wz[F][Rq][Rq][Cz]. pairs = 1 (pixel-pair GEMM, see launch_s2d_weights):
+// wz[2F][Rq][Rq+1][Cz], row p*F + f holding filter f at tap columns shifted by
+// p (zero elsewhere), plus bias2[2F] = the bias twice.
 template <class T>
 __global__ void s2d_weights_kernel(const float* __restrict__ w, long long ldk, T* __restrict__ wz, int F, int C,
-                                   int R, int S, int s, int Rq, int Cz) {
-  const int Kz = Rq * Rq * Cz;
+                                   int R, int S, int s, int Rq, int Cz, int pairs, const float* __restrict__ bias,
+                                   float* __restrict__ bias2) {
+  const int Sq = Rq + pairs;
+  const int Kz = Rq * Sq * Cz;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= F * Kz) return;
-  const int f = t / Kz, k = t - f * Kz;
+  if (pairs && t < 2 * F) bias2[t] = bias[t % F];
+  if (t >= (1 + pairs) * F * Kz) return;
+  const int row = t / Kz, k = t - row * Kz;
+  const int f = row % F, p = row / F;
   const int ab = k / Cz, ch = k - ab * Cz;
-  const int a = ab / Rq, bq = ab - a * Rq;
+  const int a = ab / Sq, bq = ab - a * Sq - p;
   float val = 0.f;
+  if (bq < 0 || bq >= Rq) {
+    wz[t] = from_f<T>(0.f);
+    return;
+  }
   if (ch < s * s * C) {
     const int c = ch % C, d = ch / C;
     const int dr = d / s, dc = d - dr * s;
@@ -1380,15 +1391,26 @@ __global__ void s2d_weights_kernel(const float* __restrict__ w, long long ldk, T
   wz[t] = from_f<T>(val);
 }
 
+// pairs = 1: dwz is the pixel-pair gradient [2F][Rq][Rq+1][Cz]; filter f's
+// s2d gradient is its even-pixel rows (tap column bq) plus its odd-pixel rows
+// (tap column bq + 1), summed in that order.
 __global__ void s2d_wgrad_gather_kernel(const float* __restrict__ dwz, float* __restrict__ dw, long long ldk,
-                                        int F, int C, int R, int S, int s, int Rq, int Cz) {
+                                        int F, int C, int R, int S, int s, int Rq, int Cz, int pairs) {
   const int K = R * S * C;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= F * K) return;
   const int f = t / K, k = t - f * K;
   const int rq = k / C, c = k - rq * C;
   const int r = rq / S, q = rq - r * S;
-  const int kz = ((r / s) * Rq + q / s) * Cz + ((r % s) * s + q % s) * C + c;
+  const int ch = ((r % s) * s + q % s) * C + c;
+  if (pairs) {
+    const int Sq = Rq + 1;
+    const long long Kp = static_cast<long long>(Rq) * Sq * Cz;
+    const long long k0 = ((r / s) * Sq + q / s) * Cz + ch;
+    dw[f * ldk + k] = __fadd_rn(dwz[f * Kp + k0], dwz[(F + f) * Kp + k0 + Cz]);
+    return;
+  }
+  const int kz = ((r / s) * Rq + q / s) * Cz + ch;
   dw[f * ldk + k] = dwz[static_cast<long long>(f) * Rq * Rq * Cz + kz];
 }
 
@@ -1605,15 +1627,16 @@ void launch_s2d_input(const float* x, T* z, int B, int C, int H, int W, int s, i
 
 template <class T>
 void launch_s2d_weights(const float* w, long long ldk, T* wz, int F, int C, int R, int S, int s, int Rq, int Cz,
-                        cudaStream_t st) {
-  const int n = F * Rq * Rq * Cz;
-  s2d_weights_kernel<T><<<(n + 255) / 256, 256, 0, st>>>(w, ldk, wz, F, C, R, S, s, Rq, Cz);
+                        cudaStream_t st, const float* bias, float* bias2) {
+  const int pairs = bias2 != nullptr ? 1 : 0;
+  const int n = std::max((1 + pairs) * F * Rq * (Rq + pairs) * Cz, 2 * F);
+  s2d_weights_kernel<T><<<(n + 255) / 256, 256, 0, st>>>(w, ldk, wz, F, C, R, S, s, Rq, Cz, pairs, bias, bias2);
 }
 
 void launch_s2d_wgrad_gather(const float* dwz, float* dw, long long ldk, int F, int C, int R, int S, int s, int Rq,
-                             int Cz, cudaStream_t st) {
+                             int Cz, cudaStream_t st, int pairs) {
   const int n = F * R * S * C;
-  s2d_wgrad_gather_kernel<<<(n + 255) / 256, 256, 0, st>>>(dwz, dw, ldk, F, C, R, S, s, Rq, Cz);
+  s2d_wgrad_gather_kernel<<<(n + 255) / 256, 256, 0, st>>>(dwz, dw, ldk, F, C, R, S, s, Rq, Cz, pairs);
 }
 
 void launch_skip_sync_fixup(float* g, const float* local, int F, int C, int R, int S, long long ldk,
@@ -1626,7 +1649,7 @@ void launch_skip_sync_fixup(float* g, const float* local, int F, int C, int R, i
   template void launch_s2d_input<T>(const float*, T*, int, int, int, int, int, int, int, int, int, \
                                     cudaStream_t);                                              \
   template void launch_s2d_weights<T>(const float*, long long, T*, int, int, int, int, int, int, \
-                                      int, cudaStream_t);                                       \
+                                      int, cudaStream_t, const float*, float*);                 \
   template void launch_im2col_t_nchw<T>(const float*, T*, int, int, int, int, int, int, int, int, int, \
                                         int, long long, cudaStream_t);                                     \
   template void launch_im2col_nchw<T>(const float*, T*, int, int, int, int, int, int, int, int, int, \

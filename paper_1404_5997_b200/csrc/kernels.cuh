@@ -172,13 +172,19 @@ void launch_s2d_input(const float* x, T* z, int B, int C, int H, int W, int s, i
                       int Cz, cudaStream_t st);
 // wz[f][(a*Rq + b)*Cz + ch] = w[f][((s*a+dr)*S + (s*b+dc))*C + c] (zero where
 // s*a+dr >= R, s*b+dc >= S or ch >= s*s*C); w rows of stride ldk.
+// bias2 != nullptr: the pixel-pair layout instead -- one GEMM row per pair of
+// horizontally adjacent output pixels (2u, 2u+1), N = 2F output columns, taps
+// (a, b') with b' in [0, Rq]: wz[p*F + f][(a*(Rq+1) + b')*Cz + ch] = the s2d
+// weight at tap (a, b' - p) (zero outside [0, Rq)), and bias2[p*F + f] = bias[f].
 template <class T>
 void launch_s2d_weights(const float* w, long long ldk, T* wz, int F, int C, int R, int S, int s, int Rq,
-                        int Cz, cudaStream_t st);
+                        int Cz, cudaStream_t st, const float* bias = nullptr, float* bias2 = nullptr);
 // Inverse map of the s2d weight gradient back to the reference layout:
 // dw[f][(r*S + q)*C + c] = dwz[f][((r/s)*Rq + q/s)*Cz + ((r%s)*s + q%s)*C + c].
+// pairs: dwz is the pixel-pair gradient [2F][Rq][Rq+1][Cz]; the two pixel
+// parities are summed (even + odd, rounded once).
 void launch_s2d_wgrad_gather(const float* dwz, float* dw, long long ldk, int F, int C, int R, int S, int s,
-                             int Rq, int Cz, cudaStream_t st);
+                             int Rq, int Cz, cudaStream_t st, int pairs = 0);
 
 // Cluster::set_skip_sync_broadcast negative control (cluster.cpp:306-314): after
 // the all-reduce (g = sum over workers), worker-owned entries -- reference flat

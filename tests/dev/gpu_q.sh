@@ -1,5 +1,5 @@
-# Quick GPU pass: facade GPU test, tolerance report of the step tests, wgrad GEMM sweep.
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_facade.py -q -m gpu > gpurun_out/facade.log 2>&1; echo "facade rc=$?"; tail -2 gpurun_out/facade.log
-HP_TOL_REPORT=1 timeout 900 python -m pytest tests/test_step_gpu.py -q -s -m gpu > gpurun_out/tol.log 2>&1; echo "tol rc=$?"; tail -2 gpurun_out/tol.log
-timeout 600 python tests/dev/wgrad_bench.py > gpurun_out/wgrad_bench.log 2>&1; echo "wgrad rc=$?"
+for i in 1 2; do
+for d in build_old/tests/dev tests/dev; do echo "== $d"; HP_DEV_CM=0 WGRAD_AUTO_ONLY=1 timeout 300 python $d/wgrad_bench.py 384x3456x25088 1600x192x107648 128x768x197120; done
+done > gpurun_out/ab.log 2>&1
+for d in build_old/tests/dev tests/dev; do LABEL=$d timeout 300 python $d/gemm_times.py | grep -E "==|wgrad"; done > gpurun_out/ab_step.log 2>&1
