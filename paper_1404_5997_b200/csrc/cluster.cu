@@ -411,9 +411,45 @@ class ClusterImpl final : public ClusterBase {
   void fc_forward_backward(int j, bool beta, int slot);
   void return_gradients(int j, int slot, cudaStream_t s);
   void marker(int tag, cudaStream_t s) {
-    if (!markers) return;
-    launch_marker(tag, s);
+    if (!markers && !tl_) return;
+    launch_marker(tag, s, tl_, tl_cap_);
     ++launches_;
+  }
+  // Dev timeline (HP_DEV_TIMELINE=<csv path>): timestamped markers around every
+  // GEMM and the main memory-bound kernels, on the stream each runs on; one
+  // CSV row per marker per step (step, name, begin/end, ns). A diagnostic of
+  // the streams' overlap -- the 1-thread marker kernels perturb the step.
+  unsigned long long* tl_ = nullptr;
+  int tl_cap_ = 0;
+  std::vector<std::string> tl_names_;
+  FILE* tl_file_ = nullptr;
+  long long tl_step_ = 0;
+  void tl_mark(const char* name, int layer, bool end, cudaStream_t s) {
+    if (!tl_) return;
+    const std::string key = std::string(name) + "[" + std::to_string(layer) + "]";
+    size_t id = 0;
+    while (id < tl_names_.size() && tl_names_[id] != key) ++id;
+    if (id == tl_names_.size()) tl_names_.push_back(key);
+    marker(1000000 + 2 * static_cast<int>(id) + (end ? 1 : 0), s);
+  }
+  void tl_flush() {
+    if (!tl_) return;
+    std::vector<unsigned long long> h(1 + 2 * static_cast<size_t>(tl_cap_));
+    HP_CUDA(cudaMemcpy(h.data(), tl_, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    const unsigned long long n = std::min<unsigned long long>(h[0], static_cast<unsigned long long>(tl_cap_));
+    for (unsigned long long i = 0; i < n; ++i) {
+      const long long tag = static_cast<long long>(h[1 + 2 * i]);
+      const unsigned long long t = h[2 + 2 * i];
+      if (tag >= 1000000) {
+        const size_t id = static_cast<size_t>((tag - 1000000) / 2);
+        fprintf(tl_file_, "%lld,%s,%s,%llu\n", tl_step_, id < tl_names_.size() ? tl_names_[id].c_str() : "?",
+                (tag & 1) ? "end" : "begin", t);
+      } else {
+        fprintf(tl_file_, "%lld,marker%lld,point,%llu\n", tl_step_, tag, t);
+      }
+    }
+    fflush(tl_file_);
+    ++tl_step_;
   }
   void sgd_fc(double lr, float gscale, bool has_gscale, const hp_hyper& hp);
   void sgd_conv(double lr, const hp_hyper& hp);
@@ -745,6 +781,14 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   ws2_ = ws2_floats_ > 0 ? arena_.make<float>(static_cast<long long>(ws2_floats_)) : nullptr;
   ws3_ = ws3_floats_ > 0 ? arena_.make<float>(static_cast<long long>(ws3_floats_)) : nullptr;
   for (auto& w : w_) build_plans(w);
+  if (const char* tl = getenv("HP_DEV_TIMELINE")) {
+    tl_cap_ = 4096;
+    HP_CUDA(cudaMalloc(&tl_, (1 + 2 * static_cast<size_t>(tl_cap_)) * sizeof(unsigned long long)));
+    HP_CUDA(cudaMemset(tl_, 0, sizeof(unsigned long long)));
+    tl_file_ = fopen(tl, "w");
+    if (!tl_file_) usage_error(std::string("HP_DEV_TIMELINE: cannot open ") + tl);
+    fprintf(tl_file_, "step,name,kind,ns\n");
+  }
   init_params();
   sent.assign(K_, {0, 0, 0, 0});
   received.assign(K_, {0, 0, 0, 0});
@@ -758,6 +802,8 @@ ClusterImpl<TA>::~ClusterImpl() {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (host_parts_) cudaFreeHost(host_parts_);
   if (host_bad_) cudaFreeHost(host_bad_);
+  if (tl_) cudaFree(tl_);
+  if (tl_file_) fclose(tl_file_);
   if (sr_) cudaStreamSynchronize(sr_);
   if (sc_) cudaStreamSynchronize(sc_);
   comm_s_.reset();
@@ -1106,7 +1152,9 @@ void ClusterImpl<TA>::gemm(const GemmPlan& p, const char* tag, int layer, cudaSt
     gemm_launch(p, st);
     HP_CUDA(cudaEventRecord(s.b, st));
   } else {
+    tl_mark(tag, layer, false, st);
     gemm_launch(p, st);
+    tl_mark(tag, layer, true, st);
   }
   launches_ += p.splits > 1 ? 2 : 1;
   gemm_flops_ += flops;
@@ -1201,7 +1249,9 @@ void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
   for (int l = 0; l < nc; ++l) {
     const ConvGeom& c = g_.cg[l];
     if (c.s2d) {
+      tl_mark("s2d_input", l, false, st_);
       launch_s2d_input<TA>(w.x_src, w.z, B, c.C, c.H, c.W, c.stride, c.pad, c.Zh, c.Zw, c.Cz, st_);
+      tl_mark("s2d_input", l, true, st_);
       ++launches_;
     } else if (!c.impl_fwd) {
       if (l == 0) {
@@ -1217,8 +1267,10 @@ void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
     OutLayout yl{};  // stage output in the next layer's q-layout
     if (l + 1 < nc && g_.cg[l + 1].in_q) yl = OutLayout{g_.cg[l + 1].Hq, g_.cg[l + 1].Wq, g_.cg[l + 1].pad};
     if (c.lrn_n > 0 && c.pk > 0) {
+      tl_mark("lrn_pool_fwd", l, false, st_);
       launch_lrn_pool_fwd<TA>(w.act[l], w.pool[l], w.widx[l], B, c.OH, c.OWs, c.F, c.lrn_n, c.lrn_alpha,
                               c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, st_, yl);
+      tl_mark("lrn_pool_fwd", l, true, st_);
       ++launches_;
     } else if (c.lrn_n > 0) {
       launch_lrn_fwd<TA>(w.act[l], w.lrn[l], w.lrn_d[l], c.P, c.F, c.lrn_n, c.lrn_alpha, c.lrn_beta,
@@ -1415,8 +1467,10 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
   const int B = static_cast<int>(b_);
   const OutLayout zl = c.in_q ? OutLayout{c.Hq, c.Wq, c.pad} : OutLayout{};  // dz layout
   if (c.pk > 0 && c.lrn_n > 0) {
+    tl_mark("lrn_pool_bwd", l, false, st_);
     launch_lrn_pool_bwd<TA>(cs.gout, w.widx[l], w.act[l], w.dz[l], B, c.OH, c.OWs, c.F, c.lrn_n, c.lrn_alpha,
                             c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, c.relu ? 1 : 0, st_, zl);
+    tl_mark("lrn_pool_bwd", l, true, st_);
     ++launches_;
   } else if (c.pk > 0) {
     launch_maxpool_bwd_w<TA, TA>(cs.gout, w.widx[l], w.dz[l], mask, B, c.OH, c.OWs, c.F, c.pk, c.ps, c.PH,
@@ -1440,7 +1494,9 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
     HP_CUDA(cudaStreamWaitEvent(ws, ev_dz_[l], 0));
   }
   // bias grad = channel sums of dz (model.cpp:184-202)
+  tl_mark("colsum", l, false, ws);
   launch_colsum<TA>(w.dz[l], c.Pq, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, ws);
+  tl_mark("colsum", l, true, ws);
   launches_ += 2;
   gemm(w.conv_wgrad[l], "conv_wgrad", l, ws);
   if (c.s2d) {
@@ -1537,6 +1593,7 @@ template <class TA>
 void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* targets, int mem_kind,
                               const hp_hyper& hp, double lr) {
   const int nl = comm_->nlocal();
+  if (tl_) HP_CUDA(cudaMemsetAsync(tl_, 0, sizeof(unsigned long long), st_));
   const double fc_lr = variable_ ? (hp.has_fc_partial_lr ? hp.fc_partial_lr : lr) : lr;
   const auto& in = g_.input;
   const long long xin = b_ * in[0] * in[1] * in[2];
@@ -1678,8 +1735,11 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
     const bool scale = num_sub_ > 1;
     sgd_fc(lr, static_cast<float>(1.0 / static_cast<double>(num_sub_)), scale, hp);
   }
+  tl_mark("sgd_conv", 0, false, st_);
   sgd_conv(lr, hp);
+  tl_mark("sgd_conv", 0, true, st_);
   for (auto& w : w_) rotate_all(w);
+  tl_mark("rotate", 0, true, st_);
   // loss partials (+ the domain-error flag) to pinned host memory
   const size_t np = static_cast<size_t>(num_sub_) * xblocks_;
   if (nl == 1 && K_ > 1) {
@@ -1838,6 +1898,7 @@ void ClusterImpl<TA>::run_step(const float* const* batches, const float* const* 
     if (graphable) graphs_[key];  // remember: capture on the next occurrence
   }
   wait_step();
+  tl_flush();
   float ms = 0.f;
   HP_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
   last_ms = ms;

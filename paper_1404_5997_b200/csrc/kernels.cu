@@ -1768,11 +1768,23 @@ void launch_rowsum(const T* x, int R, int n, long long ldx, float* out, int beta
   rowsum_kernel<T><<<static_cast<int>(blocks), threads, 0, st>>>(x, R, n, ldx, out, beta);
 }
 
-__global__ void marker_kernel(int tag) {
+// tl != nullptr (dev timeline): append (tag, %globaltimer ns) at tl[1 + 2i], i = tl[0]++.
+__global__ void marker_kernel(int tag, unsigned long long* tl, int cap) {
   if (tag < 0) asm volatile("trap;");  // never: keeps the argument live
+  if (tl) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long i = atomicAdd(tl, 1ull);
+    if (i < static_cast<unsigned long long>(cap)) {
+      tl[1 + 2 * i] = static_cast<unsigned long long>(tag);
+      tl[2 + 2 * i] = t;
+    }
+  }
 }
 
-void launch_marker(int tag, cudaStream_t st) { marker_kernel<<<1, 1, 0, st>>>(tag); }
+void launch_marker(int tag, cudaStream_t st, unsigned long long* tl, int cap) {
+  marker_kernel<<<1, 1, 0, st>>>(tag, tl, cap);
+}
 bool is_marker_kernel(const void* func) { return func == reinterpret_cast<const void*>(&marker_kernel); }
 
 __global__ void target_check_kernel(const float* __restrict__ t, long long n, int* __restrict__ bad) {

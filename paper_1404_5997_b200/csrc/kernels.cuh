@@ -74,7 +74,8 @@ int launch_xent(const float* z, long long ldzin, const float* t, int L, int c0, 
 int xent_blocks(int Ls, int n);
 
 // Debug marker: a 1-thread kernel carrying an integer tag (graph-structure tests).
-void launch_marker(int tag, cudaStream_t st);
+// tl: optional dev timeline buffer (see marker_kernel), cap entries.
+void launch_marker(int tag, cudaStream_t st, unsigned long long* tl = nullptr, int cap = 0);
 bool is_marker_kernel(const void* func);
 // Device-resident targets: bad |= any t outside [0,1] (logistic_xent's
 // DomainError, tensor.cpp:600-603, checked before a step changes any state).
