@@ -220,6 +220,7 @@ HP_API int hp_kernel_lrn_pool_bwd(int math, const float* gy, const uint8_t* widx
           float* ws = nullptr;
           const long long M = static_cast<long long>(B) * H * W;
           HP_CUDA(cudaMalloc(&ws, sizeof(float) * colsum_ws_floats(M, C)));
+          HP_CUDA(cudaMemsetAsync(ws, 0, sizeof(float) * 4, st));  // the colsum ticket
           launch_colsum<T>(static_cast<const T*>(dz), M, C, C, bias_grad, ws, st);
           HP_CUDA(cudaStreamSynchronize(st));
           HP_CUDA(cudaFree(ws));
