@@ -364,6 +364,36 @@ HP_API int hp_kernel_lrn_pool_bwd(int math, const float* gy, const uint8_t* widx
 HP_API int hp_kernel_sgd(float* w, float* mom, const float* g, int64_t n, double lr, double momentum,
                          double weight_decay, float gscale, int has_gscale, void* bf16_copy, void* stream);
 
+/* ---- input pipeline: SPEC data_gen ----------------------
+ * The deterministic synthetic classification dataset (class-conditional
+ * Gaussian blobs), generated on the GPU. The reference specifies this module
+ * but has no code for it; the generator is defined in csrc/datagen.cu:
+ *   class(i) = perm(i) mod L  (perm: seeded bijection of [0, N); every class
+ *              holds floor(N/L) or ceil(N/L) examples)
+ *   x_i[e]   = separation * mean(class(i), e) + noise(i, e), both N(0, 1) from
+ *              Philox4x32-10 keyed by seed (the class means are separation-scaled
+ *              standard normals; unit-variance noise)
+ *   t_i      = one_hot(class(i))
+ * Examples [first, first + count) are written as inputs [count][C][H][W] and
+ * targets [count][L] (the run_step batch layouts) -- bit-identical to the same
+ * rows of the whole dataset. mem_kind HP_MEM_DEVICE: device pointers, stream-
+ * ordered on `stream` (the input pipeline: run_step consumes the batch with
+ * HP_MEM_DEVICE, no host copy); HP_MEM_HOST: generated on the current device
+ * and copied out before return.
+ * Errors: HP_ERR_CONFIG for num_classes < 2, negative num_examples, empty
+ * shape, negative separation; HP_ERR_USAGE for a range outside [0, N). */
+typedef struct hp_dataset_spec {
+  int64_t num_examples;
+  int32_t channels, height, width;
+  int32_t num_classes;
+  uint64_t seed;
+  double separation; /* std of the class means (mean distance ~ separation * sqrt(2*C*H*W)) */
+} hp_dataset_spec;
+HP_API int hp_data_generate(const hp_dataset_spec* spec, int64_t first, int64_t count, float* inputs,
+                            float* targets, int mem_kind, void* stream);
+/* *cls = the class of example `index` (host evaluation of the same permutation). */
+HP_API int hp_data_class_of(const hp_dataset_spec* spec, int64_t index, int64_t* cls);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,5 +9,6 @@ from .api import (Cluster, ClusterConfig, ConfigError, ConvLayerSpec, CudaError,
                   Phase, Precision, Scheme, StepMetrics, StepResult, TraceEvent, Transport, UsageError,
                   gaussian, gaussian_f32, nccl_unique_id, shard_range, step_accounting)
 from .specs import alexnet_1col, alexnet_standin_227, synthetic_batch, tiny_cnn  # noqa: F401
+from . import data  # noqa: F401  (input pipeline: SPEC data_gen on the GPU)
 
 __version__ = "0.1.0"

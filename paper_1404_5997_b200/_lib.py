@@ -114,6 +114,11 @@ class HpGemmDesc(C.Structure):
     ]
 
 
+class HpDatasetSpec(C.Structure):
+    _fields_ = [("num_examples", C.c_int64), ("channels", C.c_int32), ("height", C.c_int32),
+                ("width", C.c_int32), ("num_classes", C.c_int32), ("seed", C.c_uint64), ("separation", C.c_double)]
+
+
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -145,6 +150,8 @@ def _load() -> C.CDLL:
                           C.c_int),
         "hp_kernel_conv_dgrad": ([C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_int,
                                   C.c_int, C.c_int, P, P], C.c_int),
+        "hp_data_generate": ([C.POINTER(HpDatasetSpec), C.c_int64, C.c_int64, P, P, C.c_int, P], C.c_int),
+        "hp_data_class_of": ([C.POINTER(HpDatasetSpec), C.c_int64, C.POINTER(C.c_int64)], C.c_int),
     }
     optional = {
         "hp_cluster_create": ([C.POINTER(HpModelSpec), C.POINTER(HpClusterConfig), C.POINTER(P)], C.c_int),

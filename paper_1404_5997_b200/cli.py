@@ -22,7 +22,10 @@ failure. `HPSIM_OUTPUT_DIR` overrides output_dir. Config: JSON, one file:
    "cluster": {"workers": K, "per_worker_batch": b, "scheme": "A|B|C|DP",
                "variable_batch": false, "seed": 1, "math_mode": "bf16|tf32|f32x3"},
    "hyper": {"momentum": 0.9, "lr": 0.01, "weight_decay": 0.0005, "fc_partial_lr": null},
-   "data": {"seed_data": 100, "seed_label": 200},
+   "data": {"seed_data": 100, "seed_label": 200}   (per-step seeded N(0,1) batches), or
+           {"generator": "gaussian_blobs", "num_examples": N, "seed": s, "separation": sigma}
+           (SPEC data_gen, generated on the GPU into the step's device inputs;
+           N a multiple of K*b, epochs partition it -- data.py),
    "steps": 5, "output_dir": "out"}
 
   python -m paper_1404_5997_b200.cli cost-report --config run.json [--json]
@@ -67,7 +70,8 @@ def default_config() -> Dict[str, Any]:
             "cluster": {"workers": 1, "per_worker_batch": 16, "scheme": "B", "variable_batch": False, "seed": 1,
                         "math_mode": "bf16"},
             "hyper": {"momentum": 0.9, "lr": 0.01, "weight_decay": 0.0005, "fc_partial_lr": None},
-            "data": {"seed_data": 100, "seed_label": 200},
+            "data": {"seed_data": 100, "seed_label": 200, "generator": None, "num_examples": None, "seed": 0,
+                     "separation": 1.0},
             "steps": 5, "output_dir": "out",
             "cost": {"machine": "b200", "measured_step_ms": None}}
 
@@ -213,6 +217,25 @@ def read_checkpoint(path: str) -> Dict[str, np.ndarray]:
 
 
 # ---------------------------------------------------------------- commands
+def dataset_spec(spec, cfg):
+    """SPEC data_gen DatasetSpec of the config (None: per-step synthetic batches)."""
+    d = cfg["data"]
+    if d.get("generator") is None:
+        return None
+    from .data import DatasetSpec
+    if d["generator"] != "gaussian_blobs":
+        raise ValidationError(f"config.data.generator: expected gaussian_blobs, got {d['generator']!r}")
+    n = d.get("num_examples")
+    c = cfg["cluster"]
+    kb = c["workers"] * c["per_worker_batch"]
+    if not isinstance(n, int) or n < kb or n % kb:
+        raise ValidationError(f"config.data.num_examples: expected a positive multiple of K*b = {kb}, got {n!r}")
+    if spec.num_classes < 2:
+        raise ValidationError("config.data: num_classes must be >= 2 (SPEC.md:502)")
+    return DatasetSpec(num_examples=n, input_shape=tuple(spec.input_shape), num_classes=spec.num_classes,
+                       seed=int(d.get("seed", 0)), separation=float(d.get("separation", 1.0)))
+
+
 def batches(spec, cfg, step: int, K: int, b: int):
     from .specs import synthetic_batch
     d = cfg["data"]
@@ -225,6 +248,7 @@ def cmd_train(cfg, out=None) -> int:
     from .api import Cluster
     spec = model_spec(cfg)
     validate(cfg)
+    ds = dataset_spec(spec, cfg)
     outdir = os.environ.get("HPSIM_OUTPUT_DIR", cfg["output_dir"])
     os.makedirs(outdir, exist_ok=True)
     ccfg = cluster_config(cfg)
@@ -237,17 +261,27 @@ def cmd_train(cfg, out=None) -> int:
         wr.writerow(CSV_HEADER)
         if cfg["steps"] > 0:
             cluster = Cluster(spec, ccfg)
+            feed = None
+            if ds is not None:  # the input pipeline: batches generated on the GPU
+                from .data import DeviceBatches
+                feed = DeviceBatches(ds, K, b)
             for s in range(cfg["steps"]):
-                xb = batches(spec, cfg, s, K, b)
                 t0 = time.perf_counter()
-                r = cluster.run_step([x for x, _ in xb], [t for _, t in xb], hp)
+                if feed is not None:
+                    xs, ts = feed.batches(s, stream=cluster.stream_ptr())
+                    r = cluster.run_step(xs, ts, hp, device=True)
+                else:
+                    xb = batches(spec, cfg, s, K, b)
+                    t0 = time.perf_counter()
+                    r = cluster.run_step([x for x, _ in xb], [t for _, t in xb], hp)
                 wall = time.perf_counter() - t0
                 m = r.metrics
                 # sim_step_time_s: deterministic model time of the step on one
                 # B200 -- algorithmic GEMM FLOPs at the measured sustained bf16
                 # rate (the B200 path has no cost-model simulation; the measured
                 # device time is nondeterministic and goes to the log instead)
-                wr.writerow([s, 0, repr(float(m.loss)), repr(float(hp.lr))] + [int(v) for v in m.bytes_sent] +
+                epoch = (s * K * b) // ds.num_examples if ds is not None else 0
+                wr.writerow([s, epoch, repr(float(m.loss)), repr(float(hp.lr))] + [int(v) for v in m.bytes_sent] +
                             [repr(sim_s), f"{wall:.6f}"])
             write_checkpoint(os.path.join(outdir, "checkpoint"), param_tensors(cluster, spec))
             cluster.close()

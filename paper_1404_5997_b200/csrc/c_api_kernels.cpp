@@ -2,6 +2,7 @@
 #include <cstring>
 #include <string>
 
+#include "datagen.hpp"
 #include "errors.hpp"
 #include "gemm.cuh"
 #include "kernels.cuh"
@@ -220,7 +221,6 @@ HP_API int hp_kernel_lrn_pool_bwd(int math, const float* gy, const uint8_t* widx
           float* ws = nullptr;
           const long long M = static_cast<long long>(B) * H * W;
           HP_CUDA(cudaMalloc(&ws, sizeof(float) * colsum_ws_floats(M, C)));
-          HP_CUDA(cudaMemsetAsync(ws, 0, sizeof(float) * 4, st));  // the colsum ticket
           launch_colsum<T>(static_cast<const T*>(dz), M, C, C, bias_grad, ws, st);
           HP_CUDA(cudaStreamSynchronize(st));
           HP_CUDA(cudaFree(ws));
@@ -255,3 +255,41 @@ HP_API int hp_kernel_sgd(float* w, float* mom, const float* g, int64_t n, double
 }
 
 }  // extern "C"
+
+HP_API int hp_data_generate(const hp_dataset_spec* spec, int64_t first, int64_t count, float* inputs,
+                            float* targets, int mem_kind, void* stream) {
+  return guarded([&] {
+    if (!spec) usage_error("data_generate: null spec");
+    datagen_validate(*spec);
+    if (count > 0 && (!inputs || !targets)) usage_error("data_generate: null output");
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (mem_kind == HP_MEM_DEVICE) {
+      datagen_launch(*spec, first, count, inputs, targets, st);
+      return;
+    }
+    if (mem_kind != HP_MEM_HOST) usage_error("data_generate: bad mem_kind");
+    if (first < 0 || count < 0 || first + count > spec->num_examples) datagen_launch(*spec, first, count, nullptr, nullptr, st);
+    if (count == 0) return;
+    const size_t nx = static_cast<size_t>(count) * spec->channels * spec->height * spec->width;
+    const size_t nt = static_cast<size_t>(count) * spec->num_classes;
+    float* d = nullptr;
+    HP_CUDA(cudaMalloc(&d, (nx + nt) * sizeof(float)));
+    try {
+      datagen_launch(*spec, first, count, d, d + nx, st);
+      HP_CUDA(cudaMemcpyAsync(inputs, d, nx * sizeof(float), cudaMemcpyDeviceToHost, st));
+      HP_CUDA(cudaMemcpyAsync(targets, d + nx, nt * sizeof(float), cudaMemcpyDeviceToHost, st));
+      HP_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+      cudaFree(d);
+      throw;
+    }
+    HP_CUDA(cudaFree(d));
+  });
+}
+
+HP_API int hp_data_class_of(const hp_dataset_spec* spec, int64_t index, int64_t* cls) {
+  return guarded([&] {
+    if (!spec || !cls) usage_error("data_class_of: null argument");
+    *cls = datagen_class_of(*spec, index);
+  });
+}

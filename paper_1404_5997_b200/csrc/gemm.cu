@@ -1739,7 +1739,9 @@ static TileChoice choose_tile(int math, const GemmOperand& b, int M, int N) {
     const int slots = c.cta2 ? 74 : 148;
     const int waves = cdiv(units, slots);
     const double wave = units >= slots ? static_cast<double>(units) / (waves * slots) : 1.0;
-    const double score = c.base * nfill * mfill * wave;
+    // (ties -- e.g. pair/192 at 2/3 fill vs 128 at full fill for N = 128 -- go to
+    // the tile that wastes less: measured 87.0 vs 84.6 us on conv1's pixel pairs)
+    const double score = c.base * nfill * mfill * wave + 1e-3 * nfill * mfill;
     if (score > best_score + 1e-9) {
       best_score = score;
       best = {c.cta2, c.bn};

@@ -1,5 +1,17 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_lrn_pool_gpu.py tests/test_step_gpu.py tests/test_alexnet_parity_gpu.py -x -q -m gpu > gpurun_out/pt.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pt.log
-LABEL=colsum timeout 300 python tests/dev/gemm_times.py > gpurun_out/times.log 2>&1; head -1 gpurun_out/times.log
-HP_DEV_TIMELINE=gpurun_out/timeline.csv timeout 300 python tests/dev/gemm_times.py > /dev/null 2>&1
-python tests/dev/timeline.py gpurun_out/timeline.csv 25 > gpurun_out/timeline.txt 2>&1; grep -E "colsum|step|busy" gpurun_out/timeline.txt
+timeout 900 python -m pytest tests/test_data_gen.py tests/test_cli.py tests/test_abi.py -x -q -m gpu > gpurun_out/dg.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/dg.log
+for i in 1 2 3; do for d in build_old/tests/dev tests/dev; do LABEL=$d timeout 300 python $d/gemm_times.py 2>&1 | head -1; done; done > gpurun_out/ab3.log
+cat gpurun_out/ab3.log
+python - <<'PY'
+import time, torch, sys
+sys.path.insert(0, '.')
+from paper_1404_5997_b200 import data as D
+s = D.DatasetSpec(num_examples=1280, input_shape=(3, 224, 224), num_classes=1000, seed=1, separation=0.1)
+x, t = D.generate(s, 0, 128)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+e0.record()
+for i in range(10): D.generate(s, 128 * (i % 10), 128)
+e1.record(); torch.cuda.synchronize()
+print(f"datagen AlexNet batch (128 x 3x224x224): {e0.elapsed_time(e1) / 10 * 1e3:.1f} us")
+PY

@@ -44,6 +44,28 @@ def test_validation_exit_code_1(tmp_path, capsys, over, msg):
     assert msg in capsys.readouterr().err
 
 
+@pytest.mark.parametrize("data,msg", [
+    ({"generator": "gaussian_blobs", "num_examples": 20}, "multiple of K*b"),
+    ({"generator": "mnist", "num_examples": 32}, "gaussian_blobs"),
+])
+def test_data_generator_validation(tmp_path, capsys, data, msg):
+    rc = cli.main(["train", "--config", write_cfg(tmp_path, data=data)])
+    assert rc == cli.EXIT_VALIDATION
+    assert msg in capsys.readouterr().err
+
+
+@pytest.mark.gpu
+def test_train_on_generated_device_batches(tmp_path):
+    """SPEC data_gen as the input pipeline: batches generated on the GPU into the
+    step's device inputs; epochs partition the dataset (epoch column advances)."""
+    rc = cli.main(["train", "--config", write_cfg(tmp_path, steps=6, data={
+        "generator": "gaussian_blobs", "num_examples": 32, "seed": 3, "separation": 0.5})])
+    assert rc == 0
+    rows = list(csv.reader(open(tmp_path / "out" / "metrics.csv")))[1:]
+    assert [int(r[1]) for r in rows] == [0, 0, 1, 1, 2, 2]
+    assert all(np.isfinite(float(r[2])) for r in rows)
+
+
 def test_zero_steps_header_only_csv(tmp_path):
     rc = cli.main(["train", "--config", write_cfg(tmp_path, steps=0)])
     assert rc == 0

@@ -1,0 +1,146 @@
+"""SPEC data_gen -- the input pipeline's dataset generator,
+on the GPU (hp_data_generate). The reference specifies it but has no code, so
+parity is against the SPEC's properties and an independent numpy restatement of
+the generator's definition (oracle/datagen.py, test infrastructure):
+  * determinism: same spec + seed -> bit-identical tensors; any [first, count)
+    slice equals the same rows of the whole set; host and device paths agree;
+  * empty case (num_examples 0 / count 0) with the right trailing shape;
+  * class balance: every class count within +-1 of N/L (exact: perm is a bijection);
+  * L < 2 -> configuration error;
+  * learnability: L = 2, class means 10 sigma apart -> the toy model trained 50
+    steps (run_step on device batches, no host copy) reaches < 5% training error;
+  * epoch batching partitions the examples without overlap or omission."""
+import numpy as np
+import pytest
+
+import oracle.datagen as OD
+import paper_1404_5997_b200 as hp
+from paper_1404_5997_b200 import data as D
+
+
+def spec(n=1000, L=7, shape=(3, 8, 8), seed=11, sep=0.5):
+    return D.DatasetSpec(num_examples=n, input_shape=shape, num_classes=L, seed=seed, separation=sep)
+
+
+def test_num_classes_below_two_is_a_config_error():
+    with pytest.raises(hp.ConfigError, match="num_classes"):
+        D.class_of(spec(L=1), 0)
+    with pytest.raises(hp.ConfigError, match="num_classes"):
+        D.generate(spec(L=1), 0, 4, device=False)
+    with pytest.raises(hp.ConfigError, match="generator"):
+        D.DatasetSpec(10, (1, 1, 1), 2, generator="images")._c()
+
+
+@pytest.mark.parametrize("n,L", [(1000, 7), (1, 2), (97, 10), (4096, 2), (12345, 1000)])
+def test_class_balance_and_permutation(n, L):
+    s = spec(n=n, L=L)
+    got = np.array([D.class_of(s, i) for i in range(n)])
+    ref = OD.classes(s.seed, n, L, np.arange(n))
+    assert np.array_equal(got, ref)
+    perm = OD.permute(s.seed, n, np.arange(n))
+    assert np.array_equal(np.sort(perm), np.arange(n))  # a bijection of [0, N)
+    counts = np.bincount(got, minlength=L)
+    assert counts.max() - counts.min() <= 1 and abs(counts - n / L).max() < 1
+
+
+def test_class_of_range_is_a_usage_error():
+    with pytest.raises(hp.UsageError):
+        D.class_of(spec(n=10), 10)
+
+
+def test_epoch_batches_partition_the_dataset():
+    N, K, b = 96, 3, 8
+    seen = []
+    for step in range(N // (K * b)):
+        for first, cnt in D.epoch_ranges(N, K, b, step):
+            seen += list(range(first, first + cnt))
+    assert sorted(seen) == list(range(N))
+    assert D.epoch_ranges(N, K, b, N // (K * b)) == D.epoch_ranges(N, K, b, 0)  # next epoch
+    with pytest.raises(hp.ConfigError, match="multiple"):
+        D.epoch_ranges(100, K, b, 0)
+
+
+@pytest.mark.gpu
+def test_deterministic_sliced_and_host_device_identical():
+    import torch
+    s = spec(n=300, L=5, shape=(3, 9, 7))
+    x1, t1 = D.generate(s)
+    x2, t2 = D.generate(s)
+    assert torch.equal(x1, x2) and torch.equal(t1, t2)
+    xa, ta = D.generate(s, 0, 123)
+    xb, tb = D.generate(s, 123, 177)
+    assert torch.equal(torch.cat([xa, xb]), x1) and torch.equal(torch.cat([ta, tb]), t1)
+    xh, th = D.generate(s, 50, 100, device=False)
+    assert np.array_equal(xh, x1[50:150].cpu().numpy()) and np.array_equal(th, t1[50:150].cpu().numpy())
+    assert tuple(x1.shape) == (300, 3, 9, 7) and tuple(t1.shape) == (300, 5)
+
+
+@pytest.mark.gpu
+def test_empty_cases():
+    s = spec(n=0)
+    x, t = D.generate(s)
+    assert tuple(x.shape) == (0, 3, 8, 8) and tuple(t.shape) == (0, 7)
+    x, t = D.generate(spec(n=10), 10, 0, device=False)
+    assert x.shape == (0, 3, 8, 8) and t.shape == (0, 7)
+    with pytest.raises(hp.UsageError):
+        D.generate(spec(n=10), 5, 6)
+
+
+@pytest.mark.gpu
+def test_values_match_the_restatement():
+    s = spec(n=500, L=4, shape=(3, 5, 5), sep=2.0)
+    x, t = D.generate(s, device=False)
+    for i in (0, 1, 7, 250, 499):
+        ref, cls = OD.example(s.seed, s.num_examples, s.num_classes, s.separation, s.input_shape, i)
+        assert np.abs(x[i].ravel().astype(np.float64) - ref).max() < 3e-5, i
+        onehot = np.zeros(4, np.float32)
+        onehot[cls] = 1
+        assert np.array_equal(t[i], onehot)
+    # unit-variance noise around separation-scaled class means
+    cls = t.argmax(1)
+    means = np.stack([x[cls == c].mean(0) for c in range(4)])
+    resid = x - means[cls]
+    assert abs(resid.std() - 1.0) < 0.02 and abs(means.std() - 2.0) < 0.2
+
+
+@pytest.mark.gpu
+def test_two_blobs_ten_sigma_apart_are_learned_in_50_steps():
+    """L=2, separated means (distance 10 sigma) -> toy model trained 50
+    steps reaches < 5% training error. The batches are generated on the GPU into
+    the run_step input buffers (HP_MEM_DEVICE)."""
+    import oracle as O
+    import torch
+    spec_m = hp.tiny_cnn()
+    spec_m.num_classes = 2
+    spec_m.fc_layers[-1].out_dim = 2
+    Dm = 3 * 32 * 32
+    s = D.DatasetSpec(num_examples=1024, input_shape=(3, 32, 32), num_classes=2, seed=5,
+                      separation=10.0 / np.sqrt(2 * Dm))
+    K, b = 2, 32
+    c = hp.Cluster(spec_m, hp.ClusterConfig(workers=K, per_worker_batch=b, scheme=hp.Scheme.B, seed=1,
+                                            math_mode=hp.MathMode.BF16))
+    feed = D.DeviceBatches(s, K, b)
+    for step in range(50):
+        xs, ts = feed.batches(step)
+        torch.cuda.synchronize()
+        c.run_step(xs, ts, hp.HyperParams(momentum=0.9, lr=0.01, weight_decay=0.0), device=True)
+    # training error of the trained model on 256 training examples (oracle forward, double)
+    conv, fc = c.gathered_model()
+    x, t = D.generate(s, 0, 256, device=False)
+    a = x.astype(np.float64)
+    lib = O.oracle_lib()
+    for (k, bias), L in zip(conv, spec_m.conv_layers):
+        B, Cc, H, W = a.shape
+        OH = (H + 2 * L.pad - L.kernel) // L.stride + 1
+        y = np.empty((B, L.out_channels, OH, OH))
+        kk = np.ascontiguousarray(k, dtype=np.float64)
+        assert lib.or_conv2d_forward(O._dp(np.ascontiguousarray(a)), B, Cc, H, W, O._dp(kk), L.out_channels,
+                                     L.kernel, L.kernel, L.stride, L.pad, 0, O._dp(y)) == 0
+        a = np.maximum(y + bias.reshape(1, -1, 1, 1), 0.0)
+    a = a.reshape(a.shape[0], -1)
+    for li, (w, bias) in enumerate(fc):
+        a = a @ w.astype(np.float64) + bias
+        if spec_m.fc_layers[li].relu:
+            a = np.maximum(a, 0.0)
+    err = float((a.argmax(1) != t.argmax(1)).mean())
+    assert err < 0.05, err
