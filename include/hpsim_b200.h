@@ -387,7 +387,8 @@ typedef struct hp_dataset_spec {
   int32_t channels, height, width;
   int32_t num_classes;
   uint64_t seed;
-  double separation; /* std of the class means (mean distance ~ separation * sqrt(2*C*H*W)) */
+  double separation; /* std of the class means: two class means differ by separation*sqrt(2) per
+                        coordinate (RMS) -- 10/sqrt(2) puts them 10 sigma apart */
 } hp_dataset_spec;
 HP_API int hp_data_generate(const hp_dataset_spec* spec, int64_t first, int64_t count, float* inputs,
                             float* targets, int mem_kind, void* stream);

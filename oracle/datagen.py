@@ -10,10 +10,11 @@ and this independent restatement of the generator's definition:
   (a lo, a hi, m, stream); class(i) = perm(i) mod L with perm a balanced
   4-round Feistel network on [0, 2^bits) (bits even, 2^bits >= N) cycle-walked
   into [0, N), round function = Philox(counter (R lo, R hi, round, 3)) low
-  `bits/2` bits; x_i[2m + j] = separation * BM_j(Philox(class, m, stream 1)) +
-  BM_j(Philox(i, m, stream 2)), BM = Box-Muller on u1 = (c0 + 1) 2^-32,
-  u2 = c1 2^-32 (computed here in float64; the GPU uses float math, so values
-  agree to ~1e-5 while the integer parts -- classes, one-hot targets -- are exact).
+  `bits/2` bits; x_i[4m + j] = separation * BM_j(Philox(class, m, stream 1)) +
+  BM_j(Philox(i, m, stream 2)), BM = Box-Muller on (c0, c1) for j = 0, 1 and
+  (c2, c3) for j = 2, 3, u1 = (c + 1) 2^-32, u2 = c' 2^-32 (computed here in
+  float64; the GPU uses float math, so values agree to ~1e-5 while the integer
+  parts -- classes, one-hot targets -- are exact).
 """
 import numpy as np
 
@@ -75,13 +76,14 @@ def _box_muller(c0, c1):
 
 
 def normals(seed, stream, a, D):
-    """The D values g(stream, a, 0..D-1)."""
-    m = np.arange((D + 1) // 2, dtype=np.uint64)
+    """The D values g(stream, a, 0..D-1): quad m = Box-Muller of (c0, c1) then (c2, c3)."""
+    m = np.arange((D + 3) // 4, dtype=np.uint64)
     a = np.uint64(a)
     c = philox(np.full_like(m, a & MASK32), np.full_like(m, a >> np.uint64(32)), m, np.full_like(m, stream), seed)
     z0, z1 = _box_muller(c[0], c[1])
-    out = np.empty(2 * len(m))
-    out[0::2], out[1::2] = z0, z1
+    z2, z3 = _box_muller(c[2], c[3])
+    out = np.empty(4 * len(m))
+    out[0::4], out[1::4], out[2::4], out[3::4] = z0, z1, z2, z3
     return out[:D]
 
 

@@ -10,9 +10,9 @@
 //   x_i[e]   = separation * g(MEAN, class(i), e) + g(NOISE, i, e)
 //   t_i      = one_hot(class(i))
 //   g(stream, a, e): standard normals from Philox4x32-10 (key = seed, counter =
-//   (a lo, a hi, e / 2, stream)); Box-Muller on the first two 32-bit outputs
-//   (u1 = (c0 + 1) 2^-32, u2 = c1 2^-32, float math) gives the pair
-//   (r cos 2 pi u2, r sin 2 pi u2) for elements (e even, e odd).
+//   (a lo, a hi, e / 4, stream)); Box-Muller on output words (c0, c1) and
+//   (c2, c3) (u1 = (c + 1) 2^-32, u2 = c' 2^-32, float math) gives
+//   (r cos 2 pi u2, r sin 2 pi u2) twice: elements 4m .. 4m+3.
 //
 // Everything is a pure function of (spec, example index, element index), so a
 // batch [first, first + count) is bit-identical to the same rows of the whole
@@ -60,16 +60,24 @@ __host__ __device__ inline void philox(uint32_t c[4], uint32_t k0, uint32_t k1) 
   }
 }
 
-// The normal pair of counter (a, pair m) of `stream`.
-__device__ inline float2 normal_pair(uint64_t seed, uint32_t stream, uint64_t a, uint32_t m) {
-  uint32_t c[4] = {static_cast<uint32_t>(a), static_cast<uint32_t>(a >> 32), m, stream};
-  philox(c, static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
-  const float u1 = (static_cast<float>(c[0]) + 1.0f) * 2.3283064365386963e-10f;  // (0, 1]
-  const float u2 = static_cast<float>(c[1]) * 2.3283064365386963e-10f;           // [0, 1]
+__device__ inline void box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
+  const float u1 = (static_cast<float>(a) + 1.0f) * 2.3283064365386963e-10f;  // (0, 1]
+  const float u2 = static_cast<float>(b) * 2.3283064365386963e-10f;           // [0, 1]
   const float r = sqrtf(-2.0f * logf(u1));
   float sn, cs;
   sincospif(2.0f * u2, &sn, &cs);
-  return make_float2(r * cs, r * sn);
+  z0 = r * cs;
+  z1 = r * sn;
+}
+
+// The four normals of counter (a, quad m) of `stream`.
+__device__ inline float4 normal_quad(uint64_t seed, uint32_t stream, uint64_t a, uint32_t m) {
+  uint32_t c[4] = {static_cast<uint32_t>(a), static_cast<uint32_t>(a >> 32), m, stream};
+  philox(c, static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+  float4 z;
+  box_muller(c[0], c[1], z.x, z.y);
+  box_muller(c[2], c[3], z.z, z.w);
+  return z;
 }
 
 struct PermKey {
@@ -106,13 +114,13 @@ PermKey perm_key(const hp_dataset_spec& s) {
   return PermKey{s.seed, bits, s.num_examples};
 }
 
-// Units of (example r, 512-element chunk): thread 0 finds the example's class
-// (a few Philox calls) once per unit; each thread then makes one element pair.
+// Units of (example r, 1024-element chunk): thread 0 finds the example's class
+// (a few Philox calls) once per unit; each thread then makes one element quad.
 __global__ void __launch_bounds__(256) datagen_kernel(hp_dataset_spec s, PermKey pk, int64_t first, int64_t count,
                                                       float* __restrict__ x, float* __restrict__ t) {
   __shared__ int64_t cls_s;
   const int64_t D = static_cast<int64_t>(s.channels) * s.height * s.width;
-  const int64_t nchunk = (D + 511) / 512;
+  const int64_t nchunk = (D + 1023) / 1024;
   const float sep = static_cast<float>(s.separation);
   for (int64_t u = blockIdx.x; u < count * nchunk; u += gridDim.x) {
     const int64_t r = u / nchunk, chunk = u - r * nchunk;
@@ -120,14 +128,14 @@ __global__ void __launch_bounds__(256) datagen_kernel(hp_dataset_spec s, PermKey
     if (threadIdx.x == 0) cls_s = permute(pk, i) % s.num_classes;
     __syncthreads();
     const int64_t cls = cls_s;
-    const int64_t e0 = chunk * 512 + 2 * threadIdx.x;
+    const int64_t e0 = chunk * 1024 + 4 * threadIdx.x;
     if (e0 < D) {
-      const uint32_t m = static_cast<uint32_t>(e0 >> 1);
-      const float2 mu = normal_pair(s.seed, kStreamMean, static_cast<uint64_t>(cls), m);
-      const float2 nz = normal_pair(s.seed, kStreamNoise, static_cast<uint64_t>(i), m);
+      const uint32_t m = static_cast<uint32_t>(e0 >> 2);
+      const float4 mu = normal_quad(s.seed, kStreamMean, static_cast<uint64_t>(cls), m);
+      const float4 nz = normal_quad(s.seed, kStreamNoise, static_cast<uint64_t>(i), m);
+      const float v[4] = {sep * mu.x + nz.x, sep * mu.y + nz.y, sep * mu.z + nz.z, sep * mu.w + nz.w};
       float* row = x + r * D;
-      row[e0] = sep * mu.x + nz.x;
-      if (e0 + 1 < D) row[e0 + 1] = sep * mu.y + nz.y;
+      for (int j = 0; j < 4 && e0 + j < D; ++j) row[e0 + j] = v[j];
     }
     if (chunk == 0)
       for (int c = threadIdx.x; c < s.num_classes; c += blockDim.x)
@@ -152,7 +160,7 @@ void datagen_launch(const hp_dataset_spec& s, int64_t first, int64_t count, floa
                 ") outside [0, " + std::to_string(s.num_examples) + ")");
   if (count == 0) return;
   const int64_t D = static_cast<int64_t>(s.channels) * s.height * s.width;
-  const int64_t units = count * ((D + 511) / 512);
+  const int64_t units = count * ((D + 1023) / 1024);
   const int blocks = static_cast<int>(std::min<int64_t>(units, 148LL * 8));
   datagen_kernel<<<blocks, 256, 0, st>>>(s, perm_key(s), first, count, x, t);
   HP_CUDA(cudaGetLastError());

@@ -1,7 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_data_gen.py tests/test_cli.py tests/test_abi.py -x -q -m gpu > gpurun_out/dg.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/dg.log
-for i in 1 2 3; do for d in build_old/tests/dev tests/dev; do LABEL=$d timeout 300 python $d/gemm_times.py 2>&1 | head -1; done; done > gpurun_out/ab3.log
-cat gpurun_out/ab3.log
+nvidia-smi --query-gpu=clocks.sm,clocks.mem,clocks.max.sm,power.draw,temperature.gpu --format=csv
+timeout 900 python -m pytest tests/test_data_gen.py tests/test_cli.py tests/test_abi.py -x -q -m gpu > gpurun_out/dg.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/dg.log
 python - <<'PY'
 import time, torch, sys
 sys.path.insert(0, '.')
@@ -15,3 +14,5 @@ for i in range(10): D.generate(s, 128 * (i % 10), 128)
 e1.record(); torch.cuda.synchronize()
 print(f"datagen AlexNet batch (128 x 3x224x224): {e0.elapsed_time(e1) / 10 * 1e3:.1f} us")
 PY
+LABEL=clk timeout 300 python tests/dev/gemm_times.py | head -1
+nvidia-smi --query-gpu=clocks.sm,clocks.mem,clocks.max.sm,power.draw,temperature.gpu --format=csv
