@@ -1293,10 +1293,16 @@ void ClusterImpl<TA>::rotate_all(Worker<TA>& w) {
                              c.Cz, st_, c.pairs ? w.cp + conv_b_off(static_cast<int>(l)) : nullptr, w.bias2);
       ++launches_;
     }
-    if (!c.impl_dgrad) continue;
-    launch_rotate_weights<TA>(w.cp + conv_k_off(static_cast<int>(l)), c.ldk, w.wrot[l], c.F, c.C, c.R,
-                              c.S, st_);
-    ++launches_;
+  }
+  // the dgrad operands of every implicit-dgrad layer, one launch
+  std::vector<RotateTensor> rt;
+  for (size_t l = 0; l < g_.cg.size(); ++l) {
+    const ConvGeom& c = g_.cg[l];
+    if (c.impl_dgrad) rt.push_back({w.cp + conv_k_off(static_cast<int>(l)), c.ldk, w.wrot[l], c.F, c.C, c.R, c.S});
+  }
+  if (!rt.empty()) {
+    launch_rotate_weights_multi<TA>(rt.data(), static_cast<int>(rt.size()), st_);
+    launches_ += (static_cast<int64_t>(rt.size()) + 7) / 8;
   }
 }
 

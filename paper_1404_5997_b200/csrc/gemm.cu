@@ -751,8 +751,12 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * SB;
           uint8_t* sb = sa + A_BYTES;
-          mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
-          if (args.ca.enabled && args.a_mn && args.ca.shift) {
+          // dev (dbg 32 / 64): skip the B / A loads of odd k-tiles (results garbage) -- is the
+          // mainloop bound by operand delivery?
+          const bool skip_b = (args.dbg & 32) && (kt & 1), skip_a = (args.dbg & 64) && (kt & 1);
+          mbar_arrive_expect_tx(&full[stage], (skip_a ? 0u : A_BYTES) + (skip_b ? 0u : B_BYTES));
+          if (skip_a) {
+          } else if (args.ca.enabled && args.a_mn && args.ca.shift) {
             load_mn_shift<false, BK, ATOM>(sa, &ta, &full[stage], args.ca, ti.m0, kBM, kt);
           } else if (args.ca.enabled && args.a_mn) {  // wgrad with im2col(x)^T as A: K = pixels
             load_b_im2col<false, BK, ATOM>(sa, &ta, &full[stage], args.ca, ti.m0, kBM, kt);
@@ -761,7 +765,8 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
           } else {
             load_tile_t<false, BK, ATOM>(sa, &ta, &full[stage], args.a_mn, ti.m0, kBM, kt * BK);
           }
-          if (args.cb.enabled && args.cb.shift) {
+          if (skip_b) {
+          } else if (args.cb.enabled && args.cb.shift) {
             load_mn_shift<false, BK, ATOM>(sb, &tb, &full[stage], args.cb, ti.n0, BN, kt);
           } else if (args.cb.enabled) {
             load_b_im2col<false, BK, ATOM>(sb, &tb, &full[stage], args.cb, ti.n0, BN, kt);

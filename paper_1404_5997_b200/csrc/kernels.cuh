@@ -161,6 +161,15 @@ void launch_maxpool_bwd_w(const float* gy, const uint8_t* widx, TO* gx, const TM
 template <class T>
 void launch_rotate_weights(const float* w, long long ldk, T* wrot, int F, int C, int R, int S,
                            cudaStream_t st);
+// The same for up to 8 layers in one launch (the step's post-update rotations).
+struct RotateTensor {
+  const float* w;
+  long long ldk;
+  void* wrot;
+  int F, C, R, S;
+};
+template <class T>
+void launch_rotate_weights_multi(const RotateTensor* ts, int n, cudaStream_t st);
 
 // Space-to-depth for a strided first layer (AlexNet conv1, stride s): the
 // stride-s RxS conv over the NCHW fp32 batch equals a stride-1 Rq x Rq conv

@@ -6,6 +6,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import torch
 import paper_1404_5997_b200 as hp
 
+if os.environ.get("HP_DEV_GEMM_DBG"):
+    from paper_1404_5997_b200._lib import lib as _l
+    _l.hp_debug_gemm_flags(int(os.environ["HP_DEV_GEMM_DBG"]))
 spec = hp.alexnet_1col()
 c = hp.Cluster(spec, hp.ClusterConfig(workers=1, per_worker_batch=128, scheme=hp.Scheme.B, seed=1,
                                       math_mode=hp.MathMode.BF16))
