@@ -891,7 +891,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     float* ws = real != nullptr ? real : reinterpret_cast<float*>(256);
     GemmPlan pl = gemm_plan(math_, a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e, 0,
                             ws, bn, cta2);
-    if (pl.splits > 1) need = std::max(need, static_cast<size_t>(pl.splits * M * N));
+    if (pl.args.raw_partial) need = std::max(need, static_cast<size_t>(pl.splits * M * N));
     else pl.args.ws = real;
     return pl;
   };
@@ -996,6 +996,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     // 0.067 vs 0.071, conv4 (F=384) 0.114 vs 0.120 faster unswapped.
     auto mfill = [](long long m) { return static_cast<double>(m) / (((m + 255) / 256) * 256); };
     const long long Kw = c.s2d ? Kz : c.Kc;
+    static const bool no_halo = getenv("HP_DEV_NO_HALO") != nullptr;  // dev: per-tap shifted B boxes
     const bool swap = (c.impl_fwd || c.s2d) && !c.pairs && c.F >= 128 && c.F <= 256 && mfill(Kw) > mfill(c.F) + 0.1;
     if (c.s2d) {
       eg.c = w.dwz;
@@ -1008,6 +1009,12 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       w.conv_wgrad.push_back(plan(xb, op(w.dz[l], 1, c.F), Kw, c.F, c.s2d ? c.P : c.Pq, eg, 1));
     } else if (c.s2d) {
       w.conv_wgrad.push_back(plan(op(w.dz[l], 1, zn), xb, zn, Kz, zrows, eg, 1));
+    } else if (c.in_q && xb.conv.shift && bf && c.S * 64 <= 256 && c.C % 64 == 0 && !no_halo) {
+      // halo B (Im2col::halo): N tiles of S*64 columns = the S taps of one kernel
+      // row of one channel block, read as one x box per k-tile
+      xb.conv.halo = 1;
+      eg.cols = ColMap{1, c.S, c.C};
+      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, c.Kc, c.Pq, eg, 1, 64 * c.S, 0));
     } else {
       w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, c.Kc, c.Pq, eg, 1));
     }
@@ -1156,7 +1163,7 @@ void ClusterImpl<TA>::gemm(const GemmPlan& p, const char* tag, int layer, cudaSt
     gemm_launch(p, st);
     tl_mark(tag, layer, true, st);
   }
-  launches_ += p.splits > 1 ? 2 : 1;
+  launches_ += p.args.raw_partial ? 2 : 1;
   gemm_flops_ += flops;
 }
 
@@ -1379,41 +1386,46 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta, int slot) {
                     fl.relu ? 1 : 0, xblocks_, st_);
     ++launches_;
   }
-  for (int li = nf - 1; li >= 0; --li) {
+  // FC weight gradients (and the fused update) feed nothing downstream in this
+  // step: they run on sf_ (serialised when profiling). dgrad_first: every
+  // layer's dgrad (the critical chain to the conv backward) is enqueued before
+  // any FC wgrad, so the update's CTAs do not sit between the dgrads; all
+  // weight reads of the turn then precede every fused update (turn j's dX uses
+  // pre-update weights, cluster.cpp:562-601).
+  cudaStream_t fs = profile ? st_ : sf_;
+  static const bool interleave = getenv("HP_DEV_FC_INTERLEAVE") != nullptr;  // dev: dgrad/wgrad per layer
+  auto wgrad = [&](int li, Worker<TA>& w) {
     const FcGeom& f = g_.fg[li];
+    const int rows = static_cast<int>(f.c1[sid(w.gid)] - f.c0[sid(w.gid)]);
+    GemmPlan pw = li == 0 && slot == 1 ? w.fc0_slot1[1] : w.fc_wgrad[li];
+    pw.args.epi.beta = beta ? 1 : 0;
+    if (fuse_sgd_) {
+      // last (or, in variable mode, every) turn: the weight update runs in
+      // the wgrad epilogue; the gradient is never stored
+      Epi& e = pw.args.epi;
+      e.sgd_w = w.fp + fc_w_off(li);
+      e.sgd_m = w.fm + fc_w_off(li);
+      e.sgd_copy = kTA == kBF16 ? static_cast<void*>(w.fpt + fc_w_off(li)) : nullptr;
+      e.sgd_mu = static_cast<float>(sgd_hp_.momentum);
+      e.sgd_s1 = static_cast<float>(-sgd_lr_);
+      e.sgd_s2 = static_cast<float>(-sgd_lr_ * sgd_hp_.weight_decay);
+      e.sgd_gscale = sgd_gscale_;
+      e.sgd_has_gscale = sgd_has_gscale_ ? 1 : 0;
+    }
+    gemm(pw, "fc_wgrad", li, fs);
+    launch_rowsum<TA>(w.fdz[li], rows, static_cast<int>(n_), ldn_, w.fgr + fc_b_off(li), beta ? 1 : 0, fs);
+    ++launches_;
+  };
+  for (int li = nf - 1; li >= 0; --li) {
     for (auto& w : w_) {
-      const int rows = static_cast<int>(f.c1[sid(w.gid)] - f.c0[sid(w.gid)]);
-      GemmPlan pw = li == 0 && slot == 1 ? w.fc0_slot1[1] : w.fc_wgrad[li];
-      pw.args.epi.beta = beta ? 1 : 0;
-      if (fuse_sgd_) {
-        // last (or, in variable mode, every) turn: the weight update runs in
-        // the wgrad epilogue; the gradient is never stored
-        Epi& e = pw.args.epi;
-        e.sgd_w = w.fp + fc_w_off(li);
-        e.sgd_m = w.fm + fc_w_off(li);
-        e.sgd_copy = kTA == kBF16 ? static_cast<void*>(w.fpt + fc_w_off(li)) : nullptr;
-        e.sgd_mu = static_cast<float>(sgd_hp_.momentum);
-        e.sgd_s1 = static_cast<float>(-sgd_lr_);
-        e.sgd_s2 = static_cast<float>(-sgd_lr_ * sgd_hp_.weight_decay);
-        e.sgd_gscale = sgd_gscale_;
-        e.sgd_has_gscale = sgd_has_gscale_ ? 1 : 0;
-        if (pw.splits > 1) pw.args.epi = e;
-      }
-      // dgrad first: it must read this layer's weights before the (fused)
-      // update of the wgrad epilogue -- turn j's dX uses pre-update weights
-      // (cluster.cpp:562-601)
       gemm(li == 0 && slot == 1 ? w.fc0_slot1[2] : w.fc_dgrad[li], "fc_dgrad", li);
-      // The weight gradient (and the fused update) feeds nothing downstream in
-      // this step: it runs on sf_, overlapping the rest of the backward
-      // (serialised when profiling).
-      cudaStream_t fs = profile ? st_ : sf_;
-      if (fs != st_) {
-        HP_CUDA(cudaEventRecord(ev_fcd_, st_));
-        HP_CUDA(cudaStreamWaitEvent(fs, ev_fcd_, 0));
+      if (interleave) {
+        if (fs != st_) {
+          HP_CUDA(cudaEventRecord(ev_fcd_, st_));
+          HP_CUDA(cudaStreamWaitEvent(fs, ev_fcd_, 0));
+        }
+        wgrad(li, w);
       }
-      gemm(pw, "fc_wgrad", li, fs);
-      launch_rowsum<TA>(w.fdz[li], rows, static_cast<int>(n_), ldn_, w.fgr + fc_b_off(li), beta ? 1 : 0, fs);
-      ++launches_;
     }
     if (li > 0 && fcK_ > 1) {
       std::vector<const float*> send(nl);
@@ -1425,6 +1437,14 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta, int slot) {
       comm_->reduce_scatter(send, recv, g_.fg[li - 1].cmax * ldn_, kTA, 1.f, st_);
       launches_ += nl;
     }
+  }
+  if (!interleave) {
+    if (fs != st_) {
+      HP_CUDA(cudaEventRecord(ev_fcd_, st_));
+      HP_CUDA(cudaStreamWaitEvent(fs, ev_fcd_, 0));
+    }
+    for (int li = nf - 1; li >= 0; --li)
+      for (auto& w : w_) wgrad(li, w);
   }
   HP_CUDA(cudaEventRecord(ev_fcw_, profile ? st_ : sf_));
   HP_CUDA(cudaEventRecord(ev_fd0_, st_));

@@ -60,6 +60,15 @@ __device__ __forceinline__ float sgd_apply(const Epi& e, long long off, float g)
   return nw;
 }
 
+// Output column of GEMM column n under e.cols (Im2col::halo order).
+__device__ __forceinline__ int map_col(const ColMap& c, int n) {
+  if (!c.enabled) return n;
+  const int blk = n >> 6, c_lo = n & 63;
+  const int s = blk % c.S, rcb = blk / c.S;
+  const int cbs = c.C >> 6, r = rcb / cbs, cb = rcb - r * cbs;
+  return (r * c.S + s) * c.C + cb * 64 + c_lo;
+}
+
 // Output row of GEMM row m under e.rows (-1: not stored).
 __device__ __forceinline__ int map_row(const RowMap& r, int m) {
   if (!r.enabled) return m;
@@ -72,6 +81,7 @@ __device__ __forceinline__ int map_row(const RowMap& r, int m) {
 
 __device__ __forceinline__ void epi_elem(const Epi& e, int m, int n, float v) {
   const int gm = m;  // GEMM row (per-row bias)
+  n = map_col(e.cols, n);
   if (e.rows.enabled) {
     m = map_row(e.rows, m);
     if (m < 0) return;
@@ -754,7 +764,8 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
           // dev (dbg 32 / 64): skip the B / A loads of odd k-tiles (results garbage) -- is the
           // mainloop bound by operand delivery?
           const bool skip_b = (args.dbg & 32) && (kt & 1), skip_a = (args.dbg & 64) && (kt & 1);
-          mbar_arrive_expect_tx(&full[stage], (skip_a ? 0u : A_BYTES) + (skip_b ? 0u : B_BYTES));
+          const uint32_t b_bytes = args.cb.halo ? static_cast<uint32_t>(args.cb.halo_rows) * 128u : B_BYTES;
+          mbar_arrive_expect_tx(&full[stage], (skip_a ? 0u : A_BYTES) + (skip_b ? 0u : b_bytes));
           if (skip_a) {
           } else if (args.ca.enabled && args.a_mn && args.ca.shift) {
             load_mn_shift<false, BK, ATOM>(sa, &ta, &full[stage], args.ca, ti.m0, kBM, kt);
@@ -766,6 +777,11 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
             load_tile_t<false, BK, ATOM>(sa, &ta, &full[stage], args.a_mn, ti.m0, kBM, kt * BK);
           }
           if (skip_b) {
+          } else if (args.cb.enabled && args.cb.halo) {
+            // one box: rows kt*BK + r*wq + base_off .. + halo_rows of channel block cb
+            const int grp = ti.n0 / BN;  // = r * (C / 64) + cb (BN = S * 64)
+            const int cbs = args.cb.C / ATOM, r = grp / cbs, cb = grp - r * cbs;
+            tma2d<false>(sb, &tb, &full[stage], cb * ATOM, kt * BK + r * args.cb.wq + args.cb.base_off);
           } else if (args.cb.enabled && args.cb.shift) {
             load_mn_shift<false, BK, ATOM>(sb, &tb, &full[stage], args.cb, ti.n0, BN, kt);
           } else if (args.cb.enabled) {
@@ -790,7 +806,8 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
                              (static_cast<uint32_t>(BN >> 3) << 17) |
                              (static_cast<uint32_t>(kBM >> 4) << 24);
       const uint32_t a_lbo = args.a_mn ? BK * 128 : 16;
-      const uint32_t b_lbo = args.b_mn ? BK * 128 : 16;
+      // (halo B: the S atoms of the tile are one row apart in the same box)
+      const uint32_t b_lbo = args.cb.halo ? 128u : args.b_mn ? BK * 128 : 16;
       // MN-major 32-bit operands use the 32B-granule 128B swizzle: 4-row
       // swizzle groups (SBO 512) instead of 8-row groups (SBO 1024).
       const uint32_t a_sbo = (ES == 4 && args.a_mn) ? 512 : 1024;
@@ -1356,6 +1373,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 // One fp32 4-vector (m, n..n+3) through the epilogue (vectorised epi_elem).
 __device__ __forceinline__ void epi_vec4(const Epi& e, int m, int n, float4 x) {
   const int gm = m;  // GEMM row (per-row bias)
+  n = map_col(e.cols, n);  // (4-column groups never straddle a 64-column block)
   m = map_row(e.rows, m);
   if (m < 0) return;
   const long long off = static_cast<long long>(m) * e.ldc + n;
@@ -1552,6 +1570,8 @@ ConvArgs conv_args(const Im2col& g) {
   c.OW = g.OW;
   c.stride = g.stride;
   c.stride_h = g.stride_h > 0 ? g.stride_h : g.stride;
+  c.halo = g.halo;
+  c.halo_rows = g.halo ? (64 + g.S - 1 + 7) / 8 * 8 : 0;
   c.lo_w = g.corners ? g.lo : -g.pad;
   c.lo_h = g.corners ? g.lo : -g.pad;
   c.shift = g.shift;
@@ -1804,11 +1824,12 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   p.args.k_tiles_per_split = kps;
   p.args.a_mn = a.mn_major;
   p.args.b_mn = b.mn_major;
-  p.args.raw_partial = splits > 1 ? 1 : 0;
+  // (halo B: the GEMM writes raw partials and epi_apply applies the column map)
+  p.args.raw_partial = splits > 1 || (b.conv.enabled && b.conv.halo) ? 1 : 0;
   p.args.dbg = g_dbg_flags;
   p.args.ws = ws;
   p.args.epi = epi;
-  if (splits > 1 && ws == nullptr) throw std::runtime_error("gemm: split-K needs a workspace");
+  if (p.args.raw_partial && ws == nullptr) throw std::runtime_error("gemm: split-K needs a workspace");
   const int b_rows = use2 ? p.bn / 2 : p.bn;
   if (a.conv.enabled) {
     // K-major: rows = output pixels (fprop / dgrad); MN-major: K = output
@@ -1823,7 +1844,12 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   } else {
     p.ta = operand_map(a, a.ptr, es, M, K, kBM);
   }
-  if (b.conv.enabled && b.conv.shift) {
+  if (b.conv.enabled && b.conv.halo) {
+    if (!b.mn_major || !b.conv.shift || use2 || p.bn != 64 * b.conv.S || b.conv.C % 64 != 0 || es != 2)
+      throw std::runtime_error("gemm: halo B needs a bf16 MN-major shift operand, 1-CTA tiles of S*64 columns");
+    p.tb = make_map(b.ptr, es, b.conv.C, static_cast<long long>(b.conv.N) * b.conv.H * b.conv.W, b.conv.C, 64,
+                    (64 + b.conv.S - 1 + 7) / 8 * 8, CU_TENSOR_MAP_SWIZZLE_128B);
+  } else if (b.conv.enabled && b.conv.shift) {
     if (!b.mn_major) throw std::runtime_error("gemm: shift-mode B must be MN-major");
     p.tb = make_map(b.ptr, es, b.conv.C, static_cast<long long>(b.conv.N) * b.conv.H * b.conv.W, b.conv.C, 128 / es,
                     BK, es == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B);
@@ -1941,7 +1967,7 @@ void gemm_launch(const GemmPlan& p, cudaStream_t s) {
     case kMathF32x3: launch_math<kMathF32x3>(p, s); break;
     default: throw std::runtime_error("gemm: bad math mode");
   }
-  if (p.splits > 1) epi_apply_launch(p.args.ws, p.splits, p.args.M, p.args.N, p.args.epi, s);
+  if (p.args.raw_partial) epi_apply_launch(p.args.ws, p.splits, p.args.M, p.args.N, p.args.epi, s);
 }
 
 }  // namespace hp

@@ -37,6 +37,14 @@ struct RowMap {
   int sH = 0, sW = 0, vH = 0, vW = 0, dH = 0, dW = 0, dp = 0;
 };
 
+// Epilogue column permutation (the halo wgrad's N order, see Im2col::halo):
+// GEMM column n = ((r * (C/64) + cb) * S + s) * 64 + c_lo is output column
+// k = (r * S + s) * C + cb * 64 + c_lo. Applied by epi_apply (split-K reduce).
+struct ColMap {
+  int enabled = 0;
+  int S = 0, C = 0;
+};
+
 struct Epi {
   void* c = nullptr;  // output
   long long ldc = 0;
@@ -62,6 +70,7 @@ struct Epi {
   float sgd_mu = 0.f, sgd_s1 = 0.f, sgd_s2 = 0.f, sgd_gscale = 1.f;
   int sgd_has_gscale = 0;
   RowMap rows;  // rows.enabled: remap output (and mask) rows; not with c_trans / sgd
+  ColMap cols;  // cols.enabled: remap output columns (epi_apply only; the GEMM writes raw partials)
 };
 
 // Implicit-GEMM convolution operand: the matrix is the im2col view of an NHWC
@@ -90,7 +99,17 @@ struct Im2col {
   // s2d conv1 pixel-pair GEMM walks W with stride 2 (one row per output pixel
   // pair) and H with stride 1.
   int stride_h = 0;
+  // halo = 1 (with shift, MN-major B of a stride-1 wgrad, S*64 <= 256): the
+  // GEMM's N index is permuted to n = ((r * C/64 + cb) * S + s) * 64 + c_lo so
+  // that an N tile of S*64 columns is the S taps (r, 0..S-1) of one 64-channel
+  // block. Those taps read the same x rows shifted by 0..S-1, so the tile's B
+  // is ONE box of 64 + S - 1 rows (rounded up to 8) and the UMMA descriptor
+  // steps between its S atoms by one row (LBO = 128 B) instead of by a whole
+  // atom: each x line crosses L2 -> SM once per tile, not once per tap.
+  // The output columns come back through Epi::cols (ColMap).
+  int halo = 0;
 };
+
 
 
 struct GemmOperand {
@@ -104,6 +123,7 @@ struct ConvArgs {            // device-side im2col bookkeeping (see Im2col)
   int enabled, C, S, OH, OW, stride, lo_w, lo_h;
   int shift, wq, base_off;   // Im2col::shift mode
   int stride_h;              // vertical stride (Im2col::stride_h, resolved)
+  int halo, halo_rows;       // Im2col::halo: B tile = one box of halo_rows rows
 };
 
 struct GemmArgs {

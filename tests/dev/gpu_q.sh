@@ -1,5 +1,7 @@
 mkdir -p gpurun_out
-for i in 1 2 3; do for d in build_r0/tests/dev tests/dev; do LABEL=$d timeout 300 python $d/gemm_times.py 2>&1 | head -1; done; done > gpurun_out/ab_r0.log
-cat gpurun_out/ab_r0.log
-for f in 0 32 64; do HP_DEV_GEMM_DBG=$f LABEL=dbg$f timeout 300 python tests/dev/gemm_times.py 2>&1 | grep -E "==|wgrad"; done > gpurun_out/skip.log
-cat gpurun_out/skip.log
+HP_DEV_PLANS=1 timeout 300 python tests/dev/one_step.py 1 2>&1 | grep "conv_wgrad" | head -5
+for i in 1 2; do
+  HP_DEV_NO_HALO=1 LABEL=nohalo timeout 300 python tests/dev/gemm_times.py 2>&1 | grep -E "==|conv_wgrad"
+  LABEL=halo timeout 300 python tests/dev/gemm_times.py 2>&1 | grep -E "==|conv_wgrad"
+done
+timeout 900 python -m pytest tests/test_alexnet_parity_gpu.py tests/test_step_gpu.py -x -q -m gpu -k "alexnet or bench" > gpurun_out/pt.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pt.log
