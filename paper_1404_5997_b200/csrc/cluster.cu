@@ -1387,13 +1387,14 @@ void ClusterImpl<TA>::fc_forward_backward(int j, bool beta, int slot) {
     ++launches_;
   }
   // FC weight gradients (and the fused update) feed nothing downstream in this
-  // step: they run on sf_ (serialised when profiling). dgrad_first: every
-  // layer's dgrad (the critical chain to the conv backward) is enqueued before
-  // any FC wgrad, so the update's CTAs do not sit between the dgrads; all
-  // weight reads of the turn then precede every fused update (turn j's dX uses
-  // pre-update weights, cluster.cpp:562-601).
+  // step: they run on sf_ (serialised when profiling), layer li's wgrad forked
+  // after layer li's dgrad -- which must read the weights before the fused
+  // update rewrites them (turn j's dX uses pre-update weights, cluster.cpp:562-601).
+  // (Dev HP_DEV_FC_DGRAD_FIRST: the whole dgrad chain first, then every wgrad;
+  // measured 1.547 -> 1.575 ms/step on one box: the update then lands on the
+  // conv backward instead of between the small FC dgrads.)
   cudaStream_t fs = profile ? st_ : sf_;
-  static const bool interleave = getenv("HP_DEV_FC_INTERLEAVE") != nullptr;  // dev: dgrad/wgrad per layer
+  static const bool interleave = getenv("HP_DEV_FC_DGRAD_FIRST") == nullptr;
   auto wgrad = [&](int li, Worker<TA>& w) {
     const FcGeom& f = g_.fg[li];
     const int rows = static_cast<int>(f.c1[sid(w.gid)] - f.c0[sid(w.gid)]);
