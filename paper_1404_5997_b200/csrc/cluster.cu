@@ -533,7 +533,9 @@ class ClusterImpl final : public ClusterBase {
   size_t ws_floats_ = 0;
   float* ws2_ = nullptr;  // split-K workspace of the conv wgrad GEMMs (side stream sw_)
   size_t ws2_floats_ = 0;
-  cudaStream_t sw_ = nullptr;          // side stream: conv bias/weight gradients (off the dgrad chain)
+  cudaStream_t sw_ = nullptr;          // side stream: conv weight gradients (off the dgrad chain)
+  cudaStream_t sb_ = nullptr;          // side stream: conv bias gradients (off both chains)
+  std::vector<cudaEvent_t> ev_bg_;     // per conv layer: its bias gradient final on sb_
   cudaStream_t sf_ = nullptr;          // side stream: FC weight gradients + fused update (off the backward chain)
   cudaEvent_t ev_fcd_ = nullptr;       // FC dgrad of the current layer done (st_)
   cudaEvent_t ev_fcw_ = nullptr;       // all FC wgrads of the turn done (sf_)
@@ -611,6 +613,7 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   HP_CUDA(cudaEventCreateWithFlags(&ev0_fc_, cudaEventDisableTiming));
   HP_CUDA(cudaStreamCreateWithFlags(&sx_, cudaStreamNonBlocking));
   HP_CUDA(cudaStreamCreateWithFlags(&sw_, cudaStreamNonBlocking));
+  HP_CUDA(cudaStreamCreateWithFlags(&sb_, cudaStreamNonBlocking));
   HP_CUDA(cudaStreamCreateWithFlags(&sf_, cudaStreamNonBlocking));
   HP_CUDA(cudaEventCreateWithFlags(&ev_fcd_, cudaEventDisableTiming));
   HP_CUDA(cudaEventCreateWithFlags(&ev_fcw_, cudaEventDisableTiming));
@@ -767,6 +770,8 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   ev_wg_.resize(g_.cg.size());
   for (auto& e : ev_dz_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : ev_wg_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  ev_bg_.resize(g_.cg.size());
+  for (auto& e : ev_bg_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   HP_CUDA(cudaMallocHost(&host_parts_, sizeof(double) * nl * num_sub_ * xblocks_));
   HP_CUDA(cudaMallocHost(&host_bad_, sizeof(int) * nl));
   // Plans first with a null workspace to size it (for both conv kernel
@@ -817,9 +822,14 @@ ClusterImpl<TA>::~ClusterImpl() {
   for (auto e : ev_layer_) cudaEventDestroy(e);
   for (auto e : ev_dz_) cudaEventDestroy(e);
   for (auto e : ev_wg_) cudaEventDestroy(e);
+  for (auto e : ev_bg_) cudaEventDestroy(e);
   if (sw_) {
     cudaStreamSynchronize(sw_);
     cudaStreamDestroy(sw_);
+  }
+  if (sb_) {
+    cudaStreamSynchronize(sb_);
+    cudaStreamDestroy(sb_);
   }
   if (sf_) {
     cudaStreamSynchronize(sf_);
@@ -1512,19 +1522,23 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
     ++launches_;
   }
   // Weight and bias gradients of this layer only feed the update (and the
-  // all-reduce), not the backward chain: they run on the side stream sw_,
-  // overlapping this layer's dgrad and the layers below (serialised on st_ when
-  // profiling, for clean per-GEMM times).
+  // all-reduce), not the backward chain: the weight gradient runs on the side
+  // stream sw_, the bias gradient on sb_ (so the wgrad chain never waits for a
+  // column sum), both overlapping this layer's dgrad and the layers below
+  // (serialised on st_ when profiling, for clean per-GEMM times).
   cudaStream_t ws = profile ? st_ : sw_;
+  cudaStream_t bs = profile ? st_ : sb_;
   if (ws != st_) {
     HP_CUDA(cudaEventRecord(ev_dz_[l], st_));
     HP_CUDA(cudaStreamWaitEvent(ws, ev_dz_[l], 0));
+    HP_CUDA(cudaStreamWaitEvent(bs, ev_dz_[l], 0));
   }
   // bias grad = channel sums of dz (model.cpp:184-202)
-  tl_mark("colsum", l, false, ws);
-  launch_colsum<TA>(w.dz[l], c.Pq, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, ws);
-  tl_mark("colsum", l, true, ws);
+  tl_mark("colsum", l, false, bs);
+  launch_colsum<TA>(w.dz[l], c.Pq, c.F, c.F, w.cgr + conv_b_off(l), w.colsum_ws, bs);
+  tl_mark("colsum", l, true, bs);
   launches_ += 2;
+  HP_CUDA(cudaEventRecord(ev_bg_[l], bs));
   gemm(w.conv_wgrad[l], "conv_wgrad", l, ws);
   if (c.s2d) {
     launch_s2d_wgrad_gather(w.dwz, w.cgr + conv_k_off(l), c.ldk, c.F, c.C, c.R, c.S, c.stride, c.Rq, c.Cz, ws,
@@ -1532,6 +1546,7 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
     ++launches_;
   }
   if (K_ > 1 && skip_sync_broadcast) {  // keep the local gradients for the negative control
+    HP_CUDA(cudaStreamWaitEvent(ws, ev_bg_[l], 0));
     const long long cnt = static_cast<long long>(c.F) * c.ldk + c.F;
     HP_CUDA(cudaMemcpyAsync(w.cgr_local + conv_k_off(l), w.cgr + conv_k_off(l), cnt * sizeof(float),
                             cudaMemcpyDeviceToDevice, ws));
@@ -1722,8 +1737,10 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
   for (int l = nc - 1; l >= 0; --l) {
     for (int i = 0; i < nl; ++i) conv_backward_layer(w_[i], l, cbs[i]);
     if (K_ > 1) {
-      // ev_wg_[l]: the last local worker's gradients of layer l (sw_ is in order)
+      // ev_wg_[l] / ev_bg_[l]: the last local worker's weight / bias gradients of
+      // layer l (sw_ and sb_ are in order)
       HP_CUDA(cudaStreamWaitEvent(sc_, ev_wg_[l], 0));
+      HP_CUDA(cudaStreamWaitEvent(sc_, ev_bg_[l], 0));
       std::vector<float*> bufs(nl);
       for (int i = 0; i < nl; ++i) bufs[i] = w_[i].cgr + conv_k_off(l);
       const long long cnt = static_cast<long long>(g_.cg[l].F) * g_.cg[l].ldk + g_.cg[l].F;
@@ -1732,6 +1749,7 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
     }
   }
   HP_CUDA(cudaStreamWaitEvent(st_, ev_wg_[0], 0));  // join sw_ (layer 0 is its last work)
+  HP_CUDA(cudaStreamWaitEvent(st_, ev_bg_[0], 0));  // join sb_
   HP_CUDA(cudaStreamWaitEvent(st_, ev_fcw_, 0));    // join sf_
   if (K_ > 1) {
     HP_CUDA(cudaEventRecord(ev_comm_, sc_));
