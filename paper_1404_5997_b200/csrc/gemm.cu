@@ -698,7 +698,13 @@ __device__ __forceinline__ TileIdx tile_idx(const GemmArgs& a, int t, int tiles_
 // 128): 2 stages, one accumulator, two CTAs per SM -- twice the epilogue warps
 // (memory-level parallelism) per SM.
 template <int BN, int MATH, bool LIGHT>
-__global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
+#ifndef HP_LIGHT_CTAS
+#define HP_LIGHT_CTAS 2  // light kernel CTAs per SM
+#endif
+#ifndef HP_LIGHT_STAGES
+#define HP_LIGHT_STAGES 2
+#endif
+__global__ void __launch_bounds__(192, LIGHT ? HP_LIGHT_CTAS : 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                 const GemmArgs args) {
   constexpr bool SPLIT = MATH == kMathF32x3;
@@ -709,7 +715,7 @@ __global__ void __launch_bounds__(192, LIGHT ? 2 : 1)
   constexpr uint32_t A_BYTES = kBM * 128;
   constexpr uint32_t B_BYTES = BN * 128;
   constexpr uint32_t SB = stage_bytes(BN, MATH);
-  constexpr int STAGES = LIGHT ? 2 : num_stages(BN, MATH);
+  constexpr int STAGES = LIGHT ? HP_LIGHT_STAGES : num_stages(BN, MATH);
   constexpr int NACC = (SPLIT || LIGHT) ? 1 : 2;
   constexpr uint32_t ACOLS = tmem_cols(BN);
   constexpr uint32_t TCOLS = ACOLS * NACC;
@@ -1867,8 +1873,8 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
     p.smem = static_cast<size_t>(num_stages2(p.bn)) * stage_bytes2(p.bn) + 1024 + 256 + kEpiSmemBytes;
   } else {
     const int total = cdiv(M, kBM) * cdiv(N, p.bn) * splits;
-    p.grid = dim3(math == kMathF32x3 ? total : std::min(total, p.light ? 296 : 148));
-    p.smem = static_cast<size_t>(p.light ? 2 : num_stages(p.bn, math)) * stage_bytes(p.bn, math) + 1024 + 256 +
+    p.grid = dim3(math == kMathF32x3 ? total : std::min(total, p.light ? 148 * HP_LIGHT_CTAS : 148));
+    p.smem = static_cast<size_t>(p.light ? HP_LIGHT_STAGES : num_stages(p.bn, math)) * stage_bytes(p.bn, math) + 1024 + 256 +
              kEpiSmemBytes;
   }
   p.valid = true;

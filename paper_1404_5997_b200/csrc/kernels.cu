@@ -1631,6 +1631,18 @@ __global__ void __launch_bounds__(256) rotate_multi_kernel(const RotateBatch b) 
   }
   __syncthreads();
   T* wr = static_cast<T*>(r.wrot);
+  if (r.C % 32 == 0) {
+    // the tile's 32 k share one tap (r, s): the index math once per thread
+    const int rs = k0 / r.C, cbase = k0 - rs * r.C;
+    const int rr = rs / r.S, sx = rs - rr * r.S;
+    const long long tap = static_cast<long long>(r.R - 1 - rr) * r.S + (r.S - 1 - sx);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = cbase + ty + 8 * j, f = f0 + tx;
+      if (f < r.F) wr[(static_cast<long long>(c) * r.R * r.S + tap) * r.F + f] = from_f<T>(tile[tx][ty + 8 * j]);
+    }
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int k = k0 + ty + 8 * j, f = f0 + tx;
