@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -891,7 +892,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     return o;
   };
   auto plan = [&](const GemmOperand& a, const GemmOperand& b, long long M, long long N, long long K,
-                  const Epi& e, int side = 0, int bn = 0, int cta2 = -1) {
+                  const Epi& e, int side = 0, int bn = 0, int cta2 = -1, const TapPairs* tp = nullptr) {
     // The plan picks its own tile and split-K; the first (sizing) pass runs
     // against a placeholder workspace and records the largest need. Side-stream
     // (wgrad) plans get their own workspace: they run concurrently with the
@@ -900,7 +901,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     size_t& need = side == 1 ? ws2_floats_ : side == 2 ? ws3_floats_ : ws_floats_;
     float* ws = real != nullptr ? real : reinterpret_cast<float*>(256);
     GemmPlan pl = gemm_plan(math_, a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e, 0,
-                            ws, bn, cta2);
+                            ws, bn, cta2, tp);
     if (pl.args.raw_partial) need = std::max(need, static_cast<size_t>(pl.splits * M * N));
     else pl.args.ws = real;
     return pl;
@@ -1014,7 +1015,40 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       xb = op(w.z, 1, 0);
       xb.conv = zview;
     }
-    if (swap) {
+    // tap pairs (TapPairs, gemm.cuh) for the swapped stride-1 wgrad: neighbouring
+    // taps of a kernel row share one x box (d = 1); an odd row's last taps pair
+    // across rows (d = wq); a leftover tap rides alone
+    TapPairs tpairs;
+    if (swap && c.in_q && xb.conv.shift && bf && c.C % 64 == 0 && !no_halo) {
+      std::vector<std::array<int, 3>> tiles;  // {tap0, tap1 (-1: none), channel block}
+      for (int cbk = 0; cbk < c.C / 64; ++cbk) {
+        std::vector<int> left;
+        for (int r = 0; r < c.R; ++r) {
+          int sx = 0;
+          for (; sx + 1 < c.S; sx += 2) tiles.push_back({r * c.S + sx, r * c.S + sx + 1, cbk});
+          if (sx < c.S) left.push_back(r * c.S + sx);
+        }
+        for (size_t i = 0; i < left.size(); i += 2)
+          tiles.push_back({left[i], i + 1 < left.size() ? left[i + 1] : -1, cbk});
+      }
+      if (tiles.size() <= 16) {
+        auto shift_of = [&](int tap) { return (tap / c.S) * c.Wq + tap % c.S; };
+        tpairs.n = static_cast<int>(tiles.size());
+        eg.rblk.enabled = 1;
+        for (int t = 0; t < tpairs.n; ++t) {
+          const auto& tl = tiles[static_cast<size_t>(t)];
+          tpairs.off[t] = shift_of(tl[0]);
+          tpairs.d[t] = tl[1] >= 0 ? shift_of(tl[1]) - shift_of(tl[0]) : 1;
+          tpairs.cb[t] = tl[2];
+          eg.rblk.blk[2 * t] = tl[0] * c.C + tl[2] * 64;
+          eg.rblk.blk[2 * t + 1] = tl[1] >= 0 ? tl[1] * c.C + tl[2] * 64 : -1;
+        }
+      }
+    }
+    if (swap && tpairs.n > 0) {
+      eg.c_trans = 1;  // element (m = k, n = f) -> dW[f][k], rows through eg.rblk
+      w.conv_wgrad.push_back(plan(xb, op(w.dz[l], 1, c.F), 128LL * tpairs.n, c.F, c.Pq, eg, 1, 0, 0, &tpairs));
+    } else if (swap) {
       eg.c_trans = 1;  // element (m = k, n = f) -> dW[f][k]
       w.conv_wgrad.push_back(plan(xb, op(w.dz[l], 1, c.F), Kw, c.F, c.s2d ? c.P : c.Pq, eg, 1));
     } else if (c.s2d) {

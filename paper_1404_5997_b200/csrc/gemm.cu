@@ -82,6 +82,11 @@ __device__ __forceinline__ int map_row(const RowMap& r, int m) {
 __device__ __forceinline__ void epi_elem(const Epi& e, int m, int n, float v) {
   const int gm = m;  // GEMM row (per-row bias)
   n = map_col(e.cols, n);
+  if (e.rblk.enabled) {
+    const int b0 = e.rblk.blk[m >> 6];
+    if (b0 < 0) return;
+    m = b0 + (m & 63);
+  }
   if (e.rows.enabled) {
     m = map_row(e.rows, m);
     if (m < 0) return;
@@ -771,8 +776,12 @@ __global__ void __launch_bounds__(192, LIGHT ? HP_LIGHT_CTAS : 1)
           // mainloop bound by operand delivery?
           const bool skip_b = (args.dbg & 32) && (kt & 1), skip_a = (args.dbg & 64) && (kt & 1);
           const uint32_t b_bytes = args.cb.halo ? static_cast<uint32_t>(args.cb.halo_rows) * 128u : B_BYTES;
-          mbar_arrive_expect_tx(&full[stage], (skip_a ? 0u : A_BYTES) + (skip_b ? 0u : b_bytes));
+          const uint32_t a_bytes = args.tp.n > 0 ? static_cast<uint32_t>(args.tp_rows) * 128u : A_BYTES;
+          mbar_arrive_expect_tx(&full[stage], (skip_a ? 0u : a_bytes) + (skip_b ? 0u : b_bytes));
           if (skip_a) {
+          } else if (args.tp.n > 0) {  // tap-pair A: one box, both atoms (TapPairs)
+            const int mt = ti.m0 / kBM;
+            tma2d<false>(sa, &ta, &full[stage], args.tp.cb[mt] * ATOM, kt * BK + args.tp.off[mt] + args.ca.base_off);
           } else if (args.ca.enabled && args.a_mn && args.ca.shift) {
             load_mn_shift<false, BK, ATOM>(sa, &ta, &full[stage], args.ca, ti.m0, kBM, kt);
           } else if (args.ca.enabled && args.a_mn) {  // wgrad with im2col(x)^T as A: K = pixels
@@ -811,7 +820,7 @@ __global__ void __launch_bounds__(192, LIGHT ? HP_LIGHT_CTAS : 1)
                              (static_cast<uint32_t>(args.b_mn) << 16) |
                              (static_cast<uint32_t>(BN >> 3) << 17) |
                              (static_cast<uint32_t>(kBM >> 4) << 24);
-      const uint32_t a_lbo = args.a_mn ? BK * 128 : 16;
+      const uint32_t a_lbo0 = args.a_mn ? BK * 128 : 16;
       // (halo B: the S atoms of the tile are one row apart in the same box)
       const uint32_t b_lbo = args.cb.halo ? 128u : args.b_mn ? BK * 128 : 16;
       // MN-major 32-bit operands use the 32B-granule 128B swizzle: 4-row
@@ -827,6 +836,8 @@ __global__ void __launch_bounds__(192, LIGHT ? HP_LIGHT_CTAS : 1)
       int local = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
         const TileIdx ti = tile_idx<BN>(args, t, tiles_m, tiles_n);
+        // tap-pair A: the tile's two atoms are d rows apart in one box
+        const uint32_t a_lbo = args.tp.n > 0 ? static_cast<uint32_t>(args.tp.d[ti.m0 / kBM]) * 128u : a_lbo0;
         const int buf = NACC == 2 ? (local & 1) : 0;
         const uint32_t use = NACC == 2 ? static_cast<uint32_t>(local >> 1) : static_cast<uint32_t>(local);
         mbar_wait(&tempty[buf], (use & 1) ^ 1);  // epilogue drained this accumulator
@@ -1784,7 +1795,7 @@ static TileChoice choose_tile(int math, const GemmOperand& b, int M, int N) {
 static bool light_ok(int math, int kt, int splits) { return math != kMathF32x3 && kt <= 4 && splits == 1; }
 
 GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
-                   const Epi& epi, int splits, float* ws, int bn, int cta2) {
+                   const Epi& epi, int splits, float* ws, int bn, int cta2, const TapPairs* tp) {
   if (M <= 0 || N <= 0 || K <= 0) throw std::runtime_error("gemm: empty problem");
   GemmPlan p;
   p.math = math;
@@ -1830,14 +1841,23 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
   p.args.k_tiles_per_split = kps;
   p.args.a_mn = a.mn_major;
   p.args.b_mn = b.mn_major;
-  // (halo B: the GEMM writes raw partials and epi_apply applies the column map)
-  p.args.raw_partial = splits > 1 || (b.conv.enabled && b.conv.halo) ? 1 : 0;
+  // (halo B / tap-pair A: the GEMM writes raw partials and epi_apply applies the maps)
+  p.args.raw_partial = splits > 1 || (b.conv.enabled && b.conv.halo) || tp ? 1 : 0;
   p.args.dbg = g_dbg_flags;
   p.args.ws = ws;
   p.args.epi = epi;
   if (p.args.raw_partial && ws == nullptr) throw std::runtime_error("gemm: split-K needs a workspace");
   const int b_rows = use2 ? p.bn / 2 : p.bn;
-  if (a.conv.enabled) {
+  if (tp) {
+    if (!a.conv.enabled || !a.conv.shift || !a.mn_major || use2 || es != 2 || tp->n * kBM != M || tp->n > 16)
+      throw std::runtime_error("gemm: tap-pair A needs a bf16 MN-major shift operand on 1-CTA tiles");
+    int dmax = 1;
+    for (int i = 0; i < tp->n; ++i) dmax = std::max(dmax, tp->d[i]);
+    p.args.tp = *tp;
+    p.args.tp_rows = (64 + dmax + 7) / 8 * 8;
+    p.ta = make_map(a.ptr, es, a.conv.C, static_cast<long long>(a.conv.N) * a.conv.H * a.conv.W, a.conv.C, 64,
+                    p.args.tp_rows, CU_TENSOR_MAP_SWIZZLE_128B);
+  } else if (a.conv.enabled) {
     // K-major: rows = output pixels (fprop / dgrad); MN-major: K = output
     // pixels, M = (tap, channel) (wgrad as im2col(x)^T . dY)
     if (a.conv.shift) {

@@ -45,6 +45,14 @@ struct ColMap {
   int S = 0, C = 0;
 };
 
+// Epilogue row-block map for transposed (c_trans) outputs: GEMM row m is
+// output row blk[m / 64] + m % 64 (blk < 0: dropped). The tap-pair wgrad's
+// M order (see TapPairs); applied by epi_apply.
+struct RowBlk {
+  int enabled = 0;
+  int blk[32] = {};
+};
+
 struct Epi {
   void* c = nullptr;  // output
   long long ldc = 0;
@@ -71,6 +79,19 @@ struct Epi {
   int sgd_has_gscale = 0;
   RowMap rows;  // rows.enabled: remap output (and mask) rows; not with c_trans / sgd
   ColMap cols;  // cols.enabled: remap output columns (epi_apply only; the GEMM writes raw partials)
+  RowBlk rblk;  // rblk.enabled: remap output rows by 64-row blocks (c_trans, epi_apply only)
+};
+
+// Tap-pair A operand (the swapped stride-1 wgrad, M = (tap, channel)): M tile t
+// is two 64-channel atoms -- taps t0, t1 of channel block cb -- whose x rows
+// differ by a fixed shift d (two neighbouring taps of a kernel row: d = 1; the
+// leftover last taps of two kernel rows: d = wq). Both atoms come from ONE TMA
+// box of 64 + d rows and the UMMA descriptor steps between them by d rows
+// (LBO = d * 128 B), halving the A bytes of the per-tap boxes. A tile with a
+// single tap uses d = 1 and a dropped second atom.
+struct TapPairs {
+  int n = 0;                 // M tiles
+  int off[16] = {}, d[16] = {}, cb[16] = {};  // first atom's row shift, atom spacing (rows), channel block
 };
 
 // Implicit-GEMM convolution operand: the matrix is the im2col view of an NHWC
@@ -139,6 +160,8 @@ struct GemmArgs {
   // channels per tap (64-channel blocks), halo rows per CTA, base-offset mode
   int sh_R, sh_S, sh_wq, sh_C, sh_halo, sh_boff;
   int dbg;  // dev flags (gemm_debug_flags): bit 0 = skip the epilogue's global traffic
+  TapPairs tp;  // tp.n > 0: tap-pair A (MN-major shift operand, 1-CTA kernel)
+  int tp_rows;  // rows of the tap-pair A box
 };
 
 // A fully prepared GEMM launch (tensor maps encoded once, reused every step).
@@ -159,7 +182,8 @@ struct GemmPlan {
 // Builds a plan. `splits` <= 0 picks a split-K factor from the tile count.
 // `ws` must hold splits*M*N floats when splits > 1 (query with gemm_ws_floats).
 GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
-                   const Epi& epi, int splits, float* ws, int bn = 0, int cta2 = -1);
+                   const Epi& epi, int splits, float* ws, int bn = 0, int cta2 = -1,
+                   const TapPairs* tp = nullptr);
 // cta2: -1 auto (pairs for M >= 256 outside 3xTF32), 0 never, 1 force.
 void gemm_set_cta2_default(bool on);
 // Dev hook: force every later auto-configured plan to (cta2, bn); -1/0 = auto.
