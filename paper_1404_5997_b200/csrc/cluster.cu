@@ -118,6 +118,7 @@ Geometry make_geometry(const hp_model_spec* s, int K, long long b) {
     cg.OH = static_cast<int>(oh);
     cg.OW = static_cast<int>(ow);
     cg.OWs = cg.OW;
+    cg.OHs = cg.OH;
     cg.relu = l.relu != 0;
     if (l.lrn_size < 0) config_error(where + ".lrn_size: must be >= 0");
     if (l.lrn_size > 5 && l.pool_kernel > 0)
@@ -651,9 +652,14 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
       // (the pool -- the only consumer -- reads the stored width; LRN-only / no-pool
       // layers keep the plain layout)
       c.pairs = !std::is_same<TA, float>::value && 2 * c.F <= 256 && (2 * c.F) % 64 == 0 && c.pk > 0 && !no_pairs;
-      c.OWs = c.pairs ? (c.OW + 1) / 2 * 2 : c.OW;
       c.Zh = c.OH + c.Rq - 1;
-      c.Zw = c.OWs + c.Rq - 1;  // pairs: pair u reads z columns 2u .. 2u + Rq
+      c.Zw = c.OW + c.Rq - 1;
+      if (c.pairs) {  // pair u reads z columns 2u .. 2u + Rq; even width (whole pair pixels)
+        c.Zw = (c.OW + 1) / 2 * 2 + c.Rq - 1;
+        c.Zw += c.Zw & 1;
+      }
+      c.OWs = c.pairs ? c.Zw : c.OW;
+      c.OHs = c.pairs ? c.Zh : c.OH;
     }
     c.impl_dgrad = l > 0 && c.stride == 1 && c.F % atom == 0 && c.pad <= c.R - 1 &&
                    c.H == c.OH + c.R - 1 - 2 * c.pad && c.W == c.OW + c.S - 1 - 2 * c.pad;
@@ -685,7 +691,7 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
     for (auto& c : g_.cg) {
       c.Hq = c.in_q ? c.H + c.pad : c.H;
       c.Wq = c.in_q ? c.W + c.pad : c.W;
-      c.Pq = c.in_q ? b_ * c.Hq * c.Wq : b_ * c.OH * c.OWs;
+      c.Pq = c.in_q ? b_ * c.Hq * c.Wq : b_ * c.OHs * c.OWs;
     }
   }
   const auto& in = g_.input;
@@ -944,14 +950,12 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       xa = op(in, 0, 0);
       xa.conv = view;
     }
-    // s2d: im2col over z. Pixel pairs: one GEMM row per pair (W walked with
-    // stride 2), Rq+1 tap columns, N = 2F (see launch_s2d_weights)
+    // s2d: im2col over z (no pairs: fp32 / tf32 math). Pixel pairs: the pair
+    // kernel [2F][Rq][Rq+1][Cz] (launch_s2d_weights), N = 2F columns
     const int sq = c.Rq + (c.pairs ? 1 : 0);
     const long long Kz = static_cast<long long>(c.Rq) * sq * c.Cz;
-    Im2col zview{1, static_cast<int>(b_), c.Zh, c.Zw, c.Cz, c.Rq, sq, c.pairs ? 2 : 1, 0, c.OH, c.OWs / (c.pairs ? 2 : 1)};
-    zview.stride_h = 1;
-    const long long zrows = b_ * c.OH * (c.OWs / (c.pairs ? 2 : 1));  // GEMM rows (pixels or pairs)
-    const int zn = c.pairs ? 2 * c.F : c.F;                              // GEMM columns
+    const Im2col zview{1, static_cast<int>(b_), c.Zh, c.Zw, c.Cz, c.Rq, c.Rq, 1, 0, c.OH, c.OW};
+    const int zn = c.pairs ? 2 * c.F : c.F;  // GEMM columns
     // bf16 stride-1 convs over zero-bordered rows: the flat-shift kernel (one
     // smem halo per channel block for all taps); output rows are the stored
     // grid, the RowMap keeps the valid ones
@@ -968,18 +972,23 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       GemmPlan pl = c.s2d ? conv_shift_plan(w.z, b_ * gH * gW, c.Cz, c.Rq, c.Rq, gW, w.wz, Kz, c.F, es)
                           : conv_shift_plan(in, c.Pq, c.C, c.R, c.S, gW, kw, c.ldk, c.F, es);
       w.conv_fwd.push_back(pl);
+    } else if (c.pairs) {
+      if (!conv_shift_supported(2 * c.Cz, c.Rq, 2, c.Zw / 2, zn)) config_error("conv1 pixel pairs: unsupported shape");
+      // pair pixels (ConvGeom::pairs): conv1 = a stride-1 Rq x 2 conv over
+      // z' [b][Zh][Zw/2][2Cz] on the flat-shift kernel. The pair weights
+      // [2F][Rq][Rq+1][Cz] are already the [2F][Rq][2][2Cz] kernel of that conv
+      // (s' = 2 s2 + q); output rows are the stored z' grid, the RowMap keeps
+      // the OH x ceil(OW/2) valid pair pixels.
+      Epi es = e;
+      es.ldc = zn;
+      es.bias = w.bias2;
+      const int pw = c.Zw / 2;
+      es.rows = RowMap{1, c.Zh, pw, c.OH, (c.OW + 1) / 2, c.OHs, pw, 0};
+      w.conv_fwd.push_back(conv_shift_plan(w.z, b_ * c.Zh * pw, 2 * c.Cz, c.Rq, 2, pw, w.wz, Kz, zn, es));
     } else if (c.s2d) {
       xa = op(w.z, 0, 0);
       xa.conv = zview;
-      if (c.pairs) {  // row = pixel pair: its 2F outputs are the two pixels' contiguous channel rows
-        e.ldc = zn;
-        e.bias = w.bias2;
-      }
-      // dev: HP_DEV_C1F=<cta2>,<bn> forces conv1's tile
-      static const char* c1f = getenv("HP_DEV_C1F");
-      int f_cta2 = -1, f_bn = 0;
-      if (c1f) sscanf(c1f, "%d,%d", &f_cta2, &f_bn);
-      w.conv_fwd.push_back(plan(xa, op(w.wz, 0, Kz), zrows, zn, Kz, e, 0, f_bn, f_cta2));
+      w.conv_fwd.push_back(plan(xa, op(w.wz, 0, Kz), c.P, c.F, Kz, e));
     } else {
       w.conv_fwd.push_back(plan(xa, op(kw, 0, c.ldk), c.P, c.F, c.Kc, e));
     }
@@ -1051,8 +1060,19 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     } else if (swap) {
       eg.c_trans = 1;  // element (m = k, n = f) -> dW[f][k]
       w.conv_wgrad.push_back(plan(xb, op(w.dz[l], 1, c.F), Kw, c.F, c.s2d ? c.P : c.Pq, eg, 1));
+    } else if (c.pairs) {
+      // pair pixels: the halo wgrad (Im2col::halo) of the Rq x 2 conv over z'
+      // (K = every stored pair pixel; dz is zero off the valid grid). Its column
+      // order maps back onto the pair kernel layout [2F][Rq][2][2Cz] = [2F][Rq][Rq+1][Cz]
+      const int pw = c.Zw / 2;
+      GemmOperand xz = op(w.z, 1, 0);
+      xz.conv = Im2col{1, static_cast<int>(b_), c.Zh, pw, 2 * c.Cz, c.Rq, 2, 1, 0, c.Zh, pw};
+      xz.conv.shift = 1;
+      xz.conv.halo = 1;
+      eg.cols = ColMap{1, 2, 2 * c.Cz};
+      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, zn), xz, zn, Kz, b_ * c.Zh * pw, eg, 1, 128, 0));
     } else if (c.s2d) {
-      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, zn), xb, zn, Kz, zrows, eg, 1));
+      w.conv_wgrad.push_back(plan(op(w.dz[l], 1, c.F), xb, c.F, Kz, c.P, eg, 1));
     } else if (c.in_q && xb.conv.shift && bf && c.S * 64 <= 256 && c.C % 64 == 0 && !no_halo) {
       // halo B (Im2col::halo): N tiles of S*64 columns = the S taps of one kernel
       // row of one channel block, read as one x box per k-tile
@@ -1319,7 +1339,7 @@ void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
     if (l + 1 < nc && g_.cg[l + 1].in_q) yl = OutLayout{g_.cg[l + 1].Hq, g_.cg[l + 1].Wq, g_.cg[l + 1].pad};
     if (c.lrn_n > 0 && c.pk > 0) {
       tl_mark("lrn_pool_fwd", l, false, st_);
-      launch_lrn_pool_fwd<TA>(w.act[l], w.pool[l], w.widx[l], B, c.OH, c.OWs, c.F, c.lrn_n, c.lrn_alpha,
+      launch_lrn_pool_fwd<TA>(w.act[l], w.pool[l], w.widx[l], B, c.OHs, c.OWs, c.F, c.lrn_n, c.lrn_alpha,
                               c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, st_, yl);
       tl_mark("lrn_pool_fwd", l, true, st_);
       ++launches_;
@@ -1328,7 +1348,7 @@ void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
                          c.lrn_k, st_);
       ++launches_;
     } else if (c.pk > 0) {
-      launch_maxpool_fwd_w<TA>(w.act[l], w.pool[l], w.widx[l], B, c.OH, c.OWs, c.F, c.pk, c.ps, c.PH,
+      launch_maxpool_fwd_w<TA>(w.act[l], w.pool[l], w.widx[l], B, c.OHs, c.OWs, c.F, c.pk, c.ps, c.PH,
                                c.PW, st_, yl);
       ++launches_;
     }
@@ -1539,12 +1559,12 @@ void ClusterImpl<TA>::conv_backward_layer(Worker<TA>& w, int l, ConvBwdState& cs
   const OutLayout zl = c.in_q ? OutLayout{c.Hq, c.Wq, c.pad} : OutLayout{};  // dz layout
   if (c.pk > 0 && c.lrn_n > 0) {
     tl_mark("lrn_pool_bwd", l, false, st_);
-    launch_lrn_pool_bwd<TA>(cs.gout, w.widx[l], w.act[l], w.dz[l], B, c.OH, c.OWs, c.F, c.lrn_n, c.lrn_alpha,
+    launch_lrn_pool_bwd<TA>(cs.gout, w.widx[l], w.act[l], w.dz[l], B, c.OHs, c.OWs, c.F, c.lrn_n, c.lrn_alpha,
                             c.lrn_beta, c.lrn_k, c.pk, c.ps, c.PH, c.PW, c.relu ? 1 : 0, st_, zl);
     tl_mark("lrn_pool_bwd", l, true, st_);
     ++launches_;
   } else if (c.pk > 0) {
-    launch_maxpool_bwd_w<TA, TA>(cs.gout, w.widx[l], w.dz[l], mask, B, c.OH, c.OWs, c.F, c.pk, c.ps, c.PH,
+    launch_maxpool_bwd_w<TA, TA>(cs.gout, w.widx[l], w.dz[l], mask, B, c.OHs, c.OWs, c.F, c.pk, c.ps, c.PH,
                                  c.PW, st_, zl);
     ++launches_;
   } else if (c.lrn_n > 0) {
@@ -2207,9 +2227,9 @@ int64_t ClusterImpl<TA>::read_decisions(int worker, int kind, int layer, void* d
     HP_CUDA(cudaStreamSynchronize(st_));
     if (kind == 0) {
       const bool next_q = layer + 1 < nc && g_.cg[layer + 1].in_q && c.pk == 0 && c.lrn_n == 0;
-      const long long H = next_q ? g_.cg[layer + 1].Hq : c.OH, W = next_q ? g_.cg[layer + 1].Wq : c.OWs;
+      const long long H = next_q ? g_.cg[layer + 1].Hq : c.OHs, W = next_q ? g_.cg[layer + 1].Wq : c.OWs;
       const long long p = next_q ? g_.cg[layer + 1].pad : 0;
-      std::vector<TA> h(static_cast<size_t>((next_q ? g_.cg[layer + 1].Pq : b_ * c.OH * c.OWs) * c.F));
+      std::vector<TA> h(static_cast<size_t>((next_q ? g_.cg[layer + 1].Pq : b_ * c.OHs * c.OWs) * c.F));
       HP_CUDA(cudaMemcpy(h.data(), w.act[layer], h.size() * sizeof(TA), cudaMemcpyDeviceToHost));
       uint8_t* m = static_cast<uint8_t*>(dst);
       for (long long b = 0; b < b_; ++b)

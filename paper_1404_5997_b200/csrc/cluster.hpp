@@ -31,8 +31,12 @@ struct ConvGeom {
   // shared-memory-bound N); the output and its gradient are
   // stored OWs = OW rounded up to even wide (the extra column never feeds the
   // pool, its gradient stays zero).
+  // With pairs the stored grid is z's own (OHs x OWs = Zh x Zw): viewed as
+  // "pair pixels" (two horizontally adjacent pixels, 2F channels) conv1 is a
+  // stride-1 3x2 conv over z' [b][Zh][Zw/2][2*Cz] -- a flat shift of the pair
+  // row index -- so it runs on the flat-shift kernel (fprop) and the halo wgrad.
   bool pairs = false;
-  int OWs = 0;                 // stored conv-output width (OW, or even for pairs)
+  int OWs = 0, OHs = 0;        // stored conv-output grid (OW x OH, or z's grid for pairs)
   // q-layout (see RowMap, gemm.cuh): this layer's input x and its dz are
   // stored as (H+pad) x (W+pad) row slots per image with a shared zero border
   // (stride-1 "same" convs): the conv is a flat shift of the row index.
