@@ -40,6 +40,10 @@ def gemm_fn(M, N, K, a_mn, b_mn, bn, cta2, splits):
 VARIANTS = ((-1, 0), (0, 128), (0, 192), (0, 256), (1, 128), (1, 256))
 if os.environ.get("WGRAD_AUTO_ONLY"):
     VARIANTS = ((-1, 0),)
+if os.environ.get("WGRAD_VARIANTS"):  # "cta2:bn,..."
+    VARIANTS = tuple(tuple(int(v) for v in x.split(":")) for x in os.environ["WGRAD_VARIANTS"].split(","))
+SPLITS = tuple(int(v) for v in os.environ.get("WGRAD_SPLITS", "0").split(","))
+MAJORS = tuple(tuple(int(c) for c in m) for m in os.environ.get("WGRAD_MAJORS", "11,00").split(","))
 shapes = [(384, 3456, 25088), (384, 1728, 25088), (256, 3456, 25088), (1600, 192, 107648), (64, 576, 387200)]
 if len(sys.argv) > 1:
     shapes = [tuple(int(v) for v in s.split("x")) for s in sys.argv[1:]]
@@ -50,9 +54,9 @@ for (M, N, K) in shapes:
     t = timeit(lambda: a @ b)
     print(f"{str((M, N, K)):25s} cublas                 {t:7.3f} {flops / t / 1e9:7.0f}", flush=True)
     del a, b
-    for (a_mn, b_mn) in ((1, 1), (0, 0)):
+    for (a_mn, b_mn) in MAJORS:
         for cta2, bn in VARIANTS:
-            for splits in (0,):
+            for splits in SPLITS:
                 try:
                     f, keep, s = gemm_fn(M, N, K, a_mn, b_mn, bn, cta2, splits)
                     t = timeit(f)
