@@ -1709,35 +1709,23 @@ int gemm_choose_bn(int M, int N) {
 
 // Split-K factor when the tile grid underfills the machine: minimise the
 // critical path, waves x (k-tiles per split + a fixed per-unit cost of ~4
-// k-tiles: pipeline fill, epilogue) + splits x red (the fp32 partials' write +
-// ordered re-read per split, in k-tile times), keeping >= 8 k-tiles per split;
-// more splits must win by >3%. Measured on the FC shapes
-// (tests/dev/fc_bench.py): fc6/fc7 fwd pick 4, fc8 8.
-static int split_for_waves(int tiles, int kt, int slots, double red = 0.0) {
+// k-tiles: pipeline fill, epilogue, partial-sum write), keeping >= 8 k-tiles
+// per split; more splits must win by >3% (partial-sum traffic). Measured on
+// the FC shapes (tests/dev/fc_bench.py): fc6/fc7 fwd pick 4, fc8 8.
+static int split_for_waves(int tiles, int kt, int slots) {
   if (tiles >= slots * 4 / 5 || kt < 16) return 1;
   int best = 1;
   double best_cost = static_cast<double>(cdiv(tiles, slots)) * (kt + 4);
   for (int s = 2; s <= std::min(64, kt / 8); ++s) {
     const int kps = cdiv(kt, s);
     const int real = cdiv(kt, kps);
-    const double cost = static_cast<double>(cdiv(tiles * real, slots)) * (kps + 4) + real * red;
+    const double cost = static_cast<double>(cdiv(tiles * real, slots)) * (kps + 4);
     if (cost < best_cost * 0.97) {  // >3% better: more splits cost partial-sum traffic
       best_cost = cost;
       best = real;
     }
   }
   return best;
-}
-
-// Cost of one more split-K partial (M x N fp32 written, then re-read by the
-// ordered reduce at ~5 TB/s) in units of one k-tile of the tile's mainloop
-// (2 x 128 x bn x BK flops at ~9.5 TF/s per SM). HP_DEV_SPLIT_RED=0 drops it.
-static double split_reduce_ktiles(int M, int N, int bn, int es) {
-  static const bool off = getenv("HP_DEV_SPLIT_RED") && atoi(getenv("HP_DEV_SPLIT_RED")) == 0;
-  if (off) return 0.0;
-  const double red_us = static_cast<double>(M) * N * 8.0 / 5.0e6;
-  const double tk_us = 2.0 * 128 * bn * (128 / es) / 9.5e6;
-  return red_us / tk_us;
 }
 
 int gemm_choose_splits(int math, int M, int N, int K, int bn) {
@@ -1753,7 +1741,7 @@ int gemm_choose_splits(int math, int M, int N, int K, int bn) {
     const int kps = cdiv(kt, splits);
     return cdiv(kt, kps);
   }
-  return split_for_waves(tiles, kt, 148, split_reduce_ktiles(M, N, bn, es));
+  return split_for_waves(tiles, kt, 148);
 }
 
 static bool g_cta2_default = true;
@@ -1833,7 +1821,7 @@ GemmPlan gemm_plan(int math, const GemmOperand& a, const GemmOperand& b, int M, 
     p.bn = (bn == 64 || bn == 128 || bn == 192 || bn == 256) ? bn : 256;
     if (splits <= 0) {
       const int tiles2 = cdiv(M, 2 * kBM) * cdiv(N, p.bn);
-      splits = split_for_waves(tiles2, kt, 74, split_reduce_ktiles(M, N, p.bn, es));
+      splits = split_for_waves(tiles2, kt, 74);
     }
   } else {
     p.bn = bn > 0 ? bn : gemm_choose_bn(M, N);
