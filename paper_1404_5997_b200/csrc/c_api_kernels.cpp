@@ -268,7 +268,7 @@ HP_API int hp_data_generate(const hp_dataset_spec* spec, int64_t first, int64_t 
       return;
     }
     if (mem_kind != HP_MEM_HOST) usage_error("data_generate: bad mem_kind");
-    if (first < 0 || count < 0 || first + count > spec->num_examples) datagen_launch(*spec, first, count, nullptr, nullptr, st);
+    datagen_check_range(*spec, first, count);
     if (count == 0) return;
     const size_t nx = static_cast<size_t>(count) * spec->channels * spec->height * spec->width;
     const size_t nt = static_cast<size_t>(count) * spec->num_classes;

@@ -153,11 +153,15 @@ void datagen_validate(const hp_dataset_spec& s) {
   if (!(s.separation >= 0.0)) config_error("data.separation: expected >= 0");
 }
 
-void datagen_launch(const hp_dataset_spec& s, int64_t first, int64_t count, float* x, float* t, cudaStream_t st) {
+void datagen_check_range(const hp_dataset_spec& s, int64_t first, int64_t count) {
   datagen_validate(s);
   if (first < 0 || count < 0 || first + count > s.num_examples)
     usage_error("data_generate: examples [" + std::to_string(first) + ", " + std::to_string(first + count) +
                 ") outside [0, " + std::to_string(s.num_examples) + ")");
+}
+
+void datagen_launch(const hp_dataset_spec& s, int64_t first, int64_t count, float* x, float* t, cudaStream_t st) {
+  datagen_check_range(s, first, count);
   if (count == 0) return;
   const int64_t D = static_cast<int64_t>(s.channels) * s.height * s.width;
   const int64_t units = count * ((D + 1023) / 1024);

@@ -9,6 +9,8 @@
 namespace hp {
 
 void datagen_validate(const hp_dataset_spec& s);
+// datagen_validate plus [first, first + count) inside [0, num_examples) (UsageError).
+void datagen_check_range(const hp_dataset_spec& s, int64_t first, int64_t count);
 // Examples [first, first + count) of the dataset into device memory: x
 // [count][C][H][W] (the reference's NCHW batch layout), t [count][L] one-hot.
 void datagen_launch(const hp_dataset_spec& s, int64_t first, int64_t count, float* x, float* t, cudaStream_t st);
