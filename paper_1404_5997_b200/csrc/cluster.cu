@@ -365,6 +365,7 @@ struct Worker {
   float* colsum_ws = nullptr;
   // GEMM plans
   std::vector<GemmPlan> conv_fwd, conv_wgrad, conv_dgrad, fc_fwd, fc_wgrad, fc_dgrad;
+  std::vector<GemmPlan> last_fwd_slices;  // micro-pipelined last conv layer (scheme C): one plan per turn's slice
   GemmPlan fc0_slot1[3];  // fc layer 0 {fwd, wgrad, dgrad} over boundary slot 1 (slot 0: the vectors)
 };
 
@@ -401,7 +402,14 @@ class ClusterImpl final : public ClusterBase {
   Worker<TA>& local(int gid);
   const Worker<TA>* local_or_null(int gid) const;
   void build_plans(Worker<TA>& w);
-  void conv_forward(Worker<TA>& w);
+  void conv_forward(Worker<TA>& w, int layers);
+  void conv_forward_last_slice(Worker<TA>& w, int j);
+  // Scheme C micro-pipelining: the last conv layer (and its
+  // pool) runs in K image slices in turn order, and turn j's slice exchange
+  // waits only for slice j -- turn 0's exchange runs under slices 1..K-1.
+  bool slice_last_ = false;
+  std::vector<cudaEvent_t> ev_slice_;
+  bool slicing() const { return slice_last_ && !w_.empty() && !w_[0].last_fwd_slices.empty(); }
   const TA* stage_in(const Worker<TA>& w, int l) const;
   void rotate_all(Worker<TA>& w);
   struct ConvBwdState {
@@ -781,6 +789,14 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   for (auto& e : ev_bg_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   HP_CUDA(cudaMallocHost(&host_parts_, sizeof(double) * nl * num_sub_ * xblocks_));
   HP_CUDA(cudaMallocHost(&host_bad_, sizeof(int) * nl));
+  {
+    const ConvGeom& lc = g_.cg.back();
+    static const bool no_slices = getenv("HP_DEV_NO_SLICES") != nullptr;  // dev: one exchange wait for the whole conv
+    slice_last_ = scheme_ == HP_SCHEME_C && !dp_ && K_ > 1 && b_ % K_ == 0 && num_sub_ == K_ &&
+                  g_.cg.size() > 1 && lc.in_q && lc.lrn_n == 0 && !no_slices;
+    ev_slice_.resize(slice_last_ ? static_cast<size_t>(K_) : 0);
+    for (auto& e : ev_slice_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   // Plans first with a null workspace to size it (for both conv kernel
   // families, so rebuild_plans can switch), then for real.
   const bool shift = use_shift;
@@ -830,6 +846,7 @@ ClusterImpl<TA>::~ClusterImpl() {
   for (auto e : ev_dz_) cudaEventDestroy(e);
   for (auto e : ev_wg_) cudaEventDestroy(e);
   for (auto e : ev_bg_) cudaEventDestroy(e);
+  for (auto e : ev_slice_) cudaEventDestroy(e);
   if (sw_) {
     cudaStreamSynchronize(sw_);
     cudaStreamDestroy(sw_);
@@ -913,6 +930,7 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
     return pl;
   };
   w.conv_fwd.clear();
+  w.last_fwd_slices.clear();
   w.conv_wgrad.clear();
   w.conv_dgrad.clear();
   w.fc_fwd.clear();
@@ -972,6 +990,18 @@ void ClusterImpl<TA>::build_plans(Worker<TA>& w) {
       GemmPlan pl = c.s2d ? conv_shift_plan(w.z, b_ * gH * gW, c.Cz, c.Rq, c.Rq, gW, w.wz, Kz, c.F, es)
                           : conv_shift_plan(in, c.Pq, c.C, c.R, c.S, gW, kw, c.ldk, c.F, es);
       w.conv_fwd.push_back(pl);
+      if (slice_last_ && l == nc - 1 && !c.s2d && !e.rows.enabled) {
+        // scheme C micro-pipelining: the same conv on each turn's image slice
+        // (q-layout images are Hq*Wq rows apart; rows outside the slice read as
+        // the zero border, exactly as inside the whole batch)
+        const long long bs = b_ / K_;
+        for (int j = 0; j < K_; ++j) {
+          Epi ej = es;
+          ej.c = w.act[l] + j * bs * c.OHs * c.OWs * c.F;
+          w.last_fwd_slices.push_back(conv_shift_plan(static_cast<const TA*>(in) + j * bs * c.Hq * c.Wq * c.C,
+                                                      bs * c.Hq * c.Wq, c.C, c.R, c.S, gW, kw, c.ldk, c.F, ej));
+        }
+      }
     } else if (c.pairs) {
       if (!conv_shift_supported(2 * c.Cz, c.Rq, 2, c.Zw / 2, zn)) config_error("conv1 pixel pairs: unsupported shape");
       // pair pixels (ConvGeom::pairs): conv1 = a stride-1 Rq x 2 conv over
@@ -1314,10 +1344,10 @@ void ClusterImpl<TA>::refresh_copies(Worker<TA>& w) {
 
 // ------------------------------------------------------------------ forward
 template <class TA>
-void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
+void ClusterImpl<TA>::conv_forward(Worker<TA>& w, int layers) {
   const int nc = static_cast<int>(g_.cg.size());
   const int B = static_cast<int>(b_);
-  for (int l = 0; l < nc; ++l) {
+  for (int l = 0; l < layers; ++l) {
     const ConvGeom& c = g_.cg[l];
     if (c.s2d) {
       tl_mark("s2d_input", l, false, st_);
@@ -1352,6 +1382,22 @@ void ClusterImpl<TA>::conv_forward(Worker<TA>& w) {
                                c.PW, st_, yl);
       ++launches_;
     }
+  }
+}
+
+// Slice j of the last conv layer: images [j*b/K, (j+1)*b/K) through the
+// layer's flat-shift GEMM (plan built on the slice's rows) and its pool.
+template <class TA>
+void ClusterImpl<TA>::conv_forward_last_slice(Worker<TA>& w, int j) {
+  const int l = static_cast<int>(g_.cg.size()) - 1;
+  const ConvGeom& c = g_.cg[l];
+  const long long bs = b_ / K_;
+  gemm(w.last_fwd_slices[static_cast<size_t>(j)], "conv_fwd", l);
+  const long long ao = j * bs * c.OHs * c.OWs * c.F, po = j * bs * c.PH * c.PW * c.F;
+  if (c.pk > 0) {
+    launch_maxpool_fwd_w<TA>(w.act[l] + ao, w.pool[l] + po, w.widx[l] + po, static_cast<int>(bs), c.OHs, c.OWs, c.F,
+                             c.pk, c.ps, c.PH, c.PW, st_, OutLayout{});
+    ++launches_;
   }
 }
 
@@ -1714,7 +1760,15 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
   }
   {
     NvtxRange r("hp.conv_forward");
-    for (auto& w : w_) conv_forward(w);
+    const int nc = static_cast<int>(g_.cg.size());
+    for (auto& w : w_) conv_forward(w, slicing() ? nc - 1 : nc);
+    if (slicing()) {  // slice-major over the workers: turn j's rows of every worker, then ev_slice_[j]
+      for (int j = 0; j < K_; ++j) {
+        for (auto& w : w_) conv_forward_last_slice(w, j);
+        marker(700 + j, st_);
+        HP_CUDA(cudaEventRecord(ev_slice_[static_cast<size_t>(j)], st_));
+      }
+    }
   }
   // The turns (cluster.cpp:507-614). The boundary exchange and the gradient
   // return run on their own stream sr_ with double-buffered boundary slots:
@@ -1726,8 +1780,12 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
   // activation buffers, and in variable mode turn j+1 reads the weights turn
   // j updated (cluster.cpp:586-601).
   cudaStream_t xs = profile ? st_ : sr_;  // serialised when profiling
-  HP_CUDA(cudaEventRecord(ev_conv_, st_));
-  HP_CUDA(cudaStreamWaitEvent(xs, ev_conv_, 0));
+  if (slicing()) {
+    HP_CUDA(cudaStreamWaitEvent(xs, ev_slice_[0], 0));  // turn 0 needs slice 0 only
+  } else {
+    HP_CUDA(cudaEventRecord(ev_conv_, st_));
+    HP_CUDA(cudaStreamWaitEvent(xs, ev_conv_, 0));
+  }
   marker(100, xs);
   route_forward(0, 0, xs);
   marker(200, xs);
@@ -1738,6 +1796,7 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
       // slot (j+1)&1 was last read by turn j-1: its fc0 forward / xent on st_
       // and its fc0 wgrad on sf_, all before turn j-1's ev_fcw_ record
       if (j >= 1) HP_CUDA(cudaStreamWaitEvent(xs, ev_fcw_, 0));
+      if (slicing()) HP_CUDA(cudaStreamWaitEvent(xs, ev_slice_[static_cast<size_t>(j + 1)], 0));
       marker(100 + j + 1, xs);
       route_forward(j + 1, slot ^ 1, xs);
       marker(200 + j + 1, xs);

@@ -81,3 +81,33 @@ def test_alexnet_k8_scheme_c_variable_runs():
     assert len(r.trace) == 3 + 2 * K
     for w in range(1, K):
         assert np.array_equal(g.param(w, 0, 4), g.param(0, 0, 4))
+
+
+@pytest.mark.parametrize("K", [2, 4])
+def test_scheme_c_turn0_exchange_overlaps_last_conv(K):
+    """Scheme C micro-pipelining: the last conv layer and its
+    pool run in K image slices in turn order (markers 700 + j after slice j),
+    and turn j's slice exchange waits for slice j only -- so turn 0's exchange
+    runs under the conv of slices 1..K-1, where without slicing it waited for
+    the whole conv forward."""
+    spec = hp.alexnet_1col()
+    b = 2 * K
+    g = hp.Cluster(spec, hp.ClusterConfig(workers=K, per_worker_batch=b, scheme=hp.Scheme.C, variable_batch=True,
+                                          seed=1, math_mode=hp.MathMode.BF16))
+    xs, ts = zip(*[hp.synthetic_batch(spec, b, worker=w) for w in range(K)])
+    hpp = hp.HyperParams(lr=1e-4)
+    g.run_step(list(xs), list(ts), hpp)
+    tags, reach = g.marker_graph(list(xs), list(ts), hpp)
+    T = {t: i for i, t in enumerate(tags)}
+    R = lambda a, b_: bool(reach[T[a], T[b_]])
+    for j in range(K):
+        assert 700 + j in T, tags
+        assert R(700 + j, 100 + j)                # turn j's exchange needs slice j
+        assert R(700 + K - 1, 300 + j)            # the FC compute follows the whole conv (stream order)
+        if j + 1 < K:
+            assert R(700 + j, 700 + j + 1)
+        if j <= 1:
+            # turns 0 and 1 exchange into fresh slots: they wait for their own slice, not the later
+            # ones (turn j >= 2 reuses turn j-2's slot and so follows its FC work, after the conv)
+            for later in range(j + 1, K):
+                assert not R(700 + later, 100 + j) and not R(700 + later, 200 + j), (j, later)
