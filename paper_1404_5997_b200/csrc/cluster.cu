@@ -791,9 +791,13 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   HP_CUDA(cudaMallocHost(&host_bad_, sizeof(int) * nl));
   {
     const ConvGeom& lc = g_.cg.back();
-    static const bool no_slices = getenv("HP_DEV_NO_SLICES") != nullptr;  // dev: one exchange wait for the whole conv
-    slice_last_ = scheme_ == HP_SCHEME_C && !dp_ && K_ > 1 && b_ % K_ == 0 && num_sub_ == K_ &&
-                  g_.cg.size() > 1 && lc.in_q && lc.lrn_n == 0 && !no_slices;
+    // Opt-in (HP_SLICE_LAST_CONV=1, read per cluster): measured a net loss on
+    // B200 at b = 128 -- K small slices of the last conv cost a wave each
+    // (8 workers, logical transport: 17.5 -> 18.2 ms per step) while the
+    // exchange they would hide is a few MB over NVLink 5.
+    const char* sl = getenv("HP_SLICE_LAST_CONV");
+    slice_last_ = sl && atoi(sl) != 0 && scheme_ == HP_SCHEME_C && !dp_ && K_ > 1 && b_ % K_ == 0 &&
+                  num_sub_ == K_ && g_.cg.size() > 1 && lc.in_q && lc.lrn_n == 0;
     ev_slice_.resize(slice_last_ ? static_cast<size_t>(K_) : 0);
     for (auto& e : ev_slice_) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }

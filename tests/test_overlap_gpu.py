@@ -60,6 +60,25 @@ def test_scheme_a_single_turn_graph():
     assert sorted(tags) == [100, 200, 300, 400, 500, 600]
 
 
+def test_sliced_last_conv_matches_unsliced(monkeypatch):
+    """The micro-pipelined schedule computes the same step: AlexNet K=2 scheme C
+    variable, bf16, sliced vs unsliced -- the conv is the same per-image
+    computation, so the parameters after the step are bit-identical."""
+    spec = hp.alexnet_1col()
+    K, b = 2, 4
+    xs, ts = zip(*[hp.synthetic_batch(spec, b, worker=w) for w in range(K)])
+    out = []
+    for sliced in ("0", "1"):
+        monkeypatch.setenv("HP_SLICE_LAST_CONV", sliced)
+        g = hp.Cluster(spec, hp.ClusterConfig(workers=K, per_worker_batch=b, scheme=hp.Scheme.C, variable_batch=True,
+                                              seed=1, math_mode=hp.MathMode.BF16))
+        r = g.run_step(list(xs), list(ts), hp.HyperParams(lr=1e-3))
+        out.append((r.metrics.loss, [g.param(w, which, l) for w in range(K) for which in range(8)
+                                     for l in range(5 if (which & 3) < 2 else 3)]))
+    assert out[0][0] == out[1][0]
+    assert all(np.array_equal(a, c) for a, c in zip(out[0][1], out[1][1]))
+
+
 def test_alexnet_k8_scheme_c_variable_runs():
     """configs[3] functional on one B200: AlexNet-1col b=128 per worker, K=8
     logical workers, scheme C (16-example slices), approximate variant (8 FC
@@ -84,12 +103,14 @@ def test_alexnet_k8_scheme_c_variable_runs():
 
 
 @pytest.mark.parametrize("K", [2, 4])
-def test_scheme_c_turn0_exchange_overlaps_last_conv(K):
+def test_scheme_c_turn0_exchange_overlaps_last_conv(K, monkeypatch):
     """Scheme C micro-pipelining: the last conv layer and its
     pool run in K image slices in turn order (markers 700 + j after slice j),
     and turn j's slice exchange waits for slice j only -- so turn 0's exchange
     runs under the conv of slices 1..K-1, where without slicing it waited for
-    the whole conv forward."""
+    the whole conv forward. Opt-in (HP_SLICE_LAST_CONV=1): at b = 128 on B200 the
+    slices' wave quantisation costs more than the exchange it hides."""
+    monkeypatch.setenv("HP_SLICE_LAST_CONV", "1")
     spec = hp.alexnet_1col()
     b = 2 * K
     g = hp.Cluster(spec, hp.ClusterConfig(workers=K, per_worker_batch=b, scheme=hp.Scheme.C, variable_batch=True,
