@@ -374,6 +374,24 @@ __device__ __forceinline__ float4 ld_bf16x4(const void* p, long long off) {
   return make_float4(a.x, a.y, b.x, b.y);
 }
 
+#ifndef HP_SGD_STREAMING
+#define HP_SGD_STREAMING 1
+#endif
+#if HP_SGD_STREAMING
+#define SGD_LD(p) __ldcs(p)
+#define SGD_ST(p, v) __stcs(p, v)
+#else
+#define SGD_LD(p) (*(p))
+#define SGD_ST(p, v) (*(p) = (v))
+#endif
+__device__ __forceinline__ void st_bf16x4_cs(void* p, long long off, float4 x) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y);
+  __nv_bfloat162 hi = __floats2bfloat162_rn(x.z, x.w);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  SGD_ST(reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p) + off), u);
+}
 __device__ __forceinline__ void st_bf16x4(void* p, long long off, float4 x) {
   __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y);
   __nv_bfloat162 hi = __floats2bfloat162_rn(x.z, x.w);
@@ -517,9 +535,9 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int
     for (int i = 0; i < 8; ++i) {
       const int m = mrow[i];
       const long long off = static_cast<long long>(m) * e.ldc + n;
-      if (m >= 0) {
-        aux[i] = *reinterpret_cast<const float4*>(e.sgd_w + off);
-        aux2[i] = *reinterpret_cast<const float4*>(e.sgd_m + off);
+      if (m >= 0) {  // streamed once: evict-first (leave L2 to the concurrent GEMMs)
+        aux[i] = SGD_LD(reinterpret_cast<const float4*>(e.sgd_w + off));
+        aux2[i] = SGD_LD(reinterpret_cast<const float4*>(e.sgd_m + off));
       }
     }
 #pragma unroll
@@ -538,9 +556,9 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int
         f4set(m4, j, d);
         f4set(w4, j, __fadd_rn(f4get(w4, j), d));
       }
-      *reinterpret_cast<float4*>(e.sgd_w + off) = w4;
-      *reinterpret_cast<float4*>(e.sgd_m + off) = m4;
-      if (e.sgd_copy) st_bf16x4(e.sgd_copy, off, w4);
+      SGD_ST(reinterpret_cast<float4*>(e.sgd_w + off), w4);
+      SGD_ST(reinterpret_cast<float4*>(e.sgd_m + off), m4);
+      if (e.sgd_copy) st_bf16x4_cs(e.sgd_copy, off, w4);
     }
     return;
   }

@@ -1,2 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_overlap_gpu.py -x -q -m gpu > gpurun_out/pt.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pt.log
+for i in 1 2; do for v in ns cs; do
+  if [ $v = ns ]; then export HP_DEV_LIB=paper_1404_5997_b200/lib/libns.so; else unset HP_DEV_LIB; fi
+  LABEL=$v timeout 300 python tests/dev/gemm_times.py 2>&1 | grep -E "==|fc_wgrad|fc_dgrad"
+done; done
