@@ -8,11 +8,13 @@ elapsed time) -- the counter tcgen05.mma kind::f16 drives on sm_100. memT% is
 sm__mem_tensor_cycles_active (tensor-core operand reads from smem/TMEM). The
 legacy sm__pipe_tensor_cycles_active counts only the HMMA (mma.sync) pipe and
 reads ~3% on tcgen05 kernels, so it is not used.
-usage: ncu_summary.py <rep|csv|csv.gz> [labels comma-separated]"""
+usage: ncu_summary.py <rep|csv|csv.gz> [labels comma-separated | --mem]
+--mem: the memory-kernel table (us, DRAM MB and TB/s, issue%, achieved occupancy, sm% / l1%)."""
 import csv, gzip, io, subprocess, sys
 
 src = sys.argv[1]
-labels = sys.argv[2].split(",") if len(sys.argv) > 2 else None
+mem = len(sys.argv) > 2 and sys.argv[2] == "--mem"
+labels = sys.argv[2].split(",") if len(sys.argv) > 2 and not mem else None
 if src.endswith(".ncu-rep"):
     text = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 elif src.endswith(".gz"):
@@ -41,6 +43,18 @@ def scale(k, to):
     return f / to
 
 
+if mem:
+    print(f"{'kernel':50s} {'us':>6s} {'dramMB':>7s} {'TB/s':>5s} {'issue%':>6s} {'warps%':>6s} {'sm%':>5s} {'l1%':>5s}")
+    for r in rows[2:]:
+        name = r[col["Kernel Name"]].split("(")[0].replace("void ", "").replace("hp::", "")[-50:]
+        t = g(r, "gpu__time_duration.sum") * scale("gpu__time_duration.sum", 1e-6)
+        dram = (g(r, "dram__bytes_read.sum") * scale("dram__bytes_read.sum", 1e6) +
+                g(r, "dram__bytes_write.sum") * scale("dram__bytes_write.sum", 1e6))
+        print(f"{name:50s} {t:6.1f} {dram:7.1f} {dram / t:5.2f} {g(r, 'sm__inst_issued.avg.pct_of_peak_sustained_active'):6.1f} "
+              f"{g(r, 'sm__warps_active.avg.pct_of_peak_sustained_active'):6.1f} "
+              f"{g(r, 'sm__throughput.avg.pct_of_peak_sustained_elapsed'):5.1f} "
+              f"{g(r, 'l1tex__throughput.avg.pct_of_peak_sustained_elapsed'):5.1f}")
+    sys.exit(0)
 TEN = "sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed"
 MEMT = "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"
 print(f"{'#':>3} {'label':12s} {'kernel':28s} {'grid':>6s} {'us':>7s} {'tensor%':>7s} {'memT%':>6s} {'dramMB':>7s} "
