@@ -1361,6 +1361,63 @@ __global__ void __launch_bounds__(256) s2d_input_kernel(const float* __restrict_
   }
 }
 
+// Space-to-depth fast path (stride 4, CC input channels, even pad and W --
+// AlexNet conv1): one thread per z pixel (b, i, j) gathers its 16*CC values
+// straight from global memory as 8-byte pairs (lanes = consecutive j, so a
+// warp's loads cover contiguous 512-byte runs of each input row; no division),
+// stages them in smem, and the block then writes its z rows' real channels as
+// 16-byte chunks with consecutive lanes on consecutive chunks (a per-thread
+// pixel store would put 32 cache lines behind every warp store).
+// Same values as s2d_input_kernel: z[b][i][j][(dr*4+dc)*CC+c] =
+// x[b][c][4i+dr-pad][4j+dc-pad] (zero outside the image).
+constexpr int kS2dBX = 64, kS2dBY = 4;
+template <class T, int CC>
+__global__ void __launch_bounds__(kS2dBX * kS2dBY) s2d4_input_kernel(const float* __restrict__ x, T* __restrict__ z,
+                                                                    int H, int W, int pad, int Zh, int Zw, int Cz) {
+  constexpr int R = 16 * CC;                      // real channels per z pixel
+  constexpr int CH = 16 / sizeof(T);              // elements per 16-byte chunk
+  constexpr int NCH = R / CH;                     // chunks per pixel
+  constexpr int RP = sizeof(T) == 2 ? R + CH : R;  // bf16: padded rows, 2-way (not 4-way) bank conflicts
+  __shared__ __align__(16) T tile[kS2dBY][kS2dBX][RP];
+  const int j = blockIdx.x * kS2dBX + threadIdx.x;
+  const int i = blockIdx.y * kS2dBY + threadIdx.y;
+  const int b = blockIdx.z;
+  if (j < Zw && i < Zh) {
+    float v[R];
+    const int w0 = 4 * j - pad;
+#pragma unroll
+    for (int dr = 0; dr < 4; ++dr) {
+      const int h = 4 * i + dr - pad;
+      const bool hv = h >= 0 && h < H;
+#pragma unroll
+      for (int c = 0; c < CC; ++c) {
+        const float* row = x + ((static_cast<long long>(b) * CC + c) * H + (hv ? h : 0)) * W;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int w = w0 + 2 * k;
+          float2 p = make_float2(0.f, 0.f);
+          if (hv && w >= 0 && w < W) p = __ldg(reinterpret_cast<const float2*>(row + w));
+          v[(dr * 4 + 2 * k) * CC + c] = p.x;
+          v[(dr * 4 + 2 * k + 1) * CC + c] = p.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; q += 4) st4<T>(&tile[threadIdx.y][threadIdx.x][q], v + q);
+  }
+  __syncthreads();
+  const int jn = min(kS2dBX, Zw - static_cast<int>(blockIdx.x) * kS2dBX);
+  const int tid = threadIdx.y * kS2dBX + threadIdx.x;
+  for (int t = tid; t < kS2dBY * jn * NCH; t += kS2dBX * kS2dBY) {
+    const int y = t / (jn * NCH), rem = t - y * (jn * NCH);
+    const int jj = rem / NCH, p = rem - jj * NCH;
+    const int ii = blockIdx.y * kS2dBY + y;
+    if (ii >= Zh) break;
+    T* dst = z + ((static_cast<long long>(b) * Zh + ii) * Zw + blockIdx.x * kS2dBX + jj) * Cz + p * CH;
+    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(&tile[y][jj][p * CH]);
+  }
+}
+
 // pairs = 0: wz[F][Rq][Rq][Cz]. pairs = 1 (pixel-pair GEMM, see launch_s2d_weights):
 // wz[2F][Rq][Rq+1][Cz], row p*F + f holding filter f at tap columns shifted by
 // p (zero elsewhere), plus bias2[2F] = the bias twice.
@@ -1684,6 +1741,11 @@ void launch_s2d_input(const float* x, T* z, int B, int C, int H, int W, int s, i
                       cudaStream_t st) {
   if (Cz % 8 != 0) throw std::runtime_error("s2d: padded channels must be a multiple of 8");
   if (static_cast<long long>(B) * Zh * Zw * Cz >= (1LL << 31)) throw std::runtime_error("s2d: too large");
+  if (s == 4 && C == 3 && pad % 2 == 0 && W % 2 == 0 && Cz >= 48 && B <= 65535) {
+    s2d4_input_kernel<T, 3><<<dim3((Zw + kS2dBX - 1) / kS2dBX, (Zh + kS2dBY - 1) / kS2dBY, B), dim3(kS2dBX, kS2dBY),
+                              0, st>>>(x, z, H, W, pad, Zh, Zw, Cz);
+    return;
+  }
   const size_t smem = static_cast<size_t>(C) * s * s * Zw * sizeof(float);
   if (smem > 200 * 1024 || Cz > 256) throw std::runtime_error("s2d: input rows too wide for smem");
   cudaFuncSetAttribute(s2d_input_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
