@@ -438,9 +438,16 @@ __device__ __forceinline__ const float* epi_stage_bias(const GemmArgs& a, float*
 // Output rows of the 8 GEMM rows m0 + 4i + (lane >> 3) a thread stores in
 // epi_chunk (-1: past M or dropped by the RowMap). Depends only on the tile
 // and the thread, so the kernels compute it once per tile.
+__device__ __forceinline__ bool epi_direct(const GemmArgs& a) {
+  return !(a.dbg & 2) && (a.raw_partial || (!a.epi.beta && !a.epi.sgd_w));
+}
 __device__ __forceinline__ void epi_rows(const GemmArgs& a, int m0, int (&mrow)[8], int& mself) {
   const int ms = m0 + (threadIdx.x & 31);
   mself = ms < a.M ? map_row(a.epi.rows, ms) : -1;
+  // the 8 staged-layout rows only where epi_chunk takes the staged path: the
+  // direct (row-per-thread) epilogues use mself alone, and the RowMap's
+  // divisions were ~40% of the conv fprop epilogue's instructions
+  if (epi_direct(a) || !epi_vec_ok(a)) return;
   const int rsub = (threadIdx.x & 31) >> 3;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -460,8 +467,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int m0, int n0, int
   // write straight from the row-per-thread layout: 32 contiguous outputs per
   // thread, no smem round trip (the staged transpose costs shared-memory
   // bandwidth the MMAs need; it pays only when the epilogue also reads HBM).
-  const bool direct = !(a.dbg & 2) && (a.raw_partial || (!a.epi.beta && !a.epi.sgd_w));
-  if (direct || !epi_vec_ok(a)) {
+  if (epi_direct(a) || !epi_vec_ok(a)) {
     epi_row32(a, m0 + lane, n0, split, v, mself, sbias, mpre);
     return;
   }
@@ -1202,18 +1208,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 // own 128 rows + halo), one weight-tile TMA per (tap, cb), 4 MMAs per tap whose
 // A descriptor starts (r*wq + s) rows into the halo.
 constexpr uint32_t kHaloBytes = 256u * 128u;
+// halo ring depth (dev knob): 3 measured no different from 2 on the step
+// (conv1 fprop, 2 channel blocks per tile, is not waiting on its halos)
+#ifndef HP_SHIFT_HALOS
+#define HP_SHIFT_HALOS 2
+#endif
+constexpr int kShiftHalos = HP_SHIFT_HALOS;
 #ifndef HP_SHIFT_CAP
 #define HP_SHIFT_CAP 12
 #endif
 __host__ __device__ constexpr uint32_t shift_b_bytes(int bn) { return static_cast<uint32_t>(bn / 2) * 128u; }
 __host__ __device__ constexpr int shift_stages(int bn) {
-  return static_cast<int>((kMaxDynSmem - 2304u - kEpiSmemBytes - 2u * kHaloBytes) / shift_b_bytes(bn)) > HP_SHIFT_CAP
+  return static_cast<int>((kMaxDynSmem - 2304u - kEpiSmemBytes - kShiftHalos * kHaloBytes) / shift_b_bytes(bn)) >
+                 HP_SHIFT_CAP
              ? HP_SHIFT_CAP
-             : static_cast<int>((kMaxDynSmem - 2304u - kEpiSmemBytes - 2u * kHaloBytes) / shift_b_bytes(bn));
+             : static_cast<int>((kMaxDynSmem - 2304u - kEpiSmemBytes - kShiftHalos * kHaloBytes) / shift_b_bytes(bn));
 }
 // barrier words (full/empty per stage + 8) and the TMEM slot, rounded to 128 B
 __host__ __device__ constexpr uint32_t shift_bar_bytes(int bn) {
-  return ((static_cast<uint32_t>(2 * shift_stages(bn) + 8) * 8u + 4u) + 127u) & ~127u;
+  return ((static_cast<uint32_t>(2 * shift_stages(bn) + 2 * kShiftHalos + 4) * 8u + 4u) + 127u) & ~127u;
 }
 
 template <int BN>
@@ -1229,13 +1242,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* halo = smem;                       // [2][256 rows][128 B]
-  uint8_t* bst = smem + 2 * kHaloBytes;       // [STAGES][BNH rows][128 B]
+  uint8_t* halo = smem;                                 // [kShiftHalos][256 rows][128 B]
+  uint8_t* bst = smem + kShiftHalos * kHaloBytes;       // [STAGES][BNH rows][128 B]
   uint64_t* full = reinterpret_cast<uint64_t*>(bst + STAGES * B_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* hfull = empty + STAGES;  // [2]
-  uint64_t* hempty = hfull + 2;      // [2]
-  uint64_t* tfull = hempty + 2;      // [2]
+  uint64_t* hfull = empty + STAGES;         // [kShiftHalos]
+  uint64_t* hempty = hfull + kShiftHalos;   // [kShiftHalos]
+  uint64_t* tfull = hempty + kShiftHalos;   // [2]
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* stg_base = reinterpret_cast<float*>(bst + STAGES * B_BYTES + shift_bar_bytes(BN));
@@ -1256,9 +1269,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kShiftHalos; ++i) {
       mbar_init(&hfull[i], 1);
       mbar_init(&hempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 256);  // both CTAs' epilogue threads (leader's copy is used)
     }
@@ -1287,7 +1302,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           mbar_wait(&hempty[hb], hphase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&hfull[hb], 2 * halo_tx);
           tma_load_2d_2sm(halo + hb * kHaloBytes, &ta, &hfull[hb], cb * 64, am);
-          if (++hb == 2) {
+          if (++hb == kShiftHalos) {
             hb = 0;
             hphase ^= 1;
           }
@@ -1349,7 +1364,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
             }
           if (elect_one()) mma_commit_2sm(&hempty[hb]);
           __syncwarp();
-          if (++hb == 2) {
+          if (++hb == kShiftHalos) {
             hb = 0;
             hphase ^= 1;
           }
@@ -1976,7 +1991,7 @@ GemmPlan conv_shift_plan(const void* x, long long rows, int C, int R, int S, int
   p.tb = make_map(w, 2, static_cast<long long>(R) * S * C, N, ldw, 64, p.bn / 2, CU_TENSOR_MAP_SWIZZLE_128B);
   const int total = cdiv(rows, 2 * kBM) * cdiv(N, p.bn);
   p.grid = dim3(2 * std::min(total, 74));
-  p.smem = 2 * kHaloBytes + static_cast<size_t>(shift_stages(p.bn)) * shift_b_bytes(p.bn) + 1024 +
+  p.smem = kShiftHalos * kHaloBytes + static_cast<size_t>(shift_stages(p.bn)) * shift_b_bytes(p.bn) + 1024 +
            shift_bar_bytes(p.bn) + kEpiSmemBytes;
   p.valid = true;
   return p;
