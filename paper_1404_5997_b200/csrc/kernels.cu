@@ -1060,7 +1060,9 @@ __global__ void __launch_bounds__(GB * TP * TP) lrn_pool_fwd_tile_kernel(
     float beta, float kk, int PH, int PW, int tiles_w, int YH, int YW, int yp) {
   constexpr int S = 2 * TP + 1, CB = GB * V, NT = GB * TP * TP;
   extern __shared__ float4 lrn_tile_sm[];
-  float* yb = reinterpret_cast<float*>(lrn_tile_sm);  // [S][S][CB]
+  // [S][S][V/4][GB][4]: a thread's channel vector as V/4 float4s GB apart, so
+  // the 8 lanes of each 128-bit smem phase touch 128 contiguous bytes
+  float* yb = reinterpret_cast<float*>(lrn_tile_sm);
   const int b = blockIdx.z, cc0 = blockIdx.y * CB;
   const int ph0 = (blockIdx.x / tiles_w) * TP, pw0 = (blockIdx.x % tiles_w) * TP;
   const int h0 = 2 * ph0, w0 = 2 * pw0;
@@ -1076,9 +1078,10 @@ __global__ void __launch_bounds__(GB * TP * TP) lrn_pool_fwd_tile_kernel(
     float o[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) o[j] = v[j + 2] * pow_neg(lrn_scale5(v + j, alpha, kk), beta);
-    float* dst = yb + pix * CB + g * V;
+    float* dst = yb + pix * CB + g * 4;
 #pragma unroll
-    for (int j = 0; j < V; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+    for (int j = 0; j < V; j += 4)
+      *reinterpret_cast<float4*>(dst + j * GB) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
   }
   __syncthreads();
   const int wdw = tid / GB, i = wdw / TP, jj = wdw - i * TP;
@@ -1086,7 +1089,7 @@ __global__ void __launch_bounds__(GB * TP * TP) lrn_pool_fwd_tile_kernel(
   if (ph >= PH || pw >= PW) return;
   float best[V];
   int bi[V];
-  const float* base = yb + ((2 * i) * S + 2 * jj) * CB + g * V;
+  const float* base = yb + ((2 * i) * S + 2 * jj) * CB + g * 4;
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
 #pragma unroll
@@ -1094,7 +1097,7 @@ __global__ void __launch_bounds__(GB * TP * TP) lrn_pool_fwd_tile_kernel(
       const float* p = base + (r * S + q) * CB;
 #pragma unroll
       for (int j = 0; j < V; j += 4) {
-        const float4 x = *reinterpret_cast<const float4*>(p + j);
+        const float4 x = *reinterpret_cast<const float4*>(p + j * GB);
         const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
