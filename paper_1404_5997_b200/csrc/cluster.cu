@@ -411,7 +411,8 @@ class ClusterImpl final : public ClusterBase {
   std::vector<cudaEvent_t> ev_slice_;
   bool slicing() const { return slice_last_ && !w_.empty() && !w_[0].last_fwd_slices.empty(); }
   const TA* stage_in(const Worker<TA>& w, int l) const;
-  void rotate_all(Worker<TA>& w);
+  // what: 1 = the s2d operand copy (conv1), 2 = the dgrad operands (rotated kernels), 3 = both
+  void rotate_all(Worker<TA>& w, int what = 3, cudaStream_t s = nullptr);
   struct ConvBwdState {
     const float* gout = nullptr;  // grad wrt the current stage's output
     bool dz_ready = false;        // dz already produced by the layer above's dgrad
@@ -549,6 +550,8 @@ class ClusterImpl final : public ClusterBase {
   cudaStream_t sf_ = nullptr;          // side stream: FC weight gradients + fused update (off the backward chain)
   cudaEvent_t ev_fcd_ = nullptr;       // FC dgrad of the current layer done (st_)
   cudaEvent_t ev_fcw_ = nullptr;       // all FC wgrads of the turn done (sf_)
+  cudaEvent_t ev_rot0_ = nullptr;      // conv forward enqueued on st_ (forks the dgrad-operand rotation)
+  cudaEvent_t ev_rot_ = nullptr;       // dgrad operands of this step's weights rotated
   float* ws3_ = nullptr;               // split-K workspace of the FC wgrad GEMMs (sf_)
   size_t ws3_floats_ = 0;
   std::vector<cudaEvent_t> ev_dz_;     // per conv layer: dz final on st_
@@ -627,6 +630,8 @@ ClusterImpl<TA>::ClusterImpl(const hp_model_spec* spec, const hp_cluster_config*
   HP_CUDA(cudaStreamCreateWithFlags(&sf_, cudaStreamNonBlocking));
   HP_CUDA(cudaEventCreateWithFlags(&ev_fcd_, cudaEventDisableTiming));
   HP_CUDA(cudaEventCreateWithFlags(&ev_fcw_, cudaEventDisableTiming));
+  HP_CUDA(cudaEventCreateWithFlags(&ev_rot0_, cudaEventDisableTiming));
+  HP_CUDA(cudaEventCreateWithFlags(&ev_rot_, cudaEventDisableTiming));
   for (auto& ps : pref_) {
     HP_CUDA(cudaEventCreateWithFlags(&ps.ready, cudaEventDisableTiming));
     HP_CUDA(cudaEventCreateWithFlags(&ps.used, cudaEventDisableTiming));
@@ -865,6 +870,8 @@ ClusterImpl<TA>::~ClusterImpl() {
   }
   if (ev_fcd_) cudaEventDestroy(ev_fcd_);
   if (ev_fcw_) cudaEventDestroy(ev_fcw_);
+  if (ev_rot0_) cudaEventDestroy(ev_rot0_);
+  if (ev_rot_) cudaEventDestroy(ev_rot_);
   if (ev_comm_) cudaEventDestroy(ev_comm_);
   if (ev0_fc_) cudaEventDestroy(ev0_fc_);
   if (sc_) cudaStreamDestroy(sc_);
@@ -1406,23 +1413,24 @@ void ClusterImpl<TA>::conv_forward_last_slice(Worker<TA>& w, int j) {
 }
 
 template <class TA>
-void ClusterImpl<TA>::rotate_all(Worker<TA>& w) {
-  for (size_t l = 0; l < g_.cg.size(); ++l) {
+void ClusterImpl<TA>::rotate_all(Worker<TA>& w, int what, cudaStream_t s) {
+  if (s == nullptr) s = st_;
+  for (size_t l = 0; l < g_.cg.size() && (what & 1); ++l) {
     const ConvGeom& c = g_.cg[l];
     if (c.s2d) {  // the s2d operand copy of the (just updated) master kernels
       launch_s2d_weights<TA>(w.cp + conv_k_off(static_cast<int>(l)), c.ldk, w.wz, c.F, c.C, c.R, c.S, c.stride, c.Rq,
-                             c.Cz, st_, c.pairs ? w.cp + conv_b_off(static_cast<int>(l)) : nullptr, w.bias2);
+                             c.Cz, s, c.pairs ? w.cp + conv_b_off(static_cast<int>(l)) : nullptr, w.bias2);
       ++launches_;
     }
   }
   // the dgrad operands of every implicit-dgrad layer, one launch
   std::vector<RotateTensor> rt;
-  for (size_t l = 0; l < g_.cg.size(); ++l) {
+  for (size_t l = 0; l < g_.cg.size() && (what & 2); ++l) {
     const ConvGeom& c = g_.cg[l];
     if (c.impl_dgrad) rt.push_back({w.cp + conv_k_off(static_cast<int>(l)), c.ldk, w.wrot[l], c.F, c.C, c.R, c.S});
   }
   if (!rt.empty()) {
-    launch_rotate_weights_multi<TA>(rt.data(), static_cast<int>(rt.size()), st_);
+    launch_rotate_weights_multi<TA>(rt.data(), static_cast<int>(rt.size()), s);
     launches_ += (static_cast<int64_t>(rt.size()) + 7) / 8;
   }
 }
@@ -1774,6 +1782,19 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
       }
     }
   }
+  {
+    // the dgrad operands (rotated bf16 kernels) of the weights the previous
+    // step's update left, on the wgrad stream (idle until the backward) once
+    // the conv forward is enqueued: the FC GEMMs leave SMs free (grids of 64-
+    // 144 CTAs) where the previous step's tail had the rotation on st_ alone
+    cudaStream_t rs = profile ? st_ : sw_;
+    if (rs != st_) {
+      HP_CUDA(cudaEventRecord(ev_rot0_, st_));
+      HP_CUDA(cudaStreamWaitEvent(rs, ev_rot0_, 0));
+    }
+    for (auto& w : w_) rotate_all(w, 2, rs);
+    HP_CUDA(cudaEventRecord(ev_rot_, rs));
+  }
   // The turns (cluster.cpp:507-614). The boundary exchange and the gradient
   // return run on their own stream sr_ with double-buffered boundary slots:
   // turn j+1's exchange is issued BEFORE turn j's FC compute and depends only
@@ -1851,6 +1872,7 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
   const int nc = static_cast<int>(g_.cg.size());
   std::vector<ConvBwdState> cbs(nl);
   NvtxRange bwd_range("hp.conv_backward_sync_sgd");
+  if (!profile) HP_CUDA(cudaStreamWaitEvent(st_, ev_rot_, 0));  // the dgrad operands (rotated during the FC phase)
   for (int l = nc - 1; l >= 0; --l) {
     for (int i = 0; i < nl; ++i) conv_backward_layer(w_[i], l, cbs[i]);
     if (K_ > 1) {
@@ -1900,7 +1922,7 @@ void ClusterImpl<TA>::enqueue(const float* const* batches, const float* const* t
   tl_mark("sgd_conv", 0, false, st_);
   sgd_conv(lr, hp);
   tl_mark("sgd_conv", 0, true, st_);
-  for (auto& w : w_) rotate_all(w);
+  for (auto& w : w_) rotate_all(w, 1);  // conv1's s2d operand: the next forward's first read
   tl_mark("rotate", 0, true, st_);
   // loss partials (+ the domain-error flag) to pinned host memory
   const size_t np = static_cast<size_t>(num_sub_) * xblocks_;
